@@ -1,0 +1,400 @@
+// HBM-bound kernels of the Llama layer: RMSNorm fwd/bwd (ln0/ln1 nodes), the
+// residual add (bda nodes), SwiGLU fwd/bwd (charged to mlp_down /
+// mlp_down_dgrad), RoPE fwd/bwd (charged to qkv / attn_bwd), AdamW and init.
+//
+// All use 16-byte vector accesses (8 x bf16) with fp32 math; row kernels are
+// warp-per-row with warp-shuffle reductions and no atomics, so every result is
+// bit-reproducible run to run (interleaved == sequential).
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "dh_capi.h"
+
+namespace dh {
+namespace {
+
+constexpr int kRowWarps = 8;  // warps per block for row kernels
+
+// ---------------------------------------------------------------- RMSNorm fwd
+
+template <int V>  // V uint4 (8 bf16) per lane: cols == V * 256
+__global__ void __launch_bounds__(kRowWarps * 32)
+    rmsnorm_fwd_reg(const uint4* __restrict__ x, const uint4* __restrict__ g, uint4* __restrict__ y,
+                    float* __restrict__ rstd, int rows, float inv_cols, float eps) {
+    const int row = blockIdx.x * kRowWarps + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const uint4* xr = x + static_cast<long long>(row) * V * 32;
+    float v[V][8];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        unpack8(xr[i * 32 + lane], v[i]);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) ss += v[i][t] * v[i][t];
+    }
+    ss = warp_sum(ss);
+    const float r = rsqrtf(ss * inv_cols + eps);
+    if (lane == 0) rstd[row] = r;
+    uint4* yr = y + static_cast<long long>(row) * V * 32;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        float gg[8], o[8];
+        unpack8(g[i * 32 + lane], gg);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o[t] = v[i][t] * r * gg[t];
+        yr[i * 32 + lane] = pack8(o);
+    }
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32)
+    rmsnorm_fwd_any(const uint4* __restrict__ x, const uint4* __restrict__ g, uint4* __restrict__ y,
+                    float* __restrict__ rstd, int rows, int vec_cols, float inv_cols, float eps) {
+    const int row = blockIdx.x * kRowWarps + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const uint4* xr = x + static_cast<long long>(row) * vec_cols;
+    float ss = 0.f;
+    for (int i = lane; i < vec_cols; i += 32) {
+        float v[8];
+        unpack8(xr[i], v);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) ss += v[t] * v[t];
+    }
+    ss = warp_sum(ss);
+    const float r = rsqrtf(ss * inv_cols + eps);
+    if (lane == 0) rstd[row] = r;
+    uint4* yr = y + static_cast<long long>(row) * vec_cols;
+    for (int i = lane; i < vec_cols; i += 32) {
+        float v[8], gg[8], o[8];
+        unpack8(xr[i], v);
+        unpack8(g[i], gg);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o[t] = v[t] * r * gg[t];
+        yr[i] = pack8(o);
+    }
+}
+
+// ---------------------------------------------------------------- RMSNorm bwd
+// xhat = x*rstd; dxhat = dy*g; dx = rstd*(dxhat - xhat*mean(dxhat*xhat)) (+ resid)
+// Column-parallel: thread t of a block owns columns [8t, 8t+8) of every row,
+// the block walks rows b, b+G, ... and reduces the per-row dot product through
+// warp shuffles + shared memory. Its dgamma column sums stay in registers and
+// land in partial[b][:]; a second kernel reduces the G rows in order (no
+// atomics => deterministic).
+__global__ void rmsnorm_bwd_cols(const uint4* __restrict__ x, const uint4* __restrict__ g,
+                                 const float* __restrict__ rstd, const uint4* __restrict__ dy,
+                                 const uint4* __restrict__ resid, uint4* __restrict__ dx,
+                                 float* __restrict__ partial, int rows, int vec_cols, float inv_cols) {
+    __shared__ float red[2][32];
+    const int t = threadIdx.x;
+    const int lane = t % 32, wid = t / 32, nw = (blockDim.x + 31) / 32;
+    float gam[8], dg[8];
+    unpack8(g[t], gam);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dg[k] = 0.f;
+    int parity = 0;
+    for (int row = blockIdx.x; row < rows; row += gridDim.x, parity ^= 1) {
+        const long long off = static_cast<long long>(row) * vec_cols + t;
+        const float r = rstd[row];
+        float xv[8], dv[8];
+        unpack8(x[off], xv);
+        unpack8(dy[off], dv);
+        float dot = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            xv[k] *= r;             // xhat
+            dg[k] += dv[k] * xv[k];
+            dv[k] *= gam[k];        // dxhat
+            dot += dv[k] * xv[k];
+        }
+        dot = warp_sum(dot);
+        if (lane == 0) red[parity][wid] = dot;
+        __syncthreads();
+        float tot = 0.f;
+        for (int w = 0; w < nw; ++w) tot += red[parity][w];
+        tot *= inv_cols;
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = r * (dv[k] - xv[k] * tot);
+        if (resid) {
+            float rv[8];
+            unpack8(resid[off], rv);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] += rv[k];
+        }
+        dx[off] = pack8(o);
+    }
+    float4* dst = reinterpret_cast<float4*>(partial + static_cast<long long>(blockIdx.x) * vec_cols * 8 + t * 8);
+    dst[0] = make_float4(dg[0], dg[1], dg[2], dg[3]);
+    dst[1] = make_float4(dg[4], dg[5], dg[6], dg[7]);
+}
+
+// dgamma_acc[c] += sum_w partial[w][c], w ascending.
+__global__ void column_reduce_add(const float* __restrict__ partial, float* __restrict__ acc, int nw,
+                                  int cols) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    float s = 0.f;
+    for (int w = 0; w < nw; ++w) s += partial[static_cast<long long>(w) * cols + c];
+    acc[c] += s;
+}
+
+// ---------------------------------------------------------------- elementwise
+
+__global__ void add_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                           uint4* __restrict__ o, long long nvec) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float x[8], y[8];
+        unpack8(a[i], x);
+        unpack8(b[i], y);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[t] += y[t];
+        o[i] = pack8(x);
+    }
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
+__global__ void swiglu_fwd_kernel(const uint4* __restrict__ gate, const uint4* __restrict__ up,
+                                  uint4* __restrict__ act, long long nvec) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float gv[8], uv[8], o[8];
+        unpack8(gate[i], gv);
+        unpack8(up[i], uv);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o[t] = gv[t] * sigmoidf_(gv[t]) * uv[t];
+        act[i] = pack8(o);
+    }
+}
+
+__global__ void swiglu_bwd_kernel(const uint4* __restrict__ gate, const uint4* __restrict__ up,
+                                  const uint4* __restrict__ dact, uint4* __restrict__ dgate,
+                                  uint4* __restrict__ dup, long long nvec) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float gv[8], uv[8], dv[8], dg[8], du[8];
+        unpack8(gate[i], gv);
+        unpack8(up[i], uv);
+        unpack8(dact[i], dv);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const float s = sigmoidf_(gv[t]);
+            const float silu = gv[t] * s;
+            du[t] = dv[t] * silu;
+            dg[t] = dv[t] * uv[t] * s * (1.f + gv[t] * (1.f - s));
+        }
+        dgate[i] = pack8(dg);
+        dup[i] = pack8(du);
+    }
+}
+
+// ---------------------------------------------------------------- RoPE
+// Half-split rotation (Llama/HF convention): pair (i, i + d/2), frequency
+// theta^(-2i/d), angle = position * frequency computed in fp64 so that the
+// rotation matches the oracle to fp32 rounding even at long positions.
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, long long ld, int tokens, int heads,
+                            int head_dim, double log_theta, int pos0, float sign) {
+    const int half = head_dim / 2;
+    const int t = blockIdx.x;
+    if (t >= tokens) return;
+    __nv_bfloat16* row = qkv + static_cast<long long>(t) * ld;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        const double inv_freq = exp(-log_theta * (2.0 * i) / head_dim);
+        const double ang = static_cast<double>(t + pos0) * inv_freq;
+        const float c = static_cast<float>(cos(ang));
+        const float s = sign * static_cast<float>(sin(ang));
+        for (int h = 0; h < heads; ++h) {
+            __nv_bfloat16* p = row + h * head_dim;
+            const float a = __bfloat162float(p[i]);
+            const float b = __bfloat162float(p[i + half]);
+            p[i] = __float2bfloat16(a * c - b * s);
+            p[i + half] = __float2bfloat16(b * c + a * s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- optimizer / init
+
+__global__ void adamw_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
+                             float* __restrict__ grad, float* __restrict__ m, float* __restrict__ v,
+                             long long n, float lr, float b1, float b2, float eps, float wd,
+                             float bc1, float bc2, float gscale, int zero_grad) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const float g = grad[i] * gscale;
+        const float mi = b1 * m[i] + (1.f - b1) * g;
+        const float vi = b2 * v[i] + (1.f - b2) * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        float p = master[i];
+        p -= lr * wd * p;
+        p -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+        master[i] = p;
+        w[i] = __float2bfloat16(p);
+        if (zero_grad) grad[i] = 0.f;
+    }
+}
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void init_normal_kernel(__nv_bfloat16* __restrict__ out, float* __restrict__ f32,
+                                   long long n, unsigned long long seed, float std_dev) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const unsigned long long r = splitmix64(seed * 0x100000001B3ull + static_cast<unsigned long long>(i));
+        const float u1 = (static_cast<float>(r >> 40) + 1.f) * (1.f / 16777217.f);
+        const float u2 = static_cast<float>((r >> 16) & 0xFFFFFF) * (1.f / 16777216.f);
+        const float z = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2) * std_dev;
+        const __nv_bfloat16 b = __float2bfloat16(z);
+        if (out) out[i] = b;
+        if (f32) f32[i] = __bfloat162float(b);
+    }
+}
+
+__global__ void fill_kernel(__nv_bfloat16* out, float v, long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = __float2bfloat16(v);
+}
+
+int grid_for(long long work, int threads) {
+    const long long blocks = (work + threads - 1) / threads;
+    return static_cast<int>(std::max<long long>(1, std::min<long long>(blocks, 148LL * 16)));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+}  // namespace dh
+
+using namespace dh;
+
+extern "C" {
+
+int dh_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols,
+                   float eps, void* stream) {
+    if (cols % 8 || !aligned16(x) || !aligned16(y) || !aligned16(gamma))
+        return set_error(DH_ERR_INVALID, "rmsnorm_fwd: cols % 8 and 16-byte alignment required");
+    if (rows <= 0) return DH_OK;
+    auto s = static_cast<cudaStream_t>(stream);
+    const dim3 grid((rows + kRowWarps - 1) / kRowWarps), block(kRowWarps * 32);
+    const auto* X = static_cast<const uint4*>(x);
+    const auto* G = static_cast<const uint4*>(gamma);
+    auto* Y = static_cast<uint4*>(y);
+    const float ic = 1.f / cols;
+    switch (cols) {
+        case 256: rmsnorm_fwd_reg<1><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
+        case 512: rmsnorm_fwd_reg<2><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
+        case 1024: rmsnorm_fwd_reg<4><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
+        case 2048: rmsnorm_fwd_reg<8><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
+        case 4096: rmsnorm_fwd_reg<16><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
+        default: rmsnorm_fwd_any<<<grid, block, 0, s>>>(X, G, Y, rstd, rows, cols / 8, ic, eps);
+    }
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy,
+                   const void* resid, void* dx, float* dgamma_acc, float* partial, int rows,
+                   int cols, void* stream) {
+    if (cols % 8 || cols / 8 > 1024 || !aligned16(x) || !aligned16(dy) || !aligned16(dx))
+        return set_error(DH_ERR_INVALID, "rmsnorm_bwd: cols % 8, cols <= 8192 and 16-byte alignment required");
+    if (rows <= 0) return DH_OK;
+    auto s = static_cast<cudaStream_t>(stream);
+    const int blocks = std::min(rows, 1184);
+    rmsnorm_bwd_cols<<<blocks, cols / 8, 0, s>>>(
+        static_cast<const uint4*>(x), static_cast<const uint4*>(gamma), rstd,
+        static_cast<const uint4*>(dy), static_cast<const uint4*>(resid), static_cast<uint4*>(dx),
+        partial, rows, cols / 8, 1.f / cols);
+    DH_CUDA_CHECK(cudaGetLastError());
+    if (dgamma_acc) {
+        column_reduce_add<<<(cols + 255) / 256, 256, 0, s>>>(partial, dgamma_acc, blocks, cols);
+        DH_CUDA_CHECK(cudaGetLastError());
+    }
+    return DH_OK;
+}
+
+int dh_add(const void* a, const void* b, void* out, long long n, void* stream) {
+    if (n % 8 || !aligned16(a) || !aligned16(b) || !aligned16(out))
+        return set_error(DH_ERR_INVALID, "add: n % 8 and 16-byte alignment required");
+    const long long nv = n / 8;
+    if (!nv) return DH_OK;
+    add_kernel<<<grid_for(nv, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(a), static_cast<const uint4*>(b), static_cast<uint4*>(out), nv);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_swiglu_fwd(const void* gate, const void* up, void* act, long long n, void* stream) {
+    if (n % 8) return set_error(DH_ERR_INVALID, "swiglu_fwd: n % 8 required");
+    const long long nv = n / 8;
+    if (!nv) return DH_OK;
+    swiglu_fwd_kernel<<<grid_for(nv, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(gate), static_cast<const uint4*>(up), static_cast<uint4*>(act), nv);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_swiglu_bwd(const void* gate, const void* up, const void* dact, void* dgate, void* dup,
+                  long long n, void* stream) {
+    if (n % 8) return set_error(DH_ERR_INVALID, "swiglu_bwd: n % 8 required");
+    const long long nv = n / 8;
+    if (!nv) return DH_OK;
+    swiglu_bwd_kernel<<<grid_for(nv, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(gate), static_cast<const uint4*>(up),
+        static_cast<const uint4*>(dact), static_cast<uint4*>(dgate), static_cast<uint4*>(dup), nv);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_rope(void* qkv, long long ld, int tokens, int n_q_heads, int n_kv_heads, int head_dim,
+            float theta, int pos0, int inverse, void* stream) {
+    if (head_dim % 2) return set_error(DH_ERR_INVALID, "rope: odd head_dim");
+    if (tokens <= 0) return DH_OK;
+    rope_kernel<<<tokens, 64, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<__nv_bfloat16*>(qkv), ld, tokens, n_q_heads + n_kv_heads, head_dim,
+        std::log(static_cast<double>(theta)), pos0, inverse ? -1.f : 1.f);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_adamw(float* master, void* weight_bf16, float* grad, float* m, float* v, long long n,
+             float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+             float grad_scale, int zero_grad, void* stream) {
+    if (n <= 0) return DH_OK;
+    const float bc1 = 1.f - std::pow(beta1, static_cast<float>(step));
+    const float bc2 = 1.f - std::pow(beta2, static_cast<float>(step));
+    adamw_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        master, static_cast<__nv_bfloat16*>(weight_bf16), grad, m, v, n, lr, beta1, beta2, eps,
+        weight_decay, bc1, bc2, grad_scale, zero_grad);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_init_normal(void* bf16_out, float* f32_out, long long n, unsigned long long seed,
+                   float std_dev, void* stream) {
+    if (n <= 0) return DH_OK;
+    init_normal_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<__nv_bfloat16*>(bf16_out), f32_out, n, seed, std_dev);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_fill_bf16(void* out, float value, long long n, void* stream) {
+    if (n <= 0) return DH_OK;
+    fill_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<__nv_bfloat16*>(out), value, n);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,365 @@
+// Persistent, warp-specialised bf16 GEMM for sm_100a on tcgen05 / TMEM / TMA.
+//
+//   D(m, n) (+)= sum_k A(m, k) * B(n, k)
+//
+// A and B are each either K-major (row-major [rows, K]: the forward GEMMs) or
+// MN-major (K rows of contiguous M / N: the dgrad B operand and both wgrad
+// operands), so every GEMM of the Megatron TP+SP layer — forward, dgrad and
+// wgrad — runs without a transpose pass. D is bf16 (optionally accumulated,
+// beta = 1) or fp32 (accumulated: the fp32 main-grad of wgrad).
+//
+// CTA = 6 warps:  warp 0  TMA producer (one lane)
+//                 warp 1  TMEM allocator + tcgen05.mma issuer (one elected lane)
+//                 warps 2-5 epilogue: tcgen05.ld TMEM -> registers -> global
+// Tile BM=128 x BN (128 or 256) x BK=64, SWIZZLE_128B smem operands, a 4-6
+// stage TMA ring (full/empty mbarriers) and a double-buffered TMEM
+// accumulator (2 x BN fp32 columns) so the epilogue of tile i overlaps the
+// main loop of tile i+1. The grid is persistent: min(tiles, SMs allowed), which
+// is how the SI executor caps a GEMM's SM footprint next to NCCL kernels.
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "dh_capi.h"
+
+namespace dh {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int kStageA = BM * BK * 2;
+    static constexpr int kStageB = BN * BK * 2;
+    static constexpr int kStageBytes = kStageA + kStageB;
+    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kTmemCols = 2 * BN;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct KParams {
+    void* d;
+    long long ldd;
+    int m, n, k;
+    int accumulate;
+    int tiles_m, tiles_n;
+};
+
+template <int BN, bool A_MN, bool B_MN, bool D_F32>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tma_a,
+                        const __grid_constant__ CUtensorMap tma_b, const KParams p) {
+    using Cfg = GemmCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + Cfg::kStages * Cfg::kStageA;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+    uint64_t* empty = full + Cfg::kStages;
+    uint64_t* tfull = empty + Cfg::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int num_tiles = p.tiles_m * p.tiles_n;
+    const int num_kb = (p.k + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma_a);
+        tma_prefetch(&tma_b);
+        for (int s = 0; s < Cfg::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = (tile % p.tiles_m) * BM;
+                const int n0 = (tile / p.tiles_m) * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+                    uint8_t* a_dst = sA + stage * Cfg::kStageA;
+                    uint8_t* b_dst = sB + stage * Cfg::kStageB;
+                    const int k0 = kb * BK;
+                    if constexpr (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < BM / 64; ++i)
+                            tma_load_2d(a_dst + i * (BK * 128), &tma_a, &full[stage], m0 + 64 * i, k0);
+                    } else {
+                        tma_load_2d(a_dst, &tma_a, &full[stage], k0, m0);
+                    }
+                    if constexpr (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < BN / 64; ++i)
+                            tma_load_2d(b_dst + i * (BK * 128), &tma_b, &full[stage], n0 + 64 * i, k0);
+                    } else {
+                        tma_load_2d(b_dst, &tma_b, &full[stage], k0, n0);
+                    }
+                    if (++stage == Cfg::kStages) stage = 0, phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t a_addr = smem_u32(sA + stage * Cfg::kStageA);
+                    const uint32_t b_addr = smem_u32(sB + stage * Cfg::kStageB);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        // K-major: advance 16 elements = 32 B inside the swizzled row.
+                        // MN-major: advance two 8-row k atoms = 2048 B.
+                        const uint64_t a_desc =
+                            A_MN ? umma_desc_sw128(a_addr + kk * 2048, BK * 128, 1024)
+                                 : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+                        const uint64_t b_desc =
+                            B_MN ? umma_desc_sw128(b_addr + kk * 2048, BK * 128, 1024)
+                                 : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+                        tc_mma_bf16(d_tmem, a_desc, b_desc, idesc, (kb | kk) != 0);
+                    }
+                    tc_commit(&empty[stage]);
+                    if (kb == num_kb - 1) tc_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++stage == Cfg::kStages) stage = 0, phase ^= 1;
+            }
+            if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int m0 = (tile % p.tiles_m) * BM;
+            const int n0 = (tile / p.tiles_m) * BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = m0 + quad * 32 + lane;
+            const bool row_ok = row < p.m;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
+                tmem_ld_wait();
+                const int col0 = n0 + c * 32;
+                if (!row_ok || col0 >= p.n) continue;
+                const bool full_chunk = col0 + 32 <= p.n;
+                if constexpr (D_F32) {
+                    float* drow = reinterpret_cast<float*>(p.d) + static_cast<long long>(row) * p.ldd + col0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                            if (p.accumulate) {
+                                const float4 o = *reinterpret_cast<const float4*>(drow + j);
+                                v.x += o.x, v.y += o.y, v.z += o.z, v.w += o.w;
+                            }
+                            *reinterpret_cast<float4*>(drow + j) = v;
+                        }
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < p.n; ++j) {
+                            float v = __uint_as_float(r[j]);
+                            if (p.accumulate) v += drow[j];
+                            drow[j] = v;
+                        }
+                    }
+                } else {
+                    __nv_bfloat16* drow =
+                        reinterpret_cast<__nv_bfloat16*>(p.d) + static_cast<long long>(row) * p.ldd + col0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            float f[8];
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) f[t] = __uint_as_float(r[j + t]);
+                            if (p.accumulate) {
+                                float o[8];
+                                unpack8(*reinterpret_cast<const uint4*>(drow + j), o);
+#pragma unroll
+                                for (int t = 0; t < 8; ++t) f[t] += o[t];
+                            }
+                            *reinterpret_cast<uint4*>(drow + j) = pack8(f);
+                        }
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < p.n; ++j) {
+                            float v = __uint_as_float(r[j]);
+                            if (p.accumulate) v += __bfloat162float(drow[j]);
+                            drow[j] = __float2bfloat16(v);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, Cfg::kTmemCols);
+    }
+}
+
+// --------------------------------------------------------------------------- host side
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+        }
+    });
+    return fn;
+}
+
+// 2D bf16 tensor map: `inner` contiguous elements per row, `outer` rows,
+// `ld` elements between rows, box = 64 x box_rows, 128-byte swizzle.
+int make_map(CUtensorMap* map, const void* base, long long inner, long long outer, long long ld,
+             int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return set_error(DH_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 2) % 16) {
+        return set_error(DH_ERR_INVALID, "gemm operand must be 16-byte aligned with 16-byte row pitch");
+    }
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(DH_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    return DH_OK;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool D_F32>
+int launch(const dh_gemm_args* g, cudaStream_t stream) {
+    using Cfg = GemmCfg<BN>;
+    CUtensorMap ma, mb;
+    int rc = A_MN ? make_map(&ma, g->a, g->m, g->k, g->lda, BK) : make_map(&ma, g->a, g->k, g->m, g->lda, BM);
+    if (rc) return rc;
+    rc = B_MN ? make_map(&mb, g->b, g->n, g->k, g->ldb, BK) : make_map(&mb, g->b, g->k, g->n, g->ldb, BN);
+    if (rc) return rc;
+    KParams p;
+    p.d = g->d;
+    p.ldd = g->ldd;
+    p.m = g->m;
+    p.n = g->n;
+    p.k = g->k;
+    p.accumulate = g->accumulate;
+    p.tiles_m = (g->m + BM - 1) / BM;
+    p.tiles_n = (g->n + BN - 1) / BN;
+    const int tiles = p.tiles_m * p.tiles_n;
+    int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
+    ctas = std::min(ctas, tiles);
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, D_F32>;
+    static bool configured = false;  // per template instance
+    if (!configured) {
+        DH_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           Cfg::kSmemBytes));
+        configured = true;
+    }
+    kern<<<ctas, kThreads, Cfg::kSmemBytes, stream>>>(ma, mb, p);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+template <int BN>
+int dispatch_major(const dh_gemm_args* g, cudaStream_t s) {
+    const int key = (g->a_mn ? 4 : 0) | (g->b_mn ? 2 : 0) | (g->d_fp32 ? 1 : 0);
+    switch (key) {
+        case 0: return launch<BN, false, false, false>(g, s);
+        case 1: return launch<BN, false, false, true>(g, s);
+        case 2: return launch<BN, false, true, false>(g, s);
+        case 3: return launch<BN, false, true, true>(g, s);
+        case 4: return launch<BN, true, false, false>(g, s);
+        case 5: return launch<BN, true, false, true>(g, s);
+        case 6: return launch<BN, true, true, false>(g, s);
+        default: return launch<BN, true, true, true>(g, s);
+    }
+}
+
+}  // namespace
+
+// Tile-N choice: the wider tile halves B re-reads; fall back to 128 when 256
+// would leave most SMs idle (few output tiles) or N is narrow.
+int gemm_pick_bn(int m, int n, int ctas) {
+    const long long t256 = static_cast<long long>((m + BM - 1) / BM) * ((n + 255) / 256);
+    if (n <= 128) return 128;
+    if (t256 < static_cast<long long>(ctas) * 3 / 4) return 128;
+    return 256;
+}
+
+int gemm(const dh_gemm_args* g, cudaStream_t s) {
+    if (g->m <= 0 || g->n <= 0 || g->k <= 0) return set_error(DH_ERR_INVALID, "gemm: empty shape");
+    const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
+    const int bn = g->tile_n ? g->tile_n : gemm_pick_bn(g->m, g->n, ctas);
+    if (bn == 256) return dispatch_major<256>(g, s);
+    if (bn == 128) return dispatch_major<128>(g, s);
+    return set_error(DH_ERR_INVALID, "gemm: tile_n must be 0, 128 or 256");
+}
+
+}  // namespace dh
+
+extern "C" int dh_gemm(const dh_gemm_args* args, void* stream) {
+    if (!args) return dh::set_error(DH_ERR_INVALID, "dh_gemm: null args");
+    return dh::gemm(args, static_cast<cudaStream_t>(stream));
+}

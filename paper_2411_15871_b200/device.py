@@ -1,0 +1,159 @@
+"""ctypes binding of the dh C ABI (include/dh_capi.h) -> libdh_b200.so.
+
+torch is used only for device memory and streams: tensors are passed to the
+native kernels as raw pointers. There is no fallback path: if the CUDA
+library is missing or no GPU is present, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libdh_b200.so")
+
+_lib = None
+
+
+class DeviceError(RuntimeError):
+    """dh status != DH_OK (maps to weft::DeviceError on the C++ side)."""
+
+
+c_void_p, c_int, c_ll, c_float, c_ull = (ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong,
+                                         ctypes.c_float, ctypes.c_ulonglong)
+
+
+class GemmArgs(ctypes.Structure):
+    _fields_ = [("a", c_void_p), ("lda", c_ll), ("a_mn", c_int),
+                ("b", c_void_p), ("ldb", c_ll), ("b_mn", c_int),
+                ("d", c_void_p), ("ldd", c_ll), ("d_fp32", c_int),
+                ("m", c_int), ("n", c_int), ("k", c_int),
+                ("accumulate", c_int), ("max_ctas", c_int), ("tile_n", c_int)]
+
+
+_SIGS = {
+    "dh_gemm": [ctypes.POINTER(GemmArgs), c_void_p],
+    "dh_rmsnorm_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float, c_void_p],
+    "dh_rmsnorm_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                       c_void_p, c_int, c_int, c_void_p],
+    "dh_add": [c_void_p, c_void_p, c_void_p, c_ll, c_void_p],
+    "dh_swiglu_fwd": [c_void_p, c_void_p, c_void_p, c_ll, c_void_p],
+    "dh_swiglu_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_ll, c_void_p],
+    "dh_rope": [c_void_p, c_ll, c_int, c_int, c_int, c_int, c_float, c_int, c_int, c_void_p],
+    "dh_attn_fwd": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_int,
+                    c_int, c_int, c_int, c_float, c_void_p],
+    "dh_attn_bwd": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
+                    c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_int, c_int, c_int,
+                    c_int, c_float, c_void_p],
+    "dh_adamw": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_ll, c_float, c_float,
+                 c_float, c_float, c_float, c_int, c_float, c_int, c_void_p],
+    "dh_init_normal": [c_void_p, c_void_p, c_ll, c_ull, c_float, c_void_p],
+    "dh_fill_bf16": [c_void_p, c_float, c_ll, c_void_p],
+}
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"CUDA library not built: {LIB_PATH} (run `make cuda`)")
+        l = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        for name, args in _SIGS.items():
+            if not hasattr(l, name):
+                continue  # symbol not built yet: calling it raises AttributeError
+            fn = getattr(l, name)
+            fn.argtypes = args
+            fn.restype = c_int
+        l.dh_last_error.restype = ctypes.c_char_p
+        _lib = l
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise DeviceError(f"dh status {rc}: {lib().dh_last_error().decode()}")
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# --------------------------------------------------------------------------- kernels
+
+def gemm(a, b, d, *, a_mn=False, b_mn=False, accumulate=False, m=None, n=None, k=None,
+         max_ctas=0, tile_n=0, stream=None):
+    """d(m,n) (+)= sum_k A(m,k) B(n,k). A = a[m,k] (K-major) or a[k,m] (a_mn);
+    B = b[n,k] (K-major) or b[k,n] (b_mn). d bf16 or fp32 [m,n]."""
+    import torch
+    if m is None:
+        m = a.shape[1] if a_mn else a.shape[0]
+    if k is None:
+        k = a.shape[0] if a_mn else a.shape[1]
+    if n is None:
+        n = b.shape[1] if b_mn else b.shape[0]
+    args = GemmArgs(a.data_ptr(), a.stride(0), int(a_mn), b.data_ptr(), b.stride(0), int(b_mn),
+                    d.data_ptr(), d.stride(0), int(d.dtype == torch.float32), m, n, k,
+                    int(accumulate), max_ctas, tile_n)
+    check(lib().dh_gemm(ctypes.byref(args), _stream(stream)))
+    return d
+
+
+def rmsnorm_fwd(x, gamma, y, rstd, eps=1e-5, stream=None):
+    rows, cols = x.shape
+    check(lib().dh_rmsnorm_fwd(_ptr(x), _ptr(gamma), _ptr(y), _ptr(rstd), rows, cols, eps,
+                               _stream(stream)))
+
+
+def rmsnorm_bwd(x, gamma, rstd, dy, dx, dgamma_acc=None, partial=None, resid=None, stream=None):
+    import torch
+    rows, cols = x.shape
+    if partial is None:
+        partial = torch.empty(min(rows, 1184) * cols, dtype=torch.float32, device=x.device)
+    check(lib().dh_rmsnorm_bwd(_ptr(x), _ptr(gamma), _ptr(rstd), _ptr(dy), _ptr(resid), _ptr(dx),
+                               _ptr(dgamma_acc), _ptr(partial), rows, cols, _stream(stream)))
+
+
+def add(a, b, out, stream=None):
+    check(lib().dh_add(_ptr(a), _ptr(b), _ptr(out), a.numel(), _stream(stream)))
+
+
+def swiglu_fwd(gate, up, act, stream=None):
+    check(lib().dh_swiglu_fwd(_ptr(gate), _ptr(up), _ptr(act), gate.numel(), _stream(stream)))
+
+
+def swiglu_bwd(gate, up, dact, dgate, dup, stream=None):
+    check(lib().dh_swiglu_bwd(_ptr(gate), _ptr(up), _ptr(dact), _ptr(dgate), _ptr(dup),
+                              gate.numel(), _stream(stream)))
+
+
+def rope(qkv, n_q_heads, n_kv_heads, head_dim, theta, pos0=0, inverse=False, tokens=None,
+         stream=None):
+    tokens = qkv.shape[0] if tokens is None else tokens
+    check(lib().dh_rope(_ptr(qkv), qkv.stride(0), tokens, n_q_heads, n_kv_heads, head_dim, theta,
+                        pos0, int(inverse), _stream(stream)))
+
+
+def attn_fwd(q, k, v, o, lse, n_q_heads, n_kv_heads, head_dim, scale, stream=None):
+    tokens = q.shape[0]
+    check(lib().dh_attn_fwd(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o),
+                            o.stride(0), _ptr(lse), tokens, n_q_heads, n_kv_heads, head_dim,
+                            scale, _stream(stream)))
+
+
+def attn_bwd(q, k, v, o, lse, do, dq, dk, dv, n_q_heads, n_kv_heads, head_dim, scale,
+             scratch=None, stream=None):
+    import torch
+    tokens = q.shape[0]
+    if scratch is None:
+        scratch = torch.empty(tokens * n_q_heads * (head_dim + 1), dtype=torch.float32,
+                              device=q.device)
+    check(lib().dh_attn_bwd(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o),
+                            o.stride(0), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv),
+                            dq.stride(0), dk.stride(0), _ptr(scratch), tokens, n_q_heads,
+                            n_kv_heads, head_dim, scale, _stream(stream)))

@@ -1,0 +1,130 @@
+"""GPU numerics of the sm_100a kernels, each against a plain PyTorch fp32
+reference of the same op (bf16 inputs, fp32 math). Tolerances are stated per
+test: bf16 storage gives ~2^-8 relative rounding per stored value."""
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2411_15871_b200 import device as dh  # noqa: E402
+
+
+def _rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+@pytest.fixture(autouse=True)
+def _seed():
+    torch.manual_seed(0)
+
+
+GEMM_SHAPES = [(128, 128, 64), (256, 512, 128), (4096, 768, 4096), (333, 200, 136),
+               (512, 4096, 512), (4096, 1792, 4096)]
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+def test_gemm_bf16_majors(shape, a_mn, b_mn):
+    m, n, k = shape
+    A = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
+    a = A.t().contiguous() if a_mn else A
+    b = B.t().contiguous() if b_mn else B
+    if (a_mn and m % 8) or (b_mn and n % 8) or k % 8:
+        pytest.skip("TMA needs 16-byte row pitch")
+    d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    dh.gemm(a, b, d, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k)
+    ref = A.float() @ B.float().t()
+    assert _rel(d, ref) < 4e-3  # bf16 output rounding only
+
+
+@pytest.mark.parametrize("tile_n", [128, 256])
+def test_gemm_accumulate_and_fp32(tile_n):
+    m, n, k = 512, 384, 256
+    A = torch.randn(k, m, device="cuda", dtype=torch.bfloat16)  # MN-major A (wgrad style)
+    B = torch.randn(k, n, device="cuda", dtype=torch.bfloat16)
+    g = torch.randn(m, n, device="cuda", dtype=torch.float32)
+    g0 = g.clone()
+    dh.gemm(A, B, g, a_mn=True, b_mn=True, accumulate=True, tile_n=tile_n)
+    ref = g0 + A.float().t() @ B.float()
+    assert (g - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
+    d = torch.randn(m, n, device="cuda", dtype=torch.bfloat16)
+    d0 = d.float().clone()
+    dh.gemm(A, B, d, a_mn=True, b_mn=True, accumulate=True, tile_n=tile_n)
+    assert _rel(d, d0 + A.float().t() @ B.float()) < 4e-3
+
+
+def test_gemm_capped_ctas():
+    A = torch.randn(2048, 1024, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(1024, 1024, device="cuda", dtype=torch.bfloat16)
+    d = torch.empty(2048, 1024, device="cuda", dtype=torch.bfloat16)
+    for cap in (1, 7, 100):
+        dh.gemm(A, B, d, max_ctas=cap)
+        assert _rel(d, A.float() @ B.float().t()) < 4e-3
+
+
+@pytest.mark.parametrize("cols", [256, 512, 4096, 1000 * 8 // 8 + 8])
+def test_rmsnorm_fwd_bwd(cols):
+    rows, eps = 777, 1e-5
+    x = torch.randn(rows, cols, device="cuda", dtype=torch.bfloat16)
+    g = (1 + 0.1 * torch.randn(cols, device="cuda")).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, device="cuda")
+    dh.rmsnorm_fwd(x, g, y, rstd, eps)
+    xf, gf = x.float().requires_grad_(), g.float().requires_grad_()
+    r = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
+    yf = xf * r * gf
+    assert _rel(y, yf) < 4e-3
+    assert torch.allclose(rstd, r.squeeze(-1).detach(), rtol=1e-5)
+    dy = torch.randn_like(x)
+    resid = torch.randn_like(x)
+    yf.backward(dy.float())
+    dx = torch.empty_like(x)
+    dgam = torch.zeros(cols, device="cuda")
+    dh.rmsnorm_bwd(x, g, rstd, dy, dx, dgamma_acc=dgam, resid=resid)
+    assert _rel(dx, xf.grad + resid.float()) < 5e-3
+    assert _rel(dgam, gf.grad) < 1e-4
+
+
+def test_swiglu_add():
+    n = 4096 * 64
+    g = torch.randn(n, device="cuda", dtype=torch.bfloat16)
+    u = torch.randn(n, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty_like(g)
+    dh.swiglu_fwd(g, u, act)
+    gf, uf = g.float().requires_grad_(), u.float().requires_grad_()
+    af = torch.nn.functional.silu(gf) * uf
+    assert _rel(act, af) < 4e-3
+    da = torch.randn_like(g)
+    af.backward(da.float())
+    dg, du = torch.empty_like(g), torch.empty_like(g)
+    dh.swiglu_bwd(g, u, da, dg, du)
+    assert _rel(dg, gf.grad) < 5e-3 and _rel(du, uf.grad) < 5e-3
+    out = torch.empty_like(g)
+    dh.add(g, u, out)
+    assert _rel(out, g.float() + u.float()) < 4e-3
+
+
+@pytest.mark.parametrize("theta,d", [(500000.0, 128), (10000.0, 64)])
+def test_rope_roundtrip(theta, d):
+    T, hq, hk = 1024, 4, 1
+    qkv = torch.randn(T, (hq + 2 * hk) * d, device="cuda", dtype=torch.bfloat16)
+    ref = qkv.float().clone()
+    pos = torch.arange(T, device="cuda", dtype=torch.float64)[:, None]
+    inv = theta ** (-torch.arange(0, d // 2, device="cuda", dtype=torch.float64) * 2 / d)
+    ang = pos * inv[None]
+    c, s = ang.cos().float(), ang.sin().float()
+    for h in range(hq + hk):
+        x = ref[:, h * d:(h + 1) * d]
+        a, b = x[:, :d // 2].clone(), x[:, d // 2:].clone()
+        x[:, :d // 2] = a * c - b * s
+        x[:, d // 2:] = b * c + a * s
+    out = qkv.clone()
+    dh.rope(out, hq, hk, d, theta)
+    assert _rel(out, ref) < 4e-3
+    assert torch.equal(out[:, (hq + hk) * d:], qkv[:, (hq + hk) * d:])  # v untouched
+    back = out.clone()
+    dh.rope(back, hq, hk, d, theta, inverse=True)
+    assert _rel(back, qkv) < 8e-3
