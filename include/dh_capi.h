@@ -90,7 +90,7 @@ int dh_rope(void* qkv, long long ld, int tokens, int n_q_heads, int n_kv_heads, 
 int dh_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 void* o, long long ldo, float* lse, int tokens, int n_q_heads, int n_kv_heads,
                 int head_dim, float scale, void* stream);
-/* dq/dk/dv written (not accumulated); `scratch` fp32 >= tokens*n_q_heads*(head_dim+1) floats. */
+/* dq/dk/dv written (not accumulated); `scratch` fp32 >= tokens*n_q_heads*(2*head_dim+1) floats. */
 int dh_attn_bwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 const void* o, long long ldo, const float* lse, const void* dout,
                 void* dq, void* dk, void* dv, long long lddq, long long lddkv, float* scratch,

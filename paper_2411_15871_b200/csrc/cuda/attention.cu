@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dkdv_kernel(
     for (int i = 0; i < D / 8; ++i)
 #pragma unroll
         for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
-    uint32_t kf[D / 16][4], vf[D / 16][4];
     const int key0 = kb * BT + warp * 16 + g;  // rows key0, key0 + 8
 
     for (int qb = kb; qb < nqb; ++qb) {
@@ -326,10 +325,6 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dkdv_kernel(
             cp_wait<0>();
         }
         __syncthreads();
-        if (qb == kb) {
-            load_a_frags<D>(kf, sK, warp * 16);
-            load_a_frags<D>(vf, sV, warp * 16);
-        }
         bf16* tQ = sQ + buf * BT * D;
         bf16* tO = sO + buf * BT * D;
         const float* L = sL + buf * BT;
@@ -340,8 +335,16 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dkdv_kernel(
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int e = 0; e < 4; ++e) p[i][e] = dp[i][e] = 0.f;
-        mma_rows_x_tileT<D>(p, kf, tQ);   // S^T (keys x queries)
-        mma_rows_x_tileT<D>(dp, vf, tO);  // dP^T
+        {   // K / V fragments are re-read from smem each q block to stay under 255 registers
+            uint32_t f[D / 16][4];
+            load_a_frags<D>(f, sK, warp * 16);
+            mma_rows_x_tileT<D>(p, f, tQ);   // S^T (keys x queries)
+        }
+        {
+            uint32_t f[D / 16][4];
+            load_a_frags<D>(f, sV, warp * 16);
+            mma_rows_x_tileT<D>(dp, f, tO);  // dP^T
+        }
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
@@ -505,13 +508,7 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dq_kernel(
     }
 }
 
-template <int D>
-int fwd_impl(const dh_attn_problem& p, cudaStream_t s);
-
 }  // namespace
-
-struct dh_attn_problem_impl {};
-
 }  // namespace dh
 
 namespace {

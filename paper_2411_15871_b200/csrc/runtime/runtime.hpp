@@ -1,0 +1,176 @@
+// Internal C++ runtime behind include/dh_capi.h: device context (lane streams,
+// collective backend), the Llama TP+SP model (memory pool, weights, activation
+// slot ring), per-template-node launchers and the SI executor.
+//
+// Ownership: dh_ctx owns streams, events and the communicator; dh_model owns
+// one device slab (the pool) carved into model state, L+1 activation slots and
+// one forward + one backward transient set. One host thread drives one ctx.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dh_capi.h"
+#include "weft/op_model.hpp"
+#include "weft/overlap_profile.hpp"
+#include "weft/pairing_search.hpp"
+
+namespace dh {
+
+int set_error(int code, const char* msg);
+inline int set_error(int code, const std::string& msg) { return set_error(code, msg.c_str()); }
+int cuda_fail(cudaError_t e, const char* what);
+
+#define RT_CUDA(expr)                                            \
+    do {                                                         \
+        cudaError_t rt_e_ = (expr);                              \
+        if (rt_e_ != cudaSuccess) return ::dh::cuda_fail(rt_e_, #expr); \
+    } while (0)
+#define RT_TRY(expr)                 \
+    do {                             \
+        int rt_rc_ = (expr);         \
+        if (rt_rc_ != DH_OK) return rt_rc_; \
+    } while (0)
+
+constexpr int kLanes = 3;  // weft::Lane: compute, local_comm, cross_comm
+
+// ------------------------------------------------------------------ collectives
+
+class Comm {
+public:
+    virtual ~Comm() = default;
+    // recv[r*count .. (r+1)*count) = send of rank r (bf16 elements)
+    virtual int all_gather(const void* send, void* recv, size_t count, cudaStream_t s) = 0;
+    // recv = sum over ranks of send[rank*count .. (rank+1)*count) (bf16)
+    virtual int reduce_scatter(const void* send, void* recv, size_t count, cudaStream_t s) = 0;
+    virtual int all_reduce_f32(float* buf, size_t count, cudaStream_t s) = 0;
+    virtual bool capturable() const = 0;
+    virtual const char* name() const = 0;
+};
+
+std::unique_ptr<Comm> make_nccl_comm(int rank, int size, const void* unique_id, int max_ctas,
+                                     int* rc);
+struct LoopbackGroup;
+std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* group, int rank, int* rc);
+
+struct Ctx {
+    int device = 0;
+    int tp_rank = 0, tp_size = 1;
+    int comm_ctas = 0;
+    std::array<cudaStream_t, kLanes> lane{};
+    std::unique_ptr<Comm> comm;
+    int sm_count = 148;
+};
+
+// ------------------------------------------------------------------ model
+
+struct ModelCfg {
+    int hidden = 0, ffn = 0, n_heads = 0, n_kv_heads = 0, head_dim = 0, layers = 0, seq = 0;
+    int micro_batches = 2;
+    float rope_theta = 500000.f, eps = 1e-5f;
+    unsigned long long seed = 1234;
+    float init_std = 0.02f;
+    // derived (per TP rank)
+    int tp = 1, rank = 0;
+    int tok_loc = 0;  // seq / tp (sequence-parallel shard)
+    int nq_l = 0, nkv_l = 0, qkv_n = 0, ffn_l = 0, attn_n = 0;
+};
+
+// Byte-offset view into the pool.
+struct Buf {
+    size_t off = 0, bytes = 0;
+};
+
+// Saved activations of one (strand, layer): lifetime = forward of that layer
+// to its backward. L+1 of these form the ring shared by both strands.
+struct Slot {
+    Buf out, rstd0, ln0_full, qkv, o, lse, x1, rstd1, ln1_full, gate, up, act;
+};
+
+struct FwdScratch {
+    Buf ln_loc, part, rs_out;
+};
+
+struct BwdScratch {
+    Buf grad[2], d_x1, dy_full, d_act, d_gate, d_up, dx_part, dx1_full, d_o, dqkv, attn_scratch,
+        ln_partial, rs_out;
+};
+
+struct LayerParams {
+    // offsets in elements into the flat parameter arrays
+    size_t g0, g1, wqkv, wo, wg, wu, wd;
+};
+
+struct Model;
+
+// One launch of the lowered schedule.
+struct Op {
+    int strand = 0;   // micro-batch index
+    int layer = 0;
+    int node = 0;     // template node id (op_model.cpp kDenseNodes)
+    int lane = 0;     // stream
+    int slot = 0;     // activation slot of (strand, layer)
+    int prev_slot = -1;  // slot holding this layer's input (layer - 1), -1 = strand input
+    bool first_dx = true;  // mlp_gate_dgrad/mlp_up_dgrad: whether this one overwrites dx_part
+    std::vector<int> waits;  // indices of ops whose completion this op waits for
+    bool barrier = false;    // step barrier before this op (all lanes joined)
+};
+
+struct Program {
+    std::vector<Op> ops;
+    int mode = 0;  // 0 SI, 1 sequential
+    std::vector<std::string> phases;
+};
+
+struct Model {
+    Ctx* ctx = nullptr;
+    ModelCfg cfg;
+    // pool
+    void* base = nullptr;
+    size_t pool_bytes = 0;
+    std::map<std::string, size_t> usage;  // bytes per category
+    // flat model state
+    size_t n_params = 0;
+    Buf w_bf16, w_master, w_grad, adam_m, adam_v;
+    std::vector<LayerParams> lp;
+    size_t gamma_elems = 0;  // LN gammas live at [0, gamma_elems) of the flat arrays
+    // activations
+    std::vector<Slot> slots;  // layers + 1
+    FwdScratch fs;
+    BwdScratch bs;
+    std::vector<Buf> mb_in, mb_dy;  // per micro-batch: input x0 and dL/dy (SP shards)
+    Buf loss;                       // fp32 [micro_batches]
+    // schedule
+    weft::LayerDag fwd_dag, bwd_dag;
+    weft::BestPlan plan;
+    bool have_plan = false;
+    Program prog;
+    std::vector<cudaEvent_t> events;
+    cudaGraphExec_t graph = nullptr;
+    int adam_step = 0;
+    int gemm_ctas_overlap = 0;  // SM cap for GEMMs that co-run with a collective
+    std::map<int, double> solo_us;  // node id -> solo time used for lowering
+
+    template <class T = void>
+    T* ptr(const Buf& b) const {
+        return reinterpret_cast<T*>(static_cast<char*>(base) + b.off);
+    }
+};
+
+int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out);
+void model_destroy(Model* m);
+int launch_node(Model& m, const Op& op, cudaStream_t s);
+int lower_program(Model& m, int mode);
+int run_program(Model& m, bool use_graph);
+int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s);
+
+}  // namespace dh
+
+struct dh_ctx : dh::Ctx {};
+struct dh_model : dh::Model {};

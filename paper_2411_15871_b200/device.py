@@ -151,7 +151,7 @@ def attn_bwd(q, k, v, o, lse, do, dq, dk, dv, n_q_heads, n_kv_heads, head_dim, s
     import torch
     tokens = q.shape[0]
     if scratch is None:
-        scratch = torch.empty(tokens * n_q_heads * (head_dim + 1), dtype=torch.float32,
+        scratch = torch.empty(tokens * n_q_heads * (2 * head_dim + 1), dtype=torch.float32,
                               device=q.device)
     check(lib().dh_attn_bwd(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o),
                             o.stride(0), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv),

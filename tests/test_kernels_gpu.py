@@ -128,3 +128,45 @@ def test_rope_roundtrip(theta, d):
     back = out.clone()
     dh.rope(back, hq, hk, d, theta, inverse=True)
     assert _rel(back, qkv) < 8e-3
+
+
+def _attn_ref(q, k, v, nq, nkv, d, scale):
+    T = q.shape[0]
+    qf = q.float().view(T, nq, d).transpose(0, 1)
+    kf = k.float().view(T, nkv, d).transpose(0, 1).repeat_interleave(nq // nkv, 0)
+    vf = v.float().view(T, nkv, d).transpose(0, 1).repeat_interleave(nq // nkv, 0)
+    s = (qf @ kf.transpose(1, 2)) * scale
+    mask = torch.ones(T, T, device=q.device, dtype=torch.bool).triu(1)
+    s = s.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ vf
+    return o.transpose(0, 1).reshape(T, nq * d), lse
+
+
+@pytest.mark.parametrize("T,nq,nkv,d", [(128, 4, 1, 64), (256, 4, 4, 128), (1000, 8, 2, 128),
+                                        (4096, 4, 1, 128)])
+def test_attention_fwd_bwd(T, nq, nkv, d):
+    scale = d ** -0.5
+    # packed qkv rows, as the qkv GEMM writes them
+    qkv = (torch.randn(T, (nq + 2 * nkv) * d, device="cuda") * 0.5).to(torch.bfloat16)
+    q, k, v = qkv[:, :nq * d], qkv[:, nq * d:(nq + nkv) * d], qkv[:, (nq + nkv) * d:]
+    o = torch.empty(T, nq * d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nq, T, device="cuda")
+    dh.attn_fwd(q, k, v, o, lse, nq, nkv, d, scale)
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    o_ref, lse_ref = _attn_ref(qf, kf, vf, nq, nkv, d, scale)
+    assert _rel(o, o_ref) < 6e-3
+    assert (lse - lse_ref).abs().max().item() < 2e-3
+    do = torch.randn_like(o)
+    o_ref.backward(do.float())
+    dqkv = torch.empty_like(qkv)
+    dq, dk, dv = dqkv[:, :nq * d], dqkv[:, nq * d:(nq + nkv) * d], dqkv[:, (nq + nkv) * d:]
+    dh.attn_bwd(q, k, v, o, lse, do, dq, dk, dv, nq, nkv, d, scale)
+    assert _rel(dq, qf.grad) < 1e-2
+    assert _rel(dk, kf.grad) < 1e-2
+    assert _rel(dv, vf.grad) < 1e-2
+    # determinism: a second backward is bit-identical
+    dqkv2 = torch.empty_like(qkv)
+    dh.attn_bwd(q, k, v, o, lse, do, dqkv2[:, :nq * d], dqkv2[:, nq * d:(nq + nkv) * d],
+                dqkv2[:, (nq + nkv) * d:], nq, nkv, d, scale)
+    assert torch.equal(dqkv, dqkv2)
