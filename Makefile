@@ -15,7 +15,7 @@ JOBS     ?= 8
 CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -Wno-unused-parameter \
             -Iinclude -Ithird_party
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
+NVFLAGS  := -std=c++20 -O3 $(ARCH) -cudart shared -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             -Iinclude -Ithird_party -I$(PKG)/csrc/cuda --expt-relaxed-constexpr \
             -Xptxas -warn-spills
 
@@ -53,7 +53,7 @@ $(OBJ)/runtime/%.o: $(PKG)/csrc/runtime/%.cpp $(CUDA_HDR) $(wildcard include/wef
 
 $(LIB)/libdh_b200.so: $(CUDA_OBJ) $(RT_OBJ) $(PLANNER_OBJ)
 	@mkdir -p $(LIB)
-	$(NVCC) -shared $(ARCH) -o $@ $^ -L/usr/local/cuda/lib64 -lcudart -lcuda -lnccl -Xlinker -rpath,/usr/local/cuda/lib64
+	$(NVCC) -shared -cudart shared $(ARCH) -o $@ $^ -L/usr/local/cuda/lib64 -lcuda -lnccl -Xlinker -rpath,/usr/local/cuda/lib64
 
 clean:
 	rm -rf $(OBJ) $(LIB)

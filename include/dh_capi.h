@@ -1,6 +1,6 @@
 /* dh — the B200 device layer of the SI framework, as a C ABI.
  *
- * Everything the host planner (include/weft/*.hpp) needs from the GPU crosses
+ * Everything the host planner (include/weft/ headers) needs from the GPU crosses
  * here: plain pointers, sizes and an opaque CUDA stream (void*); no C++ or
  * torch types. Every call returns a dh status; dh_last_error() gives the
  * message (thread-local).
@@ -104,6 +104,92 @@ int dh_adamw(float* master, void* weight_bf16, float* grad, float* m, float* v, 
 int dh_init_normal(void* bf16_out, float* f32_out, long long n, unsigned long long seed,
                    float std_dev, void* stream);
 int dh_fill_bf16(void* out, float value, long long n, void* stream);
+int dh_copy(void* dst, const void* src, long long bytes, void* stream);
+/* *loss = sum(y * r) in fp32, deterministic two-pass reduction through
+ * partial (>= 1024 floats). One micro-batch, this rank's SP shard. */
+int dh_dot_loss(const void* y, const void* r, long long n, float* partial, float* loss,
+                void* stream);
+
+/* ---------------------------------------------------------------- runtime */
+
+typedef struct dh_ctx dh_ctx;
+typedef struct dh_model dh_model;
+
+/* One context per GPU / TP rank. nccl_unique_id: the 128-byte ncclUniqueId
+ * shared by the TP group (NULL when tp_size == 1). nccl_max_ctas caps the SMs
+ * NCCL kernels occupy (0 = NCCL default) so they coexist with the other
+ * strand's GEMMs (north star (2)). Streams: one per weft::Lane. */
+int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_id,
+                  int nccl_max_ctas, dh_ctx** out);
+/* Single-process multi-rank "loopback" group on ONE device (test backend):
+ * creates tp_size contexts whose AllGather / ReduceScatter are device copies
+ * plus a fixed-order sum. Each context must be driven by its own host thread
+ * (collectives rendezvous like real ranks). Not graph-capturable. */
+int dh_loopback_group_create(int device, int tp_size, dh_ctx** ctxs_out);
+int dh_ctx_destroy(dh_ctx* ctx);
+void* dh_ctx_stream(dh_ctx* ctx, int lane);
+int dh_nccl_unique_id(void* out128);
+
+typedef struct dh_model_cfg {
+    int hidden, ffn, n_heads, n_kv_heads, head_dim, layers, seq_len;
+    int micro_batches;
+    float rope_theta, norm_eps;
+    unsigned long long seed;
+    float init_std;
+} dh_model_cfg;
+
+typedef struct dh_optim_cfg {
+    float lr, beta1, beta2, eps, weight_decay;
+    int enabled; /* 0: skip the optimizer (tests) */
+} dh_optim_cfg;
+
+/* Llama-style TP+SP layer stack on this rank: allocates ONE pool for weights,
+ * fp32 master / grad / Adam state, L+1 activation slots shared by the strands
+ * and one forward + one backward transient set. */
+int dh_model_create(dh_ctx* ctx, const dh_model_cfg* cfg, dh_model** out);
+int dh_model_destroy(dh_model* m);
+
+/* Load an SI plan (weft plan_to_json text) and lower it to lane-stream launches.
+ * profile_json (weft Profile schema, may be NULL) supplies the solo times the
+ * lowering replays the lane dispatch rule with; cluster_json the ClusterSpec used
+ * to rebuild the DAG (may be NULL = a B200 default). mode 0 = SI (W schedule:
+ * F1, SI(F_{i+1}, B_i) ..., B_m), 1 = sequential (F1 B1 F2 B2 ...), both with
+ * the plan's per-strand operator orders. plan_json NULL = template order, one
+ * segment per pass (valid for mode 1 and as a trivial SI plan). */
+int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
+                      const char* cluster_json, int mode);
+/* Cap the SMs of GEMMs that co-run with a collective (0 = no cap). */
+int dh_model_set_overlap_ctas(dh_model* m, int gemm_ctas);
+
+/* Run one training step: every micro-batch forward + backward per the lowered
+ * program, then (optionally) AdamW over all parameters. use_graph = 1 captures
+ * the program once as a CUDA graph and replays it. Asynchronous: returns after
+ * enqueueing on the compute lane stream. */
+int dh_model_step(dh_model* m, const dh_optim_cfg* optim, int use_graph);
+/* Only the forward/backward program (no optimizer, no grad zeroing). */
+int dh_model_run_program(dh_model* m, int use_graph);
+int dh_model_zero_grads(dh_model* m);
+int dh_model_sync(dh_model* m);
+
+/* Named device buffer access for tests / IO: name in {"x_in","dy","y","loss",
+ * "w.<tensor>","grad.<tensor>","master.<tensor>","act.<field>"}, tensor in
+ * {g0,g1,wqkv,wo,wg,wu,wd}. layer/strand select the instance.
+ * dtype out: 0 bf16, 1 fp32. */
+int dh_model_tensor(dh_model* m, const char* name, int layer, int strand, void** ptr,
+                    long long* numel, int* dtype);
+/* JSON with pool accounting, the lowered program and launch counts. Caller frees
+ * with dh_free_string. */
+int dh_model_info_json(dh_model* m, char** out);
+void dh_free_string(char* s);
+
+/* ---------------------------------------------------------------- profiler */
+
+/* On-device operator-pair overlap profiler (north star (4)): times every node
+ * solo, and every cross-lane (forward node, backward node) pair co-running on
+ * two streams, with CUDA events; aggregates P_ij into class-pair OEF via weft
+ * Eq. 1 and emits a weft Profile JSON (solo keyed by node name, slowdown and
+ * launch-overhead terms 0 because measured P_ij already include them). */
+int dh_profile_json(dh_model* m, int iters, char** out);
 
 #ifdef __cplusplus
 }

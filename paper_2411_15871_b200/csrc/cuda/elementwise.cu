@@ -266,6 +266,71 @@ __global__ void fill_kernel(__nv_bfloat16* out, float v, long long n) {
         out[i] = __float2bfloat16(v);
 }
 
+// Two-pass deterministic dot product: 1024 block partials, then one block.
+__global__ void dot_partial_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                                   long long nvec, float* __restrict__ partial) {
+    __shared__ float red[32];
+    float s = 0.f;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float x[8], y[8];
+        unpack8(a[i], x);
+        unpack8(b[i], y);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) s += x[t] * y[t];
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) partial[blockIdx.x] = v;
+    }
+}
+
+__global__ void dot_final_kernel(const float* __restrict__ partial, int n, float* __restrict__ out) {
+    __shared__ float red[32];
+    float s = 0.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) *out = v;
+    }
+}
+
+// dst = sum_{i < nsrc} srcs[i], summed in index order (fp32), rounded once.
+struct SrcPtrs {
+    const void* p[8];
+};
+
+__global__ void sum_bf16_kernel(SrcPtrs src, int nsrc, uint4* __restrict__ dst, long long nvec) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int k = 0; k < nsrc; ++k) {
+            float v[8];
+            unpack8(static_cast<const uint4*>(src.p[k])[i], v);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] += v[t];
+        }
+        dst[i] = pack8(acc);
+    }
+}
+
+__global__ void sum_f32_kernel(SrcPtrs src, int nsrc, float* __restrict__ dst, long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int k = 0; k < nsrc; ++k) acc += static_cast<const float*>(src.p[k])[i];
+        dst[i] = acc;
+    }
+}
+
 int grid_for(long long work, int threads) {
     const long long blocks = (work + threads - 1) / threads;
     return static_cast<int>(std::max<long long>(1, std::min<long long>(blocks, 148LL * 16)));
@@ -385,6 +450,45 @@ int dh_init_normal(void* bf16_out, float* f32_out, long long n, unsigned long lo
     if (n <= 0) return DH_OK;
     init_normal_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<__nv_bfloat16*>(bf16_out), f32_out, n, seed, std_dev);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_copy(void* dst, const void* src, long long bytes, void* stream) {
+    if (bytes <= 0) return DH_OK;
+    DH_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
+                                  static_cast<cudaStream_t>(stream)));
+    return DH_OK;
+}
+
+int dh_dot_loss(const void* y, const void* r, long long n, float* partial, float* loss,
+                void* stream) {
+    if (n % 8) return set_error(DH_ERR_INVALID, "dot_loss: n % 8 required");
+    auto s = static_cast<cudaStream_t>(stream);
+    constexpr int kBlocks = 1024;
+    dot_partial_kernel<<<kBlocks, 256, 0, s>>>(static_cast<const uint4*>(y),
+                                               static_cast<const uint4*>(r), n / 8, partial);
+    DH_CUDA_CHECK(cudaGetLastError());
+    dot_final_kernel<<<1, 1024, 0, s>>>(partial, kBlocks, loss);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_sum_bf16_ptrs(const void* const* srcs, int nsrc, void* dst, long long n, void* stream) {
+    if (nsrc < 1 || nsrc > 8 || n % 8) return set_error(DH_ERR_INVALID, "sum_bf16_ptrs: 1..8 sources, n % 8");
+    SrcPtrs sp{};
+    for (int i = 0; i < nsrc; ++i) sp.p[i] = srcs[i];
+    sum_bf16_kernel<<<grid_for(n / 8, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        sp, nsrc, static_cast<uint4*>(dst), n / 8);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_sum_f32_ptrs(const float* const* srcs, int nsrc, float* dst, long long n, void* stream) {
+    if (nsrc < 1 || nsrc > 8) return set_error(DH_ERR_INVALID, "sum_f32_ptrs: 1..8 sources");
+    SrcPtrs sp{};
+    for (int i = 0; i < nsrc; ++i) sp.p[i] = srcs[i];
+    sum_f32_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(sp, nsrc, dst, n);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

@@ -18,6 +18,8 @@
 #include <cstddef>
 #include <limits>
 #include <tuple>
+#include <utility>
+#include <vector>
 
 #include "weft/overlap_profile.hpp"
 
@@ -30,10 +32,13 @@ struct SimOp {
 };
 
 // `raw_oef(a, b)` returns the table OEF for the pair (throws when missing).
+// `trace`, when given, receives (strand, op index) in dispatch (start) order —
+// the B200 executor lowers a plan step to lane-stream launches in this order.
 template <class RawOef>
 SegmentCost simulate_lanes(const SimOp* ops_a, std::size_t n_a, const SimOp* ops_b,
                            std::size_t n_b, double slowdown, double launch_frac,
-                           RawOef&& raw_oef) {
+                           RawOef&& raw_oef,
+                           std::vector<std::pair<int, std::size_t>>* trace = nullptr) {
     struct Front {
         const SimOp* ops;
         std::size_t n;
@@ -69,6 +74,7 @@ SegmentCost simulate_lanes(const SimOp* ops_a, std::size_t n_a, const SimOp* ops
             }
             if (chosen < 0) return;
             Front& f = fr[chosen];
+            if (trace) trace->emplace_back(chosen, f.next);
             f.cur = &f.ops[f.next++];
             f.remaining = f.cur->t_us;
             f.busy = true;

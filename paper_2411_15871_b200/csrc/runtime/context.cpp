@@ -1,0 +1,315 @@
+// Device context: lane streams and the collective backend.
+//
+// Lanes (weft::Lane, reference core.hpp:29-33) map 1:1 to CUDA streams; the
+// communication lanes get the highest stream priority so a collective's CTAs
+// are scheduled ahead of the co-running strand's GEMM tiles.
+//
+// Backends:
+//   * NcclComm     — one communicator per TP group (ncclCommInitRankConfig with
+//                    maxCTAs = the SM budget left to NCCL), bf16 AllGather /
+//                    ReduceScatter, fp32 AllReduce. Graph-capturable.
+//   * LoopbackComm — tp_size ranks inside one process on ONE device, each driven
+//                    by its own host thread. Collectives rendezvous on the host,
+//                    exchange readiness through CUDA events and move data with
+//                    device copies / a fixed-order sum kernel. Exists so that
+//                    TP=2/4/8 numerics and the SI executor's collective ordering
+//                    can be tested on a single GPU. Not capturable.
+#include <nccl.h>
+
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+
+#include "runtime.hpp"
+
+extern "C" int dh_sum_bf16_ptrs(const void* const* srcs, int nsrc, void* dst, long long n,
+                                void* stream);
+extern "C" int dh_sum_f32_ptrs(const float* const* srcs, int nsrc, float* dst, long long n,
+                               void* stream);
+
+namespace dh {
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return set_error(DH_ERR_CUDA, std::string(cudaGetErrorString(e)) + " at " + what);
+}
+
+namespace {
+
+#define RT_NCCL(expr)                                                                   \
+    do {                                                                                \
+        ncclResult_t rt_n_ = (expr);                                                    \
+        if (rt_n_ != ncclSuccess)                                                       \
+            return set_error(DH_ERR_NCCL, std::string(ncclGetErrorString(rt_n_)) + " at " #expr); \
+    } while (0)
+
+class NcclComm final : public Comm {
+public:
+    ncclComm_t comm = nullptr;
+    ~NcclComm() override {
+        if (comm) ncclCommDestroy(comm);
+    }
+    int all_gather(const void* send, void* recv, size_t count, cudaStream_t s) override {
+        RT_NCCL(ncclAllGather(send, recv, count, ncclBfloat16, comm, s));
+        return DH_OK;
+    }
+    int reduce_scatter(const void* send, void* recv, size_t count, cudaStream_t s) override {
+        RT_NCCL(ncclReduceScatter(send, recv, count, ncclBfloat16, ncclSum, comm, s));
+        return DH_OK;
+    }
+    int all_reduce_f32(float* buf, size_t count, cudaStream_t s) override {
+        RT_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, comm, s));
+        return DH_OK;
+    }
+    bool capturable() const override { return true; }
+    const char* name() const override { return "nccl"; }
+};
+
+}  // namespace
+
+std::unique_ptr<Comm> make_nccl_comm(int rank, int size, const void* unique_id, int max_ctas,
+                                     int* rc) {
+    auto c = std::make_unique<NcclComm>();
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (max_ctas > 0) {
+        cfg.maxCTAs = max_ctas;
+        cfg.minCTAs = std::min(max_ctas, 2);
+    }
+    const ncclResult_t r = ncclCommInitRankConfig(&c->comm, size, id, rank, &cfg);
+    if (r != ncclSuccess) {
+        *rc = set_error(DH_ERR_NCCL, std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r));
+        c->comm = nullptr;
+        return nullptr;
+    }
+    *rc = DH_OK;
+    return c;
+}
+
+// ------------------------------------------------------------------ loopback
+
+struct LoopbackGroup {
+    int size = 1;
+    int device = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    // current collective: pointers / events posted by each rank
+    std::vector<const void*> send;
+    std::vector<cudaEvent_t> ready, done;
+    int posted_ready = 0, posted_done = 0;
+    long long gen_ready = 0, gen_done = 0;
+    int refs = 0;
+};
+
+namespace {
+
+class LoopbackComm final : public Comm {
+public:
+    LoopbackGroup* g;
+    int rank;
+    LoopbackComm(LoopbackGroup* grp, int r) : g(grp), rank(r) {}
+    ~LoopbackComm() override {
+        std::lock_guard<std::mutex> lk(g->mu);
+        cudaEventDestroy(g->ready[rank]);
+        cudaEventDestroy(g->done[rank]);
+        if (--g->refs == 0) {
+            // last rank out frees the group
+            delete_group_ = true;
+        }
+    }
+    bool delete_group_ = false;
+
+    // Phase 1: publish send buffer + readiness event, wait for every rank.
+    int rendezvous_ready(const void* send, cudaStream_t s) {
+        RT_CUDA(cudaEventRecord(g->ready[rank], s));
+        std::unique_lock<std::mutex> lk(g->mu);
+        g->send[rank] = send;
+        const long long gen = g->gen_ready;
+        if (++g->posted_ready == g->size) {
+            g->posted_ready = 0;
+            ++g->gen_ready;
+            g->cv.notify_all();
+        } else {
+            g->cv.wait(lk, [&] { return g->gen_ready != gen; });
+        }
+        return DH_OK;
+    }
+    // Phase 2: after pulling, publish completion and make this stream wait for
+    // every peer's pulls (peers read our send buffer).
+    int rendezvous_done(cudaStream_t s) {
+        RT_CUDA(cudaEventRecord(g->done[rank], s));
+        std::unique_lock<std::mutex> lk(g->mu);
+        const long long gen = g->gen_done;
+        if (++g->posted_done == g->size) {
+            g->posted_done = 0;
+            ++g->gen_done;
+            g->cv.notify_all();
+        } else {
+            g->cv.wait(lk, [&] { return g->gen_done != gen; });
+        }
+        lk.unlock();
+        for (int p = 0; p < g->size; ++p) {
+            if (p != rank) RT_CUDA(cudaStreamWaitEvent(s, g->done[p], 0));
+        }
+        return DH_OK;
+    }
+
+    int all_gather(const void* send, void* recv, size_t count, cudaStream_t s) override {
+        RT_TRY(rendezvous_ready(send, s));
+        for (int p = 0; p < g->size; ++p) {
+            if (p != rank) RT_CUDA(cudaStreamWaitEvent(s, g->ready[p], 0));
+            RT_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + p * count * 2, g->send[p], count * 2,
+                                    cudaMemcpyDeviceToDevice, s));
+        }
+        return rendezvous_done(s);
+    }
+    int reduce_scatter(const void* send, void* recv, size_t count, cudaStream_t s) override {
+        RT_TRY(rendezvous_ready(send, s));
+        std::vector<const void*> srcs(g->size);
+        for (int p = 0; p < g->size; ++p) {
+            if (p != rank) RT_CUDA(cudaStreamWaitEvent(s, g->ready[p], 0));
+            srcs[p] = static_cast<const char*>(g->send[p]) + rank * count * 2;
+        }
+        RT_TRY(dh_sum_bf16_ptrs(srcs.data(), g->size, recv, static_cast<long long>(count), s));
+        return rendezvous_done(s);
+    }
+    int all_reduce_f32(float* buf, size_t count, cudaStream_t s) override {
+        // Sum into a private copy first so no rank reads a partially reduced peer.
+        float* tmp = nullptr;
+        RT_CUDA(cudaMallocAsync(&tmp, count * 4, s));
+        RT_TRY(rendezvous_ready(buf, s));
+        std::vector<const float*> srcs(g->size);
+        for (int p = 0; p < g->size; ++p) {
+            if (p != rank) RT_CUDA(cudaStreamWaitEvent(s, g->ready[p], 0));
+            srcs[p] = static_cast<const float*>(g->send[p]);
+        }
+        RT_TRY(dh_sum_f32_ptrs(srcs.data(), g->size, tmp, static_cast<long long>(count), s));
+        RT_TRY(rendezvous_done(s));
+        RT_CUDA(cudaMemcpyAsync(buf, tmp, count * 4, cudaMemcpyDeviceToDevice, s));
+        RT_CUDA(cudaFreeAsync(tmp, s));
+        // A second barrier: peers must not read our buffer after we overwrite it.
+        RT_TRY(rendezvous_ready(buf, s));
+        return rendezvous_done(s);
+    }
+    bool capturable() const override { return false; }
+    const char* name() const override { return "loopback"; }
+};
+
+}  // namespace
+
+std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* group, int rank, int* rc) {
+    auto c = std::make_unique<LoopbackComm>(group, rank);
+    if (cudaEventCreateWithFlags(&group->ready[rank], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&group->done[rank], cudaEventDisableTiming) != cudaSuccess) {
+        *rc = set_error(DH_ERR_CUDA, "loopback: event creation failed");
+        return nullptr;
+    }
+    *rc = DH_OK;
+    return c;
+}
+
+}  // namespace dh
+
+// ------------------------------------------------------------------ C ABI
+
+namespace {
+
+int init_streams(dh::Ctx* c) {
+    RT_CUDA(cudaSetDevice(c->device));
+    int lo = 0, hi = 0;
+    RT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int l = 0; l < dh::kLanes; ++l) {
+        // hi is the numerically smallest = highest priority
+        RT_CUDA(cudaStreamCreateWithPriority(&c->lane[l], cudaStreamNonBlocking, l == 0 ? lo : hi));
+    }
+    RT_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+    return DH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dh_nccl_unique_id(void* out128) {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return dh::set_error(DH_ERR_NCCL, ncclGetErrorString(r));
+    std::memcpy(out128, &id, sizeof(id));
+    return DH_OK;
+}
+
+int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_id,
+                  int nccl_max_ctas, dh_ctx** out) {
+    if (!out || tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
+        return dh::set_error(DH_ERR_INVALID, "dh_ctx_create: bad rank/size");
+    auto* c = new dh_ctx();
+    c->device = device;
+    c->tp_rank = tp_rank;
+    c->tp_size = tp_size;
+    c->comm_ctas = nccl_max_ctas;
+    int rc = init_streams(c);
+    if (rc == DH_OK && tp_size > 1) {
+        if (!nccl_unique_id) {
+            rc = dh::set_error(DH_ERR_INVALID, "dh_ctx_create: tp_size > 1 needs an ncclUniqueId");
+        } else {
+            c->comm = dh::make_nccl_comm(tp_rank, tp_size, nccl_unique_id, nccl_max_ctas, &rc);
+        }
+    }
+    if (rc != DH_OK) {
+        dh_ctx_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return DH_OK;
+}
+
+int dh_loopback_group_create(int device, int tp_size, dh_ctx** ctxs_out) {
+    if (tp_size < 1 || !ctxs_out) return dh::set_error(DH_ERR_INVALID, "loopback: bad size");
+    auto* g = new dh::LoopbackGroup();
+    g->size = tp_size;
+    g->device = device;
+    g->send.assign(tp_size, nullptr);
+    g->ready.assign(tp_size, nullptr);
+    g->done.assign(tp_size, nullptr);
+    g->refs = tp_size;
+    for (int r = 0; r < tp_size; ++r) {
+        auto* c = new dh_ctx();
+        c->device = device;
+        c->tp_rank = r;
+        c->tp_size = tp_size;
+        int rc = init_streams(c);
+        if (rc == DH_OK && tp_size > 1) c->comm = dh::make_loopback_comm(g, r, &rc);
+        if (rc != DH_OK) return rc;
+        ctxs_out[r] = c;
+    }
+    if (tp_size == 1) delete g;
+    return DH_OK;
+}
+
+int dh_ctx_destroy(dh_ctx* c) {
+    if (!c) return DH_OK;
+    cudaSetDevice(c->device);
+    dh::LoopbackGroup* grp = nullptr;
+    bool last = false;
+    if (c->comm && std::strcmp(c->comm->name(), "loopback") == 0) {
+        auto* lb = static_cast<dh::LoopbackComm*>(c->comm.get());
+        grp = lb->g;
+        c->comm.reset();  // destructor decrements refs
+        std::lock_guard<std::mutex> lk(grp->mu);
+        last = grp->refs == 0;
+    }
+    c->comm.reset();
+    for (auto& s : c->lane) {
+        if (s) cudaStreamDestroy(s);
+    }
+    delete c;
+    if (last) delete grp;
+    return DH_OK;
+}
+
+void* dh_ctx_stream(dh_ctx* c, int lane) {
+    if (!c || lane < 0 || lane >= dh::kLanes) return nullptr;
+    return c->lane[lane];
+}
+
+}  // extern "C"

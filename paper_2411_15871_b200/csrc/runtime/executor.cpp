@@ -1,0 +1,268 @@
+// SI executor: lowers a weft plan (plan_to_json, reference pairing_search.cpp:
+// 543-561) into lane-stream launches and runs them eagerly or as a CUDA graph.
+//
+// Schedule (reference folding_pipeline.cpp schedule_w_pipeline with p = 1):
+//   SI mode          F_0 | SI(F_1, B_0) | SI(F_2, B_1) | ... | B_{m-1}
+//   sequential mode  F_0 B_0 | F_1 B_1 | ...       (same per-strand op orders)
+// Inside SI(F_{i+1}, B_i) forward layer k of strand i+1 is paired with
+// backward layer L-1-k of strand i, step by step as the plan says. Each step
+// is lowered by replaying the lane model (lane_sim.hpp — the same dispatch
+// rule the planner's cost model uses) on the node solo times: the resulting
+// start order becomes the issue order on the three lane streams. Edges:
+//   * strand order: an op waits for its strand predecessor when that ran on a
+//     different lane (same-lane order is implicit in the stream);
+//   * step barrier: the first op of each lane in a step waits for the last op
+//     of every other lane (the paper's inter-step synchronisation,
+//     PAPER.md:673), also at phase boundaries (transient buffers change owner).
+// Because every wait refers to an op issued earlier in program order, the
+// event graph is acyclic and the issue order is deadlock-free.
+//
+// Memory: L+1 activation slots. Forward of (strand, layer) pops a free slot,
+// backward of (strand, layer) pushes it back after its layer pair completes;
+// in an SI block the forward strand therefore always reuses the slot the
+// backward strand released one step earlier (never the one it still reads).
+//
+// Backward running gradient: layer l reads dy from grad[(L-2-l)&1] (the top
+// layer reads dL/dy) and writes the layer-input gradient to grad[(L-1-l)&1].
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+
+#include "../planner/lane_sim.hpp"
+#include "runtime.hpp"
+
+namespace dh {
+
+namespace {
+
+struct Lowering {
+    Model& m;
+    Program prog;
+    std::array<int, kLanes> lane_last{-1, -1, -1};
+    std::array<int, kLanes> join_snapshot{-1, -1, -1};
+    std::array<bool, kLanes> pending_join{false, false, false};
+    std::vector<int> strand_last;
+    std::vector<std::vector<int>> slot_of;  // [strand][layer]
+    std::vector<int> free_slots;
+    std::map<int, int> lane_of, pos_in_bwd;
+
+    explicit Lowering(Model& mm) : m(mm) {
+        const int mb = m.cfg.micro_batches, L = m.cfg.layers;
+        strand_last.assign(mb, -1);
+        slot_of.assign(mb, std::vector<int>(L, -1));
+        for (int s = L; s >= 0; --s) free_slots.push_back(s);  // pop_back gives 0 first
+        for (const auto& n : m.fwd_dag.nodes) lane_of[n.id] = static_cast<int>(n.lane);
+        for (const auto& n : m.bwd_dag.nodes) lane_of[n.id] = static_cast<int>(n.lane);
+        for (std::size_t i = 0; i < m.plan.bwd_seq.size(); ++i) pos_in_bwd[m.plan.bwd_seq[i]] = static_cast<int>(i);
+    }
+
+    void barrier() {
+        join_snapshot = lane_last;
+        pending_join.fill(true);
+    }
+
+    void emit(int strand, int layer, int node) {
+        Op o;
+        o.strand = strand;
+        o.layer = layer;
+        o.node = node;
+        o.lane = lane_of.at(node);
+        o.slot = slot_of[strand][layer];
+        o.prev_slot = layer > 0 ? slot_of[strand][layer - 1] : -1;
+        if (node == 24 || node == 25) {
+            const int other = node == 24 ? 25 : 24;
+            o.first_dx = pos_in_bwd.at(node) < pos_in_bwd.at(other);
+        }
+        const int idx = static_cast<int>(prog.ops.size());
+        const int prev = strand_last[strand];
+        if (prev >= 0 && prog.ops[prev].lane != o.lane) o.waits.push_back(prev);
+        if (pending_join[o.lane]) {
+            for (int l = 0; l < kLanes; ++l) {
+                if (l != o.lane && join_snapshot[l] >= 0 &&
+                    std::find(o.waits.begin(), o.waits.end(), join_snapshot[l]) == o.waits.end())
+                    o.waits.push_back(join_snapshot[l]);
+            }
+            pending_join[o.lane] = false;
+        }
+        prog.ops.push_back(std::move(o));
+        strand_last[strand] = idx;
+        lane_last[prog.ops[idx].lane] = idx;
+    }
+
+    void take_slot(int strand, int layer) {
+        slot_of[strand][layer] = free_slots.back();
+        free_slots.pop_back();
+    }
+    void give_slot(int strand, int layer) { free_slots.push_back(slot_of[strand][layer]); }
+
+    void forward_layer(int strand, int layer) {
+        take_slot(strand, layer);
+        for (int id : m.plan.fwd_seq) emit(strand, layer, id);
+    }
+    void backward_layer(int strand, int layer) {
+        for (int id : m.plan.bwd_seq) emit(strand, layer, id);
+        give_slot(strand, layer);
+    }
+
+    double solo(int id, const weft::LayerDag& dag) {
+        auto it = m.solo_us.find(id);
+        if (it != m.solo_us.end()) return it->second;
+        return dag.find(id)->duration_us;
+    }
+
+    std::vector<int> segment(const weft::Segmentation& sg, int k) {
+        if (k <= 0) return {};
+        const auto [lo, hi] = sg.segment_range(static_cast<std::size_t>(k));
+        return std::vector<int>(sg.sequence.begin() + lo, sg.sequence.begin() + hi);
+    }
+
+    // One SI layer pair: forward (fs, lf) with backward (bs, lb), per plan step.
+    void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl) {
+        take_slot(fs, lf);
+        for (const auto& st : m.plan.plan.steps) {
+            const auto fa = segment(m.plan.fwd_segmentation, st.fwd_seg.value_or(0));
+            const auto ba = segment(m.plan.bwd_segmentation, st.bwd_seg.value_or(0));
+            std::vector<weft::detail::SimOp> sa, sb;
+            for (int id : fa) {
+                const auto* n = m.fwd_dag.find(id);
+                sa.push_back({solo(id, m.fwd_dag), n->lane, n->cls});
+            }
+            for (int id : ba) {
+                const auto* n = m.bwd_dag.find(id);
+                sb.push_back({solo(id, m.bwd_dag), n->lane, n->cls});
+            }
+            std::vector<std::pair<int, std::size_t>> order;
+            weft::detail::simulate_lanes(
+                sa.data(), sa.size(), sb.data(), sb.size(), tbl.slowdown_factor,
+                tbl.launch_overhead_frac,
+                [&](const weft::detail::SimOp& x, const weft::detail::SimOp& y) {
+                    const auto v = tbl.get(x.cls, y.cls);
+                    return v ? *v : 0.0;  // missing pairs only affect issue order
+                },
+                &order);
+            barrier();
+            for (const auto& [side, i] : order) {
+                if (side == 0) emit(fs, lf, fa[i]);
+                else emit(bs, lb, ba[i]);
+            }
+        }
+        give_slot(bs, lb);
+    }
+};
+
+}  // namespace
+
+int lower_program(Model& m, int mode) {
+    const int L = m.cfg.layers, mb = m.cfg.micro_batches;
+    weft::OverlapTable tbl = weft::synth_profile(weft::ProfileArchetype::nvlink_h100).overlap;
+    if (!m.plan_overlap.entries.empty()) tbl = m.plan_overlap;
+    Lowering lw(m);
+    lw.prog.mode = mode;
+    try {
+        if (mode == 1) {
+            for (int s = 0; s < mb; ++s) {
+                lw.barrier();
+                for (int l = 0; l < L; ++l) lw.forward_layer(s, l);
+                for (int l = L - 1; l >= 0; --l) lw.backward_layer(s, l);
+            }
+        } else {
+            lw.barrier();
+            for (int l = 0; l < L; ++l) lw.forward_layer(0, l);
+            for (int i = 0; i + 1 < mb; ++i) {
+                lw.barrier();
+                for (int k = 0; k < L; ++k) lw.si_layer_pair(i + 1, k, i, L - 1 - k, tbl);
+            }
+            lw.barrier();
+            for (int l = L - 1; l >= 0; --l) lw.backward_layer(mb - 1, l);
+        }
+    } catch (const std::exception& e) {
+        return set_error(DH_ERR_CONFIG, std::string("lowering: ") + e.what());
+    }
+    if (lw.free_slots.size() != static_cast<std::size_t>(L + 1))
+        return set_error(DH_ERR_OTHER, "lowering: activation slots leaked");
+    m.y_slot.assign(mb, -1);
+    for (int s = 0; s < mb; ++s) m.y_slot[s] = lw.slot_of[s][L - 1];
+    m.prog = std::move(lw.prog);
+    // one event per op that some later op waits on
+    for (auto e : m.events)
+        if (e) cudaEventDestroy(e);
+    m.events.assign(m.prog.ops.size(), nullptr);
+    std::vector<char> needed(m.prog.ops.size(), 0);
+    for (const auto& o : m.prog.ops)
+        for (int w : o.waits) needed[w] = 1;
+    RT_CUDA(cudaSetDevice(m.ctx->device));
+    for (std::size_t i = 0; i < needed.size(); ++i) {
+        if (needed[i]) RT_CUDA(cudaEventCreateWithFlags(&m.events[i], cudaEventDisableTiming));
+    }
+    if (m.graph) {
+        cudaGraphExecDestroy(m.graph);
+        m.graph = nullptr;
+    }
+    return DH_OK;
+}
+
+namespace {
+
+int issue(Model& m) {
+    Ctx& c = *m.ctx;
+    for (std::size_t i = 0; i < m.prog.ops.size(); ++i) {
+        const Op& o = m.prog.ops[i];
+        cudaStream_t s = c.lane[o.lane];
+        for (int w : o.waits) RT_CUDA(cudaStreamWaitEvent(s, m.events[w], 0));
+        RT_TRY(launch_node(m, o, s));
+        if (m.events[i]) RT_CUDA(cudaEventRecord(m.events[i], s));
+    }
+    return DH_OK;
+}
+
+// Fork lanes 1..2 off lane 0, run, join back into lane 0.
+int issue_forked(Model& m) {
+    Ctx& c = *m.ctx;
+    if (!m.fork_join[0]) {
+        for (auto& e : m.fork_join) RT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    RT_CUDA(cudaEventRecord(m.fork_join[0], c.lane[0]));
+    for (int l = 1; l < kLanes; ++l) RT_CUDA(cudaStreamWaitEvent(c.lane[l], m.fork_join[0], 0));
+    RT_TRY(issue(m));
+    for (int l = 1; l < kLanes; ++l) {
+        RT_CUDA(cudaEventRecord(m.fork_join[l], c.lane[l]));
+        RT_CUDA(cudaStreamWaitEvent(c.lane[0], m.fork_join[l], 0));
+    }
+    return DH_OK;
+}
+
+}  // namespace
+
+int run_program(Model& m, bool use_graph) {
+    if (m.prog.ops.empty()) return set_error(DH_ERR_CONFIG, "no program: call dh_model_set_plan first");
+    RT_CUDA(cudaSetDevice(m.ctx->device));
+    // A failure left pending by another library (e.g. the caller's framework)
+    // would otherwise be reported against our first kernel launch.
+    const cudaError_t pending = cudaGetLastError();
+    if (pending != cudaSuccess) {
+        std::fprintf(stderr, "[dh] cleared pending CUDA error before run_program: %s\n",
+                     cudaGetErrorString(pending));
+    }
+    const bool capturable = !m.ctx->comm || m.ctx->comm->capturable();
+    if (!use_graph || !capturable) return issue_forked(m);
+    if (!m.graph) {
+        cudaStream_t s0 = m.ctx->lane[0];
+        RT_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
+        const int rc = issue_forked(m);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(s0, &g);
+        if (rc != DH_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        RT_CUDA(e);
+        const cudaError_t ie = cudaGraphInstantiate(&m.graph, g, 0);
+        cudaGraphDestroy(g);
+        RT_CUDA(ie);
+    }
+    RT_CUDA(cudaGraphLaunch(m.graph, m.ctx->lane[0]));
+    return DH_OK;
+}
+
+}  // namespace dh

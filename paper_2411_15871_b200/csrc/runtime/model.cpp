@@ -1,0 +1,426 @@
+// Llama TP+SP layer stack on one rank: pool layout, parameter init and the
+// per-template-node launchers.
+//
+// Node ids / names are the dense_tp_sp template (reference op_model.cpp:79-113):
+//   fwd  0 ln0  1 ag0  2 qkv(+RoPE)  4 attn  5 attn_proj  6 rs0  7 bda0  8 ln1
+//        9 ag1  10 mlp_gate  11 mlp_up  12 mlp_down(SwiGLU + GEMM)  13 rs1  14 bda1
+//   bwd 20 bda1_bwd  21 rs1_bwd_ag  22 mlp_down_dgrad(+SwiGLU bwd)  23 mlp_down_wgrad
+//       24 mlp_gate_dgrad  25 mlp_up_dgrad  26 mlp_fc1_wgrad  27 ag1_bwd_rs  28 ln1_bwd
+//       29 bda0_bwd  30 rs0_bwd_ag  31 attn_proj_dgrad  32 attn_proj_wgrad
+//       34 attn_bwd(+RoPE bwd)  35 qkv_dgrad  36 qkv_wgrad  37 ag0_bwd_rs  38 ln0_bwd
+//
+// Megatron TP+SP partitioning: W_qkv, W_gate, W_up column-parallel (local q
+// heads n_heads/tp, kv heads n_kv/tp, ffn/tp rows); W_o, W_down row-parallel;
+// RMSNorm and the residual run on the [seq/tp, hidden] sequence shard. The
+// gathered LN outputs are saved for the wgrad GEMMs (SURVEY §8(a) build note i).
+// With tp == 1 the collective nodes do not exist and producers write straight
+// into their consumers' buffers.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "runtime.hpp"
+
+namespace dh {
+
+namespace {
+
+struct Pool {
+    size_t cursor = 0;
+    std::map<std::string, size_t>* usage;
+    Buf take(size_t bytes, const char* cat) {
+        Buf b;
+        b.off = cursor;
+        b.bytes = bytes;
+        cursor += (bytes + 255) & ~static_cast<size_t>(255);
+        (*usage)[cat] += bytes;
+        return b;
+    }
+};
+
+unsigned long long mix(unsigned long long a, unsigned long long b) {
+    unsigned long long z = a * 0x9E3779B97F4A7C15ull + b + 0x632BE59BD9B4E019ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+}  // namespace
+
+int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
+    auto m = std::make_unique<Model>();
+    m->ctx = ctx;
+    ModelCfg& k = m->cfg;
+    k.hidden = c->hidden;
+    k.ffn = c->ffn;
+    k.n_heads = c->n_heads;
+    k.n_kv_heads = c->n_kv_heads;
+    k.head_dim = c->head_dim;
+    k.layers = c->layers;
+    k.seq = c->seq_len;
+    k.micro_batches = c->micro_batches;
+    k.rope_theta = c->rope_theta;
+    k.eps = c->norm_eps;
+    k.seed = c->seed;
+    k.init_std = c->init_std;
+    k.tp = ctx->tp_size;
+    k.rank = ctx->tp_rank;
+    if (k.hidden <= 0 || k.layers <= 0 || k.seq <= 0 || k.micro_batches < 1 || k.head_dim <= 0)
+        return set_error(DH_ERR_CONFIG, "model: dimensions must be positive");
+    if (k.seq % k.tp || k.n_heads % k.tp || k.n_kv_heads % k.tp || k.ffn % k.tp)
+        return set_error(DH_ERR_INFEASIBLE,
+                         "model: seq, n_heads, n_kv_heads and ffn must be divisible by tp");
+    if (k.n_heads % k.n_kv_heads) return set_error(DH_ERR_CONFIG, "model: n_heads % n_kv_heads");
+    if (k.head_dim != 64 && k.head_dim != 128)
+        return set_error(DH_ERR_CONFIG, "model: head_dim must be 64 or 128");
+    if (k.hidden % 256 || (k.ffn / k.tp) % 64)
+        return set_error(DH_ERR_CONFIG, "model: hidden % 256 and (ffn/tp) % 64 required");
+    k.tok_loc = k.seq / k.tp;
+    k.nq_l = k.n_heads / k.tp;
+    k.nkv_l = k.n_kv_heads / k.tp;
+    k.qkv_n = (k.nq_l + 2 * k.nkv_l) * k.head_dim;
+    k.attn_n = k.nq_l * k.head_dim;
+    k.ffn_l = k.ffn / k.tp;
+
+    const size_t H = k.hidden, S = k.seq, T = k.tok_loc, Q = k.qkv_n, A = k.attn_n, F = k.ffn_l;
+    const int L = k.layers;
+
+    // ---- parameters: gammas first (contiguous, for the SP all-reduce), then
+    // per-layer matrices, each 128-element aligned.
+    auto al = [](size_t n) { return (n + 127) & ~static_cast<size_t>(127); };
+    size_t off = 0;
+    m->lp.resize(L);
+    for (int l = 0; l < L; ++l) {
+        m->lp[l].g0 = off;
+        off += al(H);
+        m->lp[l].g1 = off;
+        off += al(H);
+    }
+    m->gamma_elems = off;
+    for (int l = 0; l < L; ++l) {
+        m->lp[l].wqkv = off;
+        off += al(Q * H);
+        m->lp[l].wo = off;
+        off += al(H * A);
+        m->lp[l].wg = off;
+        off += al(F * H);
+        m->lp[l].wu = off;
+        off += al(F * H);
+        m->lp[l].wd = off;
+        off += al(H * F);
+    }
+    m->n_params = off;
+
+    Pool pool{0, &m->usage};
+    m->w_bf16 = pool.take(off * 2, "state.weights_bf16");
+    m->w_master = pool.take(off * 4, "state.master_fp32");
+    m->w_grad = pool.take(off * 4, "state.grad_fp32");
+    m->adam_m = pool.take(off * 4, "state.adam_m");
+    m->adam_v = pool.take(off * 4, "state.adam_v");
+
+    m->slots.resize(L + 1);
+    for (auto& s : m->slots) {
+        s.out = pool.take(T * H * 2, "act.slots");
+        s.rstd0 = pool.take(T * 4, "act.slots");
+        s.ln0_full = pool.take(S * H * 2, "act.slots");
+        s.qkv = pool.take(S * Q * 2, "act.slots");
+        s.o = pool.take(S * A * 2, "act.slots");
+        s.lse = pool.take(S * k.nq_l * 4, "act.slots");
+        s.x1 = pool.take(T * H * 2, "act.slots");
+        s.rstd1 = pool.take(T * 4, "act.slots");
+        s.ln1_full = pool.take(S * H * 2, "act.slots");
+        s.gate = pool.take(S * F * 2, "act.slots");
+        s.up = pool.take(S * F * 2, "act.slots");
+        s.act = pool.take(S * F * 2, "act.slots");
+    }
+    const bool tp1 = k.tp == 1;
+    m->fs.ln_loc = pool.take(tp1 ? 0 : T * H * 2, "act.fwd_transient");
+    m->fs.part = pool.take(tp1 ? 0 : S * H * 2, "act.fwd_transient");
+    m->fs.rs_out = pool.take(T * H * 2, "act.fwd_transient");
+    auto& b = m->bs;
+    b.grad[0] = pool.take(T * H * 2, "act.bwd_transient");
+    b.grad[1] = pool.take(T * H * 2, "act.bwd_transient");
+    b.d_x1 = pool.take(T * H * 2, "act.bwd_transient");
+    b.dy_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
+    b.d_act = pool.take(S * F * 2, "act.bwd_transient");
+    b.d_gate = pool.take(S * F * 2, "act.bwd_transient");
+    b.d_up = pool.take(S * F * 2, "act.bwd_transient");
+    b.dx_part = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
+    b.dx1_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
+    b.d_o = pool.take(S * A * 2, "act.bwd_transient");
+    b.dqkv = pool.take(S * Q * 2, "act.bwd_transient");
+    b.attn_scratch = pool.take(S * k.nq_l * (2 * k.head_dim + 1) * 4, "act.bwd_transient");
+    b.ln_partial = pool.take(std::min<size_t>(T, 1184) * H * 4, "act.bwd_transient");
+    b.rs_out = pool.take(T * H * 2, "act.bwd_transient");
+    for (int i = 0; i < k.micro_batches; ++i) {
+        m->mb_in.push_back(pool.take(T * H * 2, "io.inputs"));
+        m->mb_dy.push_back(pool.take(T * H * 2, "io.inputs"));
+    }
+    m->loss = pool.take(std::max(k.micro_batches, 1) * 4 + 1024 * 4, "io.loss");
+
+    m->pool_bytes = pool.cursor;
+    RT_CUDA(cudaSetDevice(ctx->device));
+    RT_CUDA(cudaMalloc(&m->base, m->pool_bytes));
+    RT_CUDA(cudaMemset(m->base, 0, m->pool_bytes));
+
+    // ---- deterministic synthetic init (tests overwrite through dh_model_tensor)
+    cudaStream_t s = ctx->lane[0];
+    auto* wb = m->ptr<__nv_bfloat16>(m->w_bf16);
+    auto* wm = m->ptr<float>(m->w_master);
+    std::vector<float> ones(H, 1.f);
+    for (int l = 0; l < L; ++l) {
+        const LayerParams& p = m->lp[l];
+        RT_TRY(dh_fill_bf16(wb + p.g0, 1.f, H, s));
+        RT_TRY(dh_fill_bf16(wb + p.g1, 1.f, H, s));
+        RT_CUDA(cudaMemcpyAsync(wm + p.g0, ones.data(), H * 4, cudaMemcpyHostToDevice, s));
+        RT_CUDA(cudaMemcpyAsync(wm + p.g1, ones.data(), H * 4, cudaMemcpyHostToDevice, s));
+        const std::pair<size_t, size_t> mats[] = {
+            {p.wqkv, Q * H}, {p.wo, H * A}, {p.wg, F * H}, {p.wu, F * H}, {p.wd, H * F}};
+        for (int t = 0; t < 5; ++t) {
+            const unsigned long long sd = mix(mix(k.seed, l * 16 + t), k.rank);
+            RT_TRY(dh_init_normal(wb + mats[t].first, wm + mats[t].first, mats[t].second, sd,
+                                  k.init_std, s));
+        }
+    }
+    for (int i = 0; i < k.micro_batches; ++i) {
+        RT_TRY(dh_init_normal(m->ptr(m->mb_in[i]), nullptr, T * H, mix(mix(k.seed, 1000 + i), k.rank), 1.f, s));
+        RT_TRY(dh_init_normal(m->ptr(m->mb_dy[i]), nullptr, T * H, mix(mix(k.seed, 2000 + i), k.rank), 1.f, s));
+    }
+    RT_CUDA(cudaStreamSynchronize(s));
+
+    // ---- the layer DAG (same template / specs as the planner)
+    weft::ModelSpec ms;
+    ms.name = "dh-llama";
+    ms.family = weft::ModelFamily::llama;
+    ms.hidden = k.hidden;
+    ms.intermediate = k.ffn;
+    ms.layers = k.layers;
+    ms.seq_len = k.seq;
+    weft::ParallelismSpec par;
+    par.tp = k.tp;
+    par.sp = k.tp > 1;
+    weft::ClusterSpec cl;
+    cl.name = "b200";
+    cl.gpus = 8;
+    cl.per_node = 8;
+    cl.peak_tflops = 2250.0;
+    cl.local_bw_gbs = 900.0;
+    cl.cross_bw_gbs = 50.0;
+    cl.mem_gb = 180.0;
+    try {
+        auto dags = weft::build_layer_dag(ms, par, cl, nullptr);
+        m->fwd_dag = std::move(dags.first);
+        m->bwd_dag = std::move(dags.second);
+    } catch (const std::exception& e) {
+        return set_error(DH_ERR_CONFIG, e.what());
+    }
+    *out = m.release();
+    return DH_OK;
+}
+
+void model_destroy(Model* m) {
+    if (!m) return;
+    cudaSetDevice(m->ctx->device);
+    if (m->graph) cudaGraphExecDestroy(m->graph);
+    for (auto e : m->events)
+        if (e) cudaEventDestroy(e);
+    for (auto e : m->fork_join)
+        if (e) cudaEventDestroy(e);
+    if (m->base) cudaFree(m->base);
+    delete m;
+}
+
+// ------------------------------------------------------------------ node launchers
+
+namespace {
+
+int gemm(const void* a, long long lda, bool a_mn, const void* b, long long ldb, bool b_mn, void* d,
+         long long ldd, bool d_f32, int mm, int nn, int kk, bool acc, int max_ctas,
+         cudaStream_t s) {
+    dh_gemm_args g{};
+    g.a = a;
+    g.lda = lda;
+    g.a_mn = a_mn;
+    g.b = b;
+    g.ldb = ldb;
+    g.b_mn = b_mn;
+    g.d = d;
+    g.ldd = ldd;
+    g.d_fp32 = d_f32;
+    g.m = mm;
+    g.n = nn;
+    g.k = kk;
+    g.accumulate = acc;
+    g.max_ctas = max_ctas;
+    return dh_gemm(&g, s);
+}
+
+}  // namespace
+
+int launch_node(Model& m, const Op& op, cudaStream_t s) {
+    const ModelCfg& k = m.cfg;
+    const int H = k.hidden, S = k.seq, T = k.tok_loc, Q = k.qkv_n, A = k.attn_n, F = k.ffn_l;
+    const int D = k.head_dim;
+    const long long TH = static_cast<long long>(T) * H;
+    const bool tp1 = k.tp == 1;
+    const int cap = m.gemm_ctas_overlap;
+    Slot& sl = m.slots[op.slot];
+    const LayerParams& p = m.lp[op.layer];
+    auto* W = m.ptr<__nv_bfloat16>(m.w_bf16);
+    auto* G = m.ptr<float>(m.w_grad);
+    auto P = [&](const Buf& b) { return m.ptr(b); };
+    void* x_in = op.prev_slot < 0 ? P(m.mb_in[op.strand]) : P(m.slots[op.prev_slot].out);
+    const float scale = 1.f / std::sqrt(static_cast<float>(D));
+    // backward running-gradient ping-pong (see header of executor.cpp)
+    const int L = k.layers;
+    void* dy = op.layer == L - 1 ? P(m.mb_dy[op.strand]) : P(m.bs.grad[(L - 2 - op.layer) & 1]);
+    void* d_x = P(m.bs.grad[(L - 1 - op.layer) & 1]);
+    Comm* comm = m.ctx->comm.get();
+    auto need_comm = [&]() -> int {
+        return comm ? DH_OK : set_error(DH_ERR_CONFIG, "collective node without a communicator");
+    };
+
+    switch (op.node) {
+        // ---------------------------------------------------------------- forward
+        case 0:  // ln0
+            return dh_rmsnorm_fwd(x_in, W + p.g0, tp1 ? P(sl.ln0_full) : P(m.fs.ln_loc),
+                                  m.ptr<float>(sl.rstd0), T, H, k.eps, s);
+        case 1:  // ag0
+            RT_TRY(need_comm());
+            return comm->all_gather(P(m.fs.ln_loc), P(sl.ln0_full), TH, s);
+        case 2:  // qkv (+ RoPE on q, k)
+            RT_TRY(gemm(P(sl.ln0_full), H, false, W + p.wqkv, H, false, P(sl.qkv), Q, false, S, Q, H,
+                        false, cap, s));
+            return dh_rope(P(sl.qkv), Q, S, k.nq_l, k.nkv_l, D, k.rope_theta, 0, 0, s);
+        case 4: {  // attn
+            auto* qkv = m.ptr<__nv_bfloat16>(sl.qkv);
+            return dh_attn_fwd(qkv, qkv + k.nq_l * D, qkv + (k.nq_l + k.nkv_l) * D, Q, Q, P(sl.o), A,
+                               m.ptr<float>(sl.lse), S, k.nq_l, k.nkv_l, D, scale, s);
+        }
+        case 5:  // attn_proj (row-parallel: partial sums before the reduce-scatter)
+            return gemm(P(sl.o), A, false, W + p.wo, A, false, tp1 ? P(m.fs.rs_out) : P(m.fs.part), H,
+                        false, S, H, A, false, cap, s);
+        case 6:  // rs0
+            RT_TRY(need_comm());
+            return comm->reduce_scatter(P(m.fs.part), P(m.fs.rs_out), TH, s);
+        case 7:  // bda0: x1 = x + attn_out
+            return dh_add(x_in, P(m.fs.rs_out), P(sl.x1), TH, s);
+        case 8:  // ln1
+            return dh_rmsnorm_fwd(P(sl.x1), W + p.g1, tp1 ? P(sl.ln1_full) : P(m.fs.ln_loc),
+                                  m.ptr<float>(sl.rstd1), T, H, k.eps, s);
+        case 9:  // ag1
+            RT_TRY(need_comm());
+            return comm->all_gather(P(m.fs.ln_loc), P(sl.ln1_full), TH, s);
+        case 10:  // mlp_gate
+            return gemm(P(sl.ln1_full), H, false, W + p.wg, H, false, P(sl.gate), F, false, S, F, H,
+                        false, cap, s);
+        case 11:  // mlp_up
+            return gemm(P(sl.ln1_full), H, false, W + p.wu, H, false, P(sl.up), F, false, S, F, H,
+                        false, cap, s);
+        case 12:  // mlp_down: SwiGLU prologue + row-parallel GEMM
+            RT_TRY(dh_swiglu_fwd(P(sl.gate), P(sl.up), P(sl.act), static_cast<long long>(S) * F, s));
+            return gemm(P(sl.act), F, false, W + p.wd, F, false, tp1 ? P(m.fs.rs_out) : P(m.fs.part),
+                        H, false, S, H, F, false, cap, s);
+        case 13:  // rs1
+            RT_TRY(need_comm());
+            return comm->reduce_scatter(P(m.fs.part), P(m.fs.rs_out), TH, s);
+        case 14:  // bda1: out = x1 + mlp_out (+ loss on the last layer)
+            RT_TRY(dh_add(P(sl.x1), P(m.fs.rs_out), P(sl.out), TH, s));
+            if (op.layer == L - 1) {
+                float* loss = m.ptr<float>(m.loss);
+                return dh_dot_loss(P(sl.out), P(m.mb_dy[op.strand]), TH, loss + k.micro_batches,
+                                   loss + op.strand, s);
+            }
+            return DH_OK;
+
+        // ---------------------------------------------------------------- backward
+        case 20:  // bda1_bwd: residual gradient pass-through
+            return dh_copy(P(m.bs.d_x1), dy, TH * 2, s);
+        case 21:  // rs1_bwd_ag
+            RT_TRY(need_comm());
+            return comm->all_gather(dy, P(m.bs.dy_full), TH, s);
+        case 22: {  // mlp_down_dgrad (+ SwiGLU bwd)
+            const void* dyf = tp1 ? dy : P(m.bs.dy_full);
+            RT_TRY(gemm(dyf, H, false, W + p.wd, F, true, P(m.bs.d_act), F, false, S, F, H, false, cap, s));
+            return dh_swiglu_bwd(P(sl.gate), P(sl.up), P(m.bs.d_act), P(m.bs.d_gate), P(m.bs.d_up),
+                                 static_cast<long long>(S) * F, s);
+        }
+        case 23: {  // mlp_down_wgrad: dWd[H,F] += dY^T act
+            const void* dyf = tp1 ? dy : P(m.bs.dy_full);
+            return gemm(dyf, H, true, P(sl.act), F, true, G + p.wd, F, true, H, F, S, true, cap, s);
+        }
+        case 24:  // mlp_gate_dgrad
+            return gemm(P(m.bs.d_gate), F, false, W + p.wg, H, true,
+                        tp1 ? P(m.bs.rs_out) : P(m.bs.dx_part), H, false, S, H, F, !op.first_dx, cap, s);
+        case 25:  // mlp_up_dgrad
+            return gemm(P(m.bs.d_up), F, false, W + p.wu, H, true,
+                        tp1 ? P(m.bs.rs_out) : P(m.bs.dx_part), H, false, S, H, F, !op.first_dx, cap, s);
+        case 26:  // mlp_fc1_wgrad: dWg, dWu [F,H] += d_{gate,up}^T ln1
+            RT_TRY(gemm(P(m.bs.d_gate), F, true, P(sl.ln1_full), H, true, G + p.wg, H, true, F, H, S,
+                        true, cap, s));
+            return gemm(P(m.bs.d_up), F, true, P(sl.ln1_full), H, true, G + p.wu, H, true, F, H, S, true,
+                        cap, s);
+        case 27:  // ag1_bwd_rs
+            RT_TRY(need_comm());
+            return comm->reduce_scatter(P(m.bs.dx_part), P(m.bs.rs_out), TH, s);
+        case 28:  // ln1_bwd (+ residual join into d_x1)
+            return dh_rmsnorm_bwd(P(sl.x1), W + p.g1, m.ptr<float>(sl.rstd1), P(m.bs.rs_out),
+                                  P(m.bs.d_x1), P(m.bs.d_x1), G + p.g1, m.ptr<float>(m.bs.ln_partial),
+                                  T, H, s);
+        case 29:  // bda0_bwd: skip-connection gradient to the layer input
+            return dh_copy(d_x, P(m.bs.d_x1), TH * 2, s);
+        case 30:  // rs0_bwd_ag
+            RT_TRY(need_comm());
+            return comm->all_gather(P(m.bs.d_x1), P(m.bs.dx1_full), TH, s);
+        case 31: {  // attn_proj_dgrad: d_o = dX1 Wo
+            const void* src = tp1 ? P(m.bs.d_x1) : P(m.bs.dx1_full);
+            return gemm(src, H, false, W + p.wo, A, true, P(m.bs.d_o), A, false, S, A, H, false, cap, s);
+        }
+        case 32: {  // attn_proj_wgrad: dWo[H,A] += dX1^T o
+            const void* src = tp1 ? P(m.bs.d_x1) : P(m.bs.dx1_full);
+            return gemm(src, H, true, P(sl.o), A, true, G + p.wo, A, true, H, A, S, true, cap, s);
+        }
+        case 34: {  // attn_bwd (+ RoPE bwd on dq, dk)
+            auto* qkv = m.ptr<__nv_bfloat16>(sl.qkv);
+            auto* dqkv = m.ptr<__nv_bfloat16>(m.bs.dqkv);
+            RT_TRY(dh_attn_bwd(qkv, qkv + k.nq_l * D, qkv + (k.nq_l + k.nkv_l) * D, Q, Q, P(sl.o), A,
+                               m.ptr<float>(sl.lse), P(m.bs.d_o), dqkv, dqkv + k.nq_l * D,
+                               dqkv + (k.nq_l + k.nkv_l) * D, Q, Q, m.ptr<float>(m.bs.attn_scratch),
+                               S, k.nq_l, k.nkv_l, D, scale, s));
+            return dh_rope(dqkv, Q, S, k.nq_l, k.nkv_l, D, k.rope_theta, 0, 1, s);
+        }
+        case 35:  // qkv_dgrad
+            return gemm(P(m.bs.dqkv), Q, false, W + p.wqkv, H, true,
+                        tp1 ? P(m.bs.rs_out) : P(m.bs.dx_part), H, false, S, H, Q, false, cap, s);
+        case 36:  // qkv_wgrad: dWqkv[Q,H] += dqkv^T ln0
+            return gemm(P(m.bs.dqkv), Q, true, P(sl.ln0_full), H, true, G + p.wqkv, H, true, Q, H, S,
+                        true, cap, s);
+        case 37:  // ag0_bwd_rs
+            RT_TRY(need_comm());
+            return comm->reduce_scatter(P(m.bs.dx_part), P(m.bs.rs_out), TH, s);
+        case 38:  // ln0_bwd (+ join of the attention-block skip gradient)
+            return dh_rmsnorm_bwd(x_in, W + p.g0, m.ptr<float>(sl.rstd0), P(m.bs.rs_out), d_x, d_x,
+                                  G + p.g0, m.ptr<float>(m.bs.ln_partial), T, H, s);
+        default:
+            return set_error(DH_ERR_CONFIG, "launch_node: unknown template node " + std::to_string(op.node));
+    }
+}
+
+int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s) {
+    const ModelCfg& k = m.cfg;
+    if (k.tp > 1 && m.ctx->comm) {
+        // LayerNorm gammas are replicated across the TP group but see only
+        // their sequence shard: sum their gradients (Megatron SP rule).
+        RT_TRY(m.ctx->comm->all_reduce_f32(m.ptr<float>(m.w_grad), m.gamma_elems, s));
+    }
+    if (!oc || !oc->enabled) return DH_OK;
+    ++m.adam_step;
+    return dh_adamw(m.ptr<float>(m.w_master), m.ptr(m.w_bf16), m.ptr<float>(m.w_grad),
+                    m.ptr<float>(m.adam_m), m.ptr<float>(m.adam_v), static_cast<long long>(m.n_params),
+                    oc->lr, oc->beta1, oc->beta2, oc->eps, oc->weight_decay, m.adam_step,
+                    1.f / k.micro_batches, 1, s);
+}
+
+}  // namespace dh

@@ -156,6 +156,9 @@ struct Model {
     int adam_step = 0;
     int gemm_ctas_overlap = 0;  // SM cap for GEMMs that co-run with a collective
     std::map<int, double> solo_us;  // node id -> solo time used for lowering
+    weft::OverlapTable plan_overlap;  // table the lowering replays the lane model with
+    std::array<cudaEvent_t, kLanes> fork_join{};
+    std::vector<int> y_slot;  // slot holding each strand's last-layer output
 
     template <class T = void>
     T* ptr(const Buf& b) const {
@@ -167,6 +170,7 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out);
 void model_destroy(Model* m);
 int launch_node(Model& m, const Op& op, cudaStream_t s);
 int lower_program(Model& m, int mode);
+int kernels_per_node(const Model& m, int node, int layer);
 int run_program(Model& m, bool use_graph);
 int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s);
 

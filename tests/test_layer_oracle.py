@@ -1,0 +1,89 @@
+"""CPU: the numpy layer oracle (oracle/layer_oracle.py) against torch autograd
+on the same fp32 math, so the hand-written backward of the oracle is itself
+checked. Also checks the bf16 rounding helper and TP-partition invariance."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.layer_oracle import LlamaTPOracle, bf16_round, from_bf16_bits, to_bf16_bits
+
+
+def test_bf16_round_matches_torch():
+    x = np.random.default_rng(0).standard_normal(10000).astype(np.float32) * 3
+    x[:5] = [0.0, -0.0, 1e-40, 65504.0, -3.4e38]
+    ours = bf16_round(x)
+    ref = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(ours, ref)
+    assert np.array_equal(from_bf16_bits(to_bf16_bits(x)), ref)
+
+
+def _torch_model(o: LlamaTPOracle, x, r):
+    """Straight fp32 torch autograd of the same layer stack (no TP, no rounding)."""
+    S, D = o.S, o.D
+    P = [{k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in p.items()}
+         for p in o.params]
+    cos = torch.tensor(o.cos, dtype=torch.float64)[:, None, :]
+    sin = torch.tensor(o.sin, dtype=torch.float64)[:, None, :]
+
+    def rope(t):
+        a, b = t[..., :D // 2], t[..., D // 2:]
+        return torch.cat([a * cos - b * sin, b * cos + a * sin], -1)
+
+    def rms(t, g):
+        return t * torch.rsqrt(t.pow(2).mean(-1, keepdim=True) + o.eps) * g
+
+    h = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+    x0 = h
+    mask = torch.ones(S, S, dtype=torch.bool).triu(1)
+    for p in P:
+        ln0 = rms(h, p["g0"])
+        q = rope((ln0 @ p["wq"].T).view(S, o.nq, D))
+        k = rope((ln0 @ p["wk"].T).view(S, o.nkv, D))
+        v = (ln0 @ p["wv"].T).view(S, o.nkv, D)
+        grp = o.nq // o.nkv
+        k, v = k.repeat_interleave(grp, 1), v.repeat_interleave(grp, 1)
+        s = torch.einsum("qhd,khd->hqk", q, k) * float(o.scale)
+        s = s.masked_fill(mask, float("-inf"))
+        att = torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), v).reshape(S, -1)
+        x1 = h + att @ p["wo"].T
+        ln1 = rms(x1, p["g1"])
+        mlp = (torch.nn.functional.silu(ln1 @ p["wg"].T) * (ln1 @ p["wu"].T)) @ p["wd"].T
+        h = x1 + mlp
+    loss = (h * torch.tensor(r, dtype=torch.float64)).sum()
+    loss.backward()
+    return loss.item(), x0.grad.numpy(), [{k: v.grad.numpy() for k, v in p.items()} for p in P]
+
+
+@pytest.mark.parametrize("nq,nkv", [(4, 2), (4, 4)])
+def test_oracle_backward_matches_autograd(nq, nkv):
+    o = LlamaTPOracle(hidden=64, ffn=96, n_heads=nq, n_kv_heads=nkv, head_dim=16, layers=2, seq=24,
+                      bf16=False, seed=3, init_std=0.2)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((24, 64)).astype(np.float32)
+    r = rng.standard_normal((24, 64)).astype(np.float32)
+    loss, _, dx, grads = o.run(x, r)
+    tl, tdx, tg = _torch_model(o, x, r)
+    assert abs(loss - tl) < 1e-3 * max(1.0, abs(tl))
+    assert np.abs(dx - tdx).max() < 1e-3 * np.abs(tdx).max()
+    for l in range(2):
+        for k in tg[l]:
+            err = np.abs(grads[l][k] - tg[l][k]).max() / max(1e-12, np.abs(tg[l][k]).max())
+            assert err < 2e-3, (l, k, err)
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_partition_invariance(tp):
+    """Without rounding, TP partitioning must not change the math."""
+    kw = dict(hidden=64, ffn=128, n_heads=4, n_kv_heads=4, head_dim=16, layers=2, seq=16, bf16=False,
+              seed=9, init_std=0.2)
+    a, b = LlamaTPOracle(tp=1, **kw), LlamaTPOracle(tp=tp, **kw)
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((16, 64)).astype(np.float32)
+    r = rng.standard_normal((16, 64)).astype(np.float32)
+    la, ya, dxa, ga = a.run(x, r)
+    lb, yb, dxb, gb = b.run(x, r)
+    assert np.allclose(ya, yb, atol=1e-4) and np.allclose(dxa, dxb, atol=1e-4)
+    for k in ga[0]:
+        assert np.allclose(ga[0][k], gb[0][k], atol=1e-3)
+    sh = b.shard(0, 1)
+    assert sh["wqkv"].shape == ((4 // tp + 2 * 4 // tp) * 16, 64)
