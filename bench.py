@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark: DHelix strand interleaving on B200 — Llama-3-8B-shaped layer stack.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One rank per GPU (torchrun for N > 1); the N ranks form ONE tensor-parallel
+group (TP = N, sequence parallel), i.e. the BASELINE.json config-2 layout at
+N = 8 and its TP sweep at N = 1, 2, 4. A step is a full training step of the
+32-layer Llama-3-8B-shaped stack (h 4096, ffn 14336, 32 q / 8 kv heads, head
+dim 128, seq 4096, bf16 with fp32 accumulation and fp32 master weights):
+`micro_batches` micro-batches forward + backward under the SI schedule
+(F1 | SI(F2,B1) | ... | Bm) followed by AdamW. Synthetic random-init weights
+and synthetic inputs (no network for checkpoints or data).
+
+Prints ONE JSON line (rank 0). Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks. Inputs (the 14 GB of bf16
+weights alone) are far larger than the 126 MB L2, so no flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B200_CLUSTER = {"name": "b200_8", "gpus": 8, "per_node": 8, "peak_tflops": 2250.0,
+                "local_bw_gbs": 900.0, "cross_bw_gbs": 50.0, "mem_gb": 180.0}
+SPEC_BF16_TFLOPS = 2250.0
+METRIC = "tokens/s & MFU per B200, SI vs sequential; exposed TP comm time per layer"
+
+
+# --------------------------------------------------------------------------- helpers
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_burst": d["bf16_tflops"],
+                "bf16_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "sm_max_mhz": d.get("sm_max_mhz"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_burst": 1590.0, "bf16_sustained": 1400.0,
+            "sm_max_mhz": 1965.0, "source": "fallback"}
+
+
+def layer_flops(shape, tp):
+    """Algorithmic FLOPs of one layer forward and backward for one micro-batch on
+    one TP rank, true GQA shapes: GEMMs 2mnk, causal attention
+    2*S^2*D per q head forward (QK^T + PV, half the square), backward 2x GEMM /
+    2.5x attention."""
+    S, H, F, D = shape.seq_len, shape.hidden, shape.ffn, shape.head_dim
+    q_out = (shape.n_heads + 2 * shape.n_kv_heads) * D
+    a_in = shape.n_heads * D
+    gemm_fwd = 2.0 * S * H * (q_out + a_in + 3 * F) / tp
+    attn_fwd = 2.0 * S * S * D * shape.n_heads / tp
+    return {"fwd": gemm_fwd + attn_fwd, "bwd": 2 * gemm_fwd + 2.5 * attn_fwd,
+            "gemm_fwd": gemm_fwd, "attn_fwd": attn_fwd}
+
+
+def comm_bytes_per_layer_pair(shape, tp):
+    """Wire bytes of the 8 TP collectives of one fwd + one bwd layer (reference
+    op_model.cpp:290-296: tokens*h*2*(tp-1)/tp each)."""
+    if tp == 1:
+        return 0
+    return 8 * int(shape.seq_len * shape.hidden * 2 * (tp - 1) / tp)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def run_reference(args, world, rank):
+    """The reference's CPU implementation of the path, timed on the host cores.
+    The reference planner (weft) has no layer math, so the tokens/s workload is
+    run by the oracle port (oracle/layer_oracle.py, numpy fp32 on every core);
+    the reference planner itself (oracle/_ref) is timed beside it when built."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.layer_oracle import LlamaTPOracle
+    from paper_2411_15871_b200.runtime import LLAMA3_8B as shape
+
+    sample_seq = args.ref_seq
+    orc = LlamaTPOracle(shape.hidden, shape.ffn, shape.n_heads, shape.n_kv_heads, shape.head_dim, 1,
+                        sample_seq, tp=1, theta=shape.rope_theta, bf16=False, seed=0, init_std=0.02)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((sample_seq, shape.hidden), dtype=np.float32)
+    r = rng.standard_normal((sample_seq, shape.hidden), dtype=np.float32)
+
+    def step():
+        grads = orc.zero_grads()
+        y, c = orc.layer_fwd(0, x)
+        orc.layer_bwd(0, c, r, grads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    # one layer fwd+bwd of one micro-batch -> tokens/s of the 32-layer stack
+    value = sample_seq / (dt * shape.layers)
+    sample = (f"1 of {shape.layers} layers, 1 micro-batch, seq {sample_seq} (GEMM cost per token "
+              f"exact; attention per token {shape.seq_len // sample_seq}x cheaper than at seq "
+              f"{shape.seq_len}), fwd+bwd per step, extrapolated x{shape.layers} layers")
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "llama3-8b-shaped layer stack fwd+bwd (CPU oracle port)",
+                       "model": "llama3-8b-shaped", "global_batch": 1, "seq_len": shape.seq_len,
+                       "parallelism": "none (host CPU)"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    ref_lib = os.path.join(ROOT, "oracle", "_ref", "libweft_ref.so")
+    if os.path.exists(ref_lib):
+        from paper_2411_15871_b200.planner import PlannerLib
+        ref = PlannerLib(ref_lib, "weft_ref_")
+        r = ref.search_si_plan(shape.planner_model(), {"tp": 8, "sp": True}, B200_CLUSTER,
+                               {"archetype": "nvlink_h100"}, repeat=5)
+        line["reference_planner_ms"] = round(r["search_ms"], 3)
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+
+def cpu_baseline_sample(shape):
+    """The oracle port on this host: one layer fwd+bwd, one micro-batch, full seq."""
+    import numpy as np
+    from oracle.layer_oracle import LlamaTPOracle
+    orc = LlamaTPOracle(shape.hidden, shape.ffn, shape.n_heads, shape.n_kv_heads, shape.head_dim, 1,
+                        shape.seq_len, tp=1, theta=shape.rope_theta, bf16=False, seed=0)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((shape.seq_len, shape.hidden), dtype=np.float32)
+    r = rng.standard_normal((shape.seq_len, shape.hidden), dtype=np.float32)
+    t0 = time.perf_counter()
+    y, c = orc.layer_fwd(0, x)
+    orc.layer_bwd(0, c, r, orc.zero_grads())
+    dt = time.perf_counter() - t0
+    return {"value": round(shape.seq_len / (dt * shape.layers), 3), "unit": "tokens/s",
+            "cores": os.cpu_count(), "kind": "port",
+            "sample": f"1 of {shape.layers} layers fwd+bwd, 1 micro-batch, seq {shape.seq_len}, numpy "
+                      f"fp32 (oracle/layer_oracle.py), {dt:.1f} s, extrapolated x{shape.layers} layers"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--micro-batches", type=int, default=4)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sequential", action="store_true")
+    ap.add_argument("--ref-seq", type=int, default=1024)
+    ap.add_argument("--nccl-ctas", type=int, default=16)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2411_15871_b200 import planner
+    from paper_2411_15871_b200.runtime import LLAMA3_8B, Context, Model, nccl_unique_id
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shape = LLAMA3_8B
+    shape.micro_batches = args.micro_batches
+    shape.layers = args.layers
+    tp = world
+    nid = None
+    if tp > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    ctx = Context.create(local, rank, tp, nid, args.nccl_ctas if tp > 1 else 0)
+    model = Model(ctx, shape)
+    par = {"tp": tp, "sp": tp > 1}
+    prof_path = os.path.join(ROOT, "profiles", f"b200_profile_tp{tp}.json")
+    profile = json.load(open(prof_path)) if os.path.exists(prof_path) else {"archetype": "nvlink_h100"}
+    t0 = time.perf_counter()
+    srch = planner.lib().search_si_plan(shape.planner_model(), par, B200_CLUSTER, profile)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    profile_json = json.dumps(profile) if "solo" in profile else None
+    model.set_plan(srch["plan_json"], profile_json, mode="si")
+    if tp > 1:
+        model.set_overlap_ctas(max(1, torch.cuda.get_device_properties(local).multi_processor_count
+                                   - args.nccl_ctas))
+    optim = {"lr": 1e-5, "weight_decay": 0.0}
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(0))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(n, fn):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(n):
+            fn()
+        e.record(stream)
+        barrier()
+        ms = s.elapsed_time(e)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms / n
+
+    step = lambda: model.step(optim, use_graph=True)  # noqa: E731
+    # dominant kernel probe: mlp_gate (the largest forward GEMM) on the compute lane
+    model.probe(10)
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(local) as clk:
+        ms_si = timed(args.steps, step)
+    probe_ms, probe_n = model.probe_read()  # last step's launches
+    model.probe(-1)
+    info = model.info()
+
+    ms_seq = None
+    if not args.no_sequential:
+        model.set_plan(srch["plan_json"], profile_json, mode="sequential")
+        for _ in range(2):
+            step()
+        ms_seq = timed(max(2, args.steps // 2), step)
+        model.set_plan(srch["plan_json"], profile_json, mode="si")
+
+    # end-to-end through the public API: per step, H2D of every micro-batch's
+    # input and output-gradient from pinned host memory, the step, D2H of the losses.
+    T, H, mb = shape.seq_len // tp, shape.hidden, shape.micro_batches
+    host_in = [torch.randn(T * H, dtype=torch.bfloat16).pin_memory() for _ in range(2 * mb)]
+    dev_dst = [model.tensor("x_in", strand=i) for i in range(mb)] + \
+              [model.tensor("dy", strand=i) for i in range(mb)]
+    loss_dev = model.tensor("loss")
+    loss_host = torch.empty(mb, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            for h, d in zip(host_in, dev_dst):
+                d.copy_(h, non_blocking=True)
+        step()
+        with torch.cuda.stream(stream):
+            loss_host.copy_(loss_dev, non_blocking=True)
+        stream.synchronize()
+
+    e2e_step()
+    ms_e2e = timed(args.steps, e2e_step)
+    h2d = sum(h.numel() * 2 for h in host_in)
+    d2h = mb * 4
+
+    tokens = mb * shape.seq_len  # one TP group processes every token
+    fl = layer_flops(shape, tp)
+    flops_step = (fl["fwd"] + fl["bwd"]) * shape.layers * mb  # per GPU
+    pk = peaks()
+    value = tokens / (ms_si / 1e3)
+    per_gpu_tflops = flops_step / (ms_si / 1e3) / 1e12
+    # per layer pair (one fwd + one bwd), the BASELINE.md roofline unit
+    lp_us = ms_si * 1e3 / (shape.layers * mb)
+    t_comp_us = (fl["fwd"] + fl["bwd"]) / (pk["bf16_burst"] * 1e12) * 1e6
+    t_comm_us = comm_bytes_per_layer_pair(shape, tp) / (900e9) * 1e6
+    roof_us = max(t_comp_us, t_comm_us)
+    gemm_flops = 2.0 * shape.seq_len * shape.hidden * (shape.ffn // tp)
+    probe_avg = probe_ms / max(probe_n, 1)
+    achieved = gemm_flops / (probe_avg / 1e3) / 1e12 if probe_n else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"tp{tp}")
+
+    if rank != 0:
+        del host_in, loss_host, dev_dst, loss_dev
+        torch.cuda.synchronize()
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(shape)
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_si, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, random inputs)",
+        "config": {"workload": f"llama3-8b-shaped {shape.layers}-layer stack, TP={tp}+SP, SI schedule, "
+                               f"{mb} micro-batches x seq {shape.seq_len}, AdamW",
+                   "model": "llama3-8b-shaped", "global_batch": mb, "seq_len": shape.seq_len,
+                   "parallelism": f"tp{tp}" + ("+sp" if tp > 1 else ""),
+                   "l2": "inputs > L2 (14 GB bf16 weights), no flush"},
+        "tokens_per_s_per_gpu": round(value / world, 2),
+        "mfu": round(per_gpu_tflops / SPEC_BF16_TFLOPS, 4),
+        "tflops_per_gpu": round(per_gpu_tflops, 1),
+        "sequential": None if ms_seq is None else {
+            "ms_per_step": round(ms_seq, 3), "tokens_per_s": round(tokens / (ms_seq / 1e3), 2),
+            "si_speedup": round(ms_seq / ms_si, 4)},
+        "layer_pair_us": round(lp_us, 1),
+        "overlap_roofline_us": round(roof_us, 1),
+        "frac_of_overlap_roofline": round(roof_us / lp_us, 4),
+        "exposed_comm_us_per_layer": None if tp == 1 else "see sequential vs SI",
+        "plan": {"hidden_comm_frac_model": srch["hidden_comm_frac"], "total_us_model": srch["total_us"],
+                 "search_ms": round(plan_ms, 2), "profile": "measured" if "solo" in profile else
+                 "synthetic nvlink_h100 (no measured B200 profile committed for this tp)"},
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM, node mlp_gate "
+                     f"(M{shape.seq_len} N{shape.ffn // tp} K{shape.hidden})",
+                     "achieved": None if achieved is None else round(achieved, 1),
+                     "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
+                     "frac": None if achieved is None else round(achieved / pk["bf16_sustained"], 4),
+                     "traffic": traffic, "peak_source": pk["source"] + " bf16_tflops_sustained",
+                     "launches_timed": probe_n, "avg_launch_ms": round(probe_avg, 4)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(tokens / (ms_e2e / 1e3), 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(ms_e2e, 3)},
+        "gpu_launches": info["program"]["kernel_launches"],
+        "memory": {"pool_gb": round(info["pool_bytes"] / 1e9, 3), "slots": info["slots"],
+                   "slot_gb": round(info["slot_bytes"] / 1e9, 4),
+                   "second_strand_extra_frac": round(info["slot_bytes"] / (info["pool_bytes"] - info["slot_bytes"]), 5)},
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    # torch's pinned-host allocator records events on the streams its buffers
+    # were used on: release those before our lane streams go away.
+    del host_in, loss_host, dev_dst, loss_dev
+    torch.cuda.synchronize()
+    model.close()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

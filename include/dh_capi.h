@@ -181,6 +181,11 @@ int dh_model_tensor(dh_model* m, const char* name, int layer, int strand, void**
  * with dh_free_string. */
 int dh_model_info_json(dh_model* m, char** out);
 void dh_free_string(char* s);
+/* Timing probe: CUDA events around every launch of template node `node` (-1 =
+ * off) in the lowered program, on the launching lane stream; after a run,
+ * dh_model_probe_read returns the summed kernel time and the launch count. */
+int dh_model_probe(dh_model* m, int node);
+int dh_model_probe_read(dh_model* m, double* total_ms, int* count);
 
 /* ---------------------------------------------------------------- profiler */
 

@@ -302,4 +302,14 @@ int dh_model_info_json(dh_model* m, char** out) {
 
 void dh_free_string(char* s) { std::free(s); }
 
+int dh_model_probe(dh_model* m, int node) {
+    if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
+    return dh::set_probe(*m, node);
+}
+
+int dh_model_probe_read(dh_model* m, double* total_ms, int* count) {
+    if (!m || !total_ms || !count) return dh::set_error(DH_ERR_INVALID, "null argument");
+    return dh::read_probe(*m, total_ms, count);
+}
+
 }  // extern "C"

@@ -206,11 +206,18 @@ namespace {
 
 int issue(Model& m) {
     Ctx& c = *m.ctx;
+    std::size_t probe = 0;
     for (std::size_t i = 0; i < m.prog.ops.size(); ++i) {
         const Op& o = m.prog.ops[i];
         cudaStream_t s = c.lane[o.lane];
         for (int w : o.waits) RT_CUDA(cudaStreamWaitEvent(s, m.events[w], 0));
+        const bool probed = o.node == m.probe_node && probe < m.probe_events.size();
+        // External records stay real timing events inside a captured graph.
+        if (probed)
+            RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe].first, s, cudaEventRecordExternal));
         RT_TRY(launch_node(m, o, s));
+        if (probed)
+            RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe++].second, s, cudaEventRecordExternal));
         if (m.events[i]) RT_CUDA(cudaEventRecord(m.events[i], s));
     }
     return DH_OK;
@@ -262,6 +269,41 @@ int run_program(Model& m, bool use_graph) {
         RT_CUDA(ie);
     }
     RT_CUDA(cudaGraphLaunch(m.graph, m.ctx->lane[0]));
+    return DH_OK;
+}
+
+int set_probe(Model& m, int node) {
+    for (auto& pr : m.probe_events) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    m.probe_events.clear();
+    m.probe_node = node;
+    if (m.graph) {
+        cudaGraphExecDestroy(m.graph);
+        m.graph = nullptr;
+    }
+    if (node < 0) return DH_OK;
+    RT_CUDA(cudaSetDevice(m.ctx->device));
+    for (const auto& o : m.prog.ops) {
+        if (o.node != node) continue;
+        std::pair<cudaEvent_t, cudaEvent_t> pr{};
+        RT_CUDA(cudaEventCreate(&pr.first));
+        RT_CUDA(cudaEventCreate(&pr.second));
+        m.probe_events.push_back(pr);
+    }
+    return DH_OK;
+}
+
+int read_probe(Model& m, double* total_ms, int* count) {
+    double sum = 0.0;
+    for (auto& pr : m.probe_events) {
+        float ms = 0.f;
+        RT_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+        sum += ms;
+    }
+    *total_ms = sum;
+    *count = static_cast<int>(m.probe_events.size());
     return DH_OK;
 }
 

@@ -159,6 +159,9 @@ struct Model {
     weft::OverlapTable plan_overlap;  // table the lowering replays the lane model with
     std::array<cudaEvent_t, kLanes> fork_join{};
     std::vector<int> y_slot;  // slot holding each strand's last-layer output
+    // timing probe: events around every launch of one template node
+    int probe_node = -1;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probe_events;
 
     template <class T = void>
     T* ptr(const Buf& b) const {
@@ -173,6 +176,8 @@ int lower_program(Model& m, int mode);
 int kernels_per_node(const Model& m, int node, int layer);
 int run_program(Model& m, bool use_graph);
 int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s);
+int set_probe(Model& m, int node);
+int read_probe(Model& m, double* total_ms, int* count);
 
 }  // namespace dh
 

@@ -47,6 +47,8 @@ _SIGS = {
     "dh_model_info_json": ([c_void_p, ctypes.POINTER(c_void_p)], c_int),
     "dh_free_string": ([c_void_p], None),
     "dh_profile_json": ([c_void_p, c_int, ctypes.POINTER(c_void_p)], c_int),
+    "dh_model_probe": ([c_void_p, c_int], c_int),
+    "dh_model_probe_read": ([c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int)], c_int),
 }
 _bound = False
 
@@ -193,6 +195,15 @@ class Model:
         p = c_void_p()
         check(_lib().dh_model_info_json(self.handle, ctypes.byref(p)))
         return json.loads(_take_string(p))
+
+    def probe(self, node: int):
+        """Time every launch of template node `node` (-1 disables)."""
+        check(_lib().dh_model_probe(self.handle, node))
+
+    def probe_read(self):
+        ms, n = ctypes.c_double(), c_int()
+        check(_lib().dh_model_probe_read(self.handle, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def profile(self, iters=10) -> str:
         p = c_void_p()
