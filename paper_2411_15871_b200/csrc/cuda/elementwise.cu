@@ -131,14 +131,25 @@ __global__ void rmsnorm_bwd_cols(const uint4* __restrict__ x, const uint4* __res
     dst[1] = make_float4(dg[4], dg[5], dg[6], dg[7]);
 }
 
-// dgamma_acc[c] += sum_w partial[w][c], w ascending.
+// dgamma_acc[c] += sum_w partial[w][c]. Block = 32 columns x 8 warps; warp j
+// sums rows j, j+8, ... and the 8 warp partials are combined in warp order, so
+// the summation order is fixed (deterministic) yet the read is parallel.
 __global__ void column_reduce_add(const float* __restrict__ partial, float* __restrict__ acc, int nw,
                                   int cols) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= cols) return;
+    __shared__ float red[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + lane;
     float s = 0.f;
-    for (int w = 0; w < nw; ++w) s += partial[static_cast<long long>(w) * cols + c];
-    acc[c] += s;
+    if (c < cols)
+        for (int w = warp; w < nw; w += 8) s += partial[static_cast<long long>(w) * cols + c];
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && c < cols) {
+        float t = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t += red[j][lane];
+        acc[c] += t;
+    }
 }
 
 // ---------------------------------------------------------------- elementwise
@@ -375,14 +386,14 @@ int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const vo
         return set_error(DH_ERR_INVALID, "rmsnorm_bwd: cols % 8, cols <= 8192 and 16-byte alignment required");
     if (rows <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
-    const int blocks = std::min(rows, 1184);
+    const int blocks = std::min(rows, 296);
     rmsnorm_bwd_cols<<<blocks, cols / 8, 0, s>>>(
         static_cast<const uint4*>(x), static_cast<const uint4*>(gamma), rstd,
         static_cast<const uint4*>(dy), static_cast<const uint4*>(resid), static_cast<uint4*>(dx),
         partial, rows, cols / 8, 1.f / cols);
     DH_CUDA_CHECK(cudaGetLastError());
     if (dgamma_acc) {
-        column_reduce_add<<<(cols + 255) / 256, 256, 0, s>>>(partial, dgamma_acc, blocks, cols);
+        column_reduce_add<<<(cols + 31) / 32, 256, 0, s>>>(partial, dgamma_acc, blocks, cols);
         DH_CUDA_CHECK(cudaGetLastError());
     }
     return DH_OK;
