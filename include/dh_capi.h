@@ -105,6 +105,11 @@ int dh_init_normal(void* bf16_out, float* f32_out, long long n, unsigned long lo
                    float std_dev, void* stream);
 int dh_fill_bf16(void* out, float value, long long n, void* stream);
 int dh_copy(void* dst, const void* src, long long bytes, void* stream);
+/* Single-GPU stand-in for one rank's collective (mode 0 AllGather of `count`
+ * bf16 per rank, 1 ReduceScatter to `count`): same HBM traffic on `ctas` CTAs,
+ * held for (tp-1)*count*2 bytes / link_gbs. Not numerically a collective. */
+int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode, int ctas,
+                  double link_gbs, void* stream);
 /* *loss = sum(y * r) in fp32, deterministic two-pass reduction through
  * partial (>= 1024 floats). One micro-batch, this rank's SP shard. */
 int dh_dot_loss(const void* y, const void* r, long long n, float* partial, float* loss,
@@ -126,6 +131,11 @@ int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_
  * plus a fixed-order sum. Each context must be driven by its own host thread
  * (collectives rendezvous like real ranks). Not graph-capturable. */
 int dh_loopback_group_create(int device, int tp_size, dh_ctx** ctxs_out);
+/* Emulated TP group on ONE GPU (performance studies only): this context has
+ * the per-rank shapes of tp_size ranks, but its collectives are dh_comm_proxy
+ * kernels (comm_ctas CTAs, NVLink-time link_gbs) — numerically meaningless,
+ * timing- and SM-footprint-faithful. Graph-capturable. */
+int dh_ctx_create_emulated(int device, int tp_size, int comm_ctas, double link_gbs, dh_ctx** out);
 int dh_ctx_destroy(dh_ctx* ctx);
 void* dh_ctx_stream(dh_ctx* ctx, int lane);
 int dh_nccl_unique_id(void* out128);

@@ -342,6 +342,40 @@ __global__ void sum_f32_kernel(SrcPtrs src, int nsrc, float* __restrict__ dst, l
     }
 }
 
+// Collective stand-in for single-GPU emulation of a TP group: moves the same
+// HBM bytes a rank's AllGather / ReduceScatter would (AG: replicate the shard
+// into every slot; RS: sum the tp chunks), on a capped number of CTAs, and
+// holds those CTAs until wire_bytes / link bandwidth has elapsed (globaltimer),
+// so both the SM footprint and the duration of an NVLink collective are
+// reproduced. Numerically it is NOT a collective.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                  long long nvec_out, long long chunk_vec, int mode, int tp,
+                                  unsigned long long target_ns) {
+    const unsigned long long t0 = globaltimer_ns();
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec_out;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        if (mode == 0) {  // all-gather: out[i] = shard[i % chunk]
+            dst[i] = src[i % chunk_vec];
+        } else {          // reduce-scatter: out[i] = sum_j in[j*chunk + i]
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int j = 0; j < tp; ++j) {
+                float v[8];
+                unpack8(src[j * chunk_vec + i], v);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) acc[t] += v[t];
+            }
+            dst[i] = pack8(acc);
+        }
+    }
+    while (globaltimer_ns() - t0 < target_ns) __nanosleep(500);
+}
+
 int grid_for(long long work, int threads) {
     const long long blocks = (work + threads - 1) / threads;
     return static_cast<int>(std::max<long long>(1, std::min<long long>(blocks, 148LL * 16)));
@@ -500,6 +534,19 @@ int dh_sum_f32_ptrs(const float* const* srcs, int nsrc, float* dst, long long n,
     SrcPtrs sp{};
     for (int i = 0; i < nsrc; ++i) sp.p[i] = srcs[i];
     sum_f32_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(sp, nsrc, dst, n);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode, int ctas,
+                  double link_gbs, void* stream) {
+    if (count % 8) return set_error(DH_ERR_INVALID, "comm_proxy: count % 8 required");
+    const long long chunk = count / 8;
+    const long long nvec_out = mode == 0 ? chunk * tp : chunk;
+    const double wire = static_cast<double>(count) * 2.0 * (tp - 1);
+    const unsigned long long target = link_gbs > 0 ? static_cast<unsigned long long>(wire / link_gbs) : 0ull;
+    comm_proxy_kernel<<<std::max(1, ctas), 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec_out, chunk, mode, tp, target);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

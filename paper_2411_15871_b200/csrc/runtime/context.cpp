@@ -24,6 +24,8 @@
 
 extern "C" int dh_sum_bf16_ptrs(const void* const* srcs, int nsrc, void* dst, long long n,
                                 void* stream);
+extern "C" int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode,
+                             int ctas, double link_gbs, void* stream);
 extern "C" int dh_sum_f32_ptrs(const float* const* srcs, int nsrc, float* dst, long long n,
                                void* stream);
 
@@ -62,6 +64,22 @@ public:
     }
     bool capturable() const override { return true; }
     const char* name() const override { return "nccl"; }
+};
+
+class EmulatedComm final : public Comm {
+public:
+    int tp, ctas;
+    double link_gbs;  // bytes per ns == GB/s
+    EmulatedComm(int t, int c, double bw) : tp(t), ctas(c), link_gbs(bw) {}
+    int all_gather(const void* send, void* recv, size_t count, cudaStream_t s) override {
+        return dh_comm_proxy(send, recv, static_cast<long long>(count), tp, 0, ctas, link_gbs, s);
+    }
+    int reduce_scatter(const void* send, void* recv, size_t count, cudaStream_t s) override {
+        return dh_comm_proxy(send, recv, static_cast<long long>(count), tp, 1, ctas, link_gbs, s);
+    }
+    int all_reduce_f32(float*, size_t, cudaStream_t) override { return DH_OK; }
+    bool capturable() const override { return true; }
+    const char* name() const override { return "emulated"; }
 };
 
 }  // namespace
@@ -259,6 +277,23 @@ int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_
         dh_ctx_destroy(c);
         return rc;
     }
+    *out = c;
+    return DH_OK;
+}
+
+int dh_ctx_create_emulated(int device, int tp_size, int comm_ctas, double link_gbs, dh_ctx** out) {
+    if (!out || tp_size < 2) return dh::set_error(DH_ERR_INVALID, "emulated: tp_size >= 2 required");
+    auto* c = new dh_ctx();
+    c->device = device;
+    c->tp_rank = 0;
+    c->tp_size = tp_size;
+    c->comm_ctas = comm_ctas;
+    const int rc = init_streams(c);
+    if (rc != DH_OK) {
+        dh_ctx_destroy(c);
+        return rc;
+    }
+    c->comm = std::make_unique<dh::EmulatedComm>(tp_size, comm_ctas > 0 ? comm_ctas : 16, link_gbs);
     *out = c;
     return DH_OK;
 }

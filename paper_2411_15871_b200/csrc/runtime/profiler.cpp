@@ -1,0 +1,186 @@
+// G4: on-device operator-pair overlap profiler (north star (4)).
+//
+// Produces the weft Profile document the unchanged DP search consumes
+// (schema: reference overlap_profile.cpp:227-288; our parse_profile /
+// profile_to_json):
+//   * solo[(class, node name)] = mean CUDA-event time of the node's launch(es)
+//     on its lane stream, for every node of the layer's forward and backward
+//     DAGs (the reference keys solo times by node name, op_model.cpp:376-379);
+//   * for every cross-lane (forward node a, backward node b) pair — the only
+//     pairs the lane model ever co-runs (same-lane ops serialise) — the co-run
+//     time P_ab of a on its lane stream and b on its lane stream released by
+//     one event; OEF_ab = oef(T_a, T_b, P_ab) (Eq. 1, reference
+//     overlap_profile.cpp:92-103), averaged per unordered class pair;
+//   * slowdown_factor = launch_overhead_frac = 0: measured P already contains
+//     the interference, so the lane model must not apply it twice.
+// The forward node runs as strand 0 / slot 0, the backward node as strand 1 /
+// slot 1 so the pair touches disjoint buffers, as two micro-batches do.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "nlohmann/json.hpp"
+#include "runtime.hpp"
+
+namespace dh {
+namespace {
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timer() {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+    }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+};
+
+Op node_op(const Model& m, const weft::OpNode& n, bool fwd) {
+    Op o;
+    o.node = n.id;
+    o.lane = static_cast<int>(n.lane);
+    o.layer = 0;
+    o.strand = fwd ? 0 : std::min(1, m.cfg.micro_batches - 1);
+    o.slot = fwd ? 0 : 1;
+    o.prev_slot = -1;
+    o.first_dx = true;
+    return o;
+}
+
+int time_solo(Model& m, const Op& o, int iters, double* us) {
+    cudaStream_t s = m.ctx->lane[o.lane];
+    Timer t;
+    for (int i = 0; i < 2; ++i) RT_TRY(launch_node(m, o, s));
+    RT_CUDA(cudaEventRecord(t.a, s));
+    for (int i = 0; i < iters; ++i) RT_TRY(launch_node(m, o, s));
+    RT_CUDA(cudaEventRecord(t.b, s));
+    RT_CUDA(cudaEventSynchronize(t.b));
+    float ms = 0.f;
+    RT_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    *us = 1e3 * ms / iters;
+    return DH_OK;
+}
+
+int time_pair(Model& m, const Op& a, const Op& b, int iters, double* us) {
+    cudaStream_t sa = m.ctx->lane[a.lane], sb = m.ctx->lane[b.lane];
+    Timer t;
+    cudaEvent_t go = nullptr, done_a = nullptr, done_b = nullptr;
+    RT_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+    RT_CUDA(cudaEventCreateWithFlags(&done_a, cudaEventDisableTiming));
+    RT_CUDA(cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming));
+    cudaStream_t s0 = m.ctx->lane[0];
+    double total = 0.0;
+    int rc = DH_OK;
+    for (int i = 0; i < iters + 1 && rc == DH_OK; ++i) {
+        // release both lanes at the same instant, stop when both finished
+        cudaEventRecord(t.a, s0);
+        cudaEventRecord(go, s0);
+        cudaStreamWaitEvent(sa, go, 0);
+        cudaStreamWaitEvent(sb, go, 0);
+        rc = launch_node(m, a, sa);
+        if (rc == DH_OK) rc = launch_node(m, b, sb);
+        cudaEventRecord(done_a, sa);
+        cudaEventRecord(done_b, sb);
+        cudaStreamWaitEvent(s0, done_a, 0);
+        cudaStreamWaitEvent(s0, done_b, 0);
+        cudaEventRecord(t.b, s0);
+        cudaEventSynchronize(t.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        if (i > 0) total += ms;  // first iteration warms up
+    }
+    cudaEventDestroy(go);
+    cudaEventDestroy(done_a);
+    cudaEventDestroy(done_b);
+    if (rc != DH_OK) return rc;
+    RT_CUDA(cudaGetLastError());
+    *us = 1e3 * total / iters;
+    return DH_OK;
+}
+
+}  // namespace
+
+int profile_model(Model& m, int iters, std::string* out_json) {
+    if (m.ctx->comm && std::strcmp(m.ctx->comm->name(), "loopback") == 0)
+        return set_error(DH_ERR_CONFIG, "profiler: loopback ranks cannot be profiled one at a time");
+    RT_CUDA(cudaSetDevice(m.ctx->device));
+    for (auto s : m.ctx->lane) RT_CUDA(cudaStreamSynchronize(s));
+    iters = std::max(1, iters);
+
+    std::map<int, double> solo;
+    weft::Profile prof;
+    std::map<int, const weft::OpNode*> fwd_nodes, bwd_nodes;
+    for (const auto& n : m.fwd_dag.nodes) fwd_nodes[n.id] = &n;
+    for (const auto& n : m.bwd_dag.nodes) bwd_nodes[n.id] = &n;
+    for (auto* table : {&fwd_nodes, &bwd_nodes}) {
+        const bool fwd = table == &fwd_nodes;
+        for (const auto& [id, n] : *table) {
+            double us = 0.0;
+            RT_TRY(time_solo(m, node_op(m, *n, fwd), iters, &us));
+            solo[id] = us;
+            try {
+                prof.solo.set(n->cls, n->name, std::max(us, 1e-3));
+            } catch (const std::exception& e) {
+                return set_error(DH_ERR_OTHER, e.what());
+            }
+        }
+    }
+
+    // cross-lane (fwd, bwd) pairs -> OEF samples per unordered class pair
+    std::map<std::pair<weft::OperatorClass, weft::OperatorClass>, std::vector<double>> samples;
+    nlohmann::json pairs = nlohmann::json::array();
+    for (const auto& [ia, na] : fwd_nodes) {
+        for (const auto& [ib, nb] : bwd_nodes) {
+            if (na->lane == nb->lane) continue;
+            double p = 0.0;
+            RT_TRY(time_pair(m, node_op(m, *na, true), node_op(m, *nb, false), iters, &p));
+            const double ta = solo[ia], tb = solo[ib];
+            const double pc = std::max(p, std::max(ta, tb));  // noise floor (Eq. 1 domain)
+            double e = weft::oef(ta, tb, pc);
+            e = std::clamp(e, -0.05, 1.05);
+            auto key = na->cls <= nb->cls ? std::make_pair(na->cls, nb->cls) : std::make_pair(nb->cls, na->cls);
+            samples[key].push_back(e);
+            pairs.push_back({{"fwd", na->name}, {"bwd", nb->name}, {"t_fwd_us", ta}, {"t_bwd_us", tb},
+                             {"p_us", p}, {"oef", e}});
+        }
+    }
+    for (const auto& [key, v] : samples) {
+        double s = 0.0;
+        for (double x : v) s += x;
+        prof.overlap.set(key.first, key.second, s / v.size());
+    }
+    prof.overlap.slowdown_factor = 0.0;
+    prof.overlap.launch_overhead_frac = 0.0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceProp props{};
+    cudaGetDeviceProperties(&props, dev);
+    auto& md = prof.overlap.metadata;
+    md["hardware"] = props.name;
+    md["source"] = "dh_profile_json (on-device CUDA-event solo + pairwise co-run timing)";
+    md["comm"] = m.ctx->comm ? m.ctx->comm->name() : "none";
+    md["tp"] = std::to_string(m.cfg.tp);
+    md["seq"] = std::to_string(m.cfg.seq);
+    md["hidden"] = std::to_string(m.cfg.hidden);
+    md["iters"] = std::to_string(iters);
+    md["pairs_measured"] = std::to_string(pairs.size());
+    // The Profile document plus the raw pair table; parse_profile reads only
+    // solo / oef / interference / metadata, so the extra key is inert.
+    nlohmann::json doc = nlohmann::json::parse(weft::profile_to_json(prof));
+    doc["pairs"] = pairs;
+    *out_json = doc.dump(2) + "\n";
+    return DH_OK;
+}
+
+}  // namespace dh
+
+extern "C" int dh_profile_json(dh_model* m, int iters, char** out) {
+    if (!m || !out) return dh::set_error(DH_ERR_INVALID, "null argument");
+    std::string s;
+    RT_TRY(dh::profile_model(*m, iters, &s));
+    *out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*out, s.c_str(), s.size() + 1);
+    return DH_OK;
+}

@@ -31,6 +31,7 @@ class OptimCfg(ctypes.Structure):
 _SIGS = {
     "dh_ctx_create": ([c_int, c_int, c_int, c_void_p, c_int, ctypes.POINTER(c_void_p)], c_int),
     "dh_loopback_group_create": ([c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
+    "dh_ctx_create_emulated": ([c_int, c_int, c_int, ctypes.c_double, ctypes.POINTER(c_void_p)], c_int),
     "dh_ctx_destroy": ([c_void_p], c_int),
     "dh_ctx_stream": ([c_void_p, c_int], c_void_p),
     "dh_nccl_unique_id": ([c_void_p], c_int),
@@ -106,6 +107,14 @@ class Context:
         arr = (c_void_p * tp_size)()
         check(_lib().dh_loopback_group_create(device, tp_size, arr))
         return [cls(c_void_p(arr[r]), r, tp_size) for r in range(tp_size)]
+
+    @classmethod
+    def emulated(cls, device=0, tp_size=8, comm_ctas=16, link_gbs=770.0):
+        """Per-rank shapes of a tp_size group on one GPU, collectives replaced by
+        timing/SM-faithful proxy kernels (performance studies only)."""
+        h = c_void_p()
+        check(_lib().dh_ctx_create_emulated(device, tp_size, comm_ctas, link_gbs, ctypes.byref(h)))
+        return cls(h, 0, tp_size)
 
     def stream_ptr(self, lane=0) -> int:
         return _lib().dh_ctx_stream(self.handle, lane)
