@@ -204,6 +204,81 @@ def cpu_baseline_sample(shape):
                       f"fp32 (oracle/layer_oracle.py), {dt:.1f} s, extrapolated x{shape.layers} layers"}
 
 
+def emulated_tp_experiment(args, tp, timed_factory):
+    """TP=<tp> per-GPU shapes on this single GPU with emulated collectives
+    (dh_ctx_create_emulated: proxy kernels on the NCCL CTA budget, held for the
+    NVLink wire time at the measured 770 GB/s peer bandwidth). Measures the
+    G4 profile on-device, searches the SI plan from it with the unchanged DP,
+    then times SI, sequential and compute-only (collectives skipped) steps.
+    Numerically meaningless by construction; timing-faithful by design."""
+    import copy
+
+    import torch
+
+    from paper_2411_15871_b200 import planner
+    from paper_2411_15871_b200.runtime import LLAMA3_8B, Context, Model
+
+    shape = copy.copy(LLAMA3_8B)
+    shape.layers, shape.micro_batches = args.layers, args.micro_batches
+    link = 770.0
+    ctx = Context.emulated(0, tp, args.nccl_ctas, link)
+    m = Model(ctx, shape)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    m.set_overlap_ctas(sms - args.nccl_ctas)  # profile with the execution-time SM split
+    t0 = time.perf_counter()
+    prof = json.loads(m.profile(iters=5))
+    prof_s = time.perf_counter() - t0
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"b200_profile_tp{tp}_emulated.json"), "w") as f:
+        json.dump(prof, f, indent=1)
+    srch = planner.lib().search_si_plan(shape.planner_model(), {"tp": tp, "sp": True}, B200_CLUSTER, prof)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(0))
+    timed = timed_factory
+    step = lambda: m.step({"lr": 1e-5}, use_graph=True)  # noqa: E731
+    res = {}
+    for mode, skip in (("si", False), ("compute_only", True), ("sequential", False)):
+        m.set_plan(srch["plan_json"], json.dumps(prof), mode="sequential" if mode == "sequential" else "si")
+        m.set_overlap_ctas(sms - args.nccl_ctas)
+        m.set_skip_comm(skip)
+        for _ in range(2):
+            step()
+        res[mode] = timed(max(2, args.steps), step, stream)
+    m.set_skip_comm(False)
+    comm_nodes = {"ag0", "rs0", "ag1", "rs1", "rs1_bwd_ag", "ag1_bwd_rs", "rs0_bwd_ag", "ag0_bwd_rs"}
+    comm_solo = sum(e["t_us"] for e in prof["solo"] if e["shape"] in comm_nodes)
+    pairs = shape.layers * shape.micro_batches
+    exposed = (res["si"] - res["compute_only"]) * 1e3 / pairs
+    exposed_seq = (res["sequential"] - res["compute_only"]) * 1e3 / pairs
+    fl = layer_flops(shape, tp)
+    pk = peaks()
+    t_comp = (fl["fwd"] + fl["bwd"]) / (pk["bf16_burst"] * 1e12) * 1e6
+    t_comm = comm_bytes_per_layer_pair(shape, tp) / 900e9 * 1e6
+    roof = max(t_comp, t_comm)
+    lp = res["si"] * 1e3 / pairs
+    tokens = shape.micro_batches * shape.seq_len
+    m.close()
+    ctx.close()
+    return {
+        "what": f"TP={tp} per-GPU shapes of the same workload on ONE B200; collectives are proxy kernels "
+                f"({args.nccl_ctas} CTAs, held for wire bytes / {link:.0f} GB/s); numerics not meaningful",
+        "tokens_per_s_tp_group": round(tokens / (res["si"] / 1e3), 1),
+        "tokens_per_s_per_gpu": round(tokens / (res["si"] / 1e3) / tp, 1),
+        "ms_per_step": {k: round(v, 3) for k, v in res.items()},
+        "si_speedup_vs_sequential": round(res["sequential"] / res["si"], 4),
+        "layer_pair_us": round(lp, 1),
+        "overlap_roofline_us": round(roof, 1),
+        "frac_of_overlap_roofline": round(roof / lp, 4),
+        "comm_solo_us_per_layer_pair": round(comm_solo, 1),
+        "exposed_comm_us_per_layer_pair": {"si": round(exposed, 1), "sequential": round(exposed_seq, 1)},
+        "hidden_comm_frac": round(1.0 - exposed / comm_solo, 4) if comm_solo > 0 else None,
+        "mfu": round((fl["fwd"] + fl["bwd"]) * pairs / (res["si"] / 1e3) / 1e12 / SPEC_BF16_TFLOPS, 4),
+        "plan": {"hidden_comm_frac_model": srch["hidden_comm_frac"], "total_us_model": srch["total_us"],
+                 "fwd_cuts": json.loads(srch["plan_json"])["fwd_cuts"],
+                 "bwd_cuts": json.loads(srch["plan_json"])["bwd_cuts"]},
+        "profile_seconds": round(prof_s, 2),
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -216,6 +291,8 @@ def main():
     ap.add_argument("--no-sequential", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1024)
     ap.add_argument("--nccl-ctas", type=int, default=16)
+    ap.add_argument("--emulate-tp", type=int, default=8,
+                    help="at N=1 also run the TP=<n> per-GPU shapes with emulated collectives (0 = off)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world, rank, local = dist_setup()
@@ -262,13 +339,14 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(n, fn):
+    def timed(n, fn, on_stream=None):
+        st = stream if on_stream is None else on_stream
         barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
+        s.record(st)
         for _ in range(n):
             fn()
-        e.record(stream)
+        e.record(st)
         barrier()
         ms = s.elapsed_time(e)
         if world > 1:
@@ -338,8 +416,16 @@ def main():
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(f"tp{tp}")
 
-    if rank != 0:
+    emu = None
+    if world == 1 and args.emulate_tp > 1:
         del host_in, loss_host, dev_dst, loss_dev
+        torch.cuda.synchronize()
+        model.close()
+        emu = emulated_tp_experiment(args, args.emulate_tp, timed)
+
+    if rank != 0:
+        if world > 1:
+            del host_in, loss_host, dev_dst, loss_dev
         torch.cuda.synchronize()
         return
     cpu = None
@@ -385,13 +471,15 @@ def main():
                    "slot_gb": round(info["slot_bytes"] / 1e9, 4),
                    "second_strand_extra_frac": round(info["slot_bytes"] / (info["pool_bytes"] - info["slot_bytes"]), 5)},
         "clocks": clocks,
+        "tp_emulated": emu,
     }
     print(json.dumps(line), flush=True)
     # torch's pinned-host allocator records events on the streams its buffers
     # were used on: release those before our lane streams go away.
-    del host_in, loss_host, dev_dst, loss_dev
-    torch.cuda.synchronize()
-    model.close()
+    if emu is None:
+        del host_in, loss_host, dev_dst, loss_dev
+        torch.cuda.synchronize()
+        model.close()
     ctx.close()
 
 

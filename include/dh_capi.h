@@ -168,6 +168,12 @@ int dh_model_destroy(dh_model* m);
  * segment per pass (valid for mode 1 and as a trivial SI plan). */
 int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
                       const char* cluster_json, int mode);
+/* Host-only lowering (no GPU needed): the launch program dh_model_set_plan would
+ * build for (cfg, tp, rank, plan, mode), as JSON {"ops": [{strand, layer, node,
+ * lane, slot, prev_slot, first_dx, waits}], "slots", "fwd_seq", "bwd_seq"}.
+ * Every rank of a TP group must obtain the same collective order from it. */
+int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_json,
+                  const char* profile_json, int mode, char** out);
 /* Cap the SMs of GEMMs that co-run with a collective (0 = no cap). */
 int dh_model_set_overlap_ctas(dh_model* m, int gemm_ctas);
 
@@ -195,6 +201,9 @@ void dh_free_string(char* s);
  * off) in the lowered program, on the launching lane stream; after a run,
  * dh_model_probe_read returns the summed kernel time and the launch count. */
 int dh_model_probe(dh_model* m, int node);
+/* Measurement mode: skip every collective launch (keeps the schedule and its
+ * event edges) so T_SI - T_compute_only gives the exposed communication. */
+int dh_model_set_skip_comm(dh_model* m, int skip);
 int dh_model_probe_read(dh_model* m, double* total_ms, int* count);
 
 /* ---------------------------------------------------------------- profiler */

@@ -355,14 +355,16 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 __global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
-                                  long long nvec_out, long long chunk_vec, int mode, int tp,
+                                  long long chunk_vec, int mode, int tp,
                                   unsigned long long target_ns) {
     const unsigned long long t0 = globaltimer_ns();
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec_out;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        if (mode == 0) {  // all-gather: out[i] = shard[i % chunk]
-            dst[i] = src[i % chunk_vec];
-        } else {          // reduce-scatter: out[i] = sum_j in[j*chunk + i]
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long first = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (mode == 0) {  // all-gather: every rank slot receives the shard
+        for (int j = 0; j < tp; ++j)
+            for (long long i = first; i < chunk_vec; i += stride) dst[j * chunk_vec + i] = src[i];
+    } else {          // reduce-scatter: out[i] = sum_j in[j*chunk + i]
+        for (long long i = first; i < chunk_vec; i += stride) {
             float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int j = 0; j < tp; ++j) {
                 float v[8];
@@ -373,7 +375,7 @@ __global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restri
             dst[i] = pack8(acc);
         }
     }
-    while (globaltimer_ns() - t0 < target_ns) __nanosleep(500);
+    while (globaltimer_ns() - t0 < target_ns) __nanosleep(256);
 }
 
 int grid_for(long long work, int threads) {
@@ -542,11 +544,10 @@ int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode,
                   double link_gbs, void* stream) {
     if (count % 8) return set_error(DH_ERR_INVALID, "comm_proxy: count % 8 required");
     const long long chunk = count / 8;
-    const long long nvec_out = mode == 0 ? chunk * tp : chunk;
     const double wire = static_cast<double>(count) * 2.0 * (tp - 1);
     const unsigned long long target = link_gbs > 0 ? static_cast<unsigned long long>(wire / link_gbs) : 0ull;
     comm_proxy_kernel<<<std::max(1, ctas), 512, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec_out, chunk, mode, tp, target);
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), chunk, mode, tp, target);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

@@ -140,6 +140,57 @@ int find_tensor(dh::Model& m, const std::string& name, int layer, int strand, Te
 
 }  // namespace
 
+namespace dh {
+
+int configure_plan(Model& mm, const char* plan_json, const char* profile_json,
+                   const char* cluster_json) {
+    Model* m = &mm;
+    try {
+        m->solo_us.clear();
+        m->plan_overlap = weft::OverlapTable{};
+        weft::Profile prof;
+        if (profile_json && *profile_json) {
+            prof = weft::parse_profile(profile_json);
+            m->plan_overlap = prof.overlap;
+        }
+        if (cluster_json && *cluster_json) {
+            const json c = json::parse(cluster_json);
+            weft::ClusterSpec cl;
+            cl.name = c.value("name", std::string("custom"));
+            cl.gpus = c.at("gpus").get<int>();
+            cl.per_node = c.at("per_node").get<int>();
+            cl.peak_tflops = c.at("peak_tflops").get<double>();
+            cl.local_bw_gbs = c.at("local_bw_gbs").get<double>();
+            cl.cross_bw_gbs = c.at("cross_bw_gbs").get<double>();
+            cl.mem_gb = c.at("mem_gb").get<double>();
+            cl.bw_efficiency = c.value("bw_efficiency", 0.5);
+            RT_TRY(build_dags(*m, cl, &prof.solo));
+        }
+        for (const auto* dag : {&m->fwd_dag, &m->bwd_dag}) {
+            for (const auto& n : dag->nodes) {
+                if (auto t = prof.solo.get(n.cls, n.name)) m->solo_us[n.id] = *t;
+            }
+        }
+        if (plan_json && *plan_json) {
+            m->plan = weft::parse_plan_json(plan_json);
+            if (!weft::validate_sequence(m->fwd_dag, m->plan.fwd_seq) ||
+                !weft::validate_sequence(m->bwd_dag, m->plan.bwd_seq)) {
+                return set_error(DH_ERR_CONFIG,
+                                 "plan sequences are not valid orders of this model's layer DAG "
+                                 "(plan built for a different tp / template?)");
+            }
+        } else {
+            m->plan = trivial_plan(*m);
+        }
+        m->have_plan = true;
+    } catch (const std::exception& e) {
+        return set_error(DH_ERR_CONFIG, e.what());
+    }
+    return DH_OK;
+}
+
+}  // namespace dh
+
 extern "C" {
 
 int dh_model_create(dh_ctx* ctx, const dh_model_cfg* cfg, dh_model** out) {
@@ -160,61 +211,31 @@ int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_js
                       const char* cluster_json, int mode) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
     if (mode != 0 && mode != 1) return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI) or 1 (sequential)");
-    try {
-        m->solo_us.clear();
-        m->plan_overlap = weft::OverlapTable{};
-        weft::Profile prof;
-        if (profile_json && *profile_json) {
-            prof = weft::parse_profile(profile_json);
-            m->plan_overlap = prof.overlap;
-        }
-        if (cluster_json && *cluster_json) {
-            const json c = json::parse(cluster_json);
-            weft::ClusterSpec cl;
-            cl.name = c.value("name", std::string("custom"));
-            cl.gpus = c.at("gpus").get<int>();
-            cl.per_node = c.at("per_node").get<int>();
-            cl.peak_tflops = c.at("peak_tflops").get<double>();
-            cl.local_bw_gbs = c.at("local_bw_gbs").get<double>();
-            cl.cross_bw_gbs = c.at("cross_bw_gbs").get<double>();
-            cl.mem_gb = c.at("mem_gb").get<double>();
-            cl.bw_efficiency = c.value("bw_efficiency", 0.5);
-            weft::ModelSpec ms;
-            ms.name = "dh-llama";
-            ms.hidden = m->cfg.hidden;
-            ms.intermediate = m->cfg.ffn;
-            ms.layers = m->cfg.layers;
-            ms.seq_len = m->cfg.seq;
-            weft::ParallelismSpec par;
-            par.tp = m->cfg.tp;
-            par.sp = m->cfg.tp > 1;
-            auto dags = weft::build_layer_dag(ms, par, cl, &prof.solo);
-            m->fwd_dag = std::move(dags.first);
-            m->bwd_dag = std::move(dags.second);
-        }
-        for (const auto* dag : {&m->fwd_dag, &m->bwd_dag}) {
-            for (const auto& n : dag->nodes) {
-                if (auto t = prof.solo.get(n.cls, n.name)) m->solo_us[n.id] = *t;
-            }
-        }
-        if (plan_json && *plan_json) {
-            m->plan = weft::parse_plan_json(plan_json);
-            if (!weft::validate_sequence(m->fwd_dag, m->plan.fwd_seq) ||
-                !weft::validate_sequence(m->bwd_dag, m->plan.bwd_seq)) {
-                return dh::set_error(DH_ERR_CONFIG,
-                                     "plan sequences are not valid orders of this model's layer DAG "
-                                     "(plan built for a different tp / template?)");
-            }
-        } else {
-            m->plan = trivial_plan(*m);
-        }
-        m->have_plan = true;
-    } catch (const weft::ConfigError& e) {
-        return dh::set_error(DH_ERR_CONFIG, e.what());
-    } catch (const std::exception& e) {
-        return dh::set_error(DH_ERR_CONFIG, e.what());
-    }
+    RT_TRY(dh::configure_plan(*m, plan_json, profile_json, cluster_json));
     return dh::lower_program(*m, mode);
+}
+
+int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_json,
+                  const char* profile_json, int mode, char** out) {
+    if (!cfg || !out) return dh::set_error(DH_ERR_INVALID, "null argument");
+    if (mode != 0 && mode != 1) return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI) or 1 (sequential)");
+    dh::Model m;  // host-only: no context, no pool
+    RT_TRY(dh::derive_cfg(cfg, tp, rank, &m.cfg));
+    RT_TRY(dh::build_dags(m, dh::default_cluster(), nullptr));
+    RT_TRY(dh::configure_plan(m, plan_json, profile_json, nullptr));
+    RT_TRY(dh::lower_ops(m, mode));
+    json ops = json::array();
+    for (const auto& o : m.prog.ops) {
+        ops.push_back({{"strand", o.strand}, {"layer", o.layer}, {"node", o.node}, {"lane", o.lane},
+                       {"slot", o.slot}, {"prev_slot", o.prev_slot}, {"first_dx", o.first_dx},
+                       {"waits", o.waits}});
+    }
+    json j = {{"ops", ops}, {"slots", m.cfg.layers + 1}, {"fwd_seq", m.plan.fwd_seq},
+              {"bwd_seq", m.plan.bwd_seq}, {"mode", mode}};
+    const std::string s = j.dump();
+    *out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*out, s.c_str(), s.size() + 1);
+    return DH_OK;
 }
 
 int dh_model_set_overlap_ctas(dh_model* m, int gemm_ctas) {
@@ -301,6 +322,16 @@ int dh_model_info_json(dh_model* m, char** out) {
 }
 
 void dh_free_string(char* s) { std::free(s); }
+
+int dh_model_set_skip_comm(dh_model* m, int skip) {
+    if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
+    m->skip_comm = skip != 0;
+    if (m->graph) {
+        cudaGraphExecDestroy(m->graph);
+        m->graph = nullptr;
+    }
+    return DH_OK;
+}
 
 int dh_model_probe(dh_model* m, int node) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");

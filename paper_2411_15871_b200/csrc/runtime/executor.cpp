@@ -153,7 +153,7 @@ struct Lowering {
 
 }  // namespace
 
-int lower_program(Model& m, int mode) {
+int lower_ops(Model& m, int mode) {
     const int L = m.cfg.layers, mb = m.cfg.micro_batches;
     weft::OverlapTable tbl = weft::synth_profile(weft::ProfileArchetype::nvlink_h100).overlap;
     if (!m.plan_overlap.entries.empty()) tbl = m.plan_overlap;
@@ -184,6 +184,11 @@ int lower_program(Model& m, int mode) {
     m.y_slot.assign(mb, -1);
     for (int s = 0; s < mb; ++s) m.y_slot[s] = lw.slot_of[s][L - 1];
     m.prog = std::move(lw.prog);
+    return DH_OK;
+}
+
+int lower_program(Model& m, int mode) {
+    RT_TRY(lower_ops(m, mode));
     // one event per op that some later op waits on
     for (auto e : m.events)
         if (e) cudaEventDestroy(e);
@@ -215,7 +220,7 @@ int issue(Model& m) {
         // External records stay real timing events inside a captured graph.
         if (probed)
             RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe].first, s, cudaEventRecordExternal));
-        RT_TRY(launch_node(m, o, s));
+        if (!(m.skip_comm && o.lane != 0)) RT_TRY(launch_node(m, o, s));
         if (probed)
             RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe++].second, s, cudaEventRecordExternal));
         if (m.events[i]) RT_CUDA(cudaEventRecord(m.events[i], s));

@@ -49,10 +49,8 @@ unsigned long long mix(unsigned long long a, unsigned long long b) {
 
 }  // namespace
 
-int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
-    auto m = std::make_unique<Model>();
-    m->ctx = ctx;
-    ModelCfg& k = m->cfg;
+int derive_cfg(const dh_model_cfg* c, int tp, int rank, ModelCfg* out) {
+    ModelCfg k;
     k.hidden = c->hidden;
     k.ffn = c->ffn;
     k.n_heads = c->n_heads;
@@ -65,9 +63,10 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     k.eps = c->norm_eps;
     k.seed = c->seed;
     k.init_std = c->init_std;
-    k.tp = ctx->tp_size;
-    k.rank = ctx->tp_rank;
-    if (k.hidden <= 0 || k.layers <= 0 || k.seq <= 0 || k.micro_batches < 1 || k.head_dim <= 0)
+    k.tp = tp;
+    k.rank = rank;
+    if (k.hidden <= 0 || k.layers <= 0 || k.seq <= 0 || k.micro_batches < 1 || k.head_dim <= 0 ||
+        k.n_heads <= 0 || k.n_kv_heads <= 0 || tp < 1)
         return set_error(DH_ERR_CONFIG, "model: dimensions must be positive");
     if (k.seq % k.tp || k.n_heads % k.tp || k.n_kv_heads % k.tp || k.ffn % k.tp)
         return set_error(DH_ERR_INFEASIBLE,
@@ -83,6 +82,49 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     k.qkv_n = (k.nq_l + 2 * k.nkv_l) * k.head_dim;
     k.attn_n = k.nq_l * k.head_dim;
     k.ffn_l = k.ffn / k.tp;
+    *out = k;
+    return DH_OK;
+}
+
+weft::ClusterSpec default_cluster() {
+    weft::ClusterSpec cl;
+    cl.name = "b200";
+    cl.gpus = 8;
+    cl.per_node = 8;
+    cl.peak_tflops = 2250.0;
+    cl.local_bw_gbs = 900.0;
+    cl.cross_bw_gbs = 50.0;
+    cl.mem_gb = 180.0;
+    return cl;
+}
+
+// The layer DAG from the same template and specs the planner uses.
+int build_dags(Model& m, const weft::ClusterSpec& cl, const weft::SoloTimeTable* solo) {
+    weft::ModelSpec ms;
+    ms.name = "dh-llama";
+    ms.family = weft::ModelFamily::llama;
+    ms.hidden = m.cfg.hidden;
+    ms.intermediate = m.cfg.ffn;
+    ms.layers = m.cfg.layers;
+    ms.seq_len = m.cfg.seq;
+    weft::ParallelismSpec par;
+    par.tp = m.cfg.tp;
+    par.sp = m.cfg.tp > 1;
+    try {
+        auto dags = weft::build_layer_dag(ms, par, cl, solo);
+        m.fwd_dag = std::move(dags.first);
+        m.bwd_dag = std::move(dags.second);
+    } catch (const std::exception& e) {
+        return set_error(DH_ERR_CONFIG, e.what());
+    }
+    return DH_OK;
+}
+
+int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
+    auto m = std::make_unique<Model>();
+    m->ctx = ctx;
+    RT_TRY(derive_cfg(c, ctx->tp_size, ctx->tp_rank, &m->cfg));
+    ModelCfg& k = m->cfg;
 
     const size_t H = k.hidden, S = k.seq, T = k.tok_loc, Q = k.qkv_n, A = k.attn_n, F = k.ffn_l;
     const int L = k.layers;
@@ -190,32 +232,7 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     }
     RT_CUDA(cudaStreamSynchronize(s));
 
-    // ---- the layer DAG (same template / specs as the planner)
-    weft::ModelSpec ms;
-    ms.name = "dh-llama";
-    ms.family = weft::ModelFamily::llama;
-    ms.hidden = k.hidden;
-    ms.intermediate = k.ffn;
-    ms.layers = k.layers;
-    ms.seq_len = k.seq;
-    weft::ParallelismSpec par;
-    par.tp = k.tp;
-    par.sp = k.tp > 1;
-    weft::ClusterSpec cl;
-    cl.name = "b200";
-    cl.gpus = 8;
-    cl.per_node = 8;
-    cl.peak_tflops = 2250.0;
-    cl.local_bw_gbs = 900.0;
-    cl.cross_bw_gbs = 50.0;
-    cl.mem_gb = 180.0;
-    try {
-        auto dags = weft::build_layer_dag(ms, par, cl, nullptr);
-        m->fwd_dag = std::move(dags.first);
-        m->bwd_dag = std::move(dags.second);
-    } catch (const std::exception& e) {
-        return set_error(DH_ERR_CONFIG, e.what());
-    }
+    RT_TRY(build_dags(*m, default_cluster(), nullptr));
     *out = m.release();
     return DH_OK;
 }

@@ -161,6 +161,7 @@ struct Model {
     std::vector<int> y_slot;  // slot holding each strand's last-layer output
     // timing probe: events around every launch of one template node
     int probe_node = -1;
+    bool skip_comm = false;  // measurement mode: collectives become no-ops (compute-only time)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probe_events;
 
     template <class T = void>
@@ -169,6 +170,11 @@ struct Model {
     }
 };
 
+int derive_cfg(const dh_model_cfg* c, int tp, int rank, ModelCfg* out);
+weft::ClusterSpec default_cluster();
+int build_dags(Model& m, const weft::ClusterSpec& cl, const weft::SoloTimeTable* solo);
+int configure_plan(Model& m, const char* plan_json, const char* profile_json, const char* cluster_json);
+int lower_ops(Model& m, int mode);
 int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out);
 void model_destroy(Model* m);
 int launch_node(Model& m, const Op& op, cudaStream_t s);

@@ -57,6 +57,10 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise DeviceError(f"CUDA library not built: {LIB_PATH} (run `make cuda`)")
+        # torch bundles a newer libnccl.so.2 than the system one we link; load
+        # torch first so both resolve the soname to torch's copy (loading ours
+        # first would bind the older system NCCL and break `import torch`).
+        import torch  # noqa: F401
         l = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
         for name, args in _SIGS.items():
             if not hasattr(l, name):

@@ -49,6 +49,9 @@ _SIGS = {
     "dh_free_string": ([c_void_p], None),
     "dh_profile_json": ([c_void_p, c_int, ctypes.POINTER(c_void_p)], c_int),
     "dh_model_probe": ([c_void_p, c_int], c_int),
+    "dh_model_set_skip_comm": ([c_void_p, c_int], c_int),
+    "dh_lower_json": ([ctypes.POINTER(ModelCfg), c_int, c_int, c_char_p, c_char_p, c_int,
+                       ctypes.POINTER(c_void_p)], c_int),
     "dh_model_probe_read": ([c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int)], c_int),
 }
 _bound = False
@@ -209,6 +212,9 @@ class Model:
         """Time every launch of template node `node` (-1 disables)."""
         check(_lib().dh_model_probe(self.handle, node))
 
+    def set_skip_comm(self, skip: bool):
+        check(_lib().dh_model_set_skip_comm(self.handle, int(skip)))
+
     def probe_read(self):
         ms, n = ctypes.c_double(), c_int()
         check(_lib().dh_model_probe_read(self.handle, ctypes.byref(ms), ctypes.byref(n)))
@@ -225,4 +231,15 @@ class Model:
             self.handle = None
 
 
-__all__ = ["Context", "Model", "LlamaShape", "LLAMA3_8B", "TINY", "DeviceError", "nccl_unique_id"]
+def lower(shape: "LlamaShape", tp: int, plan_json: str | None, mode: str = "si", rank: int = 0,
+          profile_json: str | None = None) -> dict:
+    """Host-only lowering of a plan to the executor's launch program (no GPU)."""
+    cfg = shape.to_c()
+    p = c_void_p()
+    enc = lambda s: None if s is None else s.encode()  # noqa: E731
+    check(_lib().dh_lower_json(ctypes.byref(cfg), tp, rank, enc(plan_json), enc(profile_json),
+                               {"si": 0, "sequential": 1}[mode], ctypes.byref(p)))
+    return json.loads(_take_string(p))
+
+
+__all__ = ["lower", "Context", "Model", "LlamaShape", "LLAMA3_8B", "TINY", "DeviceError", "nccl_unique_id"]

@@ -1,0 +1,179 @@
+"""CPU: invariants of the SI executor's lowering (csrc/runtime/executor.cpp),
+through the host-only dh_lower_json entry point — no GPU needed.
+
+  * every event wait refers to an earlier op (acyclic, deadlock-free issue);
+  * each strand runs forward layers 0..L-1 in the plan's fwd_seq order and
+    backward layers L-1..0 in bwd_seq order, whatever the interleaving;
+  * activation-slot reuse is safe: when (strand, layer) instance B takes the
+    slot instance A used, every op of A happens-before every op of B in the
+    stream-order + event-wait graph;
+  * SI uses L+1 slots (one more than sequential), and interleaves strands;
+  * every TP rank lowers the identical collective sequence (NCCL requires it),
+    also checked across 2 gloo processes.
+"""
+import hashlib
+import json
+import os
+
+import pytest
+
+from paper_2411_15871_b200 import planner
+from paper_2411_15871_b200.runtime import LLAMA3_8B, TINY, LlamaShape, lower
+from tests.planner_corpus import B200_CLUSTER
+
+COMM_NODES = {1, 6, 9, 13, 21, 27, 30, 37}
+
+
+def _plan(shape, tp, arch="nvlink_h100", caps=None):
+    return planner.lib().search_si_plan(shape.planner_model(), {"tp": tp, "sp": tp > 1}, B200_CLUSTER,
+                                        {"archetype": arch}, caps=caps)["plan_json"]
+
+
+def _happens_before(ops):
+    """preds[i] = direct predecessors (same-lane previous op + waits)."""
+    last = {}
+    preds = []
+    for i, o in enumerate(ops):
+        p = set(o["waits"])
+        if o["lane"] in last:
+            p.add(last[o["lane"]])
+        last[o["lane"]] = i
+        preds.append(p)
+    return preds
+
+
+def _reachable_from(preds, target_set, start):
+    """Is every op in target_set an ancestor of `start`?"""
+    seen, stack = set(), [start]
+    while stack:
+        i = stack.pop()
+        for p in preds[i]:
+            if p not in seen:
+                seen.add(p)
+                stack.append(p)
+    return target_set <= seen
+
+
+def check_program(prog, shape, mb):
+    ops = prog["ops"]
+    L = shape.layers
+    for i, o in enumerate(ops):
+        assert all(w < i for w in o["waits"]), "wait on a later op"
+    for s in range(mb):
+        mine = [(o["layer"], o["node"]) for o in ops if o["strand"] == s]
+        expect = [(l, n) for l in range(L) for n in prog["fwd_seq"]] + \
+                 [(l, n) for l in reversed(range(L)) for n in prog["bwd_seq"]]
+        assert mine == expect, f"strand {s} order"
+    # slot reuse safety
+    preds = _happens_before(ops)
+    inst_ops = {}
+    for i, o in enumerate(ops):
+        inst_ops.setdefault((o["strand"], o["layer"]), []).append(i)
+    by_slot = {}
+    for key, idx in inst_ops.items():
+        by_slot.setdefault(ops[idx[0]]["slot"], []).append((idx[0], key))
+    for slot, users in by_slot.items():
+        users.sort()
+        for (_, a), (_, b) in zip(users, users[1:]):
+            a_ops, b_first = set(inst_ops[a]), inst_ops[b][0]
+            # b's first op must come after all of a's ops (a's last op on each lane suffices)
+            assert _reachable_from(preds, a_ops - {b_first}, b_first) or not (a_ops - {b_first}), \
+                f"slot {slot}: {b} may start before {a} finished"
+    # the layer input of (s, l) lives in (s, l-1)'s slot and must stay live until (s, l) bwd finishes
+    for (s, l), idx in inst_ops.items():
+        if l == 0:
+            continue
+        prev_slot = ops[inst_ops[(s, l - 1)][0]]["slot"]
+        assert all(ops[i]["prev_slot"] == prev_slot for i in idx)
+    return {o["slot"] for o in ops}
+
+
+@pytest.mark.parametrize("tp", [1, 2, 4, 8])
+@pytest.mark.parametrize("mb", [1, 2, 3])
+def test_tiny_programs(tp, mb):
+    shape = LlamaShape(**{**TINY.__dict__, "micro_batches": mb, "n_kv_heads": 4 if tp > 2 else 2})
+    if tp == 8:
+        shape = LlamaShape(**{**shape.__dict__, "n_heads": 8, "n_kv_heads": 8, "head_dim": 64, "hidden": 512,
+                              "ffn": 1024})
+    plan = _plan(shape, tp)
+    si = lower(shape, tp, plan, "si")
+    seq = lower(shape, tp, plan, "sequential")
+    used_si = check_program(si, shape, mb)
+    used_seq = check_program(seq, shape, mb)
+    assert len(used_seq) == shape.layers
+    assert len(used_si) == (shape.layers + 1 if mb > 1 else shape.layers)
+    if mb > 1:  # SI interleaves the two strands inside each SI block
+        strands = [o["strand"] for o in si["ops"]]
+        switches = sum(1 for a, b in zip(strands, strands[1:]) if a != b)
+        assert switches > 2 * shape.layers
+    if tp > 1:
+        comm = [o for o in si["ops"] if o["node"] in COMM_NODES]
+        assert comm and all(o["lane"] == 1 for o in comm)
+        assert all(o["lane"] == 0 for o in si["ops"] if o["node"] not in COMM_NODES)
+
+
+def test_llama3_8b_tp8_h100_plan_program():
+    shape = LlamaShape(**{**LLAMA3_8B.__dict__, "layers": 4, "micro_batches": 2})
+    plan = _plan(shape, 8)
+    p = json.loads(plan)
+    assert p["fwd_cuts"] == [1] and p["bwd_cuts"] == [4]
+    prog = lower(shape, 8, plan, "si")
+    check_program(prog, shape, 2)
+    # first_dx follows the plan's order of mlp_gate_dgrad / mlp_up_dgrad
+    first = p["bwd_seq"].index(24) < p["bwd_seq"].index(25)
+    for o in prog["ops"]:
+        if o["node"] == 24:
+            assert o["first_dx"] == first
+        if o["node"] == 25:
+            assert o["first_dx"] == (not first)
+
+
+def _comm_signature(shape, tp, rank, plan):
+    prog = lower(shape, tp, plan, "si", rank=rank)
+    seq = [(o["strand"], o["layer"], o["node"]) for o in prog["ops"] if o["node"] in COMM_NODES]
+    return hashlib.sha256(json.dumps(seq).encode()).hexdigest()
+
+
+def test_ranks_lower_identical_collective_order():
+    shape = LlamaShape(**{**TINY.__dict__, "n_kv_heads": 4, "micro_batches": 3})
+    plan = _plan(shape, 4, "pcie_a40")
+    sigs = {_comm_signature(shape, 4, r, plan) for r in range(4)}
+    assert len(sigs) == 1
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shape = LlamaShape(**{**TINY.__dict__, "n_kv_heads": 2, "micro_batches": 2})
+        # rank 0 plans and broadcasts (as bench.py broadcasts the NCCL unique id)
+        obj = [_plan(shape, world) if rank == 0 else None, b"\x01" * 128 if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        plan, uid = obj
+        mine = _comm_signature(shape, world, rank, plan)
+        allsig = [None] * world
+        dist.all_gather_object(allsig, mine)
+        q.put((rank, len(set(allsig)) == 1 and uid == b"\x01" * 128))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_agree_on_program():
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}
+    assert all(p.exitcode == 0 for p in procs)
