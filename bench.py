@@ -270,7 +270,8 @@ def emulated_tp_experiment(args, tp, timed_factory):
         "frac_of_overlap_roofline": round(roof / lp, 4),
         "comm_solo_us_per_layer_pair": round(comm_solo, 1),
         "exposed_comm_us_per_layer_pair": {"si": round(exposed, 1), "sequential": round(exposed_seq, 1)},
-        "hidden_comm_frac": round(1.0 - exposed / comm_solo, 4) if comm_solo > 0 else None,
+        # exposed time below zero is timing noise between the two schedules: clamp
+        "hidden_comm_frac": round(min(1.0, 1.0 - exposed / comm_solo), 4) if comm_solo > 0 else None,
         "mfu": round((fl["fwd"] + fl["bwd"]) * pairs / (res["si"] / 1e3) / 1e12 / SPEC_BF16_TFLOPS, 4),
         "plan": {"hidden_comm_frac_model": srch["hidden_comm_frac"], "total_us_model": srch["total_us"],
                  "fwd_cuts": json.loads(srch["plan_json"])["fwd_cuts"],

@@ -1,0 +1,24 @@
+"""Launch one kernel of interest a few times (for ncu --set full captures)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2411_15871_b200 import device as dh
+which = sys.argv[1] if len(sys.argv) > 1 else "gemm_tp1"
+if which.startswith("gemm"):
+    shapes = {"gemm_tp1": (4096, 14336, 4096), "gemm_tp8": (4096, 1792, 4096)}
+    m, n, k = shapes[which]
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
+    d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        dh.gemm(a, b, d)
+elif which.startswith("attn"):
+    T, nq, nkv, D = (4096, 32, 8, 128) if which == "attn_tp1" else (4096, 4, 1, 128)
+    qkv = (torch.randn(T, (nq + 2 * nkv) * D, device="cuda") * 0.5).to(torch.bfloat16)
+    q, k_, v = qkv[:, :nq * D], qkv[:, nq * D:(nq + nkv) * D], qkv[:, (nq + nkv) * D:]
+    o = torch.empty(T, nq * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nq, T, device="cuda")
+    for _ in range(3):
+        dh.attn_fwd(q, k_, v, o, lse, nq, nkv, D, D ** -0.5)
+torch.cuda.synchronize()
+print("ok", which)
