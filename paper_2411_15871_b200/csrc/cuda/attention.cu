@@ -509,6 +509,10 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dq_kernel(
 }
 
 }  // namespace
+
+int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
+                long long ldo, float* lse, int T, int nq, int nkv, float scale, cudaStream_t s);
+
 }  // namespace dh
 
 namespace {
@@ -596,7 +600,8 @@ extern "C" int dh_attn_fwd(const void* q, const void* k, const void* v, long lon
         return dh::set_error(DH_ERR_INVALID, "attn: n_q_heads must be a multiple of n_kv_heads");
     if (tokens <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
-    if (head_dim == 128) return launch_fwd<128>(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, scale, s);
+    // head_dim 128 (every production shape): tcgen05/TMEM kernel (attention_tc.cu)
+    if (head_dim == 128) return dh::attn_fwd_tc(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, scale, s);
     if (head_dim == 64) return launch_fwd<64>(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, scale, s);
     return dh::set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }

@@ -258,18 +258,20 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+}  // namespace
+
 // 2D bf16 tensor map: `inner` contiguous elements per row, `outer` rows,
-// `ld` elements between rows, box = 64 x box_rows, 128-byte swizzle.
-int make_map(CUtensorMap* map, const void* base, long long inner, long long outer, long long ld,
-             int box_rows) {
+// `ld` elements between rows, box = box_inner x box_rows, 128-byte swizzle.
+int make_tma_2d(CUtensorMap* map, const void* base, long long inner, long long outer, long long ld,
+                int box_inner, int box_rows) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return set_error(DH_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 2) % 16) {
-        return set_error(DH_ERR_INVALID, "gemm operand must be 16-byte aligned with 16-byte row pitch");
+        return set_error(DH_ERR_INVALID, "TMA operand must be 16-byte aligned with 16-byte row pitch");
     }
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
-    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -277,6 +279,13 @@ int make_map(CUtensorMap* map, const void* base, long long inner, long long oute
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(DH_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     return DH_OK;
+}
+
+namespace {
+
+int make_map(CUtensorMap* map, const void* base, long long inner, long long outer, long long ld,
+             int box_rows) {
+    return make_tma_2d(map, base, inner, outer, ld, 64, box_rows);
 }
 
 int sm_count() {
