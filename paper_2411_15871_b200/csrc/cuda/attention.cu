@@ -512,10 +512,20 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dq_kernel(
 
 int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
                 long long ldo, float* lse, int T, int nq, int nkv, float scale, cudaStream_t s);
+int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
+                const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
+                float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
+                int nq, int nkv, float scale, cudaStream_t s);
 
 }  // namespace dh
 
 namespace {
+
+#define RT_TC(expr)                 \
+    do {                            \
+        const int rc_ = (expr);     \
+        if (rc_ != DH_OK) return rc_; \
+    } while (0)
 
 template <int D>
 int launch_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
@@ -553,7 +563,11 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
         DH_CUDA_CHECK(cudaGetLastError());
     }
     const int nb = (T + BT - 1) / BT;
-    {
+    if constexpr (D == 128) {
+        // tcgen05/TMEM kernels (attention_tc.cu): dK/dV pass + dQ pass
+        RT_TC(attn_bwd_tc(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq,
+                          lddkv, T, nq, nkv, scale, s));
+    } else {
         const int smem = 6 * BT * D * 2 + 4 * BT * 4;
         static bool cfg = false;
         if (!cfg) {
@@ -567,14 +581,14 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
             static_cast<bf16*>(dk), static_cast<bf16*>(dv), lddkv, T, group, scale);
         DH_CUDA_CHECK(cudaGetLastError());
     }
-    if (group > 1) {
+    if (group > 1) {  // sum the GQA group's per-head dK/dV partials in head order
         const long long total = static_cast<long long>(nkv) * T * D;
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
         attn_bwd_group_reduce<<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
                                                      static_cast<bf16*>(dv), lddkv, T, nkv, group, D);
         DH_CUDA_CHECK(cudaGetLastError());
     }
-    {
+    if constexpr (D != 128) {
         const int smem = 6 * BT * D * 2;
         static bool cfg = false;
         if (!cfg) {

@@ -278,3 +278,497 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
 }
 
 }  // namespace dh
+
+// ===========================================================================
+// Backward (attn_bwd node), two deterministic tcgen05 kernels.
+//
+// dK/dV kernel — one CTA per (128-key block, q head); inner q tiles of 64:
+//   S^T  = K Q^T        M128 N64  K128   A=K (K-major)   B=Q (K-major)
+//   dP^T = V dO^T       M128 N64  K128   A=V (K-major)   B=dO (K-major)
+//   P^T = exp(scale S^T - lse_q), dS^T = P^T (dP^T - D_q)      (thread = key row)
+//   dV  += P^T dO       M128 N128 K64    A=P^T (smem)    B=dO (MN-major)
+//   dK  += dS^T Q       M128 N128 K64    A=dS^T (smem)   B=Q  (MN-major)
+//   TMEM: S^T x2 (64) | dP^T x2 (64) | dV (128) | dK (128) = 512 columns.
+// dQ kernel — one CTA per (128-query block, q head); inner key tiles of 64:
+//   S = Q K^T, dP = dO V^T (M128 N64 K128), dS = P (dP - D)    (thread = query row)
+//   dQ += dS K          M128 N128 K64    A=dS (smem)     B=K (MN-major)
+//   TMEM: S x2 | dP x2 | dQ = 384 columns.
+// No atomics: dQ is produced by its own pass and per-head dK/dV partials of a
+// GQA group are reduced in head order by attn_bwd_group_reduce (attention.cu).
+// ===========================================================================
+
+namespace dh {
+namespace {
+
+constexpr int BT64 = 64;
+constexpr int kTile64 = BT64 * D * 2;  // 16 KB: [2 d-halves][64 rows][128 B]
+constexpr int kHalf64 = kTile64 / 2;   // 8 KB
+
+struct KvSmem {
+    static constexpr int k = 0;                      // 32 KB
+    static constexpr int v = k + kTile;              // 32 KB
+    static constexpr int q = v + kTile;              // 2 x 16 KB
+    static constexpr int dout = q + 2 * kTile64;     // 2 x 16 KB
+    static constexpr int pt = dout + 2 * kTile64;    // 16 KB  [128 keys][64 q]
+    static constexpr int dst = pt + 16384;           // 16 KB
+    static constexpr int vec = dst + 16384;          // lse2 / D: [2][64] each
+    static constexpr int bars = vec + 4 * 64 * 4;
+    static constexpr int total = bars + 256 + 1024;
+};
+
+struct BwdParams {
+    const float* lse;
+    const float* dvec;
+    float* dk_part;
+    float* dv_part;
+    __nv_bfloat16* dk;
+    __nv_bfloat16* dv;
+    __nv_bfloat16* dq;
+    long long lddkv, lddq;
+    int T, group;
+    float scale, scale_log2;
+};
+
+// K-major 64-row tile (one 64-wide K atom per half): k-step kk over d (0..7).
+__device__ __forceinline__ uint64_t desc_k64(uint32_t base, int kk) {
+    return umma_desc_sw128(base + (kk >> 2) * kHalf64 + (kk & 3) * 32, 16, 1024);
+}
+// MN-major 64-row tile used as B with N = d: k-step kk over rows (0..3).
+__device__ __forceinline__ uint64_t desc_mn64(uint32_t base, int kk) {
+    return umma_desc_sw128(base + kk * 2048, kHalf64, 1024);
+}
+// [128 rows][64 K] single-atom K-major tile (P^T, dS^T, dS): k-step kk (0..3).
+__device__ __forceinline__ uint64_t desc_k1atom(uint32_t base, int kk) {
+    return umma_desc_sw128(base + kk * 32, 16, 1024);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                            const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                            const BwdParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + KvSmem::bars);
+    uint64_t* kv_full = bars + 0;
+    uint64_t* q_full = bars + 1;   // [2]
+    uint64_t* q_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;   // [2]
+    uint64_t* p_full = bars + 7;
+    uint64_t* mm_done = bars + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    float* vec = reinterpret_cast<float*>(sm + KvSmem::vec);  // [2][64] lse2, [2][64] D
+
+    const int kb = gridDim.x - 1 - blockIdx.x;  // early key blocks see the most queries
+    const int h = blockIdx.y;
+    const int kvh = h / p.group;
+    const int nq64 = (p.T + BT64 - 1) / BT64;
+    const int i0 = (kb * D) / BT64;  // first q tile with a query >= the block's first key
+    const int n_it = nq64 - i0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_do);
+        mbar_init(kv_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+        }
+        mbar_init(p_full, 128);
+        mbar_init(mm_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(kv_full, 2 * kTile);
+            tma_load_2d(sm + KvSmem::k, &tm_k, kv_full, kvh * D, kb * D);
+            tma_load_2d(sm + KvSmem::k + kHalf, &tm_k, kv_full, kvh * D + 64, kb * D);
+            tma_load_2d(sm + KvSmem::v, &tm_v, kv_full, kvh * D, kb * D);
+            tma_load_2d(sm + KvSmem::v + kHalf, &tm_v, kv_full, kvh * D + 64, kb * D);
+            for (int it = 0; it < n_it; ++it) {
+                const int st = it & 1, qi = i0 + it;
+                mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+                mbar_expect_tx(&q_full[st], 2 * kTile64);
+                uint8_t* qd = sm + KvSmem::q + st * kTile64;
+                uint8_t* od = sm + KvSmem::dout + st * kTile64;
+                tma_load_2d(qd, &tm_q, &q_full[st], h * D, qi * BT64);
+                tma_load_2d(qd + kHalf64, &tm_q, &q_full[st], h * D + 64, qi * BT64);
+                tma_load_2d(od, &tm_do, &q_full[st], h * D, qi * BT64);
+                tma_load_2d(od + kHalf64, &tm_do, &q_full[st], h * D + 64, qi * BT64);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
+        constexpr uint32_t id_g = umma_idesc_bf16(128, 128, false, true);
+        const uint32_t k_addr = smem_u32(sm + KvSmem::k), v_addr = smem_u32(sm + KvSmem::v);
+        const uint32_t pt_addr = smem_u32(sm + KvSmem::pt), ds_addr = smem_u32(sm + KvSmem::dst);
+        auto issue_s = [&](int it) {
+            const int st = it & 1;
+            mbar_wait(&q_full[st], (it >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t q_addr = smem_u32(sm + KvSmem::q + st * kTile64);
+                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + st * kTile64);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    tc_mma_bf16(t_s + st * 64, desc_kmajor(k_addr, kk), desc_k64(q_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16(t_dp + st * 64, desc_kmajor(v_addr, kk), desc_k64(o_addr, kk), id_s, kk > 0);
+                }
+                tc_commit(&s_full[st]);
+            }
+            __syncwarp();
+        };
+        mbar_wait(kv_full, 0);
+        if (n_it > 0) issue_s(0);
+        for (int it = 0; it < n_it; ++it) {
+            const int st = it & 1;
+            if (it + 1 < n_it) issue_s(it + 1);
+            mbar_wait(p_full, it & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t q_addr = smem_u32(sm + KvSmem::q + st * kTile64);
+                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + st * kTile64);
+#pragma unroll
+                for (int kk = 0; kk < BT64 / 16; ++kk) {
+                    tc_mma_bf16(t_dv, desc_k1atom(pt_addr, kk), desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
+                    tc_mma_bf16(t_dk, desc_k1atom(ds_addr, kk), desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
+                }
+                tc_commit(&q_empty[st]);
+                tc_commit(mm_done);
+            }
+            __syncwarp();
+        }
+    } else {
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;  // key row within the block
+        const int key = kb * D + r;
+        const int t_sm = threadIdx.x - 64;  // 0..127 among the softmax warps
+        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        uint8_t* spt = sm + KvSmem::pt;
+        uint8_t* sds = sm + KvSmem::dst;
+        for (int it = 0; it < n_it; ++it) {
+            const int st = it & 1, qi = i0 + it;
+            if (t_sm < BT64) {
+                const int q = qi * BT64 + t_sm;
+                vec[st * 64 + t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] * kLog2e : 0.f;
+                vec[128 + st * 64 + t_sm] = q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
+            }
+            named_barrier(1, 128);
+            mbar_wait(&s_full[st], (it >> 1) & 1);
+            tc_fence_after();
+            float sv[BT64], dpv[BT64];
+#pragma unroll
+            for (int c = 0; c < BT64 / 32; ++c) {
+                uint32_t a[32], b[32];
+                tmem_ld32(t_s + st * 64 + lane_off + c * 32, a);
+                tmem_ld32(t_dp + st * 64 + lane_off + c * 32, b);
+                tmem_ld_wait();
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    sv[c * 32 + t] = __uint_as_float(a[t]);
+                    dpv[c * 32 + t] = __uint_as_float(b[t]);
+                }
+            }
+            // P^T / dS^T smem is read by the previous iteration's dV/dK MMAs.
+            if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
+#pragma unroll
+            for (int c = 0; c < BT64 / 8; ++c) {
+                float pv[8], dv8[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int j = c * 8 + t;
+                    const int q = qi * BT64 + j;
+                    float e = fast_exp2(sv[j] * p.scale_log2 - vec[st * 64 + j]);
+                    if (q < key || q >= p.T || key >= p.T) e = 0.f;
+                    pv[t] = e;
+                    dv8[t] = e * (dpv[j] - vec[128 + st * 64 + j]);
+                }
+                const int off = r * 128 + ((c ^ (r & 7)) << 4);
+                *reinterpret_cast<uint4*>(spt + off) = pack8(pv);
+                *reinterpret_cast<uint4*>(sds + off) = pack8(dv8);
+            }
+            fence_async_shared();
+            tc_fence_before();
+            mbar_arrive(p_full);
+        }
+        if (n_it > 0) mbar_wait(mm_done, (n_it - 1) & 1);
+        tc_fence_after();
+        const bool ok = key < p.T;
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+            uint32_t a[32], b[32];
+            tmem_ld32(t_dk + lane_off + c * 32, a);
+            tmem_ld32(t_dv + lane_off + c * 32, b);
+            tmem_ld_wait();
+            if (!ok) continue;
+            if (p.group == 1) {
+                __nv_bfloat16* kr = p.dk + static_cast<long long>(key) * p.lddkv + kvh * D + c * 32;
+                __nv_bfloat16* vr = p.dv + static_cast<long long>(key) * p.lddkv + kvh * D + c * 32;
+#pragma unroll
+                for (int t = 0; t < 32; t += 8) {
+                    float fk[8], fv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        fk[u] = n_it > 0 ? __uint_as_float(a[t + u]) * p.scale : 0.f;
+                        fv[u] = n_it > 0 ? __uint_as_float(b[t + u]) : 0.f;
+                    }
+                    *reinterpret_cast<uint4*>(kr + t) = pack8(fk);
+                    *reinterpret_cast<uint4*>(vr + t) = pack8(fv);
+                }
+            } else {
+                float* kr = p.dk_part + (static_cast<long long>(h) * p.T + key) * D + c * 32;
+                float* vr = p.dv_part + (static_cast<long long>(h) * p.T + key) * D + c * 32;
+#pragma unroll
+                for (int t = 0; t < 32; t += 4) {
+                    *reinterpret_cast<float4*>(kr + t) =
+                        make_float4(__uint_as_float(a[t]) * p.scale, __uint_as_float(a[t + 1]) * p.scale,
+                                    __uint_as_float(a[t + 2]) * p.scale, __uint_as_float(a[t + 3]) * p.scale);
+                    *reinterpret_cast<float4*>(vr + t) =
+                        make_float4(__uint_as_float(b[t]), __uint_as_float(b[t + 1]),
+                                    __uint_as_float(b[t + 2]), __uint_as_float(b[t + 3]));
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+struct DqSmem {
+    static constexpr int q = 0;                      // 32 KB
+    static constexpr int dout = q + kTile;           // 32 KB
+    static constexpr int k = dout + kTile;           // 2 x 16 KB
+    static constexpr int v = k + 2 * kTile64;        // 2 x 16 KB
+    static constexpr int ds = v + 2 * kTile64;       // 16 KB [128 q][64 keys]
+    static constexpr int bars = ds + 16384;
+    static constexpr int total = bars + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                          const BwdParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DqSmem::bars);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;   // [2]
+    uint64_t* kv_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;    // [2]
+    uint64_t* p_full = bars + 7;
+    uint64_t* mm_done = bars + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+    const int qb = gridDim.x - 1 - blockIdx.x;
+    const int h = blockIdx.y;
+    const int kvh = h / p.group;
+    const int n_it = (qb * D + D) / BT64;  // key tiles 0 .. covering the block's last query
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_do);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+        }
+        mbar_init(p_full, 128);
+        mbar_init(mm_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(q_full, 2 * kTile);
+            tma_load_2d(sm + DqSmem::q, &tm_q, q_full, h * D, qb * D);
+            tma_load_2d(sm + DqSmem::q + kHalf, &tm_q, q_full, h * D + 64, qb * D);
+            tma_load_2d(sm + DqSmem::dout, &tm_do, q_full, h * D, qb * D);
+            tma_load_2d(sm + DqSmem::dout + kHalf, &tm_do, q_full, h * D + 64, qb * D);
+            for (int it = 0; it < n_it; ++it) {
+                const int st = it & 1;
+                mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[st], 2 * kTile64);
+                uint8_t* kd = sm + DqSmem::k + st * kTile64;
+                uint8_t* vd = sm + DqSmem::v + st * kTile64;
+                tma_load_2d(kd, &tm_k, &kv_full[st], kvh * D, it * BT64);
+                tma_load_2d(kd + kHalf64, &tm_k, &kv_full[st], kvh * D + 64, it * BT64);
+                tma_load_2d(vd, &tm_v, &kv_full[st], kvh * D, it * BT64);
+                tma_load_2d(vd + kHalf64, &tm_v, &kv_full[st], kvh * D + 64, it * BT64);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
+        constexpr uint32_t id_g = umma_idesc_bf16(128, 128, false, true);
+        const uint32_t q_addr = smem_u32(sm + DqSmem::q), o_addr = smem_u32(sm + DqSmem::dout);
+        const uint32_t ds_addr = smem_u32(sm + DqSmem::ds);
+        auto issue_s = [&](int it) {
+            const int st = it & 1;
+            mbar_wait(&kv_full[st], (it >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t k_addr = smem_u32(sm + DqSmem::k + st * kTile64);
+                const uint32_t v_addr = smem_u32(sm + DqSmem::v + st * kTile64);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    tc_mma_bf16(t_s + st * 64, desc_kmajor(q_addr, kk), desc_k64(k_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16(t_dp + st * 64, desc_kmajor(o_addr, kk), desc_k64(v_addr, kk), id_s, kk > 0);
+                }
+                tc_commit(&s_full[st]);
+            }
+            __syncwarp();
+        };
+        mbar_wait(q_full, 0);
+        issue_s(0);
+        for (int it = 0; it < n_it; ++it) {
+            const int st = it & 1;
+            if (it + 1 < n_it) issue_s(it + 1);
+            mbar_wait(p_full, it & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t k_addr = smem_u32(sm + DqSmem::k + st * kTile64);
+#pragma unroll
+                for (int kk = 0; kk < BT64 / 16; ++kk)
+                    tc_mma_bf16(t_dq, desc_k1atom(ds_addr, kk), desc_mn64(k_addr, kk), id_g, (it | kk) != 0);
+                tc_commit(&kv_empty[st]);
+                tc_commit(mm_done);
+            }
+            __syncwarp();
+        }
+    } else {
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const int qrow = qb * D + r;
+        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        const int qc = min(qrow, p.T - 1);
+        const float lse2 = p.lse[static_cast<long long>(h) * p.T + qc] * kLog2e;
+        const float dd = p.dvec[static_cast<long long>(h) * p.T + qc];
+        uint8_t* sds = sm + DqSmem::ds;
+        for (int it = 0; it < n_it; ++it) {
+            const int st = it & 1;
+            mbar_wait(&s_full[st], (it >> 1) & 1);
+            tc_fence_after();
+            float sv[BT64], dpv[BT64];
+#pragma unroll
+            for (int c = 0; c < BT64 / 32; ++c) {
+                uint32_t a[32], b[32];
+                tmem_ld32(t_s + st * 64 + lane_off + c * 32, a);
+                tmem_ld32(t_dp + st * 64 + lane_off + c * 32, b);
+                tmem_ld_wait();
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    sv[c * 32 + t] = __uint_as_float(a[t]);
+                    dpv[c * 32 + t] = __uint_as_float(b[t]);
+                }
+            }
+            if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
+#pragma unroll
+            for (int c = 0; c < BT64 / 8; ++c) {
+                float d8[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int j = c * 8 + t;
+                    const int key = it * BT64 + j;
+                    float e = fast_exp2(sv[j] * p.scale_log2 - lse2);
+                    if (key > qrow || key >= p.T) e = 0.f;
+                    d8[t] = e * (dpv[j] - dd);
+                }
+                *reinterpret_cast<uint4*>(sds + r * 128 + ((c ^ (r & 7)) << 4)) = pack8(d8);
+            }
+            fence_async_shared();
+            tc_fence_before();
+            mbar_arrive(p_full);
+        }
+        mbar_wait(mm_done, (n_it - 1) & 1);
+        tc_fence_after();
+        const bool ok = qrow < p.T;
+        __nv_bfloat16* row = p.dq + static_cast<long long>(qrow) * p.lddq + h * D;
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+            uint32_t a[32];
+            tmem_ld32(t_dq + lane_off + c * 32, a);
+            tmem_ld_wait();
+            if (!ok) continue;
+#pragma unroll
+            for (int t = 0; t < 32; t += 8) {
+                float f[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(a[t + u]) * p.scale;
+                *reinterpret_cast<uint4*>(row + c * 32 + t) = pack8(f);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace
+
+// Host launcher for the two tcgen05 backward kernels (dvec must already hold
+// D_i = rowsum(dO * O)); dk_part / dv_part are used only when group > 1.
+int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
+                const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
+                float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
+                int nq, int nkv, float scale, cudaStream_t s) {
+    CUtensorMap mk, mv, mq64, mdo64, mq, mdo, mk64, mv64;
+    const long long qcols = static_cast<long long>(nq) * D, kvcols = static_cast<long long>(nkv) * D;
+    int rc = make_tma_2d(&mk, k, kvcols, T, ldkv, 64, 128);
+    if (!rc) rc = make_tma_2d(&mv, v, kvcols, T, ldkv, 64, 128);
+    if (!rc) rc = make_tma_2d(&mq64, q, qcols, T, ldq, 64, 64);
+    if (!rc) rc = make_tma_2d(&mdo64, dout, qcols, T, ldo, 64, 64);
+    if (!rc) rc = make_tma_2d(&mq, q, qcols, T, ldq, 64, 128);
+    if (!rc) rc = make_tma_2d(&mdo, dout, qcols, T, ldo, 64, 128);
+    if (!rc) rc = make_tma_2d(&mk64, k, kvcols, T, ldkv, 64, 64);
+    if (!rc) rc = make_tma_2d(&mv64, v, kvcols, T, ldkv, 64, 64);
+    if (rc) return rc;
+    static bool cfg = false;
+    if (!cfg) {
+        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, KvSmem::total));
+        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem::total));
+        cfg = true;
+    }
+    BwdParams prm{lse, dvec, dk_part, dv_part, static_cast<__nv_bfloat16*>(dk),
+                  static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
+                  nq / nkv, scale, scale * kLog2e};
+    const int nb = (T + D - 1) / D;
+    attn_bwd_dkdv_tc_kernel<<<dim3(nb, nq), kThreads, KvSmem::total, s>>>(mk, mv, mq64, mdo64, prm);
+    DH_CUDA_CHECK(cudaGetLastError());
+    attn_bwd_dq_tc_kernel<<<dim3(nb, nq), kThreads, DqSmem::total, s>>>(mq, mdo, mk64, mv64, prm);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+}  // namespace dh
