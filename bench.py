@@ -38,6 +38,11 @@ METRIC = "tokens/s & MFU per B200, SI vs sequential; exposed TP comm time per la
 
 # --------------------------------------------------------------------------- helpers
 
+def log(msg):
+    if os.environ.get("RANK", "0") == "0":
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -226,8 +231,10 @@ def emulated_tp_experiment(args, tp, timed_factory):
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     m.set_overlap_ctas(sms - args.nccl_ctas)  # profile with the execution-time SM split
     t0 = time.perf_counter()
+    log(f"emulated tp{tp}: profiling")
     prof = json.loads(m.profile(iters=5))
     prof_s = time.perf_counter() - t0
+    log("emulated: profiled")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"b200_profile_tp{tp}_emulated.json"), "w") as f:
         json.dump(prof, f, indent=1)
@@ -243,6 +250,7 @@ def emulated_tp_experiment(args, tp, timed_factory):
         for _ in range(2):
             step()
         res[mode] = timed(max(2, args.steps), step, stream)
+        log(f"emulated {mode}: {res[mode]:.1f} ms/step")
     m.set_skip_comm(False)
     comm_nodes = {"ag0", "rs0", "ag1", "rs1", "rs1_bwd_ag", "ag1_bwd_rs", "rs0_bwd_ag", "ag0_bwd_rs"}
     comm_solo = sum(e["t_us"] for e in prof["solo"] if e["shape"] in comm_nodes)
@@ -320,7 +328,9 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     ctx = Context.create(local, rank, tp, nid, args.nccl_ctas if tp > 1 else 0)
+    log(f"context tp={tp}; creating model")
     model = Model(ctx, shape)
+    log("model created")
     par = {"tp": tp, "sp": tp > 1}
     prof_path = os.path.join(ROOT, "profiles", f"b200_profile_tp{tp}.json")
     profile = json.load(open(prof_path)) if os.path.exists(prof_path) else {"archetype": "nvlink_h100"}
@@ -359,14 +369,18 @@ def main():
     step = lambda: model.step(optim, use_graph=True)  # noqa: E731
     # dominant kernel probe: mlp_gate (the largest forward GEMM) on the compute lane
     model.probe(10)
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         step()
+        log(f"warmup step {i} issued")
+    barrier()
+    log("warmup done")
     with ClockSampler(local) as clk:
         ms_si = timed(args.steps, step)
     probe_ms, probe_n = model.probe_read()  # last step's launches
     model.probe(-1)
     info = model.info()
 
+    log(f"SI timed: {ms_si:.1f} ms/step")
     ms_seq = None
     if not args.no_sequential:
         model.set_plan(srch["plan_json"], profile_json, mode="sequential")
@@ -393,8 +407,10 @@ def main():
             loss_host.copy_(loss_dev, non_blocking=True)
         stream.synchronize()
 
+    log("sequential done")
     e2e_step()
     ms_e2e = timed(args.steps, e2e_step)
+    log("e2e done")
     h2d = sum(h.numel() * 2 for h in host_in)
     d2h = mb * 4
 

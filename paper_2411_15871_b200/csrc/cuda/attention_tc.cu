@@ -186,24 +186,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             // P smem and O are read by PV_{j-1}: wait for it before touching either.
             if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
             tc_fence_after();
-            if (mx > m_used + kRescaleThreshold || j == 0) {
-                const float m_new = fmaxf(mx, m_used);
-                if (j > 0) {
-                    const float corr = fast_exp2(m_used - m_new);
-                    l *= corr;
+            // Lazy rescale. tcgen05.ld/st are warp-collective (.sync.aligned), so
+            // the decision to touch O is made per warp (__any_sync); lanes that
+            // do not need a new maximum rescale by exactly 1.
+            const bool need = j == 0 || mx > m_used + kRescaleThreshold;
+            const float m_new = need ? fmaxf(mx, m_used) : m_used;
+            if (__any_sync(0xffffffffu, need && j > 0)) {
+                const float corr = need ? fast_exp2(m_used - m_new) : 1.f;
+                l *= corr;
 #pragma unroll 1
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t rr[32];
-                        tmem_ld32(t_o + lane_off + c * 32, rr);
-                        tmem_ld_wait();
+                for (int c = 0; c < D / 32; ++c) {
+                    uint32_t rr[32];
+                    tmem_ld32(t_o + lane_off + c * 32, rr);
+                    tmem_ld_wait();
 #pragma unroll
-                        for (int t = 0; t < 32; ++t) rr[t] = __float_as_uint(__uint_as_float(rr[t]) * corr);
-                        tmem_st32(t_o + lane_off + c * 32, rr);
-                    }
-                    tmem_st_wait();
+                    for (int t = 0; t < 32; ++t) rr[t] = __float_as_uint(__uint_as_float(rr[t]) * corr);
+                    tmem_st32(t_o + lane_off + c * 32, rr);
                 }
-                m_used = m_new;
+                tmem_st_wait();
             }
+            m_used = m_new;
             float rs = 0.f;
 #pragma unroll
             for (int c = 0; c < BKV / 8; ++c) {

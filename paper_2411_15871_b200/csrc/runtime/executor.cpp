@@ -26,6 +26,7 @@
 // layer reads dL/dy) and writes the layer-input gradient to grad[(L-1-l)&1].
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -212,6 +213,7 @@ namespace {
 int issue(Model& m) {
     Ctx& c = *m.ctx;
     std::size_t probe = 0;
+    static const bool trace = std::getenv("DH_TRACE") != nullptr;
     for (std::size_t i = 0; i < m.prog.ops.size(); ++i) {
         const Op& o = m.prog.ops[i];
         cudaStream_t s = c.lane[o.lane];
@@ -220,7 +222,12 @@ int issue(Model& m) {
         // External records stay real timing events inside a captured graph.
         if (probed)
             RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe].first, s, cudaEventRecordExternal));
+        if (trace) std::fprintf(stderr, "[dh] op %zu strand %d layer %d node %d lane %d\n", i, o.strand, o.layer, o.node, o.lane);
         if (!(m.skip_comm && o.lane != 0)) RT_TRY(launch_node(m, o, s));
+        if (trace) {
+            const cudaError_t e = cudaStreamSynchronize(s);
+            std::fprintf(stderr, "[dh]   done: %s\n", cudaGetErrorString(e));
+        }
         if (probed)
             RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe++].second, s, cudaEventRecordExternal));
         if (m.events[i]) RT_CUDA(cudaEventRecord(m.events[i], s));

@@ -170,3 +170,24 @@ def test_attention_fwd_bwd(T, nq, nkv, d):
     dh.attn_bwd(q, k, v, o, lse, do, dqkv2[:, :nq * d], dqkv2[:, nq * d:(nq + nkv) * d],
                 dqkv2[:, (nq + nkv) * d:], nq, nkv, d, scale)
     assert torch.equal(dqkv, dqkv2)
+
+
+def test_attention_forward_rescale_paths():
+    """Row maxima that keep growing for some rows only: exercises the lazy O
+    rescale with per-row (warp-divergent) decisions in the tcgen05 forward."""
+    T, nq, nkv, d = 1024, 4, 1, 128
+    scale = d ** -0.5
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = torch.randn(T, nq * d, device="cuda", generator=g)
+    q[0::2] *= 4.0
+    q[1::2] *= 0.1
+    k = torch.randn(T, nkv * d, device="cuda", generator=g)
+    k *= (1.0 + 6.0 * torch.arange(T, device="cuda") / T)[:, None]
+    v = torch.randn(T, nkv * d, device="cuda", generator=g)
+    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
+    o = torch.empty(T, nq * d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nq, T, device="cuda")
+    dh.attn_fwd(q, k, v, o, lse, nq, nkv, d, scale)
+    o_ref, lse_ref = _attn_ref(q.float(), k.float(), v.float(), nq, nkv, d, scale)
+    assert _rel(o, o_ref) < 1e-2
+    assert (lse - lse_ref).abs().max().item() < 5e-2

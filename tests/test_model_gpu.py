@@ -149,3 +149,33 @@ def test_optimizer_step_changes_weights(ctx):
     assert not torch.equal(w0, w1)
     assert float(m.tensor("grad.wqkv", 0).abs().max()) == 0.0  # zeroed for the next step
     m.close()
+
+
+def test_head_dim_128_model_vs_oracle(ctx):
+    """The production head_dim (128) routes attention through the tcgen05 kernels."""
+    shape = LlamaShape(hidden=512, ffn=1024, n_heads=4, n_kv_heads=2, head_dim=128, layers=2,
+                       seq_len=384, micro_batches=2, rope_theta=500000.0)
+    orc, m, xs, rs = _build(shape, ctx, seed=13)
+    plan = _plan(shape, 1)
+    snaps = []
+    for mode in ("si", "sequential"):
+        m.set_plan(plan, mode=mode)
+        m.zero_grads()
+        m.run_program(use_graph=True)
+        m.sync()
+        snaps.append(_snapshot(m, shape))
+    for k in snaps[0]:
+        assert torch.equal(snaps[0][k], snaps[1][k]), k
+    p = planner.parse_plan(plan)
+    first_gate = p["bwd_seq"].index(24) < p["bwd_seq"].index(25)
+    grads = orc.zero_grads()
+    for s in range(2):
+        loss, y, dx, grads = orc.run(xs[s], rs[s], grads, dx_first_gate=first_gate)
+        tol = 2e-2 * float(np.sqrt(np.sum((y * rs[s]) ** 2)))
+        assert abs(float(snaps[0]["loss"][s]) - loss) < tol
+    assert _rel(snaps[0]["dx"].numpy().reshape(dx.shape), dx) < 3e-2
+    for l in range(shape.layers):
+        ref = np.concatenate([grads[l]["wq"], grads[l]["wk"], grads[l]["wv"]], 0).reshape(-1)
+        assert _rel(snaps[0][f"{l}.wqkv"].numpy(), ref) < 3e-2
+        assert _rel(snaps[0][f"{l}.wo"].numpy(), grads[l]["wo"].reshape(-1)) < 3e-2
+    m.close()
