@@ -361,14 +361,20 @@ __global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restri
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     const long long first = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (mode == 0) {  // all-gather: every rank slot receives the shard
-        for (int j = 0; j < tp; ++j)
-            for (long long i = first; i < chunk_vec; i += stride) dst[j * chunk_vec + i] = src[i];
+        for (long long i = first; i < chunk_vec; i += stride) {
+            const uint4 v = src[i];
+            for (int j = 0; j < tp; ++j) dst[j * chunk_vec + i] = v;
+        }
     } else {          // reduce-scatter: out[i] = sum_j in[j*chunk + i]
         for (long long i = first; i < chunk_vec; i += stride) {
+            uint4 in[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) in[j] = j < tp ? src[j * chunk_vec + i] : make_uint4(0, 0, 0, 0);
             float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int j = 0; j < tp; ++j) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
                 float v[8];
-                unpack8(src[j * chunk_vec + i], v);
+                unpack8(in[j], v);
 #pragma unroll
                 for (int t = 0; t < 8; ++t) acc[t] += v[t];
             }
@@ -546,7 +552,8 @@ int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode,
     const long long chunk = count / 8;
     const double wire = static_cast<double>(count) * 2.0 * (tp - 1);
     const unsigned long long target = link_gbs > 0 ? static_cast<unsigned long long>(wire / link_gbs) : 0ull;
-    comm_proxy_kernel<<<std::max(1, ctas), 512, 0, static_cast<cudaStream_t>(stream)>>>(
+    if (tp > 8) return set_error(DH_ERR_INVALID, "comm_proxy: tp <= 8");
+    comm_proxy_kernel<<<std::max(1, ctas), 1024, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4*>(src), static_cast<uint4*>(dst), chunk, mode, tp, target);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;

@@ -10,11 +10,14 @@
 //
 // CTA = 6 warps:  warp 0  TMA producer (one lane)
 //                 warp 1  TMEM allocator + tcgen05.mma issuer (one elected lane)
-//                 warps 2-5 epilogue: tcgen05.ld TMEM -> registers -> global
-// Tile BM=128 x BN (128 or 256) x BK=64, SWIZZLE_128B smem operands, a 4-6
-// stage TMA ring (full/empty mbarriers) and a double-buffered TMEM
-// accumulator (2 x BN fp32 columns) so the epilogue of tile i overlaps the
-// main loop of tile i+1. The grid is persistent: min(tiles, SMs allowed), which
+//                 warps 2-5 epilogue: tcgen05.ld TMEM -> registers -> swizzled smem
+//                           staging (2 x 16 KB) -> TMA store (bf16) or TMA
+//                           reduce-add (fp32 main-grad accumulation); the legacy
+//                           register path remains for bf16 accumulate.
+// Tile BM=128 x BN (128, 192 or 256, picked per shape for wave quantisation) x
+// BK=64, SWIZZLE_128B smem operands, a 4-6 stage TMA ring (full/empty
+// mbarriers) and a double-buffered TMEM accumulator (2 x BN fp32 columns) so
+// the epilogue of tile i overlaps the main loop of tile i+1. The grid is persistent: min(tiles, SMs allowed), which
 // is how the SI executor caps a GEMM's SM footprint next to NCCL kernels.
 #include <algorithm>
 #include <mutex>
@@ -29,14 +32,17 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
+enum Epi { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiDirect = 2 };
+
 template <int BN>
 struct GemmCfg {
     static constexpr int kStageA = BM * BK * 2;
     static constexpr int kStageB = BN * BK * 2;
     static constexpr int kStageBytes = kStageA + kStageB;
-    static constexpr int kStages = BN == 256 ? 4 : 6;
-    static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kStages = BN == 128 ? 6 : 4;
+    static constexpr int kTmemCols = BN == 128 ? 256 : 512;
+    static constexpr int kStaging = 2 * 16384;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kStaging + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct KParams {
@@ -47,17 +53,19 @@ struct KParams {
     int tiles_m, tiles_n;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool D_F32>
+template <int BN, bool A_MN, bool B_MN, int EPI, bool D_F32>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tma_a,
-                        const __grid_constant__ CUtensorMap tma_b, const KParams p) {
+                        const __grid_constant__ CUtensorMap tma_b,
+                        const __grid_constant__ CUtensorMap tma_d, const KParams p) {
     using Cfg = GemmCfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + Cfg::kStages * Cfg::kStageA;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+    uint8_t* staging = smem + Cfg::kStages * Cfg::kStageBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + Cfg::kStaging);
     uint64_t* empty = full + Cfg::kStages;
     uint64_t* tfull = empty + Cfg::kStages;
     uint64_t* tempty = tfull + 2;
@@ -71,6 +79,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
+        if constexpr (EPI != kEpiDirect) tma_prefetch(&tma_d);
         for (int s = 0; s < Cfg::kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -159,65 +168,106 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         // ------------------------------------------------------------ epilogue
         const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        const int r = quad * 32 + lane;        // row within the tile
+        const bool leader = warp == 4 && lane == 0;  // issues the TMA stores
+        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         int acc = 0;
         uint32_t acc_phase = 0;
+        int chunk = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m0 = (tile % p.tiles_m) * BM;
             const int n0 = (tile / p.tiles_m) * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = m0 + quad * 32 + lane;
-            const bool row_ok = row < p.m;
+            if constexpr (EPI == kEpiStoreBf16) {
+                // 64-column chunks: 128 rows x 128 B, SW128-swizzled, TMA-stored.
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
-                tmem_ld_wait();
-                const int col0 = n0 + c * 32;
-                if (!row_ok || col0 >= p.n) continue;
-                const bool full_chunk = col0 + 32 <= p.n;
-                if constexpr (D_F32) {
-                    float* drow = reinterpret_cast<float*>(p.d) + static_cast<long long>(row) * p.ldd + col0;
-                    if (full_chunk) {
+                for (int c = 0; c < BN / 64; ++c, ++chunk) {
+                    uint8_t* stg = staging + (chunk & 1) * 16384;
+                    if (leader) bulk_wait_read<1>();  // store from 2 chunks ago has left stg
+                    named_barrier(2, 128);
+                    uint32_t v0[32], v1[32];
+                    tmem_ld32(tmem_base + lane_off + acc * BN + c * 64, v0);
+                    tmem_ld32(tmem_base + lane_off + acc * BN + c * 64 + 32, v1);
+                    tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-                            if (p.accumulate) {
-                                const float4 o = *reinterpret_cast<const float4*>(drow + j);
-                                v.x += o.x, v.y += o.y, v.z += o.z, v.w += o.w;
-                            }
-                            *reinterpret_cast<float4*>(drow + j) = v;
-                        }
-                    } else {
-                        for (int j = 0; j < 32 && col0 + j < p.n; ++j) {
-                            float v = __uint_as_float(r[j]);
-                            if (p.accumulate) v += drow[j];
-                            drow[j] = v;
-                        }
+                    for (int u = 0; u < 8; ++u) {
+                        float f[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            f[t] = __uint_as_float(u < 4 ? v0[u * 8 + t] : v1[(u - 4) * 8 + t]);
+                        *reinterpret_cast<uint4*>(stg + r * 128 + ((u ^ (r & 7)) << 4)) = pack8(f);
                     }
-                } else {
-                    __nv_bfloat16* drow =
-                        reinterpret_cast<__nv_bfloat16*>(p.d) + static_cast<long long>(row) * p.ldd + col0;
-                    if (full_chunk) {
+                    fence_async_shared();
+                    named_barrier(2, 128);
+                    if (leader) {
+                        tma_store_2d(&tma_d, stg, n0 + c * 64, m0);
+                        bulk_commit();
+                    }
+                }
+            } else if constexpr (EPI == kEpiAddF32) {
+                // 32-column fp32 chunks, TMA reduce-add into the fp32 main grad.
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c, ++chunk) {
+                    uint8_t* stg = staging + (chunk & 1) * 16384;
+                    if (leader) bulk_wait_read<1>();
+                    named_barrier(2, 128);
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + lane_off + acc * BN + c * 32, v);
+                    tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            float f[8];
-#pragma unroll
-                            for (int t = 0; t < 8; ++t) f[t] = __uint_as_float(r[j + t]);
-                            if (p.accumulate) {
-                                float o[8];
-                                unpack8(*reinterpret_cast<const uint4*>(drow + j), o);
-#pragma unroll
-                                for (int t = 0; t < 8; ++t) f[t] += o[t];
-                            }
-                            *reinterpret_cast<uint4*>(drow + j) = pack8(f);
+                    for (int u = 0; u < 8; ++u) {
+                        *reinterpret_cast<uint4*>(stg + r * 128 + ((u ^ (r & 7)) << 4)) =
+                            make_uint4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
+                    }
+                    fence_async_shared();
+                    named_barrier(2, 128);
+                    if (leader) {
+                        tma_reduce_add_2d(&tma_d, stg, n0 + c * 32, m0);
+                        bulk_commit();
+                    }
+                }
+            } else {
+                const int row = m0 + r;
+                const bool row_ok = row < p.m;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t rr[32];
+                    tmem_ld32(tmem_base + lane_off + acc * BN + c * 32, rr);
+                    tmem_ld_wait();
+                    const int col0 = n0 + c * 32;
+                    if (!row_ok || col0 >= p.n) continue;
+                    const bool full_chunk = col0 + 32 <= p.n;
+                    if constexpr (D_F32) {
+                        float* drow = reinterpret_cast<float*>(p.d) + static_cast<long long>(row) * p.ldd + col0;
+                        for (int j = 0; j < 32 && col0 + j < p.n; ++j) {
+                            float x = __uint_as_float(rr[j]);
+                            if (p.accumulate) x += drow[j];
+                            drow[j] = x;
                         }
                     } else {
-                        for (int j = 0; j < 32 && col0 + j < p.n; ++j) {
-                            float v = __uint_as_float(r[j]);
-                            if (p.accumulate) v += __bfloat162float(drow[j]);
-                            drow[j] = __float2bfloat16(v);
+                        __nv_bfloat16* drow =
+                            reinterpret_cast<__nv_bfloat16*>(p.d) + static_cast<long long>(row) * p.ldd + col0;
+                        if (full_chunk) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 8) {
+                                float f[8];
+#pragma unroll
+                                for (int t = 0; t < 8; ++t) f[t] = __uint_as_float(rr[j + t]);
+                                if (p.accumulate) {
+                                    float o[8];
+                                    unpack8(*reinterpret_cast<const uint4*>(drow + j), o);
+#pragma unroll
+                                    for (int t = 0; t < 8; ++t) f[t] += o[t];
+                                }
+                                *reinterpret_cast<uint4*>(drow + j) = pack8(f);
+                            }
+                        } else {
+                            for (int j = 0; j < 32 && col0 + j < p.n; ++j) {
+                                float x = __uint_as_float(rr[j]);
+                                if (p.accumulate) x += __bfloat162float(drow[j]);
+                                drow[j] = __float2bfloat16(x);
+                            }
                         }
                     }
                 }
@@ -225,6 +275,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+        if constexpr (EPI != kEpiDirect) {
+            if (leader) bulk_wait<0>();
         }
     }
 
@@ -263,17 +316,19 @@ EncodeTiledFn encode_fn() {
 // 2D bf16 tensor map: `inner` contiguous elements per row, `outer` rows,
 // `ld` elements between rows, box = box_inner x box_rows, 128-byte swizzle.
 int make_tma_2d(CUtensorMap* map, const void* base, long long inner, long long outer, long long ld,
-                int box_inner, int box_rows) {
+                int box_inner, int box_rows, bool f32) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return set_error(DH_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 2) % 16) {
+    const int esz = f32 ? 4 : 2;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * esz) % 16) {
         return set_error(DH_ERR_INVALID, "TMA operand must be 16-byte aligned with 16-byte row pitch");
     }
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
     const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+    const CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                          const_cast<void*>(base), dims,
                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -299,13 +354,21 @@ int sm_count() {
     return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool D_F32>
+template <int BN, bool A_MN, bool B_MN, int EPI, bool D_F32>
 int launch(const dh_gemm_args* g, cudaStream_t stream) {
     using Cfg = GemmCfg<BN>;
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, md;
     int rc = A_MN ? make_map(&ma, g->a, g->m, g->k, g->lda, BK) : make_map(&ma, g->a, g->k, g->m, g->lda, BM);
     if (rc) return rc;
     rc = B_MN ? make_map(&mb, g->b, g->n, g->k, g->ldb, BK) : make_map(&mb, g->b, g->k, g->n, g->ldb, BN);
+    if (rc) return rc;
+    if constexpr (EPI == kEpiStoreBf16) {
+        rc = make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 64, BM, false);
+    } else if constexpr (EPI == kEpiAddF32) {
+        rc = make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 32, BM, true);
+    } else {
+        md = ma;  // unused
+    }
     if (rc) return rc;
     KParams p;
     p.d = g->d;
@@ -319,51 +382,66 @@ int launch(const dh_gemm_args* g, cudaStream_t stream) {
     const int tiles = p.tiles_m * p.tiles_n;
     int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
     ctas = std::min(ctas, tiles);
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, D_F32>;
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, EPI, D_F32>;
     static bool configured = false;  // per template instance
     if (!configured) {
         DH_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            Cfg::kSmemBytes));
         configured = true;
     }
-    kern<<<ctas, kThreads, Cfg::kSmemBytes, stream>>>(ma, mb, p);
+    kern<<<ctas, kThreads, Cfg::kSmemBytes, stream>>>(ma, mb, md, p);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }
 
-template <int BN>
+template <int BN, int EPI, bool D_F32>
 int dispatch_major(const dh_gemm_args* g, cudaStream_t s) {
-    const int key = (g->a_mn ? 4 : 0) | (g->b_mn ? 2 : 0) | (g->d_fp32 ? 1 : 0);
+    const int key = (g->a_mn ? 2 : 0) | (g->b_mn ? 1 : 0);
     switch (key) {
-        case 0: return launch<BN, false, false, false>(g, s);
-        case 1: return launch<BN, false, false, true>(g, s);
-        case 2: return launch<BN, false, true, false>(g, s);
-        case 3: return launch<BN, false, true, true>(g, s);
-        case 4: return launch<BN, true, false, false>(g, s);
-        case 5: return launch<BN, true, false, true>(g, s);
-        case 6: return launch<BN, true, true, false>(g, s);
-        default: return launch<BN, true, true, true>(g, s);
+        case 0: return launch<BN, false, false, EPI, D_F32>(g, s);
+        case 1: return launch<BN, false, true, EPI, D_F32>(g, s);
+        case 2: return launch<BN, true, false, EPI, D_F32>(g, s);
+        default: return launch<BN, true, true, EPI, D_F32>(g, s);
     }
+}
+
+template <int BN>
+int dispatch_epi(const dh_gemm_args* g, cudaStream_t s) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(g->d) & 15) == 0 &&
+                         (g->ldd * (g->d_fp32 ? 4 : 2)) % 16 == 0;
+    if (aligned && !g->d_fp32 && !g->accumulate) return dispatch_major<BN, kEpiStoreBf16, false>(g, s);
+    if (aligned && g->d_fp32 && g->accumulate) return dispatch_major<BN, kEpiAddF32, true>(g, s);
+    if (g->d_fp32) return dispatch_major<BN, kEpiDirect, true>(g, s);
+    return dispatch_major<BN, kEpiDirect, false>(g, s);
 }
 
 }  // namespace
 
-// Tile-N choice: the wider tile halves B re-reads; fall back to 128 when 256
-// would leave most SMs idle (few output tiles) or N is narrow.
+// Tile-N choice: the fraction of issued tile area that is useful, given the
+// persistent grid's wave quantisation; ties go to the wider tile (fewer B
+// re-reads). BN 192 keeps MN-major B operands on whole 64-wide swizzle atoms.
 int gemm_pick_bn(int m, int n, int ctas) {
-    const long long t256 = static_cast<long long>((m + BM - 1) / BM) * ((n + 255) / 256);
-    if (n <= 128) return 128;
-    if (t256 < static_cast<long long>(ctas) * 3 / 4) return 128;
-    return 256;
+    const int cand[3] = {256, 192, 128};
+    int best = 128;
+    double best_eff = -1.0;
+    const long long tm = (m + BM - 1) / BM;
+    for (int bn : cand) {
+        const long long tiles = tm * ((n + bn - 1) / bn);
+        const long long waves = (tiles + ctas - 1) / ctas;
+        const double eff = static_cast<double>(m) * n / (static_cast<double>(waves) * ctas * BM * bn);
+        if (eff > best_eff + 1e-3) best_eff = eff, best = bn;
+    }
+    return best;
 }
 
 int gemm(const dh_gemm_args* g, cudaStream_t s) {
     if (g->m <= 0 || g->n <= 0 || g->k <= 0) return set_error(DH_ERR_INVALID, "gemm: empty shape");
     const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
     const int bn = g->tile_n ? g->tile_n : gemm_pick_bn(g->m, g->n, ctas);
-    if (bn == 256) return dispatch_major<256>(g, s);
-    if (bn == 128) return dispatch_major<128>(g, s);
-    return set_error(DH_ERR_INVALID, "gemm: tile_n must be 0, 128 or 256");
+    if (bn == 256) return dispatch_epi<256>(g, s);
+    if (bn == 192) return dispatch_epi<192>(g, s);
+    if (bn == 128) return dispatch_epi<128>(g, s);
+    return set_error(DH_ERR_INVALID, "gemm: tile_n must be 0, 128, 192 or 256");
 }
 
 }  // namespace dh
