@@ -421,15 +421,20 @@ int dispatch_epi(const dh_gemm_args* g, cudaStream_t s) {
 // persistent grid's wave quantisation; ties go to the wider tile (fewer B
 // re-reads). BN 192 keeps MN-major B operands on whole 64-wide swizzle atoms.
 int gemm_pick_bn(int m, int n, int ctas) {
+    // per-tile efficiency of the narrower tiles relative to 256 (measured on
+    // B200: more L2 traffic per FLOP and fewer stages), times wave efficiency
     const int cand[3] = {256, 192, 128};
-    int best = 128;
-    double best_eff = -1.0;
+    const double tile_eff[3] = {1.0, 0.85, 0.75};
+    int best = 256;
+    double best_score = -1.0;
     const long long tm = (m + BM - 1) / BM;
-    for (int bn : cand) {
+    for (int i = 0; i < 3; ++i) {
+        const int bn = cand[i];
         const long long tiles = tm * ((n + bn - 1) / bn);
         const long long waves = (tiles + ctas - 1) / ctas;
-        const double eff = static_cast<double>(m) * n / (static_cast<double>(waves) * ctas * BM * bn);
-        if (eff > best_eff + 1e-3) best_eff = eff, best = bn;
+        const double wave_eff = static_cast<double>(m) * n / (static_cast<double>(waves) * ctas * BM * bn);
+        const double score = wave_eff * tile_eff[i];
+        if (score > best_score + 1e-3) best_score = score, best = bn;
     }
     return best;
 }
