@@ -289,6 +289,193 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a 256 x 256 tile per pair of SMs.
+// Each CTA stages its own 128 rows of A and its half (128) of B per 64-wide k
+// block (32 KB/stage instead of 48 KB for 128 x 256 on one SM: 1.5x less
+// L2->SM traffic per FLOP); the even CTA issues M256 N256 MMAs that read both
+// CTAs' smem and write both CTAs' TMEM (128 lanes x 256 columns each). TMA loads
+// of both CTAs complete on the leader's full barrier; MMA commits multicast to
+// both CTAs' empty / accumulator-full barriers; both epilogues release the
+// accumulator on the leader's tempty barrier.
+
+constexpr int kPairStages = 6;
+constexpr int kPairStage = 2 * BM * BK * 2;  // A rows (128) + B half (128), 32 KB
+constexpr int kPairSmem = kPairStages * kPairStage + 2 * 16384 + 1024 + 256;
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                     const __grid_constant__ CUtensorMap tma_d, const KParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kPairStages * BM * BK * 2;
+    uint8_t* staging = smem + kPairStages * kPairStage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + 2 * 16384);
+    uint64_t* empty = full + kPairStages;
+    uint64_t* tfull = empty + kPairStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int tiles_m = p.tiles_m;  // in units of 256 rows
+    const int num_tiles = tiles_m * p.tiles_n;
+    const int num_kb = (p.k + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma_a);
+        tma_prefetch(&tma_b);
+        tma_prefetch(&tma_d);
+        for (int s = 0; s < kPairStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                const int m0 = (tile % tiles_m) * 256 + rank * BM;  // this CTA's A rows
+                const int n0 = (tile / tiles_m) * 256 + rank * 128;  // this CTA's B half
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_expect_tx(&full[stage], 2 * kPairStage);
+                    const uint32_t bar = leader_addr(&full[stage]);
+                    uint8_t* a_dst = sA + stage * BM * BK * 2;
+                    uint8_t* b_dst = sB + stage * BM * BK * 2;
+                    const int k0 = kb * BK;
+                    if constexpr (A_MN) {
+                        tma_load_2d_pair(a_dst, &tma_a, bar, m0, k0);
+                        tma_load_2d_pair(a_dst + BK * 128, &tma_a, bar, m0 + 64, k0);
+                    } else {
+                        tma_load_2d_pair(a_dst, &tma_a, bar, k0, m0);
+                    }
+                    if constexpr (B_MN) {
+                        tma_load_2d_pair(b_dst, &tma_b, bar, n0, k0);
+                        tma_load_2d_pair(b_dst + BK * 128, &tma_b, bar, n0 + 64, k0);
+                    } else {
+                        tma_load_2d_pair(b_dst, &tma_b, bar, k0, n0);
+                    }
+                    if (++stage == kPairStages) stage = 0, phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            constexpr uint32_t idesc = umma_idesc_bf16(256, 256, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t a_addr = smem_u32(sA + stage * BM * BK * 2);
+                        const uint32_t b_addr = smem_u32(sB + stage * BM * BK * 2);
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk) {
+                            const uint64_t a_desc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, BK * 128, 1024)
+                                                         : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+                            const uint64_t b_desc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, BK * 128, 1024)
+                                                         : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+                            tc_mma_bf16_pair(d_tmem, a_desc, b_desc, idesc, (kb | kk) != 0);
+                        }
+                        tc_commit_pair_mc(&empty[stage]);
+                        if (kb == num_kb - 1) tc_commit_pair_mc(&tfull[acc]);
+                    }
+                    __syncwarp();
+                    if (++stage == kPairStages) stage = 0, phase ^= 1;
+                }
+                if (++acc == 2) acc = 0, acc_phase ^= 1;
+            }
+        }
+    } else {
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const bool store_leader = warp == 4 && lane == 0;
+        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        const uint32_t tempty_leader[2] = {leader_addr(&tempty[0]), leader_addr(&tempty[1])};
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int chunk = 0;
+        for (int tile = pair; tile < num_tiles; tile += npairs) {
+            const int m0 = (tile % tiles_m) * 256 + rank * BM;
+            const int n0 = (tile / tiles_m) * 256;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            constexpr int CW = EPI == kEpiStoreBf16 ? 64 : 32;
+#pragma unroll 1
+            for (int c = 0; c < 256 / CW; ++c, ++chunk) {
+                uint8_t* stg = staging + (chunk & 1) * 16384;
+                if (store_leader) bulk_wait_read<1>();
+                named_barrier(2, 128);
+                if constexpr (EPI == kEpiStoreBf16) {
+                    uint32_t v0[32], v1[32];
+                    tmem_ld32(tmem_base + lane_off + acc * 256 + c * 64, v0);
+                    tmem_ld32(tmem_base + lane_off + acc * 256 + c * 64 + 32, v1);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        float f[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) f[t] = __uint_as_float(u < 4 ? v0[u * 8 + t] : v1[(u - 4) * 8 + t]);
+                        *reinterpret_cast<uint4*>(stg + r * 128 + ((u ^ (r & 7)) << 4)) = pack8(f);
+                    }
+                } else {
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + lane_off + acc * 256 + c * 32, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        *reinterpret_cast<uint4*>(stg + r * 128 + ((u ^ (r & 7)) << 4)) =
+                            make_uint4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
+                }
+                fence_async_shared();
+                named_barrier(2, 128);
+                if (store_leader) {
+                    if constexpr (EPI == kEpiStoreBf16) tma_store_2d(&tma_d, stg, n0 + c * CW, m0);
+                    else tma_reduce_add_2d(&tma_d, stg, n0 + c * CW, m0);
+                    bulk_commit();
+                }
+            }
+            tc_fence_before();
+            mbar_arrive_cluster(tempty_leader[acc]);
+            if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+        if (store_leader) bulk_wait<0>();
+    }
+
+    tc_fence_before();
+    cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem_base, 512);
+    }
+}
+
 // --------------------------------------------------------------------------- host side
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -394,6 +581,49 @@ int launch(const dh_gemm_args* g, cudaStream_t stream) {
     return DH_OK;
 }
 
+template <bool A_MN, bool B_MN, int EPI>
+int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
+    CUtensorMap ma, mb, md;
+    int rc = A_MN ? make_map(&ma, g->a, g->m, g->k, g->lda, BK) : make_map(&ma, g->a, g->k, g->m, g->lda, BM);
+    if (rc) return rc;
+    rc = B_MN ? make_map(&mb, g->b, g->n, g->k, g->ldb, BK) : make_map(&mb, g->b, g->k, g->n, g->ldb, 128);
+    if (rc) return rc;
+    rc = EPI == kEpiStoreBf16 ? make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 64, BM, false)
+                              : make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 32, BM, true);
+    if (rc) return rc;
+    KParams p;
+    p.d = g->d;
+    p.ldd = g->ldd;
+    p.m = g->m;
+    p.n = g->n;
+    p.k = g->k;
+    p.accumulate = g->accumulate;
+    p.tiles_m = (g->m + 255) / 256;
+    p.tiles_n = (g->n + 255) / 256;
+    const int tiles = p.tiles_m * p.tiles_n;
+    const int grid = 2 * std::min(ctas / 2, tiles);
+    auto kern = gemm_pair_kernel<A_MN, B_MN, EPI>;
+    static bool configured = false;
+    if (!configured) {
+        DH_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+        configured = true;
+    }
+    kern<<<grid, kThreads, kPairSmem, stream>>>(ma, mb, md, p);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+template <int EPI>
+int dispatch_pair(const dh_gemm_args* g, cudaStream_t s, int ctas) {
+    const int key = (g->a_mn ? 2 : 0) | (g->b_mn ? 1 : 0);
+    switch (key) {
+        case 0: return launch_pair<false, false, EPI>(g, s, ctas);
+        case 1: return launch_pair<false, true, EPI>(g, s, ctas);
+        case 2: return launch_pair<true, false, EPI>(g, s, ctas);
+        default: return launch_pair<true, true, EPI>(g, s, ctas);
+    }
+}
+
 template <int BN, int EPI, bool D_F32>
 int dispatch_major(const dh_gemm_args* g, cudaStream_t s) {
     const int key = (g->a_mn ? 2 : 0) | (g->b_mn ? 1 : 0);
@@ -417,6 +647,8 @@ int dispatch_epi(const dh_gemm_args* g, cudaStream_t s) {
 
 }  // namespace
 
+constexpr double kPairAdvantage = 1.08;  // measured per-tile gain of 256x256 pairs (see profiles/)
+
 // Tile-N choice: the fraction of issued tile area that is useful, given the
 // persistent grid's wave quantisation; ties go to the wider tile (fewer B
 // re-reads). BN 192 keeps MN-major B operands on whole 64-wide swizzle atoms.
@@ -439,10 +671,33 @@ int gemm_pick_bn(int m, int n, int ctas) {
     return best;
 }
 
+// CTA-pair 256 x 256 tiles when their wave efficiency (with the measured per-
+// tile advantage) beats the best single-CTA tile.
+bool gemm_pick_pair(int m, int n, int ctas) {
+    const int pairs = ctas / 2;
+    if (pairs < 1) return false;
+    const long long tiles = static_cast<long long>((m + 255) / 256) * ((n + 255) / 256);
+    const long long waves = (tiles + pairs - 1) / pairs;
+    const double pair_eff = static_cast<double>(m) * n / (static_cast<double>(waves) * pairs * 65536.0);
+    const int bn = gemm_pick_bn(m, n, ctas);
+    const long long t1 = static_cast<long long>((m + BM - 1) / BM) * ((n + bn - 1) / bn);
+    const long long w1 = (t1 + ctas - 1) / ctas;
+    const double one_eff = static_cast<double>(m) * n / (static_cast<double>(w1) * ctas * BM * bn) *
+                           (bn == 256 ? 1.0 : bn == 192 ? 0.85 : 0.75);
+    return pair_eff * kPairAdvantage > one_eff;
+}
+
 int gemm(const dh_gemm_args* g, cudaStream_t s) {
     if (g->m <= 0 || g->n <= 0 || g->k <= 0) return set_error(DH_ERR_INVALID, "gemm: empty shape");
     const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
-    const int bn = g->tile_n ? g->tile_n : gemm_pick_bn(g->m, g->n, ctas);
+    const bool aligned = (reinterpret_cast<uintptr_t>(g->d) & 15) == 0 &&
+                         (g->ldd * (g->d_fp32 ? 4 : 2)) % 16 == 0;
+    const bool pair_ok = aligned && ((!g->d_fp32 && !g->accumulate) || (g->d_fp32 && g->accumulate));
+    const bool want_pair = g->tile_n == 512 || (g->tile_n == 0 && gemm_pick_pair(g->m, g->n, ctas));
+    if (pair_ok && want_pair) {
+        return g->d_fp32 ? dispatch_pair<kEpiAddF32>(g, s, ctas) : dispatch_pair<kEpiStoreBf16>(g, s, ctas);
+    }
+    const int bn = g->tile_n && g->tile_n != 512 ? g->tile_n : gemm_pick_bn(g->m, g->n, ctas);
     if (bn == 256) return dispatch_epi<256>(g, s);
     if (bn == 192) return dispatch_epi<192>(g, s);
     if (bn == 128) return dispatch_epi<128>(g, s);

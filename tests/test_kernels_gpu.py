@@ -191,3 +191,28 @@ def test_attention_forward_rescale_paths():
     o_ref, lse_ref = _attn_ref(q.float(), k.float(), v.float(), nq, nkv, d, scale)
     assert _rel(o, o_ref) < 1e-2
     assert (lse - lse_ref).abs().max().item() < 5e-2
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", [(256, 256, 64), (4096, 768, 4096), (333, 200, 136), (1024, 4096, 512)])
+def test_gemm_cta_pair(shape, a_mn, b_mn):
+    """tcgen05 cta_group::2 path (tile_n=512 forces the 256x256 CTA-pair kernel)."""
+    m, n, k = shape
+    if (a_mn and m % 8) or (b_mn and n % 8):
+        pytest.skip("TMA needs 16-byte row pitch")
+    A = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
+    a = A.t().contiguous() if a_mn else A
+    b = B.t().contiguous() if b_mn else B
+    d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    dh.gemm(a, b, d, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, tile_n=512)
+    ref = A.float() @ B.float().t()
+    assert _rel(d, ref) < 4e-3
+    g = torch.randn(m, n, device="cuda", dtype=torch.float32)
+    g0 = g.clone()
+    dh.gemm(a, b, g, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, accumulate=True, tile_n=512)
+    assert (g - (g0 + ref)).abs().max().item() < 1e-3 * (g0 + ref).abs().max().item()
+    # capped grid (odd cap rounds down to whole pairs)
+    dh.gemm(a, b, d, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, tile_n=512, max_ctas=7)
+    assert _rel(d, ref) < 4e-3
