@@ -46,7 +46,8 @@ int dh_version(void);
 /* D(m,n) (+)= sum_k A(m,k) B(n,k) on tcgen05 (gemm_tcgen05.cu).
  * a_mn = 0: A(m,k) = a[m*lda + k]  (K-major)     a_mn = 1: A(m,k) = a[k*lda + m]
  * b_mn = 0: B(n,k) = b[n*ldb + k]  (K-major)     b_mn = 1: B(n,k) = b[k*ldb + n]
- * d_fp32 = 0: D bf16, d_fp32 = 1: D fp32; accumulate = 1 adds into D.
+ * d_fp32 = 0: D bf16, d_fp32 = 1: D fp32; accumulate = 1 adds into D (fp32 exact
+ * sum; bf16: D = bf16(D + bf16(acc)) on the CTA-pair path, bf16(D + acc) otherwise).
  * max_ctas caps the persistent grid (0 = every SM); tile_n 0 = auto, 128, 256. */
 typedef struct dh_gemm_args {
     const void* a;

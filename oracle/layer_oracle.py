@@ -241,7 +241,8 @@ class LlamaTPOracle:
             a = d_gate[:, sl] @ p["wg"][sl]
             b = d_up[:, sl] @ p["wu"][sl]
             first, second = (a, b) if dx_first_gate else (b, a)
-            parts.append(nm.rb(nm.rb(first) + second))
+            # the GPU accumulates the second partial with a bf16 TMA reduce-add
+            parts.append(nm.rb(nm.rb(first) + nm.rb(second)))
         g["wg"] += d_gate.T @ c["ln1"]                                         # mlp_fc1_wgrad
         g["wu"] += d_up.T @ c["ln1"]
         dln1 = self._row_parallel(parts)                                       # ag1_bwd_rs

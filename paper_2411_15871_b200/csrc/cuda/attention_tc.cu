@@ -344,7 +344,9 @@ __device__ __forceinline__ uint64_t desc_k1atom(uint32_t base, int kk) {
     return umma_desc_sw128(base + kk * 32, 16, 1024);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
+
+__global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                             const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                             const BwdParams p) {
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&q_empty[i], 1);
             mbar_init(&s_full[i], 1);
         }
-        mbar_init(p_full, 128);
+        mbar_init(p_full, 256);
         mbar_init(mm_done, 1);
         fence_barrier_init();
     }
@@ -452,13 +454,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
         }
     } else {
+        // 8 warps: quadrant (TMEM lanes) = warp & 3, column half = (warp - 2) >> 2
         const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
         const int r = quad * 32 + lane;  // key row within the block
         const int key = kb * D + r;
-        const int t_sm = threadIdx.x - 64;  // 0..127 among the softmax warps
+        const int t_sm = threadIdx.x - 64;  // 0..255 among the elementwise warps
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         uint8_t* spt = sm + KvSmem::pt;
         uint8_t* sds = sm + KvSmem::dst;
+        const int key_hi = kb * D + D - 1;
         for (int it = 0; it < n_it; ++it) {
             const int st = it & 1, qi = i0 + it;
             if (t_sm < BT64) {
@@ -466,39 +471,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                 vec[st * 64 + t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] * kLog2e : 0.f;
                 vec[128 + st * 64 + t_sm] = q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
             }
-            named_barrier(1, 128);
+            named_barrier(1, 256);
             mbar_wait(&s_full[st], (it >> 1) & 1);
             tc_fence_after();
-            float sv[BT64], dpv[BT64];
-#pragma unroll
-            for (int c = 0; c < BT64 / 32; ++c) {
-                uint32_t a[32], b[32];
-                tmem_ld32(t_s + st * 64 + lane_off + c * 32, a);
-                tmem_ld32(t_dp + st * 64 + lane_off + c * 32, b);
-                tmem_ld_wait();
-#pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                    sv[c * 32 + t] = __uint_as_float(a[t]);
-                    dpv[c * 32 + t] = __uint_as_float(b[t]);
-                }
-            }
+            uint32_t a[32], b[32];
+            tmem_ld32(t_s + st * 64 + lane_off + half * 32, a);
+            tmem_ld32(t_dp + st * 64 + lane_off + half * 32, b);
+            tmem_ld_wait();
+            // whole tile causal-visible and in range: no per-element masking
+            const bool full_tile = qi * BT64 >= key_hi && qi * BT64 + BT64 <= p.T && key_hi < p.T;
             // P^T / dS^T smem is read by the previous iteration's dV/dK MMAs.
             if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
+            const float* lv = vec + st * 64 + half * 32;
+            const float* dv_ = vec + 128 + st * 64 + half * 32;
 #pragma unroll
-            for (int c = 0; c < BT64 / 8; ++c) {
-                float pv[8], dv8[8];
+            for (int c = 0; c < 4; ++c) {
+                float pv[8], d8[8];
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int j = c * 8 + t;
-                    const int q = qi * BT64 + j;
-                    float e = fast_exp2(sv[j] * p.scale_log2 - vec[st * 64 + j]);
-                    if (q < key || q >= p.T || key >= p.T) e = 0.f;
+                    float e = fast_exp2(__uint_as_float(a[j]) * p.scale_log2 - lv[j]);
+                    if (!full_tile) {
+                        const int q = qi * BT64 + half * 32 + j;
+                        if (q < key || q >= p.T || key >= p.T) e = 0.f;
+                    }
                     pv[t] = e;
-                    dv8[t] = e * (dpv[j] - vec[128 + st * 64 + j]);
+                    d8[t] = e * (__uint_as_float(b[j]) - dv_[j]);
                 }
-                const int off = r * 128 + ((c ^ (r & 7)) << 4);
+                const int cc = half * 4 + c;
+                const int off = r * 128 + ((cc ^ (r & 7)) << 4);
                 *reinterpret_cast<uint4*>(spt + off) = pack8(pv);
-                *reinterpret_cast<uint4*>(sds + off) = pack8(dv8);
+                *reinterpret_cast<uint4*>(sds + off) = pack8(d8);
             }
             fence_async_shared();
             tc_fence_before();
@@ -508,10 +511,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const bool ok = key < p.T;
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-            uint32_t a[32], b[32];
-            tmem_ld32(t_dk + lane_off + c * 32, a);
-            tmem_ld32(t_dv + lane_off + c * 32, b);
+        for (int c = half * 2; c < half * 2 + 2; ++c) {
+            uint32_t ka[32], va[32];
+            tmem_ld32(t_dk + lane_off + c * 32, ka);
+            tmem_ld32(t_dv + lane_off + c * 32, va);
             tmem_ld_wait();
             if (!ok) continue;
             if (p.group == 1) {
@@ -522,8 +525,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float fk[8], fv[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        fk[u] = n_it > 0 ? __uint_as_float(a[t + u]) * p.scale : 0.f;
-                        fv[u] = n_it > 0 ? __uint_as_float(b[t + u]) : 0.f;
+                        fk[u] = n_it > 0 ? __uint_as_float(ka[t + u]) * p.scale : 0.f;
+                        fv[u] = n_it > 0 ? __uint_as_float(va[t + u]) : 0.f;
                     }
                     *reinterpret_cast<uint4*>(kr + t) = pack8(fk);
                     *reinterpret_cast<uint4*>(vr + t) = pack8(fv);
@@ -534,11 +537,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int t = 0; t < 32; t += 4) {
                     *reinterpret_cast<float4*>(kr + t) =
-                        make_float4(__uint_as_float(a[t]) * p.scale, __uint_as_float(a[t + 1]) * p.scale,
-                                    __uint_as_float(a[t + 2]) * p.scale, __uint_as_float(a[t + 3]) * p.scale);
+                        make_float4(__uint_as_float(ka[t]) * p.scale, __uint_as_float(ka[t + 1]) * p.scale,
+                                    __uint_as_float(ka[t + 2]) * p.scale, __uint_as_float(ka[t + 3]) * p.scale);
                     *reinterpret_cast<float4*>(vr + t) =
-                        make_float4(__uint_as_float(b[t]), __uint_as_float(b[t + 1]),
-                                    __uint_as_float(b[t + 2]), __uint_as_float(b[t + 3]));
+                        make_float4(__uint_as_float(va[t]), __uint_as_float(va[t + 1]),
+                                    __uint_as_float(va[t + 2]), __uint_as_float(va[t + 3]));
                 }
             }
         }
@@ -562,7 +565,7 @@ struct DqSmem {
     static constexpr int total = bars + 256 + 1024;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                           const BwdParams p) {
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&kv_empty[i], 1);
             mbar_init(&s_full[i], 1);
         }
-        mbar_init(p_full, 128);
+        mbar_init(p_full, 256);
         mbar_init(mm_done, 1);
         fence_barrier_init();
     }
@@ -665,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
         const int r = quad * 32 + lane;
         const int qrow = qb * D + r;
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
@@ -676,32 +680,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int st = it & 1;
             mbar_wait(&s_full[st], (it >> 1) & 1);
             tc_fence_after();
-            float sv[BT64], dpv[BT64];
-#pragma unroll
-            for (int c = 0; c < BT64 / 32; ++c) {
-                uint32_t a[32], b[32];
-                tmem_ld32(t_s + st * 64 + lane_off + c * 32, a);
-                tmem_ld32(t_dp + st * 64 + lane_off + c * 32, b);
-                tmem_ld_wait();
-#pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                    sv[c * 32 + t] = __uint_as_float(a[t]);
-                    dpv[c * 32 + t] = __uint_as_float(b[t]);
-                }
-            }
+            uint32_t a[32], b[32];
+            tmem_ld32(t_s + st * 64 + lane_off + half * 32, a);
+            tmem_ld32(t_dp + st * 64 + lane_off + half * 32, b);
+            tmem_ld_wait();
+            const bool full_tile = it * BT64 + BT64 - 1 <= qb * D && it * BT64 + BT64 <= p.T && qb * D + D <= p.T;
             if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
 #pragma unroll
-            for (int c = 0; c < BT64 / 8; ++c) {
+            for (int c = 0; c < 4; ++c) {
                 float d8[8];
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int j = c * 8 + t;
-                    const int key = it * BT64 + j;
-                    float e = fast_exp2(sv[j] * p.scale_log2 - lse2);
-                    if (key > qrow || key >= p.T) e = 0.f;
-                    d8[t] = e * (dpv[j] - dd);
+                    float e = fast_exp2(__uint_as_float(a[j]) * p.scale_log2 - lse2);
+                    if (!full_tile) {
+                        const int key = it * BT64 + half * 32 + j;
+                        if (key > qrow || key >= p.T) e = 0.f;
+                    }
+                    d8[t] = e * (__uint_as_float(b[j]) - dd);
                 }
-                *reinterpret_cast<uint4*>(sds + r * 128 + ((c ^ (r & 7)) << 4)) = pack8(d8);
+                const int cc = half * 4 + c;
+                *reinterpret_cast<uint4*>(sds + r * 128 + ((cc ^ (r & 7)) << 4)) = pack8(d8);
             }
             fence_async_shared();
             tc_fence_before();
@@ -712,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool ok = qrow < p.T;
         __nv_bfloat16* row = p.dq + static_cast<long long>(qrow) * p.lddq + h * D;
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = half * 2; c < half * 2 + 2; ++c) {
             uint32_t a[32];
             tmem_ld32(t_dq + lane_off + c * 32, a);
             tmem_ld_wait();
@@ -766,9 +765,9 @@ int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long
                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
                   nq / nkv, scale, scale * kLog2e};
     const int nb = (T + D - 1) / D;
-    attn_bwd_dkdv_tc_kernel<<<dim3(nb, nq), kThreads, KvSmem::total, s>>>(mk, mv, mq64, mdo64, prm);
+    attn_bwd_dkdv_tc_kernel<<<dim3(nb, nq), kThreadsBwd, KvSmem::total, s>>>(mk, mv, mq64, mdo64, prm);
     DH_CUDA_CHECK(cudaGetLastError());
-    attn_bwd_dq_tc_kernel<<<dim3(nb, nq), kThreads, DqSmem::total, s>>>(mq, mdo, mk64, mv64, prm);
+    attn_bwd_dq_tc_kernel<<<dim3(nb, nq), kThreadsBwd, DqSmem::total, s>>>(mq, mdo, mk64, mv64, prm);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

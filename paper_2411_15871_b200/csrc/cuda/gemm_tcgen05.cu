@@ -32,7 +32,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-enum Epi { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiDirect = 2 };
+enum Epi { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiDirect = 2, kEpiAddBf16 = 3 };
 
 template <int BN>
 struct GemmCfg {
@@ -426,13 +426,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int n0 = (tile / tiles_m) * 256;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            constexpr int CW = EPI == kEpiStoreBf16 ? 64 : 32;
+            constexpr bool kBf16 = EPI == kEpiStoreBf16 || EPI == kEpiAddBf16;
+            constexpr int CW = kBf16 ? 64 : 32;
 #pragma unroll 1
             for (int c = 0; c < 256 / CW; ++c, ++chunk) {
                 uint8_t* stg = staging + (chunk & 1) * 16384;
                 if (store_leader) bulk_wait_read<1>();
                 named_barrier(2, 128);
-                if constexpr (EPI == kEpiStoreBf16) {
+                if constexpr (kBf16) {
                     uint32_t v0[32], v1[32];
                     tmem_ld32(tmem_base + lane_off + acc * 256 + c * 64, v0);
                     tmem_ld32(tmem_base + lane_off + acc * 256 + c * 64 + 32, v1);
@@ -457,7 +458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 named_barrier(2, 128);
                 if (store_leader) {
                     if constexpr (EPI == kEpiStoreBf16) tma_store_2d(&tma_d, stg, n0 + c * CW, m0);
-                    else tma_reduce_add_2d(&tma_d, stg, n0 + c * CW, m0);
+                    else tma_reduce_add_2d(&tma_d, stg, n0 + c * CW, m0);  // f32 or bf16 add
                     bulk_commit();
                 }
             }
@@ -588,8 +589,8 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
     if (rc) return rc;
     rc = B_MN ? make_map(&mb, g->b, g->n, g->k, g->ldb, BK) : make_map(&mb, g->b, g->k, g->n, g->ldb, 128);
     if (rc) return rc;
-    rc = EPI == kEpiStoreBf16 ? make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 64, BM, false)
-                              : make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 32, BM, true);
+    rc = EPI == kEpiAddF32 ? make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 32, BM, true)
+                           : make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 64, BM, false);
     if (rc) return rc;
     KParams p;
     p.d = g->d;
@@ -692,10 +693,12 @@ int gemm(const dh_gemm_args* g, cudaStream_t s) {
     const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
     const bool aligned = (reinterpret_cast<uintptr_t>(g->d) & 15) == 0 &&
                          (g->ldd * (g->d_fp32 ? 4 : 2)) % 16 == 0;
-    const bool pair_ok = aligned && ((!g->d_fp32 && !g->accumulate) || (g->d_fp32 && g->accumulate));
+    const bool pair_ok = aligned && (g->accumulate || !g->d_fp32);
     const bool want_pair = g->tile_n == 512 || (g->tile_n == 0 && gemm_pick_pair(g->m, g->n, ctas));
     if (pair_ok && want_pair) {
-        return g->d_fp32 ? dispatch_pair<kEpiAddF32>(g, s, ctas) : dispatch_pair<kEpiStoreBf16>(g, s, ctas);
+        if (g->d_fp32) return dispatch_pair<kEpiAddF32>(g, s, ctas);
+        // bf16 accumulate = TMA reduce-add: D = bf16(D + bf16(acc))
+        return g->accumulate ? dispatch_pair<kEpiAddBf16>(g, s, ctas) : dispatch_pair<kEpiStoreBf16>(g, s, ctas);
     }
     const int bn = g->tile_n && g->tile_n != 512 ? g->tile_n : gemm_pick_bn(g->m, g->n, ctas);
     if (bn == 256) return dispatch_epi<256>(g, s);

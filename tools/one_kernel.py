@@ -23,3 +23,17 @@ elif which.startswith("attn"):
         dh.attn_fwd(q, k_, v, o, lse, nq, nkv, D, D ** -0.5)
 torch.cuda.synchronize()
 print("ok", which)
+if which.startswith("attnbwd"):
+    T, nq, nkv, D = (4096, 32, 8, 128) if which == "attnbwd_tp1" else (4096, 4, 1, 128)
+    qkv = (torch.randn(T, (nq + 2 * nkv) * D, device="cuda") * 0.5).to(torch.bfloat16)
+    q, k_, v = qkv[:, :nq * D], qkv[:, nq * D:(nq + nkv) * D], qkv[:, (nq + nkv) * D:]
+    o = torch.empty(T, nq * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nq, T, device="cuda")
+    dh.attn_fwd(q, k_, v, o, lse, nq, nkv, D, D ** -0.5)
+    do = torch.randn_like(o)
+    dqkv = torch.empty_like(qkv)
+    for _ in range(2):
+        dh.attn_bwd(q, k_, v, o, lse, do, dqkv[:, :nq * D], dqkv[:, nq * D:(nq + nkv) * D],
+                    dqkv[:, (nq + nkv) * D:], nq, nkv, D, D ** -0.5)
+    torch.cuda.synchronize()
+    print("ok", which)
