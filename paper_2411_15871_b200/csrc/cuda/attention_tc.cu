@@ -309,12 +309,12 @@ constexpr int kHalf64 = kTile64 / 2;   // 8 KB
 struct KvSmem {
     static constexpr int k = 0;                      // 32 KB
     static constexpr int v = k + kTile;              // 32 KB
-    static constexpr int q = v + kTile;              // 2 x 16 KB
-    static constexpr int dout = q + 2 * kTile64;     // 2 x 16 KB
-    static constexpr int pt = dout + 2 * kTile64;    // 16 KB  [128 keys][64 q]
-    static constexpr int dst = pt + 16384;           // 16 KB
-    static constexpr int vec = dst + 16384;          // lse2 / D: [2][64] each
-    static constexpr int bars = vec + 4 * 64 * 4;
+    static constexpr int q = v + kTile;              // 3 x 16 KB
+    static constexpr int dout = q + 3 * kTile64;     // 3 x 16 KB
+    static constexpr int pt = dout + 3 * kTile64;    // 2 x 16 KB  [128 keys][64 q]
+    static constexpr int dst = pt + 2 * 16384;       // 2 x 16 KB
+    static constexpr int vec = dst + 2 * 16384;      // per stage: lse[64], D[64] (raw)
+    static constexpr int bars = vec + 3 * 128 * 4;
     static constexpr int total = bars + 256 + 1024;
 };
 
@@ -355,13 +355,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                                              ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + KvSmem::bars);
     uint64_t* kv_full = bars + 0;
-    uint64_t* q_full = bars + 1;   // [2]
-    uint64_t* q_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;   // [2]
-    uint64_t* p_full = bars + 7;
-    uint64_t* mm_done = bars + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
-    float* vec = reinterpret_cast<float*>(sm + KvSmem::vec);  // [2][64] lse2, [2][64] D
+    uint64_t* q_full = bars + 1;   // [3] Q/dO ring
+    uint64_t* q_empty = bars + 4;  // [3]
+    uint64_t* s_full = bars + 7;   // [2] TMEM S^T/dP^T buffers
+    uint64_t* p_full = bars + 9;
+    uint64_t* mm_done = bars + 10;  // [2], one per P^T/dS^T buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    float* vec = reinterpret_cast<float*>(sm + KvSmem::vec);  // [stage][lse 64 | D 64]
 
     const int kb = gridDim.x - 1 - blockIdx.x;  // early key blocks see the most queries
     const int h = blockIdx.y;
@@ -377,13 +377,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
         mbar_init(kv_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 3; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
-            mbar_init(&s_full[i], 1);
         }
+        for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
         mbar_init(p_full, 256);
-        mbar_init(mm_done, 1);
+        mbar_init(&mm_done[0], 1);
+        mbar_init(&mm_done[1], 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -392,6 +393,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384;
+    const bool bulk_vec = (p.T % BT64) == 0;  // lse / D rows fetched by bulk copy
 
     if (warp == 0) {
         if (lane == 0) {
@@ -401,9 +403,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             tma_load_2d(sm + KvSmem::v, &tm_v, kv_full, kvh * D, kb * D);
             tma_load_2d(sm + KvSmem::v + kHalf, &tm_v, kv_full, kvh * D + 64, kb * D);
             for (int it = 0; it < n_it; ++it) {
-                const int st = it & 1, qi = i0 + it;
-                mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
-                mbar_expect_tx(&q_full[st], 2 * kTile64);
+                const int st = it % 3, qi = i0 + it;
+                mbar_wait(&q_empty[st], ((it / 3) & 1) ^ 1);
+                mbar_expect_tx(&q_full[st], 2 * kTile64 + (bulk_vec ? 512 : 0));
+                if (bulk_vec) {
+                    const long long off = static_cast<long long>(h) * p.T + qi * BT64;
+                    bulk_load_1d(vec + st * 128, p.lse + off, 256, &q_full[st]);
+                    bulk_load_1d(vec + st * 128 + 64, p.dvec + off, 256, &q_full[st]);
+                }
                 uint8_t* qd = sm + KvSmem::q + st * kTile64;
                 uint8_t* od = sm + KvSmem::dout + st * kTile64;
                 tma_load_2d(qd, &tm_q, &q_full[st], h * D, qi * BT64);
@@ -418,38 +425,39 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         const uint32_t k_addr = smem_u32(sm + KvSmem::k), v_addr = smem_u32(sm + KvSmem::v);
         const uint32_t pt_addr = smem_u32(sm + KvSmem::pt), ds_addr = smem_u32(sm + KvSmem::dst);
         auto issue_s = [&](int it) {
-            const int st = it & 1;
-            mbar_wait(&q_full[st], (it >> 1) & 1);
+            const int qs = it % 3, sb = it & 1;  // smem ring stage, TMEM buffer
+            mbar_wait(&q_full[qs], (it / 3) & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t q_addr = smem_u32(sm + KvSmem::q + st * kTile64);
-                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + st * kTile64);
+                const uint32_t q_addr = smem_u32(sm + KvSmem::q + qs * kTile64);
+                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + qs * kTile64);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    tc_mma_bf16(t_s + st * 64, desc_kmajor(k_addr, kk), desc_k64(q_addr, kk), id_s, kk > 0);
-                    tc_mma_bf16(t_dp + st * 64, desc_kmajor(v_addr, kk), desc_k64(o_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16(t_s + sb * 64, desc_kmajor(k_addr, kk), desc_k64(q_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16(t_dp + sb * 64, desc_kmajor(v_addr, kk), desc_k64(o_addr, kk), id_s, kk > 0);
                 }
-                tc_commit(&s_full[st]);
+                tc_commit(&s_full[sb]);
             }
             __syncwarp();
         };
         mbar_wait(kv_full, 0);
         if (n_it > 0) issue_s(0);
         for (int it = 0; it < n_it; ++it) {
-            const int st = it & 1;
+            const int st = it & 1, qs = it % 3;
             if (it + 1 < n_it) issue_s(it + 1);
             mbar_wait(p_full, it & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t q_addr = smem_u32(sm + KvSmem::q + st * kTile64);
-                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + st * kTile64);
+                const uint32_t q_addr = smem_u32(sm + KvSmem::q + qs * kTile64);
+                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + qs * kTile64);
+                const uint32_t pb = pt_addr + st * 16384, db = ds_addr + st * 16384;
 #pragma unroll
                 for (int kk = 0; kk < BT64 / 16; ++kk) {
-                    tc_mma_bf16(t_dv, desc_k1atom(pt_addr, kk), desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
-                    tc_mma_bf16(t_dk, desc_k1atom(ds_addr, kk), desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
+                    tc_mma_bf16(t_dv, desc_k1atom(pb, kk), desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
+                    tc_mma_bf16(t_dk, desc_k1atom(db, kk), desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
                 }
-                tc_commit(&q_empty[st]);
-                tc_commit(mm_done);
+                tc_commit(&q_empty[qs]);
+                tc_commit(&mm_done[st]);
             }
             __syncwarp();
         }
@@ -466,12 +474,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         const int key_hi = kb * D + D - 1;
         for (int it = 0; it < n_it; ++it) {
             const int st = it & 1, qi = i0 + it;
-            if (t_sm < BT64) {
-                const int q = qi * BT64 + t_sm;
-                vec[st * 64 + t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] * kLog2e : 0.f;
-                vec[128 + st * 64 + t_sm] = q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
+            if (!bulk_vec) {
+                // ragged T: stage the vectors with plain loads (s_full implies q_full)
+                named_barrier(1, 256);  // previous readers of this stage are done
+                if (t_sm < BT64) {
+                    const int q = qi * BT64 + t_sm;
+                    vec[(it % 3) * 128 + t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] : 0.f;
+                    vec[(it % 3) * 128 + 64 + t_sm] = q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
+                }
+                named_barrier(1, 256);
             }
-            named_barrier(1, 256);
             mbar_wait(&s_full[st], (it >> 1) & 1);
             tc_fence_after();
             uint32_t a[32], b[32];
@@ -480,17 +492,17 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             tmem_ld_wait();
             // whole tile causal-visible and in range: no per-element masking
             const bool full_tile = qi * BT64 >= key_hi && qi * BT64 + BT64 <= p.T && key_hi < p.T;
-            // P^T / dS^T smem is read by the previous iteration's dV/dK MMAs.
-            if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
-            const float* lv = vec + st * 64 + half * 32;
-            const float* dv_ = vec + 128 + st * 64 + half * 32;
+            // This P^T / dS^T buffer was read by the dV/dK MMAs two iterations ago.
+            if (it > 1) mbar_wait(&mm_done[st], ((it >> 1) - 1) & 1);
+            const float* lv = vec + (it % 3) * 128 + half * 32;
+            const float* dv_ = vec + (it % 3) * 128 + 64 + half * 32;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 float pv[8], d8[8];
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int j = c * 8 + t;
-                    float e = fast_exp2(__uint_as_float(a[j]) * p.scale_log2 - lv[j]);
+                    float e = fast_exp2(__uint_as_float(a[j]) * p.scale_log2 - lv[j] * kLog2e);
                     if (!full_tile) {
                         const int q = qi * BT64 + half * 32 + j;
                         if (q < key || q >= p.T || key >= p.T) e = 0.f;
@@ -499,7 +511,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                     d8[t] = e * (__uint_as_float(b[j]) - dv_[j]);
                 }
                 const int cc = half * 4 + c;
-                const int off = r * 128 + ((cc ^ (r & 7)) << 4);
+                const int off = st * 16384 + r * 128 + ((cc ^ (r & 7)) << 4);
                 *reinterpret_cast<uint4*>(spt + off) = pack8(pv);
                 *reinterpret_cast<uint4*>(sds + off) = pack8(d8);
             }
@@ -507,7 +519,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             tc_fence_before();
             mbar_arrive(p_full);
         }
-        if (n_it > 0) mbar_wait(mm_done, (n_it - 1) & 1);
+        if (n_it > 0) mbar_wait(&mm_done[(n_it - 1) & 1], ((n_it - 1) >> 1) & 1);
         tc_fence_after();
         const bool ok = key < p.T;
 #pragma unroll 1
@@ -558,10 +570,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 struct DqSmem {
     static constexpr int q = 0;                      // 32 KB
     static constexpr int dout = q + kTile;           // 32 KB
-    static constexpr int k = dout + kTile;           // 2 x 16 KB
-    static constexpr int v = k + 2 * kTile64;        // 2 x 16 KB
-    static constexpr int ds = v + 2 * kTile64;       // 16 KB [128 q][64 keys]
-    static constexpr int bars = ds + 16384;
+    static constexpr int k = dout + kTile;           // 3 x 16 KB
+    static constexpr int v = k + 3 * kTile64;        // 3 x 16 KB
+    static constexpr int ds = v + 3 * kTile64;       // 2 x 16 KB [128 q][64 keys]
+    static constexpr int bars = ds + 2 * 16384;
     static constexpr int total = bars + 256 + 1024;
 };
 
@@ -574,12 +586,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                                              ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DqSmem::bars);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [2]
-    uint64_t* p_full = bars + 7;
-    uint64_t* mm_done = bars + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* kv_full = bars + 1;   // [3] K/V ring
+    uint64_t* kv_empty = bars + 4;  // [3]
+    uint64_t* s_full = bars + 7;    // [2]
+    uint64_t* p_full = bars + 9;
+    uint64_t* mm_done = bars + 10;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
     const int qb = gridDim.x - 1 - blockIdx.x;
     const int h = blockIdx.y;
@@ -593,13 +605,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 3; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
-            mbar_init(&s_full[i], 1);
         }
+        for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
         mbar_init(p_full, 256);
-        mbar_init(mm_done, 1);
+        mbar_init(&mm_done[0], 1);
+        mbar_init(&mm_done[1], 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -617,8 +630,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             tma_load_2d(sm + DqSmem::dout, &tm_do, q_full, h * D, qb * D);
             tma_load_2d(sm + DqSmem::dout + kHalf, &tm_do, q_full, h * D + 64, qb * D);
             for (int it = 0; it < n_it; ++it) {
-                const int st = it & 1;
-                mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+                const int st = it % 3;
+                mbar_wait(&kv_empty[st], ((it / 3) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[st], 2 * kTile64);
                 uint8_t* kd = sm + DqSmem::k + st * kTile64;
                 uint8_t* vd = sm + DqSmem::v + st * kTile64;
@@ -634,35 +647,36 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         const uint32_t q_addr = smem_u32(sm + DqSmem::q), o_addr = smem_u32(sm + DqSmem::dout);
         const uint32_t ds_addr = smem_u32(sm + DqSmem::ds);
         auto issue_s = [&](int it) {
-            const int st = it & 1;
-            mbar_wait(&kv_full[st], (it >> 1) & 1);
+            const int ks = it % 3, sb = it & 1;
+            mbar_wait(&kv_full[ks], (it / 3) & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t k_addr = smem_u32(sm + DqSmem::k + st * kTile64);
-                const uint32_t v_addr = smem_u32(sm + DqSmem::v + st * kTile64);
+                const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
+                const uint32_t v_addr = smem_u32(sm + DqSmem::v + ks * kTile64);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    tc_mma_bf16(t_s + st * 64, desc_kmajor(q_addr, kk), desc_k64(k_addr, kk), id_s, kk > 0);
-                    tc_mma_bf16(t_dp + st * 64, desc_kmajor(o_addr, kk), desc_k64(v_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16(t_s + sb * 64, desc_kmajor(q_addr, kk), desc_k64(k_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16(t_dp + sb * 64, desc_kmajor(o_addr, kk), desc_k64(v_addr, kk), id_s, kk > 0);
                 }
-                tc_commit(&s_full[st]);
+                tc_commit(&s_full[sb]);
             }
             __syncwarp();
         };
         mbar_wait(q_full, 0);
         issue_s(0);
         for (int it = 0; it < n_it; ++it) {
-            const int st = it & 1;
+            const int st = it & 1, ks = it % 3;
             if (it + 1 < n_it) issue_s(it + 1);
             mbar_wait(p_full, it & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t k_addr = smem_u32(sm + DqSmem::k + st * kTile64);
+                const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
 #pragma unroll
                 for (int kk = 0; kk < BT64 / 16; ++kk)
-                    tc_mma_bf16(t_dq, desc_k1atom(ds_addr, kk), desc_mn64(k_addr, kk), id_g, (it | kk) != 0);
-                tc_commit(&kv_empty[st]);
-                tc_commit(mm_done);
+                    tc_mma_bf16(t_dq, desc_k1atom(ds_addr + st * 16384, kk), desc_mn64(k_addr, kk), id_g,
+                                (it | kk) != 0);
+                tc_commit(&kv_empty[ks]);
+                tc_commit(&mm_done[st]);
             }
             __syncwarp();
         }
@@ -685,7 +699,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             tmem_ld32(t_dp + st * 64 + lane_off + half * 32, b);
             tmem_ld_wait();
             const bool full_tile = it * BT64 + BT64 - 1 <= qb * D && it * BT64 + BT64 <= p.T && qb * D + D <= p.T;
-            if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
+            if (it > 1) mbar_wait(&mm_done[st], ((it >> 1) - 1) & 1);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 float d8[8];
@@ -700,13 +714,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                     d8[t] = e * (__uint_as_float(b[j]) - dd);
                 }
                 const int cc = half * 4 + c;
-                *reinterpret_cast<uint4*>(sds + r * 128 + ((cc ^ (r & 7)) << 4)) = pack8(d8);
+                *reinterpret_cast<uint4*>(sds + st * 16384 + r * 128 + ((cc ^ (r & 7)) << 4)) = pack8(d8);
             }
             fence_async_shared();
             tc_fence_before();
             mbar_arrive(p_full);
         }
-        mbar_wait(mm_done, (n_it - 1) & 1);
+        mbar_wait(&mm_done[(n_it - 1) & 1], ((n_it - 1) >> 1) & 1);
         tc_fence_after();
         const bool ok = qrow < p.T;
         __nv_bfloat16* row = p.dq + static_cast<long long>(qrow) * p.lddq + h * D;
