@@ -68,12 +68,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::bars);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
+    uint64_t* k_full = bars + 1;    // [2]  K ring: freed once S_j is computed
+    uint64_t* k_empty = bars + 3;   // [2]
     uint64_t* s_full = bars + 5;    // [2]
     uint64_t* p_full = bars + 7;
     uint64_t* pv_done = bars + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* v_full = bars + 9;    // [2]  V ring: freed once PV_j is accumulated
+    uint64_t* v_empty = bars + 11;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
 
     const int qb = gridDim.x - 1 - blockIdx.x;
     const int h = blockIdx.y;
@@ -87,8 +89,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&tm_v);
         mbar_init(q_full, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
             mbar_init(&s_full[i], 1);
         }
         mbar_init(p_full, 128);
@@ -107,16 +111,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(q_full, kTile);
             tma_load_2d(sm + FwdSmem::q, &tm_q, q_full, h * D, qb * BQ);
             tma_load_2d(sm + FwdSmem::q + kHalf, &tm_q, q_full, h * D + 64, qb * BQ);
-            for (int j = 0; j < n_kv; ++j) {
+            // K runs up to two blocks ahead of V (it is released as soon as S_j is done)
+            auto load_k = [&](int j) {
                 const int st = j & 1;
-                mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-                mbar_expect_tx(&kv_full[st], 2 * kTile);
+                mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(&k_full[st], kTile);
                 uint8_t* kd = sm + FwdSmem::k + st * kTile;
+                tma_load_2d(kd, &tm_k, &k_full[st], kvh * D, j * BKV);
+                tma_load_2d(kd + kHalf, &tm_k, &k_full[st], kvh * D + 64, j * BKV);
+            };
+            auto load_v = [&](int j) {
+                const int st = j & 1;
+                mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(&v_full[st], kTile);
                 uint8_t* vd = sm + FwdSmem::v + st * kTile;
-                tma_load_2d(kd, &tm_k, &kv_full[st], kvh * D, j * BKV);
-                tma_load_2d(kd + kHalf, &tm_k, &kv_full[st], kvh * D + 64, j * BKV);
-                tma_load_2d(vd, &tm_v, &kv_full[st], kvh * D, j * BKV);
-                tma_load_2d(vd + kHalf, &tm_v, &kv_full[st], kvh * D + 64, j * BKV);
+                tma_load_2d(vd, &tm_v, &v_full[st], kvh * D, j * BKV);
+                tma_load_2d(vd + kHalf, &tm_v, &v_full[st], kvh * D + 64, j * BKV);
+            };
+            load_k(0);
+            if (n_kv > 1) load_k(1);
+            for (int j = 0; j < n_kv; ++j) {
+                load_v(j);
+                if (j + 2 < n_kv) load_k(j + 2);
             }
         }
     } else if (warp == 1) {
@@ -126,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t p_addr = smem_u32(sm + FwdSmem::p);
         auto issue_s = [&](int j) {
             const int st = j & 1;
-            mbar_wait(&kv_full[st], (j >> 1) & 1);
+            mbar_wait(&k_full[st], (j >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t k_addr = smem_u32(sm + FwdSmem::k + st * kTile);
@@ -135,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_mma_bf16(t_s0 + st * 128, desc_kmajor(q_addr, kk), desc_kmajor(k_addr, kk), id_s,
                                 kk > 0);
                 tc_commit(&s_full[st]);
+                tc_commit(&k_empty[st]);
             }
             __syncwarp();
         };
@@ -143,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < n_kv; ++j) {
             if (j + 1 < n_kv) issue_s(j + 1);
             mbar_wait(p_full, j & 1);
+            mbar_wait(&v_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t v_addr = smem_u32(sm + FwdSmem::v + (j & 1) * kTile);
@@ -150,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < BKV / 16; ++kk)
                     tc_mma_bf16(t_o, desc_kmajor(p_addr, kk), desc_mnmajor(v_addr, kk), id_o,
                                 (j | kk) != 0);
-                tc_commit(&kv_empty[j & 1]);
+                tc_commit(&v_empty[j & 1]);
                 tc_commit(pv_done);
             }
             __syncwarp();
