@@ -202,8 +202,9 @@ void dh_free_string(char* s);
  * off) in the lowered program, on the launching lane stream; after a run,
  * dh_model_probe_read returns the summed kernel time and the launch count. */
 int dh_model_probe(dh_model* m, int node);
-/* Measurement mode: skip every collective launch (keeps the schedule and its
- * event edges) so T_SI - T_compute_only gives the exposed communication. */
+/* Measurement mode: re-lower the current plan without its collective nodes
+ * (compute order and step barriers unchanged) so T_SI - T_compute_only gives
+ * the exposed communication. */
 int dh_model_set_skip_comm(dh_model* m, int skip);
 int dh_model_probe_read(dh_model* m, double* total_ms, int* count);
 

@@ -365,7 +365,9 @@ __global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restri
             const uint4 v = src[i];
             for (int j = 0; j < tp; ++j) dst[j * chunk_vec + i] = v;
         }
-    } else {          // reduce-scatter: out[i] = sum_j in[j*chunk + i]
+    } else {          // reduce-scatter stand-in: out[i] = mean_j in[j*chunk + i]
+        // (the mean keeps activations bounded over many emulated layers)
+        const float inv_tp = 1.f / tp;
         for (long long i = first; i < chunk_vec; i += stride) {
             uint4 in[8];
 #pragma unroll
@@ -378,6 +380,8 @@ __global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restri
 #pragma unroll
                 for (int t = 0; t < 8; ++t) acc[t] += v[t];
             }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] *= inv_tp;
             dst[i] = pack8(acc);
         }
     }

@@ -326,11 +326,8 @@ void dh_free_string(char* s) { std::free(s); }
 int dh_model_set_skip_comm(dh_model* m, int skip) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
     m->skip_comm = skip != 0;
-    if (m->graph) {
-        cudaGraphExecDestroy(m->graph);
-        m->graph = nullptr;
-    }
-    return DH_OK;
+    if (!m->have_plan) return DH_OK;
+    return dh::lower_program(*m, m->prog.mode);  // re-lower without / with collectives
 }
 
 int dh_model_probe(dh_model* m, int node) {

@@ -64,6 +64,8 @@ struct Lowering {
     }
 
     void emit(int strand, int layer, int node) {
+        // compute-only measurement program: collectives are left out entirely
+        if (m.skip_comm && lane_of.at(node) != 0) return;
         Op o;
         o.strand = strand;
         o.layer = layer;
@@ -223,7 +225,7 @@ int issue(Model& m) {
         if (probed)
             RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe].first, s, cudaEventRecordExternal));
         if (trace) std::fprintf(stderr, "[dh] op %zu strand %d layer %d node %d lane %d\n", i, o.strand, o.layer, o.node, o.lane);
-        if (!(m.skip_comm && o.lane != 0)) RT_TRY(launch_node(m, o, s));
+        RT_TRY(launch_node(m, o, s));
         if (trace) {
             const cudaError_t e = cudaStreamSynchronize(s);
             std::fprintf(stderr, "[dh]   done: %s\n", cudaGetErrorString(e));
