@@ -87,10 +87,14 @@ int dh_swiglu_bwd(const void* gate, const void* up, const void* dact, void* dgat
 int dh_rope(void* qkv, long long ld, int tokens, int n_q_heads, int n_kv_heads, int head_dim,
             float theta, int pos0, int inverse, void* stream);
 /* Causal GQA flash attention (attention.cu). q/k/v/o are [tokens, heads*head_dim]
- * views with row pitches; lse fp32 [n_q_heads, tokens]. head_dim 64 or 128. */
+ * views with row pitches; lse fp32 [n_q_heads, tokens]. head_dim 64 or 128.
+ * `scratch` (fp32, may be NULL) enables splitting long causal rows into KV
+ * chunks when the grid is too small to balance the SMs (few heads per GPU);
+ * it is used only if scratch_floats >= dh_attn_fwd_scratch_floats(...). */
+long long dh_attn_fwd_scratch_floats(int tokens, int n_q_heads, int n_kv_heads, int head_dim);
 int dh_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
-                void* o, long long ldo, float* lse, int tokens, int n_q_heads, int n_kv_heads,
-                int head_dim, float scale, void* stream);
+                void* o, long long ldo, float* lse, float* scratch, long long scratch_floats,
+                int tokens, int n_q_heads, int n_kv_heads, int head_dim, float scale, void* stream);
 /* dq/dk/dv written (not accumulated); `scratch` fp32 >= tokens*n_q_heads*(2*head_dim+1) floats. */
 int dh_attn_bwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 const void* o, long long ldo, const float* lse, const void* dout,

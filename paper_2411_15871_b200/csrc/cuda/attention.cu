@@ -511,7 +511,9 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dq_kernel(
 }  // namespace
 
 int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
-                long long ldo, float* lse, int T, int nq, int nkv, float scale, cudaStream_t s);
+                long long ldo, float* lse, int T, int nq, int nkv, float scale, float* scratch,
+                long long scratch_floats, cudaStream_t s);
+long long attn_fwd_tc_scratch_floats(int T, int nq);
 int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
                 float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
@@ -607,15 +609,24 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
 
 }  // namespace
 
+extern "C" long long dh_attn_fwd_scratch_floats(int tokens, int n_q_heads, int n_kv_heads, int head_dim) {
+    (void)n_kv_heads;
+    if (head_dim != 128 || tokens <= 0 || n_q_heads <= 0) return 0;
+    return dh::attn_fwd_tc_scratch_floats(tokens, n_q_heads);
+}
+
 extern "C" int dh_attn_fwd(const void* q, const void* k, const void* v, long long ldq,
-                           long long ldkv, void* o, long long ldo, float* lse, int tokens,
-                           int n_q_heads, int n_kv_heads, int head_dim, float scale, void* stream) {
+                           long long ldkv, void* o, long long ldo, float* lse, float* scratch,
+                           long long scratch_floats, int tokens, int n_q_heads, int n_kv_heads,
+                           int head_dim, float scale, void* stream) {
     if (n_kv_heads <= 0 || n_q_heads % n_kv_heads)
         return dh::set_error(DH_ERR_INVALID, "attn: n_q_heads must be a multiple of n_kv_heads");
     if (tokens <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
     // head_dim 128 (every production shape): tcgen05/TMEM kernel (attention_tc.cu)
-    if (head_dim == 128) return dh::attn_fwd_tc(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, scale, s);
+    if (head_dim == 128)
+        return dh::attn_fwd_tc(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, scale,
+                               scratch, scratch_floats, s);
     if (head_dim == 64) return launch_fwd<64>(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, scale, s);
     return dh::set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }

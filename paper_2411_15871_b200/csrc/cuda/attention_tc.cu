@@ -1,8 +1,12 @@
 // Causal GQA flash attention on tcgen05 / TMEM / TMA (head_dim 128) — the
 // attn node (forward). Replaces the mma.sync path of attention.cu for D=128.
 //
-// One CTA per (128-query block, q head); KV blocks of 128 keys, causal blocks
-// only, heaviest query blocks first.
+// One CTA per work item = (128-query block, q head[, KV chunk]); KV blocks of
+// 128 keys, causal blocks only, items dispatched heaviest first across heads.
+// When the grid is too small to balance (few heads per GPU at high TP: the
+// longest causal row is the critical path), long rows are split into KV
+// chunks chosen by an LPT makespan model on the host; each chunk writes an
+// unnormalised fp32 partial (O, max, sum) and attn_fwd_combine merges them.
 //   warp 0       TMA producer: Q once, K/V through a 2-stage ring
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..5   softmax: thread = query row (its TMEM lane)
@@ -16,6 +20,12 @@
 // round trip is rare; P values are bounded by 2^8 in between.
 #include <algorithm>
 #include <cmath>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "dh_capi.h"
@@ -49,6 +59,16 @@ struct FwdParams {
     int T;
     int group;
     float scale_log2;
+    int nq;        // q heads (item index = rank * nq + head)
+    int nqb;       // 128-query blocks
+    int chunk;     // KV blocks per chunk; 0 = no split
+    int maxc;      // chunks of the longest row
+    float* part;   // split partials: O [h][qb][c][d][row], then (m, l) [h][qb][c][row][2]
+};
+
+constexpr int kMaxItems = 1024;  // split schedule entries per head (kernel parameter)
+struct FwdSched {
+    uint32_t item[kMaxItems];  // (qb << 16) | chunk, heaviest first
 };
 
 // K-major operand, 2 swizzle atoms along K (d or keys): k-step kk of 16.
@@ -62,7 +82,8 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int kk) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                       const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+                       const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
+                       const __grid_constant__ FwdSched sched) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -77,10 +98,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* v_empty = bars + 11;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
 
-    const int qb = gridDim.x - 1 - blockIdx.x;
-    const int h = blockIdx.y;
+    const int rank = blockIdx.x / p.nq;
+    const int h = blockIdx.x % p.nq;
+    int qb, ch = 0, kv0 = 0, kv1;
+    if (p.chunk) {
+        const uint32_t e = sched.item[rank];
+        qb = static_cast<int>(e >> 16);
+        ch = static_cast<int>(e & 0xffffu);
+        kv0 = ch * p.chunk;
+        kv1 = min(kv0 + p.chunk, qb + 1);
+    } else {
+        qb = p.nqb - 1 - rank;
+        kv1 = qb + 1;  // causal, BQ == BKV
+    }
+    const bool split = p.chunk && qb + 1 > p.chunk;
     const int kvh = h / p.group;
-    const int n_kv = qb + 1;  // causal, BQ == BKV
+    const int n_kv = kv1 - kv0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -117,16 +150,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
                 mbar_expect_tx(&k_full[st], kTile);
                 uint8_t* kd = sm + FwdSmem::k + st * kTile;
-                tma_load_2d(kd, &tm_k, &k_full[st], kvh * D, j * BKV);
-                tma_load_2d(kd + kHalf, &tm_k, &k_full[st], kvh * D + 64, j * BKV);
+                tma_load_2d(kd, &tm_k, &k_full[st], kvh * D, (kv0 + j) * BKV);
+                tma_load_2d(kd + kHalf, &tm_k, &k_full[st], kvh * D + 64, (kv0 + j) * BKV);
             };
             auto load_v = [&](int j) {
                 const int st = j & 1;
                 mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
                 mbar_expect_tx(&v_full[st], kTile);
                 uint8_t* vd = sm + FwdSmem::v + st * kTile;
-                tma_load_2d(vd, &tm_v, &v_full[st], kvh * D, j * BKV);
-                tma_load_2d(vd + kHalf, &tm_v, &v_full[st], kvh * D + 64, j * BKV);
+                tma_load_2d(vd, &tm_v, &v_full[st], kvh * D, (kv0 + j) * BKV);
+                tma_load_2d(vd + kHalf, &tm_v, &v_full[st], kvh * D + 64, (kv0 + j) * BKV);
             };
             load_k(0);
             if (n_kv > 1) load_k(1);
@@ -193,11 +226,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int t = 0; t < 32; ++t) s[c * 32 + t] = __uint_as_float(rr[t]) * p.scale_log2;
             }
-            const bool diag = j == qb;
+            const bool diag = kv0 + j == qb;
             float mx = -INFINITY;
 #pragma unroll
             for (int t = 0; t < BKV; ++t) {
-                const int key = j * BKV + t;
+                const int key = (kv0 + j) * BKV + t;
                 if ((diag && key > qrow) || key >= p.T) s[t] = -INFINITY;
                 mx = fmaxf(mx, s[t]);
             }
@@ -243,6 +276,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(pv_done, (n_kv - 1) & 1);
         tc_fence_after();
+        if (split) {
+            // unnormalised partial, [d][row] so a warp's stores are coalesced
+            const long long slot = (static_cast<long long>(h) * p.nqb + qb) * p.maxc + ch;
+            float* po = p.part + slot * (BQ * D) + r;
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t rr[32];
+                tmem_ld32(t_o + lane_off + c * 32, rr);
+                tmem_ld_wait();
+#pragma unroll
+                for (int t = 0; t < 32; ++t) po[(c * 32 + t) * BQ] = __uint_as_float(rr[t]);
+            }
+            float* pml = p.part + static_cast<long long>(p.nq) * p.nqb * p.maxc * (BQ * D) + slot * (2 * BQ);
+            *reinterpret_cast<float2*>(pml + 2 * r) = make_float2(m_used, l);
+            goto done;
+        }
+        {
         const float inv = l > 0.f ? 1.f / l : 0.f;
         const bool ok = qrow < p.T;
         __nv_bfloat16* orow = p.o + static_cast<long long>(qrow) * p.ldo + h * D;
@@ -262,8 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (ok) p.lse[static_cast<long long>(h) * p.T + qrow] = (m_used + log2f(l)) * (1.f / kLog2e);
+        }
     }
 
+done:
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -272,11 +324,132 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// Merge the KV-chunk partials of every split row: O = sum_c 2^(m_c-M) O_c / L,
+// L = sum_c 2^(m_c-M) l_c, lse = (M + log2 L) ln 2. Chunks are merged in chunk
+// order, so the result is deterministic. Block = (split query block, head,
+// 16-column slice of d); thread = (row, 8 columns): partial loads are
+// coalesced along rows ([d][row] layout).
+constexpr int kCombineSlices = D / 16;
+__global__ void __launch_bounds__(256) attn_fwd_combine_kernel(const FwdParams p) {
+    const int h = blockIdx.y;
+    const int qb = p.chunk + blockIdx.x;      // rows with more than one chunk
+    const int nc = (qb + p.chunk) / p.chunk;  // ceil((qb + 1) / chunk)
+    const int r = threadIdx.x & (BQ - 1);
+    const int d0 = blockIdx.z * 16 + (threadIdx.x >> 7) * 8;
+    const int qrow = qb * BQ + r;
+    if (qrow >= p.T) return;
+    const long long slot0 = (static_cast<long long>(h) * p.nqb + qb) * p.maxc;
+    const float* pml = p.part + static_cast<long long>(p.nq) * p.nqb * p.maxc * (BQ * D);
+    float mc[16], w[16];
+    float M = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        if (c < nc) {
+            mc[c] = pml[(slot0 + c) * (2 * BQ) + 2 * r];
+            M = fmaxf(M, mc[c]);
+        }
+    }
+    float L = 0.f;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        if (c < nc) {
+            w[c] = exp2f(mc[c] - M);
+            L += w[c] * pml[(slot0 + c) * (2 * BQ) + 2 * r + 1];
+        }
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    float f[8] = {};
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        if (c < nc) {
+            const float* po = p.part + (slot0 + c) * (BQ * D) + r;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f[u] += w[c] * po[(d0 + u) * BQ];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) f[u] *= inv;
+    *reinterpret_cast<uint4*>(p.o + static_cast<long long>(qrow) * p.ldo + h * D + d0) = pack8(f);
+    if (blockIdx.z == 0 && threadIdx.x < BQ)
+        p.lse[static_cast<long long>(h) * p.T + qrow] = (M + log2f(L)) * (1.f / kLog2e);
+}
+
+// Split plan for a causal forward: LPT makespan over the SMs of the item costs
+// (KV blocks + fixed per-item cost + partial write/merge for split items).
+struct FwdSplit {
+    int chunk = 0, maxc = 1, items = 0;
+    FwdSched sched;
+};
+
+double fwd_makespan(int nq, int nqb, int chunk, int sms, std::vector<std::pair<float, uint32_t>>* out) {
+    std::vector<std::pair<float, uint32_t>> it;
+    for (int qb = 0; qb < nqb; ++qb) {
+        const int nc = (qb + chunk) / chunk;
+        for (int c = 0; c < nc; ++c) {
+            const int len = std::min((c + 1) * chunk, qb + 1) - c * chunk;
+            it.push_back({len + 0.3f + (nc > 1 ? 0.5f : 0.f), (static_cast<uint32_t>(qb) << 16) | c});
+        }
+    }
+    std::stable_sort(it.begin(), it.end(), [](const auto& a, const auto& b) {
+        return a.first > b.first || (a.first == b.first && a.second > b.second);
+    });
+    std::priority_queue<double, std::vector<double>, std::greater<double>> load;
+    for (int i = 0; i < sms; ++i) load.push(0.0);
+    double span = 0.0;
+    for (const auto& e : it)
+        for (int hh = 0; hh < nq; ++hh) {
+            const double t = load.top() + e.first;
+            load.pop();
+            load.push(t);
+            span = std::max(span, t);
+        }
+    if (out) *out = std::move(it);
+    return span;
+}
+
+const FwdSplit& fwd_split_plan(int T, int nq) {
+    static std::map<std::pair<int, int>, FwdSplit> cache;  // nodes are stable: references stay valid
+    static std::mutex mu;  // loopback groups launch from several host threads
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(T, nq);
+    auto f = cache.find(key);
+    if (f != cache.end()) return f->second;
+    FwdSplit sp;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int nqb = (T + BQ - 1) / BQ;
+    // many heads x blocks per SM already balance; only small grids are split
+    if (static_cast<long long>(nq) * nqb > 4LL * sms) return cache.emplace(key, sp).first->second;
+    double best = fwd_makespan(nq, nqb, nqb, sms, nullptr);
+    for (int div : {2, 3, 4, 6, 8}) {
+        const int c = std::max(2, (nqb + div - 1) / div);
+        if (c >= nqb || (nqb + c - 1) / c > 16) continue;
+        std::vector<std::pair<float, uint32_t>> it;
+        const double ms = fwd_makespan(nq, nqb, c, sms, &it);
+        if (ms < 0.95 * best && static_cast<int>(it.size()) <= kMaxItems) {
+            best = ms;
+            sp.chunk = c;
+            sp.maxc = (nqb + c - 1) / c;
+            sp.items = static_cast<int>(it.size());
+            for (size_t i = 0; i < it.size(); ++i) sp.sched.item[i] = it[i].second;
+        }
+    }
+    return cache.emplace(key, sp).first->second;
+}
+
 }  // namespace
+
+long long attn_fwd_tc_scratch_floats(int T, int nq) {
+    const FwdSplit& sp = fwd_split_plan(T, nq);
+    if (!sp.chunk) return 0;
+    const long long nqb = (T + BQ - 1) / BQ;
+    return static_cast<long long>(nq) * nqb * sp.maxc * (BQ * D + 2 * BQ);
+}
 
 // Host launcher (dh_attn_fwd dispatches head_dim 128 here).
 int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
-                long long ldo, float* lse, int T, int nq, int nkv, float scale, cudaStream_t s) {
+                long long ldo, float* lse, int T, int nq, int nkv, float scale, float* scratch,
+                long long scratch_floats, cudaStream_t s) {
     CUtensorMap mq, mk, mv;
     int rc = make_tma_2d(&mq, q, static_cast<long long>(nq) * D, T, ldq, 64, BQ);
     if (rc) return rc;
@@ -290,10 +463,22 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
                                            FwdSmem::total));
         cfg = true;
     }
-    FwdParams prm{lse, static_cast<__nv_bfloat16*>(o), ldo, T, nq / nkv, scale * kLog2e};
-    const dim3 grid((T + BQ - 1) / BQ, nq);
-    attn_fwd_tc_kernel<<<grid, kThreads, FwdSmem::total, s>>>(mq, mk, mv, prm);
+    const int nqb = (T + BQ - 1) / BQ;
+    FwdParams prm{lse, static_cast<__nv_bfloat16*>(o), ldo, T, nq / nkv, scale * kLog2e, nq, nqb, 0, 1,
+                  scratch};
+    const FwdSplit& sp = fwd_split_plan(T, nq);
+    const bool split = sp.chunk && scratch && scratch_floats >= attn_fwd_tc_scratch_floats(T, nq);
+    if (split) {
+        prm.chunk = sp.chunk;
+        prm.maxc = sp.maxc;
+    }
+    const int grid = (split ? sp.items : nqb) * nq;
+    attn_fwd_tc_kernel<<<grid, kThreads, FwdSmem::total, s>>>(mq, mk, mv, prm, sp.sched);
     DH_CUDA_CHECK(cudaGetLastError());
+    if (split) {
+        attn_fwd_combine_kernel<<<dim3(nqb - sp.chunk, nq, kCombineSlices), 256, 0, s>>>(prm);
+        DH_CUDA_CHECK(cudaGetLastError());
+    }
     return DH_OK;
 }
 
@@ -364,10 +549,9 @@ __device__ __forceinline__ uint64_t desc_k1atom(uint32_t base, int kk) {
 
 constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
 
-__global__ void __launch_bounds__(kThreadsBwd, 1)
-    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                            const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                            const BwdParams p) {
+__device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, const CUtensorMap& tm_v,
+                                                   const CUtensorMap& tm_q, const CUtensorMap& tm_do,
+                                                   const BwdParams& p, const int kb, const int h) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -381,8 +565,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
     float* vec = reinterpret_cast<float*>(sm + KvSmem::vec);  // [stage][lse 64 | D 64]
 
-    const int kb = gridDim.x - 1 - blockIdx.x;  // early key blocks see the most queries
-    const int h = blockIdx.y;
     const int kvh = h / p.group;
     const int nq64 = (p.T + BT64 - 1) / BT64;
     const int i0 = (kb * D) / BT64;  // first q tile with a query >= the block's first key
@@ -595,10 +777,9 @@ struct DqSmem {
     static constexpr int total = bars + 256 + 1024;
 };
 
-__global__ void __launch_bounds__(kThreadsBwd, 1)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                          const BwdParams p) {
+__device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const CUtensorMap& tm_do,
+                                                 const CUtensorMap& tm_k, const CUtensorMap& tm_v,
+                                                 const BwdParams& p, const int qb, const int h) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -611,8 +792,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     uint64_t* mm_done = bars + 10;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
-    const int qb = gridDim.x - 1 - blockIdx.x;
-    const int h = blockIdx.y;
     const int kvh = h / p.group;
     const int n_it = (qb * D + D) / BT64;  // key tiles 0 .. covering the block's last query
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -766,6 +945,25 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     }
 }
 
+// One launch for both passes: the dK/dV and dQ work items are independent, so
+// interleaving them (rank r = r-th heaviest block of either kind, all heads)
+// lets the light items of one pass fill the tail of the other. With few heads
+// per GPU (high TP) the two separate grids each left their longest causal
+// block as an exposed critical path.
+__global__ void __launch_bounds__(kThreadsBwd, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                       const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
+                       const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                       const __grid_constant__ CUtensorMap tm_k64, const __grid_constant__ CUtensorMap tm_v64,
+                       const BwdParams p, const int nq, const int nb) {
+    const int rank = blockIdx.x / (2 * nq);
+    const int rem = blockIdx.x % (2 * nq);
+    if (rem < nq)
+        attn_bwd_dkdv_body(tm_k, tm_v, tm_q64, tm_do64, p, rank, rem);  // key block `rank` sees the most queries
+    else
+        attn_bwd_dq_body(tm_q, tm_do, tm_k64, tm_v64, p, nb - 1 - rank, rem - nq);
+}
+
 }  // namespace
 
 // Host launcher for the two tcgen05 backward kernels (dvec must already hold
@@ -785,21 +983,18 @@ int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long
     if (!rc) rc = make_tma_2d(&mk64, k, kvcols, T, ldkv, 64, 64);
     if (!rc) rc = make_tma_2d(&mv64, v, kvcols, T, ldkv, 64, 64);
     if (rc) return rc;
+    constexpr int smem = KvSmem::total > DqSmem::total ? KvSmem::total : DqSmem::total;
     static bool cfg = false;
     if (!cfg) {
-        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, KvSmem::total));
-        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem::total));
+        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
     BwdParams prm{lse, dvec, dk_part, dv_part, static_cast<__nv_bfloat16*>(dk),
                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
                   nq / nkv, scale, scale * kLog2e};
     const int nb = (T + D - 1) / D;
-    attn_bwd_dkdv_tc_kernel<<<dim3(nb, nq), kThreadsBwd, KvSmem::total, s>>>(mk, mv, mq64, mdo64, prm);
-    DH_CUDA_CHECK(cudaGetLastError());
-    attn_bwd_dq_tc_kernel<<<dim3(nb, nq), kThreadsBwd, DqSmem::total, s>>>(mq, mdo, mk64, mv64, prm);
+    attn_bwd_tc_kernel<<<2 * nb * nq, kThreadsBwd, smem, s>>>(mk, mv, mq64, mdo64, mq, mdo, mk64, mv64, prm, nq,
+                                                             nb);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

@@ -18,12 +18,17 @@ int kernels_per_node(const Model& m, int node, int layer) {
             return 1;
         case 2: case 12: case 22: case 26: case 28: case 38:
             return 2;
-        case 4:
-            return 1;
+        case 4:  // attn (+ KV-split combine when the launcher splits rows)
+            return m.cfg.head_dim == 128 &&
+                           dh_attn_fwd_scratch_floats(m.cfg.seq, m.cfg.nq_l,
+                                                      m.cfg.nkv_l, m.cfg.head_dim) > 0
+                       ? 2
+                       : 1;
         case 14:
             return layer == m.cfg.layers - 1 ? 3 : 1;
         case 34:
-            return 4 + (group ? 1 : 0);  // dot, dkdv, [group reduce], dq, rope
+            // dot, dK/dV + dQ (one launch for head_dim 128), [group reduce], rope
+            return (m.cfg.head_dim == 128 ? 3 : 4) + (group ? 1 : 0);
         default:
             return 0;  // collectives (NCCL / loopback copies) and memcpy pass-throughs
     }

@@ -193,7 +193,10 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     b.dx1_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
     b.d_o = pool.take(S * A * 2, "act.bwd_transient");
     b.dqkv = pool.take(S * Q * 2, "act.bwd_transient");
-    b.attn_scratch = pool.take(S * k.nq_l * (2 * k.head_dim + 1) * 4, "act.bwd_transient");
+    b.attn_scratch = pool.take(std::max<size_t>(S * k.nq_l * (2 * k.head_dim + 1),
+                                                static_cast<size_t>(dh_attn_fwd_scratch_floats(
+                                                    static_cast<int>(S), k.nq_l, k.nkv_l, k.head_dim))) * 4,
+                               "act.bwd_transient");
     b.ln_partial = pool.take(std::min<size_t>(T, 1184) * H * 4, "act.bwd_transient");
     b.rs_out = pool.take(T * H * 2, "act.bwd_transient");
     for (int i = 0; i < k.micro_batches; ++i) {
@@ -313,8 +316,11 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
             return dh_rope(P(sl.qkv), Q, S, k.nq_l, k.nkv_l, D, k.rope_theta, 0, 0, s);
         case 4: {  // attn
             auto* qkv = m.ptr<__nv_bfloat16>(sl.qkv);
+            // the transient attention scratch is shared with attn_bwd: both run on the compute lane
             return dh_attn_fwd(qkv, qkv + k.nq_l * D, qkv + (k.nq_l + k.nkv_l) * D, Q, Q, P(sl.o), A,
-                               m.ptr<float>(sl.lse), S, k.nq_l, k.nkv_l, D, scale, s);
+                               m.ptr<float>(sl.lse), m.ptr<float>(m.bs.attn_scratch),
+                               static_cast<long long>(m.bs.attn_scratch.bytes / 4), S, k.nq_l, k.nkv_l,
+                               D, scale, s);
         }
         case 5:  // attn_proj (row-parallel: partial sums before the reduce-scatter)
             return gemm(P(sl.o), A, false, W + p.wo, A, false, tp1 ? P(m.fs.rs_out) : P(m.fs.part), H,

@@ -40,8 +40,9 @@ _SIGS = {
     "dh_swiglu_fwd": [c_void_p, c_void_p, c_void_p, c_ll, c_void_p],
     "dh_swiglu_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_ll, c_void_p],
     "dh_rope": [c_void_p, c_ll, c_int, c_int, c_int, c_int, c_float, c_int, c_int, c_void_p],
-    "dh_attn_fwd": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_int,
-                    c_int, c_int, c_int, c_float, c_void_p],
+    "dh_attn_fwd_scratch_floats": [c_int, c_int, c_int, c_int],
+    "dh_attn_fwd": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
+                    c_ll, c_int, c_int, c_int, c_int, c_float, c_void_p],
     "dh_attn_bwd": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
                     c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_int, c_int, c_int,
                     c_int, c_float, c_void_p],
@@ -69,6 +70,7 @@ def lib():
             fn.argtypes = args
             fn.restype = c_int
         l.dh_last_error.restype = ctypes.c_char_p
+        l.dh_attn_fwd_scratch_floats.restype = c_ll
         _lib = l
     return _lib
 
@@ -143,11 +145,19 @@ def rope(qkv, n_q_heads, n_kv_heads, head_dim, theta, pos0=0, inverse=False, tok
                         pos0, int(inverse), _stream(stream)))
 
 
-def attn_fwd(q, k, v, o, lse, n_q_heads, n_kv_heads, head_dim, scale, stream=None):
+def attn_fwd_scratch_floats(tokens, n_q_heads, n_kv_heads, head_dim):
+    return int(lib().dh_attn_fwd_scratch_floats(tokens, n_q_heads, n_kv_heads, head_dim))
+
+
+def attn_fwd(q, k, v, o, lse, n_q_heads, n_kv_heads, head_dim, scale, stream=None, split=True):
+    """split=True allocates the KV-split scratch when the launcher wants it."""
+    import torch
     tokens = q.shape[0]
+    n = attn_fwd_scratch_floats(tokens, n_q_heads, n_kv_heads, head_dim) if split else 0
+    scratch = torch.empty(max(n, 1), dtype=torch.float32, device=q.device) if n else None
     check(lib().dh_attn_fwd(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o),
-                            o.stride(0), _ptr(lse), tokens, n_q_heads, n_kv_heads, head_dim,
-                            scale, _stream(stream)))
+                            o.stride(0), _ptr(lse), _ptr(scratch) if n else None, n, tokens,
+                            n_q_heads, n_kv_heads, head_dim, scale, _stream(stream)))
 
 
 def attn_bwd(q, k, v, o, lse, do, dq, dk, dv, n_q_heads, n_kv_heads, head_dim, scale,

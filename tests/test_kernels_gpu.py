@@ -172,6 +172,34 @@ def test_attention_fwd_bwd(T, nq, nkv, d):
     assert torch.equal(dqkv, dqkv2)
 
 
+@pytest.mark.parametrize("T,nq,nkv", [(4096, 4, 1), (3000, 2, 1), (8192, 1, 1)])
+def test_attention_fwd_kv_split(T, nq, nkv):
+    """Few heads per GPU (high TP): long causal rows are split into KV chunks
+    whose fp32 partials are merged by the combine kernel."""
+    d = 128
+    scale = d ** -0.5
+    assert dh.attn_fwd_scratch_floats(T, nq, nkv, d) > 0
+    assert dh.attn_fwd_scratch_floats(4096, 32, 8, d) == 0  # enough blocks: no split
+    qkv = (torch.randn(T, (nq + 2 * nkv) * d, device="cuda") * 0.5).to(torch.bfloat16)
+    q, k, v = qkv[:, :nq * d], qkv[:, nq * d:(nq + nkv) * d], qkv[:, (nq + nkv) * d:]
+    outs = []
+    for split in (True, False):
+        o = torch.empty(T, nq * d, device="cuda", dtype=torch.bfloat16)
+        lse = torch.empty(nq, T, device="cuda")
+        dh.attn_fwd(q, k, v, o, lse, nq, nkv, d, scale, split=split)
+        outs.append((o, lse))
+    o_ref, lse_ref = _attn_ref(q.float(), k.float(), v.float(), nq, nkv, d, scale)
+    for o, lse in outs:
+        assert _rel(o, o_ref) < 6e-3
+        assert (lse - lse_ref).abs().max().item() < 2e-3
+    assert (outs[0][1] - outs[1][1]).abs().max().item() < 1e-3
+    # split is deterministic run to run
+    o2 = torch.empty_like(outs[0][0])
+    lse2 = torch.empty_like(outs[0][1])
+    dh.attn_fwd(q, k, v, o2, lse2, nq, nkv, d, scale)
+    assert torch.equal(o2, outs[0][0]) and torch.equal(lse2, outs[0][1])
+
+
 def test_attention_forward_rescale_paths():
     """Row maxima that keep growing for some rows only: exercises the lazy O
     rescale with per-row (warp-divergent) decisions in the tcgen05 forward."""
