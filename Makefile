@@ -47,7 +47,8 @@ $(OBJ)/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(CUDA_HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(OBJ)/runtime/%.o: $(PKG)/csrc/runtime/%.cpp $(CUDA_HDR) $(wildcard include/weft/*.hpp)
+$(OBJ)/runtime/%.o: $(PKG)/csrc/runtime/%.cpp $(CUDA_HDR) $(wildcard include/weft/*.hpp) \
+                    $(wildcard $(PKG)/csrc/runtime/*.hpp) $(PKG)/csrc/planner/lane_sim.hpp
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -I/usr/local/cuda/include -I$(PKG)/csrc/planner -c $< -o $@
 

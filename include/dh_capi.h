@@ -48,7 +48,9 @@ int dh_version(void);
  * b_mn = 0: B(n,k) = b[n*ldb + k]  (K-major)     b_mn = 1: B(n,k) = b[k*ldb + n]
  * d_fp32 = 0: D bf16, d_fp32 = 1: D fp32; accumulate = 1 adds into D (fp32 exact
  * sum; bf16: D = bf16(D + bf16(acc)) on the CTA-pair path, bf16(D + acc) otherwise).
- * max_ctas caps the persistent grid (0 = every SM); tile_n 0 = auto, 128, 256. */
+ * max_ctas caps the persistent grid (0 = every SM). tile_n: 0 = auto; 128/192/256 = one
+ * CTA per 128 x tile_n tile; 512 = CTA pair (cta_group::2) per 256 x 256 tile;
+ * -128/-192/-256 = CTA pair per 256 x abs(tile_n) tile (-192 needs a K-major B). */
 typedef struct dh_gemm_args {
     const void* a;
     long long lda;
@@ -63,7 +65,18 @@ typedef struct dh_gemm_args {
     int accumulate;
     int max_ctas;
     int tile_n;
+    /* Fused SwiGLU epilogues (bf16 d, no accumulate; d2 and aux share d's row pitch ld_aux):
+     *   DH_EPI_SWIGLU_FWD     d = up = bf16(acc), d2 = act = silu(aux0 = gate) * up
+     *   DH_EPI_SWIGLU_FWD_UP  d = gate = bf16(acc), d2 = act = silu(gate) * (aux0 = up)
+     *   DH_EPI_SWIGLU_BWD     acc = d_act (rounded to bf16); d = d_gate, d2 = d_up from
+     *                         aux0 = gate, aux1 = up (d_act itself is not stored) */
+    int epilogue;
+    void* d2;
+    const void* aux0;
+    const void* aux1;
+    long long ld_aux;
 } dh_gemm_args;
+enum { DH_EPI_NONE = 0, DH_EPI_SWIGLU_FWD = 1, DH_EPI_SWIGLU_FWD_UP = 2, DH_EPI_SWIGLU_BWD = 3 };
 int dh_gemm(const dh_gemm_args* args, void* stream);
 
 /* RMSNorm over the last dim (elementwise.cu). y = x * rstd * gamma, rstd fp32 [rows]. */

@@ -56,6 +56,17 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
     return u;
 }
 
+// SwiGLU element math shared by the standalone kernels (elementwise.cu) and
+// the fused GEMM epilogues (gemm_tcgen05.cu), so both paths round identically.
+__device__ __forceinline__ float swiglu_sigmoid(float x) { return 1.f / (1.f + __expf(-x)); }
+__device__ __forceinline__ float swiglu_fwd_elem(float g, float u) { return g * swiglu_sigmoid(g) * u; }
+__device__ __forceinline__ void swiglu_bwd_elem(float g, float u, float da, float& dg, float& du) {
+    const float s = swiglu_sigmoid(g);
+    const float silu = g * s;
+    du = da * silu;
+    dg = da * u * s * (1.f + g * (1.f - s));
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);

@@ -32,7 +32,14 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-enum Epi { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiDirect = 2, kEpiAddBf16 = 3 };
+enum Epi {
+    kEpiStoreBf16 = 0,
+    kEpiAddF32 = 1,
+    kEpiDirect = 2,
+    kEpiAddBf16 = 3,
+    kEpiSwiGLUFwd = 4,  // D = bf16(acc), D2 = swiglu(aux0, D) or swiglu(D, aux0) (aux_is_up)
+    kEpiSwiGLUBwd = 5,  // acc = d_act: D = d_gate, D2 = d_up from (aux0 = gate, aux1 = up)
+};
 
 template <int BN>
 struct GemmCfg {
@@ -51,6 +58,10 @@ struct KParams {
     int m, n, k;
     int accumulate;
     int tiles_m, tiles_n;
+    const __nv_bfloat16* aux0;  // fused SwiGLU epilogues: [m, n] bf16 operands, row pitch ld_aux
+    const __nv_bfloat16* aux1;
+    long long ld_aux;
+    int aux_is_up;  // kEpiSwiGLUFwd: acc is the gate projection and aux0 holds up
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI, bool D_F32>
@@ -290,32 +301,45 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// CTA-pair variant (tcgen05 cta_group::2): a 256 x 256 tile per pair of SMs.
-// Each CTA stages its own 128 rows of A and its half (128) of B per 64-wide k
-// block (32 KB/stage instead of 48 KB for 128 x 256 on one SM: 1.5x less
-// L2->SM traffic per FLOP); the even CTA issues M256 N256 MMAs that read both
-// CTAs' smem and write both CTAs' TMEM (128 lanes x 256 columns each). TMA loads
-// of both CTAs complete on the leader's full barrier; MMA commits multicast to
-// both CTAs' empty / accumulator-full barriers; both epilogues release the
-// accumulator on the leader's tempty barrier.
+// CTA-pair variant (tcgen05 cta_group::2): a 256 x PBN tile per pair of SMs
+// (PBN 256, 192 or 128: the narrower pair tiles fill the SMs on the skinny
+// TP-sharded GEMMs). Each CTA stages its own 128 rows of A and its half
+// (PBN/2 rows) of B per 64-wide k block (32 KB/stage for PBN 256 instead of
+// 48 KB for 128 x 256 on one SM: 1.5x less L2->SM traffic per FLOP); the even
+// CTA issues M256 N<PBN> MMAs that read both CTAs' smem and write both CTAs'
+// TMEM (128 lanes x PBN columns each). TMA loads of both CTAs complete on the
+// leader's full barrier; MMA commits multicast to both CTAs' empty /
+// accumulator-full barriers; both epilogues release the accumulator on the
+// leader's tempty barrier.
 
-constexpr int kPairStages = 6;
-constexpr int kPairStage = 2 * BM * BK * 2;  // A rows (128) + B half (128), 32 KB
-constexpr int kPairSmem = kPairStages * kPairStage + 2 * 16384 + 1024 + 256;
+template <int PBN, bool FUSED = false>
+struct PairCfg {
+    static constexpr int kHalfB = PBN / 2;                    // B rows per CTA
+    static constexpr int kStageA = BM * BK * 2;               // 16 KB
+    static constexpr int kStageB = kHalfB * BK * 2;           // 16 / 12 / 8 KB
+    static constexpr int kStage = kStageA + kStageB;
+    static constexpr int kStaging = (FUSED ? 4 : 2) * 16384;  // fused: two outputs per chunk
+    static constexpr int kBudget = 232448 - kStaging - 1024 - 256;  // 227 KB opt-in smem per CTA
+    static constexpr int kStages = kBudget / kStage < 8 ? kBudget / kStage : 8;
+    static constexpr int kSmem = kStages * kStage + kStaging + 1024 + 256;
+};
 
-template <bool A_MN, bool B_MN, int EPI>
+template <int PBN, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                     const __grid_constant__ CUtensorMap tma_d, const KParams p) {
+                     const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_d2,
+                     const KParams p) {
+    constexpr bool kFused = EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd;
+    using C = PairCfg<PBN, kFused>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + kPairStages * BM * BK * 2;
-    uint8_t* staging = smem + kPairStages * kPairStage;
-    uint64_t* full = reinterpret_cast<uint64_t*>(staging + 2 * 16384);
-    uint64_t* empty = full + kPairStages;
-    uint64_t* tfull = empty + kPairStages;
+    uint8_t* sB = smem + C::kStages * C::kStageA;
+    uint8_t* staging = smem + C::kStages * C::kStage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStaging);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -332,7 +356,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
         tma_prefetch(&tma_d);
-        for (int s = 0; s < kPairStages; ++s) {
+        if constexpr (kFused) tma_prefetch(&tma_d2);
+        for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -353,14 +378,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs) {
-                const int m0 = (tile % tiles_m) * 256 + rank * BM;  // this CTA's A rows
-                const int n0 = (tile / tiles_m) * 256 + rank * 128;  // this CTA's B half
+                const int m0 = (tile % tiles_m) * 256 + rank * BM;             // this CTA's A rows
+                const int n0 = (tile / tiles_m) * PBN + rank * C::kHalfB;      // this CTA's B half
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) mbar_expect_tx(&full[stage], 2 * kPairStage);
+                    if (leader) mbar_expect_tx(&full[stage], 2 * C::kStage);
                     const uint32_t bar = leader_addr(&full[stage]);
-                    uint8_t* a_dst = sA + stage * BM * BK * 2;
-                    uint8_t* b_dst = sB + stage * BM * BK * 2;
+                    uint8_t* a_dst = sA + stage * C::kStageA;
+                    uint8_t* b_dst = sB + stage * C::kStageB;
                     const int k0 = kb * BK;
                     if constexpr (A_MN) {
                         tma_load_2d_pair(a_dst, &tma_a, bar, m0, k0);
@@ -369,18 +394,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         tma_load_2d_pair(a_dst, &tma_a, bar, k0, m0);
                     }
                     if constexpr (B_MN) {
-                        tma_load_2d_pair(b_dst, &tma_b, bar, n0, k0);
-                        tma_load_2d_pair(b_dst + BK * 128, &tma_b, bar, n0 + 64, k0);
+#pragma unroll
+                        for (int i = 0; i < C::kHalfB / 64; ++i)
+                            tma_load_2d_pair(b_dst + i * BK * 128, &tma_b, bar, n0 + i * 64, k0);
                     } else {
                         tma_load_2d_pair(b_dst, &tma_b, bar, k0, n0);
                     }
-                    if (++stage == kPairStages) stage = 0, phase ^= 1;
+                    if (++stage == C::kStages) stage = 0, phase ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
         if (leader) {
-            constexpr uint32_t idesc = umma_idesc_bf16(256, 256, A_MN, B_MN);
+            constexpr uint32_t idesc = umma_idesc_bf16(256, PBN, A_MN, B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -388,13 +414,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int tile = pair; tile < num_tiles; tile += npairs) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * 256;
+                const uint32_t d_tmem = tmem_base + acc * PBN;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (elect_one()) {
-                        const uint32_t a_addr = smem_u32(sA + stage * BM * BK * 2);
-                        const uint32_t b_addr = smem_u32(sB + stage * BM * BK * 2);
+                        const uint32_t a_addr = smem_u32(sA + stage * C::kStageA);
+                        const uint32_t b_addr = smem_u32(sB + stage * C::kStageB);
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk) {
                             const uint64_t a_desc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, BK * 128, 1024)
@@ -407,7 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         if (kb == num_kb - 1) tc_commit_pair_mc(&tfull[acc]);
                     }
                     __syncwarp();
-                    if (++stage == kPairStages) stage = 0, phase ^= 1;
+                    if (++stage == C::kStages) stage = 0, phase ^= 1;
                 }
                 if (++acc == 2) acc = 0, acc_phase ^= 1;
             }
@@ -423,20 +449,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int chunk = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs) {
             const int m0 = (tile % tiles_m) * 256 + rank * BM;
-            const int n0 = (tile / tiles_m) * 256;
+            const int n0 = (tile / tiles_m) * PBN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if constexpr (kFused) {
+                // SwiGLU fused into the epilogue: per 64-column chunk, this row's
+                // 128-byte slices of the aux operands come straight from global
+                // (whole lines), two outputs are staged and TMA-stored.
+                const bool row_ok = m0 + r < p.m;
+#pragma unroll 1
+                for (int c = 0; c < PBN / 64; ++c, ++chunk) {
+                    const int col = n0 + c * 64;
+                    uint4 a0[8], a1[8];
+                    const bool ok = row_ok && col < p.n;
+                    const uint4* x0 = reinterpret_cast<const uint4*>(p.aux0 + (m0 + r) * p.ld_aux + col);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a0[u] = ok ? __ldg(x0 + u) : make_uint4(0, 0, 0, 0);
+                    if constexpr (EPI == kEpiSwiGLUBwd) {
+                        const uint4* x1 = reinterpret_cast<const uint4*>(p.aux1 + (m0 + r) * p.ld_aux + col);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) a1[u] = ok ? __ldg(x1 + u) : make_uint4(0, 0, 0, 0);
+                    }
+                    uint8_t* stg0 = staging + (chunk & 1) * 32768;
+                    uint8_t* stg1 = stg0 + 16384;
+                    if (store_leader) bulk_wait_read<1>();
+                    named_barrier(2, 128);
+                    uint32_t v0[32], v1[32];
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64, v0);
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64 + 32, v1);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        float f[8], x[8], o0[8], o1[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            // the GEMM output as the unfused path stores it (bf16)
+                            f[t] = __bfloat162float(__float2bfloat16(
+                                __uint_as_float(u < 4 ? v0[u * 8 + t] : v1[(u - 4) * 8 + t])));
+                        }
+                        unpack8(a0[u], x);
+                        if constexpr (EPI == kEpiSwiGLUFwd) {
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) {
+                                o0[t] = f[t];
+                                o1[t] = p.aux_is_up ? swiglu_fwd_elem(f[t], x[t]) : swiglu_fwd_elem(x[t], f[t]);
+                            }
+                        } else {
+                            float y[8];
+                            unpack8(a1[u], y);
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) swiglu_bwd_elem(x[t], y[t], f[t], o0[t], o1[t]);
+                        }
+                        const int sw = (u ^ (r & 7)) << 4;
+                        *reinterpret_cast<uint4*>(stg0 + r * 128 + sw) = pack8(o0);
+                        *reinterpret_cast<uint4*>(stg1 + r * 128 + sw) = pack8(o1);
+                    }
+                    fence_async_shared();
+                    named_barrier(2, 128);
+                    if (store_leader) {
+                        tma_store_2d(&tma_d, stg0, col, m0);
+                        tma_store_2d(&tma_d2, stg1, col, m0);
+                        bulk_commit();
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive_cluster(tempty_leader[acc]);
+                if (++acc == 2) acc = 0, acc_phase ^= 1;
+                continue;
+            }
             constexpr bool kBf16 = EPI == kEpiStoreBf16 || EPI == kEpiAddBf16;
             constexpr int CW = kBf16 ? 64 : 32;
 #pragma unroll 1
-            for (int c = 0; c < 256 / CW; ++c, ++chunk) {
+            for (int c = 0; c < PBN / CW; ++c, ++chunk) {
                 uint8_t* stg = staging + (chunk & 1) * 16384;
                 if (store_leader) bulk_wait_read<1>();
                 named_barrier(2, 128);
                 if constexpr (kBf16) {
                     uint32_t v0[32], v1[32];
-                    tmem_ld32(tmem_base + lane_off + acc * 256 + c * 64, v0);
-                    tmem_ld32(tmem_base + lane_off + acc * 256 + c * 64 + 32, v1);
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64, v0);
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64 + 32, v1);
                     tmem_ld_wait();
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
@@ -447,7 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 } else {
                     uint32_t v[32];
-                    tmem_ld32(tmem_base + lane_off + acc * 256 + c * 32, v);
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 32, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
@@ -582,17 +673,29 @@ int launch(const dh_gemm_args* g, cudaStream_t stream) {
     return DH_OK;
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <int PBN, bool A_MN, bool B_MN, int EPI>
 int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
-    CUtensorMap ma, mb, md;
+    constexpr bool kFused = EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd;
+    using C = PairCfg<PBN, kFused>;
+    CUtensorMap ma, mb, md, md2;
     int rc = A_MN ? make_map(&ma, g->a, g->m, g->k, g->lda, BK) : make_map(&ma, g->a, g->k, g->m, g->lda, BM);
     if (rc) return rc;
-    rc = B_MN ? make_map(&mb, g->b, g->n, g->k, g->ldb, BK) : make_map(&mb, g->b, g->k, g->n, g->ldb, 128);
+    rc = B_MN ? make_map(&mb, g->b, g->n, g->k, g->ldb, BK) : make_map(&mb, g->b, g->k, g->n, g->ldb, C::kHalfB);
     if (rc) return rc;
     rc = EPI == kEpiAddF32 ? make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 32, BM, true)
                            : make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 64, BM, false);
     if (rc) return rc;
+    if (kFused) {
+        rc = make_tma_2d(&md2, g->d2, g->n, g->m, g->ldd, 64, BM, false);
+        if (rc) return rc;
+    } else {
+        md2 = md;  // unused
+    }
     KParams p;
+    p.aux0 = static_cast<const __nv_bfloat16*>(g->aux0);
+    p.aux1 = static_cast<const __nv_bfloat16*>(g->aux1);
+    p.ld_aux = g->ld_aux;
+    p.aux_is_up = g->epilogue == DH_EPI_SWIGLU_FWD_UP;
     p.d = g->d;
     p.ldd = g->ldd;
     p.m = g->m;
@@ -600,29 +703,39 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
     p.k = g->k;
     p.accumulate = g->accumulate;
     p.tiles_m = (g->m + 255) / 256;
-    p.tiles_n = (g->n + 255) / 256;
+    p.tiles_n = (g->n + PBN - 1) / PBN;
     const int tiles = p.tiles_m * p.tiles_n;
     const int grid = 2 * std::min(ctas / 2, tiles);
-    auto kern = gemm_pair_kernel<A_MN, B_MN, EPI>;
+    auto kern = gemm_pair_kernel<PBN, A_MN, B_MN, EPI>;
     static bool configured = false;
     if (!configured) {
-        DH_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+        DH_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         configured = true;
     }
-    kern<<<grid, kThreads, kPairSmem, stream>>>(ma, mb, md, p);
+    kern<<<grid, kThreads, C::kSmem, stream>>>(ma, mb, md, md2, p);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }
 
-template <int EPI>
+template <int PBN, int EPI>
 int dispatch_pair(const dh_gemm_args* g, cudaStream_t s, int ctas) {
     const int key = (g->a_mn ? 2 : 0) | (g->b_mn ? 1 : 0);
     switch (key) {
-        case 0: return launch_pair<false, false, EPI>(g, s, ctas);
-        case 1: return launch_pair<false, true, EPI>(g, s, ctas);
-        case 2: return launch_pair<true, false, EPI>(g, s, ctas);
-        default: return launch_pair<true, true, EPI>(g, s, ctas);
+        case 0: return launch_pair<PBN, false, false, EPI>(g, s, ctas);
+        case 1: return launch_pair<PBN, false, true, EPI>(g, s, ctas);
+        case 2: return launch_pair<PBN, true, false, EPI>(g, s, ctas);
+        default: return launch_pair<PBN, true, true, EPI>(g, s, ctas);
     }
+}
+
+template <int PBN>
+int dispatch_pair_epi(const dh_gemm_args* g, cudaStream_t s, int ctas) {
+    if (g->epilogue == DH_EPI_SWIGLU_BWD) return dispatch_pair<PBN, kEpiSwiGLUBwd>(g, s, ctas);
+    if (g->epilogue) return dispatch_pair<PBN, kEpiSwiGLUFwd>(g, s, ctas);
+    if (g->d_fp32) return dispatch_pair<PBN, kEpiAddF32>(g, s, ctas);
+    // bf16 accumulate = TMA reduce-add: D = bf16(D + bf16(acc))
+    return g->accumulate ? dispatch_pair<PBN, kEpiAddBf16>(g, s, ctas)
+                         : dispatch_pair<PBN, kEpiStoreBf16>(g, s, ctas);
 }
 
 template <int BN, int EPI, bool D_F32>
@@ -648,63 +761,109 @@ int dispatch_epi(const dh_gemm_args* g, cudaStream_t s) {
 
 }  // namespace
 
-constexpr double kPairAdvantage = 1.08;  // measured per-tile gain of 256x256 pairs (see profiles/)
+// Tile choice: per candidate tile, the fraction of issued tile area that is
+// useful given the persistent grid's wave quantisation, times the tile's
+// measured per-SM efficiency relative to the 256 x 256 CTA pair (B200, see
+// profiles/: narrower tiles re-read more operand bytes per FLOP, one-CTA tiles
+// stage both operands on one SM). Ties go to the earlier (wider) candidate.
+struct TileCand {
+    int pbn;      // > 0: CTA pair 256 x pbn; < 0: one CTA 128 x -pbn
+    double eff;   // per-SM efficiency of the tile shape
+};
+constexpr TileCand kTiles[] = {{256, 1.0}, {192, 0.95}, {128, 0.85},
+                               {-256, 0.92}, {-192, 0.80}, {-128, 0.70}};
 
-// Tile-N choice: the fraction of issued tile area that is useful, given the
-// persistent grid's wave quantisation; ties go to the wider tile (fewer B
-// re-reads). BN 192 keeps MN-major B operands on whole 64-wide swizzle atoms.
-int gemm_pick_bn(int m, int n, int ctas) {
-    // per-tile efficiency of the narrower tiles relative to 256 (measured on
-    // B200: more L2 traffic per FLOP and fewer stages), times wave efficiency
-    const int cand[3] = {256, 192, 128};
-    const double tile_eff[3] = {1.0, 0.85, 0.75};
-    int best = 256;
+double tile_score(const TileCand& t, long long m, long long n, int ctas) {
+    const bool pair = t.pbn > 0;
+    const long long bm = pair ? 256 : 128, bn = pair ? t.pbn : -t.pbn;
+    const long long units = pair ? ctas / 2 : ctas;
+    if (units < 1) return -1.0;
+    const long long tiles = ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
+    const long long waves = (tiles + units - 1) / units;
+    return static_cast<double>(m) * n / (static_cast<double>(waves) * units * bm * bn) * t.eff;
+}
+
+int gemm_pick_tile(int m, int n, int ctas, bool pair_ok, bool b_mn, bool pair_only = false) {
+    int best = pair_only ? 256 : -256;
     double best_score = -1.0;
-    const long long tm = (m + BM - 1) / BM;
-    for (int i = 0; i < 3; ++i) {
-        const int bn = cand[i];
-        const long long tiles = tm * ((n + bn - 1) / bn);
-        const long long waves = (tiles + ctas - 1) / ctas;
-        const double wave_eff = static_cast<double>(m) * n / (static_cast<double>(waves) * ctas * BM * bn);
-        const double score = wave_eff * tile_eff[i];
-        if (score > best_score + 1e-3) best_score = score, best = bn;
+    for (const TileCand& t : kTiles) {
+        if (t.pbn > 0 && !pair_ok) continue;
+        if (t.pbn < 0 && pair_only) continue;
+        if (t.pbn == 192 && b_mn) continue;  // 96-row MN-major B halves are not whole swizzle atoms
+        const double sc = tile_score(t, m, n, ctas);
+        if (sc > best_score + 1e-3) best_score = sc, best = t.pbn;
     }
     return best;
 }
 
-// CTA-pair 256 x 256 tiles when their wave efficiency (with the measured per-
-// tile advantage) beats the best single-CTA tile.
-bool gemm_pick_pair(int m, int n, int ctas) {
-    const int pairs = ctas / 2;
-    if (pairs < 1) return false;
-    const long long tiles = static_cast<long long>((m + 255) / 256) * ((n + 255) / 256);
-    const long long waves = (tiles + pairs - 1) / pairs;
-    const double pair_eff = static_cast<double>(m) * n / (static_cast<double>(waves) * pairs * 65536.0);
-    const int bn = gemm_pick_bn(m, n, ctas);
-    const long long t1 = static_cast<long long>((m + BM - 1) / BM) * ((n + bn - 1) / bn);
-    const long long w1 = (t1 + ctas - 1) / ctas;
-    const double one_eff = static_cast<double>(m) * n / (static_cast<double>(w1) * ctas * BM * bn) *
-                           (bn == 256 ? 1.0 : bn == 192 ? 0.85 : 0.75);
-    return pair_eff * kPairAdvantage > one_eff;
+#define GEMM_TRY(expr)                   \
+    do {                                  \
+        const int rc_ = (expr);           \
+        if (rc_ != DH_OK) return rc_;     \
+    } while (0)
+
+int gemm(const dh_gemm_args* g, cudaStream_t s);
+
+// SwiGLU epilogues: fused into the CTA-pair kernel when the operands allow it,
+// else the plain GEMM followed by the standalone SwiGLU kernel (same math).
+int gemm_swiglu(const dh_gemm_args* g, cudaStream_t s) {
+    if (g->accumulate || g->d_fp32 || !g->d2 || !g->aux0 || (g->epilogue == DH_EPI_SWIGLU_BWD && !g->aux1))
+        return set_error(DH_ERR_INVALID, "gemm: SwiGLU epilogue needs bf16 d, d2 and aux operands");
+    const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
+    auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    const bool fusable = ctas >= 2 && g->n % 64 == 0 && g->ldd % 8 == 0 && g->ld_aux % 8 == 0 && al16(g->d) &&
+                         al16(g->d2) && al16(g->aux0) && (!g->aux1 || al16(g->aux1)) && g->ldd == g->ld_aux;
+    if (!fusable) {
+        dh_gemm_args plain = *g;
+        plain.epilogue = DH_EPI_NONE;
+        if (g->ldd != g->n || g->ld_aux != g->n)
+            return set_error(DH_ERR_INVALID, "gemm: unfused SwiGLU fallback needs dense [m, n] operands");
+        const long long count = static_cast<long long>(g->m) * g->n;
+        if (g->epilogue == DH_EPI_SWIGLU_BWD) {
+            plain.d = g->d2;  // d_act lands in d_up, then swiglu_bwd runs in place on it
+            GEMM_TRY(gemm(&plain, s));
+            return dh_swiglu_bwd(g->aux0, g->aux1, g->d2, g->d, g->d2, count, s);
+        }
+        GEMM_TRY(gemm(&plain, s));
+        return g->epilogue == DH_EPI_SWIGLU_FWD_UP ? dh_swiglu_fwd(g->d, g->aux0, g->d2, count, s)
+                                                   : dh_swiglu_fwd(g->aux0, g->d, g->d2, count, s);
+    }
+    int pick = g->tile_n < 0 ? -g->tile_n : g->tile_n == 512 ? 256 : 0;
+    if (!pick) pick = gemm_pick_tile(g->m, g->n, ctas, true, g->b_mn, true);
+    if (pick == 192 && !g->b_mn) return dispatch_pair_epi<192>(g, s, ctas);
+    if (pick == 128) return dispatch_pair_epi<128>(g, s, ctas);
+    return dispatch_pair_epi<256>(g, s, ctas);
 }
 
 int gemm(const dh_gemm_args* g, cudaStream_t s) {
     if (g->m <= 0 || g->n <= 0 || g->k <= 0) return set_error(DH_ERR_INVALID, "gemm: empty shape");
+    if (g->epilogue) return gemm_swiglu(g, s);
     const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
     const bool aligned = (reinterpret_cast<uintptr_t>(g->d) & 15) == 0 &&
                          (g->ldd * (g->d_fp32 ? 4 : 2)) % 16 == 0;
-    const bool pair_ok = aligned && (g->accumulate || !g->d_fp32);
-    const bool want_pair = g->tile_n == 512 || (g->tile_n == 0 && gemm_pick_pair(g->m, g->n, ctas));
-    if (pair_ok && want_pair) {
-        if (g->d_fp32) return dispatch_pair<kEpiAddF32>(g, s, ctas);
-        // bf16 accumulate = TMA reduce-add: D = bf16(D + bf16(acc))
-        return g->accumulate ? dispatch_pair<kEpiAddBf16>(g, s, ctas) : dispatch_pair<kEpiStoreBf16>(g, s, ctas);
+    const bool pair_ok = aligned && (g->accumulate || !g->d_fp32) && ctas >= 2;
+    // tile_n: 0 auto; 128/192/256 one CTA 128 x tile_n; 512 = CTA pair 256 x 256;
+    // -128/-192/-256 = CTA pair 256 x |tile_n|
+    int pick;
+    if (g->tile_n == 0) pick = gemm_pick_tile(g->m, g->n, ctas, pair_ok, g->b_mn);
+    else if (g->tile_n == 512) pick = 256;
+    else if (g->tile_n < 0) pick = -g->tile_n;
+    else pick = -g->tile_n;
+    if (pick > 0 && !pair_ok) pick = -256;  // CTA pairs need an aligned bf16 or accumulated output
+    if (pick > 0) {
+        if (pick == 256) return dispatch_pair_epi<256>(g, s, ctas);
+        if (pick == 192) {
+            if (g->b_mn) return set_error(DH_ERR_INVALID, "gemm: pair tile 192 needs a K-major B");
+            return dispatch_pair_epi<192>(g, s, ctas);
+        }
+        if (pick == 128) return dispatch_pair_epi<128>(g, s, ctas);
+        return set_error(DH_ERR_INVALID, "gemm: pair tile_n must be 128, 192 or 256");
     }
-    const int bn = g->tile_n && g->tile_n != 512 ? g->tile_n : gemm_pick_bn(g->m, g->n, ctas);
+    const int bn = -pick;
     if (bn == 256) return dispatch_epi<256>(g, s);
     if (bn == 192) return dispatch_epi<192>(g, s);
     if (bn == 128) return dispatch_epi<128>(g, s);
-    return set_error(DH_ERR_INVALID, "gemm: tile_n must be 0, 128, 192 or 256");
+    return set_error(DH_ERR_INVALID, "gemm: tile_n must be 0, 128, 192, 256, 512 or -128/-192/-256");
 }
 
 }  // namespace dh

@@ -13,10 +13,10 @@ namespace dh {
 int kernels_per_node(const Model& m, int node, int layer) {
     const bool group = m.cfg.nq_l != m.cfg.nkv_l;
     switch (node) {
-        case 0: case 8: case 5: case 7: case 10: case 11: case 23: case 24: case 25: case 31:
-        case 32: case 35: case 36:
-            return 1;
-        case 2: case 12: case 22: case 26: case 28: case 38:
+        case 0: case 8: case 5: case 7: case 10: case 11: case 12: case 22: case 23: case 24: case 25:
+        case 31: case 32: case 35: case 36:
+            return 1;  // (SwiGLU fwd / bwd run inside the mlp_gate|mlp_up / mlp_down_dgrad epilogues)
+        case 2: case 26: case 28: case 38:
             return 2;
         case 4:  // attn (+ KV-split combine when the launcher splits rows)
             return m.cfg.head_dim == 128 &&

@@ -46,7 +46,7 @@ struct Lowering {
     std::vector<int> strand_last;
     std::vector<std::vector<int>> slot_of;  // [strand][layer]
     std::vector<int> free_slots;
-    std::map<int, int> lane_of, pos_in_bwd;
+    std::map<int, int> lane_of, pos_in_bwd, pos_in_fwd;
 
     explicit Lowering(Model& mm) : m(mm) {
         const int mb = m.cfg.micro_batches, L = m.cfg.layers;
@@ -56,6 +56,7 @@ struct Lowering {
         for (const auto& n : m.fwd_dag.nodes) lane_of[n.id] = static_cast<int>(n.lane);
         for (const auto& n : m.bwd_dag.nodes) lane_of[n.id] = static_cast<int>(n.lane);
         for (std::size_t i = 0; i < m.plan.bwd_seq.size(); ++i) pos_in_bwd[m.plan.bwd_seq[i]] = static_cast<int>(i);
+        for (std::size_t i = 0; i < m.plan.fwd_seq.size(); ++i) pos_in_fwd[m.plan.fwd_seq[i]] = static_cast<int>(i);
     }
 
     void barrier() {
@@ -73,6 +74,13 @@ struct Lowering {
         o.lane = lane_of.at(node);
         o.slot = slot_of[strand][layer];
         o.prev_slot = layer > 0 ? slot_of[strand][layer - 1] : -1;
+        if (node == 10 || node == 11) {
+            // both run on the compute lane in sequence order: the later one sees the
+            // other's output and applies SwiGLU in its GEMM epilogue
+            const int other = node == 10 ? 11 : 10;
+            o.fuse_swiglu = pos_in_fwd.at(node) > pos_in_fwd.at(other) &&
+                            lane_of.at(node) == lane_of.at(other);
+        }
         if (node == 24 || node == 25) {
             const int other = node == 24 ? 25 : 24;
             o.first_dx = pos_in_bwd.at(node) < pos_in_bwd.at(other);

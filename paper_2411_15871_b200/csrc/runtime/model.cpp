@@ -186,7 +186,6 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     b.grad[1] = pool.take(T * H * 2, "act.bwd_transient");
     b.d_x1 = pool.take(T * H * 2, "act.bwd_transient");
     b.dy_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
-    b.d_act = pool.take(S * F * 2, "act.bwd_transient");
     b.d_gate = pool.take(S * F * 2, "act.bwd_transient");
     b.d_up = pool.take(S * F * 2, "act.bwd_transient");
     b.dx_part = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
@@ -258,8 +257,14 @@ namespace {
 
 int gemm(const void* a, long long lda, bool a_mn, const void* b, long long ldb, bool b_mn, void* d,
          long long ldd, bool d_f32, int mm, int nn, int kk, bool acc, int max_ctas,
-         cudaStream_t s) {
+         cudaStream_t s, int epilogue = DH_EPI_NONE, void* d2 = nullptr, const void* aux0 = nullptr,
+         const void* aux1 = nullptr) {
     dh_gemm_args g{};
+    g.epilogue = epilogue;
+    g.d2 = d2;
+    g.aux0 = aux0;
+    g.aux1 = aux1;
+    g.ld_aux = ldd;
     g.a = a;
     g.lda = lda;
     g.a_mn = a_mn;
@@ -336,14 +341,15 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 9:  // ag1
             RT_TRY(need_comm());
             return comm->all_gather(P(m.fs.ln_loc), P(sl.ln1_full), TH, s);
-        case 10:  // mlp_gate
+        case 10:  // mlp_gate (+ act = silu(gate) * up in the epilogue when it runs after mlp_up)
             return gemm(P(sl.ln1_full), H, false, W + p.wg, H, false, P(sl.gate), F, false, S, F, H,
-                        false, cap, s);
-        case 11:  // mlp_up
+                        false, cap, s, op.fuse_swiglu ? DH_EPI_SWIGLU_FWD_UP : DH_EPI_NONE, P(sl.act),
+                        P(sl.up));
+        case 11:  // mlp_up (+ act in the epilogue when it runs after mlp_gate)
             return gemm(P(sl.ln1_full), H, false, W + p.wu, H, false, P(sl.up), F, false, S, F, H,
-                        false, cap, s);
-        case 12:  // mlp_down: SwiGLU prologue + row-parallel GEMM
-            RT_TRY(dh_swiglu_fwd(P(sl.gate), P(sl.up), P(sl.act), static_cast<long long>(S) * F, s));
+                        false, cap, s, op.fuse_swiglu ? DH_EPI_SWIGLU_FWD : DH_EPI_NONE, P(sl.act),
+                        P(sl.gate));
+        case 12:  // mlp_down (row-parallel; act was produced by the mlp_gate/mlp_up epilogue)
             return gemm(P(sl.act), F, false, W + p.wd, F, false, tp1 ? P(m.fs.rs_out) : P(m.fs.part),
                         H, false, S, H, F, false, cap, s);
         case 13:  // rs1
@@ -364,11 +370,10 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 21:  // rs1_bwd_ag
             RT_TRY(need_comm());
             return comm->all_gather(dy, P(m.bs.dy_full), TH, s);
-        case 22: {  // mlp_down_dgrad (+ SwiGLU bwd)
+        case 22: {  // mlp_down_dgrad with the SwiGLU backward in its epilogue (d_act never stored)
             const void* dyf = tp1 ? dy : P(m.bs.dy_full);
-            RT_TRY(gemm(dyf, H, false, W + p.wd, F, true, P(m.bs.d_act), F, false, S, F, H, false, cap, s));
-            return dh_swiglu_bwd(P(sl.gate), P(sl.up), P(m.bs.d_act), P(m.bs.d_gate), P(m.bs.d_up),
-                                 static_cast<long long>(S) * F, s);
+            return gemm(dyf, H, false, W + p.wd, F, true, P(m.bs.d_gate), F, false, S, F, H, false, cap, s,
+                        DH_EPI_SWIGLU_BWD, P(m.bs.d_up), P(sl.gate), P(sl.up));
         }
         case 23: {  // mlp_down_wgrad: dWd[H,F] += dY^T act
             const void* dyf = tp1 ? dy : P(m.bs.dy_full);

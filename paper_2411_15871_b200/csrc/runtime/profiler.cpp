@@ -46,6 +46,7 @@ Op node_op(const Model& m, const weft::OpNode& n, bool fwd) {
     o.slot = fwd ? 0 : 1;
     o.prev_slot = -1;
     o.first_dx = true;
+    o.fuse_swiglu = n.id == 11;  // the SwiGLU epilogue is charged to mlp_up (it follows mlp_gate by id)
     return o;
 }
 

@@ -98,7 +98,7 @@ struct FwdScratch {
 };
 
 struct BwdScratch {
-    Buf grad[2], d_x1, dy_full, d_act, d_gate, d_up, dx_part, dx1_full, d_o, dqkv, attn_scratch,
+    Buf grad[2], d_x1, dy_full, d_gate, d_up, dx_part, dx1_full, d_o, dqkv, attn_scratch,
         ln_partial, rs_out;
 };
 
@@ -118,6 +118,7 @@ struct Op {
     int slot = 0;     // activation slot of (strand, layer)
     int prev_slot = -1;  // slot holding this layer's input (layer - 1), -1 = strand input
     bool first_dx = true;  // mlp_gate_dgrad/mlp_up_dgrad: whether this one overwrites dx_part
+    bool fuse_swiglu = false;  // mlp_gate/mlp_up: the later of the two computes act in its epilogue
     std::vector<int> waits;  // indices of ops whose completion this op waits for
     bool barrier = false;    // step barrier before this op (all lanes joined)
 };

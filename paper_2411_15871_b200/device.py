@@ -28,7 +28,12 @@ class GemmArgs(ctypes.Structure):
                 ("b", c_void_p), ("ldb", c_ll), ("b_mn", c_int),
                 ("d", c_void_p), ("ldd", c_ll), ("d_fp32", c_int),
                 ("m", c_int), ("n", c_int), ("k", c_int),
-                ("accumulate", c_int), ("max_ctas", c_int), ("tile_n", c_int)]
+                ("accumulate", c_int), ("max_ctas", c_int), ("tile_n", c_int),
+                ("epilogue", c_int), ("d2", c_void_p), ("aux0", c_void_p), ("aux1", c_void_p),
+                ("ld_aux", c_ll)]
+
+
+EPI_NONE, EPI_SWIGLU_FWD, EPI_SWIGLU_FWD_UP, EPI_SWIGLU_BWD = 0, 1, 2, 3
 
 
 _SIGS = {
@@ -93,9 +98,10 @@ def _stream(stream):
 # --------------------------------------------------------------------------- kernels
 
 def gemm(a, b, d, *, a_mn=False, b_mn=False, accumulate=False, m=None, n=None, k=None,
-         max_ctas=0, tile_n=0, stream=None):
+         max_ctas=0, tile_n=0, stream=None, epilogue=EPI_NONE, d2=None, aux0=None, aux1=None):
     """d(m,n) (+)= sum_k A(m,k) B(n,k). A = a[m,k] (K-major) or a[k,m] (a_mn);
-    B = b[n,k] (K-major) or b[k,n] (b_mn). d bf16 or fp32 [m,n]."""
+    B = b[n,k] (K-major) or b[k,n] (b_mn). d bf16 or fp32 [m,n].
+    epilogue = EPI_SWIGLU_*: fused SwiGLU (see dh_capi.h) writing d and d2 from aux0/aux1."""
     import torch
     if m is None:
         m = a.shape[1] if a_mn else a.shape[0]
@@ -105,7 +111,8 @@ def gemm(a, b, d, *, a_mn=False, b_mn=False, accumulate=False, m=None, n=None, k
         n = b.shape[1] if b_mn else b.shape[0]
     args = GemmArgs(a.data_ptr(), a.stride(0), int(a_mn), b.data_ptr(), b.stride(0), int(b_mn),
                     d.data_ptr(), d.stride(0), int(d.dtype == torch.float32), m, n, k,
-                    int(accumulate), max_ctas, tile_n)
+                    int(accumulate), max_ctas, tile_n, epilogue, _ptr(d2), _ptr(aux0), _ptr(aux1),
+                    d.stride(0))
     check(lib().dh_gemm(ctypes.byref(args), _stream(stream)))
     return d
 
@@ -171,3 +178,11 @@ def attn_bwd(q, k, v, o, lse, do, dq, dk, dv, n_q_heads, n_kv_heads, head_dim, s
                             o.stride(0), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv),
                             dq.stride(0), dk.stride(0), _ptr(scratch), tokens, n_q_heads,
                             n_kv_heads, head_dim, scale, _stream(stream)))
+
+
+def adamw(master, weight, grad, m, v, lr, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0, step=1,
+          grad_scale=1.0, zero_grad=True, stream=None):
+    """AdamW on fp32 master weights (in place); refreshes the bf16 `weight`."""
+    check(lib().dh_adamw(_ptr(master), _ptr(weight), _ptr(grad), _ptr(m), _ptr(v), master.numel(), lr,
+                         beta1, beta2, eps, weight_decay, step, grad_scale, int(zero_grad),
+                         _stream(stream)))

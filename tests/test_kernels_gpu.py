@@ -221,26 +221,90 @@ def test_attention_forward_rescale_paths():
     assert (lse - lse_ref).abs().max().item() < 5e-2
 
 
+@pytest.mark.parametrize("tile_n", [512, -192, -128])
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", [(256, 256, 64), (4096, 768, 4096), (333, 200, 136), (1024, 4096, 512)])
-def test_gemm_cta_pair(shape, a_mn, b_mn):
-    """tcgen05 cta_group::2 path (tile_n=512 forces the 256x256 CTA-pair kernel)."""
+def test_gemm_cta_pair(shape, a_mn, b_mn, tile_n):
+    """tcgen05 cta_group::2 path: tile_n=512 forces the 256x256 CTA-pair
+    kernel, -192 / -128 the 256x192 / 256x128 pair tiles."""
     m, n, k = shape
     if (a_mn and m % 8) or (b_mn and n % 8):
         pytest.skip("TMA needs 16-byte row pitch")
+    if tile_n == -192 and b_mn:
+        pytest.skip("pair tile 192 needs a K-major B")
     A = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
     B = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
     a = A.t().contiguous() if a_mn else A
     b = B.t().contiguous() if b_mn else B
     d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
-    dh.gemm(a, b, d, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, tile_n=512)
+    dh.gemm(a, b, d, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, tile_n=tile_n)
     ref = A.float() @ B.float().t()
     assert _rel(d, ref) < 4e-3
     g = torch.randn(m, n, device="cuda", dtype=torch.float32)
     g0 = g.clone()
-    dh.gemm(a, b, g, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, accumulate=True, tile_n=512)
+    dh.gemm(a, b, g, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, accumulate=True, tile_n=tile_n)
     assert (g - (g0 + ref)).abs().max().item() < 1e-3 * (g0 + ref).abs().max().item()
     # capped grid (odd cap rounds down to whole pairs)
-    dh.gemm(a, b, d, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, tile_n=512, max_ctas=7)
+    dh.gemm(a, b, d, a_mn=a_mn, b_mn=b_mn, m=m, n=n, k=k, tile_n=tile_n, max_ctas=7)
     assert _rel(d, ref) < 4e-3
+
+
+@pytest.mark.parametrize("n,offset", [(1 << 20, 0), (1000003, 0), (4099, 1)])
+def test_adamw(n, offset):
+    """Vectorised AdamW (4 params/thread) plus the scalar tail / unaligned path
+    against a torch fp32 restatement of the same update."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    base = [torch.randn(n + offset, device="cuda", generator=g) for _ in range(4)]
+    master, grad, m, v = (t[offset:] for t in base)
+    v.abs_()
+    w = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    lr, b1, b2, eps, wd, step, gs = 3e-4, 0.9, 0.95, 1e-8, 0.1, 7, 0.5
+    gg = grad * gs
+    m_ref = b1 * m + (1 - b1) * gg
+    v_ref = b2 * v + (1 - b2) * gg * gg
+    bc1, bc2 = 1 - b1 ** step, 1 - b2 ** step
+    p_ref = master - lr * wd * master
+    p_ref = p_ref - lr * (m_ref / bc1) / (torch.sqrt(v_ref / bc2) + eps)
+    dh.adamw(master, w, grad, m, v, lr, b1, b2, eps, wd, step, gs, zero_grad=True)
+    torch.cuda.synchronize()
+    assert torch.allclose(m, m_ref, rtol=1e-6, atol=1e-7)
+    assert torch.allclose(v, v_ref, rtol=1e-6, atol=1e-7)
+    assert torch.allclose(master, p_ref, rtol=1e-6, atol=1e-6)
+    assert torch.equal(w, master.to(torch.bfloat16))
+    assert not grad.any()
+
+
+@pytest.mark.parametrize("tile_n", [0, 512, -128])
+@pytest.mark.parametrize("m,n,k", [(4096, 1792, 512), (512, 640, 256), (300, 256, 128)])
+def test_gemm_swiglu_epilogues(m, n, k, tile_n):
+    """Fused SwiGLU epilogues == the unfused GEMM + standalone SwiGLU kernel, bit
+    for bit (same tile, same element math), and close to an fp32 reference."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = (torch.randn(m, k, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    other = torch.randn(m, n, device="cuda", generator=g).to(torch.bfloat16)
+    # forward, acc = up (aux0 = gate) and acc = gate (aux0 = up)
+    for epi, gate_is_acc in ((dh.EPI_SWIGLU_FWD, False), (dh.EPI_SWIGLU_FWD_UP, True)):
+        d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        act = torch.empty_like(d)
+        dh.gemm(x, w, d, tile_n=tile_n, epilogue=epi, d2=act, aux0=other)
+        ref_d = torch.empty_like(d)
+        dh.gemm(x, w, ref_d, tile_n=tile_n if tile_n else 512)
+        ref_act = torch.empty_like(d)
+        gate, up = (ref_d, other) if gate_is_acc else (other, ref_d)
+        dh.swiglu_fwd(gate, up, ref_act)
+        assert torch.equal(d, ref_d)
+        assert torch.equal(act, ref_act)
+        gf, uf = gate.float(), up.float()
+        assert _rel(act, torch.nn.functional.silu(gf) * uf) < 1e-2
+    # backward: acc = d_act; d = d_gate, d2 = d_up
+    gate = torch.randn(m, n, device="cuda", generator=g).to(torch.bfloat16)
+    dgate, dup = torch.empty_like(gate), torch.empty_like(gate)
+    dh.gemm(x, w, dgate, tile_n=tile_n, epilogue=dh.EPI_SWIGLU_BWD, d2=dup, aux0=gate, aux1=other)
+    dact = torch.empty_like(gate)
+    dh.gemm(x, w, dact, tile_n=tile_n if tile_n else 512)
+    rg, ru = torch.empty_like(gate), torch.empty_like(gate)
+    dh.swiglu_bwd(gate, other, dact, rg, ru)
+    assert torch.equal(dgate, rg)
+    assert torch.equal(dup, ru)

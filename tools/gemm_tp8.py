@@ -38,7 +38,7 @@ shapes = [("qkv", S, Q, H, 0, 0, 0), ("attn_proj", S, H, A, 0, 0, 0), ("mlp_gate
           ("fc1_wgrad", F, H, S, 1, 1, 1), ("attn_proj_wgrad", H, A, S, 1, 1, 1),
           ("qkv_wgrad", Q, H, S, 1, 1, 1)]
 caps = [int(c) for c in os.environ.get("CAPS", "132").split(",")]
-tiles = [int(t) for t in os.environ.get("TILES", "0,128,192,256,512").split(",")]
+tiles = [int(t) for t in os.environ.get("TILES", "0,128,192,256,512,-192,-128").split(",")]
 out = []
 for name, m, n, k, amn, bmn, f32 in shapes:
     a = torch.randn((k, m) if amn else (m, k), device="cuda", dtype=torch.bfloat16)
