@@ -58,7 +58,9 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
 
 // SwiGLU element math shared by the standalone kernels (elementwise.cu) and
 // the fused GEMM epilogues (gemm_tcgen05.cu), so both paths round identically.
-__device__ __forceinline__ float swiglu_sigmoid(float x) { return 1.f / (1.f + __expf(-x)); }
+// ex2.approx + rcp.approx: the IEEE division made the fused GEMM epilogue the
+// bottleneck of the mlp GEMMs (the result is still fp32-accurate to ~2 ulp).
+__device__ __forceinline__ float swiglu_sigmoid(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
 __device__ __forceinline__ float swiglu_fwd_elem(float g, float u) { return g * swiglu_sigmoid(g) * u; }
 __device__ __forceinline__ void swiglu_bwd_elem(float g, float u, float da, float& dg, float& du) {
     const float s = swiglu_sigmoid(g);

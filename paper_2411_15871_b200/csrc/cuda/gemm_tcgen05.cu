@@ -324,10 +324,17 @@ struct PairCfg {
     static constexpr int kSmem = kStages * kStage + kStaging + 1024 + 256;
 };
 
+// Fused SwiGLU epilogues run 8 epilogue warps (two per TMEM lane quadrant, each
+// on half of a 64-column chunk): their element math would otherwise be slower
+// than the main loop it has to hide behind.
+template <int EPI>
+constexpr int pair_threads() { return EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd ? 320 : kThreads; }
+
 template <int PBN, bool A_MN, bool B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(), 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_d2,
+                     const __grid_constant__ CUtensorMap tma_x0, const __grid_constant__ CUtensorMap tma_x1,
                      const KParams p) {
     constexpr bool kFused = EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd;
     using C = PairCfg<PBN, kFused>;
@@ -341,7 +348,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + C::kStages;
     uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* xfull = tempty + 2;  // [2] fused epilogues: aux tiles of a staging set landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 2);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -363,7 +371,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 2 * 128);
+            mbar_init(&tempty[b], 2 * (pair_threads<EPI>() - 64));  // every epilogue thread of both CTAs
+            mbar_init(&xfull[b], 1);
+        }
+        if constexpr (kFused) {
+            tma_prefetch(&tma_x0);
+            if constexpr (EPI == kEpiSwiGLUBwd) tma_prefetch(&tma_x1);
         }
         fence_barrier_init();
     }
@@ -453,41 +466,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if constexpr (kFused) {
-                // SwiGLU fused into the epilogue: per 64-column chunk, this row's
-                // 128-byte slices of the aux operands come straight from global
-                // (whole lines), two outputs are staged and TMA-stored.
-                const bool row_ok = m0 + r < p.m;
+                // SwiGLU fused into the epilogue. Per 64-column chunk, one staging
+                // set (2 x 16 KB) first receives the aux tiles by TMA (issued one
+                // chunk ahead), each thread turns its row's aux + accumulator values
+                // into the two outputs in place, and the set is TMA-stored.
+                constexpr int kChunks = PBN / 64;
+                constexpr uint32_t kAuxBytes = (EPI == kEpiSwiGLUBwd ? 2 : 1) * 16384;
+                auto load_aux = [&](int ch, int t_m0, int col) {  // leader thread only
+                    uint8_t* set = staging + (ch & 1) * 32768;
+                    mbar_expect_tx(&xfull[ch & 1], kAuxBytes);
+                    tma_load_2d(set, &tma_x0, &xfull[ch & 1], col, t_m0);
+                    if constexpr (EPI == kEpiSwiGLUBwd) tma_load_2d(set + 16384, &tma_x1, &xfull[ch & 1], col, t_m0);
+                };
+                const int half = (warp - 2) >> 2;  // which 32 columns of each chunk
+                if (store_leader && chunk == 0) load_aux(0, m0, n0);
 #pragma unroll 1
-                for (int c = 0; c < PBN / 64; ++c, ++chunk) {
+                for (int c = 0; c < kChunks; ++c, ++chunk) {
                     const int col = n0 + c * 64;
-                    uint4 a0[8], a1[8];
-                    const bool ok = row_ok && col < p.n;
-                    const uint4* x0 = reinterpret_cast<const uint4*>(p.aux0 + (m0 + r) * p.ld_aux + col);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) a0[u] = ok ? __ldg(x0 + u) : make_uint4(0, 0, 0, 0);
-                    if constexpr (EPI == kEpiSwiGLUBwd) {
-                        const uint4* x1 = reinterpret_cast<const uint4*>(p.aux1 + (m0 + r) * p.ld_aux + col);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) a1[u] = ok ? __ldg(x1 + u) : make_uint4(0, 0, 0, 0);
-                    }
                     uint8_t* stg0 = staging + (chunk & 1) * 32768;
                     uint8_t* stg1 = stg0 + 16384;
-                    if (store_leader) bulk_wait_read<1>();
-                    named_barrier(2, 128);
-                    uint32_t v0[32], v1[32];
-                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64, v0);
-                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64 + 32, v1);
+                    uint32_t v0[32];
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64 + half * 32, v0);
+                    mbar_wait(&xfull[chunk & 1], (chunk >> 1) & 1);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
+                    for (int uu = 0; uu < 4; ++uu) {
+                        const int u = half * 4 + uu;
+                        const int sw = r * 128 + ((u ^ (r & 7)) << 4);
                         float f[8], x[8], o0[8], o1[8];
 #pragma unroll
                         for (int t = 0; t < 8; ++t) {
                             // the GEMM output as the unfused path stores it (bf16)
-                            f[t] = __bfloat162float(__float2bfloat16(
-                                __uint_as_float(u < 4 ? v0[u * 8 + t] : v1[(u - 4) * 8 + t])));
+                            f[t] = __bfloat162float(__float2bfloat16(__uint_as_float(v0[uu * 8 + t])));
                         }
-                        unpack8(a0[u], x);
+                        unpack8(*reinterpret_cast<const uint4*>(stg0 + sw), x);
                         if constexpr (EPI == kEpiSwiGLUFwd) {
 #pragma unroll
                             for (int t = 0; t < 8; ++t) {
@@ -496,20 +508,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             }
                         } else {
                             float y[8];
-                            unpack8(a1[u], y);
+                            unpack8(*reinterpret_cast<const uint4*>(stg1 + sw), y);
 #pragma unroll
                             for (int t = 0; t < 8; ++t) swiglu_bwd_elem(x[t], y[t], f[t], o0[t], o1[t]);
                         }
-                        const int sw = (u ^ (r & 7)) << 4;
-                        *reinterpret_cast<uint4*>(stg0 + r * 128 + sw) = pack8(o0);
-                        *reinterpret_cast<uint4*>(stg1 + r * 128 + sw) = pack8(o1);
+                        *reinterpret_cast<uint4*>(stg0 + sw) = pack8(o0);
+                        *reinterpret_cast<uint4*>(stg1 + sw) = pack8(o1);
                     }
                     fence_async_shared();
-                    named_barrier(2, 128);
+                    named_barrier(2, 256);
                     if (store_leader) {
                         tma_store_2d(&tma_d, stg0, col, m0);
                         tma_store_2d(&tma_d2, stg1, col, m0);
                         bulk_commit();
+                        // prefetch the next chunk's aux tiles into the other set once
+                        // the stores that last used it have read their data
+                        int nt = tile, nc = c + 1;
+                        if (nc == kChunks) nt += npairs, nc = 0;
+                        if (nt < num_tiles) {
+                            bulk_wait_read<1>();
+                            load_aux(chunk + 1, (nt % tiles_m) * 256 + rank * BM, (nt / tiles_m) * PBN + nc * 64);
+                        }
                     }
                 }
                 tc_fence_before();
@@ -685,11 +704,14 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
     rc = EPI == kEpiAddF32 ? make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 32, BM, true)
                            : make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 64, BM, false);
     if (rc) return rc;
+    CUtensorMap mx0, mx1;
     if (kFused) {
         rc = make_tma_2d(&md2, g->d2, g->n, g->m, g->ldd, 64, BM, false);
+        if (!rc) rc = make_tma_2d(&mx0, g->aux0, g->n, g->m, g->ld_aux, 64, BM, false);
+        if (!rc) rc = make_tma_2d(&mx1, g->aux1 ? g->aux1 : g->aux0, g->n, g->m, g->ld_aux, 64, BM, false);
         if (rc) return rc;
     } else {
-        md2 = md;  // unused
+        md2 = mx0 = mx1 = md;  // unused
     }
     KParams p;
     p.aux0 = static_cast<const __nv_bfloat16*>(g->aux0);
@@ -712,7 +734,7 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
         DH_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         configured = true;
     }
-    kern<<<grid, kThreads, C::kSmem, stream>>>(ma, mb, md, md2, p);
+    kern<<<grid, pair_threads<EPI>(), C::kSmem, stream>>>(ma, mb, md, md2, mx0, mx1, p);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

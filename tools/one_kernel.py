@@ -13,6 +13,14 @@ if which.startswith("gemm"):
     d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
     for _ in range(3):
         dh.gemm(a, b, d)
+elif which.startswith("swiglu"):
+    m, n, k = (4096, 14336, 4096) if which.endswith("tp1") else (4096, 1792, 4096)
+    a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
+    d, d2, aux0, aux1 = (torch.randn(m, n, device="cuda").to(torch.bfloat16) for _ in range(4))
+    epi = dh.EPI_SWIGLU_BWD if "bwd" in which else dh.EPI_SWIGLU_FWD
+    for _ in range(3):
+        dh.gemm(a, b, d, epilogue=epi, d2=d2, aux0=aux0, aux1=aux1)
 elif which.startswith("attn"):
     T, nq, nkv, D = (4096, 32, 8, 128) if which == "attn_tp1" else (4096, 4, 1, 128)
     qkv = (torch.randn(T, (nq + 2 * nkv) * D, device="cuda") * 0.5).to(torch.bfloat16)
