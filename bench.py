@@ -212,13 +212,16 @@ def cpu_baseline_sample(shape):
 WIDE_CAPS = {"sequences": 16, "segments": 14, "candidates": 200000}
 
 
-def emulated_tp_experiment(args, tp, timed_factory):
+def emulated_tp_experiment(args, tp, timed_factory, full=True):
     """TP=<tp> per-GPU shapes on this single GPU with emulated collectives
     (dh_ctx_create_emulated: proxy kernels on the NCCL CTA budget, held for the
     NVLink wire time at the measured 770 GB/s peer bandwidth). Measures the
     G4 profile on-device, searches the SI plan from it with the unchanged DP,
-    then times SI, sequential and compute-only (collectives skipped) steps.
-    Numerically meaningless by construction; timing-faithful by design."""
+    then times SI (default and wide search caps; plan steps joined or relaxed),
+    sequential and compute-only (collectives left out of the lowered program)
+    steps. Numerically meaningless by construction; timing-faithful by design.
+    full=False (the TP sweep points) times only the best SI variant, sequential
+    and compute-only."""
     import copy
 
     import torch
@@ -237,35 +240,41 @@ def emulated_tp_experiment(args, tp, timed_factory):
     log(f"emulated tp{tp}: profiling")
     prof = json.loads(m.profile(iters=5))
     prof_s = time.perf_counter() - t0
-    log("emulated: profiled")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"b200_profile_tp{tp}_emulated.json"), "w") as f:
         json.dump(prof, f, indent=1)
-    srch = planner.lib().search_si_plan(shape.planner_model(), {"tp": tp, "sp": True}, B200_CLUSTER, prof)
+    par = {"tp": tp, "sp": True}
+    srch = planner.lib().search_si_plan(shape.planner_model(), par, B200_CLUSTER, prof)
     # caps are an API parameter of search_si_plan: the wider search (0.1 s)
     # finds plans with more, finer segments
-    srch_wide = planner.lib().search_si_plan(shape.planner_model(), {"tp": tp, "sp": True}, B200_CLUSTER,
-                                             prof, caps=WIDE_CAPS, parallel=True)
+    srch_wide = planner.lib().search_si_plan(shape.planner_model(), par, B200_CLUSTER, prof,
+                                             caps=WIDE_CAPS, parallel=True)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(0))
     timed = timed_factory
     # lr 0: the optimizer still runs (same work), but the emulated (numerically
     # meaningless) gradients cannot drive the weights to overflow across steps
     step = lambda: m.step({"lr": 0.0}, use_graph=True)  # noqa: E731
+    # (name, plan, executor mode, collectives skipped)
+    modes = [("si", srch, "si", False), ("si_wide", srch_wide, "si", False),
+             ("si_wide_relaxed", srch_wide, "si_relaxed", False),
+             ("compute_only", srch_wide, "si_relaxed", True), ("sequential", srch_wide, "sequential", False)]
+    if not full:
+        modes = [x for x in modes if x[0] in ("si_wide_relaxed", "compute_only", "sequential")]
     res = {}
-    for mode, skip in (("si", False), ("si_wide", False), ("compute_only", True), ("sequential", False)):
-        plan = srch_wide if mode == "si_wide" else srch
-        m.set_plan(plan["plan_json"], json.dumps(prof), mode="sequential" if mode == "sequential" else "si")
+    for name, plan, mode, skip in modes:
+        m.set_plan(plan["plan_json"], json.dumps(prof), mode=mode)
         m.set_overlap_ctas(sms - args.nccl_ctas)
         m.set_skip_comm(skip)
         for _ in range(2):
             step()
-        res[mode] = timed(max(2, args.steps), step, stream)
-        log(f"emulated {mode}: {res[mode]:.1f} ms/step")
+        res[name] = timed(max(2, args.steps if full else 2), step, stream)
+        log(f"emulated tp{tp} {name}: {res[name]:.1f} ms/step")
     m.set_skip_comm(False)
     comm_nodes = {"ag0", "rs0", "ag1", "rs1", "rs1_bwd_ag", "ag1_bwd_rs", "rs0_bwd_ag", "ag0_bwd_rs"}
     comm_solo = sum(e["t_us"] for e in prof["solo"] if e["shape"] in comm_nodes)
     pairs = shape.layers * shape.micro_batches
-    best = "si_wide" if res["si_wide"] < res["si"] else "si"
+    si_modes = [k for k in res if k.startswith("si")]
+    best = min(si_modes, key=lambda k: res[k])
     exposed = (res[best] - res["compute_only"]) * 1e3 / pairs
     exposed_seq = (res["sequential"] - res["compute_only"]) * 1e3 / pairs
     fl = layer_flops(shape, tp)
@@ -280,7 +289,7 @@ def emulated_tp_experiment(args, tp, timed_factory):
     return {
         "what": f"TP={tp} per-GPU shapes of the same workload on ONE B200; collectives are proxy kernels "
                 f"({args.nccl_ctas} CTAs, held for wire bytes / {link:.0f} GB/s); numerics not meaningful",
-        "best_si_plan": best,
+        "best_si": best,
         "tokens_per_s_tp_group": round(tokens / (res[best] / 1e3), 1),
         "tokens_per_s_per_gpu": round(tokens / (res[best] / 1e3) / tp, 1),
         "ms_per_step": {k: round(v, 3) for k, v in res.items()},
@@ -313,8 +322,9 @@ def main():
     ap.add_argument("--no-sequential", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1024)
     ap.add_argument("--nccl-ctas", type=int, default=16)
-    ap.add_argument("--emulate-tp", type=int, default=8,
-                    help="at N=1 also run the TP=<n> per-GPU shapes with emulated collectives (0 = off)")
+    ap.add_argument("--emulate-tp", default="2,4,8",
+                    help="at N=1 also run these TP sizes' per-GPU shapes with emulated collectives "
+                         "(comma list; the largest gets every SI variant; 0 = off)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world, rank, local = dist_setup()
@@ -447,11 +457,20 @@ def main():
         traffic = json.load(open(tpath)).get(f"tp{tp}")
 
     emu = None
-    if world == 1 and args.emulate_tp > 1:
+    emu_sweep = {}
+    tps = [int(t) for t in str(args.emulate_tp).split(",") if int(t) > 1]
+    if world == 1 and tps:
         del host_in, loss_host, dev_dst, loss_dev
         torch.cuda.synchronize()
         model.close()
-        emu = emulated_tp_experiment(args, args.emulate_tp, timed)
+        for t in tps:
+            r = emulated_tp_experiment(args, t, timed, full=t == max(tps))
+            if t == max(tps):
+                emu = r
+            else:
+                emu_sweep[f"tp{t}"] = {k: r[k] for k in ("tokens_per_s_per_gpu", "mfu", "ms_per_step",
+                                                           "hidden_comm_frac", "frac_of_overlap_roofline",
+                                                           "exposed_comm_us_per_layer_pair", "best_si")}
 
     if rank != 0:
         if world > 1:
@@ -502,6 +521,7 @@ def main():
                    "second_strand_extra_frac": round(info["slot_bytes"] / (info["pool_bytes"] - info["slot_bytes"]), 5)},
         "clocks": clocks,
         "tp_emulated": emu,
+        "tp_emulated_sweep": emu_sweep or None,
     }
     print(json.dumps(line), flush=True)
     # torch's pinned-host allocator records events on the streams its buffers

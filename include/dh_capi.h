@@ -182,8 +182,9 @@ int dh_model_destroy(dh_model* m);
  * lowering replays the lane dispatch rule with; cluster_json the ClusterSpec used
  * to rebuild the DAG (may be NULL = a B200 default). mode 0 = SI (W schedule:
  * F1, SI(F_{i+1}, B_i) ..., B_m), 1 = sequential (F1 B1 F2 B2 ...), both with
- * the plan's per-strand operator orders. plan_json NULL = template order, one
- * segment per pass (valid for mode 1 and as a trivial SI plan). */
+ * the plan's per-strand operator orders; 2 = SI with relaxed steps (same per-lane
+ * issue order, lanes joined only at layer-pair boundaries). plan_json NULL =
+ * template order, one segment per pass (valid for mode 1 and as a trivial SI plan). */
 int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
                       const char* cluster_json, int mode);
 /* Host-only lowering (no GPU needed): the launch program dh_model_set_plan would

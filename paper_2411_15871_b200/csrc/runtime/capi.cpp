@@ -215,7 +215,8 @@ int dh_model_destroy(dh_model* m) {
 int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
                       const char* cluster_json, int mode) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
-    if (mode != 0 && mode != 1) return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI) or 1 (sequential)");
+    if (mode < 0 || mode > 2)
+        return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI), 1 (sequential) or 2 (SI, relaxed steps)");
     RT_TRY(dh::configure_plan(*m, plan_json, profile_json, cluster_json));
     return dh::lower_program(*m, mode);
 }
@@ -223,7 +224,8 @@ int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_js
 int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_json,
                   const char* profile_json, int mode, char** out) {
     if (!cfg || !out) return dh::set_error(DH_ERR_INVALID, "null argument");
-    if (mode != 0 && mode != 1) return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI) or 1 (sequential)");
+    if (mode < 0 || mode > 2)
+        return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI), 1 (sequential) or 2 (SI, relaxed steps)");
     dh::Model m;  // host-only: no context, no pool
     RT_TRY(dh::derive_cfg(cfg, tp, rank, &m.cfg));
     RT_TRY(dh::build_dags(m, dh::default_cluster(), nullptr));

@@ -129,8 +129,13 @@ struct Lowering {
     }
 
     // One SI layer pair: forward (fs, lf) with backward (bs, lb), per plan step.
-    void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl) {
+    // relaxed (mode 2): the plan's per-lane issue order is kept but only the first
+    // step of a layer pair joins the lanes (it guards the activation slot the
+    // forward strand takes over from the backward strand); inside a layer pair the
+    // two strands touch disjoint buffers, so the per-strand event edges suffice.
+    void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl, bool relaxed) {
         take_slot(fs, lf);
+        bool first_step = true;
         for (const auto& st : m.plan.plan.steps) {
             const auto fa = segment(m.plan.fwd_segmentation, st.fwd_seg.value_or(0));
             const auto ba = segment(m.plan.bwd_segmentation, st.bwd_seg.value_or(0));
@@ -152,7 +157,8 @@ struct Lowering {
                     return v ? *v : 0.0;  // missing pairs only affect issue order
                 },
                 &order);
-            barrier();
+            if (!relaxed || first_step) barrier();
+            first_step = false;
             for (const auto& [side, i] : order) {
                 if (side == 0) emit(fs, lf, fa[i]);
                 else emit(bs, lb, ba[i]);
@@ -182,7 +188,7 @@ int lower_ops(Model& m, int mode) {
             for (int l = 0; l < L; ++l) lw.forward_layer(0, l);
             for (int i = 0; i + 1 < mb; ++i) {
                 lw.barrier();
-                for (int k = 0; k < L; ++k) lw.si_layer_pair(i + 1, k, i, L - 1 - k, tbl);
+                for (int k = 0; k < L; ++k) lw.si_layer_pair(i + 1, k, i, L - 1 - k, tbl, mode == 2);
             }
             lw.barrier();
             for (int l = L - 1; l >= 0; --l) lw.backward_layer(mb - 1, l);

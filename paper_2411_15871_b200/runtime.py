@@ -172,7 +172,7 @@ class Model:
                  cluster_json: str | None = None, mode: str = "si"):
         enc = lambda s: None if s is None else s.encode()  # noqa: E731
         check(_lib().dh_model_set_plan(self.handle, enc(plan_json), enc(profile_json),
-                                       enc(cluster_json), {"si": 0, "sequential": 1}[mode]))
+                                       enc(cluster_json), {"si": 0, "sequential": 1, "si_relaxed": 2}[mode]))
 
     def set_overlap_ctas(self, n: int):
         check(_lib().dh_model_set_overlap_ctas(self.handle, n))
@@ -238,7 +238,7 @@ def lower(shape: "LlamaShape", tp: int, plan_json: str | None, mode: str = "si",
     p = c_void_p()
     enc = lambda s: None if s is None else s.encode()  # noqa: E731
     check(_lib().dh_lower_json(ctypes.byref(cfg), tp, rank, enc(plan_json), enc(profile_json),
-                               {"si": 0, "sequential": 1}[mode], ctypes.byref(p)))
+                               {"si": 0, "sequential": 1, "si_relaxed": 2}[mode], ctypes.byref(p)))
     return json.loads(_take_string(p))
 
 

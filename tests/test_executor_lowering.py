@@ -98,8 +98,19 @@ def test_tiny_programs(tp, mb):
     plan = _plan(shape, tp)
     si = lower(shape, tp, plan, "si")
     seq = lower(shape, tp, plan, "sequential")
+    rel = lower(shape, tp, plan, "si_relaxed")
     used_si = check_program(si, shape, mb)
     used_seq = check_program(seq, shape, mb)
+    # relaxed steps: the same launches in the same order, a subset of the waits
+    assert check_program(rel, shape, mb) == used_si
+    assert [(o["strand"], o["layer"], o["node"], o["lane"], o["slot"]) for o in rel["ops"]] == \
+           [(o["strand"], o["layer"], o["node"], o["lane"], o["slot"]) for o in si["ops"]]
+    # ... and every ordering it imposes is one SI also imposes (its graph is a relaxation)
+    si_preds = _happens_before(si["ops"])
+    for i, o in enumerate(rel["ops"]):
+        extra = set(o["waits"]) - set(si["ops"][i]["waits"])
+        assert not extra or _reachable_from(si_preds, extra, i)
+    assert sum(len(o["waits"]) for o in rel["ops"]) <= sum(len(o["waits"]) for o in si["ops"])
     assert len(used_seq) == shape.layers
     assert len(used_si) == (shape.layers + 1 if mb > 1 else shape.layers)
     if mb > 1:  # SI interleaves the two strands inside each SI block

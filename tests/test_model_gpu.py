@@ -86,16 +86,18 @@ def test_tp1_model_vs_oracle_and_si_equals_sequential(ctx):
     orc, m, xs, rs = _build(shape, ctx)
     plan = _plan(shape, 1)
     runs = {}
-    for mode, graph in (("si", False), ("sequential", False), ("si", True)):
+    for mode, graph in (("si", False), ("sequential", False), ("si", True), ("si_relaxed", True)):
         m.set_plan(plan, mode=mode)
         m.zero_grads()
         m.run_program(use_graph=graph)
         m.sync()
         runs[(mode, graph)] = _snapshot(m, shape)
     a, b, c = runs[("si", False)], runs[("sequential", False)], runs[("si", True)]
+    d = runs[("si_relaxed", True)]
     for k in a:
         assert torch.equal(a[k], b[k]), f"SI != sequential for {k}"
         assert torch.equal(a[k], c[k]), f"graph != eager for {k}"
+        assert torch.equal(a[k], d[k]), f"relaxed SI != SI for {k}"
 
     # oracle: strand 0 then strand 1, gradients accumulated
     p = planner.parse_plan(plan)
