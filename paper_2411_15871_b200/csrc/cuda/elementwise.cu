@@ -48,6 +48,47 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     }
 }
 
+// Row split over TPR threads (VPT 16-byte vectors each), RPB rows per block:
+// a 4096-wide row is 128 threads x 4 vectors, so even the 512-row TP=8 shards
+// put 256 blocks in flight; the row sum goes warp shuffle -> smem -> all.
+template <int VPT, int TPR, int RPB>
+__global__ void __launch_bounds__(TPR * RPB)
+    rmsnorm_fwd_split(const uint4* __restrict__ x, const uint4* __restrict__ g, uint4* __restrict__ y,
+                      float* __restrict__ rstd, int rows, float inv_cols, float eps) {
+    constexpr int kW = TPR / 32;  // warps per row
+    __shared__ float red[RPB][kW];
+    const int sub = threadIdx.x / TPR, t = threadIdx.x % TPR;
+    const int row = blockIdx.x * RPB + sub;
+    const bool ok = row < rows;
+    const long long base = static_cast<long long>(row) * (VPT * TPR);
+    float v[VPT][8];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const uint4 u = ok ? __ldcs(x + base + i * TPR + t) : make_uint4(0, 0, 0, 0);
+        unpack8(u, v[i]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ss += v[i][k] * v[i][k];
+    }
+    ss = warp_sum(ss);
+    if ((t & 31) == 0) red[sub][t / 32] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) tot += red[sub][w];
+    if (!ok) return;
+    const float r = rsqrtf(tot * inv_cols + eps);
+    if (t == 0) rstd[row] = r;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        float gg[8], o[8];
+        unpack8(g[i * TPR + t], gg);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = v[i][k] * r * gg[k];
+        y[base + i * TPR + t] = pack8(o);
+    }
+}
+
 __global__ void __launch_bounds__(kRowWarps * 32)
     rmsnorm_fwd_any(const uint4* __restrict__ x, const uint4* __restrict__ g, uint4* __restrict__ y,
                     float* __restrict__ rstd, int rows, int vec_cols, float inv_cols, float eps) {
@@ -83,6 +124,71 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 // warp shuffles + shared memory. Its dgamma column sums stay in registers and
 // land in partial[b][:]; a second kernel reduces the G rows in order (no
 // atomics => deterministic).
+// Same math, RB rows per block iteration: the RB rows' loads are all in flight
+// before the (single) block barrier that completes their RB dot products.
+template <int RB>
+__global__ void rmsnorm_bwd_rows(const uint4* __restrict__ x, const uint4* __restrict__ g,
+                                 const float* __restrict__ rstd, const uint4* __restrict__ dy,
+                                 const uint4* __restrict__ resid, uint4* __restrict__ dx,
+                                 float* __restrict__ partial, int rows, int vec_cols, float inv_cols) {
+    __shared__ float red[2][RB][32];
+    const int t = threadIdx.x;
+    const int lane = t % 32, wid = t / 32, nw = (blockDim.x + 31) / 32;
+    float gam[8], dg[8];
+    unpack8(g[t], gam);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dg[k] = 0.f;
+    int parity = 0;
+    for (int row0 = blockIdx.x * RB; row0 < rows; row0 += gridDim.x * RB, parity ^= 1) {
+        float xv[RB][8], dv[RB][8], rr[RB], dot[RB];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const int row = row0 + j;
+            const bool ok = row < rows;
+            const long long off = static_cast<long long>(row) * vec_cols + t;
+            rr[j] = ok ? rstd[row] : 0.f;
+            unpack8(ok ? x[off] : make_uint4(0, 0, 0, 0), xv[j]);
+            unpack8(ok ? dy[off] : make_uint4(0, 0, 0, 0), dv[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            dot[j] = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                xv[j][k] *= rr[j];           // xhat
+                dg[k] += dv[j][k] * xv[j][k];
+                dv[j][k] *= gam[k];          // dxhat
+                dot[j] += dv[j][k] * xv[j][k];
+            }
+            dot[j] = warp_sum(dot[j]);
+            if (lane == 0) red[parity][j][wid] = dot[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const int row = row0 + j;
+            if (row >= rows) break;
+            float tot = 0.f;
+            for (int w = 0; w < nw; ++w) tot += red[parity][j][w];
+            tot *= inv_cols;
+            const long long off = static_cast<long long>(row) * vec_cols + t;
+            float o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = rr[j] * (dv[j][k] - xv[j][k] * tot);
+            if (resid) {
+                float rv[8];
+                unpack8(resid[off], rv);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o[k] += rv[k];
+            }
+            dx[off] = pack8(o);
+        }
+    }
+    float4* dst = reinterpret_cast<float4*>(partial + static_cast<long long>(blockIdx.x) * vec_cols * 8 + t * 8);
+    dst[0] = make_float4(dg[0], dg[1], dg[2], dg[3]);
+    dst[1] = make_float4(dg[4], dg[5], dg[6], dg[7]);
+}
+
 __global__ void rmsnorm_bwd_cols(const uint4* __restrict__ x, const uint4* __restrict__ g,
                                  const float* __restrict__ rstd, const uint4* __restrict__ dy,
                                  const uint4* __restrict__ resid, uint4* __restrict__ dx,
@@ -140,8 +246,16 @@ __global__ void column_reduce_add(const float* __restrict__ partial, float* __re
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = blockIdx.x * 32 + lane;
     float s = 0.f;
-    if (c < cols)
-        for (int w = warp; w < nw; w += 8) s += partial[static_cast<long long>(w) * cols + c];
+    if (c < cols) {
+        float a[4] = {0.f, 0.f, 0.f, 0.f};  // 4 loads in flight; combined in a fixed order
+        int w = warp;
+        for (; w + 24 < nw; w += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] += partial[static_cast<long long>(w + 8 * u) * cols + c];
+        }
+        for (; w < nw; w += 8) a[0] += partial[static_cast<long long>(w) * cols + c];
+        s = (a[0] + a[1]) + (a[2] + a[3]);
+    }
     red[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && c < cols) {
@@ -201,6 +315,42 @@ __global__ void swiglu_bwd_kernel(const uint4* __restrict__ gate, const uint4* _
 // Half-split rotation (Llama/HF convention): pair (i, i + d/2), frequency
 // theta^(-2i/d), angle = position * frequency computed in fp64 so that the
 // rotation matches the oracle to fp32 rounding even at long positions.
+// Vectorised form (head_dim % 16 == 0, 16-byte aligned rows): the block's
+// threads first compute the token's half cos/sin pairs once (fp64, same formula),
+// then rotate 8 consecutive pairs per thread with 16-byte loads and stores.
+__global__ void __launch_bounds__(128) rope_vec_kernel(__nv_bfloat16* __restrict__ qkv, long long ld,
+                                                       int tokens, int heads, int head_dim,
+                                                       double log_theta, int pos0, float sign) {
+    __shared__ float cs[2][256];
+    const int half = head_dim / 2;
+    const int t = blockIdx.x;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        const double inv_freq = exp(-log_theta * (2.0 * i) / head_dim);
+        const double ang = static_cast<double>(t + pos0) * inv_freq;
+        cs[0][i] = static_cast<float>(cos(ang));
+        cs[1][i] = sign * static_cast<float>(sin(ang));
+    }
+    __syncthreads();
+    __nv_bfloat16* row = qkv + static_cast<long long>(t) * ld;
+    const int per_head = half / 8;
+    for (int w = threadIdx.x; w < heads * per_head; w += blockDim.x) {
+        const int h = w / per_head, i0 = (w % per_head) * 8;
+        uint4* pa = reinterpret_cast<uint4*>(row + h * head_dim + i0);
+        uint4* pb = reinterpret_cast<uint4*>(row + h * head_dim + half + i0);
+        float a[8], b[8], oa[8], ob[8];
+        unpack8(*pa, a);
+        unpack8(*pb, b);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float c = cs[0][i0 + k], sn = cs[1][i0 + k];
+            oa[k] = a[k] * c - b[k] * sn;
+            ob[k] = b[k] * c + a[k] * sn;
+        }
+        *pa = pack8(oa);
+        *pb = pack8(ob);
+    }
+}
+
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, long long ld, int tokens, int heads,
                             int head_dim, double log_theta, int pos0, float sign) {
     const int half = head_dim / 2;
@@ -441,7 +591,12 @@ int dh_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int r
         case 512: rmsnorm_fwd_reg<2><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
         case 1024: rmsnorm_fwd_reg<4><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
         case 2048: rmsnorm_fwd_reg<8><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
-        case 4096: rmsnorm_fwd_reg<16><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
+        case 4096:
+            rmsnorm_fwd_split<4, 128, 2><<<(rows + 1) / 2, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps);
+            break;
+        case 8192:
+            rmsnorm_fwd_split<4, 256, 1><<<rows, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps);
+            break;
         default: rmsnorm_fwd_any<<<grid, block, 0, s>>>(X, G, Y, rstd, rows, cols / 8, ic, eps);
     }
     DH_CUDA_CHECK(cudaGetLastError());
@@ -455,8 +610,9 @@ int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const vo
         return set_error(DH_ERR_INVALID, "rmsnorm_bwd: cols % 8, cols <= 8192 and 16-byte alignment required");
     if (rows <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
-    const int blocks = std::min(rows, 296);
-    rmsnorm_bwd_cols<<<blocks, cols / 8, 0, s>>>(
+    constexpr int kRB = 4;
+    const int blocks = std::min((rows + kRB - 1) / kRB, 296);
+    rmsnorm_bwd_rows<kRB><<<blocks, cols / 8, 0, s>>>(
         static_cast<const uint4*>(x), static_cast<const uint4*>(gamma), rstd,
         static_cast<const uint4*>(dy), static_cast<const uint4*>(resid), static_cast<uint4*>(dx),
         partial, rows, cols / 8, 1.f / cols);
@@ -505,6 +661,13 @@ int dh_rope(void* qkv, long long ld, int tokens, int n_q_heads, int n_kv_heads, 
             float theta, int pos0, int inverse, void* stream) {
     if (head_dim % 2) return set_error(DH_ERR_INVALID, "rope: odd head_dim");
     if (tokens <= 0) return DH_OK;
+    if (head_dim % 16 == 0 && head_dim <= 512 && aligned16(qkv) && ld % 8 == 0) {
+        rope_vec_kernel<<<tokens, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+            static_cast<__nv_bfloat16*>(qkv), ld, tokens, n_q_heads + n_kv_heads, head_dim,
+            std::log(static_cast<double>(theta)), pos0, inverse ? -1.f : 1.f);
+        DH_CUDA_CHECK(cudaGetLastError());
+        return DH_OK;
+    }
     rope_kernel<<<tokens, 64, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<__nv_bfloat16*>(qkv), ld, tokens, n_q_heads + n_kv_heads, head_dim,
         std::log(static_cast<double>(theta)), pos0, inverse ? -1.f : 1.f);
