@@ -1,23 +1,28 @@
 // Causal GQA flash attention on tcgen05 / TMEM / TMA (head_dim 128) — the
 // attn node (forward). Replaces the mma.sync path of attention.cu for D=128.
 //
-// One CTA per work item = (128-query block, q head[, KV chunk]); KV blocks of
-// 128 keys, causal blocks only, items dispatched heaviest first across heads.
+// One CTA per work item = (pair of 128-query tiles of one q head[, KV chunk]);
+// KV blocks of 128 keys, causal blocks only, items dispatched heaviest first
+// across heads. The two query tiles ping-pong on the tensor core: while the
+// softmax warps of one tile turn S into P, the MMA warp runs the other tile's
+// PV and next QK^T, so the tensor pipe is not idle during the softmax.
 // When the grid is too small to balance (few heads per GPU at high TP: the
 // longest causal row is the critical path), long rows are split into KV
 // chunks chosen by an LPT makespan model on the host; each chunk writes an
 // unnormalised fp32 partial (O, max, sum) and attn_fwd_combine merges them.
-//   warp 0       TMA producer: Q once, K/V through a 2-stage ring
+//   warp 0       TMA producer: Q tiles once, K_j / V_j through a 5-slot ring
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5   softmax: thread = query row (its TMEM lane)
-// TMEM (512 cols): S double buffer (2 x 128) + O accumulator (128).
-//   S_j = Q K_j^T            M128 N128 K128, A=Q (K-major), B=K (K-major)
-//   O  += P_j V_j            M128 N128 K128, A=P (smem, K-major), B=V (MN-major)
+//   warps 2..5   softmax of tile 0, warps 6..9 softmax of tile 1
+//                (thread = query row = its TMEM lane)
+// TMEM (512 cols): S0 | S1 | O0 | O1 (128 columns each).
+//   S_t  = Q_t K_j^T         M128 N128 K128, A=Q (smem, K-major), B=K (smem, K-major)
+//   P_t  = exp2(S_t ...)     bf16, written back over the first 64 columns of S_t
+//   O_t += P_t V_j           M128 N128 K128, A=P (TMEM), B=V (smem, MN-major)
 // The same smem tile of K/V rows serves as K-major B for QK^T and as MN-major
-// B for PV (only the descriptor differs). The MMA warp issues S_{j+1} while the
-// softmax warps work on S_j. Online softmax uses lazy rescaling: O (in TMEM) is
-// only rescaled when a row maximum grows by more than 2^8, so the tcgen05.ld/st
-// round trip is rare; P values are bounded by 2^8 in between.
+// B for PV (only the descriptor differs). P never touches shared memory, which
+// keeps the SS-mode QK^T below the shared-memory bandwidth limit. Online
+// softmax uses lazy rescaling: O (in TMEM) is only rescaled when a row maximum
+// grows by more than 2^8; P values are bounded by 2^8 in between.
 #include <algorithm>
 #include <cmath>
 #include <functional>
@@ -36,21 +41,24 @@ namespace {
 constexpr int D = 128;
 constexpr int BQ = 128;
 constexpr int BKV = 128;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
 constexpr int kTile = BQ * D * 2;       // 32 KB: [2 d-halves][128 rows][128 B]
 constexpr int kHalf = kTile / 2;        // 16 KB
+constexpr int kRing = 5;                // K/V tiles in flight: ring index 2j = K_j, 2j+1 = V_j
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
+#ifndef DH_ATTN_POLY
+#define DH_ATTN_POLY 1
+#endif
 
 struct FwdSmem {
     // offsets from the 1024-aligned base
-    static constexpr int q = 0;
-    static constexpr int k = q + kTile;          // 2 stages
-    static constexpr int v = k + 2 * kTile;      // 2 stages
-    static constexpr int p = v + 2 * kTile;
-    static constexpr int bars = p + kTile;
+    static constexpr int q = 0;                  // two query tiles
+    static constexpr int kv = q + 2 * kTile;     // kRing slots
+    static constexpr int bars = kv + kRing * kTile;
     static constexpr int total = bars + 256 + 1024;
 };
+static_assert(FwdSmem::total <= 232448, "forward smem exceeds the sm_100 limit");
 
 struct FwdParams {
     float* lse;
@@ -60,16 +68,36 @@ struct FwdParams {
     int group;
     float scale_log2;
     int nq;        // q heads (item index = rank * nq + head)
-    int nqb;       // 128-query blocks
-    int chunk;     // KV blocks per chunk; 0 = no split
+    int nkb;       // 128-key blocks (= 128-query blocks)
+    int npairs;    // query-tile pairs
+    int chunk;     // KV blocks per chunk (even); 0 = no split
     int maxc;      // chunks of the longest row
     float* part;   // split partials: O [h][qb][c][d][row], then (m, l) [h][qb][c][row][2]
 };
 
 constexpr int kMaxItems = 1024;  // split schedule entries per head (kernel parameter)
 struct FwdSched {
-    uint32_t item[kMaxItems];  // (qb << 16) | chunk, heaviest first
+    uint32_t item[kMaxItems];  // (pair << 16) | chunk, heaviest first
 };
+
+// (2^x0, 2^x1) for x <= 0 on the FMA pipe, packed fp32x2: x = n + f
+// (n = round(x), |f| <= 1/2), 2^f by a degree-3 polynomial (max relative
+// error 1.2e-4, below bf16's 2^-9 rounding of P), 2^n added to the exponent
+// bits. x is clamped at -125, so masked (-inf) scores give 2^-125, which
+// vanishes against any unmasked term.
+__device__ __forceinline__ uint64_t exp2_fma2(float x0, float x1) {
+    const uint64_t x = f2_pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+    const uint64_t t = fadd2(x, f2_pack(12582912.f, 12582912.f));  // 1.5 * 2^23: round to an integer
+    const uint64_t fr = ffma2(fadd2(t, f2_pack(-12582912.f, -12582912.f)), f2_pack(-1.f, -1.f), x);
+    uint64_t q = ffma2(f2_pack(0.05459283f, 0.05459283f), fr, f2_pack(0.24221838f, 0.24221838f));
+    q = ffma2(q, fr, f2_pack(0.69336867f, 0.69336867f));
+    q = ffma2(q, fr, f2_pack(1.f, 1.f));
+    float q0, q1, t0, t1;
+    f2_unpack(q, q0, q1);
+    f2_unpack(t, t0, t1);
+    return f2_pack(__int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23)),
+                   __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23)));
+}
 
 // K-major operand, 2 swizzle atoms along K (d or keys): k-step kk of 16.
 __device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int kk) {
@@ -89,31 +117,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::bars);
     uint64_t* q_full = bars + 0;
-    uint64_t* k_full = bars + 1;    // [2]  K ring: freed once S_j is computed
-    uint64_t* k_empty = bars + 3;   // [2]
-    uint64_t* s_full = bars + 5;    // [2]
-    uint64_t* p_full = bars + 7;
-    uint64_t* pv_done = bars + 8;
-    uint64_t* v_full = bars + 9;    // [2]  V ring: freed once PV_j is accumulated
-    uint64_t* v_empty = bars + 11;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+    uint64_t* kv_full = bars + 1;            // [kRing]
+    uint64_t* kv_empty = bars + 1 + kRing;   // [kRing]
+    uint64_t* s_full = bars + 1 + 2 * kRing;  // [2] per tile: S_t(j) computed (and PV_t(j-1) done)
+    uint64_t* p_full = s_full + 2;           // [2] per tile: P_t(j) in TMEM
+    uint64_t* o_done = s_full + 4;           // [2] per tile: last PV done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
 
     const int rank = blockIdx.x / p.nq;
     const int h = blockIdx.x % p.nq;
-    int qb, ch = 0, kv0 = 0, kv1;
+    int qp, ch = 0, kv0 = 0, kvend;
     if (p.chunk) {
         const uint32_t e = sched.item[rank];
-        qb = static_cast<int>(e >> 16);
+        qp = static_cast<int>(e >> 16);
         ch = static_cast<int>(e & 0xffffu);
         kv0 = ch * p.chunk;
-        kv1 = min(kv0 + p.chunk, qb + 1);
+        kvend = min(kv0 + p.chunk, 2 * qp + 2);
     } else {
-        qb = p.nqb - 1 - rank;
-        kv1 = qb + 1;  // causal, BQ == BKV
+        qp = p.npairs - 1 - rank;
+        kvend = 2 * qp + 2;  // causal, BQ == BKV
     }
-    const bool split = p.chunk && qb + 1 > p.chunk;
+    kvend = min(kvend, p.nkb);
+    const bool split = p.chunk && 2 * qp + 2 > p.chunk;
     const int kvh = h / p.group;
-    const int n_kv = kv1 - kv0;
+    const int n = kvend - kv0;                         // blocks of tile 1
+    const int n0 = min(kvend, 2 * qp + 1) - kv0;       // blocks of tile 0 (n or n - 1; >= 1: chunks are even)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -121,15 +149,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&k_full[i], 1);
-            mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1);
-            mbar_init(&v_empty[i], 1);
-            mbar_init(&s_full[i], 1);
+        for (int i = 0; i < kRing; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
         }
-        mbar_init(p_full, 128);
-        mbar_init(pv_done, 1);
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 128);
+            mbar_init(&o_done[t], 1);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -137,109 +165,126 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_s0 = tmem, t_o = tmem + 256;
+    const uint32_t t_s = tmem, t_o = tmem + 256;  // S_t at t_s + 128 t, O_t at t_o + 128 t
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(q_full, kTile);
-            tma_load_2d(sm + FwdSmem::q, &tm_q, q_full, h * D, qb * BQ);
-            tma_load_2d(sm + FwdSmem::q + kHalf, &tm_q, q_full, h * D + 64, qb * BQ);
-            // K runs up to two blocks ahead of V (it is released as soon as S_j is done)
-            auto load_k = [&](int j) {
-                const int st = j & 1;
-                mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
-                mbar_expect_tx(&k_full[st], kTile);
-                uint8_t* kd = sm + FwdSmem::k + st * kTile;
-                tma_load_2d(kd, &tm_k, &k_full[st], kvh * D, (kv0 + j) * BKV);
-                tma_load_2d(kd + kHalf, &tm_k, &k_full[st], kvh * D + 64, (kv0 + j) * BKV);
-            };
-            auto load_v = [&](int j) {
-                const int st = j & 1;
-                mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
-                mbar_expect_tx(&v_full[st], kTile);
-                uint8_t* vd = sm + FwdSmem::v + st * kTile;
-                tma_load_2d(vd, &tm_v, &v_full[st], kvh * D, (kv0 + j) * BKV);
-                tma_load_2d(vd + kHalf, &tm_v, &v_full[st], kvh * D + 64, (kv0 + j) * BKV);
-            };
-            load_k(0);
-            if (n_kv > 1) load_k(1);
-            for (int j = 0; j < n_kv; ++j) {
-                load_v(j);
-                if (j + 2 < n_kv) load_k(j + 2);
+            mbar_expect_tx(q_full, 2 * kTile);
+            for (int t = 0; t < 2; ++t) {
+                uint8_t* qd = sm + FwdSmem::q + t * kTile;
+                tma_load_2d(qd, &tm_q, q_full, h * D, (2 * qp + t) * BQ);
+                tma_load_2d(qd + kHalf, &tm_q, q_full, h * D + 64, (2 * qp + t) * BQ);
+            }
+            for (int idx = 0; idx < 2 * n; ++idx) {
+                const int slot = idx % kRing;
+                mbar_wait(&kv_empty[slot], ((idx / kRing) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[slot], kTile);
+                uint8_t* dst = sm + FwdSmem::kv + slot * kTile;
+                const CUtensorMap* map = (idx & 1) ? &tm_v : &tm_k;
+                const int row = (kv0 + (idx >> 1)) * BKV;
+                tma_load_2d(dst, map, &kv_full[slot], kvh * D, row);
+                tma_load_2d(dst + kHalf, map, &kv_full[slot], kvh * D + 64, row);
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);
         constexpr uint32_t id_o = umma_idesc_bf16(128, 128, false, true);
         const uint32_t q_addr = smem_u32(sm + FwdSmem::q);
-        const uint32_t p_addr = smem_u32(sm + FwdSmem::p);
-        auto issue_s = [&](int j) {
-            const int st = j & 1;
-            mbar_wait(&k_full[st], (j >> 1) & 1);
+        const uint32_t kv_addr = smem_u32(sm + FwdSmem::kv);
+        auto wait_kv = [&](int idx) {
+            mbar_wait(&kv_full[idx % kRing], (idx / kRing) & 1);
             tc_fence_after();
+        };
+        auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
             if (elect_one()) {
-                const uint32_t k_addr = smem_u32(sm + FwdSmem::k + st * kTile);
+                const uint32_t k_addr = kv_addr + ((2 * j) % kRing) * kTile;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    tc_mma_bf16(t_s0 + st * 128, desc_kmajor(q_addr, kk), desc_kmajor(k_addr, kk), id_s,
+                    tc_mma_bf16(t_s + t * 128, desc_kmajor(q_addr + t * kTile, kk), desc_kmajor(k_addr, kk), id_s,
                                 kk > 0);
-                tc_commit(&s_full[st]);
-                tc_commit(&k_empty[st]);
+                tc_commit(&s_full[t]);
             }
             __syncwarp();
         };
-        mbar_wait(q_full, 0);
-        issue_s(0);
-        for (int j = 0; j < n_kv; ++j) {
-            if (j + 1 < n_kv) issue_s(j + 1);
-            mbar_wait(p_full, j & 1);
-            mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t v_addr = smem_u32(sm + FwdSmem::v + (j & 1) * kTile);
-#pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk)
-                    tc_mma_bf16(t_o, desc_kmajor(p_addr, kk), desc_mnmajor(v_addr, kk), id_o,
-                                (j | kk) != 0);
-                tc_commit(&v_empty[j & 1]);
-                tc_commit(pv_done);
-            }
+        auto release = [&](int idx) {
+            if (elect_one()) tc_commit(&kv_empty[idx % kRing]);
             __syncwarp();
+        };
+        mbar_wait(q_full, 0);
+        wait_kv(0);
+        issue_s(0, 0);
+        issue_s(1, 0);
+        release(0);
+        for (int j = 0; j < n; ++j) {
+            wait_kv(2 * j + 1);  // V_j
+            const uint32_t v_addr = kv_addr + ((2 * j + 1) % kRing) * kTile;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int nt = t ? n : n0;
+                if (j >= nt) continue;
+                mbar_wait(&p_full[t], j & 1);
+                tc_fence_after();
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < BKV / 16; ++kk)
+                        tc_mma_bf16_ts(t_o + t * 128, t_s + t * 128 + kk * 8, desc_mnmajor(v_addr, kk), id_o,
+                                       (j | kk) != 0);
+                    if (j + 1 >= nt) tc_commit(&o_done[t]);
+                }
+                __syncwarp();
+                if (t == 1) release(2 * j + 1);  // tile 1 is the last reader of V_j
+                if (j + 1 < nt) {
+                    wait_kv(2 * j + 2);  // K_{j+1}
+                    issue_s(t, j + 1);
+                    if (t == 1) release(2 * j + 2);
+                }
+            }
         }
     } else {
         // ------------------------------------------------------------ softmax
+        const int t = (warp - 2) >> 2;
         const int quad = warp & 3;
         const int r = quad * 32 + lane;                 // row within the tile
+        const int qb = 2 * qp + t;                      // query block of this tile
         const int qrow = qb * BQ + r;                   // query position
+        const int nt = t ? n : n0;
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        uint8_t* sp = sm + FwdSmem::p;
+        const uint32_t ts = t_s + t * 128 + lane_off, to = t_o + t * 128 + lane_off;
         float m_used = -INFINITY, l = 0.f;
-        for (int j = 0; j < n_kv; ++j) {
-            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+        for (int j = 0; j < nt; ++j) {
+            mbar_wait(&s_full[t], j & 1);
             tc_fence_after();
-            float s[BKV];
+            // all four 32-column loads in flight before one wait
+            uint32_t sr[BKV];
 #pragma unroll
-            for (int c = 0; c < BKV / 32; ++c) {
-                uint32_t rr[32];
-                tmem_ld32(t_s0 + (j & 1) * 128 + lane_off + c * 32, rr);
-                tmem_ld_wait();
+            for (int c = 0; c < BKV / 32; ++c) tmem_ld32(ts + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
+            tmem_ld_wait();
+            const int kb = kv0 + j;
+            const bool masked = kb == qb || (kb + 1) * BKV > p.T;
+            auto apply_mask = [&](int c0, int c1) {
 #pragma unroll
-                for (int t = 0; t < 32; ++t) s[c * 32 + t] = __uint_as_float(rr[t]) * p.scale_log2;
-            }
-            const bool diag = kv0 + j == qb;
-            float mx = -INFINITY;
+                for (int u = c0; u < c1; ++u) {
+                    const int key = kb * BKV + u;
+                    if (key > qrow || key >= p.T) sr[u] = __float_as_uint(-INFINITY);
+                }
+            };
+            if (masked) apply_mask(0, BKV);
+            // row max as 8 independent chains (a single 128-long dependent
+            // FMNMX chain was the softmax critical path)
+            float m8[8];
 #pragma unroll
-            for (int t = 0; t < BKV; ++t) {
-                const int key = (kv0 + j) * BKV + t;
-                if ((diag && key > qrow) || key >= p.T) s[t] = -INFINITY;
-                mx = fmaxf(mx, s[t]);
-            }
-            // P smem and O are read by PV_{j-1}: wait for it before touching either.
-            if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
-            tc_fence_after();
-            // Lazy rescale. tcgen05.ld/st are warp-collective (.sync.aligned), so
-            // the decision to touch O is made per warp (__any_sync); lanes that
-            // do not need a new maximum rescale by exactly 1.
+            for (int u = 0; u < 8; ++u) m8[u] = __uint_as_float(sr[u]);
+#pragma unroll
+            for (int u = 8; u < BKV; u += 16)
+#pragma unroll
+                for (int w = 0; w < 8; ++w)
+                    m8[w] = fmax3(m8[w], __uint_as_float(sr[u + w]), __uint_as_float(sr[u + 8 + w < BKV ? u + 8 + w : u + w]));
+            const float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7])) *
+                             p.scale_log2;
+            // Lazy rescale. S_t(j) was issued after PV_t(j-1), so s_full also
+            // means O_t is quiescent. tcgen05.ld/st are warp-collective, so the
+            // decision to touch O is made per warp (__any_sync); lanes that do
+            // not need a new maximum rescale by exactly 1.
             const bool need = j == 0 || mx > m_used + kRescaleThreshold;
             const float m_new = need ? fmaxf(mx, m_used) : m_used;
             if (__any_sync(0xffffffffu, need && j > 0)) {
@@ -248,74 +293,100 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
                 for (int c = 0; c < D / 32; ++c) {
                     uint32_t rr[32];
-                    tmem_ld32(t_o + lane_off + c * 32, rr);
+                    tmem_ld32(to + c * 32, rr);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) rr[t] = __float_as_uint(__uint_as_float(rr[t]) * corr);
-                    tmem_st32(t_o + lane_off + c * 32, rr);
+                    for (int u = 0; u < 32; ++u) rr[u] = __float_as_uint(__uint_as_float(rr[u]) * corr);
+                    tmem_st32(to + c * 32, rr);
                 }
-                tmem_st_wait();
             }
             m_used = m_new;
-            float rs = 0.f;
+            const uint64_t neg_m = f2_pack(-m_used, -m_used), sc2 = f2_pack(p.scale_log2, p.scale_log2);
+            uint64_t r4[4] = {0, 0, 0, 0};  // packed row-sum partials
 #pragma unroll
-            for (int c = 0; c < BKV / 8; ++c) {
-                float pv[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    pv[t] = fast_exp2(s[c * 8 + t] - m_used);
-                    rs += pv[t];
+            for (int c = 0; c < 2; ++c) {
+                if (c == 1) {
+                    // columns 64..127 are reloaded rather than kept live across
+                    // the first half: the register budget is 168 at 10 warps
+                    tmem_ld32(ts + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
+                    tmem_ld32(ts + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
+                    tmem_ld_wait();
+                    if (masked) apply_mask(64, BKV);
                 }
-                const int atom = c >> 3, cc = c & 7;
-                *reinterpret_cast<uint4*>(sp + atom * kHalf + r * 128 + ((cc ^ (r & 7)) << 4)) = pack8(pv);
+                uint32_t pk[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const int e = c * 64 + 2 * u;
+                    const uint64_t x = ffma2(f2_pack(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2, neg_m);
+                    // a quarter of the exponentials run on the FMA pipe: both
+                    // softmax tiles together would otherwise saturate the MUFU
+                    uint64_t pp;
+                    if (DH_ATTN_POLY && (u & 3) == 3) {
+                        float x0, x1;
+                        f2_unpack(x, x0, x1);
+                        pp = exp2_fma2(x0, x1);
+                    } else {
+                        float x0, x1;
+                        f2_unpack(x, x0, x1);
+                        pp = f2_pack(fast_exp2(x0), fast_exp2(x1));
+                    }
+                    r4[u & 3] = fadd2(r4[u & 3], pp);
+                    float p0, p1;
+                    f2_unpack(pp, p0, p1);
+                    pk[u] = pack2(p0, p1);
+                }
+                tmem_st32(ts + c * 32, pk);  // P over S columns [0, 64)
             }
+            float ra, rb, rc, rd;
+            f2_unpack(fadd2(fadd2(r4[0], r4[1]), fadd2(r4[2], r4[3])), ra, rb);
+            (void)rc;
+            (void)rd;
+            const float rs = ra + rb;
             l += rs;
-            fence_async_shared();  // generic-proxy smem writes -> visible to the MMA (async proxy)
+            tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(p_full);
+            mbar_arrive(&p_full[t]);
         }
-        mbar_wait(pv_done, (n_kv - 1) & 1);
+        mbar_wait(&o_done[t], 0);
         tc_fence_after();
         if (split) {
             // unnormalised partial, [d][row] so a warp's stores are coalesced
-            const long long slot = (static_cast<long long>(h) * p.nqb + qb) * p.maxc + ch;
+            const long long slot = (static_cast<long long>(h) * (2 * p.npairs) + qb) * p.maxc + ch;
             float* po = p.part + slot * (BQ * D) + r;
 #pragma unroll 1
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t rr[32];
-                tmem_ld32(t_o + lane_off + c * 32, rr);
+                tmem_ld32(to + c * 32, rr);
                 tmem_ld_wait();
 #pragma unroll
-                for (int t = 0; t < 32; ++t) po[(c * 32 + t) * BQ] = __uint_as_float(rr[t]);
+                for (int u = 0; u < 32; ++u) po[(c * 32 + u) * BQ] = __uint_as_float(rr[u]);
             }
-            float* pml = p.part + static_cast<long long>(p.nq) * p.nqb * p.maxc * (BQ * D) + slot * (2 * BQ);
+            float* pml = p.part + static_cast<long long>(p.nq) * (2 * p.npairs) * p.maxc * (BQ * D) +
+                         slot * (2 * BQ);
             *reinterpret_cast<float2*>(pml + 2 * r) = make_float2(m_used, l);
-            goto done;
-        }
-        {
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        const bool ok = qrow < p.T;
-        __nv_bfloat16* orow = p.o + static_cast<long long>(qrow) * p.ldo + h * D;
+        } else {
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            const bool ok = qrow < p.T;
+            __nv_bfloat16* orow = p.o + static_cast<long long>(qrow) * p.ldo + h * D;
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-            uint32_t rr[32];
-            tmem_ld32(t_o + lane_off + c * 32, rr);
-            tmem_ld_wait();
-            if (ok) {
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t rr[32];
+                tmem_ld32(to + c * 32, rr);
+                tmem_ld_wait();
+                if (ok) {
 #pragma unroll
-                for (int t = 0; t < 32; t += 8) {
-                    float f[8];
+                    for (int u = 0; u < 32; u += 8) {
+                        float f[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(rr[t + u]) * inv;
-                    *reinterpret_cast<uint4*>(orow + c * 32 + t) = pack8(f);
+                        for (int w = 0; w < 8; ++w) f[w] = __uint_as_float(rr[u + w]) * inv;
+                        *reinterpret_cast<uint4*>(orow + c * 32 + u) = pack8(f);
+                    }
                 }
             }
-        }
-        if (ok) p.lse[static_cast<long long>(h) * p.T + qrow] = (m_used + log2f(l)) * (1.f / kLog2e);
+            if (ok) p.lse[static_cast<long long>(h) * p.T + qrow] = (m_used + log2f(l)) * (1.f / kLog2e);
         }
     }
 
-done:
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -326,20 +397,21 @@ done:
 
 // Merge the KV-chunk partials of every split row: O = sum_c 2^(m_c-M) O_c / L,
 // L = sum_c 2^(m_c-M) l_c, lse = (M + log2 L) ln 2. Chunks are merged in chunk
-// order, so the result is deterministic. Block = (split query block, head,
-// 16-column slice of d); thread = (row, 8 columns): partial loads are
-// coalesced along rows ([d][row] layout).
+// order, so the result is deterministic. Block = (query block, head, 16-column
+// slice of d); thread = (row, 8 columns): partial loads are coalesced along
+// rows ([d][row] layout). Query blocks from `chunk` on belong to split pairs.
 constexpr int kCombineSlices = D / 16;
 __global__ void __launch_bounds__(256) attn_fwd_combine_kernel(const FwdParams p) {
     const int h = blockIdx.y;
-    const int qb = p.chunk + blockIdx.x;      // rows with more than one chunk
-    const int nc = (qb + p.chunk) / p.chunk;  // ceil((qb + 1) / chunk)
+    const int qb = p.chunk + blockIdx.x;
+    const int nblk = min(2 * (qb >> 1) + 2, p.nkb);
+    const int nc = (nblk + p.chunk - 1) / p.chunk;
     const int r = threadIdx.x & (BQ - 1);
     const int d0 = blockIdx.z * 16 + (threadIdx.x >> 7) * 8;
     const int qrow = qb * BQ + r;
-    if (qrow >= p.T) return;
-    const long long slot0 = (static_cast<long long>(h) * p.nqb + qb) * p.maxc;
-    const float* pml = p.part + static_cast<long long>(p.nq) * p.nqb * p.maxc * (BQ * D);
+    if (qrow >= p.T || nc < 2) return;
+    const long long slot0 = (static_cast<long long>(h) * (2 * p.npairs) + qb) * p.maxc;
+    const float* pml = p.part + static_cast<long long>(p.nq) * (2 * p.npairs) * p.maxc * (BQ * D);
     float mc[16], w[16];
     float M = -INFINITY;
 #pragma unroll
@@ -375,19 +447,23 @@ __global__ void __launch_bounds__(256) attn_fwd_combine_kernel(const FwdParams p
 }
 
 // Split plan for a causal forward: LPT makespan over the SMs of the item costs
-// (KV blocks + fixed per-item cost + partial write/merge for split items).
+// in KV-block units of a tile pair (blocks + fixed per-item cost + partial
+// write/merge for split items). Chunks are even so that both tiles of a pair
+// always have work in every chunk.
 struct FwdSplit {
     int chunk = 0, maxc = 1, items = 0;
     FwdSched sched;
 };
 
-double fwd_makespan(int nq, int nqb, int chunk, int sms, std::vector<std::pair<float, uint32_t>>* out) {
+double fwd_makespan(int nq, int nkb, int chunk, int sms, std::vector<std::pair<float, uint32_t>>* out) {
     std::vector<std::pair<float, uint32_t>> it;
-    for (int qb = 0; qb < nqb; ++qb) {
-        const int nc = (qb + chunk) / chunk;
+    const int npairs = (nkb + 1) / 2;
+    for (int qp = 0; qp < npairs; ++qp) {
+        const int nblk = std::min(2 * qp + 2, nkb);
+        const int nc = (nblk + chunk - 1) / chunk;
         for (int c = 0; c < nc; ++c) {
-            const int len = std::min((c + 1) * chunk, qb + 1) - c * chunk;
-            it.push_back({len + 0.3f + (nc > 1 ? 0.5f : 0.f), (static_cast<uint32_t>(qb) << 16) | c});
+            const int len = std::min((c + 1) * chunk, nblk) - c * chunk;
+            it.push_back({len + 1.0f + (nc > 1 ? 3.0f : 0.f), (static_cast<uint32_t>(qp) << 16) | c});
         }
     }
     std::stable_sort(it.begin(), it.end(), [](const auto& a, const auto& b) {
@@ -417,19 +493,21 @@ const FwdSplit& fwd_split_plan(int T, int nq) {
     FwdSplit sp;
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int nqb = (T + BQ - 1) / BQ;
-    // many heads x blocks per SM already balance; only small grids are split
-    if (static_cast<long long>(nq) * nqb > 4LL * sms) return cache.emplace(key, sp).first->second;
-    double best = fwd_makespan(nq, nqb, nqb, sms, nullptr);
+    const int nkb = (T + BKV - 1) / BKV;
+    const int npairs = (nkb + 1) / 2;
+    // many heads x pairs per SM already balance; only small grids are split
+    if (static_cast<long long>(nq) * npairs > 2LL * sms) return cache.emplace(key, sp).first->second;
+    const int full = 2 * npairs;
+    double best = fwd_makespan(nq, nkb, full, sms, nullptr);
     for (int div : {2, 3, 4, 6, 8}) {
-        const int c = std::max(2, (nqb + div - 1) / div);
-        if (c >= nqb || (nqb + c - 1) / c > 16) continue;
+        const int c = std::max(2, 2 * ((full + 2 * div - 1) / (2 * div)));
+        if (c >= nkb || (full + c - 1) / c > 16) continue;
         std::vector<std::pair<float, uint32_t>> it;
-        const double ms = fwd_makespan(nq, nqb, c, sms, &it);
-        if (ms < 0.95 * best && static_cast<int>(it.size()) <= kMaxItems) {
+        const double ms = fwd_makespan(nq, nkb, c, sms, &it);
+        if (ms < 0.85 * best && static_cast<int>(it.size()) <= kMaxItems) {
             best = ms;
             sp.chunk = c;
-            sp.maxc = (nqb + c - 1) / c;
+            sp.maxc = (full + c - 1) / c;
             sp.items = static_cast<int>(it.size());
             for (size_t i = 0; i < it.size(); ++i) sp.sched.item[i] = it[i].second;
         }
@@ -442,8 +520,8 @@ const FwdSplit& fwd_split_plan(int T, int nq) {
 long long attn_fwd_tc_scratch_floats(int T, int nq) {
     const FwdSplit& sp = fwd_split_plan(T, nq);
     if (!sp.chunk) return 0;
-    const long long nqb = (T + BQ - 1) / BQ;
-    return static_cast<long long>(nq) * nqb * sp.maxc * (BQ * D + 2 * BQ);
+    const long long nqb2 = 2LL * (((T + BKV - 1) / BKV + 1) / 2);
+    return static_cast<long long>(nq) * nqb2 * sp.maxc * (BQ * D + 2 * BQ);
 }
 
 // Host launcher (dh_attn_fwd dispatches head_dim 128 here).
@@ -463,8 +541,9 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
                                            FwdSmem::total));
         cfg = true;
     }
-    const int nqb = (T + BQ - 1) / BQ;
-    FwdParams prm{lse, static_cast<__nv_bfloat16*>(o), ldo, T, nq / nkv, scale * kLog2e, nq, nqb, 0, 1,
+    const int nkb = (T + BKV - 1) / BKV;
+    const int npairs = (nkb + 1) / 2;
+    FwdParams prm{lse, static_cast<__nv_bfloat16*>(o), ldo, T, nq / nkv, scale * kLog2e, nq, nkb, npairs, 0, 1,
                   scratch};
     const FwdSplit& sp = fwd_split_plan(T, nq);
     const bool split = sp.chunk && scratch && scratch_floats >= attn_fwd_tc_scratch_floats(T, nq);
@@ -472,11 +551,11 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
         prm.chunk = sp.chunk;
         prm.maxc = sp.maxc;
     }
-    const int grid = (split ? sp.items : nqb) * nq;
+    const int grid = (split ? sp.items : npairs) * nq;
     attn_fwd_tc_kernel<<<grid, kThreads, FwdSmem::total, s>>>(mq, mk, mv, prm, sp.sched);
     DH_CUDA_CHECK(cudaGetLastError());
     if (split) {
-        attn_fwd_combine_kernel<<<dim3(nqb - sp.chunk, nq, kCombineSlices), 256, 0, s>>>(prm);
+        attn_fwd_combine_kernel<<<dim3(2 * npairs - sp.chunk, nq, kCombineSlices), 256, 0, s>>>(prm);
         DH_CUDA_CHECK(cudaGetLastError());
     }
     return DH_OK;

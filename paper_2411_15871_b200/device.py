@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdh_b200.so")
+# DH_LIB_PATH: load an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("DH_LIB_PATH") or os.path.join(_HERE, "lib", "libdh_b200.so")
 
 _lib = None
 
