@@ -564,21 +564,25 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
 }  // namespace dh
 
 // ===========================================================================
-// Backward (attn_bwd node), two deterministic tcgen05 kernels.
+// Backward (attn_bwd node): one launch, two deterministic tcgen05 work kinds.
 //
-// dK/dV kernel — one CTA per (128-key block, q head); inner q tiles of 64:
-//   S^T  = K Q^T        M128 N64  K128   A=K (K-major)   B=Q (K-major)
-//   dP^T = V dO^T       M128 N64  K128   A=V (K-major)   B=dO (K-major)
+// dK/dV item — one CTA per (128-key block, q head); inner q tiles of 64:
+//   S^T  = K Q^T        M128 N64  K128   A=K (smem)      B=Q (smem, K-major)
+//   dP^T = V dO^T       M128 N64  K128   A=V (smem)      B=dO (smem, K-major)
 //   P^T = exp(scale S^T - lse_q), dS^T = P^T (dP^T - D_q)      (thread = key row)
-//   dV  += P^T dO       M128 N128 K64    A=P^T (smem)    B=dO (MN-major)
-//   dK  += dS^T Q       M128 N128 K64    A=dS^T (smem)   B=Q  (MN-major)
-//   TMEM: S^T x2 (64) | dP^T x2 (64) | dV (128) | dK (128) = 512 columns.
-// dQ kernel — one CTA per (128-query block, q head); inner key tiles of 64:
+//   dV  += P^T dO       M128 N128 K64    A=P^T (TMEM)    B=dO (smem, MN-major)
+//   dK  += dS^T Q       M128 N128 K64    A=dS^T (TMEM)   B=Q  (smem, MN-major)
+//   TMEM: S^T x2 (64) | dP^T x2 (64) | dV (128) | dK (128) = 512 columns;
+//   P^T / dS^T (bf16 pairs) overwrite the first 32 columns of their S^T / dP^T
+//   buffer, so the elementwise results never pass through shared memory.
+// dQ item — one CTA per (128-query block, q head); inner key tiles of 64:
 //   S = Q K^T, dP = dO V^T (M128 N64 K128), dS = P (dP - D)    (thread = query row)
-//   dQ += dS K          M128 N128 K64    A=dS (smem)     B=K (MN-major)
+//   dQ += dS K          M128 N128 K64    A=dS (TMEM)     B=K (smem, MN-major)
 //   TMEM: S x2 | dP x2 | dQ = 384 columns.
-// No atomics: dQ is produced by its own pass and per-head dK/dV partials of a
-// GQA group are reduced in head order by attn_bwd_group_reduce (attention.cu).
+// S/dP buffers are double-buffered: the MMA warp computes tile it+1 while the
+// elementwise warps work on tile it. No atomics: dQ is produced by its own
+// items and per-head dK/dV partials of a GQA group are reduced in head order
+// by attn_bwd_group_reduce (attention.cu).
 // ===========================================================================
 
 namespace dh {
@@ -587,18 +591,27 @@ namespace {
 constexpr int BT64 = 64;
 constexpr int kTile64 = BT64 * D * 2;  // 16 KB: [2 d-halves][64 rows][128 B]
 constexpr int kHalf64 = kTile64 / 2;   // 8 KB
+constexpr int kStages = 4;             // Q/dO (dK/dV items) or K/V (dQ items) ring
 
 struct KvSmem {
-    static constexpr int k = 0;                      // 32 KB
-    static constexpr int v = k + kTile;              // 32 KB
-    static constexpr int q = v + kTile;              // 3 x 16 KB
-    static constexpr int dout = q + 3 * kTile64;     // 3 x 16 KB
-    static constexpr int pt = dout + 3 * kTile64;    // 2 x 16 KB  [128 keys][64 q]
-    static constexpr int dst = pt + 2 * 16384;       // 2 x 16 KB
-    static constexpr int vec = dst + 2 * 16384;      // per stage: lse[64], D[64] (raw)
-    static constexpr int bars = vec + 3 * 128 * 4;
+    static constexpr int k = 0;                          // 32 KB
+    static constexpr int v = k + kTile;                  // 32 KB
+    static constexpr int q = v + kTile;                  // kStages x 16 KB
+    static constexpr int dout = q + kStages * kTile64;   // kStages x 16 KB
+    static constexpr int vec = dout + kStages * kTile64; // per stage: lse[64], D[64] (raw)
+    static constexpr int bars = vec + kStages * 128 * 4;
     static constexpr int total = bars + 256 + 1024;
 };
+
+struct DqSmem {
+    static constexpr int q = 0;                          // 32 KB
+    static constexpr int dout = q + kTile;               // 32 KB
+    static constexpr int k = dout + kTile;               // kStages x 16 KB
+    static constexpr int v = k + kStages * kTile64;      // kStages x 16 KB
+    static constexpr int bars = v + kStages * kTile64;
+    static constexpr int total = bars + 256 + 1024;
+};
+static_assert(KvSmem::total <= 232448 && DqSmem::total <= 232448, "backward smem exceeds the sm_100 limit");
 
 struct BwdParams {
     const float* lse;
@@ -621,10 +634,6 @@ __device__ __forceinline__ uint64_t desc_k64(uint32_t base, int kk) {
 __device__ __forceinline__ uint64_t desc_mn64(uint32_t base, int kk) {
     return umma_desc_sw128(base + kk * 2048, kHalf64, 1024);
 }
-// [128 rows][64 K] single-atom K-major tile (P^T, dS^T, dS): k-step kk (0..3).
-__device__ __forceinline__ uint64_t desc_k1atom(uint32_t base, int kk) {
-    return umma_desc_sw128(base + kk * 32, 16, 1024);
-}
 
 constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
 
@@ -636,12 +645,12 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                                              ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + KvSmem::bars);
     uint64_t* kv_full = bars + 0;
-    uint64_t* q_full = bars + 1;   // [3] Q/dO ring
-    uint64_t* q_empty = bars + 4;  // [3]
-    uint64_t* s_full = bars + 7;   // [2] TMEM S^T/dP^T buffers
-    uint64_t* p_full = bars + 9;
-    uint64_t* mm_done = bars + 10;  // [2], one per P^T/dS^T buffer
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* q_full = bars + 1;                // [kStages] Q/dO ring
+    uint64_t* q_empty = q_full + kStages;       // [kStages]
+    uint64_t* s_full = q_empty + kStages;       // [2] TMEM S^T/dP^T buffers
+    uint64_t* p_full = s_full + 2;              // P^T/dS^T of the current tile in TMEM
+    uint64_t* acc_done = p_full + 1;            // dK/dV complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
     float* vec = reinterpret_cast<float*>(sm + KvSmem::vec);  // [stage][lse 64 | D 64]
 
     const int kvh = h / p.group;
@@ -656,14 +665,13 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
         mbar_init(kv_full, 1);
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < kStages; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
         mbar_init(p_full, 256);
-        mbar_init(&mm_done[0], 1);
-        mbar_init(&mm_done[1], 1);
+        mbar_init(acc_done, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -682,8 +690,8 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             tma_load_2d(sm + KvSmem::v, &tm_v, kv_full, kvh * D, kb * D);
             tma_load_2d(sm + KvSmem::v + kHalf, &tm_v, kv_full, kvh * D + 64, kb * D);
             for (int it = 0; it < n_it; ++it) {
-                const int st = it % 3, qi = i0 + it;
-                mbar_wait(&q_empty[st], ((it / 3) & 1) ^ 1);
+                const int st = it % kStages, qi = i0 + it;
+                mbar_wait(&q_empty[st], ((it / kStages) & 1) ^ 1);
                 mbar_expect_tx(&q_full[st], 2 * kTile64 + (bulk_vec ? 512 : 0));
                 if (bulk_vec) {
                     const long long off = static_cast<long long>(h) * p.T + qi * BT64;
@@ -702,10 +710,9 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
         constexpr uint32_t id_g = umma_idesc_bf16(128, 128, false, true);
         const uint32_t k_addr = smem_u32(sm + KvSmem::k), v_addr = smem_u32(sm + KvSmem::v);
-        const uint32_t pt_addr = smem_u32(sm + KvSmem::pt), ds_addr = smem_u32(sm + KvSmem::dst);
         auto issue_s = [&](int it) {
-            const int qs = it % 3, sb = it & 1;  // smem ring stage, TMEM buffer
-            mbar_wait(&q_full[qs], (it / 3) & 1);
+            const int qs = it % kStages, sb = it & 1;  // smem ring stage, TMEM buffer
+            mbar_wait(&q_full[qs], (it / kStages) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t q_addr = smem_u32(sm + KvSmem::q + qs * kTile64);
@@ -722,21 +729,22 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         mbar_wait(kv_full, 0);
         if (n_it > 0) issue_s(0);
         for (int it = 0; it < n_it; ++it) {
-            const int st = it & 1, qs = it % 3;
+            const int sb = it & 1, qs = it % kStages;
+            // S^T/dP^T(it+1) go into the other buffer, whose P^T/dS^T were
+            // consumed by the dV/dK MMAs of it-1 (issued before, in order).
             if (it + 1 < n_it) issue_s(it + 1);
             mbar_wait(p_full, it & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t q_addr = smem_u32(sm + KvSmem::q + qs * kTile64);
                 const uint32_t o_addr = smem_u32(sm + KvSmem::dout + qs * kTile64);
-                const uint32_t pb = pt_addr + st * 16384, db = ds_addr + st * 16384;
 #pragma unroll
                 for (int kk = 0; kk < BT64 / 16; ++kk) {
-                    tc_mma_bf16(t_dv, desc_k1atom(pb, kk), desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
-                    tc_mma_bf16(t_dk, desc_k1atom(db, kk), desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
+                    tc_mma_bf16_ts(t_dv, t_s + sb * 64 + kk * 8, desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
+                    tc_mma_bf16_ts(t_dk, t_dp + sb * 64 + kk * 8, desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
                 }
                 tc_commit(&q_empty[qs]);
-                tc_commit(&mm_done[st]);
+                if (it + 1 == n_it) tc_commit(acc_done);
             }
             __syncwarp();
         }
@@ -748,57 +756,68 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         const int key = kb * D + r;
         const int t_sm = threadIdx.x - 64;  // 0..255 among the elementwise warps
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        uint8_t* spt = sm + KvSmem::pt;
-        uint8_t* sds = sm + KvSmem::dst;
         const int key_hi = kb * D + D - 1;
+        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), m1 = f2_pack(-1.f, -1.f);
+        const uint64_t nl2e = f2_pack(-kLog2e, -kLog2e);
         for (int it = 0; it < n_it; ++it) {
-            const int st = it & 1, qi = i0 + it;
+            const int sb = it & 1, qi = i0 + it;
             if (!bulk_vec) {
                 // ragged T: stage the vectors with plain loads (s_full implies q_full)
                 named_barrier(1, 256);  // previous readers of this stage are done
                 if (t_sm < BT64) {
                     const int q = qi * BT64 + t_sm;
-                    vec[(it % 3) * 128 + t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] : 0.f;
-                    vec[(it % 3) * 128 + 64 + t_sm] = q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
+                    vec[(it % kStages) * 128 + t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] : 0.f;
+                    vec[(it % kStages) * 128 + 64 + t_sm] =
+                        q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
                 }
                 named_barrier(1, 256);
             }
-            mbar_wait(&s_full[st], (it >> 1) & 1);
+            mbar_wait(&s_full[sb], (it >> 1) & 1);
             tc_fence_after();
             uint32_t a[32], b[32];
-            tmem_ld32(t_s + st * 64 + lane_off + half * 32, a);
-            tmem_ld32(t_dp + st * 64 + lane_off + half * 32, b);
+            tmem_ld32(t_s + sb * 64 + lane_off + half * 32, a);
+            tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
             tmem_ld_wait();
+            // the other half's P^T/dS^T stores overwrite columns this half reads
+            named_barrier(2, 256);
             // whole tile causal-visible and in range: no per-element masking
             const bool full_tile = qi * BT64 >= key_hi && qi * BT64 + BT64 <= p.T && key_hi < p.T;
-            // This P^T / dS^T buffer was read by the dV/dK MMAs two iterations ago.
-            if (it > 1) mbar_wait(&mm_done[st], ((it >> 1) - 1) & 1);
-            const float* lv = vec + (it % 3) * 128 + half * 32;
-            const float* dv_ = vec + (it % 3) * 128 + 64 + half * 32;
+            // explicit shared-space loads: the aligned base pointer is generic
+            const uint32_t lv = smem_u32(vec + (it % kStages) * 128 + half * 32);
+            uint32_t pp[16], pd[16];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float pv[8], d8[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int j = c * 8 + t;
-                    float e = fast_exp2(__uint_as_float(a[j]) * p.scale_log2 - lv[j] * kLog2e);
-                    if (!full_tile) {
-                        const int q = qi * BT64 + half * 32 + j;
-                        if (q < key || q >= p.T || key >= p.T) e = 0.f;
-                    }
-                    pv[t] = e;
-                    d8[t] = e * (__uint_as_float(b[j]) - dv_[j]);
+            for (int u = 0; u < 16; ++u) {
+                float2 l2, d2;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(l2.x), "=f"(l2.y) : "r"(lv + 8 * u));
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d2.x), "=f"(d2.y) : "r"(lv + 256 + 8 * u));
+                // x = scale_log2 * s - log2e * lse
+                const uint64_t x = ffma2(f2_pack(__uint_as_float(a[2 * u]), __uint_as_float(a[2 * u + 1])), sc2,
+                                         ffma2(f2_pack(l2.x, l2.y), nl2e, 0ull));
+                float x0, x1;
+                f2_unpack(x, x0, x1);
+                float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+                if (!full_tile) {
+                    const int q = qi * BT64 + half * 32 + 2 * u;
+                    if (q < key || q >= p.T || key >= p.T) e0 = 0.f;
+                    if (q + 1 < key || q + 1 >= p.T || key >= p.T) e1 = 0.f;
                 }
-                const int cc = half * 4 + c;
-                const int off = st * 16384 + r * 128 + ((cc ^ (r & 7)) << 4);
-                *reinterpret_cast<uint4*>(spt + off) = pack8(pv);
-                *reinterpret_cast<uint4*>(sds + off) = pack8(d8);
+                const uint64_t e = f2_pack(e0, e1);
+                // dS^T = P^T (dP^T - D)
+                const uint64_t ds = ffma2(e, ffma2(f2_pack(d2.x, d2.y), m1,
+                                                   f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1]))),
+                                          0ull);
+                float s0, s1;
+                f2_unpack(ds, s0, s1);
+                pp[u] = pack2(e0, e1);
+                pd[u] = pack2(s0, s1);
             }
-            fence_async_shared();
+            tmem_st16(t_s + sb * 64 + lane_off + half * 16, pp);
+            tmem_st16(t_dp + sb * 64 + lane_off + half * 16, pd);
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(p_full);
         }
-        if (n_it > 0) mbar_wait(&mm_done[(n_it - 1) & 1], ((n_it - 1) >> 1) & 1);
+        if (n_it > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
         const bool ok = key < p.T;
 #pragma unroll 1
@@ -846,16 +865,6 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
     }
 }
 
-struct DqSmem {
-    static constexpr int q = 0;                      // 32 KB
-    static constexpr int dout = q + kTile;           // 32 KB
-    static constexpr int k = dout + kTile;           // 3 x 16 KB
-    static constexpr int v = k + 3 * kTile64;        // 3 x 16 KB
-    static constexpr int ds = v + 3 * kTile64;       // 2 x 16 KB [128 q][64 keys]
-    static constexpr int bars = ds + 2 * 16384;
-    static constexpr int total = bars + 256 + 1024;
-};
-
 __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const CUtensorMap& tm_do,
                                                  const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                  const BwdParams& p, const int qb, const int h) {
@@ -864,12 +873,12 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                                              ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DqSmem::bars);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [3] K/V ring
-    uint64_t* kv_empty = bars + 4;  // [3]
-    uint64_t* s_full = bars + 7;    // [2]
-    uint64_t* p_full = bars + 9;
-    uint64_t* mm_done = bars + 10;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* kv_full = bars + 1;              // [kStages] K/V ring
+    uint64_t* kv_empty = kv_full + kStages;    // [kStages]
+    uint64_t* s_full = kv_empty + kStages;     // [2]
+    uint64_t* p_full = s_full + 2;
+    uint64_t* acc_done = p_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
     const int kvh = h / p.group;
     const int n_it = (qb * D + D) / BT64;  // key tiles 0 .. covering the block's last query
@@ -881,14 +890,13 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         mbar_init(q_full, 1);
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < kStages; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
         mbar_init(p_full, 256);
-        mbar_init(&mm_done[0], 1);
-        mbar_init(&mm_done[1], 1);
+        mbar_init(acc_done, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -906,8 +914,8 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
             tma_load_2d(sm + DqSmem::dout, &tm_do, q_full, h * D, qb * D);
             tma_load_2d(sm + DqSmem::dout + kHalf, &tm_do, q_full, h * D + 64, qb * D);
             for (int it = 0; it < n_it; ++it) {
-                const int st = it % 3;
-                mbar_wait(&kv_empty[st], ((it / 3) & 1) ^ 1);
+                const int st = it % kStages;
+                mbar_wait(&kv_empty[st], ((it / kStages) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[st], 2 * kTile64);
                 uint8_t* kd = sm + DqSmem::k + st * kTile64;
                 uint8_t* vd = sm + DqSmem::v + st * kTile64;
@@ -921,10 +929,9 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
         constexpr uint32_t id_g = umma_idesc_bf16(128, 128, false, true);
         const uint32_t q_addr = smem_u32(sm + DqSmem::q), o_addr = smem_u32(sm + DqSmem::dout);
-        const uint32_t ds_addr = smem_u32(sm + DqSmem::ds);
         auto issue_s = [&](int it) {
-            const int ks = it % 3, sb = it & 1;
-            mbar_wait(&kv_full[ks], (it / 3) & 1);
+            const int ks = it % kStages, sb = it & 1;
+            mbar_wait(&kv_full[ks], (it / kStages) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
@@ -941,7 +948,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         mbar_wait(q_full, 0);
         issue_s(0);
         for (int it = 0; it < n_it; ++it) {
-            const int st = it & 1, ks = it % 3;
+            const int sb = it & 1, ks = it % kStages;
             if (it + 1 < n_it) issue_s(it + 1);
             mbar_wait(p_full, it & 1);
             tc_fence_after();
@@ -949,10 +956,9 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                 const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
 #pragma unroll
                 for (int kk = 0; kk < BT64 / 16; ++kk)
-                    tc_mma_bf16(t_dq, desc_k1atom(ds_addr + st * 16384, kk), desc_mn64(k_addr, kk), id_g,
-                                (it | kk) != 0);
+                    tc_mma_bf16_ts(t_dq, t_dp + sb * 64 + kk * 8, desc_mn64(k_addr, kk), id_g, (it | kk) != 0);
                 tc_commit(&kv_empty[ks]);
-                tc_commit(&mm_done[st]);
+                if (it + 1 == n_it) tc_commit(acc_done);
             }
             __syncwarp();
         }
@@ -965,38 +971,43 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         const int qc = min(qrow, p.T - 1);
         const float lse2 = p.lse[static_cast<long long>(h) * p.T + qc] * kLog2e;
         const float dd = p.dvec[static_cast<long long>(h) * p.T + qc];
-        uint8_t* sds = sm + DqSmem::ds;
+        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nl2 = f2_pack(-lse2, -lse2);
+        const uint64_t nd2 = f2_pack(-dd, -dd);
         for (int it = 0; it < n_it; ++it) {
-            const int st = it & 1;
-            mbar_wait(&s_full[st], (it >> 1) & 1);
+            const int sb = it & 1;
+            mbar_wait(&s_full[sb], (it >> 1) & 1);
             tc_fence_after();
             uint32_t a[32], b[32];
-            tmem_ld32(t_s + st * 64 + lane_off + half * 32, a);
-            tmem_ld32(t_dp + st * 64 + lane_off + half * 32, b);
+            tmem_ld32(t_s + sb * 64 + lane_off + half * 32, a);
+            tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
             tmem_ld_wait();
+            named_barrier(2, 256);  // the other half's dS stores overwrite columns this half reads
             const bool full_tile = it * BT64 + BT64 - 1 <= qb * D && it * BT64 + BT64 <= p.T && qb * D + D <= p.T;
-            if (it > 1) mbar_wait(&mm_done[st], ((it >> 1) - 1) & 1);
+            uint32_t pd[16];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float d8[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int j = c * 8 + t;
-                    float e = fast_exp2(__uint_as_float(a[j]) * p.scale_log2 - lse2);
-                    if (!full_tile) {
-                        const int key = it * BT64 + half * 32 + j;
-                        if (key > qrow || key >= p.T) e = 0.f;
-                    }
-                    d8[t] = e * (__uint_as_float(b[j]) - dd);
+            for (int u = 0; u < 16; ++u) {
+                const uint64_t x = ffma2(f2_pack(__uint_as_float(a[2 * u]), __uint_as_float(a[2 * u + 1])), sc2, nl2);
+                float x0, x1;
+                f2_unpack(x, x0, x1);
+                float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+                if (!full_tile) {
+                    const int key = it * BT64 + half * 32 + 2 * u;
+                    if (key > qrow || key >= p.T) e0 = 0.f;
+                    if (key + 1 > qrow || key + 1 >= p.T) e1 = 0.f;
                 }
-                const int cc = half * 4 + c;
-                *reinterpret_cast<uint4*>(sds + st * 16384 + r * 128 + ((cc ^ (r & 7)) << 4)) = pack8(d8);
+                const uint64_t ds =
+                    ffma2(f2_pack(e0, e1), fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), nd2),
+                          0ull);
+                float s0, s1;
+                f2_unpack(ds, s0, s1);
+                pd[u] = pack2(s0, s1);
             }
-            fence_async_shared();
+            tmem_st16(t_dp + sb * 64 + lane_off + half * 16, pd);
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(p_full);
         }
-        mbar_wait(&mm_done[(n_it - 1) & 1], ((n_it - 1) >> 1) & 1);
+        mbar_wait(acc_done, 0);
         tc_fence_after();
         const bool ok = qrow < p.T;
         __nv_bfloat16* row = p.dq + static_cast<long long>(qrow) * p.lddq + h * D;
@@ -1024,11 +1035,11 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     }
 }
 
-// One launch for both passes: the dK/dV and dQ work items are independent, so
+// One launch for both kinds: the dK/dV and dQ work items are independent, so
 // interleaving them (rank r = r-th heaviest block of either kind, all heads)
-// lets the light items of one pass fill the tail of the other. With few heads
-// per GPU (high TP) the two separate grids each left their longest causal
-// block as an exposed critical path.
+// lets the light items of one kind fill the tail of the other. With few heads
+// per GPU (high TP) two separate grids each left their longest causal block as
+// an exposed critical path.
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
@@ -1045,7 +1056,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 
 }  // namespace
 
-// Host launcher for the two tcgen05 backward kernels (dvec must already hold
+// Host launcher for the tcgen05 backward (dvec must already hold
 // D_i = rowsum(dO * O)); dk_part / dv_part are used only when group > 1.
 int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
