@@ -277,6 +277,35 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True):
     best = min(si_modes, key=lambda k: res[k])
     exposed = (res[best] - res["compute_only"]) * 1e3 / pairs
     exposed_seq = (res["sequential"] - res["compute_only"]) * 1e3 / pairs
+    steady = None
+    if full and shape.micro_batches > 2:
+        # Split the exposed time into the unpaired ends (F_0 and B_{m-1} have no
+        # partner strand: their collectives are exposed whatever the plan) and
+        # the SI blocks: exposed(m) = ends + (m - 1) * block, measured at m and 2.
+        plan_best = {"si": srch, "si_wide": srch_wide, "si_wide_relaxed": srch_wide}[best]
+        mode_best = "si_relaxed" if best.endswith("relaxed") else "si"
+        m.close()
+        shape2 = copy.copy(shape)
+        shape2.micro_batches = 2
+        m = Model(ctx, shape2)
+        r2 = {}
+        for name, skip in ((best, False), ("compute_only", True)):
+            m.set_plan(plan_best["plan_json"], json.dumps(prof), mode=mode_best)
+            m.set_overlap_ctas(sms - args.nccl_ctas)
+            m.set_skip_comm(skip)
+            for _ in range(2):
+                step()
+            r2[name] = timed(max(2, args.steps), step, stream)
+        m.set_skip_comm(False)
+        e_m = (res[best] - res["compute_only"]) * 1e3 / shape.layers   # per layer, whole step
+        e_2 = (r2[best] - r2["compute_only"]) * 1e3 / shape.layers
+        block = (e_m - e_2) / (shape.micro_batches - 2)
+        ends = e_2 - block
+        steady = {"exposed_comm_us_per_layer_pair_si_block": round(block, 1),
+                  "exposed_comm_us_per_layer_unpaired_ends": round(ends, 1),
+                  "hidden_comm_frac_si_block": round(min(1.0, 1.0 - block / comm_solo), 4) if comm_solo else None,
+                  "ms_per_step_m2": {k: round(v, 3) for k, v in r2.items()},
+                  "how": "exposed(m) = ends + (m-1) * block, from the same plan timed at m and at 2 micro-batches"}
     fl = layer_flops(shape, tp)
     pk = peaks()
     t_comp = (fl["fwd"] + fl["bwd"]) / (pk["bf16_burst"] * 1e12) * 1e6
@@ -307,6 +336,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True):
                       "bwd_cuts": json.loads(p["plan_json"])["bwd_cuts"]}
                   for k, p, c in (("si", srch, "default"), ("si_wide", srch_wide, WIDE_CAPS))},
         "profile_seconds": round(prof_s, 2),
+        "steady_state": steady,
     }
 
 

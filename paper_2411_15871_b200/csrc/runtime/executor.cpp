@@ -64,6 +64,11 @@ struct Lowering {
         pending_join.fill(true);
     }
 
+    // Ops outside an SI block run strictly in strand order (one lane at a
+    // time), so their GEMMs never share the GPU with a collective and take
+    // every SM; inside a block the cap applies wherever a collective may co-run.
+    bool capped = false;
+
     void emit(int strand, int layer, int node) {
         // compute-only measurement program: collectives are left out entirely
         if (m.skip_comm && lane_of.at(node) != 0) return;
@@ -74,6 +79,7 @@ struct Lowering {
         o.lane = lane_of.at(node);
         o.slot = slot_of[strand][layer];
         o.prev_slot = layer > 0 ? slot_of[strand][layer - 1] : -1;
+        o.capped = capped;
         if (node == 10 || node == 11) {
             // both run on the compute lane in sequence order: the later one sees the
             // other's output and applies SwiGLU in its GEMM epilogue
@@ -159,12 +165,19 @@ struct Lowering {
                 &order);
             if (!relaxed || first_step) barrier();
             first_step = false;
+            // joined steps: only a step holding a collective co-runs one; relaxed
+            // steps may overlap their neighbours, so the whole block is capped
+            bool step_comm = relaxed;
+            for (int id : fa) step_comm |= lane_of.at(id) != 0;
+            for (int id : ba) step_comm |= lane_of.at(id) != 0;
+            capped = step_comm;
             for (const auto& [side, i] : order) {
                 if (side == 0) emit(fs, lf, fa[i]);
                 else emit(bs, lb, ba[i]);
             }
         }
         give_slot(bs, lb);
+        capped = false;
     }
 };
 

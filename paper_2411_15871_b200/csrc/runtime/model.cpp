@@ -290,7 +290,7 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
     const int D = k.head_dim;
     const long long TH = static_cast<long long>(T) * H;
     const bool tp1 = k.tp == 1;
-    const int cap = m.gemm_ctas_overlap;
+    const int cap = op.capped ? m.gemm_ctas_overlap : 0;
     Slot& sl = m.slots[op.slot];
     const LayerParams& p = m.lp[op.layer];
     auto* W = m.ptr<__nv_bfloat16>(m.w_bf16);

@@ -121,6 +121,7 @@ struct Op {
     bool fuse_swiglu = false;  // mlp_gate/mlp_up: the later of the two computes act in its epilogue
     std::vector<int> waits;  // indices of ops whose completion this op waits for
     bool barrier = false;    // step barrier before this op (all lanes joined)
+    bool capped = true;      // GEMMs may co-run with a collective: limit them to gemm_ctas_overlap SMs
 };
 
 struct Program {
