@@ -35,6 +35,16 @@
 #include "common.cuh"
 #include "dh_capi.h"
 
+#ifdef DH_ATTN_TRACE
+__device__ long long g_attn_trace[1 << 14];
+extern "C" int dh_attn_trace_read(long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(long long) * n) == cudaSuccess ? 0 : 1;
+}
+#define ATR(idx) do { if (blockIdx.x == DH_ATTN_TRACE) g_attn_trace[(idx)] = clock64(); } while (0)
+#else
+#define ATR(idx) do { } while (0)
+#endif
+
 namespace dh {
 namespace {
 
@@ -113,8 +123,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
                        const __grid_constant__ FwdSched sched) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+    // offset arithmetic on the __shared__ array keeps the pointer in the shared
+    // space (plain loads compile to LDS rather than generic LD)
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::bars);
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;            // [kRing]
@@ -641,8 +652,9 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                                                    const CUtensorMap& tm_q, const CUtensorMap& tm_do,
                                                    const BwdParams& p, const int kb, const int h) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+    // offset arithmetic on the __shared__ array keeps the pointer in the shared
+    // space (plain loads compile to LDS rather than generic LD)
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + KvSmem::bars);
     uint64_t* kv_full = bars + 0;
     uint64_t* q_full = bars + 1;                // [kStages] Q/dO ring
@@ -733,7 +745,9 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             // S^T/dP^T(it+1) go into the other buffer, whose P^T/dS^T were
             // consumed by the dV/dK MMAs of it-1 (issued before, in order).
             if (it + 1 < n_it) issue_s(it + 1);
+            if (lane == 0) ATR(it * 8 + 0);
             mbar_wait(p_full, it & 1);
+            if (lane == 0) ATR(it * 8 + 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t q_addr = smem_u32(sm + KvSmem::q + qs * kTile64);
@@ -772,24 +786,26 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 }
                 named_barrier(1, 256);
             }
+            if (threadIdx.x == 64) ATR(it * 8 + 2);
             mbar_wait(&s_full[sb], (it >> 1) & 1);
+            if (threadIdx.x == 64) ATR(it * 8 + 3);
             tc_fence_after();
             uint32_t a[32], b[32];
             tmem_ld32(t_s + sb * 64 + lane_off + half * 32, a);
             tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
             tmem_ld_wait();
             // the other half's P^T/dS^T stores overwrite columns this half reads
+            if (threadIdx.x == 64) ATR(it * 8 + 5);
             named_barrier(2, 256);
+            if (threadIdx.x == 64) ATR(it * 8 + 6);
             // whole tile causal-visible and in range: no per-element masking
             const bool full_tile = qi * BT64 >= key_hi && qi * BT64 + BT64 <= p.T && key_hi < p.T;
-            // explicit shared-space loads: the aligned base pointer is generic
-            const uint32_t lv = smem_u32(vec + (it % kStages) * 128 + half * 32);
+            const float2* lv = reinterpret_cast<const float2*>(vec + (it % kStages) * 128 + half * 32);
+            const float2* dv2 = reinterpret_cast<const float2*>(vec + (it % kStages) * 128 + 64 + half * 32);
             uint32_t pp[16], pd[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
-                float2 l2, d2;
-                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(l2.x), "=f"(l2.y) : "r"(lv + 8 * u));
-                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d2.x), "=f"(d2.y) : "r"(lv + 256 + 8 * u));
+                const float2 l2 = lv[u], d2 = dv2[u];
                 // x = scale_log2 * s - log2e * lse
                 const uint64_t x = ffma2(f2_pack(__uint_as_float(a[2 * u]), __uint_as_float(a[2 * u + 1])), sc2,
                                          ffma2(f2_pack(l2.x, l2.y), nl2e, 0ull));
@@ -811,10 +827,12 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 pp[u] = pack2(e0, e1);
                 pd[u] = pack2(s0, s1);
             }
+            if (threadIdx.x == 64) ATR(it * 8 + 7);
             tmem_st16(t_s + sb * 64 + lane_off + half * 16, pp);
             tmem_st16(t_dp + sb * 64 + lane_off + half * 16, pd);
             tmem_st_wait();
             tc_fence_before();
+            if (threadIdx.x == 64) ATR(it * 8 + 4);
             mbar_arrive(p_full);
         }
         if (n_it > 0) mbar_wait(acc_done, 0);
@@ -869,8 +887,9 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                                                  const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                  const BwdParams& p, const int qb, const int h) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+    // offset arithmetic on the __shared__ array keeps the pointer in the shared
+    // space (plain loads compile to LDS rather than generic LD)
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DqSmem::bars);
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;              // [kStages] K/V ring
