@@ -614,17 +614,19 @@ struct KvSmem {
     static constexpr int total = bars + 256 + 1024;
 };
 
+constexpr int kDqStages = 6;  // K/V ring of the dQ items (Q and dO live in TMEM)
 struct DqSmem {
-    static constexpr int q = 0;                          // 32 KB
-    static constexpr int dout = q + kTile;               // 32 KB
-    static constexpr int k = dout + kTile;               // kStages x 16 KB
-    static constexpr int v = k + kStages * kTile64;      // kStages x 16 KB
-    static constexpr int bars = v + kStages * kTile64;
+    static constexpr int k = 0;                          // kDqStages x 16 KB
+    static constexpr int v = k + kDqStages * kTile64;    // kDqStages x 16 KB
+    static constexpr int bars = v + kDqStages * kTile64;
     static constexpr int total = bars + 256 + 1024;
 };
 static_assert(KvSmem::total <= 232448 && DqSmem::total <= 232448, "backward smem exceeds the sm_100 limit");
 
 struct BwdParams {
+    const __nv_bfloat16* q;     // raw rows for the TMEM-resident Q / dO of the dQ items
+    const __nv_bfloat16* dout;
+    long long ldq, ldo;
     const float* lse;
     const float* dvec;
     float* dk_part;
@@ -891,10 +893,10 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     // space (plain loads compile to LDS rather than generic LD)
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DqSmem::bars);
-    uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;              // [kStages] K/V ring
-    uint64_t* kv_empty = kv_full + kStages;    // [kStages]
-    uint64_t* s_full = kv_empty + kStages;     // [2]
+    uint64_t* q_full = bars + 0;               // Q / dO rows stored into TMEM
+    uint64_t* kv_full = bars + 1;              // [kDqStages] K/V ring
+    uint64_t* kv_empty = kv_full + kDqStages;  // [kDqStages]
+    uint64_t* s_full = kv_empty + kDqStages;   // [2]
     uint64_t* p_full = s_full + 2;
     uint64_t* acc_done = p_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
@@ -904,12 +906,10 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        tma_prefetch(&tm_q);
-        tma_prefetch(&tm_do);
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
-        mbar_init(q_full, 1);
-        for (int i = 0; i < kStages; ++i) {
+        mbar_init(q_full, 256);
+        for (int i = 0; i < kDqStages; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
@@ -923,18 +923,15 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256;
+    // S x2 | dP x2 | dQ | Q (bf16 pairs) | dO (bf16 pairs): Q and dO are the A
+    // operands of every S / dP MMA, so they are read from TMEM, not shared memory
+    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256, t_qa = tmem + 384, t_doa = tmem + 448;
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(q_full, 2 * kTile);
-            tma_load_2d(sm + DqSmem::q, &tm_q, q_full, h * D, qb * D);
-            tma_load_2d(sm + DqSmem::q + kHalf, &tm_q, q_full, h * D + 64, qb * D);
-            tma_load_2d(sm + DqSmem::dout, &tm_do, q_full, h * D, qb * D);
-            tma_load_2d(sm + DqSmem::dout + kHalf, &tm_do, q_full, h * D + 64, qb * D);
             for (int it = 0; it < n_it; ++it) {
-                const int st = it % kStages;
-                mbar_wait(&kv_empty[st], ((it / kStages) & 1) ^ 1);
+                const int st = it % kDqStages;
+                mbar_wait(&kv_empty[st], ((it / kDqStages) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[st], 2 * kTile64);
                 uint8_t* kd = sm + DqSmem::k + st * kTile64;
                 uint8_t* vd = sm + DqSmem::v + st * kTile64;
@@ -947,29 +944,31 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     } else if (warp == 1) {
         constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
         constexpr uint32_t id_g = umma_idesc_bf16(128, 128, false, true);
-        const uint32_t q_addr = smem_u32(sm + DqSmem::q), o_addr = smem_u32(sm + DqSmem::dout);
         auto issue_s = [&](int it) {
-            const int ks = it % kStages, sb = it & 1;
-            mbar_wait(&kv_full[ks], (it / kStages) & 1);
+            const int ks = it % kDqStages, sb = it & 1;
+            mbar_wait(&kv_full[ks], (it / kDqStages) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
                 const uint32_t v_addr = smem_u32(sm + DqSmem::v + ks * kTile64);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    tc_mma_bf16(t_s + sb * 64, desc_kmajor(q_addr, kk), desc_k64(k_addr, kk), id_s, kk > 0);
-                    tc_mma_bf16(t_dp + sb * 64, desc_kmajor(o_addr, kk), desc_k64(v_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16_ts(t_s + sb * 64, t_qa + kk * 8, desc_k64(k_addr, kk), id_s, kk > 0);
+                    tc_mma_bf16_ts(t_dp + sb * 64, t_doa + kk * 8, desc_k64(v_addr, kk), id_s, kk > 0);
                 }
                 tc_commit(&s_full[sb]);
             }
             __syncwarp();
         };
         mbar_wait(q_full, 0);
+        tc_fence_after();
         issue_s(0);
         for (int it = 0; it < n_it; ++it) {
-            const int sb = it & 1, ks = it % kStages;
+            const int sb = it & 1, ks = it % kDqStages;
             if (it + 1 < n_it) issue_s(it + 1);
+            if (lane == 0) ATR(it * 8 + 0);
             mbar_wait(p_full, it & 1);
+            if (lane == 0) ATR(it * 8 + 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
@@ -992,15 +991,42 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         const float dd = p.dvec[static_cast<long long>(h) * p.T + qc];
         const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nl2 = f2_pack(-lse2, -lse2);
         const uint64_t nd2 = f2_pack(-dd, -dd);
+        {
+            // this thread's query row of Q (half 0) or dO (half 1) into its TMEM lane:
+            // row-major bf16 pairs are exactly the packed A-operand columns
+            const __nv_bfloat16* src = half ? p.dout + static_cast<long long>(qc) * p.ldo + h * D
+                                            : p.q + static_cast<long long>(qc) * p.ldq + h * D;
+            const bool in = qrow < p.T;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t w[32];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint4 x = in ? *reinterpret_cast<const uint4*>(src + c * 64 + u * 8) : make_uint4(0, 0, 0, 0);
+                    w[4 * u] = x.x;
+                    w[4 * u + 1] = x.y;
+                    w[4 * u + 2] = x.z;
+                    w[4 * u + 3] = x.w;
+                }
+                tmem_st32((half ? t_doa : t_qa) + lane_off + c * 32, w);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(q_full);
+        }
         for (int it = 0; it < n_it; ++it) {
             const int sb = it & 1;
+            if (threadIdx.x == 64) ATR(it * 8 + 2);
             mbar_wait(&s_full[sb], (it >> 1) & 1);
+            if (threadIdx.x == 64) ATR(it * 8 + 3);
             tc_fence_after();
             uint32_t a[32], b[32];
             tmem_ld32(t_s + sb * 64 + lane_off + half * 32, a);
             tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
             tmem_ld_wait();
+            if (threadIdx.x == 64) ATR(it * 8 + 5);
             named_barrier(2, 256);  // the other half's dS stores overwrite columns this half reads
+            if (threadIdx.x == 64) ATR(it * 8 + 6);
             const bool full_tile = it * BT64 + BT64 - 1 <= qb * D && it * BT64 + BT64 <= p.T && qb * D + D <= p.T;
             uint32_t pd[16];
 #pragma unroll
@@ -1021,9 +1047,11 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                 f2_unpack(ds, s0, s1);
                 pd[u] = pack2(s0, s1);
             }
+            if (threadIdx.x == 64) ATR(it * 8 + 7);
             tmem_st16(t_dp + sb * 64 + lane_off + half * 16, pd);
             tmem_st_wait();
             tc_fence_before();
+            if (threadIdx.x == 64) ATR(it * 8 + 4);
             mbar_arrive(p_full);
         }
         mbar_wait(acc_done, 0);
@@ -1098,7 +1126,8 @@ int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long
         DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
-    BwdParams prm{lse, dvec, dk_part, dv_part, static_cast<__nv_bfloat16*>(dk),
+    BwdParams prm{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(dout), ldq, ldo,
+                  lse, dvec, dk_part, dv_part, static_cast<__nv_bfloat16*>(dk),
                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
                   nq / nkv, scale, scale * kLog2e};
     const int nb = (T + D - 1) / D;
