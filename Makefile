@@ -6,6 +6,7 @@
 # Outputs land in-tree (paper_2411_15871_b200/lib/) so they travel to the GPU box.
 
 CXX      ?= g++
+LINK_CXX ?= /usr/bin/g++
 NVCC     ?= /usr/local/cuda/bin/nvcc
 PKG      := paper_2411_15871_b200
 LIB      := $(PKG)/lib
@@ -39,9 +40,12 @@ $(OBJ)/planner/%.o: $(PKG)/csrc/planner/%.cpp $(wildcard include/weft/*.hpp) $(P
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
+# Linked by the system g++ so that libstdc++ is the shared system copy: a
+# toolchain that only offers a static libstdc++ would export a private copy
+# that clashes with the one numpy/torch load into the same process.
 $(LIB)/libweft_b200.so: $(PLANNER_OBJ)
 	@mkdir -p $(LIB)
-	$(CXX) -shared -o $@ $^ -pthread
+	$(LINK_CXX) -shared -o $@ $^ -pthread
 
 $(OBJ)/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(CUDA_HDR)
 	@mkdir -p $(dir $@)

@@ -10,6 +10,12 @@
  *   weft_dp_align_json       <- dp_align / brute_force_align (pairing_search.hpp:55,63)
  *   weft_search_json         <- search_si_plan + plan_to_json (pairing_search.hpp:93-98)
  *   weft_profile_roundtrip_json <- parse_profile + profile_to_json (overlap_profile.hpp:76-79)
+ *   weft_pipeline_json       <- fold_layers, schedule_w_pipeline / _1f1b / _bidirectional,
+ *                               bubble_ratio, pp_comm_volume, validate_schedule, trace/CSV
+ *                               export (folding_pipeline.hpp:23-103)
+ *   weft_memory_json         <- simulate_memory, max_model_size, default footprints
+ *                               (memory_sim.hpp:47-79)
+ *   weft_estimate_json       <- estimate_iteration_time (estimate.hpp:45-50)
  *
  * Every call returns a weft status (0 ok; 2 ConfigError, 3 InfeasibleError,
  * 4 MissingProfileEntry — the reference CLI's exit codes, weft_main.cpp:20-23;
@@ -36,6 +42,9 @@ int weft_dp_align_json(const char* request, char** out);
 int weft_search_json(const char* request, char** out);
 int weft_profile_roundtrip_json(const char* request, char** out);
 int weft_templates_json(const char* request, char** out);  /* builtin_template_json (op_model.hpp:59) */
+int weft_pipeline_json(const char* request, char** out);
+int weft_memory_json(const char* request, char** out);
+int weft_estimate_json(const char* request, char** out);
 const char* weft_last_error(void);
 void weft_free(char* p);
 

@@ -16,12 +16,19 @@
 //   profile:      a profile document (parse_profile schema) or {"archetype": "..."}
 //   caps:         {sequences, segments, candidates}; barrier_cost_us, parallel, threads
 //   metadata:     {str: str} passed to plan_to_json
+//   schedule:     {discipline, m, p, f_us, b_us, si_us}            (pipeline_json)
+//   memory:       {act_bytes_per_layer, state_bytes_per_layer, capacity_bytes,
+//                  slack_bytes, layers} or {"defaults": true}      (memory_json)
+//   source, microbatches, intra_batch_tp_hidden_frac              (estimate_json)
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
 
 #include "nlohmann/json.hpp"
+#include "weft/estimate.hpp"
+#include "weft/folding_pipeline.hpp"
+#include "weft/memory_sim.hpp"
 #include "weft/op_model.hpp"
 #include "weft/overlap_profile.hpp"
 #include "weft/pairing_search.hpp"
@@ -283,5 +290,110 @@ void WEFT_API(free)(char* p) { std::free(p); }
 extern "C" int WEFT_API(templates_json)(const char* request, char** out) {
     return guarded(request, out, [](const json&) {
         return json{{"builtin_template_json", weft::builtin_template_json()}};
+    });
+}
+
+namespace {
+
+weft::PipelineSchedule schedule_from(const json& j) {
+    const auto disc = weft::parse_discipline(j.value("discipline", std::string("w_shape")));
+    const int m = j.at("m").get<int>(), p = j.at("p").get<int>();
+    weft::BlockDurations d;
+    d.f_us = j.value("f_us", d.f_us);
+    d.b_us = j.value("b_us", d.b_us);
+    d.si_us = j.value("si_us", d.si_us);
+    switch (disc) {
+        case weft::Discipline::w_shape: return weft::schedule_w_pipeline(m, p, d);
+        case weft::Discipline::one_f_one_b: return weft::schedule_1f1b(m, p, d);
+        case weft::Discipline::bidirectional: return weft::schedule_bidirectional(m, p, d);
+    }
+    throw weft::ConfigError("unknown discipline");
+}
+
+weft::MemoryConfig memory_from(const json& req) {
+    const json& j = req.at("memory");
+    weft::MemoryConfig c;
+    if (j.value("defaults", false)) {
+        const auto model = model_from(req.at("model"));
+        const auto par = par_from(req.value("parallelism", json::object()));
+        c.act_bytes_per_layer = weft::default_act_bytes_per_layer(model, par);
+        c.state_bytes_per_layer = weft::default_state_bytes_per_layer(model, par);
+        c.layers = model.layers;
+    }
+    c.act_bytes_per_layer = j.value("act_bytes_per_layer", c.act_bytes_per_layer);
+    c.state_bytes_per_layer = j.value("state_bytes_per_layer", c.state_bytes_per_layer);
+    c.capacity_bytes = j.value("capacity_bytes", c.capacity_bytes);
+    c.slack_bytes = j.value("slack_bytes", c.slack_bytes);
+    c.layers = j.value("layers", c.layers);
+    return c;
+}
+
+}  // namespace
+
+// fold_layers + schedule_* + analyses (reference folding_pipeline.hpp:23-103)
+extern "C" int WEFT_API(pipeline_json)(const char* request, char** out) {
+    return guarded(request, out, [](const json& req) {
+        const auto s = schedule_from(req.at("schedule"));
+        json r = {{"trace_json", weft::schedule_to_trace_json(s)},
+                  {"csv", weft::schedule_to_csv(s)},
+                  {"makespan_us", s.makespan_us()},
+                  {"bubble_ratio", weft::bubble_ratio(s)},
+                  {"violations", weft::validate_schedule(s)},
+                  {"pp_transfers", weft::pp_comm_volume(s, 1).transfers}};
+        if (req.contains("fold_layers")) {
+            const auto lay = weft::fold_layers(req.at("fold_layers").get<int>(), s.p);
+            json g = json::array();
+            for (const auto& x : lay.gpus) g.push_back({x.front_lo, x.front_hi, x.back_lo, x.back_hi});
+            r["fold"] = g;
+        }
+        return r;
+    });
+}
+
+// simulate_memory / max_model_size (reference memory_sim.hpp:47-79)
+extern "C" int WEFT_API(memory_json)(const char* request, char** out) {
+    return guarded(request, out, [](const json& req) {
+        const auto cfg = memory_from(req);
+        json r = json::object();
+        if (req.contains("schedule")) {
+            const auto tl = weft::simulate_memory(schedule_from(req.at("schedule")), cfg);
+            r["peaks_json"] = weft::peaks_to_json(tl, cfg);
+            r["timeline_csv"] = weft::timeline_to_csv(tl);
+        }
+        if (req.contains("max_model")) {
+            const json& mm = req.at("max_model");
+            const auto res = weft::max_model_size(
+                model_from(req.at("model")), par_from(req.value("parallelism", json::object())), cfg,
+                weft::parse_discipline(mm.value("discipline", std::string("w_shape"))), mm.value("m", 8));
+            r["max_layers"] = res.layers;
+            r["max_params"] = res.param_count;
+        }
+        r["act_bytes_per_layer"] = cfg.act_bytes_per_layer;
+        r["state_bytes_per_layer"] = cfg.state_bytes_per_layer;
+        return r;
+    });
+}
+
+// estimate_iteration_time (reference estimate.hpp:45-50)
+extern "C" int WEFT_API(estimate_json)(const char* request, char** out) {
+    return guarded(request, out, [](const json& req) {
+        const auto prof = profile_from(req);
+        weft::EstimateOptions opt;
+        opt.microbatches = req.value("microbatches", opt.microbatches);
+        opt.intra_batch_tp_hidden_frac = req.value("intra_batch_tp_hidden_frac", opt.intra_batch_tp_hidden_frac);
+        if (req.contains("caps")) {
+            const json& c = req.at("caps");
+            opt.search.caps.sequences = c.value("sequences", opt.search.caps.sequences);
+            opt.search.caps.segments = c.value("segments", opt.search.caps.segments);
+            opt.search.caps.candidates = c.value("candidates", opt.search.caps.candidates);
+        }
+        const auto r = weft::estimate_iteration_time(
+            model_from(req.at("model")), cluster_from(req.at("cluster")),
+            par_from(req.value("parallelism", json::object())),
+            weft::parse_plan_source(req.value("source", std::string("dhelix"))), prof, opt);
+        return json{{"makespan_us", r.makespan_us},   {"tflops_per_gpu", r.tflops_per_gpu},
+                    {"mfu", r.mfu},                   {"hidden_comm_frac", r.hidden_comm_frac},
+                    {"layer_fwd_us", r.layer_fwd_us}, {"layer_bwd_us", r.layer_bwd_us},
+                    {"layer_pair_us", r.layer_pair_us}};
     });
 }

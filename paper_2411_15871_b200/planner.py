@@ -44,7 +44,8 @@ class MissingProfileEntry(WeftError):
 _STATUS = {2: ConfigError, 3: InfeasibleError, 4: MissingProfileEntry}
 
 _FUNCS = ("build_dag_json", "topo_orders_json", "segment_cost_json", "dp_align_json",
-          "search_json", "profile_roundtrip_json", "templates_json")
+          "search_json", "profile_roundtrip_json", "templates_json", "pipeline_json", "memory_json",
+          "estimate_json")
 
 
 class PlannerLib:
@@ -117,6 +118,31 @@ class PlannerLib:
 
     def builtin_template_json(self):
         return self.call("templates_json", {})["builtin_template_json"]
+
+    def pipeline(self, discipline, m, p, f_us=1.0, b_us=1.0, si_us=2.0, fold_layers=None):
+        """schedule_{w_pipeline,1f1b,bidirectional} + analyses (folding_pipeline.hpp)."""
+        req = {"schedule": {"discipline": discipline, "m": m, "p": p, "f_us": f_us, "b_us": b_us,
+                            "si_us": si_us}}
+        if fold_layers is not None:
+            req["fold_layers"] = fold_layers
+        return self.call("pipeline_json", req)
+
+    def memory(self, memory, schedule=None, model=None, parallelism=None, max_model=None):
+        """simulate_memory / max_model_size / default footprints (memory_sim.hpp)."""
+        req = {"memory": memory}
+        for k, v in (("schedule", schedule), ("model", model), ("parallelism", parallelism),
+                     ("max_model", max_model)):
+            if v is not None:
+                req[k] = v
+        return self.call("memory_json", req)
+
+    def estimate(self, model, parallelism, cluster, profile, source="dhelix", microbatches=8, caps=None):
+        """estimate_iteration_time (estimate.hpp)."""
+        req = {"model": model, "parallelism": parallelism, "cluster": cluster, "profile": profile,
+               "source": source, "microbatches": microbatches}
+        if caps:
+            req["caps"] = caps
+        return self.call("estimate_json", req)
 
 
 _default: PlannerLib | None = None

@@ -177,13 +177,14 @@ def test_error_mapping():
 
 def test_reference_catch_suites_against_our_library():
     """The reference's own tests (proj/tests/test_{op_model,overlap_profile,
-    pairing_search}.cpp), compiled unmodified against our planner."""
+    pairing_search,folding_pipeline,memory_sim}.cpp), compiled unmodified
+    against our planner."""
     exe = os.path.join(ROOT, "oracle", "_ref", "ours_suite")
     if not os.path.exists(exe):
         pytest.skip("oracle/_ref/ours_suite not built")
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "cases=48 passed=48 failed=0" in out.stdout
+    assert "cases=75 passed=75 failed=0" in out.stdout
 
 
 def test_reference_catch_suites_against_reference():
