@@ -212,6 +212,28 @@ def cpu_baseline_sample(shape):
 WIDE_CAPS = {"sequences": 16, "segments": 14, "candidates": 200000}
 
 
+def memory_vs_model(planner, info, shape):
+    """Measured pool against the reference memory replay (simulate_memory,
+    memory_sim.cpp:33-83) of the same schedule on one stage, fed with the
+    measured per-layer slot (activation) and state bytes: the replay frees and
+    allocates at the same block end, so it sees no second-strand cost; the
+    pool holds one extra layer slot for it."""
+    L, mb = shape.layers, shape.micro_batches
+    state = sum(v for k, v in info["usage"].items() if k.startswith("state."))
+    act = info["slot_bytes"]
+    cfg = {"act_bytes_per_layer": act, "state_bytes_per_layer": state // L,
+           "capacity_bytes": 180 * 1024 ** 3, "layers": L}
+    peaks = {}
+    for disc in ("w_shape", "one_f_one_b"):
+        r = planner.lib().memory(cfg, schedule={"discipline": disc, "m": mb, "p": 1})
+        peaks[disc] = json.loads(r["peaks_json"])["peak_bytes"]
+    measured = state + info["slots"] * act
+    return {"simulate_memory_peak_gb": {k: round(v / 1e9, 3) for k, v in peaks.items()},
+            "measured_state_plus_slots_gb": round(measured / 1e9, 3),
+            "measured_extra_vs_replay_frac": round(measured / peaks["w_shape"] - 1.0, 5),
+            "transients_gb": round((info["pool_bytes"] - measured) / 1e9, 3)}
+
+
 def emulated_tp_experiment(args, tp, timed_factory, full=True):
     """TP=<tp> per-GPU shapes on this single GPU with emulated collectives
     (dh_ctx_create_emulated: proxy kernels on the NCCL CTA budget, held for the
@@ -270,6 +292,20 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True):
         res[name] = timed(max(2, args.steps if full else 2), step, stream)
         log(f"emulated tp{tp} {name}: {res[name]:.1f} ms/step")
     m.set_skip_comm(False)
+    # the reference's iteration model (estimate_iteration_time) on the measured
+    # profile, next to the measured steps (the model has no optimizer step)
+    model_vs_measured = None
+    if full:
+        est = {}
+        for src, caps in (("megatron_baseline", None), ("wavelet_rr", None), ("dhelix", WIDE_CAPS)):
+            r = planner.lib().estimate(shape.planner_model(), par, B200_CLUSTER, prof, source=src,
+                                       microbatches=shape.micro_batches, caps=caps)
+            est[src] = {"ms": round(r["makespan_us"] / 1e3, 3), "hidden_comm_frac": round(r["hidden_comm_frac"], 4)}
+        model_vs_measured = {"modeled_no_optimizer": est,
+                             "measured_ms": {"sequential": round(res["sequential"], 3),
+                                             "si": round(min(v for k, v in res.items() if k.startswith("si")), 3)},
+                             "how": "estimate_iteration_time(W for wavelet_rr/dhelix, 1F1B for megatron; p=1) "
+                                    "fed with this run's measured profile"}
     comm_nodes = {"ag0", "rs0", "ag1", "rs1", "rs1_bwd_ag", "ag1_bwd_rs", "rs0_bwd_ag", "ag0_bwd_rs"}
     comm_solo = sum(e["t_us"] for e in prof["solo"] if e["shape"] in comm_nodes)
     pairs = shape.layers * shape.micro_batches
@@ -337,6 +373,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True):
                   for k, p, c in (("si", srch, "default"), ("si_wide", srch_wide, WIDE_CAPS))},
         "profile_seconds": round(prof_s, 2),
         "steady_state": steady,
+        "model_vs_measured": model_vs_measured,
     }
 
 
@@ -432,6 +469,7 @@ def main():
     probe_ms, probe_n = model.probe_read()  # last step's launches
     model.probe(-1)
     info = model.info()
+    mem_check = memory_vs_model(planner, info, shape)
 
     log(f"SI timed: {ms_si:.1f} ms/step")
     ms_seq = None
@@ -548,7 +586,8 @@ def main():
         "gpu_launches": info["program"]["kernel_launches"],
         "memory": {"pool_gb": round(info["pool_bytes"] / 1e9, 3), "slots": info["slots"],
                    "slot_gb": round(info["slot_bytes"] / 1e9, 4),
-                   "second_strand_extra_frac": round(info["slot_bytes"] / (info["pool_bytes"] - info["slot_bytes"]), 5)},
+                   "second_strand_extra_frac": round(info["slot_bytes"] / (info["pool_bytes"] - info["slot_bytes"]), 5),
+                   "vs_reference_model": mem_check},
         "clocks": clocks,
         "tp_emulated": emu,
         "tp_emulated_sweep": emu_sweep or None,

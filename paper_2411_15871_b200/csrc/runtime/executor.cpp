@@ -1,7 +1,8 @@
 // SI executor: lowers a weft plan (plan_to_json, reference pairing_search.cpp:
 // 543-561) into lane-stream launches and runs them eagerly or as a CUDA graph.
 //
-// Schedule (reference folding_pipeline.cpp schedule_w_pipeline with p = 1):
+// Schedule (reference folding_pipeline.cpp schedule_w_pipeline with p = 1; the
+// SI block order is taken from our schedule_w_pipeline(m, 1)):
 //   SI mode          F_0 | SI(F_1, B_0) | SI(F_2, B_1) | ... | B_{m-1}
 //   sequential mode  F_0 B_0 | F_1 B_1 | ...       (same per-strand op orders)
 // Inside SI(F_{i+1}, B_i) forward layer k of strand i+1 is paired with
@@ -32,6 +33,7 @@
 
 #include "../planner/lane_sim.hpp"
 #include "runtime.hpp"
+#include "weft/folding_pipeline.hpp"
 
 namespace dh {
 
@@ -197,14 +199,21 @@ int lower_ops(Model& m, int mode) {
                 for (int l = L - 1; l >= 0; --l) lw.backward_layer(s, l);
             }
         } else {
-            lw.barrier();
-            for (int l = 0; l < L; ++l) lw.forward_layer(0, l);
-            for (int i = 0; i + 1 < mb; ++i) {
+            // The block order is the reference W schedule on one stage
+            // (schedule_w_pipeline(m, 1): F_1 | SI(F_{i+1}, B_i) ... | B_m, every
+            // visit spanning the whole layer stack); only its order is used.
+            const weft::PipelineSchedule ws = weft::schedule_w_pipeline(mb, 1, weft::BlockDurations{});
+            for (const auto& blk : ws.blocks) {
                 lw.barrier();
-                for (int k = 0; k < L; ++k) lw.si_layer_pair(i + 1, k, i, L - 1 - k, tbl, mode == 2);
+                if (blk.kind == weft::BlockKind::F) {
+                    for (int l = 0; l < L; ++l) lw.forward_layer(*blk.fwd_mb - 1, l);
+                } else if (blk.kind == weft::BlockKind::B) {
+                    for (int l = L - 1; l >= 0; --l) lw.backward_layer(*blk.bwd_mb - 1, l);
+                } else {
+                    for (int k = 0; k < L; ++k)
+                        lw.si_layer_pair(*blk.fwd_mb - 1, k, *blk.bwd_mb - 1, L - 1 - k, tbl, mode == 2);
+                }
             }
-            lw.barrier();
-            for (int l = L - 1; l >= 0; --l) lw.backward_layer(mb - 1, l);
         }
     } catch (const std::exception& e) {
         return set_error(DH_ERR_CONFIG, std::string("lowering: ") + e.what());
