@@ -20,6 +20,6 @@ buf = (ctypes.c_longlong * 1024)()
 dh.lib().dh_attn_trace_read(buf, 1024)
 t0 = buf[3]
 print("it mma_s_issued(it+1) mma_got_p(it) | ew: wait_s got_s ld_done bar_done math_done arrive   (cycles rel. to it0 s_full)")
-for it in range(64):
+for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 64):
     r = [buf[it * 8 + j] - t0 for j in range(8)]
     print(it, r[0], r[1], "|", r[2], r[3], r[5], r[6], r[7], r[4])
