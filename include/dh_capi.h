@@ -118,6 +118,19 @@ int dh_attn_bwd(const void* q, const void* k, const void* v, long long ldq, long
 int dh_adamw(float* master, void* weight_bf16, float* grad, float* m, float* v, long long n,
              float lr, float beta1, float beta2, float eps, float weight_decay, int step,
              float grad_scale, int zero_grad, void* stream);
+/* AdamW whose hyperparameters live in device memory (9 floats written by
+ * dh_adamw_set_hparams): capturable in a CUDA graph that replays every step.
+ * enabled == 0 turns the launch into a no-op. Gradients are zeroed after use.
+ * Same per-element math as dh_adamw with the same (lr, betas, eps, wd, step). */
+typedef struct dh_adamw_hparams {
+    float lr, beta1, beta2, eps, weight_decay;
+    float bc1, bc2;    /* 1 - beta^step, computed on the host as dh_adamw does */
+    float grad_scale;
+    int enabled;
+} dh_adamw_hparams;
+int dh_adamw_set_hparams(float* hp_dev, const dh_adamw_hparams* v, void* stream);
+int dh_adamw_dev(float* master, void* weight_bf16, float* grad, float* m, float* v, long long n,
+                 const float* hp_dev, void* stream);
 /* Deterministic normal(0, std) init of bf16 (and optional fp32 master) from (seed, offset). */
 int dh_init_normal(void* bf16_out, float* f32_out, long long n, unsigned long long seed,
                    float std_dev, void* stream);
@@ -194,6 +207,11 @@ int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_js
 int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_json,
                   const char* profile_json, int mode, char** out);
 /* Cap the SMs of GEMMs that co-run with a collective (0 = no cap). */
+/* In-program optimizer (default on): per-layer AdamW ops on the cross lane
+ * overlap the last strand's backward; only the LN gammas are updated after the
+ * program. Off: one AdamW over all parameters after the program (bitwise the
+ * same weights). Takes effect at the next dh_model_set_plan. */
+int dh_model_set_fuse_optimizer(dh_model* m, int on);
 int dh_model_set_overlap_ctas(dh_model* m, int gemm_ctas);
 
 /* Run one training step: every micro-batch forward + backward per the lowered

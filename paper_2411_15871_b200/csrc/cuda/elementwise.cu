@@ -423,6 +423,39 @@ __global__ void __launch_bounds__(256) adamw_vec4_kernel(float4* __restrict__ ma
     }
 }
 
+// Same update with the hyperparameters read from device memory
+// (dh_adamw_hparams layout), so a captured CUDA graph can run it every step;
+// hp[8] == 0 makes it a no-op (program replays without an optimizer step).
+__global__ void __launch_bounds__(256) adamw_vec4_dev_kernel(float4* __restrict__ master, uint2* __restrict__ w,
+                                                             float4* __restrict__ grad, float4* __restrict__ m,
+                                                             float4* __restrict__ v, long long n4,
+                                                             const float* __restrict__ hp) {
+    if (hp[8] == 0.f) return;
+    const float lr = hp[0], b1 = hp[1], b2 = hp[2], eps = hp[3], wd = hp[4], bc1 = hp[5], bc2 = hp[6],
+                gscale = hp[7];
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const float4 g4 = __ldcs(grad + i);
+        float4 m4 = __ldcs(m + i), v4 = __ldcs(v + i), p4 = __ldcs(master + i);
+        adamw_one(p4.x, m4.x, v4.x, g4.x * gscale, lr, b1, b2, eps, wd, bc1, bc2);
+        adamw_one(p4.y, m4.y, v4.y, g4.y * gscale, lr, b1, b2, eps, wd, bc1, bc2);
+        adamw_one(p4.z, m4.z, v4.z, g4.z * gscale, lr, b1, b2, eps, wd, bc1, bc2);
+        adamw_one(p4.w, m4.w, v4.w, g4.w * gscale, lr, b1, b2, eps, wd, bc1, bc2);
+        __stcs(m + i, m4);
+        __stcs(v + i, v4);
+        __stcs(master + i, p4);
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(p4.x, p4.y), hi = __floats2bfloat162_rn(p4.z, p4.w);
+        __stcs(w + i, make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi)));
+        __stcs(grad + i, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+}
+
+__global__ void adamw_set_hparams_kernel(float* hp, dh_adamw_hparams v) {
+    const float vals[9] = {v.lr, v.beta1, v.beta2, v.eps, v.weight_decay, v.bc1, v.bc2, v.grad_scale,
+                           static_cast<float>(v.enabled)};
+    for (int i = 0; i < 9; ++i) hp[i] = vals[i];
+}
+
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
     z += 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -697,6 +730,27 @@ int dh_adamw(float* master, void* weight_bf16, float* grad, float* m, float* v, 
         adamw_kernel<<<grid_for(n - head, 256), 256, 0, s>>>(
             master + head, static_cast<__nv_bfloat16*>(weight_bf16) + head, grad + head, m + head, v + head,
             n - head, lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale, zero_grad);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_adamw_set_hparams(float* hp_dev, const dh_adamw_hparams* v, void* stream) {
+    if (!hp_dev || !v) return dh::set_error(DH_ERR_INVALID, "adamw hparams: null argument");
+    adamw_set_hparams_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(hp_dev, *v);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_adamw_dev(float* master, void* weight_bf16, float* grad, float* m, float* v, long long n,
+                 const float* hp_dev, void* stream) {
+    if (n <= 0) return DH_OK;
+    const bool aligned = aligned16(master) && aligned16(grad) && aligned16(m) && aligned16(v) &&
+                         (reinterpret_cast<uintptr_t>(weight_bf16) & 7) == 0;
+    if (!aligned || n % 4) return dh::set_error(DH_ERR_INVALID, "adamw_dev: operands must be 16-byte aligned, n % 4 == 0");
+    const long long n4 = n / 4;
+    adamw_vec4_dev_kernel<<<grid_for(n4, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<float4*>(master), static_cast<uint2*>(weight_bf16), reinterpret_cast<float4*>(grad),
+        reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, hp_dev);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

@@ -18,6 +18,8 @@ int kernels_per_node(const Model& m, int node, int layer) {
             return 1;  // (SwiGLU fwd / bwd run inside the mlp_gate|mlp_up / mlp_down_dgrad epilogues)
         case 2: case 26: case 28: case 38:
             return 2;
+        case kOptNode:
+            return 1;
         case 4:  // attn (+ KV-split combine when the launcher splits rows)
             return m.cfg.head_dim == 128 &&
                            dh_attn_fwd_scratch_floats(m.cfg.seq, m.cfg.nq_l,
@@ -245,6 +247,12 @@ int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_js
     return DH_OK;
 }
 
+int dh_model_set_fuse_optimizer(dh_model* m, int on) {
+    if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
+    m->fuse_optimizer = on != 0;
+    return DH_OK;
+}
+
 int dh_model_set_overlap_ctas(dh_model* m, int gemm_ctas) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
     m->gemm_ctas_overlap = gemm_ctas;
@@ -262,6 +270,7 @@ int dh_model_run_program(dh_model* m, int use_graph) {
 
 int dh_model_step(dh_model* m, const dh_optim_cfg* optim, int use_graph) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
+    RT_TRY(dh::arm_optimizer(*m, optim, m->ctx->lane[0]));
     RT_TRY(dh::run_program(*m, use_graph != 0));
     return dh::run_optimizer(*m, optim, m->ctx->lane[0]);
 }

@@ -109,6 +109,27 @@ struct Lowering {
         lane_last[prog.ops[idx].lane] = idx;
     }
 
+    // AdamW of `layer` once the last strand's backward of it is done: it waits
+    // for that strand's last op (the strand runs in total order, and every
+    // gradient writer of the layer is on the compute lane ahead of it) and
+    // stays off the strand chains, so the backward continues meanwhile.
+    void emit_opt(int strand, int layer) {
+        if (!m.fuse_optimizer) return;
+        Op o;
+        o.strand = -1;
+        o.layer = layer;
+        o.node = kOptNode;
+        o.lane = kLanes - 1;
+        o.slot = -1;
+        o.prev_slot = -1;
+        o.capped = false;
+        o.waits.push_back(strand_last[strand]);
+        prog.ops.push_back(std::move(o));
+        lane_last[kLanes - 1] = static_cast<int>(prog.ops.size()) - 1;
+        has_opt = true;
+    }
+    bool has_opt = false;
+
     void take_slot(int strand, int layer) {
         slot_of[strand][layer] = free_slots.back();
         free_slots.pop_back();
@@ -196,7 +217,10 @@ int lower_ops(Model& m, int mode) {
             for (int s = 0; s < mb; ++s) {
                 lw.barrier();
                 for (int l = 0; l < L; ++l) lw.forward_layer(s, l);
-                for (int l = L - 1; l >= 0; --l) lw.backward_layer(s, l);
+                for (int l = L - 1; l >= 0; --l) {
+                    lw.backward_layer(s, l);
+                    if (s == mb - 1) lw.emit_opt(s, l);
+                }
             }
         } else {
             // The block order is the reference W schedule on one stage
@@ -208,7 +232,10 @@ int lower_ops(Model& m, int mode) {
                 if (blk.kind == weft::BlockKind::F) {
                     for (int l = 0; l < L; ++l) lw.forward_layer(*blk.fwd_mb - 1, l);
                 } else if (blk.kind == weft::BlockKind::B) {
-                    for (int l = L - 1; l >= 0; --l) lw.backward_layer(*blk.bwd_mb - 1, l);
+                    for (int l = L - 1; l >= 0; --l) {
+                        lw.backward_layer(*blk.bwd_mb - 1, l);
+                        if (*blk.bwd_mb == mb) lw.emit_opt(mb - 1, l);
+                    }
                 } else {
                     for (int k = 0; k < L; ++k)
                         lw.si_layer_pair(*blk.fwd_mb - 1, k, *blk.bwd_mb - 1, L - 1 - k, tbl, mode == 2);
@@ -220,6 +247,7 @@ int lower_ops(Model& m, int mode) {
     }
     if (lw.free_slots.size() != static_cast<std::size_t>(L + 1))
         return set_error(DH_ERR_OTHER, "lowering: activation slots leaked");
+    m.prog_has_opt = lw.has_opt;
     m.y_slot.assign(mb, -1);
     for (int s = 0; s < mb; ++s) m.y_slot[s] = lw.slot_of[s][L - 1];
     m.prog = std::move(lw.prog);

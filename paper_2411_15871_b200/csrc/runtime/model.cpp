@@ -203,6 +203,7 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         m->mb_dy.push_back(pool.take(T * H * 2, "io.inputs"));
     }
     m->loss = pool.take(std::max(k.micro_batches, 1) * 4 + 1024 * 4, "io.loss");
+    m->opt_hp = pool.take(64, "io.optim");
 
     m->pool_bytes = pool.cursor;
     RT_CUDA(cudaSetDevice(ctx->device));
@@ -431,6 +432,12 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 38:  // ln0_bwd (+ join of the attention-block skip gradient)
             return dh_rmsnorm_bwd(x_in, W + p.g0, m.ptr<float>(sl.rstd0), P(m.bs.rs_out), d_x, d_x,
                                   G + p.g0, m.ptr<float>(m.bs.ln_partial), T, H, s);
+        case kOptNode: {  // AdamW of this layer's matrices (wqkv .. wd are contiguous)
+            const size_t lo = p.wqkv, hi = op.layer + 1 < L ? m.lp[op.layer + 1].wqkv : m.n_params;
+            return dh_adamw_dev(m.ptr<float>(m.w_master) + lo, W + lo, G + lo, m.ptr<float>(m.adam_m) + lo,
+                                m.ptr<float>(m.adam_v) + lo, static_cast<long long>(hi - lo),
+                                m.ptr<float>(m.opt_hp), s);
+        }
         default:
             return set_error(DH_ERR_CONFIG, "launch_node: unknown template node " + std::to_string(op.node));
     }
@@ -444,11 +451,35 @@ int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s) {
         RT_TRY(m.ctx->comm->all_reduce_f32(m.ptr<float>(m.w_grad), m.gamma_elems, s));
     }
     if (!oc || !oc->enabled) return DH_OK;
+    // with the per-layer AdamW ops in the program only the gammas remain
+    const bool fused = m.fuse_optimizer && m.prog_has_opt;
+    const long long n = static_cast<long long>(fused ? m.gamma_elems : m.n_params);
+    RT_TRY(dh_adamw(m.ptr<float>(m.w_master), m.ptr(m.w_bf16), m.ptr<float>(m.w_grad), m.ptr<float>(m.adam_m),
+                    m.ptr<float>(m.adam_v), n, oc->lr, oc->beta1, oc->beta2, oc->eps, oc->weight_decay,
+                    m.adam_step, 1.f / k.micro_batches, 1, s));
+    if (fused) {  // disarm: a later bare program replay must not update the weights
+        dh_adamw_hparams off{};
+        RT_TRY(dh_adamw_set_hparams(m.ptr<float>(m.opt_hp), &off, s));
+    }
+    return DH_OK;
+}
+
+// Arms the in-program AdamW ops for this step (before the program runs).
+int arm_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s) {
+    if (!oc || !oc->enabled) return DH_OK;
     ++m.adam_step;
-    return dh_adamw(m.ptr<float>(m.w_master), m.ptr(m.w_bf16), m.ptr<float>(m.w_grad),
-                    m.ptr<float>(m.adam_m), m.ptr<float>(m.adam_v), static_cast<long long>(m.n_params),
-                    oc->lr, oc->beta1, oc->beta2, oc->eps, oc->weight_decay, m.adam_step,
-                    1.f / k.micro_batches, 1, s);
+    if (!(m.fuse_optimizer && m.prog_has_opt)) return DH_OK;
+    dh_adamw_hparams hp{};
+    hp.lr = oc->lr;
+    hp.beta1 = oc->beta1;
+    hp.beta2 = oc->beta2;
+    hp.eps = oc->eps;
+    hp.weight_decay = oc->weight_decay;
+    hp.bc1 = 1.f - std::pow(oc->beta1, static_cast<float>(m.adam_step));  // as dh_adamw
+    hp.bc2 = 1.f - std::pow(oc->beta2, static_cast<float>(m.adam_step));
+    hp.grad_scale = 1.f / m.cfg.micro_batches;
+    hp.enabled = 1;
+    return dh_adamw_set_hparams(m.ptr<float>(m.opt_hp), &hp, s);
 }
 
 }  // namespace dh

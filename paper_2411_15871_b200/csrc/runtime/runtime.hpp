@@ -109,6 +109,12 @@ struct LayerParams {
 
 struct Model;
 
+// Pseudo node of the lowered program: AdamW of one layer's matrices, issued on
+// the cross lane right after the last strand's backward of that layer, so the
+// optimizer overlaps the rest of the backward pass (device-side hyperparameters,
+// a no-op unless dh_model_step armed them).
+constexpr int kOptNode = 100;
+
 // One launch of the lowered schedule.
 struct Op {
     int strand = 0;   // micro-batch index
@@ -157,6 +163,9 @@ struct Model {
     cudaGraphExec_t graph = nullptr;
     int adam_step = 0;
     int gemm_ctas_overlap = 0;  // SM cap for GEMMs that co-run with a collective
+    bool fuse_optimizer = true;  // per-layer AdamW ops inside the program (kOptNode)
+    bool prog_has_opt = false;   // the lowered program contains them
+    Buf opt_hp;                   // dh_adamw_hparams as 9 floats
     std::map<int, double> solo_us;  // node id -> solo time used for lowering
     weft::OverlapTable plan_overlap;  // table the lowering replays the lane model with
     std::array<cudaEvent_t, kLanes> fork_join{};
@@ -184,6 +193,7 @@ int lower_program(Model& m, int mode);
 int kernels_per_node(const Model& m, int node, int layer);
 int run_program(Model& m, bool use_graph);
 int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s);
+int arm_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s);
 int set_probe(Model& m, int node);
 int read_probe(Model& m, double* total_ms, int* count);
 

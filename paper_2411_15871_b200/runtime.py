@@ -39,6 +39,7 @@ _SIGS = {
     "dh_model_destroy": ([c_void_p], c_int),
     "dh_model_set_plan": ([c_void_p, c_char_p, c_char_p, c_char_p, c_int], c_int),
     "dh_model_set_overlap_ctas": ([c_void_p, c_int], c_int),
+    "dh_model_set_fuse_optimizer": ([c_void_p, c_int], c_int),
     "dh_model_step": ([c_void_p, ctypes.POINTER(OptimCfg), c_int], c_int),
     "dh_model_run_program": ([c_void_p, c_int], c_int),
     "dh_model_zero_grads": ([c_void_p], c_int),
@@ -173,6 +174,10 @@ class Model:
         enc = lambda s: None if s is None else s.encode()  # noqa: E731
         check(_lib().dh_model_set_plan(self.handle, enc(plan_json), enc(profile_json),
                                        enc(cluster_json), {"si": 0, "sequential": 1, "si_relaxed": 2}[mode]))
+
+    def set_fuse_optimizer(self, on: bool):
+        """Per-layer AdamW inside the program (default); effective at the next set_plan."""
+        check(_lib().dh_model_set_fuse_optimizer(self.handle, int(on)))
 
     def set_overlap_ctas(self, n: int):
         check(_lib().dh_model_set_overlap_ctas(self.handle, n))

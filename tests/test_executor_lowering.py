@@ -9,7 +9,8 @@ through the host-only dh_lower_json entry point — no GPU needed.
     stream-order + event-wait graph;
   * SI uses L+1 slots (one more than sequential), and interleaves strands;
   * every TP rank lowers the identical collective sequence (NCCL requires it),
-    also checked across 2 gloo processes.
+    also checked across 2 gloo processes;
+  * the per-layer AdamW ops happen after every gradient writer of their layer.
 """
 import hashlib
 import json
@@ -85,7 +86,17 @@ def check_program(prog, shape, mb):
             continue
         prev_slot = ops[inst_ops[(s, l - 1)][0]]["slot"]
         assert all(ops[i]["prev_slot"] == prev_slot for i in idx)
-    return {o["slot"] for o in ops}
+    # the in-program AdamW of layer l (strand -1, node 100) runs after every
+    # strand's backward of layer l, once per layer, on the cross lane
+    opt = [i for i, o in enumerate(ops) if o["node"] == 100]
+    if opt:
+        assert sorted(ops[i]["layer"] for i in opt) == list(range(L))
+        for i in opt:
+            l = ops[i]["layer"]
+            writers = {j for j, o in enumerate(ops) if o["strand"] >= 0 and o["layer"] == l
+                       and o["node"] in prog["bwd_seq"]}
+            assert _reachable_from(preds, writers, i), f"AdamW of layer {l} may run before its gradients"
+    return {o["slot"] for o in ops if o["node"] != 100}
 
 
 @pytest.mark.parametrize("tp", [1, 2, 4, 8])
@@ -120,7 +131,8 @@ def test_tiny_programs(tp, mb):
     if tp > 1:
         comm = [o for o in si["ops"] if o["node"] in COMM_NODES]
         assert comm and all(o["lane"] == 1 for o in comm)
-        assert all(o["lane"] == 0 for o in si["ops"] if o["node"] not in COMM_NODES)
+        assert all(o["lane"] == 0 for o in si["ops"] if o["node"] not in COMM_NODES and o["node"] != 100)
+        assert all(o["lane"] == 2 for o in si["ops"] if o["node"] == 100)
 
 
 def test_llama3_8b_tp8_h100_plan_program():

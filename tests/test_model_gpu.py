@@ -135,7 +135,8 @@ def test_single_microbatch_outputs(ctx):
     assert _rel(m.tensor("dx").float().cpu().numpy().reshape(dx_ref.shape), dx_ref) < 3e-2
     info = m.info()
     assert info["slots"] == shape.layers + 1
-    assert info["program"]["ops"] == shape.layers * (10 + 14)  # tp=1: 10 fwd + 14 bwd nodes
+    # tp=1: 10 fwd + 14 bwd nodes, plus the layer's in-program AdamW op
+    assert info["program"]["ops"] == shape.layers * (10 + 14 + 1)
     m.close()
 
 
@@ -151,6 +152,26 @@ def test_optimizer_step_changes_weights(ctx):
     assert not torch.equal(w0, w1)
     assert float(m.tensor("grad.wqkv", 0).abs().max()) == 0.0  # zeroed for the next step
     m.close()
+
+
+def test_in_program_optimizer_matches_post_step_adamw(ctx):
+    """Per-layer AdamW ops overlapping the last backward give bitwise the
+    weights, master copy and moments of one AdamW after the program."""
+    shape = _tiny(mb=2, layers=2)
+    out = []
+    for fuse in (True, False):
+        orc, m, xs, rs = _build(shape, ctx)
+        m.set_fuse_optimizer(fuse)
+        m.set_plan(_plan(shape, 1), mode="si")
+        m.zero_grads()
+        for _ in range(3):
+            m.step({"lr": 1e-3, "weight_decay": 0.01}, use_graph=True)
+        m.sync()
+        out.append({f"{k}{l}": m.tensor(k, l).float().cpu().clone() for k in ("w.wqkv", "w.wd", "w.g0", "master.wd")
+                    for l in range(2)})
+        m.close()
+    for k in out[0]:
+        assert torch.equal(out[0][k], out[1][k]), k
 
 
 def test_head_dim_128_model_vs_oracle(ctx):
