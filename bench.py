@@ -234,7 +234,7 @@ def memory_vs_model(planner, info, shape):
             "transients_gb": round((info["pool_bytes"] - measured) / 1e9, 3)}
 
 
-def emulated_tp_experiment(args, tp, timed_factory, full=True):
+def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, layers=None, micro_batches=None):
     """TP=<tp> per-GPU shapes on this single GPU with emulated collectives
     (dh_ctx_create_emulated: proxy kernels on the NCCL CTA budget, held for the
     NVLink wire time at the measured 770 GB/s peer bandwidth). Measures the
@@ -251,8 +251,9 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True):
     from paper_2411_15871_b200 import planner
     from paper_2411_15871_b200.runtime import LLAMA3_8B, Context, Model
 
-    shape = copy.copy(LLAMA3_8B)
-    shape.layers, shape.micro_batches = args.layers, args.micro_batches
+    shape = copy.copy(base_shape or LLAMA3_8B)
+    shape.layers = layers or args.layers
+    shape.micro_batches = micro_batches or args.micro_batches
     link = 770.0
     ctx = Context.emulated(0, tp, args.nccl_ctas, link)
     m = Model(ctx, shape)
@@ -389,6 +390,7 @@ def main():
     ap.add_argument("--no-sequential", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1024)
     ap.add_argument("--nccl-ctas", type=int, default=16)
+    ap.add_argument("--no-configs", action="store_true", help="skip the config-3 / config-5 emulated slices")
     ap.add_argument("--emulate-tp", default="2,4,8",
                     help="at N=1 also run these TP sizes' per-GPU shapes with emulated collectives "
                          "(comma list; the largest gets every SI variant; 0 = off)")
@@ -540,6 +542,19 @@ def main():
                                                            "hidden_comm_frac", "frac_of_overlap_roofline",
                                                            "exposed_comm_us_per_layer_pair", "best_si")}
 
+    # the other BASELINE.json dense configs at their per-GPU shapes (emulated
+    # collectives, a slice of the layer stack: per-layer-pair metrics)
+    other_cfgs = {}
+    if world == 1 and tps and not args.no_configs:
+        from paper_2411_15871_b200.runtime import GPT3_13B, LLAMA2_70B
+        for name, base, tpc, nl in (("c3_gpt3_13b_tp4", GPT3_13B, 4, 8), ("c5_llama2_70b_tp4", LLAMA2_70B, 4, 4)):
+            r = emulated_tp_experiment(args, tpc, timed, full=False, base_shape=base, layers=nl, micro_batches=4)
+            other_cfgs[name] = {"layers_in_slice": nl, "micro_batches": 4,
+                                **{k: r[k] for k in ("tokens_per_s_per_gpu", "mfu", "ms_per_step", "layer_pair_us",
+                                                     "overlap_roofline_us", "frac_of_overlap_roofline",
+                                                     "hidden_comm_frac", "si_speedup_vs_sequential",
+                                                     "exposed_comm_us_per_layer_pair", "best_si")}}
+
     if rank != 0:
         if world > 1:
             del host_in, loss_host, dev_dst, loss_dev
@@ -591,6 +606,7 @@ def main():
         "clocks": clocks,
         "tp_emulated": emu,
         "tp_emulated_sweep": emu_sweep or None,
+        "tp_emulated_other_configs": other_cfgs or None,
     }
     print(json.dumps(line), flush=True)
     # torch's pinned-host allocator records events on the streams its buffers

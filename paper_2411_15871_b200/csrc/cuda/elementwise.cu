@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 // Same math, RB rows per block iteration: the RB rows' loads are all in flight
 // before the (single) block barrier that completes their RB dot products.
 template <int RB>
-__global__ void rmsnorm_bwd_rows(const uint4* __restrict__ x, const uint4* __restrict__ g,
+__global__ void __launch_bounds__(RB == 1 ? 1024 : 512) rmsnorm_bwd_rows(const uint4* __restrict__ x, const uint4* __restrict__ g,
                                  const float* __restrict__ rstd, const uint4* __restrict__ dy,
                                  const uint4* __restrict__ resid, uint4* __restrict__ dx,
                                  float* __restrict__ partial, int rows, int vec_cols, float inv_cols) {
@@ -643,12 +643,15 @@ int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const vo
         return set_error(DH_ERR_INVALID, "rmsnorm_bwd: cols % 8, cols <= 8192 and 16-byte alignment required");
     if (rows <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
-    constexpr int kRB = 4;
-    const int blocks = std::min((rows + kRB - 1) / kRB, 296);
-    rmsnorm_bwd_rows<kRB><<<blocks, cols / 8, 0, s>>>(
-        static_cast<const uint4*>(x), static_cast<const uint4*>(gamma), rstd,
-        static_cast<const uint4*>(dy), static_cast<const uint4*>(resid), static_cast<uint4*>(dx),
-        partial, rows, cols / 8, 1.f / cols);
+    // up to 4096 columns: 4 rows per barrier (512 threads); wider rows (e.g.
+    // hidden 8192 at 1024 threads) one row, within the 64-register budget
+    const bool wide = cols / 8 > 512;
+    const int rb = wide ? 1 : 4;
+    const int blocks = std::min((rows + rb - 1) / rb, 296);
+    auto kern = wide ? rmsnorm_bwd_rows<1> : rmsnorm_bwd_rows<4>;
+    kern<<<blocks, cols / 8, 0, s>>>(static_cast<const uint4*>(x), static_cast<const uint4*>(gamma), rstd,
+                                      static_cast<const uint4*>(dy), static_cast<const uint4*>(resid),
+                                      static_cast<uint4*>(dx), partial, rows, cols / 8, 1.f / cols);
     DH_CUDA_CHECK(cudaGetLastError());
     if (dgamma_acc) {
         column_reduce_add<<<(cols + 31) / 32, 256, 0, s>>>(partial, dgamma_acc, blocks, cols);

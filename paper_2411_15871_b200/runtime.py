@@ -158,6 +158,13 @@ LLAMA3_8B = LlamaShape(hidden=4096, ffn=14336, n_heads=32, n_kv_heads=8, head_di
                        seq_len=4096, rope_theta=500000.0)
 TINY = LlamaShape(hidden=256, ffn=768, n_heads=4, n_kv_heads=2, head_dim=64, layers=4, seq_len=128,
                   rope_theta=10000.0)
+# BASELINE.json config 3 (GPT-3-13B-shaped: MHA, 40 x 128 heads; the dense_tp_sp
+# template models every non-MoE family with a gated MLP, reference op_model.cpp:409)
+GPT3_13B = LlamaShape(hidden=5120, ffn=20480, n_heads=40, n_kv_heads=40, head_dim=128, layers=40,
+                      seq_len=2048, rope_theta=10000.0)
+# BASELINE.json config 5 (Llama-2-70B-shaped, GQA 64 / 8 heads)
+LLAMA2_70B = LlamaShape(hidden=8192, ffn=28672, n_heads=64, n_kv_heads=8, head_dim=128, layers=80,
+                        seq_len=8192, rope_theta=10000.0)
 
 
 class Model:

@@ -65,7 +65,7 @@ def test_gemm_capped_ctas():
         assert _rel(d, A.float() @ B.float().t()) < 4e-3
 
 
-@pytest.mark.parametrize("cols", [256, 512, 4096, 1000 * 8 // 8 + 8])
+@pytest.mark.parametrize("cols", [256, 512, 4096, 1000 * 8 // 8 + 8, 5120, 8192])
 def test_rmsnorm_fwd_bwd(cols):
     rows, eps = 777, 1e-5
     x = torch.randn(rows, cols, device="cuda", dtype=torch.bfloat16)
