@@ -157,6 +157,10 @@ typedef struct dh_model dh_model;
  * strand's GEMMs (north star (2)). Streams: one per weft::Lane. */
 int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_id,
                   int nccl_max_ctas, dh_ctx** out);
+/* Single-process pipeline group on ONE device (test backend): pp_size stage
+ * contexts (TP = 1) whose point-to-point activation / gradient transfers are
+ * staged device copies matched in program order (never blocking the sender). */
+int dh_loopback_pp_group_create(int device, int pp_size, dh_ctx** ctxs_out);
 /* Single-process multi-rank "loopback" group on ONE device (test backend):
  * creates tp_size contexts whose AllGather / ReduceScatter are device copies
  * plus a fixed-order sum. Each context must be driven by its own host thread
@@ -177,6 +181,12 @@ typedef struct dh_model_cfg {
     float rope_theta, norm_eps;
     unsigned long long seed;
     float init_std;
+    /* Pipeline stage (zero = single stage, the defaults): `layers` are this
+     * stage's layers of the U-fold (weft fold_layers), `split_layer` the local
+     * index where the way-back half starts (its input arrives from the next
+     * stage, 0 = contiguous), `slots` the activation slots (0 = layers + 1;
+     * pipelined micro-batches need more), pp_rank / pp_size the stage. */
+    int slots, split_layer, pp_rank, pp_size;
 } dh_model_cfg;
 
 typedef struct dh_optim_cfg {
@@ -198,6 +208,8 @@ int dh_model_destroy(dh_model* m);
  * the plan's per-strand operator orders; 2 = SI with relaxed steps (same per-lane
  * issue order, lanes joined only at layer-pair boundaries). plan_json NULL =
  * template order, one segment per pass (valid for mode 1 and as a trivial SI plan). */
+/* mode 3: W pipeline stage (weft schedule_w_pipeline(micro_batches, pp_size) blocks of
+ * this pp_rank; SI visits pair the plan's steps as mode 0). */
 int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
                       const char* cluster_json, int mode);
 /* Host-only lowering (no GPU needed): the launch program dh_model_set_plan would

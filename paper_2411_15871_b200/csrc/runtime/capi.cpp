@@ -20,6 +20,8 @@ int kernels_per_node(const Model& m, int node, int layer) {
             return 2;
         case kOptNode:
             return 1;
+        case kSendAct: case kRecvAct: case kSendGrad: case kRecvGrad:
+            return 0;  // staged device copies
         case 4:  // attn (+ KV-split combine when the launcher splits rows)
             return m.cfg.head_dim == 128 &&
                            dh_attn_fwd_scratch_floats(m.cfg.seq, m.cfg.nq_l,
@@ -217,8 +219,11 @@ int dh_model_destroy(dh_model* m) {
 int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
                       const char* cluster_json, int mode) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
-    if (mode < 0 || mode > 2)
-        return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI), 1 (sequential) or 2 (SI, relaxed steps)");
+    if (mode < 0 || mode > 3)
+        return dh::set_error(DH_ERR_INVALID,
+                             "mode must be 0 (SI), 1 (sequential), 2 (SI, relaxed steps) or 3 (W pipeline stage)");
+    if (mode == 3 && m->cfg.pp_size != m->ctx->pp_size)
+        return dh::set_error(DH_ERR_CONFIG, "w_pipeline: dh_model_cfg.pp_size differs from the context's stage group");
     RT_TRY(dh::configure_plan(*m, plan_json, profile_json, cluster_json));
     return dh::lower_program(*m, mode);
 }
@@ -226,8 +231,9 @@ int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_js
 int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_json,
                   const char* profile_json, int mode, char** out) {
     if (!cfg || !out) return dh::set_error(DH_ERR_INVALID, "null argument");
-    if (mode < 0 || mode > 2)
-        return dh::set_error(DH_ERR_INVALID, "mode must be 0 (SI), 1 (sequential) or 2 (SI, relaxed steps)");
+    if (mode < 0 || mode > 3)
+        return dh::set_error(DH_ERR_INVALID,
+                             "mode must be 0 (SI), 1 (sequential), 2 (SI, relaxed steps) or 3 (W pipeline stage)");
     dh::Model m;  // host-only: no context, no pool
     RT_TRY(dh::derive_cfg(cfg, tp, rank, &m.cfg));
     RT_TRY(dh::build_dags(m, dh::default_cluster(), nullptr));
@@ -237,9 +243,9 @@ int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_js
     for (const auto& o : m.prog.ops) {
         ops.push_back({{"strand", o.strand}, {"layer", o.layer}, {"node", o.node}, {"lane", o.lane},
                        {"slot", o.slot}, {"prev_slot", o.prev_slot}, {"first_dx", o.first_dx},
-                       {"waits", o.waits}});
+                       {"peer", o.peer}, {"waits", o.waits}});
     }
-    json j = {{"ops", ops}, {"slots", m.cfg.layers + 1}, {"fwd_seq", m.plan.fwd_seq},
+    json j = {{"ops", ops}, {"slots", m.cfg.slots > 0 ? m.cfg.slots : m.cfg.layers + 1}, {"fwd_seq", m.plan.fwd_seq},
               {"bwd_seq", m.plan.bwd_seq}, {"mode", mode}};
     const std::string s = j.dump();
     *out = static_cast<char*>(std::malloc(s.size() + 1));

@@ -18,7 +18,10 @@
 
 #include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "runtime.hpp"
 
@@ -215,6 +218,70 @@ public:
 
 }  // namespace
 
+// ------------------------------------------------------------------ loopback pipeline transfers
+
+// One mailbox per (src stage, dst stage, tag). A send copies the payload into
+// a private staging buffer on the sender's stream and posts it with an event;
+// the matching recv (program order) waits for that event, copies out and frees
+// the staging buffer on its own stream. Sends never wait for the receiver, so
+// any schedule whose transfers follow its data dependencies cannot deadlock.
+struct P2PGroup {
+    std::mutex mu;
+    std::condition_variable cv;
+    struct Msg {
+        void* staging;
+        size_t bytes;
+        cudaEvent_t ready;
+    };
+    std::map<std::tuple<int, int, int>, std::deque<Msg>> box;  // (src, dst, tag)
+};
+
+namespace {
+
+class LoopbackP2P final : public Comm {
+public:
+    LoopbackP2P(std::shared_ptr<P2PGroup> g, int r) : g_(std::move(g)), rank_(r) {}
+    int all_gather(const void*, void*, size_t, cudaStream_t) override { return unsupported(); }
+    int reduce_scatter(const void*, void*, size_t, cudaStream_t) override { return unsupported(); }
+    int all_reduce_f32(float*, size_t, cudaStream_t) override { return unsupported(); }
+    int send(const void* buf, size_t bytes, int peer, int tag, cudaStream_t s) override {
+        P2PGroup::Msg msg{nullptr, bytes, nullptr};
+        RT_CUDA(cudaMallocAsync(&msg.staging, bytes, s));
+        RT_CUDA(cudaMemcpyAsync(msg.staging, buf, bytes, cudaMemcpyDeviceToDevice, s));
+        RT_CUDA(cudaEventCreateWithFlags(&msg.ready, cudaEventDisableTiming));
+        RT_CUDA(cudaEventRecord(msg.ready, s));
+        std::lock_guard<std::mutex> lk(g_->mu);
+        g_->box[{rank_, peer, tag}].push_back(msg);
+        g_->cv.notify_all();
+        return DH_OK;
+    }
+    int recv(void* buf, size_t bytes, int peer, int tag, cudaStream_t s) override {
+        P2PGroup::Msg msg;
+        {
+            std::unique_lock<std::mutex> lk(g_->mu);
+            auto& q = g_->box[{peer, rank_, tag}];
+            g_->cv.wait(lk, [&] { return !q.empty(); });
+            msg = q.front();
+            q.pop_front();
+        }
+        if (msg.bytes != bytes) return set_error(DH_ERR_OTHER, "pipeline transfer: size mismatch between stages");
+        RT_CUDA(cudaStreamWaitEvent(s, msg.ready, 0));
+        RT_CUDA(cudaEventDestroy(msg.ready));
+        RT_CUDA(cudaMemcpyAsync(buf, msg.staging, bytes, cudaMemcpyDeviceToDevice, s));
+        RT_CUDA(cudaFreeAsync(msg.staging, s));
+        return DH_OK;
+    }
+    bool capturable() const override { return false; }
+    const char* name() const override { return "loopback_p2p"; }
+
+private:
+    int unsupported() { return set_error(DH_ERR_CONFIG, "loopback_p2p: pipeline transfers only"); }
+    std::shared_ptr<P2PGroup> g_;
+    int rank_;
+};
+
+}  // namespace
+
 std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* group, int rank, int* rc) {
     auto c = std::make_unique<LoopbackComm>(group, rank);
     if (cudaEventCreateWithFlags(&group->ready[rank], cudaEventDisableTiming) != cudaSuccess ||
@@ -295,6 +362,22 @@ int dh_ctx_create_emulated(int device, int tp_size, int comm_ctas, double link_g
     }
     c->comm = std::make_unique<dh::EmulatedComm>(tp_size, comm_ctas > 0 ? comm_ctas : 16, link_gbs);
     *out = c;
+    return DH_OK;
+}
+
+int dh_loopback_pp_group_create(int device, int pp_size, dh_ctx** ctxs_out) {
+    if (pp_size < 1 || !ctxs_out) return dh::set_error(DH_ERR_INVALID, "loopback pp: bad size");
+    auto g = std::make_shared<dh::P2PGroup>();
+    for (int r = 0; r < pp_size; ++r) {
+        auto* c = new dh_ctx();
+        c->device = device;
+        c->pp_rank = r;
+        c->pp_size = pp_size;
+        const int rc = init_streams(c);
+        if (rc != DH_OK) return rc;
+        if (pp_size > 1) c->pp = std::make_unique<dh::LoopbackP2P>(g, r);
+        ctxs_out[r] = c;
+    }
     return DH_OK;
 }
 

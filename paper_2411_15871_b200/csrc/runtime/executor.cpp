@@ -39,6 +39,8 @@ namespace dh {
 
 namespace {
 
+int n_slots(const Model& m) { return m.cfg.slots > 0 ? m.cfg.slots : m.cfg.layers + 1; }
+
 struct Lowering {
     Model& m;
     Program prog;
@@ -54,7 +56,7 @@ struct Lowering {
         const int mb = m.cfg.micro_batches, L = m.cfg.layers;
         strand_last.assign(mb, -1);
         slot_of.assign(mb, std::vector<int>(L, -1));
-        for (int s = L; s >= 0; --s) free_slots.push_back(s);  // pop_back gives 0 first
+        for (int s = n_slots(m) - 1; s >= 0; --s) free_slots.push_back(s);  // pop_back gives 0 first
         for (const auto& n : m.fwd_dag.nodes) lane_of[n.id] = static_cast<int>(n.lane);
         for (const auto& n : m.bwd_dag.nodes) lane_of[n.id] = static_cast<int>(n.lane);
         for (std::size_t i = 0; i < m.plan.bwd_seq.size(); ++i) pos_in_bwd[m.plan.bwd_seq[i]] = static_cast<int>(i);
@@ -71,25 +73,31 @@ struct Lowering {
     // every SM; inside a block the cap applies wherever a collective may co-run.
     bool capped = false;
 
-    void emit(int strand, int layer, int node) {
+    void emit(int strand, int layer, int node, int peer = -1) {
+        const bool xfer = node >= kSendAct && node <= kRecvGrad;
         // compute-only measurement program: collectives are left out entirely
-        if (m.skip_comm && lane_of.at(node) != 0) return;
+        if (m.skip_comm && !xfer && lane_of.at(node) != 0) return;
         Op o;
         o.strand = strand;
         o.layer = layer;
         o.node = node;
-        o.lane = lane_of.at(node);
+        o.peer = peer;
+        // pipeline transfers are stream-ordered copies on the compute lane: the
+        // running-gradient buffer they read is rewritten by the next backward op
+        o.lane = xfer ? 0 : lane_of.at(node);
         o.slot = slot_of[strand][layer];
         o.prev_slot = layer > 0 ? slot_of[strand][layer - 1] : -1;
         o.capped = capped;
-        if (node == 10 || node == 11) {
+        if (xfer) {
+            // nothing node-specific
+        } else if (node == 10 || node == 11) {
             // both run on the compute lane in sequence order: the later one sees the
             // other's output and applies SwiGLU in its GEMM epilogue
             const int other = node == 10 ? 11 : 10;
             o.fuse_swiglu = pos_in_fwd.at(node) > pos_in_fwd.at(other) &&
                             lane_of.at(node) == lane_of.at(other);
         }
-        if (node == 24 || node == 25) {
+        if (!xfer && (node == 24 || node == 25)) {
             const int other = node == 24 ? 25 : 24;
             o.first_dx = pos_in_bwd.at(node) < pos_in_bwd.at(other);
         }
@@ -131,6 +139,8 @@ struct Lowering {
     bool has_opt = false;
 
     void take_slot(int strand, int layer) {
+        if (free_slots.empty())
+            throw std::runtime_error("not enough activation slots for this schedule (dh_model_cfg.slots)");
         slot_of[strand][layer] = free_slots.back();
         free_slots.pop_back();
     }
@@ -164,6 +174,10 @@ struct Lowering {
     // two strands touch disjoint buffers, so the per-strand event edges suffice.
     void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl, bool relaxed) {
         take_slot(fs, lf);
+        if (pending_recv_act.first == fs) {
+            emit(fs, lf, kRecvAct, pending_recv_act.second);
+            pending_recv_act = {-1, -1};
+        }
         bool first_step = true;
         for (const auto& st : m.plan.plan.steps) {
             const auto fa = segment(m.plan.fwd_segmentation, st.fwd_seg.value_or(0));
@@ -202,6 +216,61 @@ struct Lowering {
         give_slot(bs, lb);
         capped = false;
     }
+
+    // ---- W pipeline stage (mode 3)
+    // Local layers [0, c) are the way-down half and [c, L) the way-back half of
+    // this stage's U-fold share (the last stage's two halves are contiguous and
+    // visited at once). Transfers cross to the neighbour on the weft u_path.
+    struct Visit {
+        int lo, hi;         // forward span [lo, hi); the backward span is its mirror
+        int peer_in, peer_out;  // -1: global first / last layer (no transfer)
+    };
+    Visit visit_of(const weft::Block& b) const {
+        const int L = m.cfg.layers, c = L / 2, d = m.cfg.pp_rank, p = m.cfg.pp_size;
+        Visit v;
+        if (b.half_stages == 2) {  // turn (last stage), or the whole pass at p = 1
+            v = {0, L, p > 1 ? d - 1 : -1, p > 1 ? d - 1 : -1};
+        } else if (b.half == weft::HalfDir::down) {
+            v = {0, c, d > 0 ? d - 1 : -1, d + 1};
+        } else {
+            v = {c, L, d + 1, d > 0 ? d - 1 : -1};
+        }
+        return v;
+    }
+    void fwd_visit(int strand, const Visit& v) {
+        take_slot(strand, v.lo);
+        if (v.peer_in >= 0) emit(strand, v.lo, kRecvAct, v.peer_in);
+        for (int id : m.plan.fwd_seq) emit(strand, v.lo, id);
+        for (int l = v.lo + 1; l < v.hi; ++l) forward_layer(strand, l);
+        if (v.peer_out >= 0) emit(strand, v.hi - 1, kSendAct, v.peer_out);
+    }
+    // backward span: mirror of the forward span (layers L-1-k for k in [lo, hi))
+    void bwd_visit(int strand, const Visit& v, bool last_strand) {
+        const int L = m.cfg.layers;
+        const int top = L - 1 - v.lo, bottom = L - v.hi;
+        if (v.peer_in >= 0) emit(strand, top, kRecvGrad, v.peer_in);
+        for (int l = top; l >= bottom; --l) {
+            backward_layer(strand, l);
+            if (last_strand) emit_opt(strand, l);
+        }
+        if (v.peer_out >= 0) emit(strand, bottom, kSendGrad, v.peer_out);
+    }
+    void si_visit(int fs, int bs, const Visit& v, const weft::OverlapTable& tbl, bool relaxed) {
+        const int L = m.cfg.layers;
+        if (v.peer_in >= 0) {
+            // the forward strand's first slot is taken by its first layer pair
+            emit(bs, L - 1 - v.lo, kRecvGrad, v.peer_in);
+        }
+        for (int k = v.lo; k < v.hi; ++k) {
+            if (k == v.lo && v.peer_in >= 0) pending_recv_act = {fs, v.peer_in};
+            si_layer_pair(fs, k, bs, L - 1 - k, tbl, relaxed);
+        }
+        if (v.peer_out >= 0) {
+            emit(fs, v.hi - 1, kSendAct, v.peer_out);
+            emit(bs, L - v.hi, kSendGrad, v.peer_out);
+        }
+    }
+    std::pair<int, int> pending_recv_act{-1, -1};  // (strand, peer) to receive right after a slot take
 };
 
 }  // namespace
@@ -220,6 +289,24 @@ int lower_ops(Model& m, int mode) {
                 for (int l = L - 1; l >= 0; --l) {
                     lw.backward_layer(s, l);
                     if (s == mb - 1) lw.emit_opt(s, l);
+                }
+            }
+        } else if (mode == 3) {
+            const int p = m.cfg.pp_size, d = m.cfg.pp_rank;
+            if (L % 2 || m.cfg.split != (d + 1 < p ? L / 2 : 0))
+                return set_error(DH_ERR_CONFIG, "w_pipeline: a stage holds an even number of layers, split at L/2 "
+                                                "except on the last stage");
+            const weft::PipelineSchedule ws = weft::schedule_w_pipeline(mb, p, weft::BlockDurations{});
+            for (const auto& blk : ws.blocks) {
+                if (blk.device != d) continue;
+                lw.barrier();
+                const auto v = lw.visit_of(blk);
+                if (blk.kind == weft::BlockKind::F) {
+                    lw.fwd_visit(*blk.fwd_mb - 1, v);
+                } else if (blk.kind == weft::BlockKind::B) {
+                    lw.bwd_visit(*blk.bwd_mb - 1, v, *blk.bwd_mb == mb);
+                } else {
+                    lw.si_visit(*blk.fwd_mb - 1, *blk.bwd_mb - 1, v, tbl, false);
                 }
             }
         } else {
@@ -245,7 +332,7 @@ int lower_ops(Model& m, int mode) {
     } catch (const std::exception& e) {
         return set_error(DH_ERR_CONFIG, std::string("lowering: ") + e.what());
     }
-    if (lw.free_slots.size() != static_cast<std::size_t>(L + 1))
+    if (lw.free_slots.size() != static_cast<std::size_t>(n_slots(m)))
         return set_error(DH_ERR_OTHER, "lowering: activation slots leaked");
     m.prog_has_opt = lw.has_opt;
     m.y_slot.assign(mb, -1);

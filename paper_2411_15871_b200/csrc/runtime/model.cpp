@@ -63,8 +63,14 @@ int derive_cfg(const dh_model_cfg* c, int tp, int rank, ModelCfg* out) {
     k.eps = c->norm_eps;
     k.seed = c->seed;
     k.init_std = c->init_std;
+    k.slots = c->slots;
+    k.split = c->split_layer;
+    k.pp_rank = c->pp_rank;
+    k.pp_size = c->pp_size > 0 ? c->pp_size : 1;
     k.tp = tp;
     k.rank = rank;
+    if (k.split < 0 || k.split >= c->layers || k.slots < 0 || k.pp_rank < 0 || k.pp_rank >= k.pp_size)
+        return set_error(DH_ERR_CONFIG, "model: bad pipeline stage fields (split_layer, slots, pp_rank/pp_size)");
     if (k.hidden <= 0 || k.layers <= 0 || k.seq <= 0 || k.micro_batches < 1 || k.head_dim <= 0 ||
         k.n_heads <= 0 || k.n_kv_heads <= 0 || tp < 1)
         return set_error(DH_ERR_CONFIG, "model: dimensions must be positive");
@@ -162,7 +168,7 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     m->adam_m = pool.take(off * 4, "state.adam_m");
     m->adam_v = pool.take(off * 4, "state.adam_v");
 
-    m->slots.resize(L + 1);
+    m->slots.resize(k.slots > 0 ? k.slots : L + 1);
     for (auto& s : m->slots) {
         s.out = pool.take(T * H * 2, "act.slots");
         s.rstd0 = pool.take(T * 4, "act.slots");
@@ -201,6 +207,10 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     for (int i = 0; i < k.micro_batches; ++i) {
         m->mb_in.push_back(pool.take(T * H * 2, "io.inputs"));
         m->mb_dy.push_back(pool.take(T * H * 2, "io.inputs"));
+        if (k.split > 0) {
+            m->mid_in.push_back(pool.take(T * H * 2, "io.stage"));
+            m->mid_dy.push_back(pool.take(T * H * 2, "io.stage"));
+        }
     }
     m->loss = pool.take(std::max(k.micro_batches, 1) * 4 + 1024 * 4, "io.loss");
     m->opt_hp = pool.take(64, "io.optim");
@@ -285,6 +295,13 @@ int gemm(const void* a, long long lda, bool a_mn, const void* b, long long ldb, 
 
 }  // namespace
 
+// Transfer tag: activations and gradients of a micro-batch travel on separate
+// channels (a stage may send one before it receives the other).
+int xfer_tag(const Op& op) {
+    const bool act = op.node == kSendAct || op.node == kRecvAct;
+    return (act ? 0 : 1) + 2 * op.strand;
+}
+
 int launch_node(Model& m, const Op& op, cudaStream_t s) {
     const ModelCfg& k = m.cfg;
     const int H = k.hidden, S = k.seq, T = k.tok_loc, Q = k.qkv_n, A = k.attn_n, F = k.ffn_l;
@@ -292,16 +309,25 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
     const long long TH = static_cast<long long>(T) * H;
     const bool tp1 = k.tp == 1;
     const int cap = op.capped ? m.gemm_ctas_overlap : 0;
-    Slot& sl = m.slots[op.slot];
+    Slot& sl = m.slots[op.slot < 0 ? 0 : op.slot];  // (optimizer ops own no slot)
     const LayerParams& p = m.lp[op.layer];
     auto* W = m.ptr<__nv_bfloat16>(m.w_bf16);
     auto* G = m.ptr<float>(m.w_grad);
     auto P = [&](const Buf& b) { return m.ptr(b); };
-    void* x_in = op.prev_slot < 0 ? P(m.mb_in[op.strand]) : P(m.slots[op.prev_slot].out);
+    // a split stage's way-back half starts from the activation the next stage sent
+    // (strand -1: the per-layer optimizer op, which reads no activations)
+    const bool act = op.strand >= 0;
+    void* x_in = !act                                   ? nullptr
+                 : k.split > 0 && op.layer == k.split   ? P(m.mid_in[op.strand])
+                 : op.prev_slot < 0                     ? P(m.mb_in[op.strand])
+                                                        : P(m.slots[op.prev_slot].out);
     const float scale = 1.f / std::sqrt(static_cast<float>(D));
     // backward running-gradient ping-pong (see header of executor.cpp)
     const int L = k.layers;
-    void* dy = op.layer == L - 1 ? P(m.mb_dy[op.strand]) : P(m.bs.grad[(L - 2 - op.layer) & 1]);
+    void* dy = !act                                      ? nullptr
+               : op.layer == L - 1                         ? P(m.mb_dy[op.strand])
+               : k.split > 0 && op.layer == k.split - 1    ? P(m.mid_dy[op.strand])
+                                                           : P(m.bs.grad[(L - 2 - op.layer) & 1]);
     void* d_x = P(m.bs.grad[(L - 1 - op.layer) & 1]);
     Comm* comm = m.ctx->comm.get();
     auto need_comm = [&]() -> int {
@@ -432,6 +458,21 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 38:  // ln0_bwd (+ join of the attention-block skip gradient)
             return dh_rmsnorm_bwd(x_in, W + p.g0, m.ptr<float>(sl.rstd0), P(m.bs.rs_out), d_x, d_x,
                                   G + p.g0, m.ptr<float>(m.bs.ln_partial), T, H, s);
+        case kSendAct:  // output of this visit's last layer -> next stage
+            return m.ctx->pp ? m.ctx->pp->send(P(m.slots[op.slot].out), TH * 2, op.peer, xfer_tag(op), s)
+                             : set_error(DH_ERR_CONFIG, "pipeline transfer without a stage group");
+        case kRecvAct:  // input of this visit's first layer
+            return m.ctx->pp ? m.ctx->pp->recv(k.split > 0 && op.layer == k.split ? P(m.mid_in[op.strand])
+                                                                                 : P(m.mb_in[op.strand]),
+                                               TH * 2, op.peer, xfer_tag(op), s)
+                             : set_error(DH_ERR_CONFIG, "pipeline transfer without a stage group");
+        case kSendGrad:  // input gradient of this visit's lowest layer -> previous stage
+            return m.ctx->pp ? m.ctx->pp->send(d_x, TH * 2, op.peer, xfer_tag(op), s)
+                             : set_error(DH_ERR_CONFIG, "pipeline transfer without a stage group");
+        case kRecvGrad:  // dL/d(output) of this visit's top layer
+            return m.ctx->pp ? m.ctx->pp->recv(op.layer == L - 1 ? P(m.mb_dy[op.strand]) : P(m.mid_dy[op.strand]),
+                                               TH * 2, op.peer, xfer_tag(op), s)
+                             : set_error(DH_ERR_CONFIG, "pipeline transfer without a stage group");
         case kOptNode: {  // AdamW of this layer's matrices (wqkv .. wd are contiguous)
             const size_t lo = p.wqkv, hi = op.layer + 1 < L ? m.lp[op.layer + 1].wqkv : m.n_params;
             return dh_adamw_dev(m.ptr<float>(m.w_master) + lo, W + lo, G + lo, m.ptr<float>(m.adam_m) + lo,

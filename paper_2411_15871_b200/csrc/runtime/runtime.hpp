@@ -50,6 +50,14 @@ public:
     // recv = sum over ranks of send[rank*count .. (rank+1)*count) (bf16)
     virtual int reduce_scatter(const void* send, void* recv, size_t count, cudaStream_t s) = 0;
     virtual int all_reduce_f32(float* buf, size_t count, cudaStream_t s) = 0;
+    // point-to-point (pipeline stages): a recv matches the send with the same
+    // (peer pair, tag); the two stages may issue different tags in different orders
+    virtual int send(const void* buf, size_t bytes, int peer, int tag, cudaStream_t s) {
+        return set_error(DH_ERR_CONFIG, std::string(name()) + ": no point-to-point transfers");
+    }
+    virtual int recv(void* buf, size_t bytes, int peer, int tag, cudaStream_t s) {
+        return set_error(DH_ERR_CONFIG, std::string(name()) + ": no point-to-point transfers");
+    }
     virtual bool capturable() const = 0;
     virtual const char* name() const = 0;
 };
@@ -65,6 +73,8 @@ struct Ctx {
     int comm_ctas = 0;
     std::array<cudaStream_t, kLanes> lane{};
     std::unique_ptr<Comm> comm;
+    std::unique_ptr<Comm> pp;  // pipeline-stage transfers (weft SendRecv, cross lane)
+    int pp_rank = 0, pp_size = 1;
     int sm_count = 148;
 };
 
@@ -73,6 +83,7 @@ struct Ctx {
 struct ModelCfg {
     int hidden = 0, ffn = 0, n_heads = 0, n_kv_heads = 0, head_dim = 0, layers = 0, seq = 0;
     int micro_batches = 2;
+    int slots = 0, split = 0, pp_rank = 0, pp_size = 1;  // pipeline stage (dh_model_cfg)
     float rope_theta = 500000.f, eps = 1e-5f;
     unsigned long long seed = 1234;
     float init_std = 0.02f;
@@ -114,6 +125,9 @@ struct Model;
 // optimizer overlaps the rest of the backward pass (device-side hyperparameters,
 // a no-op unless dh_model_step armed them).
 constexpr int kOptNode = 100;
+// Pipeline transfers of one (strand, layer): the activation leaving / entering
+// a visit and the gradient leaving / entering it (peer = Op::peer).
+constexpr int kSendAct = 101, kRecvAct = 102, kSendGrad = 103, kRecvGrad = 104;
 
 // One launch of the lowered schedule.
 struct Op {
@@ -128,6 +142,7 @@ struct Op {
     std::vector<int> waits;  // indices of ops whose completion this op waits for
     bool barrier = false;    // step barrier before this op (all lanes joined)
     bool capped = true;      // GEMMs may co-run with a collective: limit them to gemm_ctas_overlap SMs
+    int peer = -1;           // pipeline transfers: the other stage
 };
 
 struct Program {
@@ -153,6 +168,7 @@ struct Model {
     FwdScratch fs;
     BwdScratch bs;
     std::vector<Buf> mb_in, mb_dy;  // per micro-batch: input x0 and dL/dy (SP shards)
+    std::vector<Buf> mid_in, mid_dy;  // split stage: input of the way-back half / dy of the way-down half
     Buf loss;                       // fp32 [micro_batches]
     // schedule
     weft::LayerDag fwd_dag, bwd_dag;

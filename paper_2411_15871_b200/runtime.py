@@ -20,7 +20,8 @@ class ModelCfg(ctypes.Structure):
     _fields_ = [("hidden", c_int), ("ffn", c_int), ("n_heads", c_int), ("n_kv_heads", c_int),
                 ("head_dim", c_int), ("layers", c_int), ("seq_len", c_int),
                 ("micro_batches", c_int), ("rope_theta", c_float), ("norm_eps", c_float),
-                ("seed", ctypes.c_ulonglong), ("init_std", c_float)]
+                ("seed", ctypes.c_ulonglong), ("init_std", c_float),
+                ("slots", c_int), ("split_layer", c_int), ("pp_rank", c_int), ("pp_size", c_int)]
 
 
 class OptimCfg(ctypes.Structure):
@@ -31,6 +32,7 @@ class OptimCfg(ctypes.Structure):
 _SIGS = {
     "dh_ctx_create": ([c_int, c_int, c_int, c_void_p, c_int, ctypes.POINTER(c_void_p)], c_int),
     "dh_loopback_group_create": ([c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
+    "dh_loopback_pp_group_create": ([c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
     "dh_ctx_create_emulated": ([c_int, c_int, c_int, ctypes.c_double, ctypes.POINTER(c_void_p)], c_int),
     "dh_ctx_destroy": ([c_void_p], c_int),
     "dh_ctx_stream": ([c_void_p, c_int], c_void_p),
@@ -107,6 +109,13 @@ class Context:
         return cls(h, tp_rank, tp_size)
 
     @classmethod
+    def loopback_pp_group(cls, device=0, pp_size=2):
+        """pp_size pipeline-stage contexts on one device (staged-copy transfers)."""
+        arr = (c_void_p * pp_size)()
+        check(_lib().dh_loopback_pp_group_create(device, pp_size, arr))
+        return [cls(c_void_p(arr[r]), 0, 1) for r in range(pp_size)]
+
+    @classmethod
     def loopback_group(cls, device=0, tp_size=2):
         arr = (c_void_p * tp_size)()
         check(_lib().dh_loopback_group_create(device, tp_size, arr))
@@ -143,11 +152,17 @@ class LlamaShape:
     norm_eps: float = 1e-5
     seed: int = 1234
     init_std: float = 0.02
+    # pipeline stage (dh_model_cfg): 0 = single stage
+    slots: int = 0
+    split_layer: int = 0
+    pp_rank: int = 0
+    pp_size: int = 0
 
     def to_c(self) -> ModelCfg:
         return ModelCfg(self.hidden, self.ffn, self.n_heads, self.n_kv_heads, self.head_dim,
                         self.layers, self.seq_len, self.micro_batches, self.rope_theta,
-                        self.norm_eps, self.seed, self.init_std)
+                        self.norm_eps, self.seed, self.init_std, self.slots, self.split_layer,
+                        self.pp_rank, self.pp_size)
 
     def planner_model(self) -> dict:
         return {"name": "llama", "family": "llama", "hidden": self.hidden,
@@ -180,7 +195,8 @@ class Model:
                  cluster_json: str | None = None, mode: str = "si"):
         enc = lambda s: None if s is None else s.encode()  # noqa: E731
         check(_lib().dh_model_set_plan(self.handle, enc(plan_json), enc(profile_json),
-                                       enc(cluster_json), {"si": 0, "sequential": 1, "si_relaxed": 2}[mode]))
+                                       enc(cluster_json), {"si": 0, "sequential": 1, "si_relaxed": 2,
+                                                             "w_pipeline": 3}[mode]))
 
     def set_fuse_optimizer(self, on: bool):
         """Per-layer AdamW inside the program (default); effective at the next set_plan."""
@@ -250,7 +266,7 @@ def lower(shape: "LlamaShape", tp: int, plan_json: str | None, mode: str = "si",
     p = c_void_p()
     enc = lambda s: None if s is None else s.encode()  # noqa: E731
     check(_lib().dh_lower_json(ctypes.byref(cfg), tp, rank, enc(plan_json), enc(profile_json),
-                               {"si": 0, "sequential": 1, "si_relaxed": 2}[mode], ctypes.byref(p)))
+                               {"si": 0, "sequential": 1, "si_relaxed": 2, "w_pipeline": 3}[mode], ctypes.byref(p)))
     return json.loads(_take_string(p))
 
 
