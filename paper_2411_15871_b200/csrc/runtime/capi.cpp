@@ -245,7 +245,8 @@ int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_js
                        {"slot", o.slot}, {"prev_slot", o.prev_slot}, {"first_dx", o.first_dx},
                        {"peer", o.peer}, {"waits", o.waits}});
     }
-    json j = {{"ops", ops}, {"slots", m.cfg.slots > 0 ? m.cfg.slots : m.cfg.layers + 1}, {"fwd_seq", m.plan.fwd_seq},
+    json j = {{"ops", ops}, {"slots", m.cfg.slots > 0 ? m.cfg.slots : m.cfg.layers + 1},
+              {"peak_slots", m.peak_slots}, {"fwd_seq", m.plan.fwd_seq},
               {"bwd_seq", m.plan.bwd_seq}, {"mode", mode}};
     const std::string s = j.dump();
     *out = static_cast<char*>(std::malloc(s.size() + 1));

@@ -50,6 +50,7 @@ struct Lowering {
     std::vector<int> strand_last;
     std::vector<std::vector<int>> slot_of;  // [strand][layer]
     std::vector<int> free_slots;
+    int peak_slots = 0;  // most activation slots held at once
     std::map<int, int> lane_of, pos_in_bwd, pos_in_fwd;
 
     explicit Lowering(Model& mm) : m(mm) {
@@ -143,6 +144,7 @@ struct Lowering {
             throw std::runtime_error("not enough activation slots for this schedule (dh_model_cfg.slots)");
         slot_of[strand][layer] = free_slots.back();
         free_slots.pop_back();
+        peak_slots = std::max(peak_slots, n_slots(m) - static_cast<int>(free_slots.size()));
     }
     void give_slot(int strand, int layer) { free_slots.push_back(slot_of[strand][layer]); }
 
@@ -335,6 +337,7 @@ int lower_ops(Model& m, int mode) {
     if (lw.free_slots.size() != static_cast<std::size_t>(n_slots(m)))
         return set_error(DH_ERR_OTHER, "lowering: activation slots leaked");
     m.prog_has_opt = lw.has_opt;
+    m.peak_slots = lw.peak_slots;
     m.y_slot.assign(mb, -1);
     for (int s = 0; s < mb; ++s) m.y_slot[s] = lw.slot_of[s][L - 1];
     m.prog = std::move(lw.prog);

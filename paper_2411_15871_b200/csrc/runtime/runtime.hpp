@@ -181,6 +181,7 @@ struct Model {
     int gemm_ctas_overlap = 0;  // SM cap for GEMMs that co-run with a collective
     bool fuse_optimizer = true;  // per-layer AdamW ops inside the program (kOptNode)
     bool prog_has_opt = false;   // the lowered program contains them
+    int peak_slots = 0;          // activation slots the lowered program holds at once
     Buf opt_hp;                   // dh_adamw_hparams as 9 floats
     std::map<int, double> solo_us;  // node id -> solo time used for lowering
     weft::OverlapTable plan_overlap;  // table the lowering replays the lane model with

@@ -61,7 +61,7 @@ def check_program(prog, shape, mb):
     for i, o in enumerate(ops):
         assert all(w < i for w in o["waits"]), "wait on a later op"
     for s in range(mb):
-        mine = [(o["layer"], o["node"]) for o in ops if o["strand"] == s]
+        mine = [(o["layer"], o["node"]) for o in ops if o["strand"] == s and o["node"] < 100]  # (not transfers)
         expect = [(l, n) for l in range(L) for n in prog["fwd_seq"]] + \
                  [(l, n) for l in reversed(range(L)) for n in prog["bwd_seq"]]
         assert mine == expect, f"strand {s} order"
@@ -200,3 +200,50 @@ def test_gloo_two_ranks_agree_on_program():
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: True, 1: True}
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _stage_shape(shape, layers, p, d, mb, slots=None):
+    c = layers // (2 * p)
+    return LlamaShape(**{**shape.__dict__, "layers": 2 * c, "split_layer": c if d + 1 < p else 0,
+                         "pp_rank": d, "pp_size": p, "micro_batches": mb, "slots": slots or mb * 2 * c + 1})
+
+
+@pytest.mark.parametrize("p,layers,mb", [(2, 4, 4), (2, 8, 8), (4, 16, 6)])
+def test_w_pipeline_stage_programs(p, layers, mb):
+    """Mode 3 (W pipeline stage): every stage runs each of its micro-batches'
+    forward / backward over its U-fold layers in plan order, every transfer has
+    exactly one matching transfer on the peer (same tag: kind and micro-batch),
+    and the per-layer AdamW follows the last micro-batch's backward."""
+    plan = _plan(TINY, 1)
+    progs = [lower(_stage_shape(TINY, layers, p, d, mb), 1, plan, "w_pipeline") for d in range(p)]
+    sends, recvs = {}, {}
+    for d, prog in enumerate(progs):
+        shape = _stage_shape(TINY, layers, p, d, mb)
+        check_program(prog, shape, mb)
+        for o in prog["ops"]:
+            kind = {101: "act", 102: "act", 103: "grad", 104: "grad"}.get(o["node"])
+            if kind:
+                key = (d, o["peer"], kind, o["strand"]) if o["node"] in (101, 103) else (o["peer"], d, kind, o["strand"])
+                book = sends if o["node"] in (101, 103) else recvs
+                assert key not in book
+                book[key] = o
+    assert set(sends) == set(recvs) and sends
+    # each micro-batch crosses every stage boundary twice per pass (down and back up)
+    assert len(sends) == 2 * 2 * (p - 1) * mb
+
+
+def test_w_pipeline_slots_vs_reference_memory_replay():
+    """Activation slots the stage program holds at once against the reference
+    memory replay of the same W schedule (simulate_memory, one byte per layer
+    activation): the replay frees and allocates at the same block end, the
+    executor's SI visits need one extra slot (the forward strand takes its
+    slot before the backward strand returns one)."""
+    layers, p, mb = 80, 2, 8  # config 5's layer count on PP = 2
+    plan = _plan(TINY, 1)
+    sched = {"discipline": "w_shape", "m": mb, "p": p}
+    replay = planner.lib().memory({"act_bytes_per_layer": 1, "state_bytes_per_layer": 0, "layers": layers,
+                                   "capacity_bytes": 1 << 40}, schedule=sched)
+    dev = json.loads(replay["peaks_json"])["devices"]
+    for d in range(p):
+        prog = lower(_stage_shape(TINY, layers, p, d, mb, slots=8 * layers), 1, plan, "w_pipeline")
+        assert dev[d]["peak_bytes"] <= prog["peak_slots"] <= dev[d]["peak_bytes"] + 1, (d, prog["peak_slots"], dev[d])
