@@ -1,4 +1,5 @@
 // extern "C" face of the runtime (include/dh_capi.h, "runtime" section).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -13,9 +14,17 @@ namespace dh {
 int kernels_per_node(const Model& m, int node, int layer) {
     const bool group = m.cfg.nq_l != m.cfg.nkv_l;
     switch (node) {
-        case 0: case 8: case 5: case 7: case 10: case 11: case 12: case 22: case 23: case 24: case 25:
+        case 10: case 11: {  // (+ standalone SwiGLU on the later of the two when not in its epilogue)
+            if (m.swiglu_in_epilogue) return 1;
+            const auto& fs = m.plan.fwd_seq;
+            const auto pos = [&](int id) { return std::find(fs.begin(), fs.end(), id) - fs.begin(); };
+            return pos(node) > pos(node == 10 ? 11 : 10) ? 2 : 1;
+        }
+        case 22:
+            return m.swiglu_in_epilogue ? 1 : 2;
+        case 0: case 8: case 5: case 7: case 12: case 23: case 24: case 25:
         case 31: case 32: case 35: case 36:
-            return 1;  // (SwiGLU fwd / bwd run inside the mlp_gate|mlp_up / mlp_down_dgrad epilogues)
+            return 1;
         case 2: case 26: case 28: case 38:
             return 2;
         case kOptNode:

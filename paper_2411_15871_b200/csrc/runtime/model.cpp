@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "runtime.hpp"
@@ -194,6 +195,15 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     b.dy_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
     b.d_gate = pool.take(S * F * 2, "act.bwd_transient");
     b.d_up = pool.take(S * F * 2, "act.bwd_transient");
+    {
+        // SwiGLU runs in the mlp GEMM epilogues by default. Measured on B200 the
+        // standalone kernels after plain GEMMs were no faster even at TP=8
+        // (1.5 waves of 256x256 pair tiles, where the epilogue is least hidden)
+        // and lost overlap under SI; DH_SWIGLU_EPILOGUE=0 selects them.
+        const char* env = std::getenv("DH_SWIGLU_EPILOGUE");
+        m->swiglu_in_epilogue = env ? std::atoi(env) != 0 : true;
+        if (!m->swiglu_in_epilogue) b.d_act = pool.take(S * F * 2, "act.bwd_transient");
+    }
     b.dx_part = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
     b.dx1_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
     b.d_o = pool.take(S * A * 2, "act.bwd_transient");
@@ -368,14 +378,18 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 9:  // ag1
             RT_TRY(need_comm());
             return comm->all_gather(P(m.fs.ln_loc), P(sl.ln1_full), TH, s);
-        case 10:  // mlp_gate (+ act = silu(gate) * up in the epilogue when it runs after mlp_up)
-            return gemm(P(sl.ln1_full), H, false, W + p.wg, H, false, P(sl.gate), F, false, S, F, H,
-                        false, cap, s, op.fuse_swiglu ? DH_EPI_SWIGLU_FWD_UP : DH_EPI_NONE, P(sl.act),
-                        P(sl.up));
-        case 11:  // mlp_up (+ act in the epilogue when it runs after mlp_gate)
-            return gemm(P(sl.ln1_full), H, false, W + p.wu, H, false, P(sl.up), F, false, S, F, H,
-                        false, cap, s, op.fuse_swiglu ? DH_EPI_SWIGLU_FWD : DH_EPI_NONE, P(sl.act),
-                        P(sl.gate));
+        case 10:    // mlp_gate (+ act = silu(gate) * up when it runs after mlp_up)
+        case 11: {  // mlp_up (+ act when it runs after mlp_gate)
+            const bool gate = op.node == 10;
+            const bool epi = op.fuse_swiglu && m.swiglu_in_epilogue;
+            RT_TRY(gemm(P(sl.ln1_full), H, false, W + (gate ? p.wg : p.wu), H, false, P(gate ? sl.gate : sl.up), F,
+                        false, S, F, H, false, cap, s,
+                        epi ? (gate ? DH_EPI_SWIGLU_FWD_UP : DH_EPI_SWIGLU_FWD) : DH_EPI_NONE, P(sl.act),
+                        P(gate ? sl.up : sl.gate)));
+            if (op.fuse_swiglu && !epi)
+                return dh_swiglu_fwd(P(sl.gate), P(sl.up), P(sl.act), static_cast<long long>(S) * F, s);
+            return DH_OK;
+        }
         case 12:  // mlp_down (row-parallel; act was produced by the mlp_gate/mlp_up epilogue)
             return gemm(P(sl.act), F, false, W + p.wd, F, false, tp1 ? P(m.fs.rs_out) : P(m.fs.part),
                         H, false, S, H, F, false, cap, s);
@@ -397,10 +411,14 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 21:  // rs1_bwd_ag
             RT_TRY(need_comm());
             return comm->all_gather(dy, P(m.bs.dy_full), TH, s);
-        case 22: {  // mlp_down_dgrad with the SwiGLU backward in its epilogue (d_act never stored)
+        case 22: {  // mlp_down_dgrad + SwiGLU backward (in its epilogue: d_act never stored)
             const void* dyf = tp1 ? dy : P(m.bs.dy_full);
-            return gemm(dyf, H, false, W + p.wd, F, true, P(m.bs.d_gate), F, false, S, F, H, false, cap, s,
-                        DH_EPI_SWIGLU_BWD, P(m.bs.d_up), P(sl.gate), P(sl.up));
+            if (m.swiglu_in_epilogue)
+                return gemm(dyf, H, false, W + p.wd, F, true, P(m.bs.d_gate), F, false, S, F, H, false, cap, s,
+                            DH_EPI_SWIGLU_BWD, P(m.bs.d_up), P(sl.gate), P(sl.up));
+            RT_TRY(gemm(dyf, H, false, W + p.wd, F, true, P(m.bs.d_act), F, false, S, F, H, false, cap, s));
+            return dh_swiglu_bwd(P(sl.gate), P(sl.up), P(m.bs.d_act), P(m.bs.d_gate), P(m.bs.d_up),
+                                 static_cast<long long>(S) * F, s);
         }
         case 23: {  // mlp_down_wgrad: dWd[H,F] += dY^T act
             const void* dyf = tp1 ? dy : P(m.bs.dy_full);

@@ -109,7 +109,7 @@ struct FwdScratch {
 };
 
 struct BwdScratch {
-    Buf grad[2], d_x1, dy_full, d_gate, d_up, dx_part, dx1_full, d_o, dqkv, attn_scratch,
+    Buf grad[2], d_x1, dy_full, d_gate, d_up, d_act, dx_part, dx1_full, d_o, dqkv, attn_scratch,
         ln_partial, rs_out;
 };
 
@@ -180,6 +180,10 @@ struct Model {
     int adam_step = 0;
     int gemm_ctas_overlap = 0;  // SM cap for GEMMs that co-run with a collective
     bool fuse_optimizer = true;  // per-layer AdamW ops inside the program (kOptNode)
+    // SwiGLU in the mlp GEMM epilogues (fwd: the later of mlp_gate / mlp_up; bwd:
+    // mlp_down_dgrad) when the GEMM has enough waves to hide the epilogue;
+    // otherwise standalone kernels after plain GEMMs (decided at model create)
+    bool swiglu_in_epilogue = true;
     bool prog_has_opt = false;   // the lowered program contains them
     int peak_slots = 0;          // activation slots the lowered program holds at once
     Buf opt_hp;                   // dh_adamw_hparams as 9 floats

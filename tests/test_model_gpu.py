@@ -81,7 +81,16 @@ def ctx():
     c.close()
 
 
-def test_tp1_model_vs_oracle_and_si_equals_sequential(ctx):
+@pytest.fixture(params=["auto", "0"], ids=["swiglu_epilogue", "swiglu_standalone"])
+def swiglu_mode(request, monkeypatch):
+    """SwiGLU in the mlp GEMM epilogues (default) or as standalone kernels
+    after plain GEMMs (DH_SWIGLU_EPILOGUE=0)."""
+    if request.param != "auto":
+        monkeypatch.setenv("DH_SWIGLU_EPILOGUE", request.param)
+    return request.param
+
+
+def test_tp1_model_vs_oracle_and_si_equals_sequential(ctx, swiglu_mode):
     shape = _tiny(mb=2)
     orc, m, xs, rs = _build(shape, ctx)
     plan = _plan(shape, 1)
@@ -174,7 +183,7 @@ def test_in_program_optimizer_matches_post_step_adamw(ctx):
         assert torch.equal(out[0][k], out[1][k]), k
 
 
-def test_head_dim_128_model_vs_oracle(ctx):
+def test_head_dim_128_model_vs_oracle(ctx, swiglu_mode):
     """The production head_dim (128) routes attention through the tcgen05 kernels."""
     shape = LlamaShape(hidden=512, ffn=1024, n_heads=4, n_kv_heads=2, head_dim=128, layers=2,
                        seq_len=384, micro_batches=2, rope_theta=500000.0)
