@@ -242,8 +242,8 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     then times SI (default and wide search caps; plan steps joined or relaxed),
     sequential and compute-only (collectives left out of the lowered program)
     steps. Numerically meaningless by construction; timing-faithful by design.
-    full=False (the TP sweep points) times only the best SI variant, sequential
-    and compute-only."""
+    full=False (the TP sweep points and other configs) times the default-caps
+    joined SI plan and the wide-caps relaxed one, sequential and compute-only."""
     import copy
 
     import torch
@@ -282,7 +282,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
              ("si_wide_relaxed", srch_wide, "si_relaxed", False),
              ("compute_only", srch_wide, "si_relaxed", True), ("sequential", srch_wide, "sequential", False)]
     if not full:
-        modes = [x for x in modes if x[0] in ("si_wide_relaxed", "compute_only", "sequential")]
+        modes = [x for x in modes if x[0] in ("si", "si_wide_relaxed", "compute_only", "sequential")]
     res = {}
     for name, plan, mode, skip in modes:
         m.set_plan(plan["plan_json"], json.dumps(prof), mode=mode)
@@ -290,7 +290,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
         m.set_skip_comm(skip)
         for _ in range(2):
             step()
-        res[name] = timed(max(2, args.steps if full else 2), step, stream)
+        res[name] = timed(max(10, 2 * args.steps) if full else max(3, args.steps), step, stream)  # emulated steps are short: more of them for stable deltas
         log(f"emulated tp{tp} {name}: {res[name]:.1f} ms/step")
     m.set_skip_comm(False)
     # the reference's iteration model (estimate_iteration_time) on the measured
@@ -332,7 +332,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
             m.set_skip_comm(skip)
             for _ in range(2):
                 step()
-            r2[name] = timed(max(2, args.steps), step, stream)
+            r2[name] = timed(max(10, 2 * args.steps), step, stream)
         m.set_skip_comm(False)
         e_m = (res[best] - res["compute_only"]) * 1e3 / shape.layers   # per layer, whole step
         e_2 = (r2[best] - r2["compute_only"]) * 1e3 / shape.layers

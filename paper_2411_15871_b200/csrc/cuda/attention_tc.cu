@@ -25,6 +25,7 @@
 // grows by more than 2^8; P values are bounded by 2^8 in between.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -510,12 +511,15 @@ const FwdSplit& fwd_split_plan(int T, int nq) {
     if (static_cast<long long>(nq) * npairs > 2LL * sms) return cache.emplace(key, sp).first->second;
     const int full = 2 * npairs;
     double best = fwd_makespan(nq, nkb, full, sms, nullptr);
+    // DH_ATTN_FWD_CHUNK=<even KV blocks> forces a chunk size (tuning runs)
+    const char* force = std::getenv("DH_ATTN_FWD_CHUNK");
+    const int forced = force ? std::atoi(force) : 0;
     for (int div : {2, 3, 4, 6, 8}) {
-        const int c = std::max(2, 2 * ((full + 2 * div - 1) / (2 * div)));
-        if (c >= nkb || (full + c - 1) / c > 16) continue;
+        const int c = forced ? forced : std::max(2, 2 * ((full + 2 * div - 1) / (2 * div)));
+        if (c >= nkb || (full + c - 1) / c > 16 || c % 2) continue;
         std::vector<std::pair<float, uint32_t>> it;
         const double ms = fwd_makespan(nq, nkb, c, sms, &it);
-        if (ms < 0.85 * best && static_cast<int>(it.size()) <= kMaxItems) {
+        if ((forced || ms < 0.85 * best) && static_cast<int>(it.size()) <= kMaxItems) {
             best = ms;
             sp.chunk = c;
             sp.maxc = (full + c - 1) / c;
