@@ -201,7 +201,7 @@ class LlamaTPOracle:
     def layer_fwd(self, l, x):
         nm, p, tp, D = self.nm, self.params[l], self.tp, self.D
         S = self.S
-        nq_l, nkv_l, F_l = self.nq // tp, self.nkv // tp, self.F // tp
+        nq_l = self.nq // tp
         ln0, rstd0 = rmsnorm_fwd(x, p["g0"], self.eps, nm)                     # ln0 (+ ag0)
         q = nm.rb(ln0 @ p["wq"].T).reshape(S, self.nq, D)                      # qkv
         k = nm.rb(ln0 @ p["wk"].T).reshape(S, self.nkv, D)
@@ -215,37 +215,28 @@ class LlamaTPOracle:
                                    for r in range(tp)])                       # attn_proj + rs0
         x1 = nm.rb(x + attn)                                                   # bda0
         ln1, rstd1 = rmsnorm_fwd(x1, p["g1"], self.eps, nm)                   # ln1 (+ ag1)
+        cache = dict(x=x, ln0=ln0, rstd0=rstd0, q=q, k=k, v=v, o=o, lse=lse, x1=x1, ln1=ln1,
+                     rstd1=rstd1)
+        y = nm.rb(x1 + self._mlp_fwd(l, ln1, cache))                           # bda1
+        return y, cache
+
+    def _mlp_fwd(self, l, ln1, cache):
+        """Dense SwiGLU MLP of layer l (mlp_gate, mlp_up, mlp_down + rs1)."""
+        nm, p, tp = self.nm, self.params[l], self.tp
+        F_l = self.F // tp
         gate = nm.rb(ln1 @ p["wg"].T)                                          # mlp_gate
         up = nm.rb(ln1 @ p["wu"].T)                                            # mlp_up
         act = nm.rb(silu(gate) * up)                                           # mlp_down
-        mlp = self._row_parallel([act[:, r * F_l:(r + 1) * F_l] @ p["wd"][:, r * F_l:(r + 1) * F_l].T
-                                  for r in range(tp)])                        # + rs1
-        y = nm.rb(x1 + mlp)                                                    # bda1
-        cache = dict(x=x, ln0=ln0, rstd0=rstd0, q=q, k=k, v=v, o=o, lse=lse, x1=x1, ln1=ln1,
-                     rstd1=rstd1, gate=gate, up=up, act=act)
-        return y, cache
+        cache.update(gate=gate, up=up, act=act)
+        return self._row_parallel([act[:, r * F_l:(r + 1) * F_l] @ p["wd"][:, r * F_l:(r + 1) * F_l].T
+                                   for r in range(tp)])                       # + rs1
 
     def layer_bwd(self, l, c, dy, grads, dx_first_gate=True):
         nm, p, tp, D, S = self.nm, self.params[l], self.tp, self.D, self.S
-        nq_l, nkv_l, F_l = self.nq // tp, self.nkv // tp, self.F // tp
+        nq_l, nkv_l = self.nq // tp, self.nkv // tp
         g = grads[l]
         d_x1 = dy.copy()                                                       # bda1_bwd
-        d_act = nm.rb(dy @ p["wd"])                                            # mlp_down_dgrad
-        sg = 1.0 / (1.0 + np.exp(-c["gate"]))
-        d_up = nm.rb(d_act * c["gate"] * sg)
-        d_gate = nm.rb(d_act * c["up"] * sg * (1.0 + c["gate"] * (1.0 - sg)))
-        g["wd"] += dy.T @ c["act"]                                             # mlp_down_wgrad
-        parts = []
-        for r in range(tp):                                                    # gate/up dgrad
-            sl = slice(r * F_l, (r + 1) * F_l)
-            a = d_gate[:, sl] @ p["wg"][sl]
-            b = d_up[:, sl] @ p["wu"][sl]
-            first, second = (a, b) if dx_first_gate else (b, a)
-            # the GPU accumulates the second partial with a bf16 TMA reduce-add
-            parts.append(nm.rb(nm.rb(first) + nm.rb(second)))
-        g["wg"] += d_gate.T @ c["ln1"]                                         # mlp_fc1_wgrad
-        g["wu"] += d_up.T @ c["ln1"]
-        dln1 = self._row_parallel(parts)                                       # ag1_bwd_rs
+        dln1 = self._mlp_bwd(l, c, dy, g, dx_first_gate)
         dxn, dg1 = rmsnorm_bwd(c["x1"], p["g1"], c["rstd1"], dln1)             # ln1_bwd
         d_x1 = nm.rb(dxn + d_x1)
         g["g1"] += dg1
@@ -269,6 +260,27 @@ class LlamaTPOracle:
         g["g0"] += dg0
         return nm.rb(dxn + d_x)
 
+    def _mlp_bwd(self, l, c, dy, g, dx_first_gate=True):
+        """Dense MLP backward of layer l: dL/d(ln1 output) after ag1_bwd_rs."""
+        nm, p, tp = self.nm, self.params[l], self.tp
+        F_l = self.F // tp
+        d_act = nm.rb(dy @ p["wd"])                                            # mlp_down_dgrad
+        sg = 1.0 / (1.0 + np.exp(-c["gate"]))
+        d_up = nm.rb(d_act * c["gate"] * sg)
+        d_gate = nm.rb(d_act * c["up"] * sg * (1.0 + c["gate"] * (1.0 - sg)))
+        g["wd"] += dy.T @ c["act"]                                             # mlp_down_wgrad
+        parts = []
+        for r in range(tp):                                                    # gate/up dgrad
+            sl = slice(r * F_l, (r + 1) * F_l)
+            a = d_gate[:, sl] @ p["wg"][sl]
+            b = d_up[:, sl] @ p["wu"][sl]
+            first, second = (a, b) if dx_first_gate else (b, a)
+            # the GPU accumulates the second partial with a bf16 TMA reduce-add
+            parts.append(nm.rb(nm.rb(first) + nm.rb(second)))
+        g["wg"] += d_gate.T @ c["ln1"]                                         # mlp_fc1_wgrad
+        g["wu"] += d_up.T @ c["ln1"]
+        return self._row_parallel(parts)                                       # ag1_bwd_rs
+
     def zero_grads(self):
         return [{k: np.zeros_like(v, dtype=np.float32) for k, v in p.items()} for p in self.params]
 
@@ -286,3 +298,134 @@ class LlamaTPOracle:
         for l in reversed(range(self.L)):
             d = self.layer_bwd(l, caches[l], d, grads, dx_first_gate)
         return loss, y, d, grads
+
+
+# --------------------------------------------------------------------------- MoE layer
+
+
+class MoEOracle(LlamaTPOracle):
+    """The reference's moe_ep layer (proj/src/op_model.cpp:121-169: router ->
+    permute -> [a2a_dispatch] -> expert_fc1 -> expert_fc2 -> [a2a_combine] ->
+    unpermute -> bda1) at TP = EP = 1, restated as the B200 model computes it
+    (csrc/runtime/moe.cpp). The reference has no MoE math either; this is OUR
+    definition (unpinned, cross-checked against torch autograd):
+
+      router   logits = ln1 @ wr^T (fp32), p = softmax(logits), top-k experts by
+               p (ties: lower expert id), weights w = p_top / sum(p_top)
+      permute  each expert owns `capacity` slots, filled by its (token, k)
+               assignments in (token, k) order; assignments beyond capacity
+               are dropped (they contribute nothing)
+      experts  SwiGLU FFN per expert: act = silu(xp w1g^T) * (xp w1u^T),
+               y = act w2^T (empty slots are zero rows)
+      unpermute moe[t] = sum_k w[t,k] y[slot(t,k)]  (k ascending, fp32, one rounding)
+    """
+
+    def __init__(self, hidden, ffn, n_heads, n_kv_heads, head_dim, layers, seq, experts, topk=2,
+                 capacity=None, theta=10000.0, eps=1e-5, bf16=True, seed=0, init_std=0.02):
+        super().__init__(hidden, ffn, n_heads, n_kv_heads, head_dim, layers, seq, tp=1, theta=theta,
+                         eps=eps, bf16=bf16, seed=seed, init_std=init_std)
+        self.E, self.K = experts, topk
+        self.C = capacity if capacity is not None else moe_capacity(seq, experts, topk)
+        rng = np.random.default_rng(seed + 7919)
+        H, F = hidden, ffn
+
+        def w(*shape):
+            return bf16_round(rng.standard_normal(shape, dtype=np.float32) * init_std)
+
+        for p in self.params:
+            for k in ("wg", "wu", "wd"):
+                del p[k]
+            p["wr"] = w(experts, H)
+            p["w1g"] = w(experts, F, H)
+            p["w1u"] = w(experts, F, H)
+            p["w2"] = w(experts, H, F)
+
+    def route(self, ln1, wr):
+        """-> (probs [S,E] f32, ids [S,K], weights [S,K] f32, slot [S,K] (-1 dropped))."""
+        logits = ln1.astype(np.float32) @ wr.T.astype(np.float32)
+        z = logits - logits.max(1, keepdims=True)
+        e = np.exp(z)
+        probs = (e / e.sum(1, keepdims=True)).astype(np.float32)
+        ids = np.argsort(-probs, axis=1, kind="stable")[:, :self.K]
+        top = np.take_along_axis(probs, ids, 1)
+        wts = (top / top.sum(1, keepdims=True)).astype(np.float32)
+        slot = np.full(ids.shape, -1, np.int64)
+        fill = np.zeros(self.E, np.int64)
+        for t in range(ids.shape[0]):
+            for k in range(self.K):
+                ex = ids[t, k]
+                if fill[ex] < self.C:
+                    slot[t, k] = ex * self.C + fill[ex]
+                    fill[ex] += 1
+        return probs, ids, wts, slot
+
+    def _mlp_fwd(self, l, ln1, cache):
+        nm, p, E, C, F = self.nm, self.params[l], self.E, self.C, self.F
+        probs, ids, wts, slot = self.route(ln1, p["wr"])                         # router
+        xp = np.zeros((E * C, self.H), np.float32)                              # permute
+        for t, k in zip(*np.nonzero(slot >= 0)):
+            xp[slot[t, k]] = ln1[t]
+        gate = np.zeros((E * C, F), np.float32)
+        up = np.zeros((E * C, F), np.float32)
+        y = np.zeros((E * C, self.H), np.float32)
+        for e in range(E):                                                      # expert_fc1
+            rows = slice(e * C, (e + 1) * C)
+            gate[rows] = nm.rb(xp[rows] @ p["w1g"][e].T)
+            up[rows] = nm.rb(xp[rows] @ p["w1u"][e].T)
+        act = nm.rb(silu(gate) * up)
+        for e in range(E):                                                      # expert_fc2
+            rows = slice(e * C, (e + 1) * C)
+            y[rows] = nm.rb(act[rows] @ p["w2"][e].T)
+        moe = np.zeros_like(ln1, dtype=np.float32)                              # unpermute
+        for k in range(self.K):
+            sk = slot[:, k]
+            ok = sk >= 0
+            moe[ok] += wts[ok, k:k + 1] * y[sk[ok]]
+        cache.update(probs=probs, ids=ids, wts=wts, slot=slot, xp=xp, gate=gate, up=up, act=act, y=y)
+        return nm.rb(moe)
+
+    def _mlp_bwd(self, l, c, dy, g, dx_first_gate=True):
+        nm, p, E, C, K = self.nm, self.params[l], self.E, self.C, self.K
+        slot, wts, ids, probs = c["slot"], c["wts"], c["ids"], c["probs"]
+        dys = np.zeros_like(c["y"])                                             # unpermute_bwd
+        dw = np.zeros(wts.shape, np.float32)
+        for t, k in zip(*np.nonzero(slot >= 0)):
+            s_ = slot[t, k]
+            dys[s_] = wts[t, k] * dy[t]
+            dw[t, k] = float(np.dot(c["y"][s_].astype(np.float64), dy[t].astype(np.float64)))
+        dys = nm.rb(dys)
+        d_act = np.zeros_like(c["act"])
+        for e in range(E):                                                      # expert_fc2_dgrad
+            rows = slice(e * C, (e + 1) * C)
+            d_act[rows] = nm.rb(dys[rows] @ p["w2"][e])
+            g["w2"][e] += dys[rows].T @ c["act"][rows]                          # expert_fc2_wgrad
+        sg = 1.0 / (1.0 + np.exp(-c["gate"]))
+        d_up = nm.rb(d_act * c["gate"] * sg)
+        d_gate = nm.rb(d_act * c["up"] * sg * (1.0 + c["gate"] * (1.0 - sg)))
+        dxp = np.zeros_like(c["xp"])
+        for e in range(E):                                                      # expert_fc1_dgrad
+            rows = slice(e * C, (e + 1) * C)
+            dxp[rows] = nm.rb(nm.rb(d_gate[rows] @ p["w1g"][e]) + nm.rb(d_up[rows] @ p["w1u"][e]))
+            g["w1g"][e] += d_gate[rows].T @ c["xp"][rows]                       # expert_fc1_wgrad
+            g["w1u"][e] += d_up[rows].T @ c["xp"][rows]
+        dln1 = np.zeros((slot.shape[0], self.H), np.float32)                    # permute_bwd
+        for k in range(K):
+            sk = slot[:, k]
+            ok = sk >= 0
+            dln1[ok] += dxp[sk[ok]]
+        dln1 = nm.rb(dln1)
+        # router_bwd: through the top-k renormalisation and the softmax
+        top = np.take_along_axis(probs, ids, 1)
+        ssum = top.sum(1, keepdims=True)
+        dtop = dw / ssum - (dw * top).sum(1, keepdims=True) / ssum ** 2
+        dp = np.zeros_like(probs)
+        np.put_along_axis(dp, ids, dtop.astype(np.float32), 1)
+        dlogits = (probs * (dp - (probs * dp).sum(1, keepdims=True))).astype(np.float32)
+        g["wr"] += dlogits.T @ c["ln1"]
+        return nm.rb(dln1 + dlogits @ p["wr"])
+
+
+def moe_capacity(tokens, experts, topk, factor=1.25, multiple=128):
+    """Slots per expert: ceil(tokens * topk / experts * factor), rounded up to a multiple of `multiple`."""
+    c = int(np.ceil(tokens * topk / experts * factor))
+    return (c + multiple - 1) // multiple * multiple

@@ -87,3 +87,74 @@ def test_tp_partition_invariance(tp):
         assert np.allclose(ga[0][k], gb[0][k], atol=1e-3)
     sh = b.shard(0, 1)
     assert sh["wqkv"].shape == ((4 // tp + 2 * 4 // tp) * 16, 64)
+
+
+def _torch_moe(o, x, r):
+    """fp64 torch autograd of the MoE layer stack with the oracle's routing
+    decisions (top-k ids and capacity slots) held fixed, as they are
+    non-differentiable; weights flow through softmax and the renormalisation."""
+    from oracle.layer_oracle import MoEOracle  # noqa: F401
+    S, D = o.S, o.D
+    P = [{k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in p.items()} for p in o.params]
+    cos = torch.tensor(o.cos, dtype=torch.float64)[:, None, :]
+    sin = torch.tensor(o.sin, dtype=torch.float64)[:, None, :]
+
+    def rope(t):
+        a, b = t[..., :D // 2], t[..., D // 2:]
+        return torch.cat([a * cos - b * sin, b * cos + a * sin], -1)
+
+    def rms(t, g):
+        return t * torch.rsqrt(t.pow(2).mean(-1, keepdim=True) + o.eps) * g
+
+    h = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+    x0 = h
+    mask = torch.ones(S, S, dtype=torch.bool).triu(1)
+    for p in P:
+        ln0 = rms(h, p["g0"])
+        q = rope((ln0 @ p["wq"].T).view(S, o.nq, D))
+        k = rope((ln0 @ p["wk"].T).view(S, o.nkv, D))
+        v = (ln0 @ p["wv"].T).view(S, o.nkv, D)
+        grp = o.nq // o.nkv
+        k, v = k.repeat_interleave(grp, 1), v.repeat_interleave(grp, 1)
+        s = torch.einsum("qhd,khd->hqk", q, k) * float(o.scale)
+        s = s.masked_fill(mask, float("-inf"))
+        att = torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), v).reshape(S, -1)
+        x1 = h + att @ p["wo"].T
+        ln1 = rms(x1, p["g1"])
+        probs = torch.softmax(ln1 @ p["wr"].T, -1)
+        _, ids, _, slot = o.route(ln1.detach().numpy().astype(np.float32), p["wr"].detach().numpy())
+        ids_t = torch.tensor(ids)
+        top = probs.gather(1, ids_t)
+        w = top / top.sum(1, keepdim=True)
+        moe = torch.zeros_like(ln1)
+        for t in range(S):
+            for kk in range(o.K):
+                if slot[t, kk] < 0:
+                    continue
+                e = int(ids[t, kk])
+                xe = ln1[t]
+                y = (torch.nn.functional.silu(p["w1g"][e] @ xe) * (p["w1u"][e] @ xe)) @ p["w2"][e].T
+                moe = moe.index_add(0, torch.tensor([t]), (w[t, kk] * y)[None])
+        h = x1 + moe
+    loss = (h * torch.tensor(r, dtype=torch.float64)).sum()
+    loss.backward()
+    return loss.item(), x0.grad.numpy(), [{k: v.grad.numpy() for k, v in p.items()} for p in P]
+
+
+@pytest.mark.parametrize("capacity", [16, 6])  # 6: some assignments dropped
+def test_moe_oracle_backward_matches_autograd(capacity):
+    from oracle.layer_oracle import MoEOracle
+    o = MoEOracle(hidden=64, ffn=48, n_heads=4, n_kv_heads=2, head_dim=16, layers=1, seq=16, experts=4,
+                  topk=2, capacity=capacity, bf16=False, seed=2, init_std=0.3)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((16, 64)).astype(np.float32)
+    r = rng.standard_normal((16, 64)).astype(np.float32)
+    loss, _, dx, grads = o.run(x, r)
+    _, cache = o.layer_fwd(0, x)
+    assert (cache["slot"] < 0).any() == (capacity == 6)  # the small capacity drops assignments
+    tl, tdx, tg = _torch_moe(o, x, r)
+    assert abs(loss - tl) < 1e-3 * max(1.0, abs(tl))
+    assert np.abs(dx - tdx).max() < 1e-3 * np.abs(tdx).max()
+    for k in tg[0]:
+        err = np.abs(grads[0][k] - tg[0][k]).max() / max(1e-12, np.abs(tg[0][k]).max())
+        assert err < 2e-3, (k, err)
