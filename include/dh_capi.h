@@ -137,8 +137,9 @@ int dh_init_normal(void* bf16_out, float* f32_out, long long n, unsigned long lo
 int dh_fill_bf16(void* out, float value, long long n, void* stream);
 int dh_copy(void* dst, const void* src, long long bytes, void* stream);
 /* Single-GPU stand-in for one rank's collective (mode 0 AllGather of `count`
- * bf16 per rank, 1 ReduceScatter to `count`): same HBM traffic on `ctas` CTAs,
- * held for (tp-1)*count*2 bytes / link_gbs. Not numerically a collective. */
+ * bf16 per rank, 1 ReduceScatter to `count`, 2 AllToAll of a `count`-element
+ * buffer): same HBM traffic on `ctas` CTAs, held for the wire bytes ((tp-1)*count*2,
+ * a2a (tp-1)/tp*count*2) / link_gbs. Not numerically a collective. */
 int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode, int ctas,
                   double link_gbs, void* stream);
 /* *loss = sum(y * r) in fp32, deterministic two-pass reduction through
@@ -146,6 +147,38 @@ int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode,
 int dh_dot_loss(const void* y, const void* r, long long n, float* partial, float* loss,
                 void* stream);
 
+/* ---------------------------------------------------------------- MoE (moe.cu)
+ * Nodes of the moe_ep template (reference op_model.cpp:121-169). Slot layout:
+ * expert e owns rows [e*C, (e+1)*C) of a [E*C, hidden] block (C = capacity per
+ * expert per source rank); assignment a = t*topk + k. Empty slots are zero rows. */
+/* router (9): probs fp32 [T,E] = softmax(x wr^T), ids int32 [T,K] = top-k by
+ * probability (ties: lower expert), wts fp32 [T,K] = top / sum(top). E <= 64, K <= 8. */
+int dh_moe_router_fwd(const void* x, const void* wr, float* probs, int* ids, float* wts, int tokens,
+                      int hidden, int experts, int topk, void* stream);
+/* permute (10), part 1: slot[a] = e*C + (rank of a among expert e's assignments in
+ * (t, k) order) or -1 past capacity; slot_src[e*C + j] = a or -1 (empty). */
+int dh_moe_assign(const int* ids, int tokens, int topk, int experts, int capacity, int* slot,
+                  int* slot_src, void* stream);
+/* permute (10), part 2: xp[s] = x[slot_src[s] / topk] (zero row when empty). */
+int dh_moe_permute(const void* x, const int* slot_src, void* xp, int n_slots, int topk, int hidden,
+                   void* stream);
+/* unpermute (15): out[t] = bf16(sum_k wts[t,k] * y[slot[t,k]]), k ascending, fp32. */
+int dh_moe_unpermute(const void* y, const int* slot, const float* wts, void* out, int tokens, int topk,
+                     int hidden, void* stream);
+/* unpermute_bwd (21): dys[s] = bf16(wts[a] * dy[t]); dw[a] = <y[s], dy[t]> (a = slot_src[s]). */
+int dh_moe_unpermute_bwd(const void* dy, const void* y, const int* slot_src, const float* wts, void* dys,
+                         float* dw, int n_slots, int topk, int hidden, void* stream);
+/* permute_bwd (28): dx[t] = bf16(sum_k dxp[slot[t,k]]). */
+int dh_moe_permute_bwd(const void* dxp, const int* slot, void* dx, int tokens, int topk, int hidden,
+                       void* stream);
+/* router_bwd (29): through the top-k renormalisation and the softmax (dropped
+ * assignments carry no weight gradient); dx_out = bf16(dx_in + dlogits wr),
+ * dwr[E,H] += dlogits^T x (fp32, fixed-order). scratch: fp32, at least
+ * dh_moe_router_bwd_scratch_floats(tokens, hidden, experts). */
+long long dh_moe_router_bwd_scratch_floats(int tokens, int hidden, int experts);
+int dh_moe_router_bwd(const float* probs, const int* ids, const int* slot, const float* dw, const void* x,
+                      const void* wr, const void* dx_in, void* dx_out, float* dwr, float* scratch, int tokens,
+                      int hidden, int experts, int topk, void* stream);
 /* ---------------------------------------------------------------- runtime */
 
 typedef struct dh_ctx dh_ctx;
@@ -187,6 +220,12 @@ typedef struct dh_model_cfg {
      * stage, 0 = contiguous), `slots` the activation slots (0 = layers + 1;
      * pipelined micro-batches need more), pp_rank / pp_size the stage. */
     int slots, split_layer, pp_rank, pp_size;
+    /* MoE (moe_ep template, zero = dense): experts > 1 makes the MLP a top-`topk`
+     * mixture of `experts` SwiGLU experts with `capacity` slots per expert per
+     * source rank (0 = ceil(1.25 * seq * topk / experts) rounded up to 128).
+     * The context's group is then the EP group (attention runs data-parallel,
+     * TP = 1) and each rank holds experts / group_size experts. */
+    int experts, topk, capacity;
 } dh_model_cfg;
 
 typedef struct dh_optim_cfg {

@@ -326,6 +326,7 @@ class MoEOracle(LlamaTPOracle):
                          eps=eps, bf16=bf16, seed=seed, init_std=init_std)
         self.E, self.K = experts, topk
         self.C = capacity if capacity is not None else moe_capacity(seq, experts, topk)
+        self.forced, self.flips, self.tie_tol = [], 0, 1e-2
         rng = np.random.default_rng(seed + 7919)
         H, F = hidden, ffn
 
@@ -341,12 +342,29 @@ class MoEOracle(LlamaTPOracle):
             p["w2"] = w(experts, H, F)
 
     def route(self, ln1, wr):
-        """-> (probs [S,E] f32, ids [S,K], weights [S,K] f32, slot [S,K] (-1 dropped))."""
+        """-> (probs [S,E] f32, ids [S,K], weights [S,K] f32, slot [S,K] (-1 dropped)).
+
+        `self.forced` (a queue of [S,K] id arrays, one per route() call) replaces
+        the top-k choice by the device's, for tokens where the two differ only
+        by a near-tie (logit gap below `tie_tol` of the logits' spread): the
+        device's ln1 differs from ours by bf16 rounding, which can flip such a
+        token. Any other disagreement raises."""
         logits = ln1.astype(np.float32) @ wr.T.astype(np.float32)
         z = logits - logits.max(1, keepdims=True)
         e = np.exp(z)
         probs = (e / e.sum(1, keepdims=True)).astype(np.float32)
         ids = np.argsort(-probs, axis=1, kind="stable")[:, :self.K]
+        if self.forced:
+            fid = np.asarray(self.forced.pop(0), np.int64).reshape(ids.shape)
+            spread = float(np.std(logits)) or 1.0
+            for t in np.nonzero((np.sort(fid, 1) != np.sort(ids, 1)).any(1))[0]:
+                kth = np.sort(logits[t])[::-1][self.K - 1]
+                worst = min(logits[t, fid[t]])
+                if kth - worst > self.tie_tol * spread:
+                    raise AssertionError(f"token {t}: device routes to {fid[t]}, oracle to {ids[t]} "
+                                         f"(logit gap {kth - worst:.3g} is not a near-tie)")
+                self.flips += 1
+            ids = fid
         top = np.take_along_axis(probs, ids, 1)
         wts = (top / top.sum(1, keepdims=True)).astype(np.float32)
         slot = np.full(ids.shape, -1, np.int64)

@@ -571,6 +571,8 @@ __global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restri
             const uint4 v = src[i];
             for (int j = 0; j < tp; ++j) dst[j * chunk_vec + i] = v;
         }
+    } else if (mode == 2) {  // all-to-all stand-in: every element read and written once
+        for (long long i = first; i < chunk_vec; i += stride) dst[i] = src[i];
     } else {          // reduce-scatter stand-in: out[i] = mean_j in[j*chunk + i]
         // (the mean keeps activations bounded over many emulated layers)
         const float inv_tp = 1.f / tp;
@@ -810,7 +812,9 @@ int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode,
                   double link_gbs, void* stream) {
     if (count % 8) return set_error(DH_ERR_INVALID, "comm_proxy: count % 8 required");
     const long long chunk = count / 8;
-    const double wire = static_cast<double>(count) * 2.0 * (tp - 1);
+    // mode 2 (all-to-all): count is the whole buffer, (tp-1)/tp of it crosses the wire
+    const double wire = mode == 2 ? static_cast<double>(count) * 2.0 * (tp - 1) / tp
+                                  : static_cast<double>(count) * 2.0 * (tp - 1);
     const unsigned long long target = link_gbs > 0 ? static_cast<unsigned long long>(wire / link_gbs) : 0ull;
     if (tp > 8) return set_error(DH_ERR_INVALID, "comm_proxy: tp <= 8");
     comm_proxy_kernel<<<std::max(1, ctas), 1024, 0, static_cast<cudaStream_t>(stream)>>>(

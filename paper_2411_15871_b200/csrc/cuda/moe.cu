@@ -1,0 +1,472 @@
+// MoE kernels of the moe_ep layer template (reference op_model.cpp:121-169):
+//   router      (9)  logits = ln1 wr^T (fp32), softmax, top-k, renormalised weights
+//   permute     (10) capacity-slot assignment in (token, k) order + row gather
+//   unpermute   (15) out[t] = sum_k w[t,k] y[slot(t,k)]       (k ascending, fp32)
+//   unpermute_bwd (21), permute_bwd (28), router_bwd (29)
+// The expert FFNs (expert_fc1 / expert_fc2 and their grads) are per-expert
+// tcgen05 GEMMs (gemm_tcgen05.cu) over the contiguous slot block of each
+// expert; the all-to-alls are collectives (runtime/context.cpp).
+//
+// Slot layout: expert e owns slots [e*C, (e+1)*C) of a [E*C, hidden] row block,
+// so expert-major blocks are contiguous and the rows bound for EP rank r
+// (experts [r*E_loc, (r+1)*E_loc)) form one contiguous chunk. Empty slots are
+// zero rows (their GEMM rows contribute nothing to any gradient).
+//
+// HBM-bound row kernels, warp per row, 16-byte vectors; every reduction has a
+// fixed order and no atomics, so results are bit-reproducible (SI == sequential).
+// The fp32 sums mirror oracle/layer_oracle.py MoEOracle term by term
+// (__fmul_rn / __fadd_rn so no FMA contraction changes the rounding).
+#include <algorithm>
+
+#include "common.cuh"
+#include "dh_capi.h"
+
+namespace dh {
+namespace {
+
+constexpr int kMaxExperts = 64;
+constexpr int kMaxTopk = 8;
+constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ long long warp_id_global() {
+    return (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+}
+__device__ __forceinline__ long long warps_total() {
+    return static_cast<long long>(gridDim.x) * blockDim.x / 32;
+}
+
+// ---------------------------------------------------------------- router fwd
+// One warp per token. Each lane owns 8-column vectors c = lane, lane+32, ...;
+// logits[e] = warp_sum of its partial dots (E <= 64, two passes of 32).
+template <int EB>  // experts handled per pass (register block)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    router_fwd_kernel(const uint4* __restrict__ x, const uint4* __restrict__ wr, float* __restrict__ probs,
+                      int* __restrict__ ids, float* __restrict__ wts, int tokens, int hvec, int E, int K) {
+    const int lane = threadIdx.x & 31;
+    for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
+        const uint4* xr = x + t * hvec;
+        float logit[kMaxExperts];
+        for (int e0 = 0; e0 < E; e0 += EB) {
+            float acc[EB];
+#pragma unroll
+            for (int j = 0; j < EB; ++j) acc[j] = 0.f;
+            for (int c = lane; c < hvec; c += 32) {
+                float xv[8];
+                unpack8(xr[c], xv);
+#pragma unroll
+                for (int j = 0; j < EB; ++j) {
+                    if (e0 + j < E) {
+                        float wv[8];
+                        unpack8(__ldg(wr + static_cast<long long>(e0 + j) * hvec + c), wv);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) acc[j] = fmaf(xv[i], wv[i], acc[j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < EB; ++j) {
+                const float v = warp_sum(acc[j]);
+                if (e0 + j < E) logit[e0 + j] = v;
+            }
+        }
+        // softmax over E (every lane holds every logit)
+        float mx = logit[0];
+        for (int e = 1; e < E; ++e) mx = fmaxf(mx, logit[e]);
+        float sum = 0.f;
+        for (int e = 0; e < E; ++e) {
+            logit[e] = expf(logit[e] - mx);
+            sum = __fadd_rn(sum, logit[e]);
+        }
+        for (int e = 0; e < E; ++e) logit[e] = __fdiv_rn(logit[e], sum);
+        for (int e = lane; e < E; e += 32) probs[t * E + e] = logit[e];
+        // top-k by probability, ties to the lower expert id (stable argsort of -p)
+        if (lane == 0) {
+            unsigned long long taken = 0ull;
+            int sel[kMaxTopk];
+            float top[kMaxTopk];
+            float tsum = 0.f;
+            for (int k = 0; k < K; ++k) {
+                int best = -1;
+                float bv = 0.f;
+                for (int e = 0; e < E; ++e) {
+                    if (taken >> e & 1ull) continue;
+                    if (best < 0 || logit[e] > bv) {
+                        best = e;
+                        bv = logit[e];
+                    }
+                }
+                taken |= 1ull << best;
+                sel[k] = best;
+                top[k] = bv;
+                tsum = __fadd_rn(tsum, bv);
+            }
+            for (int k = 0; k < K; ++k) {
+                ids[t * K + k] = sel[k];
+                wts[t * K + k] = __fdiv_rn(top[k], tsum);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- slot assignment
+// One block per expert scans the (token, k) assignments in order; the running
+// count gives each of its assignments a slot (or drops it past capacity).
+constexpr int kAssignThreads = 1024;
+
+__global__ void __launch_bounds__(kAssignThreads)
+    assign_kernel(const int* __restrict__ ids, int n_assign, int C, int* __restrict__ slot,
+                  int* __restrict__ slot_src) {
+    __shared__ int warp_cnt[kAssignThreads / 32];
+    __shared__ int base_sh;
+    const int e = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) base_sh = 0;
+    __syncthreads();
+    for (int a0 = 0; a0 < n_assign; a0 += kAssignThreads) {
+        const int a = a0 + threadIdx.x;
+        const bool mine = a < n_assign && ids[a] == e;
+        const unsigned ball = __ballot_sync(0xffffffffu, mine);
+        if (lane == 0) warp_cnt[w] = __popc(ball);
+        __syncthreads();
+        int before = base_sh;
+        for (int i = 0; i < w; ++i) before += warp_cnt[i];
+        const int rank = before + __popc(ball & ((1u << lane) - 1u));
+        if (mine) {
+            if (rank < C) {
+                slot[a] = e * C + rank;
+                slot_src[e * C + rank] = a;
+            } else {
+                slot[a] = -1;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int i = 0; i < kAssignThreads / 32; ++i) tot += warp_cnt[i];
+            base_sh += tot;
+        }
+        __syncthreads();
+    }
+    for (int j = min(base_sh, C) + threadIdx.x; j < C; j += kAssignThreads) slot_src[e * C + j] = -1;
+}
+
+// ---------------------------------------------------------------- permute
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    permute_kernel(const uint4* __restrict__ x, const int* __restrict__ slot_src, uint4* __restrict__ xp,
+                   int n_slots, int K, int hvec) {
+    const int lane = threadIdx.x & 31;
+    for (long long s = warp_id_global(); s < n_slots; s += warps_total()) {
+        const int a = slot_src[s];
+        uint4* dst = xp + s * hvec;
+        if (a < 0) {
+            for (int c = lane; c < hvec; c += 32) dst[c] = make_uint4(0, 0, 0, 0);
+        } else {
+            const uint4* src = x + static_cast<long long>(a / K) * hvec;
+            for (int c = lane; c < hvec; c += 32) dst[c] = src[c];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- unpermute (weighted combine)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    unpermute_kernel(const uint4* __restrict__ y, const int* __restrict__ slot, const float* __restrict__ wts,
+                     uint4* __restrict__ out, int tokens, int K, int hvec) {
+    const int lane = threadIdx.x & 31;
+    for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
+        int sl[kMaxTopk];
+        float w[kMaxTopk];
+        for (int k = 0; k < K; ++k) {
+            sl[k] = slot[t * K + k];
+            w[k] = wts[t * K + k];
+        }
+        for (int c = lane; c < hvec; c += 32) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int k = 0; k < K; ++k) {
+                if (sl[k] < 0) continue;
+                float v[8];
+                unpack8(y[static_cast<long long>(sl[k]) * hvec + c], v);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w[k], v[i]));
+            }
+            out[t * hvec + c] = pack8(acc);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- unpermute bwd
+// dys[s] = bf16(w * dy[t]); dw[a] = <y[s], dy[t]> for the assignment a in slot s.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    unpermute_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ y,
+                         const int* __restrict__ slot_src, const float* __restrict__ wts,
+                         uint4* __restrict__ dys, float* __restrict__ dw, int n_slots, int K, int hvec) {
+    const int lane = threadIdx.x & 31;
+    for (long long s = warp_id_global(); s < n_slots; s += warps_total()) {
+        const int a = slot_src[s];
+        uint4* dst = dys + s * hvec;
+        if (a < 0) {
+            for (int c = lane; c < hvec; c += 32) dst[c] = make_uint4(0, 0, 0, 0);
+            continue;
+        }
+        const float w = wts[a];
+        const uint4* g = dy + static_cast<long long>(a / K) * hvec;
+        const uint4* yr = y + s * hvec;
+        float dot = 0.f;
+        for (int c = lane; c < hvec; c += 32) {
+            float gv[8], yv[8], o[8];
+            unpack8(g[c], gv);
+            unpack8(yr[c], yv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                o[i] = __fmul_rn(w, gv[i]);
+                dot = fmaf(yv[i], gv[i], dot);
+            }
+            dst[c] = pack8(o);
+        }
+        dot = warp_sum(dot);
+        if (lane == 0) dw[a] = dot;
+    }
+}
+
+// ---------------------------------------------------------------- permute bwd
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    permute_bwd_kernel(const uint4* __restrict__ dxp, const int* __restrict__ slot, uint4* __restrict__ dx,
+                       int tokens, int K, int hvec) {
+    const int lane = threadIdx.x & 31;
+    for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
+        int sl[kMaxTopk];
+        for (int k = 0; k < K; ++k) sl[k] = slot[t * K + k];
+        for (int c = lane; c < hvec; c += 32) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int k = 0; k < K; ++k) {
+                if (sl[k] < 0) continue;
+                float v[8];
+                unpack8(dxp[static_cast<long long>(sl[k]) * hvec + c], v);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], v[i]);
+            }
+            dx[t * hvec + c] = pack8(acc);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- router bwd
+// Per token: dtop = dw/ssum - <dw, top>/ssum^2 through the renormalisation,
+// dp scattered to the chosen experts, dlogits = p * (dp - <p, dp>) (softmax),
+// then dx = bf16(dx_in + dlogits wr). Dropped assignments carry dw = 0.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    router_bwd_kernel(const float* __restrict__ probs, const int* __restrict__ ids, const int* __restrict__ slot,
+                      const float* __restrict__ dw, const uint4* __restrict__ wr, const uint4* __restrict__ dx_in,
+                      uint4* __restrict__ dx_out, float* __restrict__ dlogits, int tokens, int E, int K, int hvec) {
+    const int lane = threadIdx.x & 31;
+    for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
+        // every lane computes the (tiny) per-token math redundantly
+        float dwk[kMaxTopk], top[kMaxTopk];
+        int id[kMaxTopk];
+        float ssum = 0.f, dot = 0.f;
+        for (int k = 0; k < K; ++k) {
+            id[k] = ids[t * K + k];
+            top[k] = probs[t * E + id[k]];
+            dwk[k] = slot[t * K + k] >= 0 ? dw[t * K + k] : 0.f;
+            ssum = __fadd_rn(ssum, top[k]);
+            dot = __fadd_rn(dot, __fmul_rn(dwk[k], top[k]));
+        }
+        const float ss2 = __fmul_rn(ssum, ssum);
+        float pdp = 0.f;  // <p, dp>: only the chosen experts have dp != 0
+        float dtop[kMaxTopk];
+        for (int k = 0; k < K; ++k) {
+            dtop[k] = __fsub_rn(__fdiv_rn(dwk[k], ssum), __fdiv_rn(dot, ss2));
+        }
+        // <p, dp> summed in expert order (numpy's row sum order over E)
+        for (int e = 0; e < E; ++e) {
+            for (int k = 0; k < K; ++k)
+                if (id[k] == e) pdp = __fadd_rn(pdp, __fmul_rn(top[k], dtop[k]));
+        }
+        // dlogits[e] for the lane's experts; wr rows combined into dx below
+        float dl[kMaxExperts];
+        for (int e = 0; e < E; ++e) {
+            float dp = 0.f;
+            for (int k = 0; k < K; ++k)
+                if (id[k] == e) dp = dtop[k];
+            const float p = probs[t * E + e];
+            dl[e] = __fmul_rn(p, __fsub_rn(dp, pdp));
+        }
+        for (int e = lane; e < E; e += 32) dlogits[t * E + e] = dl[e];
+        for (int c = lane; c < hvec; c += 32) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int e = 0; e < E; ++e) {
+                float wv[8];
+                unpack8(__ldg(wr + static_cast<long long>(e) * hvec + c), wv);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = fmaf(dl[e], wv[i], acc[i]);
+            }
+            float base[8];
+            unpack8(dx_in[t * hvec + c], base);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(base[i], acc[i]);
+            dx_out[t * hvec + c] = pack8(acc);
+        }
+    }
+}
+
+// dwr[E, H] partials: block (column block of 256, token split); thread = one
+// column, E accumulators. partial[split][e][col].
+constexpr int kDwrCols = 256;
+constexpr int kDwrTok = 32;  // tokens staged per smem round
+
+__global__ void __launch_bounds__(kDwrCols)
+    router_dwr_partial_kernel(const float* __restrict__ dlogits, const __nv_bfloat16* __restrict__ x,
+                              float* __restrict__ partial, int tokens, int H, int E, int tok_per_split) {
+    __shared__ float dl[kDwrTok][kMaxExperts];
+    const int col = blockIdx.x * kDwrCols + threadIdx.x;
+    const int t0 = blockIdx.y * tok_per_split, t1 = min(tokens, t0 + tok_per_split);
+    float acc[kMaxExperts];
+#pragma unroll
+    for (int e = 0; e < kMaxExperts; ++e) acc[e] = 0.f;
+    for (int tb = t0; tb < t1; tb += kDwrTok) {
+        const int nt = min(kDwrTok, t1 - tb);
+        __syncthreads();
+        for (int i = threadIdx.x; i < nt * E; i += kDwrCols) dl[i / E][i % E] = dlogits[(tb + i / E) * static_cast<long long>(E) + i % E];
+        __syncthreads();
+        for (int j = 0; j < nt; ++j) {
+            const float xv = col < H ? __bfloat162float(x[static_cast<long long>(tb + j) * H + col]) : 0.f;
+#pragma unroll
+            for (int e = 0; e < kMaxExperts; ++e)
+                if (e < E) acc[e] = fmaf(dl[j][e], xv, acc[e]);
+        }
+    }
+    if (col < H) {
+        float* p = partial + static_cast<long long>(blockIdx.y) * E * H;
+#pragma unroll
+        for (int e = 0; e < kMaxExperts; ++e)
+            if (e < E) p[static_cast<long long>(e) * H + col] = acc[e];
+    }
+}
+
+__global__ void router_dwr_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dwr, int splits,
+                                         long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float s = 0.f;
+        for (int j = 0; j < splits; ++j) s += partial[j * n + i];
+        dwr[i] += s;
+    }
+}
+
+int row_grid(long long rows) {
+    const long long b = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    return static_cast<int>(std::max<long long>(1, std::min<long long>(b, 148LL * 16)));
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int dwr_splits(int tokens, int H) {
+    const int col_blocks = (H + kDwrCols - 1) / kDwrCols;
+    int splits = std::max(1, (2 * 148 + col_blocks - 1) / col_blocks);
+    return std::min(splits, std::max(1, tokens / kDwrTok));
+}
+
+}  // namespace
+}  // namespace dh
+
+using namespace dh;
+
+extern "C" {
+
+int dh_moe_router_fwd(const void* x, const void* wr, float* probs, int* ids, float* wts, int tokens,
+                      int hidden, int experts, int topk, void* stream) {
+    if (experts < 2 || experts > kMaxExperts || topk < 1 || topk > kMaxTopk || topk > experts)
+        return set_error(DH_ERR_INVALID, "moe_router_fwd: 2 <= experts <= 64, 1 <= topk <= min(8, experts)");
+    if (hidden % 8 || !al16(x) || !al16(wr)) return set_error(DH_ERR_INVALID, "moe_router_fwd: hidden % 8, 16-B alignment");
+    if (tokens <= 0) return DH_OK;
+    router_fwd_kernel<16><<<row_grid(tokens), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(x), static_cast<const uint4*>(wr), probs, ids, wts, tokens, hidden / 8,
+        experts, topk);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_moe_assign(const int* ids, int tokens, int topk, int experts, int capacity, int* slot, int* slot_src,
+                  void* stream) {
+    if (experts < 1 || capacity < 1) return set_error(DH_ERR_INVALID, "moe_assign: experts, capacity >= 1");
+    assign_kernel<<<experts, kAssignThreads, 0, static_cast<cudaStream_t>(stream)>>>(ids, tokens * topk, capacity,
+                                                                                   slot, slot_src);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_moe_permute(const void* x, const int* slot_src, void* xp, int n_slots, int topk, int hidden, void* stream) {
+    if (hidden % 8 || !al16(x) || !al16(xp)) return set_error(DH_ERR_INVALID, "moe_permute: hidden % 8, 16-B alignment");
+    if (n_slots <= 0) return DH_OK;
+    permute_kernel<<<row_grid(n_slots), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(x), slot_src, static_cast<uint4*>(xp), n_slots, topk, hidden / 8);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_moe_unpermute(const void* y, const int* slot, const float* wts, void* out, int tokens, int topk, int hidden,
+                     void* stream) {
+    if (hidden % 8 || topk > kMaxTopk || !al16(y) || !al16(out))
+        return set_error(DH_ERR_INVALID, "moe_unpermute: hidden % 8, topk <= 8, 16-B alignment");
+    if (tokens <= 0) return DH_OK;
+    unpermute_kernel<<<row_grid(tokens), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(y), slot, wts, static_cast<uint4*>(out), tokens, topk, hidden / 8);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_moe_unpermute_bwd(const void* dy, const void* y, const int* slot_src, const float* wts, void* dys, float* dw,
+                         int n_slots, int topk, int hidden, void* stream) {
+    if (hidden % 8 || !al16(dy) || !al16(y) || !al16(dys))
+        return set_error(DH_ERR_INVALID, "moe_unpermute_bwd: hidden % 8, 16-B alignment");
+    if (n_slots <= 0) return DH_OK;
+    unpermute_bwd_kernel<<<row_grid(n_slots), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(dy), static_cast<const uint4*>(y), slot_src, wts, static_cast<uint4*>(dys), dw,
+        n_slots, topk, hidden / 8);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_moe_permute_bwd(const void* dxp, const int* slot, void* dx, int tokens, int topk, int hidden, void* stream) {
+    if (hidden % 8 || topk > kMaxTopk || !al16(dxp) || !al16(dx))
+        return set_error(DH_ERR_INVALID, "moe_permute_bwd: hidden % 8, topk <= 8, 16-B alignment");
+    if (tokens <= 0) return DH_OK;
+    permute_bwd_kernel<<<row_grid(tokens), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(dxp), slot, static_cast<uint4*>(dx), tokens, topk, hidden / 8);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+long long dh_moe_router_bwd_scratch_floats(int tokens, int hidden, int experts) {
+    return static_cast<long long>(tokens) * experts +
+           static_cast<long long>(dwr_splits(tokens, hidden)) * experts * hidden;
+}
+
+int dh_moe_router_bwd(const float* probs, const int* ids, const int* slot, const float* dw, const void* x,
+                      const void* wr, const void* dx_in, void* dx_out, float* dwr, float* scratch, int tokens,
+                      int hidden, int experts, int topk, void* stream) {
+    if (experts < 2 || experts > kMaxExperts || topk < 1 || topk > kMaxTopk)
+        return set_error(DH_ERR_INVALID, "moe_router_bwd: 2 <= experts <= 64, 1 <= topk <= 8");
+    if (hidden % 8 || !al16(x) || !al16(wr) || !al16(dx_in) || !al16(dx_out))
+        return set_error(DH_ERR_INVALID, "moe_router_bwd: hidden % 8, 16-B alignment");
+    if (tokens <= 0) return DH_OK;
+    auto s = static_cast<cudaStream_t>(stream);
+    float* dlogits = scratch;
+    float* partial = scratch + static_cast<long long>(tokens) * experts;
+    router_bwd_kernel<<<row_grid(tokens), kWarpsPerBlock * 32, 0, s>>>(
+        probs, ids, slot, dw, static_cast<const uint4*>(wr), static_cast<const uint4*>(dx_in),
+        static_cast<uint4*>(dx_out), dlogits, tokens, experts, topk, hidden / 8);
+    DH_CUDA_CHECK(cudaGetLastError());
+    const int splits = dwr_splits(tokens, hidden);
+    const int per = (tokens + splits - 1) / splits;
+    const dim3 grid((hidden + kDwrCols - 1) / kDwrCols, splits);
+    router_dwr_partial_kernel<<<grid, kDwrCols, 0, s>>>(dlogits, static_cast<const __nv_bfloat16*>(x), partial,
+                                                        tokens, hidden, experts, per);
+    DH_CUDA_CHECK(cudaGetLastError());
+    const long long n = static_cast<long long>(experts) * hidden;
+    router_dwr_reduce_kernel<<<static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(
+        partial, dwr, splits, n);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+}  // extern "C"

@@ -11,7 +11,31 @@ using nlohmann::json;
 namespace dh {
 
 // Kernels this repo launches for one node (NCCL kernels and memcpys excluded).
+namespace {
+int dense_kernels(const Model& m, int node, int layer);
+}
+
 int kernels_per_node(const Model& m, int node, int layer) {
+    if (m.cfg.moe && node < kOptNode) {
+        const int el = m.cfg.e_loc;
+        switch (node) {
+            case 9: case 15: case 21: case 28: return 1;
+            case 10: return 2;                      // assign + gather
+            case 13: case 23: case 24: return el;   // one GEMM per local expert
+            case 12: case 25: case 26: return 2 * el;
+            case 29: return 3;                      // token pass, dwr partials, reduce
+            case 11: case 14: case 22: case 27: return 0;  // all-to-all (NCCL / copies)
+            default: {
+                const int d = moe_dense_id(node);
+                return d < 0 ? 0 : dense_kernels(m, d, layer);
+            }
+        }
+    }
+    return dense_kernels(m, node, layer);
+}
+
+namespace {
+int dense_kernels(const Model& m, int node, int layer) {
     const bool group = m.cfg.nq_l != m.cfg.nkv_l;
     switch (node) {
         case 10: case 11: {  // (+ standalone SwiGLU on the later of the two when not in its epilogue)
@@ -46,6 +70,7 @@ int kernels_per_node(const Model& m, int node, int layer) {
             return 0;  // collectives (NCCL / loopback copies) and memcpy pass-throughs
     }
 }
+}  // namespace
 
 }  // namespace dh
 
@@ -112,6 +137,11 @@ int find_tensor(dh::Model& m, const std::string& name, int layer, int strand, Te
     else if (t == "wg") off = p.wg, n = F * H;
     else if (t == "wu") off = p.wu, n = F * H;
     else if (t == "wd") off = p.wd, n = H * F;
+    // MoE: router [E,H]; stacked local experts w1g / w1u [e_loc,F,H], w2 [e_loc,H,F]
+    else if (k.moe && t == "wr") off = p.wr, n = static_cast<long long>(k.experts) * H;
+    else if (k.moe && t == "w1g") off = p.wg, n = static_cast<long long>(k.e_loc) * F * H;
+    else if (k.moe && t == "w1u") off = p.wu, n = static_cast<long long>(k.e_loc) * F * H;
+    else if (k.moe && t == "w2") off = p.wd, n = static_cast<long long>(k.e_loc) * H * F;
     else if (kind != "act") return bad("unknown parameter");
     if (kind == "w") {
         r->ptr = m.ptr<char>(m.w_bf16) + off * 2;
@@ -141,7 +171,10 @@ int find_tensor(dh::Model& m, const std::string& name, int layer, int strand, Te
             {"out", {&s.out, 0}},       {"rstd0", {&s.rstd0, 1}}, {"ln0_full", {&s.ln0_full, 0}},
             {"qkv", {&s.qkv, 0}},       {"o", {&s.o, 0}},         {"lse", {&s.lse, 1}},
             {"x1", {&s.x1, 0}},         {"rstd1", {&s.rstd1, 1}}, {"ln1_full", {&s.ln1_full, 0}},
-            {"gate", {&s.gate, 0}},     {"up", {&s.up, 0}},       {"act", {&s.act, 0}}};
+            {"gate", {&s.gate, 0}},     {"up", {&s.up, 0}},       {"act", {&s.act, 0}},
+            {"probs", {&s.probs, 1}},   {"wts", {&s.wts, 1}},     {"ids", {&s.ids, 1}},
+            {"mslot", {&s.mslot, 1}},   {"slot_src", {&s.slot_src, 1}}, {"xe", {&s.xe, 0}},
+            {"y_moe", {&s.y, 0}}};
         for (const auto& [fname, bd] : fields) {
             if (t == fname) {
                 r->ptr = m.ptr(*bd.first);

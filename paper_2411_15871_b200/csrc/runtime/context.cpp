@@ -65,6 +65,27 @@ public:
         RT_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, comm, s));
         return DH_OK;
     }
+    // Grouped point-to-point: per (peer, group) one chunk each way; messages
+    // between a pair match in issue order (group ascending on both sides).
+    int all_to_all(const void* send, void* recv, size_t chunk, int groups, bool combine,
+                   cudaStream_t s) override {
+        int size = 0;
+        RT_NCCL(ncclCommCount(comm, &size));
+        const auto* sb = static_cast<const char*>(send);
+        auto* rb = static_cast<char*>(recv);
+        const size_t bytes = chunk * 2;
+        RT_NCCL(ncclGroupStart());
+        for (int p = 0; p < size; ++p) {
+            for (int g = 0; g < groups; ++g) {
+                const size_t so = combine ? static_cast<size_t>(g) * size + p : static_cast<size_t>(p) * groups + g;
+                const size_t ro = combine ? static_cast<size_t>(p) * groups + g : static_cast<size_t>(g) * size + p;
+                RT_NCCL(ncclSend(sb + so * bytes, chunk, ncclBfloat16, p, comm, s));
+                RT_NCCL(ncclRecv(rb + ro * bytes, chunk, ncclBfloat16, p, comm, s));
+            }
+        }
+        RT_NCCL(ncclGroupEnd());
+        return DH_OK;
+    }
     bool capturable() const override { return true; }
     const char* name() const override { return "nccl"; }
 };
@@ -81,6 +102,12 @@ public:
         return dh_comm_proxy(send, recv, static_cast<long long>(count), tp, 1, ctas, link_gbs, s);
     }
     int all_reduce_f32(float*, size_t, cudaStream_t) override { return DH_OK; }
+    // the a2a's HBM traffic (every byte read and written once) held for the
+    // (ep-1)/ep of the buffer that crosses NVLink; the copy keeps layouts fixed
+    int all_to_all(const void* send, void* recv, size_t chunk, int groups, bool,
+                   cudaStream_t s) override {
+        return dh_comm_proxy(send, recv, static_cast<long long>(chunk) * groups * tp, tp, 2, ctas, link_gbs, s);
+    }
     bool capturable() const override { return true; }
     const char* name() const override { return "emulated"; }
 };
@@ -210,6 +237,24 @@ public:
         RT_CUDA(cudaFreeAsync(tmp, s));
         // A second barrier: peers must not read our buffer after we overwrite it.
         RT_TRY(rendezvous_ready(buf, s));
+        return rendezvous_done(s);
+    }
+    int all_to_all(const void* send, void* recv, size_t chunk, int groups, bool combine,
+                   cudaStream_t s) override {
+        RT_TRY(rendezvous_ready(send, s));
+        const size_t bytes = chunk * 2;
+        const int size = g->size;
+        for (int p = 0; p < size; ++p) {
+            if (p != rank) RT_CUDA(cudaStreamWaitEvent(s, g->ready[p], 0));
+            for (int q = 0; q < groups; ++q) {
+                // pull peer p's chunk addressed to this rank
+                const size_t so = combine ? static_cast<size_t>(q) * size + rank : static_cast<size_t>(rank) * groups + q;
+                const size_t ro = combine ? static_cast<size_t>(p) * groups + q : static_cast<size_t>(q) * size + p;
+                RT_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + ro * bytes,
+                                        static_cast<const char*>(g->send[p]) + so * bytes, bytes,
+                                        cudaMemcpyDeviceToDevice, s));
+            }
+        }
         return rendezvous_done(s);
     }
     bool capturable() const override { return false; }

@@ -91,6 +91,8 @@ struct Lowering {
         o.capped = capped;
         if (xfer) {
             // nothing node-specific
+        } else if (m.cfg.moe) {
+            // moe_ep ids: no cross-node fusion flags (expert_fc1 fuses its own SwiGLU)
         } else if (node == 10 || node == 11) {
             // both run on the compute lane in sequence order: the later one sees the
             // other's output and applies SwiGLU in its GEMM epilogue
@@ -98,7 +100,7 @@ struct Lowering {
             o.fuse_swiglu = pos_in_fwd.at(node) > pos_in_fwd.at(other) &&
                             lane_of.at(node) == lane_of.at(other);
         }
-        if (!xfer && (node == 24 || node == 25)) {
+        if (!xfer && !m.cfg.moe && (node == 24 || node == 25)) {
             const int other = node == 24 ? 25 : 24;
             o.first_dx = pos_in_bwd.at(node) < pos_in_bwd.at(other);
         }

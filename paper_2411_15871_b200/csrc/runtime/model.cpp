@@ -70,6 +70,23 @@ int derive_cfg(const dh_model_cfg* c, int tp, int rank, ModelCfg* out) {
     k.pp_size = c->pp_size > 0 ? c->pp_size : 1;
     k.tp = tp;
     k.rank = rank;
+    if (c->experts > 1) {
+        // MoE: the group is the EP group; attention and the router run
+        // data-parallel (TP = 1) on this rank's own micro-batches
+        k.moe = true;
+        k.experts = c->experts;
+        k.topk = c->topk > 0 ? c->topk : 2;
+        k.ep = tp;
+        k.ep_rank = rank;
+        k.tp = 1;
+        k.rank = 0;
+        if (k.topk > k.experts || k.topk > 8 || k.experts > 64)
+            return set_error(DH_ERR_CONFIG, "model: MoE needs topk <= min(8, experts), experts <= 64");
+        if (k.experts % k.ep) return set_error(DH_ERR_INFEASIBLE, "model: experts must be divisible by the EP size");
+        k.e_loc = k.experts / k.ep;
+        k.capacity = c->capacity > 0 ? c->capacity : moe_capacity(c->seq_len, k.experts, k.topk);
+        k.moe_rows = k.experts * k.capacity;
+    }
     if (k.split < 0 || k.split >= c->layers || k.slots < 0 || k.pp_rank < 0 || k.pp_rank >= k.pp_size)
         return set_error(DH_ERR_CONFIG, "model: bad pipeline stage fields (split_layer, slots, pp_rank/pp_size)");
     if (k.hidden <= 0 || k.layers <= 0 || k.seq <= 0 || k.micro_batches < 1 || k.head_dim <= 0 ||
@@ -117,6 +134,14 @@ int build_dags(Model& m, const weft::ClusterSpec& cl, const weft::SoloTimeTable*
     weft::ParallelismSpec par;
     par.tp = m.cfg.tp;
     par.sp = m.cfg.tp > 1;
+    if (m.cfg.moe) {  // moe_ep template (reference op_model.cpp:410)
+        ms.name = "dh-moe";
+        ms.family = weft::ModelFamily::phi_moe;
+        ms.experts = m.cfg.experts;
+        ms.topk = m.cfg.topk;
+        par.ep = m.cfg.ep;
+        par.dp = m.cfg.ep;  // the EP group is a subset of the DP group (presets.cpp validate)
+    }
     try {
         auto dags = weft::build_layer_dag(ms, par, cl, solo);
         m.fwd_dag = std::move(dags.first);
@@ -153,12 +178,15 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         off += al(Q * H);
         m->lp[l].wo = off;
         off += al(H * A);
+        const size_t ex = k.moe ? static_cast<size_t>(k.e_loc) : 1;  // stacked local experts
+        m->lp[l].wr = off;
+        off += k.moe ? al(static_cast<size_t>(k.experts) * H) : 0;
         m->lp[l].wg = off;
-        off += al(F * H);
+        off += al(ex * F * H);
         m->lp[l].wu = off;
-        off += al(F * H);
+        off += al(ex * F * H);
         m->lp[l].wd = off;
-        off += al(H * F);
+        off += al(ex * H * F);
     }
     m->n_params = off;
 
@@ -169,6 +197,9 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     m->adam_m = pool.take(off * 4, "state.adam_m");
     m->adam_v = pool.take(off * 4, "state.adam_v");
 
+    // MLP rows: tokens (dense) or this rank's expert slot rows (MoE)
+    const size_t MR = k.moe ? static_cast<size_t>(k.moe_rows) : S;
+    const size_t E = k.experts, K = k.topk;
     m->slots.resize(k.slots > 0 ? k.slots : L + 1);
     for (auto& s : m->slots) {
         s.out = pool.take(T * H * 2, "act.slots");
@@ -180,21 +211,45 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         s.x1 = pool.take(T * H * 2, "act.slots");
         s.rstd1 = pool.take(T * 4, "act.slots");
         s.ln1_full = pool.take(S * H * 2, "act.slots");
-        s.gate = pool.take(S * F * 2, "act.slots");
-        s.up = pool.take(S * F * 2, "act.slots");
-        s.act = pool.take(S * F * 2, "act.slots");
+        s.gate = pool.take(MR * F * 2, "act.slots");
+        s.up = pool.take(MR * F * 2, "act.slots");
+        s.act = pool.take(MR * F * 2, "act.slots");
+        if (k.moe) {
+            s.probs = pool.take(T * E * 4, "act.slots");
+            s.ids = pool.take(T * K * 4, "act.slots");
+            s.wts = pool.take(T * K * 4, "act.slots");
+            s.mslot = pool.take(T * K * 4, "act.slots");
+            s.slot_src = pool.take(MR * 4, "act.slots");
+            s.xe = pool.take(MR * H * 2, "act.slots");
+            s.y = pool.take(MR * H * 2, "act.slots");
+        }
     }
     const bool tp1 = k.tp == 1;
     m->fs.ln_loc = pool.take(tp1 ? 0 : T * H * 2, "act.fwd_transient");
     m->fs.part = pool.take(tp1 ? 0 : S * H * 2, "act.fwd_transient");
     m->fs.rs_out = pool.take(T * H * 2, "act.fwd_transient");
+    const bool a2a = k.moe && k.ep > 1;
+    m->fs.xp = pool.take(a2a ? MR * H * 2 : 0, "act.fwd_transient");
+    m->fs.ye = pool.take(a2a ? MR * H * 2 : 0, "act.fwd_transient");
     auto& b = m->bs;
     b.grad[0] = pool.take(T * H * 2, "act.bwd_transient");
     b.grad[1] = pool.take(T * H * 2, "act.bwd_transient");
     b.d_x1 = pool.take(T * H * 2, "act.bwd_transient");
     b.dy_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
-    b.d_gate = pool.take(S * F * 2, "act.bwd_transient");
-    b.d_up = pool.take(S * F * 2, "act.bwd_transient");
+    b.d_gate = pool.take(MR * F * 2, "act.bwd_transient");
+    b.d_up = pool.take(MR * F * 2, "act.bwd_transient");
+    if (k.moe) {
+        b.dys = pool.take(a2a ? MR * H * 2 : 0, "act.bwd_transient");
+        b.dys_e = pool.take(MR * H * 2, "act.bwd_transient");
+        b.dxe = pool.take(MR * H * 2, "act.bwd_transient");
+        b.dxp = pool.take(a2a ? MR * H * 2 : 0, "act.bwd_transient");
+        b.dln1p = pool.take(T * H * 2, "act.bwd_transient");
+        b.dw = pool.take(T * K * 4, "act.bwd_transient");
+        b.router_scratch = pool.take(
+            static_cast<size_t>(dh_moe_router_bwd_scratch_floats(static_cast<int>(T), static_cast<int>(H),
+                                                                 static_cast<int>(E))) * 4,
+            "act.bwd_transient");
+    }
     {
         // SwiGLU runs in the mlp GEMM epilogues by default. Measured on B200 the
         // standalone kernels after plain GEMMs were no faster even at TP=8
@@ -202,7 +257,7 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         // and lost overlap under SI; DH_SWIGLU_EPILOGUE=0 selects them.
         const char* env = std::getenv("DH_SWIGLU_EPILOGUE");
         m->swiglu_in_epilogue = env ? std::atoi(env) != 0 : true;
-        if (!m->swiglu_in_epilogue) b.d_act = pool.take(S * F * 2, "act.bwd_transient");
+        if (!m->swiglu_in_epilogue) b.d_act = pool.take(MR * F * 2, "act.bwd_transient");
     }
     b.dx_part = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
     b.dx1_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
@@ -241,6 +296,23 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         RT_TRY(dh_fill_bf16(wb + p.g1, 1.f, H, s));
         RT_CUDA(cudaMemcpyAsync(wm + p.g0, ones.data(), H * 4, cudaMemcpyHostToDevice, s));
         RT_CUDA(cudaMemcpyAsync(wm + p.g1, ones.data(), H * 4, cudaMemcpyHostToDevice, s));
+        if (k.moe) {
+            // replicated (data-parallel) attention / router weights: the same on
+            // every EP rank; expert matrices seeded by their global expert id
+            const std::pair<size_t, size_t> rep[] = {{p.wqkv, Q * H}, {p.wo, H * A}, {p.wr, E * H}};
+            for (int t = 0; t < 3; ++t)
+                RT_TRY(dh_init_normal(wb + rep[t].first, wm + rep[t].first, rep[t].second,
+                                      mix(k.seed, l * 16 + t), k.init_std, s));
+            for (int e = 0; e < k.e_loc; ++e) {
+                const int ge = k.ep_rank * k.e_loc + e;
+                const std::pair<size_t, size_t> mats[] = {
+                    {p.wg + e * F * H, F * H}, {p.wu + e * F * H, F * H}, {p.wd + e * H * F, H * F}};
+                for (int t = 0; t < 3; ++t)
+                    RT_TRY(dh_init_normal(wb + mats[t].first, wm + mats[t].first, mats[t].second,
+                                          mix(mix(k.seed, l * 16 + 8 + t), 4096 + ge), k.init_std, s));
+            }
+            continue;
+        }
         const std::pair<size_t, size_t> mats[] = {
             {p.wqkv, Q * H}, {p.wo, H * A}, {p.wg, F * H}, {p.wu, F * H}, {p.wd, H * F}};
         for (int t = 0; t < 5; ++t) {
@@ -250,12 +322,16 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         }
     }
     for (int i = 0; i < k.micro_batches; ++i) {
-        RT_TRY(dh_init_normal(m->ptr(m->mb_in[i]), nullptr, T * H, mix(mix(k.seed, 1000 + i), k.rank), 1.f, s));
-        RT_TRY(dh_init_normal(m->ptr(m->mb_dy[i]), nullptr, T * H, mix(mix(k.seed, 2000 + i), k.rank), 1.f, s));
+        const int r = k.moe ? k.ep_rank : k.rank;  // MoE ranks see different data
+        RT_TRY(dh_init_normal(m->ptr(m->mb_in[i]), nullptr, T * H, mix(mix(k.seed, 1000 + i), r), 1.f, s));
+        RT_TRY(dh_init_normal(m->ptr(m->mb_dy[i]), nullptr, T * H, mix(mix(k.seed, 2000 + i), r), 1.f, s));
     }
     RT_CUDA(cudaStreamSynchronize(s));
 
     RT_TRY(build_dags(*m, default_cluster(), nullptr));
+    // EP > 1: replicated weights need their data-parallel gradient all-reduce
+    // before AdamW, so the optimizer runs after the program
+    if (k.moe && k.ep > 1) m->fuse_optimizer = false;
     *out = m.release();
     return DH_OK;
 }
@@ -344,7 +420,14 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         return comm ? DH_OK : set_error(DH_ERR_CONFIG, "collective node without a communicator");
     };
 
-    switch (op.node) {
+    int node = op.node;
+    if (k.moe) {
+        int dense = -1;
+        RT_TRY(launch_moe_node(m, op, s, dy, &dense));
+        if (dense < 0) return DH_OK;  // an MoE node, launched
+        node = dense;
+    }
+    switch (node) {
         // ---------------------------------------------------------------- forward
         case 0:  // ln0
             return dh_rmsnorm_fwd(x_in, W + p.g0, tp1 ? P(sl.ln0_full) : P(m.fs.ln_loc),
@@ -498,7 +581,7 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
                                 m.ptr<float>(m.opt_hp), s);
         }
         default:
-            return set_error(DH_ERR_CONFIG, "launch_node: unknown template node " + std::to_string(op.node));
+            return set_error(DH_ERR_CONFIG, "launch_node: unknown template node " + std::to_string(node));
     }
 }
 
@@ -509,13 +592,19 @@ int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s) {
         // their sequence shard: sum their gradients (Megatron SP rule).
         RT_TRY(m.ctx->comm->all_reduce_f32(m.ptr<float>(m.w_grad), m.gamma_elems, s));
     }
+    if (k.moe && k.ep > 1 && m.ctx->comm) {
+        // data-parallel replicas (gammas, attention, router): sum over the EP group
+        float* g = m.ptr<float>(m.w_grad);
+        RT_TRY(m.ctx->comm->all_reduce_f32(g, m.gamma_elems, s));
+        for (const auto& p : m.lp) RT_TRY(m.ctx->comm->all_reduce_f32(g + p.wqkv, p.wg - p.wqkv, s));
+    }
     if (!oc || !oc->enabled) return DH_OK;
     // with the per-layer AdamW ops in the program only the gammas remain
     const bool fused = m.fuse_optimizer && m.prog_has_opt;
     const long long n = static_cast<long long>(fused ? m.gamma_elems : m.n_params);
     RT_TRY(dh_adamw(m.ptr<float>(m.w_master), m.ptr(m.w_bf16), m.ptr<float>(m.w_grad), m.ptr<float>(m.adam_m),
                     m.ptr<float>(m.adam_v), n, oc->lr, oc->beta1, oc->beta2, oc->eps, oc->weight_decay,
-                    m.adam_step, 1.f / k.micro_batches, 1, s));
+                    m.adam_step, 1.f / (k.micro_batches * (k.moe ? k.ep : 1)), 1, s));
     if (fused) {  // disarm: a later bare program replay must not update the weights
         dh_adamw_hparams off{};
         RT_TRY(dh_adamw_set_hparams(m.ptr<float>(m.opt_hp), &off, s));
@@ -536,7 +625,7 @@ int arm_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s) {
     hp.weight_decay = oc->weight_decay;
     hp.bc1 = 1.f - std::pow(oc->beta1, static_cast<float>(m.adam_step));  // as dh_adamw
     hp.bc2 = 1.f - std::pow(oc->beta2, static_cast<float>(m.adam_step));
-    hp.grad_scale = 1.f / m.cfg.micro_batches;
+    hp.grad_scale = 1.f / (m.cfg.micro_batches * (m.cfg.moe ? m.cfg.ep : 1));
     hp.enabled = 1;
     return dh_adamw_set_hparams(m.ptr<float>(m.opt_hp), &hp, s);
 }

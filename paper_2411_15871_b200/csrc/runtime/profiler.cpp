@@ -46,7 +46,8 @@ Op node_op(const Model& m, const weft::OpNode& n, bool fwd) {
     o.slot = fwd ? 0 : 1;
     o.prev_slot = -1;
     o.first_dx = true;
-    o.fuse_swiglu = n.id == 11;  // the SwiGLU epilogue is charged to mlp_up (it follows mlp_gate by id)
+    // the SwiGLU epilogue is charged to mlp_up (it follows mlp_gate by id); moe_ep ids differ
+    o.fuse_swiglu = !m.cfg.moe && n.id == 11;
     return o;
 }
 
@@ -120,6 +121,8 @@ int profile_model(Model& m, int iters, std::string* out_json) {
         for (const auto& [id, n] : *table) {
             double us = 0.0;
             RT_TRY(time_solo(m, node_op(m, *n, fwd), iters, &us));
+            // event-timer floor: a sub-microsecond node can read as 0, which Eq. 1 rejects
+            us = std::max(us, 1e-3);
             solo[id] = us;
             try {
                 prof.solo.set(n->cls, n->name, std::max(us, 1e-3));
@@ -139,7 +142,12 @@ int profile_model(Model& m, int iters, std::string* out_json) {
             RT_TRY(time_pair(m, node_op(m, *na, true), node_op(m, *nb, false), iters, &p));
             const double ta = solo[ia], tb = solo[ib];
             const double pc = std::max(p, std::max(ta, tb));  // noise floor (Eq. 1 domain)
-            double e = weft::oef(ta, tb, pc);
+            double e = 0.0;
+            try {
+                e = weft::oef(ta, tb, pc);
+            } catch (const std::exception& ex) {
+                return set_error(DH_ERR_OTHER, ex.what());
+            }
             e = std::clamp(e, -0.05, 1.05);
             auto key = na->cls <= nb->cls ? std::make_pair(na->cls, nb->cls) : std::make_pair(nb->cls, na->cls);
             samples[key].push_back(e);
@@ -180,7 +188,11 @@ int profile_model(Model& m, int iters, std::string* out_json) {
 extern "C" int dh_profile_json(dh_model* m, int iters, char** out) {
     if (!m || !out) return dh::set_error(DH_ERR_INVALID, "null argument");
     std::string s;
-    RT_TRY(dh::profile_model(*m, iters, &s));
+    try {
+        RT_TRY(dh::profile_model(*m, iters, &s));
+    } catch (const std::exception& e) {  // nothing may unwind through the C ABI
+        return dh::set_error(DH_ERR_OTHER, std::string("profiler: ") + e.what());
+    }
     *out = static_cast<char*>(std::malloc(s.size() + 1));
     std::memcpy(*out, s.c_str(), s.size() + 1);
     return DH_OK;

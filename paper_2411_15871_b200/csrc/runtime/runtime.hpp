@@ -50,6 +50,13 @@ public:
     // recv = sum over ranks of send[rank*count .. (rank+1)*count) (bf16)
     virtual int reduce_scatter(const void* send, void* recv, size_t count, cudaStream_t s) = 0;
     virtual int all_reduce_f32(float* buf, size_t count, cudaStream_t s) = 0;
+    // MoE all-to-all of bf16 chunks (`chunk` elements), `groups` chunks per peer:
+    //   dispatch (combine = false): send [dst][g][chunk] -> recv [g][src][chunk]
+    //   combine  (combine = true):  send [g][dst][chunk] -> recv [src][g][chunk]
+    virtual int all_to_all(const void* send, void* recv, size_t chunk, int groups, bool combine,
+                           cudaStream_t s) {
+        return set_error(DH_ERR_CONFIG, std::string(name()) + ": no all-to-all");
+    }
     // point-to-point (pipeline stages): a recv matches the send with the same
     // (peer pair, tag); the two stages may issue different tags in different orders
     virtual int send(const void* buf, size_t bytes, int peer, int tag, cudaStream_t s) {
@@ -87,6 +94,11 @@ struct ModelCfg {
     float rope_theta = 500000.f, eps = 1e-5f;
     unsigned long long seed = 1234;
     float init_std = 0.02f;
+    // MoE (moe_ep template): experts > 1; the context group is the EP group
+    int experts = 0, topk = 0, capacity = 0;
+    bool moe = false;
+    int ep = 1, ep_rank = 0, e_loc = 0;  // EP group, experts held by this rank
+    int moe_rows = 0;                    // experts * capacity: slot rows on either side of the a2a
     // derived (per TP rank)
     int tp = 1, rank = 0;
     int tok_loc = 0;  // seq / tp (sequence-parallel shard)
@@ -100,22 +112,28 @@ struct Buf {
 
 // Saved activations of one (strand, layer): lifetime = forward of that layer
 // to its backward. L+1 of these form the ring shared by both strands.
+// MoE layers add the routing state and the expert-side rows (gate / up / act
+// then hold moe_rows rows: the slot rows of this rank's experts).
 struct Slot {
     Buf out, rstd0, ln0_full, qkv, o, lse, x1, rstd1, ln1_full, gate, up, act;
+    Buf probs, ids, wts, mslot, slot_src, xe, y;  // MoE: router outputs, slot maps, expert in / out
 };
 
 struct FwdScratch {
     Buf ln_loc, part, rs_out;
+    Buf xp, ye;  // MoE with ep > 1: a2a send buffer of the permuted rows, expert outputs
 };
 
 struct BwdScratch {
     Buf grad[2], d_x1, dy_full, d_gate, d_up, d_act, dx_part, dx1_full, d_o, dqkv, attn_scratch,
         ln_partial, rs_out;
+    Buf dys, dys_e, dxe, dxp, dln1p, dw, router_scratch;  // MoE
 };
 
 struct LayerParams {
     // offsets in elements into the flat parameter arrays
-    size_t g0, g1, wqkv, wo, wg, wu, wd;
+    // (MoE: wg / wu / wd are the e_loc stacked expert w1g / w1u / w2, wr the router)
+    size_t g0, g1, wqkv, wo, wr, wg, wu, wd;
 };
 
 struct Model;
@@ -210,6 +228,11 @@ int lower_ops(Model& m, int mode);
 int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out);
 void model_destroy(Model* m);
 int launch_node(Model& m, const Op& op, cudaStream_t s);
+// MoE-only nodes of the moe_ep template (moe.cpp); `dense_id` gets the
+// dense_tp_sp id of a shared (attention / norm / residual) node, else -1.
+int launch_moe_node(Model& m, const Op& op, cudaStream_t s, void* dy, int* dense_id);
+int moe_dense_id(int moe_node);
+int moe_capacity(int tokens, int experts, int topk);
 int lower_program(Model& m, int mode);
 int kernels_per_node(const Model& m, int node, int layer);
 int run_program(Model& m, bool use_graph);

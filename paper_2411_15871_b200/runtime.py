@@ -21,7 +21,8 @@ class ModelCfg(ctypes.Structure):
                 ("head_dim", c_int), ("layers", c_int), ("seq_len", c_int),
                 ("micro_batches", c_int), ("rope_theta", c_float), ("norm_eps", c_float),
                 ("seed", ctypes.c_ulonglong), ("init_std", c_float),
-                ("slots", c_int), ("split_layer", c_int), ("pp_rank", c_int), ("pp_size", c_int)]
+                ("slots", c_int), ("split_layer", c_int), ("pp_rank", c_int), ("pp_size", c_int),
+                ("experts", c_int), ("topk", c_int), ("capacity", c_int)]
 
 
 class OptimCfg(ctypes.Structure):
@@ -157,16 +158,34 @@ class LlamaShape:
     split_layer: int = 0
     pp_rank: int = 0
     pp_size: int = 0
+    # MoE (moe_ep template; 0 = dense): experts, top-k, slots per expert per
+    # source rank (0 = ceil(1.25 * seq * topk / experts) rounded up to 128)
+    experts: int = 0
+    topk: int = 0
+    capacity: int = 0
+
+    @property
+    def moe(self) -> bool:
+        return self.experts > 1
 
     def to_c(self) -> ModelCfg:
         return ModelCfg(self.hidden, self.ffn, self.n_heads, self.n_kv_heads, self.head_dim,
                         self.layers, self.seq_len, self.micro_batches, self.rope_theta,
                         self.norm_eps, self.seed, self.init_std, self.slots, self.split_layer,
-                        self.pp_rank, self.pp_size)
+                        self.pp_rank, self.pp_size, self.experts, self.topk, self.capacity)
 
     def planner_model(self) -> dict:
+        if self.moe:
+            return {"name": "moe", "family": "phi_moe", "hidden": self.hidden,
+                    "intermediate": self.ffn, "layers": self.layers, "seq_len": self.seq_len,
+                    "experts": self.experts, "topk": self.topk or 2}
         return {"name": "llama", "family": "llama", "hidden": self.hidden,
                 "intermediate": self.ffn, "layers": self.layers, "seq_len": self.seq_len}
+
+    def moe_capacity(self) -> int:
+        k = self.topk or 2
+        c = -(-self.seq_len * k * 5 // (4 * self.experts))
+        return self.capacity or (c + 127) // 128 * 128
 
 
 LLAMA3_8B = LlamaShape(hidden=4096, ffn=14336, n_heads=32, n_kv_heads=8, head_dim=128, layers=32,
@@ -180,6 +199,12 @@ GPT3_13B = LlamaShape(hidden=5120, ffn=20480, n_heads=40, n_kv_heads=40, head_di
 # BASELINE.json config 5 (Llama-2-70B-shaped, GQA 64 / 8 heads)
 LLAMA2_70B = LlamaShape(hidden=8192, ffn=28672, n_heads=64, n_kv_heads=8, head_dim=128, layers=80,
                         seq_len=8192, rope_theta=10000.0)
+# BASELINE.json config 4 (Phi-3.5-MoE-shaped: 16 experts top-2, expert ffn 6400,
+# GQA 32 / 8 heads; seq 3072 as the reference's phi presets, presets.cpp phi-42B)
+PHI35_MOE = LlamaShape(hidden=4096, ffn=6400, n_heads=32, n_kv_heads=8, head_dim=128, layers=32,
+                       seq_len=3072, rope_theta=10000.0, experts=16, topk=2)
+TINY_MOE = LlamaShape(hidden=256, ffn=512, n_heads=4, n_kv_heads=2, head_dim=64, layers=2, seq_len=128,
+                      rope_theta=10000.0, experts=4, topk=2)
 
 
 class Model:
@@ -270,4 +295,5 @@ def lower(shape: "LlamaShape", tp: int, plan_json: str | None, mode: str = "si",
     return json.loads(_take_string(p))
 
 
-__all__ = ["lower", "Context", "Model", "LlamaShape", "LLAMA3_8B", "TINY", "DeviceError", "nccl_unique_id"]
+__all__ = ["lower", "Context", "Model", "LlamaShape", "LLAMA3_8B", "TINY", "PHI35_MOE", "TINY_MOE",
+           "DeviceError", "nccl_unique_id"]
