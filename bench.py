@@ -62,6 +62,14 @@ def layer_flops(shape, tp):
     S, H, F, D = shape.seq_len, shape.hidden, shape.ffn, shape.head_dim
     q_out = (shape.n_heads + 2 * shape.n_kv_heads) * D
     a_in = shape.n_heads * D
+    if getattr(shape, "moe", False):
+        # MoE (EP = tp ranks, attention data-parallel): router + the S*topk routed
+        # rows through a 3-matrix SwiGLU expert (capacity padding is not counted)
+        k = shape.topk or 2
+        gemm_fwd = 2.0 * S * H * (q_out + a_in + shape.experts) + 2.0 * S * k * H * 3 * F
+        attn_fwd = 2.0 * S * S * D * shape.n_heads
+        return {"fwd": gemm_fwd + attn_fwd, "bwd": 2 * gemm_fwd + 2.5 * attn_fwd,
+                "gemm_fwd": gemm_fwd, "attn_fwd": attn_fwd}
     gemm_fwd = 2.0 * S * H * (q_out + a_in + 3 * F) / tp
     attn_fwd = 2.0 * S * S * D * shape.n_heads / tp
     return {"fwd": gemm_fwd + attn_fwd, "bwd": 2 * gemm_fwd + 2.5 * attn_fwd,
@@ -73,6 +81,8 @@ def comm_bytes_per_layer_pair(shape, tp):
     op_model.cpp:290-296: tokens*h*2*(tp-1)/tp each)."""
     if tp == 1:
         return 0
+    if getattr(shape, "moe", False):  # 4 EP all-to-alls (op_model.cpp:297-301: tokens*topk*h*2*(ep-1)/ep)
+        return 4 * int(shape.seq_len * (shape.topk or 2) * shape.hidden * 2 * (tp - 1) / tp)
     return 8 * int(shape.seq_len * shape.hidden * 2 * (tp - 1) / tp)
 
 
@@ -266,7 +276,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"b200_profile_tp{tp}_emulated.json"), "w") as f:
         json.dump(prof, f, indent=1)
-    par = {"tp": tp, "sp": True}
+    par = {"tp": 1, "ep": tp, "dp": tp} if shape.moe else {"tp": tp, "sp": True}
     srch = planner.lib().search_si_plan(shape.planner_model(), par, B200_CLUSTER, prof)
     # caps are an API parameter of search_si_plan: the wider search (0.1 s)
     # finds plans with more, finer segments
@@ -286,7 +296,8 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     res = {}
     for name, plan, mode, skip in modes:
         m.set_plan(plan["plan_json"], json.dumps(prof), mode=mode)
-        m.set_overlap_ctas(sms - args.nccl_ctas)
+        m.set_overlap_ctas(getattr(args, "overlap_ctas", None) if getattr(args, "overlap_ctas", None) is not None
+                           else sms - args.nccl_ctas)
         m.set_skip_comm(skip)
         for _ in range(2):
             step()
@@ -307,7 +318,8 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
                                              "si": round(min(v for k, v in res.items() if k.startswith("si")), 3)},
                              "how": "estimate_iteration_time(W for wavelet_rr/dhelix, 1F1B for megatron; p=1) "
                                     "fed with this run's measured profile"}
-    comm_nodes = {"ag0", "rs0", "ag1", "rs1", "rs1_bwd_ag", "ag1_bwd_rs", "rs0_bwd_ag", "ag0_bwd_rs"}
+    comm_nodes = ({"a2a_dispatch", "a2a_combine", "a2a_combine_bwd", "a2a_dispatch_bwd"} if shape.moe else
+                  {"ag0", "rs0", "ag1", "rs1", "rs1_bwd_ag", "ag1_bwd_rs", "rs0_bwd_ag", "ag0_bwd_rs"})
     comm_solo = sum(e["t_us"] for e in prof["solo"] if e["shape"] in comm_nodes)
     pairs = shape.layers * shape.micro_batches
     si_modes = [k for k in res if k.startswith("si")]
@@ -353,7 +365,8 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     m.close()
     ctx.close()
     return {
-        "what": f"TP={tp} per-GPU shapes of the same workload on ONE B200; collectives are proxy kernels "
+        "what": f"{'EP' if shape.moe else 'TP'}={tp} per-GPU shapes of the same workload on ONE B200; "
+                f"collectives are proxy kernels "
                 f"({args.nccl_ctas} CTAs, held for wire bytes / {link:.0f} GB/s); numerics not meaningful",
         "best_si": best,
         "tokens_per_s_tp_group": round(tokens / (res[best] / 1e3), 1),
@@ -546,8 +559,9 @@ def main():
     # collectives, a slice of the layer stack: per-layer-pair metrics)
     other_cfgs = {}
     if world == 1 and tps and not args.no_configs:
-        from paper_2411_15871_b200.runtime import GPT3_13B, LLAMA2_70B
-        for name, base, tpc, nl in (("c3_gpt3_13b_tp4", GPT3_13B, 4, 8), ("c5_llama2_70b_tp4", LLAMA2_70B, 4, 4)):
+        from paper_2411_15871_b200.runtime import GPT3_13B, LLAMA2_70B, PHI35_MOE
+        for name, base, tpc, nl in (("c3_gpt3_13b_tp4", GPT3_13B, 4, 8), ("c5_llama2_70b_tp4", LLAMA2_70B, 4, 4),
+                                    ("c4_phi35_moe_ep8", PHI35_MOE, 8, 4)):
             r = emulated_tp_experiment(args, tpc, timed, full=False, base_shape=base, layers=nl, micro_batches=4)
             other_cfgs[name] = {"layers_in_slice": nl, "micro_batches": 4,
                                 **{k: r[k] for k in ("tokens_per_s_per_gpu", "mfu", "ms_per_step", "layer_pair_us",

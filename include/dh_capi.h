@@ -151,8 +151,9 @@ int dh_dot_loss(const void* y, const void* r, long long n, float* partial, float
  * Nodes of the moe_ep template (reference op_model.cpp:121-169). Slot layout:
  * expert e owns rows [e*C, (e+1)*C) of a [E*C, hidden] block (C = capacity per
  * expert per source rank); assignment a = t*topk + k. Empty slots are zero rows. */
-/* router (9): probs fp32 [T,E] = softmax(x wr^T), ids int32 [T,K] = top-k by
- * probability (ties: lower expert), wts fp32 [T,K] = top / sum(top). E <= 64, K <= 8. */
+/* router (9): probs fp32 [T,E] = softmax(x wr^T) (the logits GEMM on tcgen05, fp32
+ * out), ids int32 [T,K] = top-k by probability (ties: lower expert), wts fp32 [T,K]
+ * = top / sum(top). E <= 64 and a multiple of 4, K <= 8. */
 int dh_moe_router_fwd(const void* x, const void* wr, float* probs, int* ids, float* wts, int tokens,
                       int hidden, int experts, int topk, void* stream);
 /* permute (10), part 1: slot[a] = e*C + (rank of a among expert e's assignments in
@@ -172,8 +173,9 @@ int dh_moe_unpermute_bwd(const void* dy, const void* y, const int* slot_src, con
 int dh_moe_permute_bwd(const void* dxp, const int* slot, void* dx, int tokens, int topk, int hidden,
                        void* stream);
 /* router_bwd (29): through the top-k renormalisation and the softmax (dropped
- * assignments carry no weight gradient); dx_out = bf16(dx_in + dlogits wr),
- * dwr[E,H] += dlogits^T x (fp32, fixed-order). scratch: fp32, at least
+ * assignments carry no weight gradient); dlogits (bf16) then feeds two tcgen05
+ * GEMMs: dx_out = dx_in + dlogits wr (bf16 accumulate; dx_out may equal dx_in),
+ * dwr[E,H] += dlogits^T x (fp32). scratch: fp32, at least
  * dh_moe_router_bwd_scratch_floats(tokens, hidden, experts). */
 long long dh_moe_router_bwd_scratch_floats(int tokens, int hidden, int experts);
 int dh_moe_router_bwd(const float* probs, const int* ids, const int* slot, const float* dw, const void* x,

@@ -17,6 +17,7 @@
 // The fp32 sums mirror oracle/layer_oracle.py MoEOracle term by term
 // (__fmul_rn / __fadd_rn so no FMA contraction changes the rounding).
 #include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 #include "dh_capi.h"
@@ -36,75 +37,62 @@ __device__ __forceinline__ long long warps_total() {
 }
 
 // ---------------------------------------------------------------- router fwd
-// One warp per token. Each lane owns 8-column vectors c = lane, lane+32, ...;
-// logits[e] = warp_sum of its partial dots (E <= 64, two passes of 32).
-template <int EB>  // experts handled per pass (register block)
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    router_fwd_kernel(const uint4* __restrict__ x, const uint4* __restrict__ wr, float* __restrict__ probs,
-                      int* __restrict__ ids, float* __restrict__ wts, int tokens, int hvec, int E, int K) {
-    const int lane = threadIdx.x & 31;
-    for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
-        const uint4* xr = x + t * hvec;
-        float logit[kMaxExperts];
-        for (int e0 = 0; e0 < E; e0 += EB) {
-            float acc[EB];
+// The logits GEMM (ln1 wr^T, fp32 out) runs on the tensor cores (dh_gemm); this
+// kernel turns a token's logits row into softmax probabilities (in place) and
+// its top-k. Thread per token; loops over kMaxExperts are unrolled so every
+// per-token array stays in registers.
+__global__ void __launch_bounds__(128)
+    router_topk_kernel(float* __restrict__ probs, int* __restrict__ ids, float* __restrict__ wts, int tokens,
+                       int E, int K) {
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= tokens) return;
+    float* row = probs + t * E;
+    float p[kMaxExperts];
+    float mx = -INFINITY;
 #pragma unroll
-            for (int j = 0; j < EB; ++j) acc[j] = 0.f;
-            for (int c = lane; c < hvec; c += 32) {
-                float xv[8];
-                unpack8(xr[c], xv);
+    for (int e = 0; e < kMaxExperts; ++e) {
+        p[e] = e < E ? row[e] : -INFINITY;
+        mx = fmaxf(mx, p[e]);
+    }
+    float sum = 0.f;
 #pragma unroll
-                for (int j = 0; j < EB; ++j) {
-                    if (e0 + j < E) {
-                        float wv[8];
-                        unpack8(__ldg(wr + static_cast<long long>(e0 + j) * hvec + c), wv);
+    for (int e = 0; e < kMaxExperts; ++e) {
+        p[e] = e < E ? expf(p[e] - mx) : 0.f;
+        sum = __fadd_rn(sum, p[e]);
+    }
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) acc[j] = fmaf(xv[i], wv[i], acc[j]);
-                    }
-                }
-            }
+    for (int e = 0; e < kMaxExperts; ++e) {
+        p[e] = __fdiv_rn(p[e], sum);
+        if (e < E) row[e] = p[e];
+    }
+    // top-k by probability, ties to the lower expert id (stable argsort of -p)
+    unsigned long long taken = 0ull;
+    int sel[kMaxTopk];
+    float top[kMaxTopk];
+    float tsum = 0.f;
 #pragma unroll
-            for (int j = 0; j < EB; ++j) {
-                const float v = warp_sum(acc[j]);
-                if (e0 + j < E) logit[e0 + j] = v;
-            }
-        }
-        // softmax over E (every lane holds every logit)
-        float mx = logit[0];
-        for (int e = 1; e < E; ++e) mx = fmaxf(mx, logit[e]);
-        float sum = 0.f;
-        for (int e = 0; e < E; ++e) {
-            logit[e] = expf(logit[e] - mx);
-            sum = __fadd_rn(sum, logit[e]);
-        }
-        for (int e = 0; e < E; ++e) logit[e] = __fdiv_rn(logit[e], sum);
-        for (int e = lane; e < E; e += 32) probs[t * E + e] = logit[e];
-        // top-k by probability, ties to the lower expert id (stable argsort of -p)
-        if (lane == 0) {
-            unsigned long long taken = 0ull;
-            int sel[kMaxTopk];
-            float top[kMaxTopk];
-            float tsum = 0.f;
-            for (int k = 0; k < K; ++k) {
-                int best = -1;
-                float bv = 0.f;
-                for (int e = 0; e < E; ++e) {
-                    if (taken >> e & 1ull) continue;
-                    if (best < 0 || logit[e] > bv) {
-                        best = e;
-                        bv = logit[e];
-                    }
-                }
-                taken |= 1ull << best;
-                sel[k] = best;
-                top[k] = bv;
-                tsum = __fadd_rn(tsum, bv);
-            }
-            for (int k = 0; k < K; ++k) {
-                ids[t * K + k] = sel[k];
-                wts[t * K + k] = __fdiv_rn(top[k], tsum);
+    for (int k = 0; k < kMaxTopk; ++k) {
+        if (k >= K) break;
+        int best = -1;
+        float bv = 0.f;
+#pragma unroll
+        for (int e = 0; e < kMaxExperts; ++e) {
+            if (e >= E || (taken >> e & 1ull)) continue;
+            if (best < 0 || p[e] > bv) {
+                best = e;
+                bv = p[e];
             }
         }
+        taken |= 1ull << best;
+        sel[k] = best;
+        top[k] = bv;
+        tsum = __fadd_rn(tsum, bv);
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxTopk; ++k) {
+        if (k >= K) break;
+        ids[t * K + k] = sel[k];
+        wts[t * K + k] = __fdiv_rn(top[k], tsum);
     }
 }
 
@@ -250,105 +238,53 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }
 
 // ---------------------------------------------------------------- router bwd
-// Per token: dtop = dw/ssum - <dw, top>/ssum^2 through the renormalisation,
-// dp scattered to the chosen experts, dlogits = p * (dp - <p, dp>) (softmax),
-// then dx = bf16(dx_in + dlogits wr). Dropped assignments carry dw = 0.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    router_bwd_kernel(const float* __restrict__ probs, const int* __restrict__ ids, const int* __restrict__ slot,
-                      const float* __restrict__ dw, const uint4* __restrict__ wr, const uint4* __restrict__ dx_in,
-                      uint4* __restrict__ dx_out, float* __restrict__ dlogits, int tokens, int E, int K, int hvec) {
-    const int lane = threadIdx.x & 31;
-    for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
-        // every lane computes the (tiny) per-token math redundantly
-        float dwk[kMaxTopk], top[kMaxTopk];
-        int id[kMaxTopk];
-        float ssum = 0.f, dot = 0.f;
-        for (int k = 0; k < K; ++k) {
-            id[k] = ids[t * K + k];
-            top[k] = probs[t * E + id[k]];
-            dwk[k] = slot[t * K + k] >= 0 ? dw[t * K + k] : 0.f;
-            ssum = __fadd_rn(ssum, top[k]);
-            dot = __fadd_rn(dot, __fmul_rn(dwk[k], top[k]));
-        }
-        const float ss2 = __fmul_rn(ssum, ssum);
-        float pdp = 0.f;  // <p, dp>: only the chosen experts have dp != 0
-        float dtop[kMaxTopk];
-        for (int k = 0; k < K; ++k) {
-            dtop[k] = __fsub_rn(__fdiv_rn(dwk[k], ssum), __fdiv_rn(dot, ss2));
-        }
-        // <p, dp> summed in expert order (numpy's row sum order over E)
-        for (int e = 0; e < E; ++e) {
-            for (int k = 0; k < K; ++k)
-                if (id[k] == e) pdp = __fadd_rn(pdp, __fmul_rn(top[k], dtop[k]));
-        }
-        // dlogits[e] for the lane's experts; wr rows combined into dx below
-        float dl[kMaxExperts];
-        for (int e = 0; e < E; ++e) {
-            float dp = 0.f;
-            for (int k = 0; k < K; ++k)
-                if (id[k] == e) dp = dtop[k];
-            const float p = probs[t * E + e];
-            dl[e] = __fmul_rn(p, __fsub_rn(dp, pdp));
-        }
-        for (int e = lane; e < E; e += 32) dlogits[t * E + e] = dl[e];
-        for (int c = lane; c < hvec; c += 32) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int e = 0; e < E; ++e) {
-                float wv[8];
-                unpack8(__ldg(wr + static_cast<long long>(e) * hvec + c), wv);
+// Per token (thread): dtop = dw/ssum - <dw, top>/ssum^2 through the
+// renormalisation, dp scattered to the chosen experts, dlogits = p * (dp -
+// <p, dp>) through the softmax; written as bf16, the operand of the two
+// router-gradient GEMMs (dx += dlogits wr, dwr += dlogits^T ln1).
+// Dropped assignments carry dw = 0.
+__global__ void __launch_bounds__(128)
+    router_dlogits_kernel(const float* __restrict__ probs, const int* __restrict__ ids, const int* __restrict__ slot,
+                          const float* __restrict__ dw, __nv_bfloat16* __restrict__ dlogits, int ld, int tokens,
+                          int E, int K) {
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= tokens) return;
+    float dwk[kMaxTopk], top[kMaxTopk];
+    int id[kMaxTopk];
+    float ssum = 0.f, dot = 0.f;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc[i] = fmaf(dl[e], wv[i], acc[i]);
-            }
-            float base[8];
-            unpack8(dx_in[t * hvec + c], base);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(base[i], acc[i]);
-            dx_out[t * hvec + c] = pack8(acc);
-        }
+    for (int k = 0; k < kMaxTopk; ++k) {
+        id[k] = -1;
+        dwk[k] = top[k] = 0.f;
+        if (k >= K) continue;
+        id[k] = ids[t * K + k];
+        top[k] = probs[t * E + id[k]];
+        dwk[k] = slot[t * K + k] >= 0 ? dw[t * K + k] : 0.f;
+        ssum = __fadd_rn(ssum, top[k]);
+        dot = __fadd_rn(dot, __fmul_rn(dwk[k], top[k]));
     }
-}
-
-// dwr[E, H] partials: block (column block of 256, token split); thread = one
-// column, E accumulators. partial[split][e][col].
-constexpr int kDwrCols = 256;
-constexpr int kDwrTok = 32;  // tokens staged per smem round
-
-__global__ void __launch_bounds__(kDwrCols)
-    router_dwr_partial_kernel(const float* __restrict__ dlogits, const __nv_bfloat16* __restrict__ x,
-                              float* __restrict__ partial, int tokens, int H, int E, int tok_per_split) {
-    __shared__ float dl[kDwrTok][kMaxExperts];
-    const int col = blockIdx.x * kDwrCols + threadIdx.x;
-    const int t0 = blockIdx.y * tok_per_split, t1 = min(tokens, t0 + tok_per_split);
-    float acc[kMaxExperts];
+    const float ss2 = __fmul_rn(ssum, ssum);
+    float dtop[kMaxTopk];
 #pragma unroll
-    for (int e = 0; e < kMaxExperts; ++e) acc[e] = 0.f;
-    for (int tb = t0; tb < t1; tb += kDwrTok) {
-        const int nt = min(kDwrTok, t1 - tb);
-        __syncthreads();
-        for (int i = threadIdx.x; i < nt * E; i += kDwrCols) dl[i / E][i % E] = dlogits[(tb + i / E) * static_cast<long long>(E) + i % E];
-        __syncthreads();
-        for (int j = 0; j < nt; ++j) {
-            const float xv = col < H ? __bfloat162float(x[static_cast<long long>(tb + j) * H + col]) : 0.f;
+    for (int k = 0; k < kMaxTopk; ++k) dtop[k] = __fsub_rn(__fdiv_rn(dwk[k], ssum), __fdiv_rn(dot, ss2));
+    // <p, dp> in expert order: only the chosen experts have dp != 0
+    float pdp = 0.f;
 #pragma unroll
-            for (int e = 0; e < kMaxExperts; ++e)
-                if (e < E) acc[e] = fmaf(dl[j][e], xv, acc[e]);
-        }
+    for (int e = 0; e < kMaxExperts; ++e) {
+#pragma unroll
+        for (int k = 0; k < kMaxTopk; ++k)
+            if (e < E && id[k] == e) pdp = __fadd_rn(pdp, __fmul_rn(top[k], dtop[k]));
     }
-    if (col < H) {
-        float* p = partial + static_cast<long long>(blockIdx.y) * E * H;
+    const float* pr = probs + t * E;
+    __nv_bfloat16* out = dlogits + t * ld;
 #pragma unroll
-        for (int e = 0; e < kMaxExperts; ++e)
-            if (e < E) p[static_cast<long long>(e) * H + col] = acc[e];
-    }
-}
-
-__global__ void router_dwr_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dwr, int splits,
-                                         long long n) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float s = 0.f;
-        for (int j = 0; j < splits; ++j) s += partial[j * n + i];
-        dwr[i] += s;
+    for (int e = 0; e < kMaxExperts; ++e) {
+        if (e >= E) break;
+        float dp = 0.f;
+#pragma unroll
+        for (int k = 0; k < kMaxTopk; ++k)
+            if (id[k] == e) dp = dtop[k];
+        out[e] = __float2bfloat16_rn(__fmul_rn(pr[e], __fsub_rn(dp, pdp)));
     }
 }
 
@@ -359,11 +295,6 @@ int row_grid(long long rows) {
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int dwr_splits(int tokens, int H) {
-    const int col_blocks = (H + kDwrCols - 1) / kDwrCols;
-    int splits = std::max(1, (2 * 148 + col_blocks - 1) / col_blocks);
-    return std::min(splits, std::max(1, tokens / kDwrTok));
-}
 
 }  // namespace
 }  // namespace dh
@@ -376,11 +307,23 @@ int dh_moe_router_fwd(const void* x, const void* wr, float* probs, int* ids, flo
                       int hidden, int experts, int topk, void* stream) {
     if (experts < 2 || experts > kMaxExperts || topk < 1 || topk > kMaxTopk || topk > experts)
         return set_error(DH_ERR_INVALID, "moe_router_fwd: 2 <= experts <= 64, 1 <= topk <= min(8, experts)");
-    if (hidden % 8 || !al16(x) || !al16(wr)) return set_error(DH_ERR_INVALID, "moe_router_fwd: hidden % 8, 16-B alignment");
     if (tokens <= 0) return DH_OK;
-    router_fwd_kernel<16><<<row_grid(tokens), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4*>(x), static_cast<const uint4*>(wr), probs, ids, wts, tokens, hidden / 8,
-        experts, topk);
+    if (experts % 4) return set_error(DH_ERR_INVALID, "moe_router_fwd: experts % 4 (16-byte logits rows)");
+    // logits = x wr^T on the tensor cores, fp32, into the probability buffer
+    dh_gemm_args g{};
+    g.a = x;
+    g.lda = hidden;
+    g.b = wr;
+    g.ldb = hidden;
+    g.d = probs;
+    g.ldd = experts;
+    g.d_fp32 = 1;
+    g.m = tokens;
+    g.n = experts;
+    g.k = hidden;
+    if (int rc = dh_gemm(&g, stream)) return rc;
+    router_topk_kernel<<<(tokens + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(probs, ids, wts, tokens,
+                                                                                           experts, topk);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }
@@ -437,8 +380,8 @@ int dh_moe_permute_bwd(const void* dxp, const int* slot, void* dx, int tokens, i
 }
 
 long long dh_moe_router_bwd_scratch_floats(int tokens, int hidden, int experts) {
-    return static_cast<long long>(tokens) * experts +
-           static_cast<long long>(dwr_splits(tokens, hidden)) * experts * hidden;
+    (void)hidden;
+    return static_cast<long long>(tokens) * ((experts + 7) / 8 * 8) / 2 + 64;  // bf16 dlogits [T, E] (16-B rows)
 }
 
 int dh_moe_router_bwd(const float* probs, const int* ids, const int* slot, const float* dw, const void* x,
@@ -446,27 +389,45 @@ int dh_moe_router_bwd(const float* probs, const int* ids, const int* slot, const
                       int hidden, int experts, int topk, void* stream) {
     if (experts < 2 || experts > kMaxExperts || topk < 1 || topk > kMaxTopk)
         return set_error(DH_ERR_INVALID, "moe_router_bwd: 2 <= experts <= 64, 1 <= topk <= 8");
-    if (hidden % 8 || !al16(x) || !al16(wr) || !al16(dx_in) || !al16(dx_out))
-        return set_error(DH_ERR_INVALID, "moe_router_bwd: hidden % 8, 16-B alignment");
     if (tokens <= 0) return DH_OK;
+    const int ld = (experts + 7) / 8 * 8;  // row pitch of the bf16 dlogits: a TMA-legal 16-byte multiple
     auto s = static_cast<cudaStream_t>(stream);
-    float* dlogits = scratch;
-    float* partial = scratch + static_cast<long long>(tokens) * experts;
-    router_bwd_kernel<<<row_grid(tokens), kWarpsPerBlock * 32, 0, s>>>(
-        probs, ids, slot, dw, static_cast<const uint4*>(wr), static_cast<const uint4*>(dx_in),
-        static_cast<uint4*>(dx_out), dlogits, tokens, experts, topk, hidden / 8);
+    auto* dl = reinterpret_cast<__nv_bfloat16*>(scratch);
+    router_dlogits_kernel<<<(tokens + 127) / 128, 128, 0, s>>>(probs, ids, slot, dw, dl, ld, tokens, experts, topk);
     DH_CUDA_CHECK(cudaGetLastError());
-    const int splits = dwr_splits(tokens, hidden);
-    const int per = (tokens + splits - 1) / splits;
-    const dim3 grid((hidden + kDwrCols - 1) / kDwrCols, splits);
-    router_dwr_partial_kernel<<<grid, kDwrCols, 0, s>>>(dlogits, static_cast<const __nv_bfloat16*>(x), partial,
-                                                        tokens, hidden, experts, per);
-    DH_CUDA_CHECK(cudaGetLastError());
-    const long long n = static_cast<long long>(experts) * hidden;
-    router_dwr_reduce_kernel<<<static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(
-        partial, dwr, splits, n);
-    DH_CUDA_CHECK(cudaGetLastError());
-    return DH_OK;
+    if (dx_out != dx_in)
+        DH_CUDA_CHECK(cudaMemcpyAsync(dx_out, dx_in, static_cast<size_t>(tokens) * hidden * 2,
+                                      cudaMemcpyDeviceToDevice, s));
+    // dx += dlogits wr   (K = experts)
+    dh_gemm_args g{};
+    g.a = dl;
+    g.lda = ld;
+    g.b = wr;
+    g.ldb = hidden;
+    g.b_mn = 1;
+    g.d = dx_out;
+    g.ldd = hidden;
+    g.m = tokens;
+    g.n = hidden;
+    g.k = experts;
+    g.accumulate = 1;
+    if (int rc = dh_gemm(&g, stream)) return rc;
+    // dwr += dlogits^T x   (fp32 gradient, K = tokens)
+    dh_gemm_args w{};
+    w.a = dl;
+    w.lda = ld;
+    w.a_mn = 1;
+    w.b = x;
+    w.ldb = hidden;
+    w.b_mn = 1;
+    w.d = dwr;
+    w.ldd = hidden;
+    w.d_fp32 = 1;
+    w.m = experts;
+    w.n = hidden;
+    w.k = tokens;
+    w.accumulate = 1;
+    return dh_gemm(&w, stream);
 }
 
 }  // extern "C"

@@ -19,11 +19,12 @@ int kernels_per_node(const Model& m, int node, int layer) {
     if (m.cfg.moe && node < kOptNode) {
         const int el = m.cfg.e_loc;
         switch (node) {
-            case 9: case 15: case 21: case 28: return 1;
+            case 15: case 21: case 28: return 1;
             case 10: return 2;                      // assign + gather
             case 13: case 23: case 24: return el;   // one GEMM per local expert
             case 12: case 25: case 26: return 2 * el;
-            case 29: return 3;                      // token pass, dwr partials, reduce
+            case 9: return 2;                       // logits GEMM + softmax/top-k
+            case 29: return 3;                      // dlogits, dx GEMM, dwr GEMM
             case 11: case 14: case 22: case 27: return 0;  // all-to-all (NCCL / copies)
             default: {
                 const int d = moe_dense_id(node);

@@ -125,7 +125,9 @@ struct Lowering {
     // gradient writer of the layer is on the compute lane ahead of it) and
     // stays off the strand chains, so the backward continues meanwhile.
     void emit_opt(int strand, int layer) {
-        if (!m.fuse_optimizer) return;
+        // EP > 1: the replicated weights' data-parallel all-reduce must precede
+        // their AdamW, so the whole optimizer runs after the program
+        if (!m.fuse_optimizer || (m.cfg.moe && m.cfg.ep > 1)) return;
         Op o;
         o.strand = -1;
         o.layer = layer;

@@ -243,7 +243,6 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         b.dys_e = pool.take(MR * H * 2, "act.bwd_transient");
         b.dxe = pool.take(MR * H * 2, "act.bwd_transient");
         b.dxp = pool.take(a2a ? MR * H * 2 : 0, "act.bwd_transient");
-        b.dln1p = pool.take(T * H * 2, "act.bwd_transient");
         b.dw = pool.take(T * K * 4, "act.bwd_transient");
         b.router_scratch = pool.take(
             static_cast<size_t>(dh_moe_router_bwd_scratch_floats(static_cast<int>(T), static_cast<int>(H),

@@ -166,11 +166,11 @@ int launch_moe_node(Model& m, const Op& op, cudaStream_t s, void* dy, int* dense
             return DH_OK;
         case 27:  // a2a_dispatch_bwd (expert -> source, the combine layout)
             return comm->all_to_all(P(m.bs.dxe), dxp, static_cast<size_t>(C) * H, k.e_loc, true, s);
-        case 28:  // permute_bwd: sum each token's slot gradients
-            return dh_moe_permute_bwd(dxp, I(sl.mslot), P(m.bs.dln1p), T, K, H, s);
-        case 29:  // router_bwd: + the routing path; the total dL/d ln1 goes to ln1_bwd
+        case 28:  // permute_bwd: sum each token's slot gradients (into ln1_bwd's input)
+            return dh_moe_permute_bwd(dxp, I(sl.mslot), P(m.bs.rs_out), T, K, H, s);
+        case 29:  // router_bwd: adds the routing path (tensor-core GEMMs) to dL/d ln1 in place
             return dh_moe_router_bwd(Fp(sl.probs), I(sl.ids), I(sl.mslot), Fp(m.bs.dw), P(sl.ln1_full), W + p.wr,
-                                     P(m.bs.dln1p), P(m.bs.rs_out), G + p.wr, Fp(m.bs.router_scratch), T, H, E,
+                                     P(m.bs.rs_out), P(m.bs.rs_out), G + p.wr, Fp(m.bs.router_scratch), T, H, E,
                                      K, s);
         default:
             return set_error(DH_ERR_CONFIG, "launch_moe_node: unknown moe_ep node " + std::to_string(op.node));

@@ -127,7 +127,7 @@ struct FwdScratch {
 struct BwdScratch {
     Buf grad[2], d_x1, dy_full, d_gate, d_up, d_act, dx_part, dx1_full, d_o, dqkv, attn_scratch,
         ln_partial, rs_out;
-    Buf dys, dys_e, dxe, dxp, dln1p, dw, router_scratch;  // MoE
+    Buf dys, dys_e, dxe, dxp, dw, router_scratch;  // MoE
 };
 
 struct LayerParams {

@@ -282,3 +282,38 @@ def test_ep2_loopback_vs_oracle():
                 err = _rel(outs[r][0]["si"][f"{l}.{name}"].numpy(), ref.reshape(-1))
                 assert err < 3e-2, (r, l, name, err)
 
+
+
+def test_ep2_optimizer_keeps_replicas_identical():
+    """EP = 2 training step with AdamW: the replicated (attention, router, gamma)
+    gradients are all-reduced over the EP group before the update, so both
+    ranks' replicas stay bitwise identical while each rank's experts move."""
+    ep = 2
+    shape = _shape(mb=2)
+    orc = _oracle(shape, seed=23)
+    xs, rs = _inputs(shape, 2 * ep, seed=29)
+    plan = _plan(shape, ep)
+    ctxs = Context.loopback_group(0, ep)
+
+    def rank_main(r):
+        torch.cuda.set_device(0)
+        m = Model(ctxs[r], shape)
+        _load(m, orc, shape, xs[2 * r:2 * r + 2], rs[2 * r:2 * r + 2], ep, r)
+        # fp32 master copies: a 1e-3 step on a ~1.0 gamma is below the bf16 ulp
+        w0 = {n: m.tensor("master." + n, 0).cpu().clone() for n in DENSE_W + MOE_W}
+        m.set_plan(plan, mode="si")
+        m.zero_grads()
+        m.step({"lr": 1e-3}, use_graph=True)
+        m.sync()
+        w1 = {n: m.tensor("master." + n, 0).cpu().clone() for n in DENSE_W + MOE_W}
+        m.close()
+        return w0, w1
+
+    outs = _run_ranks(rank_main, ep)
+    for c in ctxs:
+        c.close()
+    for n in DENSE_W + ("wr",):
+        assert torch.equal(outs[0][1][n], outs[1][1][n]), f"replica {n} diverged across EP ranks"
+    for r in range(ep):
+        for n in DENSE_W + MOE_W:
+            assert not torch.equal(outs[r][0][n], outs[r][1][n]), f"rank {r}: {n} not updated"
