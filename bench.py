@@ -357,7 +357,9 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
                   "how": "exposed(m) = ends + (m-1) * block, from the same plan timed at m and at 2 micro-batches"}
     fl = layer_flops(shape, tp)
     pk = peaks()
-    t_comp = (fl["fwd"] + fl["bwd"]) / (pk["bf16_burst"] * 1e12) * 1e6
+    # a layer pair inside a long step runs at the sustained (power-limited) clock:
+    # the sustained bf16 figure is the compute denominator (B200_PROFILING.md rule)
+    t_comp = (fl["fwd"] + fl["bwd"]) / (pk["bf16_sustained"] * 1e12) * 1e6
     t_comm = comm_bytes_per_layer_pair(shape, tp) / 900e9 * 1e6
     roof = max(t_comp, t_comm)
     lp = res[best] * 1e3 / pairs
@@ -528,7 +530,7 @@ def main():
     per_gpu_tflops = flops_step / (ms_si / 1e3) / 1e12
     # per layer pair (one fwd + one bwd), the BASELINE.md roofline unit
     lp_us = ms_si * 1e3 / (shape.layers * mb)
-    t_comp_us = (fl["fwd"] + fl["bwd"]) / (pk["bf16_burst"] * 1e12) * 1e6
+    t_comp_us = (fl["fwd"] + fl["bwd"]) / (pk["bf16_sustained"] * 1e12) * 1e6
     t_comm_us = comm_bytes_per_layer_pair(shape, tp) / (900e9) * 1e6
     roof_us = max(t_comp_us, t_comm_us)
     gemm_flops = 2.0 * shape.seq_len * shape.hidden * (shape.ffn // tp)
@@ -597,6 +599,8 @@ def main():
         "layer_pair_us": round(lp_us, 1),
         "overlap_roofline_us": round(roof_us, 1),
         "frac_of_overlap_roofline": round(roof_us / lp_us, 4),
+        "overlap_roofline_how": "max(layer-pair FLOPs / sustained bf16 TF/s of MEASURED_PEAKS.json, "
+                                "TP wire bytes / 900 GB/s)",
         "exposed_comm_us_per_layer": None if tp == 1 else "see sequential vs SI",
         "plan": {"hidden_comm_frac_model": srch["hidden_comm_frac"], "total_us_model": srch["total_us"],
                  "search_ms": round(plan_ms, 2), "profile": "measured" if "solo" in profile else

@@ -56,6 +56,16 @@ _SIGS = {
                  c_float, c_float, c_float, c_int, c_float, c_int, c_void_p],
     "dh_init_normal": [c_void_p, c_void_p, c_ll, c_ull, c_float, c_void_p],
     "dh_fill_bf16": [c_void_p, c_float, c_ll, c_void_p],
+    "dh_moe_router_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
+    "dh_moe_assign": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
+    "dh_moe_permute": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p],
+    "dh_moe_unpermute": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p],
+    "dh_moe_unpermute_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                             c_void_p],
+    "dh_moe_permute_bwd": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p],
+    "dh_moe_router_bwd_scratch_floats": [c_int, c_int, c_int],
+    "dh_moe_router_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                          c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
 }
 
 
@@ -77,6 +87,8 @@ def lib():
             fn.restype = c_int
         l.dh_last_error.restype = ctypes.c_char_p
         l.dh_attn_fwd_scratch_floats.restype = c_ll
+        if hasattr(l, "dh_moe_router_bwd_scratch_floats"):
+            l.dh_moe_router_bwd_scratch_floats.restype = c_ll
         _lib = l
     return _lib
 
@@ -187,3 +199,46 @@ def adamw(master, weight, grad, m, v, lr, beta1=0.9, beta2=0.95, eps=1e-8, weigh
     check(lib().dh_adamw(_ptr(master), _ptr(weight), _ptr(grad), _ptr(m), _ptr(v), master.numel(), lr,
                          beta1, beta2, eps, weight_decay, step, grad_scale, int(zero_grad),
                          _stream(stream)))
+
+
+# --------------------------------------------------------------------------- MoE (moe.cu)
+
+def moe_router_fwd(x, wr, probs, ids, wts, topk, stream=None):
+    """probs [T,E] f32 = softmax(x wr^T); ids int32 / wts f32 [T,K] = top-k."""
+    T, H = x.shape
+    check(lib().dh_moe_router_fwd(_ptr(x), _ptr(wr), _ptr(probs), _ptr(ids), _ptr(wts), T, H, wr.shape[0], topk,
+                                  _stream(stream)))
+
+
+def moe_assign(ids, experts, capacity, slot, slot_src, stream=None):
+    T, K = ids.shape
+    check(lib().dh_moe_assign(_ptr(ids), T, K, experts, capacity, _ptr(slot), _ptr(slot_src), _stream(stream)))
+
+
+def moe_permute(x, slot_src, xp, topk, stream=None):
+    check(lib().dh_moe_permute(_ptr(x), _ptr(slot_src), _ptr(xp), xp.shape[0], topk, x.shape[1], _stream(stream)))
+
+
+def moe_unpermute(y, slot, wts, out, stream=None):
+    T, K = slot.shape
+    check(lib().dh_moe_unpermute(_ptr(y), _ptr(slot), _ptr(wts), _ptr(out), T, K, out.shape[1], _stream(stream)))
+
+
+def moe_unpermute_bwd(dy, y, slot_src, wts, dys, dw, topk, stream=None):
+    check(lib().dh_moe_unpermute_bwd(_ptr(dy), _ptr(y), _ptr(slot_src), _ptr(wts), _ptr(dys), _ptr(dw),
+                                     y.shape[0], topk, y.shape[1], _stream(stream)))
+
+
+def moe_permute_bwd(dxp, slot, dx, stream=None):
+    T, K = slot.shape
+    check(lib().dh_moe_permute_bwd(_ptr(dxp), _ptr(slot), _ptr(dx), T, K, dx.shape[1], _stream(stream)))
+
+
+def moe_router_bwd(probs, ids, slot, dw, x, wr, dx_in, dx_out, dwr, stream=None):
+    import torch
+    T, H = x.shape
+    E, K = wr.shape[0], ids.shape[1]
+    n = int(lib().dh_moe_router_bwd_scratch_floats(T, H, E))
+    scratch = torch.empty(n, dtype=torch.float32, device=x.device)
+    check(lib().dh_moe_router_bwd(_ptr(probs), _ptr(ids), _ptr(slot), _ptr(dw), _ptr(x), _ptr(wr), _ptr(dx_in),
+                                  _ptr(dx_out), _ptr(dwr), _ptr(scratch), T, H, E, K, _stream(stream)))
