@@ -488,8 +488,10 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
             return DH_OK;
 
         // ---------------------------------------------------------------- backward
-        case 20:  // bda1_bwd: residual gradient pass-through
-            return dh_copy(P(m.bs.d_x1), dy, TH * 2, s);
+        case 20:  // bda1_bwd: residual gradient pass-through. No kernel: ln1_bwd joins
+            // the skip gradient straight from dy (still intact then: the running-gradient
+            // ping-pong rewrites dy only at the next layer's ln0_bwd)
+            return DH_OK;
         case 21:  // rs1_bwd_ag
             RT_TRY(need_comm());
             return comm->all_gather(dy, P(m.bs.dy_full), TH, s);
@@ -520,12 +522,13 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 27:  // ag1_bwd_rs
             RT_TRY(need_comm());
             return comm->reduce_scatter(P(m.bs.dx_part), P(m.bs.rs_out), TH, s);
-        case 28:  // ln1_bwd (+ residual join into d_x1)
+        case 28:  // ln1_bwd (+ residual join: d_x1 = RMSNorm'(.) + dy)
             return dh_rmsnorm_bwd(P(sl.x1), W + p.g1, m.ptr<float>(sl.rstd1), P(m.bs.rs_out),
-                                  P(m.bs.d_x1), P(m.bs.d_x1), G + p.g1, m.ptr<float>(m.bs.ln_partial),
+                                  dy, P(m.bs.d_x1), G + p.g1, m.ptr<float>(m.bs.ln_partial),
                                   T, H, s);
-        case 29:  // bda0_bwd: skip-connection gradient to the layer input
-            return dh_copy(d_x, P(m.bs.d_x1), TH * 2, s);
+        case 29:  // bda0_bwd: skip-connection gradient to the layer input. No kernel:
+            // ln0_bwd joins it from d_x1 (rewritten only by the next layer's ln1_bwd)
+            return DH_OK;
         case 30:  // rs0_bwd_ag
             RT_TRY(need_comm());
             return comm->all_gather(P(m.bs.d_x1), P(m.bs.dx1_full), TH, s);
@@ -555,8 +558,8 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 37:  // ag0_bwd_rs
             RT_TRY(need_comm());
             return comm->reduce_scatter(P(m.bs.dx_part), P(m.bs.rs_out), TH, s);
-        case 38:  // ln0_bwd (+ join of the attention-block skip gradient)
-            return dh_rmsnorm_bwd(x_in, W + p.g0, m.ptr<float>(sl.rstd0), P(m.bs.rs_out), d_x, d_x,
+        case 38:  // ln0_bwd (+ join of the attention-block skip gradient d_x1)
+            return dh_rmsnorm_bwd(x_in, W + p.g0, m.ptr<float>(sl.rstd0), P(m.bs.rs_out), P(m.bs.d_x1), d_x,
                                   G + p.g0, m.ptr<float>(m.bs.ln_partial), T, H, s);
         case kSendAct:  // output of this visit's last layer -> next stage
             return m.ctx->pp ? m.ctx->pp->send(P(m.slots[op.slot].out), TH * 2, op.peer, xfer_tag(op), s)
