@@ -74,7 +74,9 @@ struct Lowering {
     // every SM; inside a block the cap applies wherever a collective may co-run.
     bool capped = false;
 
-    void emit(int strand, int layer, int node, int peer = -1) {
+    // deps (optional): the op's data predecessors (op indices) replace the
+    // strand-order wait, so a strand can overlap its own independent ops
+    void emit(int strand, int layer, int node, int peer = -1, const std::vector<int>* deps = nullptr) {
         const bool xfer = node >= kSendAct && node <= kRecvGrad;
         // compute-only measurement program: collectives are left out entirely
         if (m.skip_comm && !xfer && lane_of.at(node) != 0) return;
@@ -106,7 +108,14 @@ struct Lowering {
         }
         const int idx = static_cast<int>(prog.ops.size());
         const int prev = strand_last[strand];
-        if (prev >= 0 && prog.ops[prev].lane != o.lane) o.waits.push_back(prev);
+        if (deps) {
+            for (int d : *deps)  // same-lane predecessors are ordered by the stream
+                if (d >= 0 && prog.ops[d].lane != o.lane &&
+                    std::find(o.waits.begin(), o.waits.end(), d) == o.waits.end())
+                    o.waits.push_back(d);
+        } else if (prev >= 0 && prog.ops[prev].lane != o.lane) {
+            o.waits.push_back(prev);
+        }
         if (pending_join[o.lane]) {
             for (int l = 0; l < kLanes; ++l) {
                 if (l != o.lane && join_snapshot[l] >= 0 &&
@@ -158,6 +167,40 @@ struct Lowering {
     }
     void backward_layer(int strand, int layer) {
         for (int id : m.plan.bwd_seq) emit(strand, layer, id);
+        give_slot(strand, layer);
+    }
+    // Backward of a strand that runs alone (the unpaired B_m of the SI
+    // schedule): the plan's order on each lane, but waits on data
+    // predecessors only (the layer DAG's edges; sources wait for the previous
+    // layer's last op), so a collective overlaps its own strand's independent
+    // work — e.g. ag1_bwd_rs under mlp_fc1_wgrad, ag0_bwd_rs under qkv_wgrad.
+    // Every transient buffer's next writer is a DAG or stream-order successor
+    // of its readers (tests/test_executor_lowering.py, buffer hazards). GEMMs
+    // issued while a collective of the layer is still open are capped like
+    // co-running ones.
+    void backward_layer_dag(int strand, int layer) {
+        std::map<int, std::vector<int>> preds;
+        for (const auto& [a, b] : m.bwd_dag.edges) preds[b].push_back(a);
+        std::map<int, int> at;  // node id -> op index
+        std::vector<int> open_comm;  // comm nodes whose consumers are not emitted yet
+        const int prev_last = strand_last[strand];
+        int last = prev_last;
+        for (int id : m.plan.bwd_seq) {
+            std::vector<int> deps;
+            for (int p : preds[id]) deps.push_back(at.at(p));
+            if (deps.empty() && prev_last >= 0) deps.push_back(prev_last);
+            for (int p : preds[id]) open_comm.erase(std::remove(open_comm.begin(), open_comm.end(), p), open_comm.end());
+            const bool comm = lane_of.at(id) != 0;
+            capped = !comm && !open_comm.empty();
+            emit(strand, layer, id, -1, &deps);
+            at[id] = static_cast<int>(prog.ops.size()) - 1;
+            if (comm) open_comm.push_back(id);
+            // the layer's completion point for the next layer's sources: its
+            // compute-lane tail (every comm op feeds a later compute op)
+            if (prog.ops.back().lane == 0) last = at[id];
+        }
+        capped = false;
+        strand_last[strand] = last;
         give_slot(strand, layer);
     }
 
@@ -326,7 +369,7 @@ int lower_ops(Model& m, int mode) {
                     for (int l = 0; l < L; ++l) lw.forward_layer(*blk.fwd_mb - 1, l);
                 } else if (blk.kind == weft::BlockKind::B) {
                     for (int l = L - 1; l >= 0; --l) {
-                        lw.backward_layer(*blk.bwd_mb - 1, l);
+                        lw.backward_layer_dag(*blk.bwd_mb - 1, l);
                         if (*blk.bwd_mb == mb) lw.emit_opt(mb - 1, l);
                     }
                 } else {

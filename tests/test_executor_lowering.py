@@ -247,3 +247,152 @@ def test_w_pipeline_slots_vs_reference_memory_replay():
     for d in range(p):
         prog = lower(_stage_shape(TINY, layers, p, d, mb, slots=8 * layers), 1, plan, "w_pipeline")
         assert dev[d]["peak_bytes"] <= prog["peak_slots"] <= dev[d]["peak_bytes"] + 1, (d, prog["peak_slots"], dev[d])
+
+
+# ---------------------------------------------------------------------------
+# Transient-buffer hazards. The bwd transient set, the fwd transient set and
+# the running-gradient ping-pong are shared by every (strand, layer); each
+# node's reads / writes below restate csrc/runtime/model.cpp launch_node and
+# csrc/runtime/moe.cpp. Every two accesses to one buffer where either writes
+# must be ordered (program order) in the stream + event happens-before graph:
+# RAW, WAR and WAW across lanes, strands and layers, in every executor mode.
+
+def _dense_access(node, tp, L, l, s):
+    """(reads, writes) of shared buffers for one dense op (activation slots excluded)."""
+    t1 = tp == 1
+    dy = f"mb_dy{s}" if l == L - 1 else f"grad{(L - 2 - l) & 1}"
+    dx = f"grad{(L - 1 - l) & 1}"
+    x_in = f"mb_in{s}" if l == 0 else None
+    part = "fs.rs_out" if t1 else "fs.part"
+    dpart = "bs.rs_out" if t1 else "bs.dx_part"
+    R, W = set(), set()
+    if node == 0:
+        R |= {x_in}; W |= set() if t1 else {"fs.ln_loc"}
+    elif node in (1, 9):
+        R |= {"fs.ln_loc"}
+    elif node == 4:
+        R |= {"bs.attn_scratch"}; W |= {"bs.attn_scratch"}
+    elif node in (5, 12):
+        W |= {part}
+    elif node in (6, 13):
+        R |= {"fs.part"}; W |= {"fs.rs_out"}
+    elif node == 7:
+        R |= {x_in, "fs.rs_out"}
+    elif node == 8:
+        W |= set() if t1 else {"fs.ln_loc"}
+    elif node == 14:
+        R |= {"fs.rs_out"} | ({f"mb_dy{s}", "loss"} if l == L - 1 else set())
+        W |= {"loss"} if l == L - 1 else set()
+    elif node == 21:
+        R |= {dy}; W |= {"bs.dy_full"}
+    elif node in (22, 23):
+        R |= {dy if t1 else "bs.dy_full"}; W |= {"bs.d_gate", "bs.d_up"} if node == 22 else set()
+    elif node in (24, 25):
+        R |= {"bs.d_gate", "bs.d_up", dpart}; W |= {dpart}
+    elif node == 26:
+        R |= {"bs.d_gate", "bs.d_up"}
+    elif node in (27, 37):
+        R |= {"bs.dx_part"}; W |= {"bs.rs_out"}
+    elif node == 28:
+        R |= {"bs.rs_out", dy}; W |= {"bs.d_x1", "bs.ln_partial"}
+    elif node == 30:
+        R |= {"bs.d_x1"}; W |= {"bs.dx1_full"}
+    elif node in (31, 32):
+        R |= {"bs.d_x1" if t1 else "bs.dx1_full"}; W |= {"bs.d_o"} if node == 31 else set()
+    elif node == 34:
+        R |= {"bs.d_o", "bs.attn_scratch"}; W |= {"bs.dqkv", "bs.attn_scratch"}
+    elif node == 35:
+        R |= {"bs.dqkv"}; W |= {dpart}
+    elif node == 36:
+        R |= {"bs.dqkv"}
+    elif node == 38:
+        R |= {x_in, "bs.rs_out", "bs.d_x1"}; W |= {dx, "bs.ln_partial"}
+    return R - {None}, W
+
+
+MOE_DENSE = {0: 0, 2: 2, 4: 4, 5: 5, 7: 7, 8: 8, 16: 14, 20: 20, 30: 28, 31: 29, 33: 31, 34: 32, 36: 34, 37: 35,
+             38: 36, 40: 38}
+
+
+def _moe_access(node, ep, L, l, s):
+    if node in MOE_DENSE:
+        return _dense_access(MOE_DENSE[node], 1, L, l, s)
+    a2a = ep > 1
+    dy = f"mb_dy{s}" if l == L - 1 else f"grad{(L - 2 - l) & 1}"
+    R, W = set(), set()
+    if node == 10:
+        W |= {"fs.xp"} if a2a else set()
+    elif node == 11:
+        R |= {"fs.xp"}
+    elif node == 13:
+        W |= {"fs.ye"} if a2a else set()
+    elif node == 14:
+        R |= {"fs.ye"}
+    elif node == 15:
+        W |= {"fs.rs_out"}
+    elif node == 21:
+        R |= {dy}; W |= {"bs.dys" if a2a else "bs.dys_e", "bs.dw"}
+    elif node == 22:
+        R |= {"bs.dys"}; W |= {"bs.dys_e"}
+    elif node in (23, 24):
+        R |= {"bs.dys_e"}; W |= {"bs.d_gate", "bs.d_up"} if node == 23 else set()
+    elif node == 25:
+        R |= {"bs.d_gate", "bs.d_up"}; W |= {"bs.dxe"}
+    elif node == 26:
+        R |= {"bs.d_gate", "bs.d_up"}
+    elif node == 27:
+        R |= {"bs.dxe"}; W |= {"bs.dxp"}
+    elif node == 28:
+        R |= {"bs.dxp" if a2a else "bs.dxe"}; W |= {"bs.rs_out"}
+    elif node == 29:
+        R |= {"bs.dw", "bs.rs_out"}; W |= {"bs.rs_out", "bs.router_scratch"}
+    return R, W
+
+
+def check_buffer_hazards(prog, L, access):
+    ops = prog["ops"]
+    preds = _happens_before(ops)
+    anc = []
+    for i, p in enumerate(preds):
+        a = 0
+        for j in p:
+            a |= anc[j] | (1 << j)
+        anc.append(a)
+    last_w, reads_since = {}, {}
+    for j, o in enumerate(ops):
+        if o["strand"] < 0 or o["node"] >= 100:
+            continue
+        R, W = access(o["node"], L, o["layer"], o["strand"])
+        for b in R | W:
+            w = last_w.get(b)
+            if w is not None:
+                assert anc[j] >> w & 1, f"{b}: op {j} {o} not ordered after writer {w} {ops[w]}"
+        for b in W:
+            for r in reads_since.get(b, ()):
+                assert anc[j] >> r & 1, f"{b}: writer {j} {o} not ordered after reader {r} {ops[r]}"
+        for b in R:
+            reads_since.setdefault(b, []).append(j)
+        for b in W:
+            last_w[b] = j
+            reads_since[b] = []
+
+
+@pytest.mark.parametrize("tp", [1, 2, 4])
+@pytest.mark.parametrize("mode", ["si", "si_relaxed", "sequential"])
+def test_transient_buffer_hazards_dense(tp, mode):
+    shape = LlamaShape(**{**TINY.__dict__, "micro_batches": 3, "n_kv_heads": 4})
+    for arch in ("nvlink_h100", "pcie_a40"):
+        prog = lower(shape, tp, _plan(shape, tp, arch), mode)
+        check_buffer_hazards(prog, shape.layers, lambda n, L, l, s: _dense_access(n, tp, L, l, s))
+
+
+@pytest.mark.parametrize("ep", [1, 2, 4])
+@pytest.mark.parametrize("mode", ["si", "si_relaxed", "sequential"])
+def test_transient_buffer_hazards_moe(ep, mode):
+    from paper_2411_15871_b200.runtime import TINY_MOE
+    shape = LlamaShape(**{**TINY_MOE.__dict__, "micro_batches": 3})
+    for arch in ("nvlink_h100", "pcie_a40"):
+        plan = planner.lib().search_si_plan(shape.planner_model(), {"tp": 1, "ep": ep, "dp": ep}, B200_CLUSTER,
+                                            {"archetype": arch})["plan_json"]
+        prog = lower(shape, ep, plan, mode)
+        check_buffer_hazards(prog, shape.layers, lambda n, L, l, s: _moe_access(n, ep, L, l, s))
