@@ -293,16 +293,23 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
              ("compute_only", srch_wide, "si_relaxed", True), ("sequential", srch_wide, "sequential", False)]
     if not full:
         modes = [x for x in modes if x[0] in ("si", "si_wide_relaxed", "compute_only", "sequential")]
-    res = {}
-    for name, plan, mode, skip in modes:
-        m.set_plan(plan["plan_json"], json.dumps(prof), mode=mode)
-        m.set_overlap_ctas(getattr(args, "overlap_ctas", None) if getattr(args, "overlap_ctas", None) is not None
-                           else sms - args.nccl_ctas)
-        m.set_skip_comm(skip)
-        for _ in range(2):
-            step()
-        res[name] = timed(max(10, 2 * args.steps) if full else max(3, args.steps), step, stream)  # emulated steps are short: more of them for stable deltas
-        log(f"emulated tp{tp} {name}: {res[name]:.1f} ms/step")
+    # The modes are timed in interleaved rounds (a clock drift under the power
+    # cap then biases no mode) and averaged; emulated steps are short, so more
+    # of them are timed for stable differences between modes.
+    rounds, per_round = (2, max(10, 2 * args.steps)) if full else (2, max(4, args.steps))
+    samples = {name: [] for name, *_ in modes}
+    for _ in range(rounds):
+        for name, plan, mode, skip in modes:
+            m.set_plan(plan["plan_json"], json.dumps(prof), mode=mode)
+            m.set_overlap_ctas(getattr(args, "overlap_ctas", None) if getattr(args, "overlap_ctas", None) is not None
+                               else sms - args.nccl_ctas)
+            m.set_skip_comm(skip)
+            for _ in range(2):
+                step()
+            samples[name].append(timed(per_round, step, stream))
+    res = {name: sum(v) / len(v) for name, v in samples.items()}
+    for name in res:
+        log(f"emulated tp{tp} {name}: {res[name]:.1f} ms/step (rounds: {', '.join(f'{x:.1f}' for x in samples[name])})")
     m.set_skip_comm(False)
     # the reference's iteration model (estimate_iteration_time) on the measured
     # profile, next to the measured steps (the model has no optimizer step)

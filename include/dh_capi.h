@@ -82,6 +82,10 @@ int dh_gemm(const dh_gemm_args* args, void* stream);
 /* RMSNorm over the last dim (elementwise.cu). y = x * rstd * gamma, rstd fp32 [rows]. */
 int dh_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols,
                    float eps, void* stream);
+/* Fused residual add + RMSNorm (bda0 + ln1): x_out = bf16(x + resid), y = RMSNorm(x_out);
+ * bitwise dh_add followed by dh_rmsnorm_fwd. resid NULL = dh_rmsnorm_fwd. */
+int dh_add_rmsnorm_fwd(const void* x, const void* resid, void* x_out, const void* gamma, void* y,
+                       float* rstd, int rows, int cols, float eps, void* stream);
 /* dx = RMSNorm'(dy) (+ resid if non-null); dgamma_acc[cols] += sum_rows dy*x*rstd,
  * reduced deterministically through `partial` (fp32, >= 1184*cols floats). */
 int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy,

@@ -16,21 +16,42 @@ namespace {
 
 constexpr int kRowWarps = 8;  // warps per block for row kernels
 
+// Row input of the RMSNorm forward. With a residual `b` (the fused bda0 + ln1
+// node) the input is bf16(x + b), exactly what dh_add stores; it is written to
+// `xo` and normalised from its rounded value, so the fused kernel is bitwise
+// the add kernel followed by the plain RMSNorm.
+__device__ __forceinline__ uint4 norm_input(const uint4* __restrict__ x, const uint4* __restrict__ b,
+                                            uint4* __restrict__ xo, long long i, bool ok) {
+    if (!ok) return make_uint4(0, 0, 0, 0);
+    uint4 u = __ldcs(x + i);
+    if (b) {
+        float p[8], q[8];
+        unpack8(u, p);
+        unpack8(__ldcs(b + i), q);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) p[t] += q[t];
+        u = pack8(p);
+        xo[i] = u;
+    }
+    return u;
+}
+
 // ---------------------------------------------------------------- RMSNorm fwd
 
 template <int V>  // V uint4 (8 bf16) per lane: cols == V * 256
 __global__ void __launch_bounds__(kRowWarps * 32)
     rmsnorm_fwd_reg(const uint4* __restrict__ x, const uint4* __restrict__ g, uint4* __restrict__ y,
-                    float* __restrict__ rstd, int rows, float inv_cols, float eps) {
+                    float* __restrict__ rstd, int rows, float inv_cols, float eps,
+                    const uint4* __restrict__ b = nullptr, uint4* __restrict__ xo = nullptr) {
     const int row = blockIdx.x * kRowWarps + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     if (row >= rows) return;
-    const uint4* xr = x + static_cast<long long>(row) * V * 32;
+    const long long xr = static_cast<long long>(row) * V * 32;
     float v[V][8];
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-        unpack8(xr[i * 32 + lane], v[i]);
+        unpack8(norm_input(x, b, xo, xr + i * 32 + lane, true), v[i]);
 #pragma unroll
         for (int t = 0; t < 8; ++t) ss += v[i][t] * v[i][t];
     }
@@ -54,7 +75,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 template <int VPT, int TPR, int RPB>
 __global__ void __launch_bounds__(TPR * RPB)
     rmsnorm_fwd_split(const uint4* __restrict__ x, const uint4* __restrict__ g, uint4* __restrict__ y,
-                      float* __restrict__ rstd, int rows, float inv_cols, float eps) {
+                      float* __restrict__ rstd, int rows, float inv_cols, float eps,
+                      const uint4* __restrict__ b = nullptr, uint4* __restrict__ xo = nullptr) {
     constexpr int kW = TPR / 32;  // warps per row
     __shared__ float red[RPB][kW];
     const int sub = threadIdx.x / TPR, t = threadIdx.x % TPR;
@@ -65,8 +87,7 @@ __global__ void __launch_bounds__(TPR * RPB)
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-        const uint4 u = ok ? __ldcs(x + base + i * TPR + t) : make_uint4(0, 0, 0, 0);
-        unpack8(u, v[i]);
+        unpack8(norm_input(x, b, xo, base + i * TPR + t, ok), v[i]);
 #pragma unroll
         for (int k = 0; k < 8; ++k) ss += v[i][k] * v[i][k];
     }
@@ -91,15 +112,18 @@ __global__ void __launch_bounds__(TPR * RPB)
 
 __global__ void __launch_bounds__(kRowWarps * 32)
     rmsnorm_fwd_any(const uint4* __restrict__ x, const uint4* __restrict__ g, uint4* __restrict__ y,
-                    float* __restrict__ rstd, int rows, int vec_cols, float inv_cols, float eps) {
+                    float* __restrict__ rstd, int rows, int vec_cols, float inv_cols, float eps,
+                    const uint4* __restrict__ b = nullptr, uint4* __restrict__ xo = nullptr) {
     const int row = blockIdx.x * kRowWarps + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     if (row >= rows) return;
-    const uint4* xr = x + static_cast<long long>(row) * vec_cols;
+    const long long r0 = static_cast<long long>(row) * vec_cols;
+    // the second pass re-reads this thread's own inputs (the fused sum from xo)
+    const uint4* xr = (b ? xo : x) + r0;
     float ss = 0.f;
     for (int i = lane; i < vec_cols; i += 32) {
         float v[8];
-        unpack8(xr[i], v);
+        unpack8(norm_input(x, b, xo, r0 + i, true), v);
 #pragma unroll
         for (int t = 0; t < 8; ++t) ss += v[t] * v[t];
     }
@@ -610,32 +634,41 @@ using namespace dh;
 
 extern "C" {
 
-int dh_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols,
-                   float eps, void* stream) {
-    if (cols % 8 || !aligned16(x) || !aligned16(y) || !aligned16(gamma))
+int dh_add_rmsnorm_fwd(const void* x, const void* resid, void* x_out, const void* gamma, void* y, float* rstd,
+                       int rows, int cols, float eps, void* stream) {
+    if (cols % 8 || !aligned16(x) || !aligned16(y) || !aligned16(gamma) || (resid && (!aligned16(resid) ||
+                                                                                      !aligned16(x_out))))
         return set_error(DH_ERR_INVALID, "rmsnorm_fwd: cols % 8 and 16-byte alignment required");
+    if (resid && !x_out) return set_error(DH_ERR_INVALID, "add_rmsnorm_fwd: x_out required with a residual");
     if (rows <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
     const dim3 grid((rows + kRowWarps - 1) / kRowWarps), block(kRowWarps * 32);
     const auto* X = static_cast<const uint4*>(x);
+    const auto* B = static_cast<const uint4*>(resid);
+    auto* XO = static_cast<uint4*>(x_out);
     const auto* G = static_cast<const uint4*>(gamma);
     auto* Y = static_cast<uint4*>(y);
     const float ic = 1.f / cols;
     switch (cols) {
-        case 256: rmsnorm_fwd_reg<1><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
-        case 512: rmsnorm_fwd_reg<2><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
-        case 1024: rmsnorm_fwd_reg<4><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
-        case 2048: rmsnorm_fwd_reg<8><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps); break;
+        case 256: rmsnorm_fwd_reg<1><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO); break;
+        case 512: rmsnorm_fwd_reg<2><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO); break;
+        case 1024: rmsnorm_fwd_reg<4><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO); break;
+        case 2048: rmsnorm_fwd_reg<8><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO); break;
         case 4096:
-            rmsnorm_fwd_split<4, 128, 2><<<(rows + 1) / 2, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps);
+            rmsnorm_fwd_split<4, 128, 2><<<(rows + 1) / 2, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO);
             break;
         case 8192:
-            rmsnorm_fwd_split<4, 256, 1><<<rows, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps);
+            rmsnorm_fwd_split<4, 256, 1><<<rows, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO);
             break;
-        default: rmsnorm_fwd_any<<<grid, block, 0, s>>>(X, G, Y, rstd, rows, cols / 8, ic, eps);
+        default: rmsnorm_fwd_any<<<grid, block, 0, s>>>(X, G, Y, rstd, rows, cols / 8, ic, eps, B, XO);
     }
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
+}
+
+int dh_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols,
+                   float eps, void* stream) {
+    return dh_add_rmsnorm_fwd(x, nullptr, nullptr, gamma, y, rstd, rows, cols, eps, stream);
 }
 
 int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy,

@@ -156,27 +156,45 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }
 
 // ---------------------------------------------------------------- unpermute (weighted combine)
+// Warp per token; KT (compile-time top-k) and two column vectors per step keep
+// 2*KT independent 16-byte gathers in flight per lane.
+template <int KT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     unpermute_kernel(const uint4* __restrict__ y, const int* __restrict__ slot, const float* __restrict__ wts,
-                     uint4* __restrict__ out, int tokens, int K, int hvec) {
+                     uint4* __restrict__ out, int tokens, int hvec) {
     const int lane = threadIdx.x & 31;
     for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
-        int sl[kMaxTopk];
-        float w[kMaxTopk];
-        for (int k = 0; k < K; ++k) {
-            sl[k] = slot[t * K + k];
-            w[k] = wts[t * K + k];
-        }
-        for (int c = lane; c < hvec; c += 32) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int k = 0; k < K; ++k) {
-                if (sl[k] < 0) continue;
-                float v[8];
-                unpack8(y[static_cast<long long>(sl[k]) * hvec + c], v);
+        int sl[KT];
+        float w[KT];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w[k], v[i]));
+        for (int k = 0; k < KT; ++k) {
+            sl[k] = slot[t * KT + k];
+            w[k] = wts[t * KT + k];
+        }
+        for (int c0 = lane; c0 < hvec; c0 += 64) {
+            uint4 v[KT][2];
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int c = c0 + 32 * j;
+                    v[k][j] = sl[k] >= 0 && c < hvec ? y[static_cast<long long>(sl[k]) * hvec + c] : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int c = c0 + 32 * j;
+                if (c >= hvec) break;
+                float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int k = 0; k < KT; ++k) {
+                    if (sl[k] < 0) continue;  // dropped: no term (not even +0 * w)
+                    float f[8];
+                    unpack8(v[k][j], f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w[k], f[i]));
+                }
+                out[t * hvec + c] = pack8(acc);
             }
-            out[t * hvec + c] = pack8(acc);
         }
     }
 }
@@ -216,23 +234,39 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }
 
 // ---------------------------------------------------------------- permute bwd
+template <int KT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     permute_bwd_kernel(const uint4* __restrict__ dxp, const int* __restrict__ slot, uint4* __restrict__ dx,
-                       int tokens, int K, int hvec) {
+                       int tokens, int hvec) {
     const int lane = threadIdx.x & 31;
     for (long long t = warp_id_global(); t < tokens; t += warps_total()) {
-        int sl[kMaxTopk];
-        for (int k = 0; k < K; ++k) sl[k] = slot[t * K + k];
-        for (int c = lane; c < hvec; c += 32) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int k = 0; k < K; ++k) {
-                if (sl[k] < 0) continue;
-                float v[8];
-                unpack8(dxp[static_cast<long long>(sl[k]) * hvec + c], v);
+        int sl[KT];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], v[i]);
+        for (int k = 0; k < KT; ++k) sl[k] = slot[t * KT + k];
+        for (int c0 = lane; c0 < hvec; c0 += 64) {
+            uint4 v[KT][2];
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int c = c0 + 32 * j;
+                    v[k][j] = sl[k] >= 0 && c < hvec ? dxp[static_cast<long long>(sl[k]) * hvec + c] : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int c = c0 + 32 * j;
+                if (c >= hvec) break;
+                float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int k = 0; k < KT; ++k) {
+                    if (sl[k] < 0) continue;
+                    float f[8];
+                    unpack8(v[k][j], f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], f[i]);
+                }
+                dx[t * hvec + c] = pack8(acc);
             }
-            dx[t * hvec + c] = pack8(acc);
         }
     }
 }
@@ -351,8 +385,18 @@ int dh_moe_unpermute(const void* y, const int* slot, const float* wts, void* out
     if (hidden % 8 || topk > kMaxTopk || !al16(y) || !al16(out))
         return set_error(DH_ERR_INVALID, "moe_unpermute: hidden % 8, topk <= 8, 16-B alignment");
     if (tokens <= 0) return DH_OK;
-    unpermute_kernel<<<row_grid(tokens), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4*>(y), slot, wts, static_cast<uint4*>(out), tokens, topk, hidden / 8);
+    auto s = static_cast<cudaStream_t>(stream);
+    const auto* Y = static_cast<const uint4*>(y);
+    auto* O = static_cast<uint4*>(out);
+    const int g = row_grid(tokens), hv = hidden / 8;
+    switch (topk) {
+#define DH_UNPERMUTE(KT) \
+    case KT: unpermute_kernel<KT><<<g, kWarpsPerBlock * 32, 0, s>>>(Y, slot, wts, O, tokens, hv); break;
+        DH_UNPERMUTE(1) DH_UNPERMUTE(2) DH_UNPERMUTE(3) DH_UNPERMUTE(4)
+        DH_UNPERMUTE(5) DH_UNPERMUTE(6) DH_UNPERMUTE(7) DH_UNPERMUTE(8)
+#undef DH_UNPERMUTE
+        default: return set_error(DH_ERR_INVALID, "moe_unpermute: 1 <= topk <= 8");
+    }
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }
@@ -373,8 +417,18 @@ int dh_moe_permute_bwd(const void* dxp, const int* slot, void* dx, int tokens, i
     if (hidden % 8 || topk > kMaxTopk || !al16(dxp) || !al16(dx))
         return set_error(DH_ERR_INVALID, "moe_permute_bwd: hidden % 8, topk <= 8, 16-B alignment");
     if (tokens <= 0) return DH_OK;
-    permute_bwd_kernel<<<row_grid(tokens), kWarpsPerBlock * 32, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4*>(dxp), slot, static_cast<uint4*>(dx), tokens, topk, hidden / 8);
+    auto s = static_cast<cudaStream_t>(stream);
+    const auto* X = static_cast<const uint4*>(dxp);
+    auto* O = static_cast<uint4*>(dx);
+    const int g = row_grid(tokens), hv = hidden / 8;
+    switch (topk) {
+#define DH_PERMUTE_BWD(KT) \
+    case KT: permute_bwd_kernel<KT><<<g, kWarpsPerBlock * 32, 0, s>>>(X, slot, O, tokens, hv); break;
+        DH_PERMUTE_BWD(1) DH_PERMUTE_BWD(2) DH_PERMUTE_BWD(3) DH_PERMUTE_BWD(4)
+        DH_PERMUTE_BWD(5) DH_PERMUTE_BWD(6) DH_PERMUTE_BWD(7) DH_PERMUTE_BWD(8)
+#undef DH_PERMUTE_BWD
+        default: return set_error(DH_ERR_INVALID, "moe_permute_bwd: 1 <= topk <= 8");
+    }
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

@@ -47,7 +47,7 @@ int dense_kernels(const Model& m, int node, int layer) {
         }
         case 22:
             return m.swiglu_in_epilogue ? 1 : 2;
-        case 0: case 8: case 5: case 7: case 12: case 23: case 24: case 25:
+        case 0: case 5: case 7: case 12: case 23: case 24: case 25:
         case 31: case 32: case 35: case 36:
             return 1;
         case 2: case 26: case 28: case 38:

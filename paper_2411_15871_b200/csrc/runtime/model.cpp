@@ -452,11 +452,12 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 6:  // rs0
             RT_TRY(need_comm());
             return comm->reduce_scatter(P(m.fs.part), P(m.fs.rs_out), TH, s);
-        case 7:  // bda0: x1 = x + attn_out
-            return dh_add(x_in, P(m.fs.rs_out), P(sl.x1), TH, s);
-        case 8:  // ln1
-            return dh_rmsnorm_fwd(P(sl.x1), W + p.g1, tp1 ? P(sl.ln1_full) : P(m.fs.ln_loc),
-                                  m.ptr<float>(sl.rstd1), T, H, k.eps, s);
+        case 7:  // bda0: x1 = x + attn_out, fused with ln1 (its only consumer, next in
+            // every forward order): one pass writes x1 and ln1's output
+            return dh_add_rmsnorm_fwd(x_in, P(m.fs.rs_out), P(sl.x1), W + p.g1,
+                                      tp1 ? P(sl.ln1_full) : P(m.fs.ln_loc), m.ptr<float>(sl.rstd1), T, H, k.eps, s);
+        case 8:  // ln1: computed by bda0's fused kernel
+            return DH_OK;
         case 9:  // ag1
             RT_TRY(need_comm());
             return comm->all_gather(P(m.fs.ln_loc), P(sl.ln1_full), TH, s);

@@ -40,6 +40,8 @@ EPI_NONE, EPI_SWIGLU_FWD, EPI_SWIGLU_FWD_UP, EPI_SWIGLU_BWD = 0, 1, 2, 3
 _SIGS = {
     "dh_gemm": [ctypes.POINTER(GemmArgs), c_void_p],
     "dh_rmsnorm_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float, c_void_p],
+    "dh_add_rmsnorm_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float,
+                           c_void_p],
     "dh_rmsnorm_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                        c_void_p, c_int, c_int, c_void_p],
     "dh_add": [c_void_p, c_void_p, c_void_p, c_ll, c_void_p],
@@ -134,6 +136,13 @@ def rmsnorm_fwd(x, gamma, y, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
     check(lib().dh_rmsnorm_fwd(_ptr(x), _ptr(gamma), _ptr(y), _ptr(rstd), rows, cols, eps,
                                _stream(stream)))
+
+
+def add_rmsnorm_fwd(x, resid, x_out, gamma, y, rstd, eps=1e-5, stream=None):
+    """x_out = bf16(x + resid); y = RMSNorm(x_out) (the fused bda0 + ln1 node)."""
+    rows, cols = x.shape
+    check(lib().dh_add_rmsnorm_fwd(_ptr(x), _ptr(resid), _ptr(x_out), _ptr(gamma), _ptr(y), _ptr(rstd), rows, cols,
+                                   eps, _stream(stream)))
 
 
 def rmsnorm_bwd(x, gamma, rstd, dy, dx, dgamma_acc=None, partial=None, resid=None, stream=None):

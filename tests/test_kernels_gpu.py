@@ -308,3 +308,19 @@ def test_gemm_swiglu_epilogues(m, n, k, tile_n):
     dh.swiglu_bwd(gate, other, dact, rg, ru)
     assert torch.equal(dgate, rg)
     assert torch.equal(dup, ru)
+
+
+@pytest.mark.parametrize("rows,cols", [(96, 256), (512, 4096), (33, 8192), (40, 1000)])
+def test_add_rmsnorm_fused_equals_add_then_norm(rows, cols):
+    """The fused bda0 + ln1 kernel is bitwise dh_add followed by dh_rmsnorm_fwd."""
+    torch.manual_seed(rows + cols)
+    x = torch.randn(rows, cols, device="cuda").to(torch.bfloat16)
+    r = torch.randn(rows, cols, device="cuda").to(torch.bfloat16)
+    g = (1 + 0.1 * torch.randn(cols, device="cuda")).to(torch.bfloat16)
+    x1, y1, s1 = torch.empty_like(x), torch.empty_like(x), torch.empty(rows, device="cuda")
+    dh.add(x, r, x1)
+    dh.rmsnorm_fwd(x1, g, y1, s1)
+    x2, y2, s2 = torch.empty_like(x), torch.empty_like(x), torch.empty(rows, device="cuda")
+    dh.add_rmsnorm_fwd(x, r, x2, g, y2, s2)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2) and torch.equal(y1, y2) and torch.equal(s1, s2)
