@@ -413,6 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // slice of d); thread = (row, 8 columns): partial loads are coalesced along
 // rows ([d][row] layout). Query blocks from `chunk` on belong to split pairs.
 constexpr int kCombineSlices = D / 16;
+// MAXC >= the row's chunk count: every load is issued unconditionally (chunk
+// indices clamped, surplus chunks weighted 0), so a thread has all of its
+// MAXC x 8 partial loads in flight at once instead of one dependent L2 round
+// trip per chunk and column.
+template <int MAXC>
 __global__ void __launch_bounds__(256) attn_fwd_combine_kernel(const FwdParams p) {
     const int h = blockIdx.y;
     const int qb = p.chunk + blockIdx.x;
@@ -424,33 +429,30 @@ __global__ void __launch_bounds__(256) attn_fwd_combine_kernel(const FwdParams p
     if (qrow >= p.T || nc < 2) return;
     const long long slot0 = (static_cast<long long>(h) * (2 * p.npairs) + qb) * p.maxc;
     const float* pml = p.part + static_cast<long long>(p.nq) * (2 * p.npairs) * p.maxc * (BQ * D);
-    float mc[16], w[16];
+    float2 ml[MAXC];
+    float pv[MAXC][8];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        const long long sc = slot0 + min(c, nc - 1);
+        ml[c] = *reinterpret_cast<const float2*>(pml + sc * (2 * BQ) + 2 * r);
+        const float* po = p.part + sc * (BQ * D) + r;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pv[c][u] = po[(d0 + u) * BQ];
+    }
     float M = -INFINITY;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-        if (c < nc) {
-            mc[c] = pml[(slot0 + c) * (2 * BQ) + 2 * r];
-            M = fmaxf(M, mc[c]);
-        }
-    }
-    float L = 0.f;
+    for (int c = 0; c < MAXC; ++c) M = c < nc ? fmaxf(M, ml[c].x) : M;
+    float L = 0.f, f[8] = {};
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-        if (c < nc) {
-            w[c] = exp2f(mc[c] - M);
-            L += w[c] * pml[(slot0 + c) * (2 * BQ) + 2 * r + 1];
+    for (int c = 0; c < MAXC; ++c) {
+        if (c < nc) {  // chunk order: deterministic
+            const float w = exp2f(ml[c].x - M);
+            L += w * ml[c].y;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f[u] += w * pv[c][u];
         }
     }
     const float inv = L > 0.f ? 1.f / L : 0.f;
-    float f[8] = {};
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-        if (c < nc) {
-            const float* po = p.part + (slot0 + c) * (BQ * D) + r;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) f[u] += w[c] * po[(d0 + u) * BQ];
-        }
-    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) f[u] *= inv;
     *reinterpret_cast<uint4*>(p.o + static_cast<long long>(qrow) * p.ldo + h * D + d0) = pack8(f);
@@ -508,7 +510,8 @@ const FwdSplit& fwd_split_plan(int T, int nq) {
     const int nkb = (T + BKV - 1) / BKV;
     const int npairs = (nkb + 1) / 2;
     // many heads x pairs per SM already balance; only small grids are split
-    if (static_cast<long long>(nq) * npairs > 2LL * sms) return cache.emplace(key, sp).first->second;
+    // (measured on B200: 16 heads x 16 pairs, 1.7 items per SM, run faster unsplit)
+    if (2LL * nq * npairs > 3LL * sms) return cache.emplace(key, sp).first->second;
     const int full = 2 * npairs;
     double best = fwd_makespan(nq, nkb, full, sms, nullptr);
     // DH_ATTN_FWD_CHUNK=<even KV blocks> forces a chunk size (tuning runs)
@@ -570,7 +573,11 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
     attn_fwd_tc_kernel<<<grid, kThreads, FwdSmem::total, s>>>(mq, mk, mv, prm, sp.sched);
     DH_CUDA_CHECK(cudaGetLastError());
     if (split) {
-        attn_fwd_combine_kernel<<<dim3(2 * npairs - sp.chunk, nq, kCombineSlices), 256, 0, s>>>(prm);
+        const dim3 cg(2 * npairs - sp.chunk, nq, kCombineSlices);
+        if (sp.maxc <= 2) attn_fwd_combine_kernel<2><<<cg, 256, 0, s>>>(prm);
+        else if (sp.maxc <= 4) attn_fwd_combine_kernel<4><<<cg, 256, 0, s>>>(prm);
+        else if (sp.maxc <= 8) attn_fwd_combine_kernel<8><<<cg, 256, 0, s>>>(prm);
+        else attn_fwd_combine_kernel<16><<<cg, 256, 0, s>>>(prm);
         DH_CUDA_CHECK(cudaGetLastError());
     }
     return DH_OK;
