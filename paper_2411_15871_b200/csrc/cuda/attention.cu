@@ -247,20 +247,26 @@ template <int D>
 __global__ void attn_bwd_dot_kernel(const bf16* __restrict__ o, long long ldo,
                                     const bf16* __restrict__ dout, float* __restrict__ dvec, int T,
                                     int heads) {
-    const int wid = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (wid >= T * heads) return;
-    const int t = wid / heads, h = wid % heads;
-    const bf16* orow = o + static_cast<long long>(t) * ldo + h * D;
-    const bf16* drow = dout + static_cast<long long>(t) * ldo + h * D;
+    // D/8 lanes per (token, head) row, one 16-byte vector of O and dO each
+    constexpr int kL = D / 8;
+    const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long row = gid / kL;
+    const int sub = static_cast<int>(gid % kL);
+    const bool ok = row < static_cast<long long>(T) * heads;
     float sum = 0.f;
-    for (int d = lane * 2; d < D; d += 64) {
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + d));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(drow + d));
-        sum += a.x * b.x + a.y * b.y;
+    int t = 0, h = 0;
+    if (ok) {
+        t = static_cast<int>(row / heads);
+        h = static_cast<int>(row % heads);
+        float a[8], b[8];
+        unpack8(*reinterpret_cast<const uint4*>(o + static_cast<long long>(t) * ldo + h * D + sub * 8), a);
+        unpack8(*reinterpret_cast<const uint4*>(dout + static_cast<long long>(t) * ldo + h * D + sub * 8), b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sum += a[i] * b[i];
     }
-    sum = warp_sum(sum);
-    if (lane == 0) dvec[static_cast<long long>(h) * T + t] = sum;
+#pragma unroll
+    for (int off = kL / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (ok && sub == 0) dvec[static_cast<long long>(h) * T + t] = sum;
 }
 
 // dK, dV for one kv block and one q head: warp w owns keys [16w, 16w+16).
@@ -393,25 +399,46 @@ __global__ void __launch_bounds__(kThr) attn_bwd_dkdv_kernel(
 }
 
 // Sum the GQA group's per-head partials in head order -> bf16 dk, dv.
+// VEC: 8 consecutive d per thread (two 16-byte loads per partial, one 16-byte
+// store) when the partials are 16-byte aligned; else one element per thread.
+template <bool VEC>
 __global__ void attn_bwd_group_reduce(const float* __restrict__ dk_part,
                                       const float* __restrict__ dv_part, bf16* __restrict__ dk,
                                       bf16* __restrict__ dv, long long lddkv, int T, int n_kv,
                                       int group, int D) {
-    const long long total = static_cast<long long>(n_kv) * T * D;
+    constexpr int W = VEC ? 8 : 1;
+    const long long total = static_cast<long long>(n_kv) * T * (D / W);
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int d = static_cast<int>(i % D);
-        const long long rest = i / D;
+        const int d = static_cast<int>(i % (D / W)) * W;
+        const long long rest = i / (D / W);
         const int t = static_cast<int>(rest % T);
         const int kvh = static_cast<int>(rest / T);
-        float sk = 0.f, sv = 0.f;
-        for (int j = 0; j < group; ++j) {
+        float sk[W] = {}, sv[W] = {};
+        for (int j = 0; j < group; ++j) {  // head order: deterministic
             const long long off = (static_cast<long long>(kvh * group + j) * T + t) * D + d;
-            sk += dk_part[off];
-            sv += dv_part[off];
+#pragma unroll
+            for (int u = 0; u < W; u += (VEC ? 4 : 1)) {
+                if constexpr (VEC) {
+                    const float4 kk = *reinterpret_cast<const float4*>(dk_part + off + u);
+                    const float4 vv = *reinterpret_cast<const float4*>(dv_part + off + u);
+                    sk[u] += kk.x; sk[u + 1] += kk.y; sk[u + 2] += kk.z; sk[u + 3] += kk.w;
+                    sv[u] += vv.x; sv[u + 1] += vv.y; sv[u + 2] += vv.z; sv[u + 3] += vv.w;
+                } else {
+                    sk[u] += dk_part[off + u];
+                    sv[u] += dv_part[off + u];
+                }
+            }
         }
-        dk[static_cast<long long>(t) * lddkv + kvh * D + d] = __float2bfloat16(sk);
-        dv[static_cast<long long>(t) * lddkv + kvh * D + d] = __float2bfloat16(sv);
+        bf16* pk = dk + static_cast<long long>(t) * lddkv + kvh * D + d;
+        bf16* pv = dv + static_cast<long long>(t) * lddkv + kvh * D + d;
+        if constexpr (VEC) {
+            *reinterpret_cast<uint4*>(pk) = pack8(sk);
+            *reinterpret_cast<uint4*>(pv) = pack8(sv);
+        } else {
+            *pk = __float2bfloat16(sk[0]);
+            *pv = __float2bfloat16(sv[0]);
+        }
     }
 }
 
@@ -558,9 +585,10 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
     float* dvec = scratch;
     float* dk_part = scratch + static_cast<long long>(nq) * T;
     float* dv_part = dk_part + static_cast<long long>(nq) * T * D;
+    if (ldo % 8 || (reinterpret_cast<uintptr_t>(o) & 15) || (reinterpret_cast<uintptr_t>(dout) & 15))
+        return set_error(DH_ERR_INVALID, "attn_bwd: O / dO need 16-byte aligned rows (ldo % 8 == 0)");
     {
-        const int warps = T * nq;
-        attn_bwd_dot_kernel<D><<<(warps + 7) / 8, 256, 0, s>>>(
+        attn_bwd_dot_kernel<D><<<static_cast<int>((static_cast<long long>(T) * nq * (D / 8) + 255) / 256), 256, 0, s>>>(
             static_cast<const bf16*>(o), ldo, static_cast<const bf16*>(dout), dvec, T, nq);
         DH_CUDA_CHECK(cudaGetLastError());
     }
@@ -584,10 +612,18 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
         DH_CUDA_CHECK(cudaGetLastError());
     }
     if (group > 1) {  // sum the GQA group's per-head dK/dV partials in head order
-        const long long total = static_cast<long long>(nkv) * T * D;
+        const bool vec = (reinterpret_cast<uintptr_t>(dk_part) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(dv_part) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(dv) & 15) == 0 &&
+                         lddkv % 8 == 0;
+        const long long total = static_cast<long long>(nkv) * T * (vec ? D / 8 : D);
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-        attn_bwd_group_reduce<<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
-                                                     static_cast<bf16*>(dv), lddkv, T, nkv, group, D);
+        if (vec)
+            attn_bwd_group_reduce<true><<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
+                                                               static_cast<bf16*>(dv), lddkv, T, nkv, group, D);
+        else
+            attn_bwd_group_reduce<false><<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
+                                                                static_cast<bf16*>(dv), lddkv, T, nkv, group, D);
         DH_CUDA_CHECK(cudaGetLastError());
     }
     if constexpr (D != 128) {
