@@ -288,9 +288,13 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     # meaningless) gradients cannot drive the weights to overflow across steps
     step = lambda: m.step({"lr": 0.0}, use_graph=True)  # noqa: E731
     # (name, plan, executor mode, collectives skipped)
+    # compute_only keeps the SI lowering's GEMM SM caps (the same kernels as SI
+    # with the collectives left out); compute_only_all_sms lifts the caps, so the
+    # cost of reserving SMs for the collectives is visible on its own
     modes = [("si", srch, "si", False), ("si_wide", srch_wide, "si", False),
              ("si_wide_relaxed", srch_wide, "si_relaxed", False),
-             ("compute_only", srch_wide, "si_relaxed", True), ("sequential", srch_wide, "sequential", False)]
+             ("compute_only", srch_wide, "si_relaxed", True), ("compute_only_all_sms", srch_wide, "si_relaxed", True),
+             ("sequential", srch_wide, "sequential", False)]
     if not full:
         modes = [x for x in modes if x[0] in ("si", "si_wide_relaxed", "compute_only", "sequential")]
     # The modes are timed in interleaved rounds (a clock drift under the power
@@ -301,8 +305,8 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     for _ in range(rounds):
         for name, plan, mode, skip in modes:
             m.set_plan(plan["plan_json"], json.dumps(prof), mode=mode)
-            m.set_overlap_ctas(getattr(args, "overlap_ctas", None) if getattr(args, "overlap_ctas", None) is not None
-                               else sms - args.nccl_ctas)
+            cap = getattr(args, "overlap_ctas", None)
+            m.set_overlap_ctas(0 if name == "compute_only_all_sms" else cap if cap is not None else sms - args.nccl_ctas)
             m.set_skip_comm(skip)
             for _ in range(2):
                 step()
@@ -330,6 +334,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     comm_solo = sum(e["t_us"] for e in prof["solo"] if e["shape"] in comm_nodes)
     pairs = shape.layers * shape.micro_batches
     si_modes = [k for k in res if k.startswith("si")]
+    all_sms = res.get("compute_only_all_sms")
     best = min(si_modes, key=lambda k: res[k])
     exposed = (res[best] - res["compute_only"]) * 1e3 / pairs
     exposed_seq = (res["sequential"] - res["compute_only"]) * 1e3 / pairs
@@ -389,6 +394,10 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
         "exposed_comm_us_per_layer_pair": {best: round(exposed, 1), "sequential": round(exposed_seq, 1)},
         # exposed time below zero is timing noise between the two schedules: clamp
         "hidden_comm_frac": round(min(1.0, 1.0 - exposed / comm_solo), 4) if comm_solo > 0 else None,
+        # the stricter reading: exposed = SI - compute-only on ALL SMs (the SM cap
+        # the collectives need counted as exposed communication)
+        "hidden_comm_frac_vs_all_sm_compute": None if all_sms is None or not comm_solo else
+        round(min(1.0, 1.0 - (res[best] - all_sms) * 1e3 / pairs / comm_solo), 4),
         "mfu": round((fl["fwd"] + fl["bwd"]) * pairs / (res[best] / 1e3) / 1e12 / SPEC_BF16_TFLOPS, 4),
         "plans": {k: {"caps": c, "hidden_comm_frac_model": p["hidden_comm_frac"], "total_us_model": p["total_us"],
                       "fwd_cuts": json.loads(p["plan_json"])["fwd_cuts"],
