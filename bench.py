@@ -298,9 +298,9 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     if not full:
         modes = [x for x in modes if x[0] in ("si", "si_wide_relaxed", "compute_only", "sequential")]
     # The modes are timed in interleaved rounds (a clock drift under the power
-    # cap then biases no mode) and averaged; emulated steps are short, so more
-    # of them are timed for stable differences between modes.
-    rounds, per_round = (2, max(10, 2 * args.steps)) if full else (2, max(4, args.steps))
+    # cap then biases no mode) and the median round is kept; emulated steps are
+    # short, so more of them are timed for stable differences between modes.
+    rounds, per_round = (3, max(10, 2 * args.steps)) if full else (3, max(4, args.steps))
     samples = {name: [] for name, *_ in modes}
     for _ in range(rounds):
         for name, plan, mode, skip in modes:
@@ -311,7 +311,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
             for _ in range(2):
                 step()
             samples[name].append(timed(per_round, step, stream))
-    res = {name: sum(v) / len(v) for name, v in samples.items()}
+    res = {name: sorted(v)[len(v) // 2] for name, v in samples.items()}  # median round
     for name in res:
         log(f"emulated tp{tp} {name}: {res[name]:.1f} ms/step (rounds: {', '.join(f'{x:.1f}' for x in samples[name])})")
     m.set_skip_comm(False)
