@@ -33,12 +33,15 @@ struct SimOp {
 
 // `raw_oef(a, b)` returns the table OEF for the pair (throws when missing).
 // `trace`, when given, receives (strand, op index) in dispatch (start) order —
-// the B200 executor lowers a plan step to lane-stream launches in this order.
+// the B200 executor lowers a plan step to lane-stream launches in this order;
+// `spans` (with `trace`) receives each traced op's simulated (start, end).
+// Neither output changes the arithmetic.
 template <class RawOef>
 SegmentCost simulate_lanes(const SimOp* ops_a, std::size_t n_a, const SimOp* ops_b,
                            std::size_t n_b, double slowdown, double launch_frac,
                            RawOef&& raw_oef,
-                           std::vector<std::pair<int, std::size_t>>* trace = nullptr) {
+                           std::vector<std::pair<int, std::size_t>>* trace = nullptr,
+                           std::vector<std::pair<double, double>>* spans = nullptr) {
     struct Front {
         const SimOp* ops;
         std::size_t n;
@@ -47,6 +50,7 @@ SegmentCost simulate_lanes(const SimOp* ops_a, std::size_t n_a, const SimOp* ops
         double remaining = 0.0;
         double release = 0.0;
         bool busy = false;
+        std::size_t span = 0;  // index of the current op in *spans
     };
     std::array<Front, 2> fr{Front{ops_a, n_a}, Front{ops_b, n_b}};
     std::array<int, 3> owner{-1, -1, -1};
@@ -75,6 +79,10 @@ SegmentCost simulate_lanes(const SimOp* ops_a, std::size_t n_a, const SimOp* ops
             if (chosen < 0) return;
             Front& f = fr[chosen];
             if (trace) trace->emplace_back(chosen, f.next);
+            if (trace && spans) {
+                f.span = spans->size();
+                spans->emplace_back(clock, clock);
+            }
             f.cur = &f.ops[f.next++];
             f.remaining = f.cur->t_us;
             f.busy = true;
@@ -106,6 +114,7 @@ SegmentCost simulate_lanes(const SimOp* ops_a, std::size_t n_a, const SimOp* ops
             const double r = s == 0 ? r0 : r1;
             cost.lane_busy_us[static_cast<int>(f.cur->lane)] += dt;
             if (f.remaining / r <= dt) {
+                if (trace && spans) (*spans)[f.span].second = clock + dt;
                 f.remaining = 0.0;
                 f.busy = false;
                 owner[static_cast<int>(f.cur->lane)] = -1;

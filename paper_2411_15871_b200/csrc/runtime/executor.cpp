@@ -241,6 +241,7 @@ struct Lowering {
                 sb.push_back({solo(id, m.bwd_dag), n->lane, n->cls});
             }
             std::vector<std::pair<int, std::size_t>> order;
+            std::vector<std::pair<double, double>> spans;
             weft::detail::simulate_lanes(
                 sa.data(), sa.size(), sb.data(), sb.size(), tbl.slowdown_factor,
                 tbl.launch_overhead_frac,
@@ -248,16 +249,25 @@ struct Lowering {
                     const auto v = tbl.get(x.cls, y.cls);
                     return v ? *v : 0.0;  // missing pairs only affect issue order
                 },
-                &order);
+                &order, &spans);
             if (!relaxed || first_step) barrier();
             first_step = false;
-            // joined steps: only a step holding a collective co-runs one; relaxed
-            // steps may overlap their neighbours, so the whole block is capped
-            bool step_comm = relaxed;
-            for (int id : fa) step_comm |= lane_of.at(id) != 0;
-            for (int id : ba) step_comm |= lane_of.at(id) != 0;
-            capped = step_comm;
-            for (const auto& [side, i] : order) {
+            // Joined steps: a compute op is capped when its simulated interval
+            // overlaps one of the step's collectives (the lane model's timeline
+            // on the measured solo times); relaxed steps may overlap their
+            // neighbours, so the whole block is capped.
+            auto is_comm = [&](std::size_t t) {
+                const auto& [side, i] = order[t];
+                return lane_of.at(side == 0 ? fa[i] : ba[i]) != 0;
+            };
+            for (std::size_t t = 0; t < order.size(); ++t) {
+                const auto& [side, i] = order[t];
+                bool cap = relaxed;
+                if (!relaxed && !is_comm(t)) {
+                    for (std::size_t c = 0; c < order.size() && !cap; ++c)
+                        cap = is_comm(c) && spans[c].first < spans[t].second && spans[t].first < spans[c].second;
+                }
+                capped = cap;
                 if (side == 0) emit(fs, lf, fa[i]);
                 else emit(bs, lb, ba[i]);
             }
