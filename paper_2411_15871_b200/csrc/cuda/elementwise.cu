@@ -851,13 +851,14 @@ int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode,
                                   : static_cast<double>(count) * 2.0 * (tp - 1);
     const unsigned long long target = link_gbs > 0 ? static_cast<unsigned long long>(wire / link_gbs) : 0ull;
     if (tp > 8) return set_error(DH_ERR_INVALID, "comm_proxy: tp <= 8");
-    // Each proxy CTA reserves 48 KB of shared memory (unused), as a collective
-    // kernel's staging buffers do: it then cannot co-reside on an SM with a
-    // ~200 KB GEMM or attention CTA, so the emulation, like NCCL, only runs on
-    // SMs those kernels leave free (DH_PROXY_SMEM_KB overrides, 0 = none).
+    // DH_PROXY_SMEM_KB=<n> makes each proxy CTA reserve n KB of shared memory
+    // (unused), as a collective kernel's staging buffers would: it then cannot
+    // co-reside with a ~200 KB GEMM or attention CTA. Off by default: with 48 KB
+    // the TP=8 numbers were the same within noise, but one full bench run stalled
+    // in the TP=8 profiling after the TP=2/4 sweeps (not reproduced, not understood).
     static const int smem_kb = [] {
         const char* e = std::getenv("DH_PROXY_SMEM_KB");
-        return e ? std::atoi(e) : 48;
+        return e ? std::atoi(e) : 0;
     }();
     comm_proxy_kernel<<<std::max(1, ctas), 1024, smem_kb * 1024, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4*>(src), static_cast<uint4*>(dst), chunk, mode, tp, target);
