@@ -264,6 +264,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     shape = copy.copy(base_shape or LLAMA3_8B)
     shape.layers = layers or args.layers
     shape.micro_batches = micro_batches or args.micro_batches
+    shape.slots = shape.layers + 2  # mode 4 (deferred weight gradients) holds one more slot
     link = 770.0
     ctx = Context.emulated(0, tp, args.nccl_ctas, link)
     m = Model(ctx, shape)
@@ -293,10 +294,12 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     # cost of reserving SMs for the collectives is visible on its own
     modes = [("si", srch, "si", False), ("si_wide", srch_wide, "si", False),
              ("si_wide_relaxed", srch_wide, "si_relaxed", False),
+             ("si_wide_deferred", srch_wide, "si_deferred", False),
              ("compute_only", srch_wide, "si_relaxed", True), ("compute_only_all_sms", srch_wide, "si_relaxed", True),
              ("sequential", srch_wide, "sequential", False)]
     if not full:
-        modes = [x for x in modes if x[0] in ("si", "si_wide_relaxed", "compute_only", "sequential")]
+        modes = [x for x in modes if x[0] in ("si", "si_wide_relaxed", "si_wide_deferred", "compute_only",
+                                              "sequential")]
     # The modes are timed in interleaved rounds (a clock drift under the power
     # cap then biases no mode) and the median round is kept; emulated steps are
     # short, so more of them are timed for stable differences between modes.
@@ -343,8 +346,8 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
         # Split the exposed time into the unpaired ends (F_0 and B_{m-1} have no
         # partner strand: their collectives are exposed whatever the plan) and
         # the SI blocks: exposed(m) = ends + (m - 1) * block, measured at m and 2.
-        plan_best = {"si": srch, "si_wide": srch_wide, "si_wide_relaxed": srch_wide}[best]
-        mode_best = "si_relaxed" if best.endswith("relaxed") else "si"
+        plan_best = {"si": srch, "si_wide": srch_wide, "si_wide_relaxed": srch_wide, "si_wide_deferred": srch_wide}[best]
+        mode_best = {"si_wide_relaxed": "si_relaxed", "si_wide_deferred": "si_deferred"}.get(best, "si")
         m.close()
         shape2 = copy.copy(shape)
         shape2.micro_batches = 2

@@ -262,9 +262,10 @@ int dh_model_destroy(dh_model* m) {
 int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
                       const char* cluster_json, int mode) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
-    if (mode < 0 || mode > 3)
+    if (mode < 0 || mode > 4)
         return dh::set_error(DH_ERR_INVALID,
-                             "mode must be 0 (SI), 1 (sequential), 2 (SI, relaxed steps) or 3 (W pipeline stage)");
+                             "mode must be 0 (SI), 1 (sequential), 2 (SI, relaxed steps), 3 (W pipeline stage) "
+                             "or 4 (SI, relaxed steps, deferred attention weight gradients)");
     if (mode == 3 && m->cfg.pp_size != m->ctx->pp_size)
         return dh::set_error(DH_ERR_CONFIG, "w_pipeline: dh_model_cfg.pp_size differs from the context's stage group");
     RT_TRY(dh::configure_plan(*m, plan_json, profile_json, cluster_json));
@@ -274,9 +275,10 @@ int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_js
 int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_json,
                   const char* profile_json, int mode, char** out) {
     if (!cfg || !out) return dh::set_error(DH_ERR_INVALID, "null argument");
-    if (mode < 0 || mode > 3)
+    if (mode < 0 || mode > 4)
         return dh::set_error(DH_ERR_INVALID,
-                             "mode must be 0 (SI), 1 (sequential), 2 (SI, relaxed steps) or 3 (W pipeline stage)");
+                             "mode must be 0 (SI), 1 (sequential), 2 (SI, relaxed steps), 3 (W pipeline stage) "
+                             "or 4 (SI, relaxed steps, deferred attention weight gradients)");
     dh::Model m;  // host-only: no context, no pool
     RT_TRY(dh::derive_cfg(cfg, tp, rank, &m.cfg));
     RT_TRY(dh::build_dags(m, dh::default_cluster(), nullptr));

@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <tuple>
 
 #include "../planner/lane_sim.hpp"
 #include "runtime.hpp"
@@ -221,16 +222,83 @@ struct Lowering {
     // step of a layer pair joins the lanes (it guards the activation slot the
     // forward strand takes over from the backward strand); inside a layer pair the
     // two strands touch disjoint buffers, so the per-strand event edges suffice.
+    // Mode 4 (relaxed steps + deferred weight gradients): the backward strand's
+    // trailing attention weight gradients (attn_proj_wgrad, qkv_wgrad: sinks
+    // that only read the layer's slot, dqkv and the attention-output gradient)
+    // are issued after the NEXT layer pair's first step, where they fill the
+    // compute lane while that pair's leading collectives (rs1_bwd_ag, ag0) run.
+    // Their layer's activation slot is released after them, so the schedule
+    // needs one activation slot more (dh_model_cfg.slots >= L + 2).
+    struct Deferred {
+        int strand = -1, layer = -1;
+        std::vector<int> nodes;
+    } deferred;
+    bool defer_wgrads = false;
+
+    void flush_deferred() {
+        if (deferred.strand < 0) return;
+        std::map<int, std::vector<int>> preds;
+        for (const auto& [a, b] : m.bwd_dag.edges) preds[b].push_back(a);
+        const int keep_last = strand_last[deferred.strand];
+        for (int id : deferred.nodes) {
+            std::vector<int> deps;
+            for (int p : preds[id]) deps.push_back(bwd_op_at.at({deferred.strand, deferred.layer, p}));
+            capped = true;  // may co-run with the next pair's collectives
+            emit(deferred.strand, deferred.layer, id, -1, &deps);
+        }
+        capped = false;
+        strand_last[deferred.strand] = keep_last;  // the strand's chain continues from its own ops
+        give_slot(deferred.strand, deferred.layer);
+        deferred = Deferred{};
+    }
+    std::map<std::tuple<int, int, int>, int> bwd_op_at;  // (strand, layer, node) -> op index (mode 4)
+
     void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl, bool relaxed) {
         take_slot(fs, lf);
         if (pending_recv_act.first == fs) {
             emit(fs, lf, kRecvAct, pending_recv_act.second);
             pending_recv_act = {-1, -1};
         }
+        // The backward strand's leading ops up to its first collective (bda1_bwd,
+        // rs1_bwd_ag) depend only on the previous layer's gradient, ready when
+        // the pair starts: they join the first step, so the collective runs
+        // under that step's compute instead of stalling the GEMM that waits for
+        // it in a later, joined step (tools/op_timeline.py measured that stall
+        // as the largest exposed collective inside SI blocks). DH_SI_HOIST=0 off.
+        static const bool hoist_on = [] {
+            const char* e = std::getenv("DH_SI_HOIST");
+            return !e || std::atoi(e) != 0;
+        }();
+        std::vector<int> hoist;
+        if (hoist_on) {
+            for (int id : m.plan.bwd_seq) {
+                hoist.push_back(id);
+                if (lane_of.at(id) != 0) break;
+            }
+            if (hoist.empty() || lane_of.at(hoist.back()) == 0) hoist.clear();  // no collective
+        }
+        auto hoisted = [&](int id) { return std::find(hoist.begin(), hoist.end(), id) != hoist.end(); };
+        // this pair's deferrable tail: the attention weight gradients after the
+        // backward layer's last collective (dense template ids 32, 36)
+        std::vector<int> defer_now;
+        if (defer_wgrads && !m.cfg.moe) {
+            int last_comm = -1;
+            for (std::size_t i = 0; i < m.plan.bwd_seq.size(); ++i)
+                if (lane_of.at(m.plan.bwd_seq[i]) != 0) last_comm = static_cast<int>(i);
+            for (std::size_t i = last_comm + 1; last_comm >= 0 && i < m.plan.bwd_seq.size(); ++i) {
+                const int id = m.plan.bwd_seq[i];
+                if (id == 32 || id == 36) defer_now.push_back(id);
+            }
+        }
+        auto deferred_here = [&](int id) { return std::find(defer_now.begin(), defer_now.end(), id) != defer_now.end(); };
         bool first_step = true;
+        t_first_done_flush = true;  // the previous pair's deferred ops follow this pair's first step
         for (const auto& st : m.plan.plan.steps) {
             const auto fa = segment(m.plan.fwd_segmentation, st.fwd_seg.value_or(0));
-            const auto ba = segment(m.plan.bwd_segmentation, st.bwd_seg.value_or(0));
+            std::vector<int> ba;
+            if (first_step) ba = hoist;
+            for (int id : segment(m.plan.bwd_segmentation, st.bwd_seg.value_or(0)))
+                if (!hoisted(id) && !deferred_here(id)) ba.push_back(id);
             std::vector<weft::detail::SimOp> sa, sb;
             for (int id : fa) {
                 const auto* n = m.fwd_dag.find(id);
@@ -267,14 +335,34 @@ struct Lowering {
                     for (std::size_t c = 0; c < order.size() && !cap; ++c)
                         cap = is_comm(c) && spans[c].first < spans[t].second && spans[t].first < spans[c].second;
                 }
+                if (side == 1 && deferred.strand >= 0 && (ba[i] == 28 || ba[i] == 30 || ba[i] == 34)) {
+                    // the next layer is about to overwrite an input of the deferred
+                    // gradients (d_x1 / dx1_full / dqkv): issue them first
+                    flush_deferred();
+                }
                 capped = cap;
-                if (side == 0) emit(fs, lf, fa[i]);
-                else emit(bs, lb, ba[i]);
+                if (side == 0) {
+                    emit(fs, lf, fa[i]);
+                } else {
+                    emit(bs, lb, ba[i]);
+                    bwd_op_at[{bs, lb, ba[i]}] = static_cast<int>(prog.ops.size()) - 1;
+                }
             }
+            if (t_first_done_flush) flush_deferred();
+            t_first_done_flush = false;
         }
-        give_slot(bs, lb);
+        if (t_first_done_flush) flush_deferred();  // (a plan without steps)
+        t_first_done_flush = false;
+        if (!defer_now.empty()) {
+            deferred.strand = bs;
+            deferred.layer = lb;
+            deferred.nodes = defer_now;  // slot released by flush_deferred()
+        } else {
+            give_slot(bs, lb);
+        }
         capped = false;
     }
+    bool t_first_done_flush = false;
 
     // ---- W pipeline stage (mode 3)
     // Local layers [0, c) are the way-down half and [c, L) the way-back half of
@@ -338,6 +426,8 @@ int lower_ops(Model& m, int mode) {
     const int L = m.cfg.layers, mb = m.cfg.micro_batches;
     weft::OverlapTable tbl = weft::synth_profile(weft::ProfileArchetype::nvlink_h100).overlap;
     if (!m.plan_overlap.entries.empty()) tbl = m.plan_overlap;
+    if (mode == 4 && n_slots(m) < L + 2)
+        return set_error(DH_ERR_CONFIG, "mode 4 (deferred weight gradients) needs dh_model_cfg.slots >= layers + 2");
     Lowering lw(m);
     lw.prog.mode = mode;
     try {
@@ -383,8 +473,11 @@ int lower_ops(Model& m, int mode) {
                         if (*blk.bwd_mb == mb) lw.emit_opt(mb - 1, l);
                     }
                 } else {
+                    lw.defer_wgrads = mode == 4;
                     for (int k = 0; k < L; ++k)
-                        lw.si_layer_pair(*blk.fwd_mb - 1, k, *blk.bwd_mb - 1, L - 1 - k, tbl, mode == 2);
+                        lw.si_layer_pair(*blk.fwd_mb - 1, k, *blk.bwd_mb - 1, L - 1 - k, tbl, mode == 2 || mode == 4);
+                    lw.flush_deferred();  // the block's last pair: nothing to hide them under
+                    lw.defer_wgrads = false;
                 }
             }
         }
@@ -423,7 +516,14 @@ int lower_program(Model& m, int mode) {
 
 namespace {
 
-int issue(Model& m) {
+// DH_OP_TIMES=<file> (eager runs only): CUDA events around every op, dumped
+// as JSON lines (op, strand, layer, node, lane, start/end ms from the first op)
+// after the program — the on-device timeline tools/op_timeline.py analyses.
+struct OpTimes {
+    std::vector<cudaEvent_t> ev;  // 2 per op
+};
+
+int issue(Model& m, OpTimes* ot = nullptr) {
     Ctx& c = *m.ctx;
     std::size_t probe = 0;
     static const bool trace = std::getenv("DH_TRACE") != nullptr;
@@ -436,7 +536,9 @@ int issue(Model& m) {
         if (probed)
             RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe].first, s, cudaEventRecordExternal));
         if (trace) std::fprintf(stderr, "[dh] op %zu strand %d layer %d node %d lane %d\n", i, o.strand, o.layer, o.node, o.lane);
+        if (ot) RT_CUDA(cudaEventRecord(ot->ev[2 * i], s));
         RT_TRY(launch_node(m, o, s));
+        if (ot) RT_CUDA(cudaEventRecord(ot->ev[2 * i + 1], s));
         if (trace) {
             const cudaError_t e = cudaStreamSynchronize(s);
             std::fprintf(stderr, "[dh]   done: %s\n", cudaGetErrorString(e));
@@ -449,14 +551,14 @@ int issue(Model& m) {
 }
 
 // Fork lanes 1..2 off lane 0, run, join back into lane 0.
-int issue_forked(Model& m) {
+int issue_forked(Model& m, OpTimes* ot = nullptr) {
     Ctx& c = *m.ctx;
     if (!m.fork_join[0]) {
         for (auto& e : m.fork_join) RT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     RT_CUDA(cudaEventRecord(m.fork_join[0], c.lane[0]));
     for (int l = 1; l < kLanes; ++l) RT_CUDA(cudaStreamWaitEvent(c.lane[l], m.fork_join[0], 0));
-    RT_TRY(issue(m));
+    RT_TRY(issue(m, ot));
     for (int l = 1; l < kLanes; ++l) {
         RT_CUDA(cudaEventRecord(m.fork_join[l], c.lane[l]));
         RT_CUDA(cudaStreamWaitEvent(c.lane[0], m.fork_join[l], 0));
@@ -477,6 +579,29 @@ int run_program(Model& m, bool use_graph) {
                      cudaGetErrorString(pending));
     }
     const bool capturable = !m.ctx->comm || m.ctx->comm->capturable();
+    if (const char* path = std::getenv("DH_OP_TIMES"); path && !use_graph) {
+        OpTimes ot;
+        ot.ev.assign(2 * m.prog.ops.size(), nullptr);
+        for (auto& e : ot.ev) RT_CUDA(cudaEventCreate(&e));
+        const int rc = issue_forked(m, &ot);
+        if (rc == DH_OK) {
+            RT_CUDA(cudaStreamSynchronize(m.ctx->lane[0]));
+            if (FILE* f = std::fopen(path, "w")) {
+                for (std::size_t i = 0; i < m.prog.ops.size(); ++i) {
+                    float a = 0.f, b = 0.f;
+                    cudaEventElapsedTime(&a, ot.ev[0], ot.ev[2 * i]);
+                    cudaEventElapsedTime(&b, ot.ev[0], ot.ev[2 * i + 1]);
+                    const Op& o = m.prog.ops[i];
+                    std::fprintf(f, "{\"op\": %zu, \"strand\": %d, \"layer\": %d, \"node\": %d, \"lane\": %d, "
+                                    "\"capped\": %d, \"start_ms\": %.6f, \"end_ms\": %.6f}\n",
+                                 i, o.strand, o.layer, o.node, o.lane, o.capped ? 1 : 0, a, b);
+                }
+                std::fclose(f);
+            }
+        }
+        for (auto e : ot.ev) cudaEventDestroy(e);
+        return rc;
+    }
     if (!use_graph || !capturable) return issue_forked(m);
     if (!m.graph) {
         cudaStream_t s0 = m.ctx->lane[0];

@@ -221,7 +221,7 @@ class Model:
         enc = lambda s: None if s is None else s.encode()  # noqa: E731
         check(_lib().dh_model_set_plan(self.handle, enc(plan_json), enc(profile_json),
                                        enc(cluster_json), {"si": 0, "sequential": 1, "si_relaxed": 2,
-                                                             "w_pipeline": 3}[mode]))
+                                                             "w_pipeline": 3, "si_deferred": 4}[mode]))
 
     def set_fuse_optimizer(self, on: bool):
         """Per-layer AdamW inside the program (default); effective at the next set_plan."""
@@ -291,7 +291,8 @@ def lower(shape: "LlamaShape", tp: int, plan_json: str | None, mode: str = "si",
     p = c_void_p()
     enc = lambda s: None if s is None else s.encode()  # noqa: E731
     check(_lib().dh_lower_json(ctypes.byref(cfg), tp, rank, enc(plan_json), enc(profile_json),
-                               {"si": 0, "sequential": 1, "si_relaxed": 2, "w_pipeline": 3}[mode], ctypes.byref(p)))
+                               {"si": 0, "sequential": 1, "si_relaxed": 2, "w_pipeline": 3, "si_deferred": 4}[mode],
+                               ctypes.byref(p)))
     return json.loads(_take_string(p))
 
 

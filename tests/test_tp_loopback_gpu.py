@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle.layer_oracle import bf16_round  # noqa: E402
 from paper_2411_15871_b200 import planner  # noqa: E402
-from paper_2411_15871_b200.runtime import Context, Model  # noqa: E402
+from paper_2411_15871_b200.runtime import Context, LlamaShape, Model  # noqa: E402
 from tests.test_model_gpu import B200, _rel, _tiny, _upload  # noqa: E402
 from oracle.layer_oracle import LlamaTPOracle  # noqa: E402
 
@@ -42,7 +42,8 @@ def _run_ranks(fn, tp):
 
 @pytest.mark.parametrize("tp", [2, 4])
 def test_tp_loopback_vs_oracle_and_si_equals_sequential(tp):
-    shape = _tiny(mb=2, layers=2, nkv=4)
+    # one spare activation slot: mode 4 (deferred weight gradients) needs L + 2
+    shape = LlamaShape(**{**_tiny(mb=2, layers=2, nkv=4).__dict__, "slots": 4})
     orc = LlamaTPOracle(shape.hidden, shape.ffn, shape.n_heads, shape.n_kv_heads, shape.head_dim,
                         shape.layers, shape.seq_len, tp=tp, theta=shape.rope_theta, bf16=True, seed=21,
                         init_std=0.05)
@@ -66,7 +67,7 @@ def test_tp_loopback_vs_oracle_and_si_equals_sequential(tp):
             _upload(m.tensor("dy", strand=s), rs[s][r * T:(r + 1) * T])
         torch.cuda.synchronize()
         res = {}
-        for mode in ("si", "sequential"):
+        for mode in ("si", "sequential", "si_deferred"):
             m.set_plan(plan, mode=mode)
             m.zero_grads()
             m.run_program(use_graph=True)  # loopback is not capturable: runs eagerly
@@ -84,9 +85,10 @@ def test_tp_loopback_vs_oracle_and_si_equals_sequential(tp):
     for c in ctxs:
         c.close()
     for r in range(tp):
-        si, seq = outs[r][0]["si"], outs[r][0]["sequential"]
+        si, seq, dfr = outs[r][0]["si"], outs[r][0]["sequential"], outs[r][0]["si_deferred"]
         for k in si:
             assert torch.equal(si[k], seq[k]), f"rank {r}: SI != sequential for {k}"
+            assert torch.equal(si[k], dfr[k]), f"rank {r}: SI with deferred wgrads != SI for {k}"
         assert outs[r][1]["program"]["comm"] == "loopback"
 
     p = planner.parse_plan(plan)
