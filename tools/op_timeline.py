@@ -23,7 +23,7 @@ ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--mb", type=int, default=4)
 ap.add_argument("--mode", default="si")
 a = ap.parse_args()
-shape = LlamaShape(**{**LLAMA3_8B.__dict__, "layers": a.layers, "micro_batches": a.mb})
+shape = LlamaShape(**{**LLAMA3_8B.__dict__, "layers": a.layers, "micro_batches": a.mb, "slots": a.layers + 2})
 ctx = Context.emulated(0, a.tp, 16, 770.0)
 m = Model(ctx, shape)
 m.set_overlap_ctas(148 - 16)
