@@ -244,6 +244,29 @@ def memory_vs_model(planner, info, shape):
             "transients_gb": round((info["pool_bytes"] - measured) / 1e9, 3)}
 
 
+def emulated_subprocess(config, group, layers, micro_batches, args, full, timeout):
+    """One emulated experiment (tools/run_config.py) in a child process under a
+    timeout: a stall or crash there is reported in its entry, and the headline
+    line (measured before) is still printed."""
+    import subprocess
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "run_config.py"), config, "--layers", str(layers),
+           "--micro-batches", str(micro_batches), "--steps", str(args.steps), "--nccl-ctas", str(args.nccl_ctas)]
+    if group:
+        cmd += ["--group", str(group)]
+    if full:
+        cmd.append("--full")
+    log(f"emulated {config} group={group or 'default'}: child process")
+    try:
+        p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": f"timed out after {timeout} s"}
+    sys.stderr.write(p.stderr)
+    lines = [x for x in p.stdout.splitlines() if x.startswith("{")]
+    if p.returncode != 0 or not lines:
+        return {"error": f"exit {p.returncode}: {(p.stderr or '').strip().splitlines()[-1:] }"}
+    return json.loads(lines[-1])
+
+
 def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, layers=None, micro_batches=None):
     """TP=<tp> per-GPU shapes on this single GPU with emulated collectives
     (dh_ctx_create_emulated: proxy kernels on the NCCL CTA budget, held for the
@@ -567,10 +590,15 @@ def main():
         del host_in, loss_host, dev_dst, loss_dev
         torch.cuda.synchronize()
         model.close()
+        ctx.close()
+        torch.cuda.empty_cache()
         for t in tps:
-            r = emulated_tp_experiment(args, t, timed, full=t == max(tps))
+            r = emulated_subprocess("llama3", t, args.layers, args.micro_batches, args, full=t == max(tps),
+                                    timeout=900 if t == max(tps) else 420)
             if t == max(tps):
                 emu = r
+            elif "error" in r:
+                emu_sweep[f"tp{t}"] = r
             else:
                 emu_sweep[f"tp{t}"] = {k: r[k] for k in ("tokens_per_s_per_gpu", "mfu", "ms_per_step",
                                                            "hidden_comm_frac", "frac_of_overlap_roofline",
@@ -580,10 +608,12 @@ def main():
     # collectives, a slice of the layer stack: per-layer-pair metrics)
     other_cfgs = {}
     if world == 1 and tps and not args.no_configs:
-        from paper_2411_15871_b200.runtime import GPT3_13B, LLAMA2_70B, PHI35_MOE
-        for name, base, tpc, nl in (("c3_gpt3_13b_tp4", GPT3_13B, 4, 8), ("c5_llama2_70b_tp4", LLAMA2_70B, 4, 4),
-                                    ("c4_phi35_moe_ep8", PHI35_MOE, 8, 4)):
-            r = emulated_tp_experiment(args, tpc, timed, full=False, base_shape=base, layers=nl, micro_batches=4)
+        for name, cfg, nl in (("c3_gpt3_13b_tp4", "c3", 8), ("c5_llama2_70b_tp4", "c5", 4),
+                              ("c4_phi35_moe_ep8", "c4", 4)):
+            r = emulated_subprocess(cfg, 0, nl, 4, args, full=False, timeout=420)
+            if "error" in r:
+                other_cfgs[name] = r
+                continue
             other_cfgs[name] = {"layers_in_slice": nl, "micro_batches": 4,
                                 **{k: r[k] for k in ("tokens_per_s_per_gpu", "mfu", "ms_per_step", "layer_pair_us",
                                                      "overlap_roofline_us", "frac_of_overlap_roofline",

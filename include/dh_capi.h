@@ -254,7 +254,10 @@ int dh_model_destroy(dh_model* m);
  * issue order, lanes joined only at layer-pair boundaries). plan_json NULL =
  * template order, one segment per pass (valid for mode 1 and as a trivial SI plan). */
 /* mode 3: W pipeline stage (weft schedule_w_pipeline(micro_batches, pp_size) blocks of
- * this pp_rank; SI visits pair the plan's steps as mode 0). */
+ * this pp_rank; SI visits pair the plan's steps as mode 0).
+ * mode 4: as mode 2, with the backward layer's trailing attention weight gradients
+ * issued after the next layer pair's first step (needs cfg.slots >= layers + 2).
+ * Every mode computes bitwise the same losses and gradients. */
 int dh_model_set_plan(dh_model* m, const char* plan_json, const char* profile_json,
                       const char* cluster_json, int mode);
 /* Host-only lowering (no GPU needed): the launch program dh_model_set_plan would

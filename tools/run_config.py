@@ -1,6 +1,8 @@
-"""Run one BASELINE.json config's emulated slice alone (bench.py's
-emulated_tp_experiment), e.g. `python tools/run_config.py c4` on a GPU box.
-Prints one JSON object; the full bench runs the same function."""
+"""Run one emulated experiment of bench.py (emulated_tp_experiment) in its own
+process: a BASELINE.json config slice (`c3`, `c4`, `c5`) or the Llama-3-8B
+stack at a TP size (`llama3 --group 8`). Prints one JSON object as the last
+line. bench.py runs each emulated experiment this way, under a timeout, so a
+failure there cannot take the headline measurement with it."""
 import argparse
 import json
 import os
@@ -15,7 +17,8 @@ import bench  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("config", choices=["c3", "c4", "c5"])
+    ap.add_argument("config", choices=["c3", "c4", "c5", "llama3"])
+    ap.add_argument("--group", type=int, default=0, help="TP / EP group size (default: the config's)")
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--micro-batches", type=int, default=4)
     ap.add_argument("--steps", type=int, default=5)
@@ -25,8 +28,10 @@ def main():
     a = ap.parse_args()
     import torch
 
-    from paper_2411_15871_b200.runtime import GPT3_13B, LLAMA2_70B, PHI35_MOE
-    base, group = {"c3": (GPT3_13B, 4), "c4": (PHI35_MOE, 8), "c5": (LLAMA2_70B, 4)}[a.config]
+    from paper_2411_15871_b200.runtime import GPT3_13B, LLAMA2_70B, LLAMA3_8B, PHI35_MOE
+    base, group = {"c3": (GPT3_13B, 4), "c4": (PHI35_MOE, 8), "c5": (LLAMA2_70B, 4),
+                   "llama3": (LLAMA3_8B, 8)}[a.config]
+    group = a.group or group
 
     def timed(n, fn, st):
         torch.cuda.synchronize()
