@@ -1,6 +1,6 @@
 """On-device timeline of one SI training step (eager issue, CUDA events around
 every op: DH_OP_TIMES) at TP=<tp> per-GPU shapes with emulated collectives.
-Reports where the compute lane idles and which collectives are exposed
+Also writes a Chrome trace (lanes as rows). Reports where the compute lane idles and which collectives are exposed
 (collective running while the compute lane is idle), split by what the idle
 compute op was waiting for. Writes gpurun_out/op_timeline_tp<tp>.json."""
 import argparse
@@ -99,3 +99,13 @@ res = {"tp": a.tp, "layers": a.layers, "micro_batches": a.mb, "mode": a.mode, "s
        "top_compute_gaps": [{"gap": k, "ms": round(v, 3), "count": gap_n[k]} for k, v in gaps.most_common(15)]}
 print(json.dumps(res, indent=1))
 json.dump({"summary": res, "ops": ops}, open(os.path.join(ROOT, "gpurun_out", f"op_timeline_tp{a.tp}.json"), "w"))
+# Chrome trace (chrome://tracing, Perfetto): one row per lane, an event per op
+lane_names = {0: "compute", 1: "local_comm", 2: "cross_comm"}
+events = [{"name": "process_name", "ph": "M", "pid": 0, "args": {"name": f"SI step, TP={a.tp} ({a.mode})"}}]
+events += [{"name": "thread_name", "ph": "M", "pid": 0, "tid": l, "args": {"name": n}} for l, n in lane_names.items()]
+for o in ops:
+    events.append({"name": names.get(o["node"], str(o["node"])), "ph": "X", "pid": 0, "tid": o["lane"],
+                   "ts": o["start_ms"] * 1e3, "dur": max(0.0, (o["end_ms"] - o["start_ms"]) * 1e3),
+                   "args": {"strand": o["strand"], "layer": o["layer"], "capped": o["capped"]}})
+json.dump({"traceEvents": events}, open(os.path.join(ROOT, "gpurun_out", f"op_timeline_tp{a.tp}_{a.mode}.trace.json"),
+                                        "w"))
