@@ -228,7 +228,7 @@ typedef struct dh_model_cfg {
     int slots, split_layer, pp_rank, pp_size;
     /* MoE (moe_ep template, zero = dense): experts > 1 makes the MLP a top-`topk`
      * mixture of `experts` SwiGLU experts with `capacity` slots per expert per
-     * source rank (0 = ceil(1.25 * seq * topk / experts) rounded up to 128).
+     * source rank (0 = ceil(1.25 * seq * topk / experts) rounded up to 32).
      * The context's group is then the EP group (attention runs data-parallel,
      * TP = 1) and each rank holds experts / group_size experts. */
     int experts, topk, capacity;

@@ -443,7 +443,7 @@ class MoEOracle(LlamaTPOracle):
         return nm.rb(dln1 + dlogits @ p["wr"])
 
 
-def moe_capacity(tokens, experts, topk, factor=1.25, multiple=128):
+def moe_capacity(tokens, experts, topk, factor=1.25, multiple=32):
     """Slots per expert: ceil(tokens * topk / experts * factor), rounded up to a multiple of `multiple`."""
     c = int(np.ceil(tokens * topk / experts * factor))
     return (c + multiple - 1) // multiple * multiple

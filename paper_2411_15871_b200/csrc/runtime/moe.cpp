@@ -19,9 +19,10 @@
 namespace dh {
 
 int moe_capacity(int tokens, int experts, int topk) {
-    // oracle/layer_oracle.py moe_capacity: ceil(1.25 * tokens * topk / experts), to a multiple of 128
+    // oracle/layer_oracle.py moe_capacity: ceil(1.25 * tokens * topk / experts), to a multiple of 32
+    // (a slot count the GEMM tiles need not divide; coarser rounding only adds empty rows)
     const long long c = (static_cast<long long>(tokens) * topk * 5 + 4LL * experts - 1) / (4LL * experts);
-    return static_cast<int>((c + 127) / 128 * 128);
+    return static_cast<int>((c + 31) / 32 * 32);
 }
 
 int moe_dense_id(int n) {

@@ -159,7 +159,7 @@ class LlamaShape:
     pp_rank: int = 0
     pp_size: int = 0
     # MoE (moe_ep template; 0 = dense): experts, top-k, slots per expert per
-    # source rank (0 = ceil(1.25 * seq * topk / experts) rounded up to 128)
+    # source rank (0 = ceil(1.25 * seq * topk / experts) rounded up to 32)
     experts: int = 0
     topk: int = 0
     capacity: int = 0
@@ -185,7 +185,7 @@ class LlamaShape:
     def moe_capacity(self) -> int:
         k = self.topk or 2
         c = -(-self.seq_len * k * 5 // (4 * self.experts))
-        return self.capacity or (c + 127) // 128 * 128
+        return self.capacity or (c + 31) // 32 * 32
 
 
 LLAMA3_8B = LlamaShape(hidden=4096, ffn=14336, n_heads=32, n_kv_heads=8, head_dim=128, layers=32,

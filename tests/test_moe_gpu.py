@@ -150,7 +150,7 @@ def test_router_and_assignment_on_device_ln1(ctx):
     m.close()
 
 
-@pytest.mark.parametrize("capacity", [0, 48], ids=["no_drops", "drops"])
+@pytest.mark.parametrize("capacity", [0, 128, 48], ids=["default_capacity", "no_drops", "drops"])
 def test_ep1_moe_vs_oracle_and_si_equals_sequential(ctx, capacity):
     shape = _shape(mb=2, capacity=capacity)
     orc = _oracle(shape)

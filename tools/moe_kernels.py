@@ -1,5 +1,5 @@
 """Launch each MoE kernel once at config-4 shapes (Phi-3.5-MoE: seq 3072,
-hidden 4096, 16 experts, top-2, capacity 512) for an ncu capture of achieved
+hidden 4096, 16 experts, top-2, capacity 512 — the pre-rounding-change capacity) for an ncu capture of achieved
 DRAM bandwidth (same recipe as tools/hbm_kernels.py):
 
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
