@@ -292,7 +292,7 @@ struct Lowering {
         }
         auto deferred_here = [&](int id) { return std::find(defer_now.begin(), defer_now.end(), id) != defer_now.end(); };
         bool first_step = true;
-        t_first_done_flush = true;  // the previous pair's deferred ops follow this pair's first step
+        flush_after_step = true;  // the previous pair's deferred ops follow this pair's first step
         for (const auto& st : m.plan.plan.steps) {
             const auto fa = segment(m.plan.fwd_segmentation, st.fwd_seg.value_or(0));
             std::vector<int> ba;
@@ -348,11 +348,11 @@ struct Lowering {
                     bwd_op_at[{bs, lb, ba[i]}] = static_cast<int>(prog.ops.size()) - 1;
                 }
             }
-            if (t_first_done_flush) flush_deferred();
-            t_first_done_flush = false;
+            if (flush_after_step) flush_deferred();
+            flush_after_step = false;
         }
-        if (t_first_done_flush) flush_deferred();  // (a plan without steps)
-        t_first_done_flush = false;
+        if (flush_after_step) flush_deferred();  // (a plan without steps)
+        flush_after_step = false;
         if (!defer_now.empty()) {
             deferred.strand = bs;
             deferred.layer = lb;
@@ -362,7 +362,7 @@ struct Lowering {
         }
         capped = false;
     }
-    bool t_first_done_flush = false;
+    bool flush_after_step = false;  // a deferred set from the previous pair awaits this pair's first step
 
     // ---- W pipeline stage (mode 3)
     // Local layers [0, c) are the way-down half and [c, L) the way-back half of
