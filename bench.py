@@ -181,8 +181,11 @@ def run_reference(args, world, rank):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "llama3-8b-shaped layer stack fwd+bwd (CPU oracle port)",
-                       "model": "llama3-8b-shaped", "global_batch": 1, "seq_len": shape.seq_len,
+            # the same workload as our arm's line, run by the CPU port on a bounded sample
+            "config": {"workload": f"llama3-8b-shaped {shape.layers}-layer stack fwd+bwd, "
+                                   f"{args.micro_batches} micro-batches x seq {shape.seq_len} "
+                                   f"(CPU oracle port, sampled: see cpu_baseline.sample)",
+                       "model": "llama3-8b-shaped", "global_batch": args.micro_batches, "seq_len": shape.seq_len,
                        "parallelism": "none (host CPU)"},
             "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": sample},
