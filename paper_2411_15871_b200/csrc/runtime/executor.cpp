@@ -252,6 +252,27 @@ struct Lowering {
         deferred = Deferred{};
     }
     std::map<std::tuple<int, int, int>, int> bwd_op_at;  // (strand, layer, node) -> op index (mode 4)
+    // qkv_wgrad stays in its own pair, issued just before the forward strand's
+    // bda1 (which waits for rs1); only attn_proj_wgrad crosses into the next pair.
+    // Measured at TP=8 shapes: 231.9-232.2 -> 230.1-230.5 ms/step against
+    // deferring both (DH_SI_SPLIT_DEFER=0 restores that).
+    bool split_defer = [] {
+        const char* e = std::getenv("DH_SI_SPLIT_DEFER");
+        return !e || std::atoi(e) != 0;
+    }();
+    void emit_deferred_now(int strand, int layer, int id, std::vector<int>& pending) {
+        std::map<int, std::vector<int>> preds;
+        for (const auto& [a, b] : m.bwd_dag.edges) preds[b].push_back(a);
+        std::vector<int> deps;
+        for (int p : preds[id]) deps.push_back(bwd_op_at.at({strand, layer, p}));
+        const int keep_last = strand_last[strand];
+        const bool keep_cap = capped;
+        capped = true;
+        emit(strand, layer, id, -1, &deps);
+        capped = keep_cap;
+        strand_last[strand] = keep_last;
+        pending.erase(std::remove(pending.begin(), pending.end(), id), pending.end());
+    }
 
     void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl, bool relaxed) {
         take_slot(fs, lf);
@@ -334,6 +355,12 @@ struct Lowering {
                 if (!relaxed && !is_comm(t)) {
                     for (std::size_t c = 0; c < order.size() && !cap; ++c)
                         cap = is_comm(c) && spans[c].first < spans[t].second && spans[t].first < spans[c].second;
+                }
+                if (side == 0 && fa[i] == 14 && split_defer && std::find(defer_now.begin(), defer_now.end(), 36) != defer_now.end() &&
+                    bwd_op_at.count({bs, lb, 34})) {
+                    // qkv_wgrad of this pair fills the forward strand's last stall (bda1
+                    // waits for rs1): issue it before bda1 once attn_bwd is out
+                    emit_deferred_now(bs, lb, 36, defer_now);
                 }
                 if (side == 1 && deferred.strand >= 0 && (ba[i] == 28 || ba[i] == 30 || ba[i] == 34)) {
                     // the next layer is about to overwrite an input of the deferred

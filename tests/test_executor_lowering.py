@@ -452,7 +452,8 @@ def test_deferred_wgrad_programs(tp, mb):
 def test_deferred_wgrads_with_measured_tp8_profile():
     """With the measured B200 TP=8 profile the wide-caps plan ends the backward
     layer with ag0_bwd_rs, attn_proj_wgrad, qkv_wgrad, ln0_bwd: mode 4 issues
-    those two weight gradients after the next layer's leading collective."""
+    qkv_wgrad right before the forward strand's bda1 (waiting for rs1) and
+    attn_proj_wgrad after the next layer's leading collective."""
     prof = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "profiles",
                                        "r01_b200_profile_tp8_emulated.json")))
     shape = LlamaShape(**{**LLAMA3_8B.__dict__, "layers": 4, "micro_batches": 3, "slots": 6})
@@ -468,7 +469,11 @@ def test_deferred_wgrads_with_measured_tp8_profile():
     pos = {(o["strand"], o["layer"], o["node"]): i for i, o in enumerate(prog["ops"])}
     late = [k for k in pos if k[2] in (32, 36) and (k[0], k[1] - 1, 21) in pos and
             pos[k] > pos[(k[0], k[1] - 1, 21)]]
-    assert len(late) >= 2 * 2 * (shape.layers - 1)  # both wgrads, 2 SI blocks, all but each block's last pair
+    # attn_proj_wgrad crosses into the next pair (2 SI blocks, all but each block's
+    # last pair); qkv_wgrad stays in its pair, right before the forward strand's bda1
+    assert len([k for k in late if k[2] == 32]) >= 2 * (shape.layers - 1)
+    fwd_bda1 = [i for i, o in enumerate(prog["ops"]) if o["node"] == 14]
+    assert any(prog["ops"][i - 1]["node"] == 36 for i in fwd_bda1)
 
 
 def test_deferred_wgrads_single_step_plan():
