@@ -317,3 +317,68 @@ def test_ep2_optimizer_keeps_replicas_identical():
     for r in range(ep):
         for n in DENSE_W + MOE_W:
             assert not torch.equal(outs[r][0][n], outs[r][1][n]), f"rank {r}: {n} not updated"
+
+
+@pytest.mark.parametrize("T,E,K,C", [(200, 8, 1, 16), (96, 16, 3, 12), (130, 12, 2, 16)])
+def test_moe_kernels_vs_oracle_edge_cases(T, E, K, C):
+    """Kernel level, against the oracle's routing and numpy restatements: top-1 /
+    top-3, expert counts that are not powers of two, token counts that are not
+    multiples of anything, and capacities small enough to drop most assignments."""
+    from paper_2411_15871_b200 import device as dh
+    H = 256
+    rng = np.random.default_rng(T + E + K)
+    x = bf16_round(rng.standard_normal((T, H)).astype(np.float32))
+    wr = bf16_round((rng.standard_normal((E, H)) * 0.05).astype(np.float32))
+    orc = MoEOracle(H, 256, 4, 2, 64, 1, T, E, topk=K, capacity=C, bf16=True, seed=1)
+    probs, ids, wts, slot = orc.route(x, wr)
+    cuda = dict(device="cuda")
+    xd = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    wrd = torch.from_numpy(wr).to(torch.bfloat16).cuda()
+    pd = torch.empty(T, E, **cuda)
+    idd = torch.empty(T, K, dtype=torch.int32, **cuda)
+    wd = torch.empty(T, K, **cuda)
+    dh.moe_router_fwd(xd, wrd, pd, idd, wd, K)
+    srt = np.sort(probs, 1)[:, ::-1]
+    decisive = (srt[:, K - 1] - srt[:, K]) > 1e-5 if K < E else np.ones(T, bool)
+    assert np.array_equal(idd.cpu().numpy()[decisive], ids[decisive])
+    assert np.max(np.abs(pd.cpu().numpy() - probs)) < 1e-5
+    # slots from the device's own expert choice (near-ties aside, the same)
+    ids_dev = idd.cpu().numpy().astype(np.int64)
+    sl = torch.empty(T, K, dtype=torch.int32, **cuda)
+    src = torch.empty(E * C, dtype=torch.int32, **cuda)
+    dh.moe_assign(idd, E, C, sl, src)
+    fill, ref_slot = np.zeros(E, np.int64), np.full((T, K), -1, np.int64)
+    for t in range(T):
+        for k in range(K):
+            e = ids_dev[t, k]
+            if fill[e] < C:
+                ref_slot[t, k] = e * C + fill[e]
+                fill[e] += 1
+    assert np.array_equal(sl.cpu().numpy(), ref_slot)
+    assert (ref_slot < 0).any()
+    # permute / unpermute / their backwards against numpy on the same slots
+    xp = torch.empty(E * C, H, dtype=torch.bfloat16, **cuda)
+    dh.moe_permute(xd, src, xp, K)
+    ref_xp = np.zeros((E * C, H), np.float32)
+    for t in range(T):
+        for k in range(K):
+            if ref_slot[t, k] >= 0:
+                ref_xp[ref_slot[t, k]] = x[t]
+    assert np.array_equal(xp.float().cpu().numpy(), ref_xp)
+    y = bf16_round(rng.standard_normal((E * C, H)).astype(np.float32))
+    yd = torch.from_numpy(y).to(torch.bfloat16).cuda()
+    out = torch.empty(T, H, dtype=torch.bfloat16, **cuda)
+    dh.moe_unpermute(yd, sl, wd, out)
+    w_dev = wd.cpu().numpy()
+    ref_out = np.zeros((T, H), np.float32)
+    for k in range(K):
+        ok = ref_slot[:, k] >= 0
+        ref_out[ok] += w_dev[ok, k:k + 1] * y[ref_slot[ok, k]]
+    assert np.array_equal(out.float().cpu().numpy(), bf16_round(ref_out))
+    dxp = torch.empty(T, H, dtype=torch.bfloat16, **cuda)
+    dh.moe_permute_bwd(yd, sl, dxp)
+    ref_dx = np.zeros((T, H), np.float32)
+    for k in range(K):
+        ok = ref_slot[:, k] >= 0
+        ref_dx[ok] += y[ref_slot[ok, k]]
+    assert np.array_equal(dxp.float().cpu().numpy(), bf16_round(ref_dx))
