@@ -222,7 +222,9 @@ def cpu_baseline_sample(shape):
                       f"fp32 (oracle/layer_oracle.py), {dt:.1f} s, extrapolated x{shape.layers} layers"}
 
 
-WIDE_CAPS = {"sequences": 16, "segments": 14, "candidates": 200000}
+# wide plan search (0.9 s at TP=8): 64 candidate sequences per strand; measured at
+# TP=8 shapes 228.9 ms/step vs 229.3-230.7 with 16 sequences / 200k candidates
+WIDE_CAPS = {"sequences": 64, "segments": 14, "candidates": 1000000}
 
 
 def memory_vs_model(planner, info, shape):

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--nccl-ctas", type=int, default=16)
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--overlap-ctas", type=int, default=None, help="GEMM SM cap under SI (0 = none)")
+    ap.add_argument("--wide-caps", default=None, help="JSON caps for the wide plan search (default: bench.WIDE_CAPS)")
     a = ap.parse_args()
     import torch
 
@@ -43,6 +44,8 @@ def main():
         torch.cuda.synchronize()
         return s.elapsed_time(e) / n
 
+    if a.wide_caps:
+        bench.WIDE_CAPS = json.loads(a.wide_caps)
     args = types.SimpleNamespace(nccl_ctas=a.nccl_ctas, steps=a.steps, layers=a.layers,
                                  micro_batches=a.micro_batches, overlap_ctas=a.overlap_ctas)
     r = bench.emulated_tp_experiment(args, group, timed, full=a.full, base_shape=base, layers=a.layers,
