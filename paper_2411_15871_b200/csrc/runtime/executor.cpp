@@ -272,7 +272,11 @@ struct Lowering {
         capped = keep_cap;
         strand_last[strand] = keep_last;
         pending.erase(std::remove(pending.begin(), pending.end(), id), pending.end());
+        issued_early.push_back(id);
     }
+    // ids of the current pair already issued ahead of their step (never cleared
+    // within the pair, so a later step cannot issue them a second time)
+    std::vector<int> issued_early;
 
     void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl, bool relaxed) {
         take_slot(fs, lf);
@@ -311,7 +315,11 @@ struct Lowering {
                 if (id == 32 || id == 36) defer_now.push_back(id);
             }
         }
-        auto deferred_here = [&](int id) { return std::find(defer_now.begin(), defer_now.end(), id) != defer_now.end(); };
+        issued_early.clear();
+        auto deferred_here = [&](int id) {
+            return std::find(defer_now.begin(), defer_now.end(), id) != defer_now.end() ||
+                   std::find(issued_early.begin(), issued_early.end(), id) != issued_early.end();
+        };
         bool first_step = true;
         flush_after_step = true;  // the previous pair's deferred ops follow this pair's first step
         for (const auto& st : m.plan.plan.steps) {

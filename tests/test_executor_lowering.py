@@ -488,3 +488,27 @@ def test_deferred_wgrads_single_step_plan():
     prog, rel = lower(shape, 2, plan, "si_deferred"), lower(shape, 2, plan, "si_relaxed")
     check_buffer_hazards(prog, shape.layers, acc)
     assert observed_writers(prog, shape.layers, acc) == observed_writers(rel, shape.layers, acc)
+
+
+def test_deferred_wgrads_issue_each_node_once():
+    """Mode 4 with split deferral: a plan whose backward strand has trailing
+    backward-only steps and places qkv_wgrad (36) after ag0_bwd_rs (37).
+    qkv_wgrad is issued early, before the forward strand's bda1. A later step
+    must not issue it again (qkv_wgrad accumulates, so a second issue would
+    double dWqkv silently). Every (strand, layer, node) appears exactly once."""
+    from collections import Counter
+    shape = LlamaShape(**{**TINY.__dict__, "micro_batches": 2, "n_kv_heads": 2, "slots": TINY.layers + 2})
+    plan = json.loads(_plan(shape, 2))
+    plan.update(bwd_seq=[20, 21, 22, 26, 24, 25, 27, 23, 28, 29, 30, 31, 34, 35, 37, 32, 36, 38],
+                fwd_cuts=[], bwd_cuts=[15],
+                steps=[{"fwd_seg": 1, "bwd_seg": 1}, {"fwd_seg": None, "bwd_seg": 2}])
+    plan_json = json.dumps(plan)
+    prog = lower(shape, 2, plan_json, "si_deferred")
+    rel = lower(shape, 2, plan_json, "si_relaxed")
+    cnt = Counter((o["strand"], o["layer"], o["node"]) for o in prog["ops"] if o["node"] != 100)
+    assert max(cnt.values()) == 1, [k for k, v in cnt.items() if v > 1]
+    assert sorted(cnt) == sorted((o["strand"], o["layer"], o["node"]) for o in rel["ops"] if o["node"] != 100)
+    check_program(prog, shape, 2, strict_order=False)
+    acc = lambda n, L, l, s: _dense_access(n, 2, L, l, s)  # noqa: E731
+    check_buffer_hazards(prog, shape.layers, acc)
+    assert observed_writers(prog, shape.layers, acc) == observed_writers(rel, shape.layers, acc)
