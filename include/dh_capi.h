@@ -138,6 +138,9 @@ int dh_adamw_dev(float* master, void* weight_bf16, float* grad, float* m, float*
 /* Deterministic normal(0, std) init of bf16 (and optional fp32 master) from (seed, offset). */
 int dh_init_normal(void* bf16_out, float* f32_out, long long n, unsigned long long seed,
                    float std_dev, void* stream);
+/* Holds `stream` for `ns` nanoseconds (one thread, globaltimer): a launch gate
+ * so ops queued behind it start together, free of host launch latency. */
+int dh_spin_ns(long long ns, void* stream);
 int dh_fill_bf16(void* out, float value, long long n, void* stream);
 int dh_copy(void* dst, const void* src, long long bytes, void* stream);
 /* Single-GPU stand-in for one rank's collective (mode 0 AllGather of `count`
@@ -191,11 +194,20 @@ typedef struct dh_ctx dh_ctx;
 typedef struct dh_model dh_model;
 
 /* One context per GPU / TP rank. nccl_unique_id: the 128-byte ncclUniqueId
- * shared by the TP group (NULL when tp_size == 1). nccl_max_ctas caps the SMs
+ * shared by the TP group (NULL when tp_size == 1; with tp_size == 1 and an id,
+ * a one-rank communicator that only dh_comm_run uses). nccl_max_ctas caps the SMs
  * NCCL kernels occupy (0 = NCCL default) so they coexist with the other
  * strand's GEMMs (north star (2)). Streams: one per weft::Lane. */
 int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_id,
                   int nccl_max_ctas, dh_ctx** out);
+/* One W-pipeline stage on one GPU (weft SendRecv between stages, reference
+ * folding_pipeline.cpp:157-192): a dh_ctx_create context for this stage's TP
+ * group plus a stage group of pp_size ranks over NCCL (pp_unique_id shared by
+ * the stage group; NULL when pp_size == 1). Activations and gradients travel
+ * on two communicators split from the stage group, each on its own stream,
+ * so a stage's sends never block its compute stream. Not graph-capturable. */
+int dh_ctx_create_pp(int device, int tp_rank, int tp_size, const void* tp_unique_id, int pp_rank, int pp_size,
+                     const void* pp_unique_id, int nccl_max_ctas, dh_ctx** out);
 /* Single-process pipeline group on ONE device (test backend): pp_size stage
  * contexts (TP = 1) whose point-to-point activation / gradient transfers are
  * staged device copies matched in program order (never blocking the sender). */
@@ -211,6 +223,17 @@ int dh_loopback_group_create(int device, int tp_size, dh_ctx** ctxs_out);
  * timing- and SM-footprint-faithful. Graph-capturable. */
 int dh_ctx_create_emulated(int device, int tp_size, int comm_ctas, double link_gbs, dh_ctx** out);
 int dh_ctx_destroy(dh_ctx* ctx);
+/* One collective of the context's TP / EP group on lane stream `lane`,
+ * enqueue-only (the same backend call the SI executor issues for an ag / rs /
+ * a2a node; reference comm bytes op_model.cpp:290-301). bf16 elements, except
+ * DH_COMM_ALL_REDUCE_F32 (fp32; recv may equal send):
+ *   ALL_GATHER      recv[r*count + i] = send_r[i]
+ *   REDUCE_SCATTER  recv[i] = sum_r send_r[rank*count + i]
+ *   ALL_TO_ALL      recv[src*count + i] = send_src[rank*count + i]
+ * Used to time each collective alone (bench.py: NVLink bus GB/s) and to test
+ * the backends against their definitions. */
+enum { DH_COMM_ALL_GATHER = 0, DH_COMM_REDUCE_SCATTER = 1, DH_COMM_ALL_REDUCE_F32 = 2, DH_COMM_ALL_TO_ALL = 3 };
+int dh_comm_run(dh_ctx* ctx, int op, const void* send, void* recv, long long count, int lane);
 void* dh_ctx_stream(dh_ctx* ctx, int lane);
 int dh_nccl_unique_id(void* out128);
 
@@ -294,10 +317,13 @@ int dh_model_tensor(dh_model* m, const char* name, int layer, int strand, void**
  * with dh_free_string. */
 int dh_model_info_json(dh_model* m, char** out);
 void dh_free_string(char* s);
-/* Timing probe: CUDA events around every launch of template node `node` (-1 =
- * off) in the lowered program, on the launching lane stream; after a run,
- * dh_model_probe_read returns the summed kernel time and the launch count. */
+/* Timing probes: CUDA events around every launch of template node `node` in
+ * the lowered program, on the launching lane stream. Each call adds a node to
+ * the probed set (-1 = clear all). After a run, dh_model_probe_read_node
+ * returns one node's summed time and launch count (dh_model_probe_read: the
+ * first probed node). Re-arm after dh_model_set_plan (the program changed). */
 int dh_model_probe(dh_model* m, int node);
+int dh_model_probe_read_node(dh_model* m, int node, double* total_ms, int* count);
 /* Measurement mode: re-lower the current plan without its collective nodes
  * (compute order and step barriers unchanged) so T_SI - T_compute_only gives
  * the exposed communication. */

@@ -621,6 +621,14 @@ __global__ void comm_proxy_kernel(const uint4* __restrict__ src, uint4* __restri
     while (globaltimer_ns() - t0 < target_ns) __nanosleep(256);
 }
 
+// One thread that holds its stream for `ns` nanoseconds (globaltimer): the
+// overlap profiler queues the measured ops behind it, so their host-side
+// launch cost never shows up between the timing events.
+__global__ void spin_kernel(unsigned long long ns) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (globaltimer_ns() - t0 < ns) __nanosleep(128);
+}
+
 int grid_for(long long work, int threads) {
     const long long blocks = (work + threads - 1) / threads;
     return static_cast<int>(std::max<long long>(1, std::min<long long>(blocks, 148LL * 16)));
@@ -862,6 +870,13 @@ int dh_comm_proxy(const void* src, void* dst, long long count, int tp, int mode,
     }();
     comm_proxy_kernel<<<std::max(1, ctas), 1024, smem_kb * 1024, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4*>(src), static_cast<uint4*>(dst), chunk, mode, tp, target);
+    DH_CUDA_CHECK(cudaGetLastError());
+    return DH_OK;
+}
+
+int dh_spin_ns(long long ns, void* stream) {
+    if (ns <= 0) return DH_OK;
+    spin_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<unsigned long long>(ns));
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

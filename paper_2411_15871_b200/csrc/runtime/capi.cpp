@@ -338,6 +338,7 @@ int dh_model_sync(dh_model* m) {
     if (!m) return dh::set_error(DH_ERR_INVALID, "null model");
     RT_CUDA(cudaSetDevice(m->ctx->device));
     for (auto s : m->ctx->lane) RT_CUDA(cudaStreamSynchronize(s));
+    if (m->ctx->pp) RT_TRY(m->ctx->pp->sync());
     return DH_OK;
 }
 
@@ -405,7 +406,12 @@ int dh_model_probe(dh_model* m, int node) {
 
 int dh_model_probe_read(dh_model* m, double* total_ms, int* count) {
     if (!m || !total_ms || !count) return dh::set_error(DH_ERR_INVALID, "null argument");
-    return dh::read_probe(*m, total_ms, count);
+    return dh::read_probe(*m, -1, total_ms, count);
+}
+
+int dh_model_probe_read_node(dh_model* m, int node, double* total_ms, int* count) {
+    if (!m || !total_ms || !count) return dh::set_error(DH_ERR_INVALID, "null argument");
+    return dh::read_probe(*m, node, total_ms, count);
 }
 
 }  // extern "C"

@@ -16,6 +16,7 @@
 //                    can be tested on a single GPU. Not capturable.
 #include <nccl.h>
 
+#include <array>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -50,8 +51,15 @@ namespace {
 class NcclComm final : public Comm {
 public:
     ncclComm_t comm = nullptr;
+    float* one = nullptr;  // barrier operand
     ~NcclComm() override {
         if (comm) ncclCommDestroy(comm);
+        if (one) cudaFree(one);
+    }
+    int barrier(cudaStream_t s) override {
+        if (!one) RT_CUDA(cudaMalloc(&one, sizeof(float)));
+        RT_NCCL(ncclAllReduce(one, one, 1, ncclFloat32, ncclSum, comm, s));
+        return DH_OK;
     }
     int all_gather(const void* send, void* recv, size_t count, cudaStream_t s) override {
         RT_NCCL(ncclAllGather(send, recv, count, ncclBfloat16, comm, s));
@@ -112,7 +120,93 @@ public:
     const char* name() const override { return "emulated"; }
 };
 
+// Pipeline-stage transfers over NCCL (weft SendRecv between W-pipeline
+// stages, one GPU each). NCCL matches point-to-point messages per direction
+// in issue order, not by tag, and a stage may send a micro-batch's activation
+// before it receives an earlier one's gradient (the W schedule does, see
+// tests/test_executor_lowering.py). So activations and gradients travel on
+// two communicators split from the stage group, each with its own stream:
+// within one kind, sender and receiver issue in micro-batch order. A send
+// first copies the payload into a staging buffer on the issuing (compute)
+// stream, so the next op may overwrite the source, and the NCCL send then
+// runs on the kind's stream; it never blocks the compute stream. A receive
+// runs on the kind's stream and the compute stream waits for it.
+class NcclP2P final : public Comm {
+public:
+    ncclComm_t base = nullptr;
+    std::array<ncclComm_t, 2> kind_comm{};
+    std::array<cudaStream_t, 2> kind_stream{};
+    std::array<cudaEvent_t, 2> to_kind{}, from_kind{};  // re-recorded per transfer
+    ~NcclP2P() override {
+        for (auto c : kind_comm)
+            if (c) ncclCommDestroy(c);
+        if (base) ncclCommDestroy(base);
+        for (auto st : kind_stream)
+            if (st) cudaStreamDestroy(st);
+        for (auto e : to_kind)
+            if (e) cudaEventDestroy(e);
+        for (auto e : from_kind)
+            if (e) cudaEventDestroy(e);
+    }
+    int init(int rank, int size, const void* unique_id) {
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof(id));
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        RT_NCCL(ncclCommInitRankConfig(&base, size, id, rank, &cfg));
+        int lo = 0, hi = 0;
+        RT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        for (int k = 0; k < 2; ++k) {
+            ncclConfig_t c2 = NCCL_CONFIG_INITIALIZER;
+            RT_NCCL(ncclCommSplit(base, 0, rank, &kind_comm[k], &c2));
+            RT_CUDA(cudaStreamCreateWithPriority(&kind_stream[k], cudaStreamNonBlocking, hi));
+            RT_CUDA(cudaEventCreateWithFlags(&to_kind[k], cudaEventDisableTiming));
+            RT_CUDA(cudaEventCreateWithFlags(&from_kind[k], cudaEventDisableTiming));
+        }
+        return DH_OK;
+    }
+    int all_gather(const void*, void*, size_t, cudaStream_t) override { return unsupported(); }
+    int reduce_scatter(const void*, void*, size_t, cudaStream_t) override { return unsupported(); }
+    int all_reduce_f32(float*, size_t, cudaStream_t) override { return unsupported(); }
+    int send(const void* buf, size_t bytes, int peer, int tag, cudaStream_t s) override {
+        const int k = tag & 1;  // xfer_tag: 0 activation, 1 gradient (+ 2 * micro-batch)
+        void* staging = nullptr;
+        RT_CUDA(cudaMallocAsync(&staging, bytes, s));
+        RT_CUDA(cudaMemcpyAsync(staging, buf, bytes, cudaMemcpyDeviceToDevice, s));
+        RT_CUDA(cudaEventRecord(to_kind[k], s));
+        RT_CUDA(cudaStreamWaitEvent(kind_stream[k], to_kind[k], 0));
+        RT_NCCL(ncclSend(staging, bytes, ncclChar, peer, kind_comm[k], kind_stream[k]));
+        RT_CUDA(cudaFreeAsync(staging, kind_stream[k]));
+        return DH_OK;
+    }
+    int recv(void* buf, size_t bytes, int peer, int tag, cudaStream_t s) override {
+        const int k = tag & 1;
+        // the destination is free once the compute stream got here
+        RT_CUDA(cudaEventRecord(to_kind[k], s));
+        RT_CUDA(cudaStreamWaitEvent(kind_stream[k], to_kind[k], 0));
+        RT_NCCL(ncclRecv(buf, bytes, ncclChar, peer, kind_comm[k], kind_stream[k]));
+        RT_CUDA(cudaEventRecord(from_kind[k], kind_stream[k]));
+        RT_CUDA(cudaStreamWaitEvent(s, from_kind[k], 0));
+        return DH_OK;
+    }
+    int sync() override {
+        for (auto st : kind_stream) RT_CUDA(cudaStreamSynchronize(st));
+        return DH_OK;
+    }
+    bool capturable() const override { return false; }
+    const char* name() const override { return "nccl_p2p"; }
+
+private:
+    int unsupported() { return set_error(DH_ERR_CONFIG, "nccl_p2p: pipeline transfers only"); }
+};
+
 }  // namespace
+
+std::unique_ptr<Comm> make_nccl_p2p(int rank, int size, const void* unique_id, int* rc) {
+    auto c = std::make_unique<NcclP2P>();
+    *rc = c->init(rank, size, unique_id);
+    if (*rc != DH_OK) return nullptr;
+    return c;
+}
 
 std::unique_ptr<Comm> make_nccl_comm(int rank, int size, const void* unique_id, int max_ctas,
                                      int* rc) {
@@ -378,7 +472,9 @@ int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_
     c->tp_size = tp_size;
     c->comm_ctas = nccl_max_ctas;
     int rc = init_streams(c);
-    if (rc == DH_OK && tp_size > 1) {
+    // tp_size == 1 with an id: a one-rank NCCL communicator (the model issues no
+    // collectives at TP = 1; dh_comm_run exercises the NCCL path on one GPU)
+    if (rc == DH_OK && (tp_size > 1 || nccl_unique_id)) {
         if (!nccl_unique_id) {
             rc = dh::set_error(DH_ERR_INVALID, "dh_ctx_create: tp_size > 1 needs an ncclUniqueId");
         } else {
@@ -388,6 +484,26 @@ int dh_ctx_create(int device, int tp_rank, int tp_size, const void* nccl_unique_
     if (rc != DH_OK) {
         dh_ctx_destroy(c);
         return rc;
+    }
+    *out = c;
+    return DH_OK;
+}
+
+int dh_ctx_create_pp(int device, int tp_rank, int tp_size, const void* tp_unique_id, int pp_rank, int pp_size,
+                     const void* pp_unique_id, int nccl_max_ctas, dh_ctx** out) {
+    if (!out || pp_size < 1 || pp_rank < 0 || pp_rank >= pp_size || (pp_size > 1 && !pp_unique_id))
+        return dh::set_error(DH_ERR_INVALID, "dh_ctx_create_pp: bad stage rank/size or missing ncclUniqueId");
+    dh_ctx* c = nullptr;
+    RT_TRY(dh_ctx_create(device, tp_rank, tp_size, tp_unique_id, nccl_max_ctas, &c));
+    c->pp_rank = pp_rank;
+    c->pp_size = pp_size;
+    if (pp_size > 1) {
+        int rc = DH_OK;
+        c->pp = dh::make_nccl_p2p(pp_rank, pp_size, pp_unique_id, &rc);
+        if (rc != DH_OK) {
+            dh_ctx_destroy(c);
+            return rc;
+        }
     }
     *out = c;
     return DH_OK;
@@ -468,6 +584,24 @@ int dh_ctx_destroy(dh_ctx* c) {
     delete c;
     if (last) delete grp;
     return DH_OK;
+}
+
+int dh_comm_run(dh_ctx* c, int op, const void* send, void* recv, long long count, int lane) {
+    if (!c || lane < 0 || lane >= dh::kLanes || count < 0)
+        return dh::set_error(DH_ERR_INVALID, "dh_comm_run: bad context, lane or count");
+    if (!c->comm) return dh::set_error(DH_ERR_CONFIG, "dh_comm_run: the context has no TP/EP communicator");
+    RT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t s = c->lane[lane];
+    const auto n = static_cast<size_t>(count);
+    switch (op) {
+        case DH_COMM_ALL_GATHER: return c->comm->all_gather(send, recv, n, s);
+        case DH_COMM_REDUCE_SCATTER: return c->comm->reduce_scatter(send, recv, n, s);
+        case DH_COMM_ALL_REDUCE_F32:
+            if (send != recv) RT_CUDA(cudaMemcpyAsync(recv, send, n * 4, cudaMemcpyDeviceToDevice, s));
+            return c->comm->all_reduce_f32(static_cast<float*>(recv), n, s);
+        case DH_COMM_ALL_TO_ALL: return c->comm->all_to_all(send, recv, n, 1, false, s);
+        default: return dh::set_error(DH_ERR_INVALID, "dh_comm_run: unknown op");
+    }
 }
 
 void* dh_ctx_stream(dh_ctx* c, int lane) {

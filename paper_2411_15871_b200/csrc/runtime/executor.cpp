@@ -560,16 +560,17 @@ struct OpTimes {
 
 int issue(Model& m, OpTimes* ot = nullptr) {
     Ctx& c = *m.ctx;
-    std::size_t probe = 0;
+    std::map<int, std::size_t> probe;  // node -> next probe slot
     static const bool trace = std::getenv("DH_TRACE") != nullptr;
     for (std::size_t i = 0; i < m.prog.ops.size(); ++i) {
         const Op& o = m.prog.ops[i];
         cudaStream_t s = c.lane[o.lane];
         for (int w : o.waits) RT_CUDA(cudaStreamWaitEvent(s, m.events[w], 0));
-        const bool probed = o.node == m.probe_node && probe < m.probe_events.size();
+        auto pe = m.probe_events.find(o.node);
+        std::pair<cudaEvent_t, cudaEvent_t>* pr = nullptr;
+        if (pe != m.probe_events.end() && probe[o.node] < pe->second.size()) pr = &pe->second[probe[o.node]++];
         // External records stay real timing events inside a captured graph.
-        if (probed)
-            RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe].first, s, cudaEventRecordExternal));
+        if (pr) RT_CUDA(cudaEventRecordWithFlags(pr->first, s, cudaEventRecordExternal));
         if (trace) std::fprintf(stderr, "[dh] op %zu strand %d layer %d node %d lane %d\n", i, o.strand, o.layer, o.node, o.lane);
         if (ot) RT_CUDA(cudaEventRecord(ot->ev[2 * i], s));
         RT_TRY(launch_node(m, o, s));
@@ -578,8 +579,7 @@ int issue(Model& m, OpTimes* ot = nullptr) {
             const cudaError_t e = cudaStreamSynchronize(s);
             std::fprintf(stderr, "[dh]   done: %s\n", cudaGetErrorString(e));
         }
-        if (probed)
-            RT_CUDA(cudaEventRecordWithFlags(m.probe_events[probe++].second, s, cudaEventRecordExternal));
+        if (pr) RT_CUDA(cudaEventRecordWithFlags(pr->second, s, cudaEventRecordExternal));
         if (m.events[i]) RT_CUDA(cudaEventRecord(m.events[i], s));
     }
     return DH_OK;
@@ -657,38 +657,57 @@ int run_program(Model& m, bool use_graph) {
     return DH_OK;
 }
 
+// node < 0 clears every probe; otherwise adds `node` to the probed set.
 int set_probe(Model& m, int node) {
-    for (auto& pr : m.probe_events) {
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
+    if (node < 0) {
+        for (auto& [n, v] : m.probe_events)
+            for (auto& pr : v) {
+                cudaEventDestroy(pr.first);
+                cudaEventDestroy(pr.second);
+            }
+        m.probe_events.clear();
+        m.probe_nodes.clear();
+    } else if (std::find(m.probe_nodes.begin(), m.probe_nodes.end(), node) == m.probe_nodes.end()) {
+        m.probe_nodes.push_back(node);
     }
-    m.probe_events.clear();
-    m.probe_node = node;
     if (m.graph) {
         cudaGraphExecDestroy(m.graph);
         m.graph = nullptr;
     }
     if (node < 0) return DH_OK;
     RT_CUDA(cudaSetDevice(m.ctx->device));
+    auto& v = m.probe_events[node];
+    for (auto& pr : v) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    v.clear();
     for (const auto& o : m.prog.ops) {
         if (o.node != node) continue;
         std::pair<cudaEvent_t, cudaEvent_t> pr{};
         RT_CUDA(cudaEventCreate(&pr.first));
         RT_CUDA(cudaEventCreate(&pr.second));
-        m.probe_events.push_back(pr);
+        v.push_back(pr);
     }
     return DH_OK;
 }
 
-int read_probe(Model& m, double* total_ms, int* count) {
+// node < 0: the first probed node
+int read_probe(Model& m, int node, double* total_ms, int* count) {
+    if (node < 0 && !m.probe_nodes.empty()) node = m.probe_nodes.front();
     double sum = 0.0;
-    for (auto& pr : m.probe_events) {
-        float ms = 0.f;
-        RT_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
-        sum += ms;
+    int n = 0;
+    auto it = m.probe_events.find(node);
+    if (it != m.probe_events.end()) {
+        for (auto& pr : it->second) {
+            float ms = 0.f;
+            RT_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+            sum += ms;
+        }
+        n = static_cast<int>(it->second.size());
     }
     *total_ms = sum;
-    *count = static_cast<int>(m.probe_events.size());
+    *count = n;
     return DH_OK;
 }
 

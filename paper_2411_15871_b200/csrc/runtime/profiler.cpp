@@ -22,6 +22,8 @@
 #include "nlohmann/json.hpp"
 #include "runtime.hpp"
 
+extern "C" int dh_spin_ns(long long ns, void* stream);
+
 namespace dh {
 namespace {
 
@@ -51,42 +53,42 @@ Op node_op(const Model& m, const weft::OpNode& n, bool fwd) {
     return o;
 }
 
-int time_solo(Model& m, const Op& o, int iters, double* us) {
-    cudaStream_t s = m.ctx->lane[o.lane];
-    Timer t;
-    for (int i = 0; i < 2; ++i) RT_TRY(launch_node(m, o, s));
-    RT_CUDA(cudaEventRecord(t.a, s));
-    for (int i = 0; i < iters; ++i) RT_TRY(launch_node(m, o, s));
-    RT_CUDA(cudaEventRecord(t.b, s));
-    RT_CUDA(cudaEventSynchronize(t.b));
-    float ms = 0.f;
-    RT_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
-    *us = 1e3 * ms / iters;
-    return DH_OK;
-}
+// One measurement harness for solo and pair times (so Eq. 1 compares like with
+// like): every iteration first aligns the ranks on the device (a one-element
+// all-reduce, when the context has a communicator: a collective's time must
+// not include waiting for a late peer), then queues the op(s) behind a
+// device-side gate on lane 0 (dh_spin_ns). The start event is recorded when
+// the gate opens, so the host cost of the launches (tensor-map encoding,
+// NCCL enqueue) falls inside the gate, not between the events; both lanes are
+// released by the same event and the stop event waits for both.
+constexpr long long kGateNs = 150000;
 
-int time_pair(Model& m, const Op& a, const Op& b, int iters, double* us) {
-    cudaStream_t sa = m.ctx->lane[a.lane], sb = m.ctx->lane[b.lane];
+int time_gated(Model& m, const Op& a, const Op* b, int iters, double* us) {
+    cudaStream_t s0 = m.ctx->lane[0];
+    cudaStream_t sa = m.ctx->lane[a.lane], sb = b ? m.ctx->lane[b->lane] : nullptr;
     Timer t;
     cudaEvent_t go = nullptr, done_a = nullptr, done_b = nullptr;
     RT_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
     RT_CUDA(cudaEventCreateWithFlags(&done_a, cudaEventDisableTiming));
     RT_CUDA(cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming));
-    cudaStream_t s0 = m.ctx->lane[0];
     double total = 0.0;
     int rc = DH_OK;
     for (int i = 0; i < iters + 1 && rc == DH_OK; ++i) {
-        // release both lanes at the same instant, stop when both finished
+        if (m.ctx->comm) rc = m.ctx->comm->barrier(s0);
+        if (rc == DH_OK) rc = dh_spin_ns(kGateNs, s0);
+        if (rc != DH_OK) break;
         cudaEventRecord(t.a, s0);
         cudaEventRecord(go, s0);
         cudaStreamWaitEvent(sa, go, 0);
-        cudaStreamWaitEvent(sb, go, 0);
+        if (sb && sb != sa) cudaStreamWaitEvent(sb, go, 0);
         rc = launch_node(m, a, sa);
-        if (rc == DH_OK) rc = launch_node(m, b, sb);
+        if (rc == DH_OK && b) rc = launch_node(m, *b, sb);
         cudaEventRecord(done_a, sa);
-        cudaEventRecord(done_b, sb);
         cudaStreamWaitEvent(s0, done_a, 0);
-        cudaStreamWaitEvent(s0, done_b, 0);
+        if (sb) {
+            cudaEventRecord(done_b, sb);
+            cudaStreamWaitEvent(s0, done_b, 0);
+        }
         cudaEventRecord(t.b, s0);
         cudaEventSynchronize(t.b);
         float ms = 0.f;
@@ -101,6 +103,10 @@ int time_pair(Model& m, const Op& a, const Op& b, int iters, double* us) {
     *us = 1e3 * total / iters;
     return DH_OK;
 }
+
+int time_solo(Model& m, const Op& o, int iters, double* us) { return time_gated(m, o, nullptr, iters, us); }
+
+int time_pair(Model& m, const Op& a, const Op& b, int iters, double* us) { return time_gated(m, a, &b, iters, us); }
 
 }  // namespace
 

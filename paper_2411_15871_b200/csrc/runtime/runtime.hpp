@@ -65,12 +65,17 @@ public:
     virtual int recv(void* buf, size_t bytes, int peer, int tag, cudaStream_t s) {
         return set_error(DH_ERR_CONFIG, std::string(name()) + ": no point-to-point transfers");
     }
+    // wait until every transfer this backend issued on its own streams is done
+    virtual int sync() { return DH_OK; }
+    // device-side rank alignment on stream s (the profiler's per-iteration start)
+    virtual int barrier(cudaStream_t s) { return DH_OK; }
     virtual bool capturable() const = 0;
     virtual const char* name() const = 0;
 };
 
 std::unique_ptr<Comm> make_nccl_comm(int rank, int size, const void* unique_id, int max_ctas,
                                      int* rc);
+std::unique_ptr<Comm> make_nccl_p2p(int rank, int size, const void* unique_id, int* rc);
 struct LoopbackGroup;
 std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* group, int rank, int* rc);
 
@@ -209,10 +214,10 @@ struct Model {
     weft::OverlapTable plan_overlap;  // table the lowering replays the lane model with
     std::array<cudaEvent_t, kLanes> fork_join{};
     std::vector<int> y_slot;  // slot holding each strand's last-layer output
-    // timing probe: events around every launch of one template node
-    int probe_node = -1;
+    // timing probes: events around every launch of the probed template nodes
+    std::vector<int> probe_nodes;
     bool skip_comm = false;  // measurement mode: collectives become no-ops (compute-only time)
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probe_events;
+    std::map<int, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> probe_events;  // node -> per launch
 
     template <class T = void>
     T* ptr(const Buf& b) const {
@@ -239,7 +244,7 @@ int run_program(Model& m, bool use_graph);
 int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s);
 int arm_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s);
 int set_probe(Model& m, int node);
-int read_probe(Model& m, double* total_ms, int* count);
+int read_probe(Model& m, int node, double* total_ms, int* count);
 
 }  // namespace dh
 

@@ -32,11 +32,14 @@ class OptimCfg(ctypes.Structure):
 
 _SIGS = {
     "dh_ctx_create": ([c_int, c_int, c_int, c_void_p, c_int, ctypes.POINTER(c_void_p)], c_int),
+    "dh_ctx_create_pp": ([c_int, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_int,
+                          ctypes.POINTER(c_void_p)], c_int),
     "dh_loopback_group_create": ([c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
     "dh_loopback_pp_group_create": ([c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
     "dh_ctx_create_emulated": ([c_int, c_int, c_int, ctypes.c_double, ctypes.POINTER(c_void_p)], c_int),
     "dh_ctx_destroy": ([c_void_p], c_int),
     "dh_ctx_stream": ([c_void_p, c_int], c_void_p),
+    "dh_comm_run": ([c_void_p, c_int, c_void_p, c_void_p, c_ll, c_int], c_int),
     "dh_nccl_unique_id": ([c_void_p], c_int),
     "dh_model_create": ([c_void_p, ctypes.POINTER(ModelCfg), ctypes.POINTER(c_void_p)], c_int),
     "dh_model_destroy": ([c_void_p], c_int),
@@ -57,6 +60,7 @@ _SIGS = {
     "dh_lower_json": ([ctypes.POINTER(ModelCfg), c_int, c_int, c_char_p, c_char_p, c_int,
                        ctypes.POINTER(c_void_p)], c_int),
     "dh_model_probe_read": ([c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int)], c_int),
+    "dh_model_probe_read_node": ([c_void_p, c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int)], c_int),
 }
 _bound = False
 
@@ -110,6 +114,16 @@ class Context:
         return cls(h, tp_rank, tp_size)
 
     @classmethod
+    def create_pp(cls, device=0, pp_rank=0, pp_size=2, pp_id: bytes | None = None, tp_rank=0, tp_size=1,
+                  tp_id: bytes | None = None, nccl_max_ctas=0):
+        """One W-pipeline stage on `device`: stage transfers over NCCL (dh_ctx_create_pp)."""
+        h = c_void_p()
+        buf = lambda b: ctypes.create_string_buffer(b, 128) if b else None  # noqa: E731
+        check(_lib().dh_ctx_create_pp(device, tp_rank, tp_size, buf(tp_id), pp_rank, pp_size, buf(pp_id),
+                                      nccl_max_ctas, ctypes.byref(h)))
+        return cls(h, tp_rank, tp_size)
+
+    @classmethod
     def loopback_pp_group(cls, device=0, pp_size=2):
         """pp_size pipeline-stage contexts on one device (staged-copy transfers)."""
         arr = (c_void_p * pp_size)()
@@ -129,6 +143,13 @@ class Context:
         h = c_void_p()
         check(_lib().dh_ctx_create_emulated(device, tp_size, comm_ctas, link_gbs, ctypes.byref(h)))
         return cls(h, 0, tp_size)
+
+    COMM_OPS = {"all_gather": 0, "reduce_scatter": 1, "all_reduce_f32": 2, "all_to_all": 3}
+
+    def collective(self, op: str, send, recv, count: int, lane: int = 1):
+        """Enqueue one collective of this context's group (dh_comm_run) on a lane
+        stream; `send` / `recv` are CUDA tensors (bf16, fp32 for all_reduce_f32)."""
+        check(_lib().dh_comm_run(self.handle, self.COMM_OPS[op], send.data_ptr(), recv.data_ptr(), count, lane))
 
     def stream_ptr(self, lane=0) -> int:
         return _lib().dh_ctx_stream(self.handle, lane)
@@ -262,15 +283,16 @@ class Model:
         return json.loads(_take_string(p))
 
     def probe(self, node: int):
-        """Time every launch of template node `node` (-1 disables)."""
+        """Also time every launch of template node `node` (-1 clears all probes)."""
         check(_lib().dh_model_probe(self.handle, node))
 
     def set_skip_comm(self, skip: bool):
         check(_lib().dh_model_set_skip_comm(self.handle, int(skip)))
 
-    def probe_read(self):
+    def probe_read(self, node: int = -1):
+        """(summed ms, launches) of probed node `node` (-1: the first probed)."""
         ms, n = ctypes.c_double(), c_int()
-        check(_lib().dh_model_probe_read(self.handle, ctypes.byref(ms), ctypes.byref(n)))
+        check(_lib().dh_model_probe_read_node(self.handle, node, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
 
     def profile(self, iters=10) -> str:

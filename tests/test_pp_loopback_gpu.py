@@ -91,3 +91,97 @@ def test_w_pipeline_stages_equal_single_stage(p, layers, mb):
     assert seen == set(want)
     for ctx in ctxs:
         ctx.close()
+
+
+# ---------------------------------------------------------------------------
+# Helpers shared with the two-GPU NCCL stage test (tests/test_nccl_multi_gpu.py):
+# the stage's weights and inputs are rebuilt from the same seeds in each
+# process, so no tensors cross process boundaries.
+LAYERS, MB, P = 4, 4, 2
+
+
+def _pp_shape():
+    return _tiny(mb=MB, layers=LAYERS)
+
+
+def stage_plan():
+    return planner.lib().search_si_plan(_pp_shape().planner_model(), {"tp": 1}, B200,
+                                        {"archetype": "nvlink_h100"})["plan_json"]
+
+
+def reference_single_stage(plan):
+    """The whole stack on one device (sequential SI program): numpy results."""
+    shape = _pp_shape()
+    ctx = Context.create(0)
+    _, ref, _, _ = _build(shape, ctx)
+    ref.set_plan(plan, mode="sequential")
+    ref.zero_grads()
+    ref.run_program(use_graph=True)
+    ref.sync()
+    want = {"loss": ref.tensor("loss").cpu().numpy().copy(), "dx": ref.tensor("dx").float().cpu().numpy().copy()}
+    for g in range(LAYERS):
+        for n in NAMES:
+            want[f"{g}.{n}"] = ref.tensor("grad." + n, g).cpu().numpy().copy()
+    ref.close()
+    ctx.close()
+    return want
+
+
+def run_stage(ctx, d, p, plan, layers):
+    """Stage d of a p-stage W pipeline on `ctx` (weights of its U-fold layers,
+    the inputs on stage 0); returns its gradients (and loss / dx on stage 0)."""
+    import numpy as np
+
+    from oracle.layer_oracle import LlamaTPOracle, bf16_round
+    from paper_2411_15871_b200.runtime import LlamaShape, Model
+    from tests.test_model_gpu import _upload
+    shape = _pp_shape()
+    orc = LlamaTPOracle(shape.hidden, shape.ffn, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.layers,
+                        shape.seq_len, tp=1, theta=shape.rope_theta, bf16=True, seed=5, init_std=0.05)
+    fold = _fold(layers, p)
+    c = layers // (2 * p)
+    st = LlamaShape(**{**shape.__dict__, "layers": 2 * c, "split_layer": c if d + 1 < p else 0,
+                       "pp_rank": d, "pp_size": p, "slots": MB * 2 * c + 1})
+    m = Model(ctx, st)
+    for local, g in enumerate(fold[d]):
+        sh = orc.shard(g, 0)
+        for n in NAMES:
+            _upload(m.tensor("w." + n, local), sh[n])
+            _upload(m.tensor("master." + n, local), sh[n])
+    rng = np.random.default_rng(11)  # tests.test_model_gpu._build's input stream
+    for s in range(MB):
+        x = bf16_round(rng.standard_normal((shape.seq_len, shape.hidden)).astype(np.float32))
+        r = bf16_round(rng.standard_normal((shape.seq_len, shape.hidden)).astype(np.float32))
+        if d == 0:
+            _upload(m.tensor("x_in", strand=s), x)
+            _upload(m.tensor("dy", strand=s), r)
+    torch.cuda.synchronize()
+    m.set_plan(plan, mode="w_pipeline")
+    m.zero_grads()
+    m.run_program(use_graph=False)
+    m.sync()
+    got = {f"{g}.{n}": m.tensor("grad." + n, local).cpu().numpy().copy() for local, g in enumerate(fold[d])
+           for n in NAMES}
+    if d == 0:
+        got["loss"] = m.tensor("loss").cpu().numpy().copy()
+        got["dx"] = m.tensor("dx").float().cpu().numpy().copy()
+    m.close()
+    return got
+
+
+def test_w_pipeline_helpers_loopback():
+    """run_stage over the loopback stage group equals the single-stage stack
+    (the same helpers the two-GPU NCCL test runs one per process)."""
+    import numpy as np
+    plan = stage_plan()
+    want = reference_single_stage(plan)
+    ctxs = Context.loopback_pp_group(0, P)
+    outs = _run_ranks(lambda d: (torch.cuda.set_device(0), run_stage(ctxs[d], d, P, plan, LAYERS))[1], P)
+    got = {}
+    for o in outs:
+        got.update(o)
+    assert set(got) == set(want)
+    for k, v in want.items():
+        assert np.array_equal(got[k], v), k
+    for c in ctxs:
+        c.close()
