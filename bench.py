@@ -443,7 +443,21 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
             r = planner.lib().estimate(shape.planner_model(), par, B200_CLUSTER, prof, source=src,
                                        microbatches=shape.micro_batches, caps=caps)
             est[src] = {"ms": round(r["makespan_us"] / 1e3, 3), "hidden_comm_frac": round(r["hidden_comm_frac"], 4)}
-        model_vs_measured = {"modeled_no_optimizer": est,
+        # the reference's comparison report (compare_report, report.cpp:179-223)
+        # on a scenario whose profile is this run's measured table
+        prof_path = os.path.join(ROOT, "gpurun_out", f"b200_profile_tp{tp}_emulated.json")
+        try:
+            rep = planner.lib().compare({"name": f"b200-{'ep' if shape.moe else 'tp'}{tp}-measured",
+                                         "model": shape.planner_model(), "cluster": B200_CLUSTER,
+                                         "parallelism": par, "microbatches": shape.micro_batches,
+                                         "profile": {"path": prof_path}, "caps": WIDE_CAPS,
+                                         "parallel_search": True})
+            compare = {"config_hash": rep["config_hash"],
+                       "rows": [{k: r[k] for k in ("plan_source", "makespan_us", "speedup", "hidden_comm_frac",
+                                                   "peak_bytes", "bubble_ratio")} for r in rep["report"]["rows"]]}
+        except Exception as e:  # noqa: BLE001
+            compare = {"error": str(e)[:200]}
+        model_vs_measured = {"compare_report": compare, "modeled_no_optimizer": est,
                              "measured_ms": {"sequential": round(res["sequential"], 3), "si": round(res[best], 3)},
                              "how": "estimate_iteration_time(W for wavelet_rr/dhelix, 1F1B for megatron; p=1) "
                                     "fed with this run's measured profile"}

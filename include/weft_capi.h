@@ -16,6 +16,9 @@
  *   weft_memory_json         <- simulate_memory, max_model_size, default footprints
  *                               (memory_sim.hpp:47-79)
  *   weft_estimate_json       <- estimate_iteration_time (estimate.hpp:45-50)
+ *   weft_compare_json        <- parse_scenario + compare_report + report_to_json/csv
+ *                               (report.hpp:42-66)
+ *   weft_comm_volume_json    <- comm_volume_estimate (comm_volume.hpp:26-29)
  *
  * Every call returns a weft status (0 ok; 2 ConfigError, 3 InfeasibleError,
  * 4 MissingProfileEntry — the reference CLI's exit codes, weft_main.cpp:20-23;
@@ -45,6 +48,8 @@ int weft_templates_json(const char* request, char** out);  /* builtin_template_j
 int weft_pipeline_json(const char* request, char** out);
 int weft_memory_json(const char* request, char** out);
 int weft_estimate_json(const char* request, char** out);
+int weft_compare_json(const char* request, char** out);
+int weft_comm_volume_json(const char* request, char** out);
 const char* weft_last_error(void);
 void weft_free(char* p);
 

@@ -20,6 +20,8 @@
 //   memory:       {act_bytes_per_layer, state_bytes_per_layer, capacity_bytes,
 //                  slack_bytes, layers} or {"defaults": true}      (memory_json)
 //   source, microbatches, intra_batch_tp_hidden_frac              (estimate_json)
+//   scenario:     a scenario document (parse_scenario schema)      (compare_json)
+//   tokens, microbatches                                          (comm_volume_json)
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -33,6 +35,8 @@
 #include "weft/overlap_profile.hpp"
 #include "weft/pairing_search.hpp"
 #include "weft/presets.hpp"
+#include "weft/comm_volume.hpp"
+#include "weft/report.hpp"
 
 #ifdef WEFT_CAPI_REF
 #define WEFT_API(name) weft_ref_##name
@@ -395,5 +399,29 @@ extern "C" int WEFT_API(estimate_json)(const char* request, char** out) {
                     {"mfu", r.mfu},                   {"hidden_comm_frac", r.hidden_comm_frac},
                     {"layer_fwd_us", r.layer_fwd_us}, {"layer_bwd_us", r.layer_bwd_us},
                     {"layer_pair_us", r.layer_pair_us}};
+    });
+}
+
+// compare_report on a scenario document (reference report.hpp:56-63)
+extern "C" int WEFT_API(compare_json)(const char* request, char** out) {
+    return guarded(request, out, [](const json& req) {
+        const weft::Scenario sc = weft::parse_scenario(req.at("scenario").dump());
+        const weft::CompareReport rep = weft::compare_report(sc);
+        return json{{"report_json", weft::report_to_json(rep)},
+                    {"report_csv", weft::report_to_csv(rep)},
+                    {"config_hash", rep.config_hash},
+                    {"canonical_json", sc.canonical_json()}};
+    });
+}
+
+// comm_volume_estimate (reference comm_volume.hpp:26-29)
+extern "C" int WEFT_API(comm_volume_json)(const char* request, char** out) {
+    return guarded(request, out, [](const json& req) {
+        const auto v = weft::comm_volume_estimate(
+            model_from(req.at("model")), cluster_from(req.at("cluster")),
+            par_from(req.value("parallelism", json::object())), req.at("tokens").get<std::int64_t>(),
+            req.value("microbatches", 1));
+        return json{{"local_bytes", v.local_bytes}, {"cross_bytes", v.cross_bytes}, {"local_us", v.local_us},
+                    {"cross_us", v.cross_us}, {"cross_time_ratio", v.cross_time_ratio}};
     });
 }

@@ -144,6 +144,17 @@ class PlannerLib:
             req["caps"] = caps
         return self.call("estimate_json", req)
 
+    def compare(self, scenario: dict):
+        """compare_report on a scenario document (report.hpp): one row per plan source."""
+        r = self.call("compare_json", {"scenario": scenario})
+        r["report"] = json.loads(r["report_json"])
+        return r
+
+    def comm_volume(self, model, parallelism, cluster, tokens, microbatches=1):
+        """comm_volume_estimate (comm_volume.hpp)."""
+        return self.call("comm_volume_json", {"model": model, "parallelism": parallelism, "cluster": cluster,
+                                              "tokens": tokens, "microbatches": microbatches})
+
 
 _default: PlannerLib | None = None
 

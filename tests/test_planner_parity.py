@@ -177,14 +177,14 @@ def test_error_mapping():
 
 def test_reference_catch_suites_against_our_library():
     """The reference's own tests (proj/tests/test_{op_model,overlap_profile,
-    pairing_search,folding_pipeline,memory_sim}.cpp), compiled unmodified
-    against our planner."""
+    pairing_search,folding_pipeline,memory_sim,runner}.cpp), compiled
+    unmodified against our planner: all 88 cases, as against the reference."""
     exe = os.path.join(ROOT, "oracle", "_ref", "ours_suite")
     if not os.path.exists(exe):
         pytest.skip("oracle/_ref/ours_suite not built")
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "cases=75 passed=75 failed=0" in out.stdout
+    assert "cases=88 passed=88 failed=0" in out.stdout
 
 
 def test_reference_catch_suites_against_reference():
@@ -198,3 +198,48 @@ def test_reference_catch_suites_against_reference():
 def test_shipped_template_file_matches_builtin():
     with open(os.path.join(ROOT, "data", "dag_templates.json")) as f:
         assert json.loads(f.read()) == json.loads(lib().builtin_template_json())
+
+
+SCENARIOS = [
+    {"name": "llama25b-a40", "model": "llama-25B", "cluster": "a40_64",
+     "parallelism": {"dp": 4, "tp": 8, "pp": 2, "sp": True}, "microbatches": 8,
+     "profile": {"archetype": "pcie_a40"}, "caps": {"sequences": 8, "segments": 5, "candidates": 512}, "seed": 7},
+    {"name": "c2-b200", "model": {"name": "llama3-8b", "family": "llama", "hidden": 4096, "intermediate": 14336,
+                                  "layers": 32, "seq_len": 4096},
+     "cluster": B200_CLUSTER, "parallelism": {"tp": 8, "sp": True}, "microbatches": 8,
+     "profile": {"archetype": "nvlink_h100"}, "barrier_cost_us": 2.5, "parallel_search": True,
+     "memory": {"capacity_bytes": 180 * 2 ** 30}},
+    {"name": "c5-pp2", "model": {"name": "llama2-70b", "family": "llama", "hidden": 8192, "intermediate": 28672,
+                                 "layers": 80, "seq_len": 8192},
+     "cluster": B200_CLUSTER, "parallelism": {"tp": 4, "pp": 2, "sp": True}, "microbatches": 6,
+     "profile": {"archetype": "nvlink_a800"}, "caps": {"sequences": 4, "segments": 4, "candidates": 256}},
+    {"name": "phi-ep", "model": "phi-42B", "cluster": "a40_64", "parallelism": {"dp": 16, "pp": 4, "ep": 8},
+     "microbatches": 8, "profile": {"archetype": "nvlink_h100"}, "caps": {"sequences": 4, "segments": 4, "candidates": 128}},
+]
+
+
+@pytest.mark.parametrize("sc", SCENARIOS, ids=[s["name"] for s in SCENARIOS])
+def test_compare_report_byte_identical_to_reference(sc, ref):
+    """compare_report (reference report.cpp:179-223): JSON and CSV reports and
+    the config hash are byte-identical to the reference's on the same scenario."""
+    a, b = lib().compare(sc), ref.compare(sc)
+    assert a["config_hash"] == b["config_hash"]
+    assert a["report_json"] == b["report_json"]
+    assert a["report_csv"] == b["report_csv"]
+    assert [r["plan_source"] for r in a["report"]["rows"]] == ["megatron_baseline", "intra_batch", "wavelet_rr",
+                                                               "dhelix"]
+
+
+def test_compare_report_schema_errors():
+    with pytest.raises(ConfigError, match="typo_field"):
+        lib().compare({**SCENARIOS[0], "typo_field": 1})
+
+
+@pytest.mark.parametrize("par", [{"tp": 8, "sp": True}, {"tp": 4, "dp": 2, "sp": True}, {"tp": 2, "cp": 2, "dp": 2},
+                                 {"dp": 8}, {"tp": 1, "ep": 8, "dp": 8}])
+def test_comm_volume_equals_reference(par, ref):
+    model = {"name": "phi", "family": "phi_moe", "hidden": 4096, "intermediate": 6400, "layers": 32,
+             "seq_len": 3072, "experts": 16, "topk": 2} if par.get("ep", 1) > 1 else CONFIGS["c2_llama3_8b_tp8"][0]
+    a = lib().comm_volume(model, par, B200_CLUSTER, 4096, 8)
+    b = ref.comm_volume(model, par, B200_CLUSTER, 4096, 8)
+    assert a == b
