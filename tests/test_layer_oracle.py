@@ -158,3 +158,54 @@ def test_moe_oracle_backward_matches_autograd(capacity):
     for k in tg[0]:
         err = np.abs(grads[0][k] - tg[0][k]).max() / max(1e-12, np.abs(tg[0][k]).max())
         assert err < 2e-3, (k, err)
+
+
+# --------------------------------------------------------------------------- pinned to transformers' Llama
+
+def _hf_golden():
+    import importlib.util
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("make_hf_llama_golden",
+                                                  os.path.join(root, "tests", "golden", "make_hf_llama_golden.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod, np.load(os.path.join(root, "tests", "golden", "hf_llama_layers.npz"))
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("case", ["tiny_d64", "gqa_d128"])
+def test_oracle_matches_transformers_llama_golden(case):
+    """The layer oracle (fp32, bf16 rounding off) against golden vectors from
+    HuggingFace transformers' LlamaDecoderLayer in fp64 (committed fixture,
+    tests/golden/make_hf_llama_golden.py): output, input gradient, and every
+    weight gradient's norm and 64 random projections. Tolerance 2e-5 relative
+    (fp32 vs fp64 arithmetic)."""
+    gen, gold = _hf_golden()
+    c = gen.CASES[case]
+    orc = gen.oracle_for(c)
+    x, r = gen.inputs_for(c)
+    _, y, dx, grads = orc.run(x, r)
+    flat = {f"{l}.{k}": g for l, gl in enumerate(grads) for k, g in gl.items()}
+    mine = gen.summarise(y, dx, flat, c["seed"])
+    assert _rel(mine["y"], gold[f"{case}/y"]) < 2e-5
+    assert _rel(mine["dx"], gold[f"{case}/dx"]) < 2e-5
+    for k in flat:
+        assert _rel(mine[f"g.{k}.norm"], gold[f"{case}/g.{k}.norm"]) < 2e-5, k
+        assert _rel(mine[f"g.{k}.proj"], gold[f"{case}/g.{k}.proj"]) < 2e-5, k
+
+
+def test_transformers_llama_live_matches_fixture():
+    """Regenerate the HF vectors live (when transformers is importable) and
+    compare them to the committed fixture: the fixture is what the script makes."""
+    pytest.importorskip("transformers")
+    gen, gold = _hf_golden()
+    c = gen.CASES["tiny_d64"]
+    y, dx, grads = gen.hf_run(c)
+    live = gen.summarise(y, dx, grads, c["seed"])
+    for k, v in live.items():
+        assert _rel(v, gold[f"tiny_d64/{k}"]) < 1e-6, k
