@@ -374,7 +374,8 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
     prof = json.loads(m.profile(iters=5))
     prof_s = time.perf_counter() - t0
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"b200_profile_tp{tp}_emulated.json"), "w") as f:
+    tag = f"{'ep' if shape.moe else 'tp'}{tp}_h{shape.hidden}"
+    with open(os.path.join(ROOT, "gpurun_out", f"b200_profile_{tag}_emulated.json"), "w") as f:
         json.dump(prof, f, indent=1)
     par = {"tp": 1, "ep": tp, "dp": tp} if shape.moe else {"tp": tp, "sp": True}
     srch = planner.lib().search_si_plan(shape.planner_model(), par, B200_CLUSTER, prof)
@@ -445,7 +446,7 @@ def emulated_tp_experiment(args, tp, timed_factory, full=True, base_shape=None, 
             est[src] = {"ms": round(r["makespan_us"] / 1e3, 3), "hidden_comm_frac": round(r["hidden_comm_frac"], 4)}
         # the reference's comparison report (compare_report, report.cpp:179-223)
         # on a scenario whose profile is this run's measured table
-        prof_path = os.path.join(ROOT, "gpurun_out", f"b200_profile_tp{tp}_emulated.json")
+        prof_path = os.path.join(ROOT, "gpurun_out", f"b200_profile_{tag}_emulated.json")
         try:
             rep = planner.lib().compare({"name": f"b200-{'ep' if shape.moe else 'tp'}{tp}-measured",
                                          "model": shape.planner_model(), "cluster": B200_CLUSTER,
@@ -614,8 +615,6 @@ def main():
     from paper_2411_15871_b200 import planner
     from paper_2411_15871_b200.runtime import LLAMA3_8B, Context, Model, nccl_unique_id
 
-    if os.environ.get("DH_BENCH_SHARE_DEVICE"):  # experiment: every rank on device 0
-        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -104,7 +104,26 @@ int time_gated(Model& m, const Op& a, const Op* b, int iters, double* us) {
     return DH_OK;
 }
 
-int time_solo(Model& m, const Op& o, int iters, double* us) { return time_gated(m, o, nullptr, iters, us); }
+int time_solo_gated(Model& m, const Op& o, int iters, double* us) { return time_gated(m, o, nullptr, iters, us); }
+
+// Back-to-back launches on the op's lane: the duration an op takes inside a
+// stream of work (what the plan's duration model needs), as opposed to the
+// gated single launch (what Eq. 1 compares a gated pair against).
+int time_solo_stream(Model& m, const Op& o, int iters, double* us) {
+    cudaStream_t s = m.ctx->lane[o.lane];
+    Timer t;
+    if (m.ctx->comm) RT_TRY(m.ctx->comm->barrier(s));
+    for (int i = 0; i < 2; ++i) RT_TRY(launch_node(m, o, s));
+    if (m.ctx->comm) RT_TRY(m.ctx->comm->barrier(s));
+    RT_CUDA(cudaEventRecord(t.a, s));
+    for (int i = 0; i < iters; ++i) RT_TRY(launch_node(m, o, s));
+    RT_CUDA(cudaEventRecord(t.b, s));
+    RT_CUDA(cudaEventSynchronize(t.b));
+    float ms = 0.f;
+    RT_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    *us = 1e3 * ms / iters;
+    return DH_OK;
+}
 
 int time_pair(Model& m, const Op& a, const Op& b, int iters, double* us) { return time_gated(m, a, &b, iters, us); }
 
@@ -125,11 +144,12 @@ int profile_model(Model& m, int iters, std::string* out_json) {
     for (auto* table : {&fwd_nodes, &bwd_nodes}) {
         const bool fwd = table == &fwd_nodes;
         for (const auto& [id, n] : *table) {
-            double us = 0.0;
-            RT_TRY(time_solo(m, node_op(m, *n, fwd), iters, &us));
+            double us = 0.0, ug = 0.0;
+            RT_TRY(time_solo_stream(m, node_op(m, *n, fwd), iters, &us));
+            RT_TRY(time_solo_gated(m, node_op(m, *n, fwd), iters, &ug));
             // event-timer floor: a sub-microsecond node can read as 0, which Eq. 1 rejects
             us = std::max(us, 1e-3);
-            solo[id] = us;
+            solo[id] = std::max(ug, 1e-3);
             try {
                 prof.solo.set(n->cls, n->name, std::max(us, 1e-3));
             } catch (const std::exception& e) {
