@@ -1,5 +1,7 @@
-// Causal GQA flash attention on tcgen05 / TMEM / TMA (head_dim 128) — the
-// attn node (forward). Replaces the mma.sync path of attention.cu for D=128.
+// Causal GQA flash attention on tcgen05 / TMEM / TMA (head_dim 64 or 128) —
+// the attn node (forward) and attn_bwd (backward). Every kernel is a template
+// on the head dimension D: a 128-row tile of D columns is D/64 swizzle atoms
+// ("d-halves") of 64 bf16 each, so D = 64 is one atom and D = 128 two.
 //
 // One CTA per work item = (pair of 128-query tiles of one q head[, KV chunk]);
 // KV blocks of 128 keys, causal blocks only, items dispatched heaviest first
@@ -49,12 +51,13 @@ extern "C" int dh_attn_trace_read(long long* out, int n) {
 namespace dh {
 namespace {
 
-constexpr int D = 128;
 constexpr int BQ = 128;
 constexpr int BKV = 128;
 constexpr int kThreads = 320;
-constexpr int kTile = BQ * D * 2;       // 32 KB: [2 d-halves][128 rows][128 B]
-constexpr int kHalf = kTile / 2;        // 16 KB
+// a 128-row tile: [D/64 d-halves][128 rows][128 B] (32 KB at D = 128)
+template <int D>
+constexpr int tile_bytes() { return BQ * D * 2; }
+constexpr int kHalf = BQ * 64 * 2;      // 16 KB: one d-half of a 128-row tile
 constexpr int kRing = 5;                // K/V tiles in flight: ring index 2j = K_j, 2j+1 = V_j
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
@@ -62,14 +65,16 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units
 #define DH_ATTN_POLY 1
 #endif
 
+template <int D>
 struct FwdSmem {
+    static constexpr int kTile = tile_bytes<D>();
     // offsets from the 1024-aligned base
     static constexpr int q = 0;                  // two query tiles
     static constexpr int kv = q + 2 * kTile;     // kRing slots
     static constexpr int bars = kv + kRing * kTile;
     static constexpr int total = bars + 256 + 1024;
 };
-static_assert(FwdSmem::total <= 232448, "forward smem exceeds the sm_100 limit");
+static_assert(FwdSmem<128>::total <= 232448, "forward smem exceeds the sm_100 limit");
 
 struct FwdParams {
     float* lse;
@@ -119,10 +124,13 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int kk) {
     return umma_desc_sw128(base + kk * 2048, kHalf, 1024);
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
                        const __grid_constant__ FwdSched sched) {
+    using FwdSmem = dh::FwdSmem<D>;
+    constexpr int kTile = FwdSmem::kTile;
     extern __shared__ uint8_t smem_raw[];
     // offset arithmetic on the __shared__ array keeps the pointer in the shared
     // space (plain loads compile to LDS rather than generic LD)
@@ -184,8 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(q_full, 2 * kTile);
             for (int t = 0; t < 2; ++t) {
                 uint8_t* qd = sm + FwdSmem::q + t * kTile;
-                tma_load_2d(qd, &tm_q, q_full, h * D, (2 * qp + t) * BQ);
-                tma_load_2d(qd + kHalf, &tm_q, q_full, h * D + 64, (2 * qp + t) * BQ);
+#pragma unroll
+                for (int hh = 0; hh < D / 64; ++hh)
+                    tma_load_2d(qd + hh * kHalf, &tm_q, q_full, h * D + 64 * hh, (2 * qp + t) * BQ);
             }
             for (int idx = 0; idx < 2 * n; ++idx) {
                 const int slot = idx % kRing;
@@ -194,13 +203,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* dst = sm + FwdSmem::kv + slot * kTile;
                 const CUtensorMap* map = (idx & 1) ? &tm_v : &tm_k;
                 const int row = (kv0 + (idx >> 1)) * BKV;
-                tma_load_2d(dst, map, &kv_full[slot], kvh * D, row);
-                tma_load_2d(dst + kHalf, map, &kv_full[slot], kvh * D + 64, row);
+#pragma unroll
+                for (int hh = 0; hh < D / 64; ++hh)
+                    tma_load_2d(dst + hh * kHalf, map, &kv_full[slot], kvh * D + 64 * hh, row);
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);
-        constexpr uint32_t id_o = umma_idesc_bf16(128, 128, false, true);
+        constexpr uint32_t id_o = umma_idesc_bf16(128, D, false, true);
         const uint32_t q_addr = smem_u32(sm + FwdSmem::q);
         const uint32_t kv_addr = smem_u32(sm + FwdSmem::kv);
         auto wait_kv = [&](int idx) {
@@ -412,12 +422,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // order, so the result is deterministic. Block = (query block, head, 16-column
 // slice of d); thread = (row, 8 columns): partial loads are coalesced along
 // rows ([d][row] layout). Query blocks from `chunk` on belong to split pairs.
-constexpr int kCombineSlices = D / 16;
+template <int D>
+constexpr int combine_slices() { return D / 16; }
 // MAXC >= the row's chunk count: every load is issued unconditionally (chunk
 // indices clamped, surplus chunks weighted 0), so a thread has all of its
 // MAXC x 8 partial loads in flight at once instead of one dependent L2 round
 // trip per chunk and column.
-template <int MAXC>
+template <int MAXC, int D>
 __global__ void __launch_bounds__(256) attn_fwd_combine_kernel(const FwdParams p) {
     const int h = blockIdx.y;
     const int qb = p.chunk + blockIdx.x;
@@ -535,17 +546,19 @@ const FwdSplit& fwd_split_plan(int T, int nq) {
 
 }  // namespace
 
-long long attn_fwd_tc_scratch_floats(int T, int nq) {
+long long attn_fwd_tc_scratch_floats(int T, int nq, int D) {
     const FwdSplit& sp = fwd_split_plan(T, nq);
     if (!sp.chunk) return 0;
     const long long nqb2 = 2LL * (((T + BKV - 1) / BKV + 1) / 2);
     return static_cast<long long>(nq) * nqb2 * sp.maxc * (BQ * D + 2 * BQ);
 }
 
-// Host launcher (dh_attn_fwd dispatches head_dim 128 here).
-int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
-                long long ldo, float* lse, int T, int nq, int nkv, float scale, float* scratch,
-                long long scratch_floats, cudaStream_t s) {
+namespace {
+
+template <int D>
+int attn_fwd_tc_d(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
+                  long long ldo, float* lse, int T, int nq, int nkv, float scale, float* scratch,
+                  long long scratch_floats, cudaStream_t s) {
     CUtensorMap mq, mk, mv;
     int rc = make_tma_2d(&mq, q, static_cast<long long>(nq) * D, T, ldq, 64, BQ);
     if (rc) return rc;
@@ -555,8 +568,8 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
     if (rc) return rc;
     static bool cfg = false;
     if (!cfg) {
-        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           FwdSmem::total));
+        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           FwdSmem<D>::total));
         cfg = true;
     }
     const int nkb = (T + BKV - 1) / BKV;
@@ -564,23 +577,36 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
     FwdParams prm{lse, static_cast<__nv_bfloat16*>(o), ldo, T, nq / nkv, scale * kLog2e, nq, nkb, npairs, 0, 1,
                   scratch};
     const FwdSplit& sp = fwd_split_plan(T, nq);
-    const bool split = sp.chunk && scratch && scratch_floats >= attn_fwd_tc_scratch_floats(T, nq);
+    const bool split = sp.chunk && scratch && scratch_floats >= attn_fwd_tc_scratch_floats(T, nq, D);
     if (split) {
         prm.chunk = sp.chunk;
         prm.maxc = sp.maxc;
     }
     const int grid = (split ? sp.items : npairs) * nq;
-    attn_fwd_tc_kernel<<<grid, kThreads, FwdSmem::total, s>>>(mq, mk, mv, prm, sp.sched);
+    attn_fwd_tc_kernel<D><<<grid, kThreads, FwdSmem<D>::total, s>>>(mq, mk, mv, prm, sp.sched);
     DH_CUDA_CHECK(cudaGetLastError());
     if (split) {
-        const dim3 cg(2 * npairs - sp.chunk, nq, kCombineSlices);
-        if (sp.maxc <= 2) attn_fwd_combine_kernel<2><<<cg, 256, 0, s>>>(prm);
-        else if (sp.maxc <= 4) attn_fwd_combine_kernel<4><<<cg, 256, 0, s>>>(prm);
-        else if (sp.maxc <= 8) attn_fwd_combine_kernel<8><<<cg, 256, 0, s>>>(prm);
-        else attn_fwd_combine_kernel<16><<<cg, 256, 0, s>>>(prm);
+        const dim3 cg(2 * npairs - sp.chunk, nq, combine_slices<D>());
+        if (sp.maxc <= 2) attn_fwd_combine_kernel<2, D><<<cg, 256, 0, s>>>(prm);
+        else if (sp.maxc <= 4) attn_fwd_combine_kernel<4, D><<<cg, 256, 0, s>>>(prm);
+        else if (sp.maxc <= 8) attn_fwd_combine_kernel<8, D><<<cg, 256, 0, s>>>(prm);
+        else attn_fwd_combine_kernel<16, D><<<cg, 256, 0, s>>>(prm);
         DH_CUDA_CHECK(cudaGetLastError());
     }
     return DH_OK;
+}
+
+}  // namespace
+
+// Host launcher (dh_attn_fwd dispatches here for head_dim 64 and 128).
+int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
+                long long ldo, float* lse, int T, int nq, int nkv, int D, float scale, float* scratch,
+                long long scratch_floats, cudaStream_t s) {
+    if (D == 128)
+        return attn_fwd_tc_d<128>(q, k, v, ldq, ldkv, o, ldo, lse, T, nq, nkv, scale, scratch, scratch_floats, s);
+    if (D == 64)
+        return attn_fwd_tc_d<64>(q, k, v, ldq, ldkv, o, ldo, lse, T, nq, nkv, scale, scratch, scratch_floats, s);
+    return set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }
 
 }  // namespace dh
@@ -611,28 +637,32 @@ namespace dh {
 namespace {
 
 constexpr int BT64 = 64;
-constexpr int kTile64 = BT64 * D * 2;  // 16 KB: [2 d-halves][64 rows][128 B]
-constexpr int kHalf64 = kTile64 / 2;   // 8 KB
-constexpr int kStages = 4;             // Q/dO (dK/dV items) or K/V (dQ items) ring
+constexpr int kHalf64 = BT64 * 64 * 2;  // 8 KB: one d-half of a 64-row tile
+constexpr int kStages = 4;              // Q/dO (dK/dV items) or K/V (dQ items) ring
 
+template <int D>
 struct KvSmem {
-    static constexpr int k = 0;                          // 32 KB
-    static constexpr int v = k + kTile;                  // 32 KB
-    static constexpr int q = v + kTile;                  // kStages x 16 KB
-    static constexpr int dout = q + kStages * kTile64;   // kStages x 16 KB
+    static constexpr int kTile = tile_bytes<D>();        // 128-row K / V tile
+    static constexpr int kTile64 = BT64 * D * 2;         // 64-row tile: [D/64 d-halves][64 rows][128 B]
+    static constexpr int k = 0;
+    static constexpr int v = k + kTile;
+    static constexpr int q = v + kTile;                  // kStages 64-row tiles
+    static constexpr int dout = q + kStages * kTile64;   // kStages 64-row tiles
     static constexpr int vec = dout + kStages * kTile64; // per stage: lse[64], D[64] (raw)
     static constexpr int bars = vec + kStages * 128 * 4;
     static constexpr int total = bars + 256 + 1024;
 };
 
 constexpr int kDqStages = 6;  // K/V ring of the dQ items (Q and dO live in TMEM)
+template <int D>
 struct DqSmem {
-    static constexpr int k = 0;                          // kDqStages x 16 KB
-    static constexpr int v = k + kDqStages * kTile64;    // kDqStages x 16 KB
+    static constexpr int kTile64 = BT64 * D * 2;
+    static constexpr int k = 0;                          // kDqStages 64-row tiles
+    static constexpr int v = k + kDqStages * kTile64;    // kDqStages 64-row tiles
     static constexpr int bars = v + kDqStages * kTile64;
     static constexpr int total = bars + 256 + 1024;
 };
-static_assert(KvSmem::total <= 232448 && DqSmem::total <= 232448, "backward smem exceeds the sm_100 limit");
+static_assert(KvSmem<128>::total <= 232448 && DqSmem<128>::total <= 232448, "backward smem exceeds the sm_100 limit");
 
 struct BwdParams {
     const __nv_bfloat16* q;     // raw rows for the TMEM-resident Q / dO of the dQ items
@@ -661,9 +691,12 @@ __device__ __forceinline__ uint64_t desc_mn64(uint32_t base, int kk) {
 
 constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
 
+template <int D>
 __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                    const CUtensorMap& tm_q, const CUtensorMap& tm_do,
                                                    const BwdParams& p, const int kb, const int h) {
+    using KvSmem = dh::KvSmem<D>;
+    constexpr int kTile = KvSmem::kTile, kTile64 = KvSmem::kTile64;
     extern __shared__ uint8_t smem_raw[];
     // offset arithmetic on the __shared__ array keeps the pointer in the shared
     // space (plain loads compile to LDS rather than generic LD)
@@ -680,7 +713,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
 
     const int kvh = h / p.group;
     const int nq64 = (p.T + BT64 - 1) / BT64;
-    const int i0 = (kb * D) / BT64;  // first q tile with a query >= the block's first key
+    const int i0 = (kb * BKV) / BT64;  // first q tile with a query >= the block's first key
     const int n_it = nq64 - i0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -710,10 +743,11 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
     if (warp == 0) {
         if (lane == 0) {
             mbar_expect_tx(kv_full, 2 * kTile);
-            tma_load_2d(sm + KvSmem::k, &tm_k, kv_full, kvh * D, kb * D);
-            tma_load_2d(sm + KvSmem::k + kHalf, &tm_k, kv_full, kvh * D + 64, kb * D);
-            tma_load_2d(sm + KvSmem::v, &tm_v, kv_full, kvh * D, kb * D);
-            tma_load_2d(sm + KvSmem::v + kHalf, &tm_v, kv_full, kvh * D + 64, kb * D);
+#pragma unroll
+            for (int hh = 0; hh < D / 64; ++hh) {
+                tma_load_2d(sm + KvSmem::k + hh * kHalf, &tm_k, kv_full, kvh * D + 64 * hh, kb * BKV);
+                tma_load_2d(sm + KvSmem::v + hh * kHalf, &tm_v, kv_full, kvh * D + 64 * hh, kb * BKV);
+            }
             for (int it = 0; it < n_it; ++it) {
                 const int st = it % kStages, qi = i0 + it;
                 mbar_wait(&q_empty[st], ((it / kStages) & 1) ^ 1);
@@ -725,15 +759,16 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 }
                 uint8_t* qd = sm + KvSmem::q + st * kTile64;
                 uint8_t* od = sm + KvSmem::dout + st * kTile64;
-                tma_load_2d(qd, &tm_q, &q_full[st], h * D, qi * BT64);
-                tma_load_2d(qd + kHalf64, &tm_q, &q_full[st], h * D + 64, qi * BT64);
-                tma_load_2d(od, &tm_do, &q_full[st], h * D, qi * BT64);
-                tma_load_2d(od + kHalf64, &tm_do, &q_full[st], h * D + 64, qi * BT64);
+#pragma unroll
+                for (int hh = 0; hh < D / 64; ++hh) {
+                    tma_load_2d(qd + hh * kHalf64, &tm_q, &q_full[st], h * D + 64 * hh, qi * BT64);
+                    tma_load_2d(od + hh * kHalf64, &tm_do, &q_full[st], h * D + 64 * hh, qi * BT64);
+                }
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
-        constexpr uint32_t id_g = umma_idesc_bf16(128, 128, false, true);
+        constexpr uint32_t id_g = umma_idesc_bf16(128, D, false, true);
         const uint32_t k_addr = smem_u32(sm + KvSmem::k), v_addr = smem_u32(sm + KvSmem::v);
         auto issue_s = [&](int it) {
             const int qs = it % kStages, sb = it & 1;  // smem ring stage, TMEM buffer
@@ -780,10 +815,10 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;
         const int r = quad * 32 + lane;  // key row within the block
-        const int key = kb * D + r;
+        const int key = kb * BKV + r;
         const int t_sm = threadIdx.x - 64;  // 0..255 among the elementwise warps
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const int key_hi = kb * D + D - 1;
+        const int key_hi = kb * BKV + BKV - 1;
         const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), m1 = f2_pack(-1.f, -1.f);
         const uint64_t nl2e = f2_pack(-kLog2e, -kLog2e);
         for (int it = 0; it < n_it; ++it) {
@@ -852,7 +887,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         tc_fence_after();
         const bool ok = key < p.T;
 #pragma unroll 1
-        for (int c = half * 2; c < half * 2 + 2; ++c) {
+        for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
             uint32_t ka[32], va[32];
             tmem_ld32(t_dk + lane_off + c * 32, ka);
             tmem_ld32(t_dv + lane_off + c * 32, va);
@@ -896,9 +931,12 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
     }
 }
 
+template <int D>
 __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const CUtensorMap& tm_do,
                                                  const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                  const BwdParams& p, const int qb, const int h) {
+    using DqSmem = dh::DqSmem<D>;
+    constexpr int kTile64 = DqSmem::kTile64;
     extern __shared__ uint8_t smem_raw[];
     // offset arithmetic on the __shared__ array keeps the pointer in the shared
     // space (plain loads compile to LDS rather than generic LD)
@@ -913,7 +951,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
     const int kvh = h / p.group;
-    const int n_it = (qb * D + D) / BT64;  // key tiles 0 .. covering the block's last query
+    const int n_it = (qb * BQ + BQ) / BT64;  // key tiles 0 .. covering the block's last query
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -946,15 +984,16 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                 mbar_expect_tx(&kv_full[st], 2 * kTile64);
                 uint8_t* kd = sm + DqSmem::k + st * kTile64;
                 uint8_t* vd = sm + DqSmem::v + st * kTile64;
-                tma_load_2d(kd, &tm_k, &kv_full[st], kvh * D, it * BT64);
-                tma_load_2d(kd + kHalf64, &tm_k, &kv_full[st], kvh * D + 64, it * BT64);
-                tma_load_2d(vd, &tm_v, &kv_full[st], kvh * D, it * BT64);
-                tma_load_2d(vd + kHalf64, &tm_v, &kv_full[st], kvh * D + 64, it * BT64);
+#pragma unroll
+                for (int hh = 0; hh < D / 64; ++hh) {
+                    tma_load_2d(kd + hh * kHalf64, &tm_k, &kv_full[st], kvh * D + 64 * hh, it * BT64);
+                    tma_load_2d(vd + hh * kHalf64, &tm_v, &kv_full[st], kvh * D + 64 * hh, it * BT64);
+                }
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
-        constexpr uint32_t id_g = umma_idesc_bf16(128, 128, false, true);
+        constexpr uint32_t id_g = umma_idesc_bf16(128, D, false, true);
         auto issue_s = [&](int it) {
             const int ks = it % kDqStages, sb = it & 1;
             mbar_wait(&kv_full[ks], (it / kDqStages) & 1);
@@ -995,7 +1034,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;
         const int r = quad * 32 + lane;
-        const int qrow = qb * D + r;
+        const int qrow = qb * BQ + r;
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         const int qc = min(qrow, p.T - 1);
         const float lse2 = p.lse[static_cast<long long>(h) * p.T + qc] * kLog2e;
@@ -1009,7 +1048,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                                             : p.q + static_cast<long long>(qc) * p.ldq + h * D;
             const bool in = qrow < p.T;
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
+            for (int c = 0; c < D / 64; ++c) {
                 uint32_t w[32];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -1038,7 +1077,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
             if (threadIdx.x == 64) ATR(it * 8 + 5);
             named_barrier(2, 256);  // the other half's dS stores overwrite columns this half reads
             if (threadIdx.x == 64) ATR(it * 8 + 6);
-            const bool full_tile = it * BT64 + BT64 - 1 <= qb * D && it * BT64 + BT64 <= p.T && qb * D + D <= p.T;
+            const bool full_tile = it * BT64 + BT64 - 1 <= qb * BQ && it * BT64 + BT64 <= p.T && qb * BQ + BQ <= p.T;
             uint32_t pd[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
@@ -1070,7 +1109,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         const bool ok = qrow < p.T;
         __nv_bfloat16* row = p.dq + static_cast<long long>(qrow) * p.lddq + h * D;
 #pragma unroll 1
-        for (int c = half * 2; c < half * 2 + 2; ++c) {
+        for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
             uint32_t a[32];
             tmem_ld32(t_dq + lane_off + c * 32, a);
             tmem_ld_wait();
@@ -1098,6 +1137,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
 // lets the light items of one kind fill the tail of the other. With few heads
 // per GPU (high TP) two separate grids each left their longest causal block as
 // an exposed critical path.
+template <int D>
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
@@ -1107,19 +1147,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     const int rank = blockIdx.x / (2 * nq);
     const int rem = blockIdx.x % (2 * nq);
     if (rem < nq)
-        attn_bwd_dkdv_body(tm_k, tm_v, tm_q64, tm_do64, p, rank, rem);  // key block `rank` sees the most queries
+        attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q64, tm_do64, p, rank, rem);  // key block `rank` sees the most queries
     else
-        attn_bwd_dq_body(tm_q, tm_do, tm_k64, tm_v64, p, nb - 1 - rank, rem - nq);
+        attn_bwd_dq_body<D>(tm_q, tm_do, tm_k64, tm_v64, p, nb - 1 - rank, rem - nq);
 }
 
-}  // namespace
-
-// Host launcher for the tcgen05 backward (dvec must already hold
-// D_i = rowsum(dO * O)); dk_part / dv_part are used only when group > 1.
-int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
-                const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
-                float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
-                int nq, int nkv, float scale, cudaStream_t s) {
+template <int D>
+int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, long long ldkv, const void* dout,
+                  long long ldo, const float* lse, const float* dvec, float* dk_part, float* dv_part, void* dq,
+                  void* dk, void* dv, long long lddq, long long lddkv, int T, int nq, int nkv, float scale,
+                  cudaStream_t s) {
     CUtensorMap mk, mv, mq64, mdo64, mq, mdo, mk64, mv64;
     const long long qcols = static_cast<long long>(nq) * D, kvcols = static_cast<long long>(nkv) * D;
     int rc = make_tma_2d(&mk, k, kvcols, T, ldkv, 64, 128);
@@ -1131,21 +1168,38 @@ int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long
     if (!rc) rc = make_tma_2d(&mk64, k, kvcols, T, ldkv, 64, 64);
     if (!rc) rc = make_tma_2d(&mv64, v, kvcols, T, ldkv, 64, 64);
     if (rc) return rc;
-    constexpr int smem = KvSmem::total > DqSmem::total ? KvSmem::total : DqSmem::total;
+    constexpr int smem = KvSmem<D>::total > DqSmem<D>::total ? KvSmem<D>::total : DqSmem<D>::total;
     static bool cfg = false;
     if (!cfg) {
-        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
     BwdParams prm{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(dout), ldq, ldo,
                   lse, dvec, dk_part, dv_part, static_cast<__nv_bfloat16*>(dk),
                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
                   nq / nkv, scale, scale * kLog2e};
-    const int nb = (T + D - 1) / D;
-    attn_bwd_tc_kernel<<<2 * nb * nq, kThreadsBwd, smem, s>>>(mk, mv, mq64, mdo64, mq, mdo, mk64, mv64, prm, nq,
-                                                             nb);
+    const int nb = (T + BKV - 1) / BKV;
+    attn_bwd_tc_kernel<D><<<2 * nb * nq, kThreadsBwd, smem, s>>>(mk, mv, mq64, mdo64, mq, mdo, mk64, mv64, prm,
+                                                                nq, nb);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
+}
+
+}  // namespace
+
+// Host launcher for the tcgen05 backward (dvec must already hold
+// D_i = rowsum(dO * O)); dk_part / dv_part are used only when group > 1.
+int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
+                const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
+                float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
+                int nq, int nkv, int D, float scale, cudaStream_t s) {
+    if (D == 128)
+        return attn_bwd_tc_d<128>(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq,
+                                  lddkv, T, nq, nkv, scale, s);
+    if (D == 64)
+        return attn_bwd_tc_d<64>(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq,
+                                 lddkv, T, nq, nkv, scale, s);
+    return set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }
 
 }  // namespace dh

@@ -57,16 +57,12 @@ int dense_kernels(const Model& m, int node, int layer) {
         case kSendAct: case kRecvAct: case kSendGrad: case kRecvGrad:
             return 0;  // staged device copies
         case 4:  // attn (+ KV-split combine when the launcher splits rows)
-            return m.cfg.head_dim == 128 &&
-                           dh_attn_fwd_scratch_floats(m.cfg.seq, m.cfg.nq_l,
-                                                      m.cfg.nkv_l, m.cfg.head_dim) > 0
-                       ? 2
-                       : 1;
+            return dh_attn_fwd_scratch_floats(m.cfg.seq, m.cfg.nq_l, m.cfg.nkv_l, m.cfg.head_dim) > 0 ? 2 : 1;
         case 14:
             return layer == m.cfg.layers - 1 ? 3 : 1;
         case 34:
-            // dot, dK/dV + dQ (one launch for head_dim 128), [group reduce], rope
-            return (m.cfg.head_dim == 128 ? 3 : 4) + (group ? 1 : 0);
+            // dot, dK/dV + dQ (one tcgen05 launch), [group reduce], rope
+            return 3 + (group ? 1 : 0);
         default:
             return 0;  // collectives (NCCL / loopback copies) and memcpy pass-throughs
     }

@@ -53,15 +53,31 @@ Op node_op(const Model& m, const weft::OpNode& n, bool fwd) {
     return o;
 }
 
-// One measurement harness for solo and pair times (so Eq. 1 compares like with
-// like): every iteration first aligns the ranks on the device (a one-element
-// all-reduce, when the context has a communicator: a collective's time must
-// not include waiting for a late peer), then queues the op(s) behind a
-// device-side gate on lane 0 (dh_spin_ns). The start event is recorded when
-// the gate opens, so the host cost of the launches (tensor-map encoding,
-// NCCL enqueue) falls inside the gate, not between the events; both lanes are
-// released by the same event and the stop event waits for both.
+// One measurement harness for single ops and pairs (so Eq. 1 compares like
+// with like): every iteration first aligns the ranks on the device (a
+// one-element all-reduce, when the context has a communicator: a collective's
+// time must not include waiting for a late peer); both lanes are released by
+// one event and the stop event waits for both. In gated mode the op(s) are
+// also queued behind a device-side gate on lane 0 (dh_spin_ns), so the host
+// cost of the launches falls before the start event; in the ungated modes that
+// launch skew is part of the measurement, as it is in the executor.
 constexpr long long kGateNs = 150000;
+
+// DH_PROFILE_HARNESS selects how Eq. 1's inputs are measured:
+//   0  round-1 harness: pairs co-launched from the host (launch skew included),
+//      OEF against back-to-back solo times;
+//   1  gated: pairs and single ops queued behind a device-side gate, OEF
+//      against the gated single-op times;
+//   2  (default) consistent ungated: pairs and single ops launched the same way
+//      from the host (skew included in both), OEF against those single-op times.
+// The solo table the plan search reads is the back-to-back time in every mode.
+int harness_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("DH_PROFILE_HARNESS");
+        return e ? std::atoi(e) : 2;
+    }();
+    return mode;
+}
 
 int time_gated(Model& m, const Op& a, const Op* b, int iters, double* us) {
     cudaStream_t s0 = m.ctx->lane[0];
@@ -73,9 +89,10 @@ int time_gated(Model& m, const Op& a, const Op* b, int iters, double* us) {
     RT_CUDA(cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming));
     double total = 0.0;
     int rc = DH_OK;
+    const bool gated = harness_mode() == 1;
     for (int i = 0; i < iters + 1 && rc == DH_OK; ++i) {
         if (m.ctx->comm) rc = m.ctx->comm->barrier(s0);
-        if (rc == DH_OK) rc = dh_spin_ns(kGateNs, s0);
+        if (rc == DH_OK && gated) rc = dh_spin_ns(kGateNs, s0);
         if (rc != DH_OK) break;
         cudaEventRecord(t.a, s0);
         cudaEventRecord(go, s0);
@@ -149,7 +166,7 @@ int profile_model(Model& m, int iters, std::string* out_json) {
             RT_TRY(time_solo_gated(m, node_op(m, *n, fwd), iters, &ug));
             // event-timer floor: a sub-microsecond node can read as 0, which Eq. 1 rejects
             us = std::max(us, 1e-3);
-            solo[id] = std::max(ug, 1e-3);
+            solo[id] = harness_mode() == 0 ? us : std::max(ug, 1e-3);
             try {
                 prof.solo.set(n->cls, n->name, std::max(us, 1e-3));
             } catch (const std::exception& e) {
@@ -200,6 +217,7 @@ int profile_model(Model& m, int iters, std::string* out_json) {
     md["seq"] = std::to_string(m.cfg.seq);
     md["hidden"] = std::to_string(m.cfg.hidden);
     md["iters"] = std::to_string(iters);
+    md["harness"] = std::to_string(harness_mode());
     md["pairs_measured"] = std::to_string(pairs.size());
     // The Profile document plus the raw pair table; parse_profile reads only
     // solo / oef / interference / metadata, so the extra key is inert.

@@ -13,6 +13,14 @@ if which.startswith("gemm"):
     d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
     for _ in range(3):
         dh.gemm(a, b, d)
+elif which.startswith("wgrad"):
+    # mlp_fc1_wgrad's GEMM: dW[F,H] += d_gate^T ln1 (A and B MN-major, fp32 reduce-add)
+    S, H, F = 4096, 4096, 14336 if which.endswith("tp1") else 1792
+    a = torch.randn(S, F, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(S, H, device="cuda", dtype=torch.bfloat16)
+    d = torch.zeros(F, H, device="cuda", dtype=torch.float32)
+    for _ in range(3):
+        dh.gemm(a, b, d, a_mn=True, b_mn=True, accumulate=True)
 elif which.startswith("swiglu"):
     m, n, k = (4096, 14336, 4096) if which.endswith("tp1") else (4096, 1792, 4096)
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
