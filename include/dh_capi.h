@@ -112,7 +112,23 @@ long long dh_attn_fwd_scratch_floats(int tokens, int n_q_heads, int n_kv_heads, 
 int dh_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 void* o, long long ldo, float* lse, float* scratch, long long scratch_floats,
                 int tokens, int n_q_heads, int n_kv_heads, int head_dim, float scale, void* stream);
-/* dq/dk/dv written (not accumulated); `scratch` fp32 >= tokens*n_q_heads*(2*head_dim+1) floats. */
+/* Context-parallel form (the cp_kv_exchange path): `tokens` query rows at
+ * global positions [q_offset, q_offset + tokens) attend causally to
+ * `tokens_kv` key rows (q_offset a multiple of 256, q_offset + tokens <=
+ * tokens_kv). dh_attn_fwd is the case tokens_kv == tokens, q_offset == 0. */
+long long dh_attn_fwd_scratch_floats_ex(int tokens, int n_q_heads, int n_kv_heads, int head_dim, int tokens_kv,
+                                        int q_offset);
+int dh_attn_fwd_ex(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
+                   long long ldo, float* lse, float* scratch, long long scratch_floats, int tokens, int tokens_kv,
+                   int q_offset, int n_q_heads, int n_kv_heads, int head_dim, float scale, void* stream);
+/* dq/dk/dv written (not accumulated); `scratch` fp32 >= tokens*n_q_heads*(2*head_dim+1) floats
+ * (dh_attn_bwd_scratch_floats; the _ex form: dk/dv cover all tokens_kv key rows, each the
+ * gradient from this call's queries only). */
+long long dh_attn_bwd_scratch_floats(int tokens, int n_q_heads, int head_dim, int tokens_kv);
+int dh_attn_bwd_ex(const void* q, const void* k, const void* v, long long ldq, long long ldkv, const void* o,
+                   long long ldo, const float* lse, const void* dout, void* dq, void* dk, void* dv, long long lddq,
+                   long long lddkv, float* scratch, int tokens, int tokens_kv, int q_offset, int n_q_heads,
+                   int n_kv_heads, int head_dim, float scale, void* stream);
 int dh_attn_bwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 const void* o, long long ldo, const float* lse, const void* dout,
                 void* dq, void* dk, void* dv, long long lddq, long long lddkv, float* scratch,
@@ -255,6 +271,14 @@ typedef struct dh_model_cfg {
      * The context's group is then the EP group (attention runs data-parallel,
      * TP = 1) and each rank holds experts / group_size experts. */
     int experts, topk, capacity;
+    /* Context parallelism (dense only, zero = off): with context_parallel = 1
+     * the context's group is the CP group (TP = 1). Each rank holds seq_len /
+     * group_size consecutive tokens (a multiple of 256) at global positions
+     * rank * seq_len / group_size onward; cp_kv_exchange all-gathers the
+     * layer's K/V over the group before attn (and again before attn_bwd, which
+     * reduce-scatters the dK/dV partials back to their owners). Weights are
+     * replicated: their gradients are summed over the group before AdamW. */
+    int context_parallel;
 } dh_model_cfg;
 
 typedef struct dh_optim_cfg {

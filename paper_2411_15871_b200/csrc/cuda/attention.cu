@@ -99,12 +99,12 @@ __global__ void attn_bwd_group_reduce(const float* __restrict__ dk_part,
 
 int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
                 long long ldo, float* lse, int T, int nq, int nkv, int D, float scale, float* scratch,
-                long long scratch_floats, cudaStream_t s);
-long long attn_fwd_tc_scratch_floats(int T, int nq, int D);
+                long long scratch_floats, int T_kv, int q_offset, cudaStream_t s);
+long long attn_fwd_tc_scratch_floats(int T, int nq, int D, int T_kv, int q_offset);
 int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
                 float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
-                int nq, int nkv, int D, float scale, cudaStream_t s);
+                int nq, int nkv, int D, float scale, int T_kv, int q_offset, cudaStream_t s);
 
 }  // namespace dh
 
@@ -114,12 +114,12 @@ template <int D>
 int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                const void* o, long long ldo, const float* lse, const void* dout, void* dq, void* dk,
                void* dv, long long lddq, long long lddkv, float* scratch, int T, int nq, int nkv,
-               float scale, cudaStream_t s) {
+               float scale, int T_kv, int q_offset, cudaStream_t s) {
     using namespace dh;
     const int group = nq / nkv;
     float* dvec = scratch;
     float* dk_part = scratch + static_cast<long long>(nq) * T;
-    float* dv_part = dk_part + static_cast<long long>(nq) * T * D;
+    float* dv_part = dk_part + static_cast<long long>(nq) * T_kv * D;
     if (ldo % 8 || (reinterpret_cast<uintptr_t>(o) & 15) || (reinterpret_cast<uintptr_t>(dout) & 15))
         return set_error(DH_ERR_INVALID, "attn_bwd: O / dO need 16-byte aligned rows (ldo % 8 == 0)");
     attn_bwd_dot_kernel<D><<<static_cast<int>((static_cast<long long>(T) * nq * (D / 8) + 255) / 256), 256, 0, s>>>(
@@ -127,21 +127,21 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
     DH_CUDA_CHECK(cudaGetLastError());
     // tcgen05/TMEM kernel (attention_tc.cu): dK/dV items + dQ items in one launch
     const int rc = attn_bwd_tc(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq, lddkv,
-                               T, nq, nkv, D, scale, s);
+                               T, nq, nkv, D, scale, T_kv, q_offset, s);
     if (rc != DH_OK) return rc;
     if (group > 1) {  // sum the GQA group's per-head dK/dV partials in head order
         const bool vec = (reinterpret_cast<uintptr_t>(dk_part) & 15) == 0 &&
                          (reinterpret_cast<uintptr_t>(dv_part) & 15) == 0 &&
                          (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(dv) & 15) == 0 &&
                          lddkv % 8 == 0;
-        const long long total = static_cast<long long>(nkv) * T * (vec ? D / 8 : D);
+        const long long total = static_cast<long long>(nkv) * T_kv * (vec ? D / 8 : D);
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
         if (vec)
             attn_bwd_group_reduce<true><<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
-                                                               static_cast<bf16*>(dv), lddkv, T, nkv, group, D);
+                                                               static_cast<bf16*>(dv), lddkv, T_kv, nkv, group, D);
         else
             attn_bwd_group_reduce<false><<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
-                                                                static_cast<bf16*>(dv), lddkv, T, nkv, group, D);
+                                                                static_cast<bf16*>(dv), lddkv, T_kv, nkv, group, D);
         DH_CUDA_CHECK(cudaGetLastError());
     }
     return DH_OK;
@@ -149,23 +149,56 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
 
 }  // namespace
 
-extern "C" long long dh_attn_fwd_scratch_floats(int tokens, int n_q_heads, int n_kv_heads, int head_dim) {
+extern "C" long long dh_attn_fwd_scratch_floats_ex(int tokens, int n_q_heads, int n_kv_heads, int head_dim,
+                                                   int tokens_kv, int q_offset) {
     (void)n_kv_heads;
     if ((head_dim != 128 && head_dim != 64) || tokens <= 0 || n_q_heads <= 0) return 0;
-    return dh::attn_fwd_tc_scratch_floats(tokens, n_q_heads, head_dim);
+    return dh::attn_fwd_tc_scratch_floats(tokens, n_q_heads, head_dim, tokens_kv, q_offset);
+}
+
+extern "C" long long dh_attn_fwd_scratch_floats(int tokens, int n_q_heads, int n_kv_heads, int head_dim) {
+    return dh_attn_fwd_scratch_floats_ex(tokens, n_q_heads, n_kv_heads, head_dim, tokens, 0);
+}
+
+extern "C" long long dh_attn_bwd_scratch_floats(int tokens, int n_q_heads, int head_dim, int tokens_kv) {
+    return static_cast<long long>(n_q_heads) * (tokens + 2LL * tokens_kv * head_dim);
+}
+
+extern "C" int dh_attn_fwd_ex(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
+                              long long ldo, float* lse, float* scratch, long long scratch_floats, int tokens,
+                              int tokens_kv, int q_offset, int n_q_heads, int n_kv_heads, int head_dim, float scale,
+                              void* stream) {
+    if (n_kv_heads <= 0 || n_q_heads % n_kv_heads)
+        return dh::set_error(DH_ERR_INVALID, "attn: n_q_heads must be a multiple of n_kv_heads");
+    if (tokens <= 0) return DH_OK;
+    // tcgen05/TMEM kernel (attention_tc.cu) for head_dim 64 and 128
+    return dh::attn_fwd_tc(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, head_dim, scale,
+                           scratch, scratch_floats, tokens_kv, q_offset, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int dh_attn_fwd(const void* q, const void* k, const void* v, long long ldq,
                            long long ldkv, void* o, long long ldo, float* lse, float* scratch,
                            long long scratch_floats, int tokens, int n_q_heads, int n_kv_heads,
                            int head_dim, float scale, void* stream) {
+    return dh_attn_fwd_ex(q, k, v, ldq, ldkv, o, ldo, lse, scratch, scratch_floats, tokens, tokens, 0, n_q_heads,
+                          n_kv_heads, head_dim, scale, stream);
+}
+
+extern "C" int dh_attn_bwd_ex(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
+                              const void* o, long long ldo, const float* lse, const void* dout, void* dq, void* dk,
+                              void* dv, long long lddq, long long lddkv, float* scratch, int tokens, int tokens_kv,
+                              int q_offset, int n_q_heads, int n_kv_heads, int head_dim, float scale, void* stream) {
     if (n_kv_heads <= 0 || n_q_heads % n_kv_heads)
         return dh::set_error(DH_ERR_INVALID, "attn: n_q_heads must be a multiple of n_kv_heads");
     if (tokens <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
-    // tcgen05/TMEM kernel (attention_tc.cu) for head_dim 64 and 128
-    return dh::attn_fwd_tc(q, k, v, ldq, ldkv, o, ldo, lse, tokens, n_q_heads, n_kv_heads, head_dim, scale,
-                           scratch, scratch_floats, s);
+    if (head_dim == 128)
+        return launch_bwd<128>(q, k, v, ldq, ldkv, o, ldo, lse, dout, dq, dk, dv, lddq, lddkv, scratch, tokens,
+                               n_q_heads, n_kv_heads, scale, tokens_kv, q_offset, s);
+    if (head_dim == 64)
+        return launch_bwd<64>(q, k, v, ldq, ldkv, o, ldo, lse, dout, dq, dk, dv, lddq, lddkv, scratch, tokens,
+                              n_q_heads, n_kv_heads, scale, tokens_kv, q_offset, s);
+    return dh::set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }
 
 extern "C" int dh_attn_bwd(const void* q, const void* k, const void* v, long long ldq,
@@ -173,15 +206,6 @@ extern "C" int dh_attn_bwd(const void* q, const void* k, const void* v, long lon
                            const void* dout, void* dq, void* dk, void* dv, long long lddq,
                            long long lddkv, float* scratch, int tokens, int n_q_heads,
                            int n_kv_heads, int head_dim, float scale, void* stream) {
-    if (n_kv_heads <= 0 || n_q_heads % n_kv_heads)
-        return dh::set_error(DH_ERR_INVALID, "attn: n_q_heads must be a multiple of n_kv_heads");
-    if (tokens <= 0) return DH_OK;
-    auto s = static_cast<cudaStream_t>(stream);
-    if (head_dim == 128)
-        return launch_bwd<128>(q, k, v, ldq, ldkv, o, ldo, lse, dout, dq, dk, dv, lddq, lddkv, scratch,
-                               tokens, n_q_heads, n_kv_heads, scale, s);
-    if (head_dim == 64)
-        return launch_bwd<64>(q, k, v, ldq, ldkv, o, ldo, lse, dout, dq, dk, dv, lddq, lddkv, scratch,
-                              tokens, n_q_heads, n_kv_heads, scale, s);
-    return dh::set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
+    return dh_attn_bwd_ex(q, k, v, ldq, ldkv, o, ldo, lse, dout, dq, dk, dv, lddq, lddkv, scratch, tokens, tokens, 0,
+                          n_q_heads, n_kv_heads, head_dim, scale, stream);
 }

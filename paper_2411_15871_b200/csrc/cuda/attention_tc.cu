@@ -32,6 +32,7 @@
 #include <map>
 #include <mutex>
 #include <queue>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -80,15 +81,18 @@ struct FwdParams {
     float* lse;
     __nv_bfloat16* o;
     long long ldo;
-    int T;
+    int T;         // query rows (this rank's)
     int group;
     float scale_log2;
     int nq;        // q heads (item index = rank * nq + head)
-    int nkb;       // 128-key blocks (= 128-query blocks)
+    int nkb;       // 128-key blocks of the keys (T_kv)
     int npairs;    // query-tile pairs
     int chunk;     // KV blocks per chunk (even); 0 = no split
     int maxc;      // chunks of the longest row
     float* part;   // split partials: O [h][qb][c][d][row], then (m, l) [h][qb][c][row][2]
+    int T_kv;      // key rows
+    int qo;        // query offset in 128-blocks (context parallelism: the rank's first
+                   // query sits at global position qo * 128; even, so chunks stay even)
 };
 
 constexpr int kMaxItems = 1024;  // split schedule entries per head (kernel parameter)
@@ -152,16 +156,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         qp = static_cast<int>(e >> 16);
         ch = static_cast<int>(e & 0xffffu);
         kv0 = ch * p.chunk;
-        kvend = min(kv0 + p.chunk, 2 * qp + 2);
+        kvend = min(kv0 + p.chunk, p.qo + 2 * qp + 2);
     } else {
         qp = p.npairs - 1 - rank;
-        kvend = 2 * qp + 2;  // causal, BQ == BKV
+        kvend = p.qo + 2 * qp + 2;  // causal, BQ == BKV
     }
     kvend = min(kvend, p.nkb);
-    const bool split = p.chunk && 2 * qp + 2 > p.chunk;
+    const bool split = p.chunk && p.qo + 2 * qp + 2 > p.chunk;
     const int kvh = h / p.group;
-    const int n = kvend - kv0;                         // blocks of tile 1
-    const int n0 = min(kvend, 2 * qp + 1) - kv0;       // blocks of tile 0 (n or n - 1; >= 1: chunks are even)
+    const int n = kvend - kv0;                              // blocks of tile 1
+    const int n0 = min(kvend, p.qo + 2 * qp + 1) - kv0;     // blocks of tile 0 (n or n - 1; >= 1: chunks are even)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -268,7 +272,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quad = warp & 3;
         const int r = quad * 32 + lane;                 // row within the tile
         const int qb = 2 * qp + t;                      // query block of this tile
-        const int qrow = qb * BQ + r;                   // query position
+        const int qrow = qb * BQ + r;                   // query row (this rank's)
+        const int qpos = (p.qo + qb) * BQ + r;          // its global position (causal mask)
         const int nt = t ? n : n0;
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         const uint32_t ts = t_s + t * 128 + lane_off, to = t_o + t * 128 + lane_off;
@@ -282,12 +287,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BKV / 32; ++c) tmem_ld32(ts + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
             tmem_ld_wait();
             const int kb = kv0 + j;
-            const bool masked = kb == qb || (kb + 1) * BKV > p.T;
+            const bool masked = kb == p.qo + qb || (kb + 1) * BKV > p.T_kv;
             auto apply_mask = [&](int c0, int c1) {
 #pragma unroll
                 for (int u = c0; u < c1; ++u) {
                     const int key = kb * BKV + u;
-                    if (key > qrow || key >= p.T) sr[u] = __float_as_uint(-INFINITY);
+                    if (key > qpos || key >= p.T_kv) sr[u] = __float_as_uint(-INFINITY);
                 }
             };
             if (masked) apply_mask(0, BKV);
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // L = sum_c 2^(m_c-M) l_c, lse = (M + log2 L) ln 2. Chunks are merged in chunk
 // order, so the result is deterministic. Block = (query block, head, 16-column
 // slice of d); thread = (row, 8 columns): partial loads are coalesced along
-// rows ([d][row] layout). Query blocks from `chunk` on belong to split pairs.
+// rows ([d][row] layout). Blocks of unsplit rows (fewer than 2 chunks) exit.
 template <int D>
 constexpr int combine_slices() { return D / 16; }
 // MAXC >= the row's chunk count: every load is issued unconditionally (chunk
@@ -431,8 +436,8 @@ constexpr int combine_slices() { return D / 16; }
 template <int MAXC, int D>
 __global__ void __launch_bounds__(256) attn_fwd_combine_kernel(const FwdParams p) {
     const int h = blockIdx.y;
-    const int qb = p.chunk + blockIdx.x;
-    const int nblk = min(2 * (qb >> 1) + 2, p.nkb);
+    const int qb = blockIdx.x;
+    const int nblk = min(p.qo + 2 * (qb >> 1) + 2, p.nkb);
     const int nc = (nblk + p.chunk - 1) / p.chunk;
     const int r = threadIdx.x & (BQ - 1);
     const int d0 = blockIdx.z * 16 + (threadIdx.x >> 7) * 8;
@@ -480,11 +485,14 @@ struct FwdSplit {
     FwdSched sched;
 };
 
-double fwd_makespan(int nq, int nkb, int chunk, int sms, std::vector<std::pair<float, uint32_t>>* out) {
+// KV blocks a query-tile pair reads: causal up to its second tile's diagonal
+int pair_blocks(int qp, int qo, int nkb) { return std::min(qo + 2 * qp + 2, nkb); }
+
+double fwd_makespan(int nq, int npairs, int qo, int nkb, int chunk, int sms,
+                    std::vector<std::pair<float, uint32_t>>* out) {
     std::vector<std::pair<float, uint32_t>> it;
-    const int npairs = (nkb + 1) / 2;
     for (int qp = 0; qp < npairs; ++qp) {
-        const int nblk = std::min(2 * qp + 2, nkb);
+        const int nblk = pair_blocks(qp, qo, nkb);
         const int nc = (nblk + chunk - 1) / chunk;
         for (int c = 0; c < nc; ++c) {
             const int len = std::min((c + 1) * chunk, nblk) - c * chunk;
@@ -508,31 +516,32 @@ double fwd_makespan(int nq, int nkb, int chunk, int sms, std::vector<std::pair<f
     return span;
 }
 
-const FwdSplit& fwd_split_plan(int T, int nq) {
-    static std::map<std::pair<int, int>, FwdSplit> cache;  // nodes are stable: references stay valid
+// T: query rows, T_kv: key rows, qo: query offset in 128-blocks
+const FwdSplit& fwd_split_plan(int T, int nq, int T_kv, int qo) {
+    static std::map<std::tuple<int, int, int, int>, FwdSplit> cache;  // nodes are stable: references stay valid
     static std::mutex mu;  // loopback groups launch from several host threads
     std::lock_guard<std::mutex> lock(mu);
-    auto key = std::make_pair(T, nq);
+    auto key = std::make_tuple(T, nq, T_kv, qo);
     auto f = cache.find(key);
     if (f != cache.end()) return f->second;
     FwdSplit sp;
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int nkb = (T + BKV - 1) / BKV;
-    const int npairs = (nkb + 1) / 2;
+    const int nkb = (T_kv + BKV - 1) / BKV;
+    const int npairs = ((T + BQ - 1) / BQ + 1) / 2;
     // many heads x pairs per SM already balance; only small grids are split
     // (measured on B200: 16 heads x 16 pairs, 1.7 items per SM, run faster unsplit)
     if (2LL * nq * npairs > 3LL * sms) return cache.emplace(key, sp).first->second;
-    const int full = 2 * npairs;
-    double best = fwd_makespan(nq, nkb, full, sms, nullptr);
+    const int full = pair_blocks(npairs - 1, qo, nkb);  // the longest row
+    double best = fwd_makespan(nq, npairs, qo, nkb, full, sms, nullptr);
     // DH_ATTN_FWD_CHUNK=<even KV blocks> forces a chunk size (tuning runs)
     const char* force = std::getenv("DH_ATTN_FWD_CHUNK");
     const int forced = force ? std::atoi(force) : 0;
     for (int div : {2, 3, 4, 6, 8}) {
         const int c = forced ? forced : std::max(2, 2 * ((full + 2 * div - 1) / (2 * div)));
-        if (c >= nkb || (full + c - 1) / c > 16 || c % 2) continue;
+        if (c >= full || (full + c - 1) / c > 16 || c % 2) continue;
         std::vector<std::pair<float, uint32_t>> it;
-        const double ms = fwd_makespan(nq, nkb, c, sms, &it);
+        const double ms = fwd_makespan(nq, npairs, qo, nkb, c, sms, &it);
         if ((forced || ms < 0.85 * best) && static_cast<int>(it.size()) <= kMaxItems) {
             best = ms;
             sp.chunk = c;
@@ -546,10 +555,10 @@ const FwdSplit& fwd_split_plan(int T, int nq) {
 
 }  // namespace
 
-long long attn_fwd_tc_scratch_floats(int T, int nq, int D) {
-    const FwdSplit& sp = fwd_split_plan(T, nq);
+long long attn_fwd_tc_scratch_floats(int T, int nq, int D, int T_kv, int q_offset) {
+    const FwdSplit& sp = fwd_split_plan(T, nq, T_kv, q_offset / BQ);
     if (!sp.chunk) return 0;
-    const long long nqb2 = 2LL * (((T + BKV - 1) / BKV + 1) / 2);
+    const long long nqb2 = 2LL * (((T + BQ - 1) / BQ + 1) / 2);
     return static_cast<long long>(nq) * nqb2 * sp.maxc * (BQ * D + 2 * BQ);
 }
 
@@ -558,13 +567,13 @@ namespace {
 template <int D>
 int attn_fwd_tc_d(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
                   long long ldo, float* lse, int T, int nq, int nkv, float scale, float* scratch,
-                  long long scratch_floats, cudaStream_t s) {
+                  long long scratch_floats, int T_kv, int q_offset, cudaStream_t s) {
     CUtensorMap mq, mk, mv;
     int rc = make_tma_2d(&mq, q, static_cast<long long>(nq) * D, T, ldq, 64, BQ);
     if (rc) return rc;
-    rc = make_tma_2d(&mk, k, static_cast<long long>(nkv) * D, T, ldkv, 64, BKV);
+    rc = make_tma_2d(&mk, k, static_cast<long long>(nkv) * D, T_kv, ldkv, 64, BKV);
     if (rc) return rc;
-    rc = make_tma_2d(&mv, v, static_cast<long long>(nkv) * D, T, ldkv, 64, BKV);
+    rc = make_tma_2d(&mv, v, static_cast<long long>(nkv) * D, T_kv, ldkv, 64, BKV);
     if (rc) return rc;
     static bool cfg = false;
     if (!cfg) {
@@ -572,12 +581,14 @@ int attn_fwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
                                            FwdSmem<D>::total));
         cfg = true;
     }
-    const int nkb = (T + BKV - 1) / BKV;
-    const int npairs = (nkb + 1) / 2;
+    const int nkb = (T_kv + BKV - 1) / BKV;
+    const int npairs = ((T + BQ - 1) / BQ + 1) / 2;
+    const int qo = q_offset / BQ;
     FwdParams prm{lse, static_cast<__nv_bfloat16*>(o), ldo, T, nq / nkv, scale * kLog2e, nq, nkb, npairs, 0, 1,
-                  scratch};
-    const FwdSplit& sp = fwd_split_plan(T, nq);
-    const bool split = sp.chunk && scratch && scratch_floats >= attn_fwd_tc_scratch_floats(T, nq, D);
+                  scratch, T_kv, qo};
+    const FwdSplit& sp = fwd_split_plan(T, nq, T_kv, qo);
+    const bool split =
+        sp.chunk && scratch && scratch_floats >= attn_fwd_tc_scratch_floats(T, nq, D, T_kv, q_offset);
     if (split) {
         prm.chunk = sp.chunk;
         prm.maxc = sp.maxc;
@@ -586,7 +597,7 @@ int attn_fwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
     attn_fwd_tc_kernel<D><<<grid, kThreads, FwdSmem<D>::total, s>>>(mq, mk, mv, prm, sp.sched);
     DH_CUDA_CHECK(cudaGetLastError());
     if (split) {
-        const dim3 cg(2 * npairs - sp.chunk, nq, combine_slices<D>());
+        const dim3 cg(2 * npairs, nq, combine_slices<D>());
         if (sp.maxc <= 2) attn_fwd_combine_kernel<2, D><<<cg, 256, 0, s>>>(prm);
         else if (sp.maxc <= 4) attn_fwd_combine_kernel<4, D><<<cg, 256, 0, s>>>(prm);
         else if (sp.maxc <= 8) attn_fwd_combine_kernel<8, D><<<cg, 256, 0, s>>>(prm);
@@ -598,14 +609,20 @@ int attn_fwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
 
 }  // namespace
 
-// Host launcher (dh_attn_fwd dispatches here for head_dim 64 and 128).
+// Host launcher (dh_attn_fwd dispatches here for head_dim 64 and 128). T
+// query rows at global positions [q_offset, q_offset + T) attend causally to
+// T_kv key rows (context parallelism: q_offset = rank * T, keys gathered).
 int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
                 long long ldo, float* lse, int T, int nq, int nkv, int D, float scale, float* scratch,
-                long long scratch_floats, cudaStream_t s) {
+                long long scratch_floats, int T_kv, int q_offset, cudaStream_t s) {
+    if (q_offset % (2 * BQ) || q_offset + T > T_kv)
+        return set_error(DH_ERR_INVALID, "attn: q_offset must be a multiple of 256 and q_offset + T <= T_kv");
     if (D == 128)
-        return attn_fwd_tc_d<128>(q, k, v, ldq, ldkv, o, ldo, lse, T, nq, nkv, scale, scratch, scratch_floats, s);
+        return attn_fwd_tc_d<128>(q, k, v, ldq, ldkv, o, ldo, lse, T, nq, nkv, scale, scratch, scratch_floats, T_kv,
+                                  q_offset, s);
     if (D == 64)
-        return attn_fwd_tc_d<64>(q, k, v, ldq, ldkv, o, ldo, lse, T, nq, nkv, scale, scratch, scratch_floats, s);
+        return attn_fwd_tc_d<64>(q, k, v, ldq, ldkv, o, ldo, lse, T, nq, nkv, scale, scratch, scratch_floats, T_kv,
+                                 q_offset, s);
     return set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }
 
@@ -621,8 +638,10 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
 //   dV  += P^T dO       M128 N128 K64    A=P^T (TMEM)    B=dO (smem, MN-major)
 //   dK  += dS^T Q       M128 N128 K64    A=dS^T (TMEM)   B=Q  (smem, MN-major)
 //   TMEM: S^T x2 (64) | dP^T x2 (64) | dV (128) | dK (128) = 512 columns;
-//   P^T / dS^T (bf16 pairs) overwrite the first 32 columns of their S^T / dP^T
-//   buffer, so the elementwise results never pass through shared memory.
+//   P^T / dS^T (bf16 pairs) overwrite the fp32 S^T / dP^T columns of the half
+//   of the q tile they come from (columns [32 h, 32 h + 16) for half h), so the
+//   elementwise results never pass through shared memory and the two halves of
+//   the elementwise warps never write columns the other reads (no barrier).
 // dQ item — one CTA per (128-query block, q head); inner key tiles of 64:
 //   S = Q K^T, dP = dO V^T (M128 N64 K128), dS = P (dP - D)    (thread = query row)
 //   dQ += dS K          M128 N128 K64    A=dS (TMEM)     B=K (smem, MN-major)
@@ -676,8 +695,10 @@ struct BwdParams {
     __nv_bfloat16* dv;
     __nv_bfloat16* dq;
     long long lddkv, lddq;
-    int T, group;
+    int T, group;   // T: query rows (this rank's)
     float scale, scale_log2;
+    int T_kv;       // key rows
+    int qo;         // query offset in 128-blocks (context parallelism), even
 };
 
 // K-major 64-row tile (one 64-wide K atom per half): k-step kk over d (0..7).
@@ -713,8 +734,9 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
 
     const int kvh = h / p.group;
     const int nq64 = (p.T + BT64 - 1) / BT64;
-    const int i0 = (kb * BKV) / BT64;  // first q tile with a query >= the block's first key
-    const int n_it = nq64 - i0;
+    // first local q tile with a query at or after the block's first key
+    const int i0 = max(0, (kb - p.qo) * BKV / BT64);
+    const int n_it = max(0, nq64 - i0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -802,8 +824,10 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 const uint32_t o_addr = smem_u32(sm + KvSmem::dout + qs * kTile64);
 #pragma unroll
                 for (int kk = 0; kk < BT64 / 16; ++kk) {
-                    tc_mma_bf16_ts(t_dv, t_s + sb * 64 + kk * 8, desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
-                    tc_mma_bf16_ts(t_dk, t_dp + sb * 64 + kk * 8, desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
+                    // P^T / dS^T: q columns [32 h, 32 h + 32) packed at column 32 h (see below)
+                    const uint32_t pc = (kk >> 1) * 32 + (kk & 1) * 8;
+                    tc_mma_bf16_ts(t_dv, t_s + sb * 64 + pc, desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
+                    tc_mma_bf16_ts(t_dk, t_dp + sb * 64 + pc, desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
                 }
                 tc_commit(&q_empty[qs]);
                 if (it + 1 == n_it) tc_commit(acc_done);
@@ -842,12 +866,11 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             tmem_ld32(t_s + sb * 64 + lane_off + half * 32, a);
             tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
             tmem_ld_wait();
-            // the other half's P^T/dS^T stores overwrite columns this half reads
             if (threadIdx.x == 64) ATR(it * 8 + 5);
-            named_barrier(2, 256);
             if (threadIdx.x == 64) ATR(it * 8 + 6);
             // whole tile causal-visible and in range: no per-element masking
-            const bool full_tile = qi * BT64 >= key_hi && qi * BT64 + BT64 <= p.T && key_hi < p.T;
+            const int qg0 = p.qo * BQ + qi * BT64;  // global position of the tile's first query
+            const bool full_tile = qg0 >= key_hi && qi * BT64 + BT64 <= p.T && key_hi < p.T_kv;
             const float2* lv = reinterpret_cast<const float2*>(vec + (it % kStages) * 128 + half * 32);
             const float2* dv2 = reinterpret_cast<const float2*>(vec + (it % kStages) * 128 + 64 + half * 32);
             uint32_t pp[16], pd[16];
@@ -861,9 +884,10 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 f2_unpack(x, x0, x1);
                 float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
                 if (!full_tile) {
-                    const int q = qi * BT64 + half * 32 + 2 * u;
-                    if (q < key || q >= p.T || key >= p.T) e0 = 0.f;
-                    if (q + 1 < key || q + 1 >= p.T || key >= p.T) e1 = 0.f;
+                    const int q = qi * BT64 + half * 32 + 2 * u;  // local row; global position q + qo * BQ
+                    const int qg = q + p.qo * BQ;
+                    if (qg < key || q >= p.T || key >= p.T_kv) e0 = 0.f;
+                    if (qg + 1 < key || q + 1 >= p.T || key >= p.T_kv) e1 = 0.f;
                 }
                 const uint64_t e = f2_pack(e0, e1);
                 // dS^T = P^T (dP^T - D)
@@ -876,8 +900,10 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 pd[u] = pack2(s0, s1);
             }
             if (threadIdx.x == 64) ATR(it * 8 + 7);
-            tmem_st16(t_s + sb * 64 + lane_off + half * 16, pp);
-            tmem_st16(t_dp + sb * 64 + lane_off + half * 16, pd);
+            // each half packs its bf16 pairs over the start of the fp32 columns it
+            // read itself, so no half overwrites columns the other still reads
+            tmem_st16(t_s + sb * 64 + lane_off + half * 32, pp);
+            tmem_st16(t_dp + sb * 64 + lane_off + half * 32, pd);
             tmem_st_wait();
             tc_fence_before();
             if (threadIdx.x == 64) ATR(it * 8 + 4);
@@ -885,7 +911,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         }
         if (n_it > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
-        const bool ok = key < p.T;
+        const bool ok = key < p.T_kv;
 #pragma unroll 1
         for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
             uint32_t ka[32], va[32];
@@ -908,16 +934,21 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                     *reinterpret_cast<uint4*>(vr + t) = pack8(fv);
                 }
             } else {
-                float* kr = p.dk_part + (static_cast<long long>(h) * p.T + key) * D + c * 32;
-                float* vr = p.dv_part + (static_cast<long long>(h) * p.T + key) * D + c * 32;
+                float* kr = p.dk_part + (static_cast<long long>(h) * p.T_kv + key) * D + c * 32;
+                float* vr = p.dv_part + (static_cast<long long>(h) * p.T_kv + key) * D + c * 32;
+                // keys after every query of this rank (context parallelism) get no
+                // gradient; TMEM was never written for them (select, not multiply)
+                const bool any = n_it > 0;
 #pragma unroll
                 for (int t = 0; t < 32; t += 4) {
-                    *reinterpret_cast<float4*>(kr + t) =
-                        make_float4(__uint_as_float(ka[t]) * p.scale, __uint_as_float(ka[t + 1]) * p.scale,
-                                    __uint_as_float(ka[t + 2]) * p.scale, __uint_as_float(ka[t + 3]) * p.scale);
-                    *reinterpret_cast<float4*>(vr + t) =
-                        make_float4(__uint_as_float(va[t]), __uint_as_float(va[t + 1]),
-                                    __uint_as_float(va[t + 2]), __uint_as_float(va[t + 3]));
+                    float k4[4], v4[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        k4[u] = any ? __uint_as_float(ka[t + u]) * p.scale : 0.f;
+                        v4[u] = any ? __uint_as_float(va[t + u]) : 0.f;
+                    }
+                    *reinterpret_cast<float4*>(kr + t) = make_float4(k4[0], k4[1], k4[2], k4[3]);
+                    *reinterpret_cast<float4*>(vr + t) = make_float4(v4[0], v4[1], v4[2], v4[3]);
                 }
             }
         }
@@ -951,7 +982,8 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
     const int kvh = h / p.group;
-    const int n_it = (qb * BQ + BQ) / BT64;  // key tiles 0 .. covering the block's last query
+    // key tiles 0 .. covering the block's last query (global position)
+    const int n_it = min((p.qo * BQ + qb * BQ + BQ) / BT64, (p.T_kv + BT64 - 1) / BT64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -1024,7 +1056,8 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                 const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
 #pragma unroll
                 for (int kk = 0; kk < BT64 / 16; ++kk)
-                    tc_mma_bf16_ts(t_dq, t_dp + sb * 64 + kk * 8, desc_mn64(k_addr, kk), id_g, (it | kk) != 0);
+                    tc_mma_bf16_ts(t_dq, t_dp + sb * 64 + (kk >> 1) * 32 + (kk & 1) * 8, desc_mn64(k_addr, kk), id_g,
+                                   (it | kk) != 0);
                 tc_commit(&kv_empty[ks]);
                 if (it + 1 == n_it) tc_commit(acc_done);
             }
@@ -1075,9 +1108,9 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
             tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
             tmem_ld_wait();
             if (threadIdx.x == 64) ATR(it * 8 + 5);
-            named_barrier(2, 256);  // the other half's dS stores overwrite columns this half reads
             if (threadIdx.x == 64) ATR(it * 8 + 6);
-            const bool full_tile = it * BT64 + BT64 - 1 <= qb * BQ && it * BT64 + BT64 <= p.T && qb * BQ + BQ <= p.T;
+            const int qg0 = (p.qo + qb) * BQ;  // global position of the block's first query
+            const bool full_tile = it * BT64 + BT64 - 1 <= qg0 && it * BT64 + BT64 <= p.T_kv && qb * BQ + BQ <= p.T;
             uint32_t pd[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
@@ -1087,8 +1120,9 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                 float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
                 if (!full_tile) {
                     const int key = it * BT64 + half * 32 + 2 * u;
-                    if (key > qrow || key >= p.T) e0 = 0.f;
-                    if (key + 1 > qrow || key + 1 >= p.T) e1 = 0.f;
+                    const int qpos = qg0 + r;
+                    if (key > qpos || key >= p.T_kv) e0 = 0.f;
+                    if (key + 1 > qpos || key + 1 >= p.T_kv) e1 = 0.f;
                 }
                 const uint64_t ds =
                     ffma2(f2_pack(e0, e1), fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), nd2),
@@ -1098,7 +1132,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
                 pd[u] = pack2(s0, s1);
             }
             if (threadIdx.x == 64) ATR(it * 8 + 7);
-            tmem_st16(t_dp + sb * 64 + lane_off + half * 16, pd);
+            tmem_st16(t_dp + sb * 64 + lane_off + half * 32, pd);  // over this half's own fp32 columns
             tmem_st_wait();
             tc_fence_before();
             if (threadIdx.x == 64) ATR(it * 8 + 4);
@@ -1143,30 +1177,45 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                        const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
                        const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k64, const __grid_constant__ CUtensorMap tm_v64,
-                       const BwdParams p, const int nq, const int nb) {
-    const int rank = blockIdx.x / (2 * nq);
-    const int rem = blockIdx.x % (2 * nq);
-    if (rem < nq)
-        attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q64, tm_do64, p, rank, rem);  // key block `rank` sees the most queries
+                       const BwdParams p, const int nq, const int nb_kv, const int nb_q) {
+    // rank r: key block r (the low blocks see the most queries) and query
+    // block nb_q - 1 - r (the high blocks see the most keys), every head;
+    // past the shorter of the two ranges only the longer kind remains
+    const int both = min(nb_kv, nb_q);
+    int rank, rem;
+    bool dkdv;
+    if (static_cast<int>(blockIdx.x) < 2 * nq * both) {
+        rank = blockIdx.x / (2 * nq);
+        rem = blockIdx.x % (2 * nq);
+        dkdv = rem < nq;
+        if (!dkdv) rem -= nq;
+    } else {
+        const int i = blockIdx.x - 2 * nq * both;
+        rank = both + i / nq;
+        rem = i % nq;
+        dkdv = nb_kv > nb_q;
+    }
+    if (dkdv)
+        attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q64, tm_do64, p, rank, rem);
     else
-        attn_bwd_dq_body<D>(tm_q, tm_do, tm_k64, tm_v64, p, nb - 1 - rank, rem - nq);
+        attn_bwd_dq_body<D>(tm_q, tm_do, tm_k64, tm_v64, p, nb_q - 1 - rank, rem);
 }
 
 template <int D>
 int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, long long ldkv, const void* dout,
                   long long ldo, const float* lse, const float* dvec, float* dk_part, float* dv_part, void* dq,
                   void* dk, void* dv, long long lddq, long long lddkv, int T, int nq, int nkv, float scale,
-                  cudaStream_t s) {
+                  int T_kv, int q_offset, cudaStream_t s) {
     CUtensorMap mk, mv, mq64, mdo64, mq, mdo, mk64, mv64;
     const long long qcols = static_cast<long long>(nq) * D, kvcols = static_cast<long long>(nkv) * D;
-    int rc = make_tma_2d(&mk, k, kvcols, T, ldkv, 64, 128);
-    if (!rc) rc = make_tma_2d(&mv, v, kvcols, T, ldkv, 64, 128);
+    int rc = make_tma_2d(&mk, k, kvcols, T_kv, ldkv, 64, 128);
+    if (!rc) rc = make_tma_2d(&mv, v, kvcols, T_kv, ldkv, 64, 128);
     if (!rc) rc = make_tma_2d(&mq64, q, qcols, T, ldq, 64, 64);
     if (!rc) rc = make_tma_2d(&mdo64, dout, qcols, T, ldo, 64, 64);
     if (!rc) rc = make_tma_2d(&mq, q, qcols, T, ldq, 64, 128);
     if (!rc) rc = make_tma_2d(&mdo, dout, qcols, T, ldo, 64, 128);
-    if (!rc) rc = make_tma_2d(&mk64, k, kvcols, T, ldkv, 64, 64);
-    if (!rc) rc = make_tma_2d(&mv64, v, kvcols, T, ldkv, 64, 64);
+    if (!rc) rc = make_tma_2d(&mk64, k, kvcols, T_kv, ldkv, 64, 64);
+    if (!rc) rc = make_tma_2d(&mv64, v, kvcols, T_kv, ldkv, 64, 64);
     if (rc) return rc;
     constexpr int smem = KvSmem<D>::total > DqSmem<D>::total ? KvSmem<D>::total : DqSmem<D>::total;
     static bool cfg = false;
@@ -1177,10 +1226,10 @@ int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
     BwdParams prm{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(dout), ldq, ldo,
                   lse, dvec, dk_part, dv_part, static_cast<__nv_bfloat16*>(dk),
                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
-                  nq / nkv, scale, scale * kLog2e};
-    const int nb = (T + BKV - 1) / BKV;
-    attn_bwd_tc_kernel<D><<<2 * nb * nq, kThreadsBwd, smem, s>>>(mk, mv, mq64, mdo64, mq, mdo, mk64, mv64, prm,
-                                                                nq, nb);
+                  nq / nkv, scale, scale * kLog2e, T_kv, q_offset / BQ};
+    const int nb_kv = (T_kv + BKV - 1) / BKV, nb_q = (T + BQ - 1) / BQ;
+    attn_bwd_tc_kernel<D><<<(nb_kv + nb_q) * nq, kThreadsBwd, smem, s>>>(mk, mv, mq64, mdo64, mq, mdo, mk64, mv64,
+                                                                        prm, nq, nb_kv, nb_q);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }
@@ -1192,13 +1241,15 @@ int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
 int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
                 const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
                 float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
-                int nq, int nkv, int D, float scale, cudaStream_t s) {
+                int nq, int nkv, int D, float scale, int T_kv, int q_offset, cudaStream_t s) {
+    if (q_offset % (2 * BQ) || q_offset + T > T_kv)
+        return set_error(DH_ERR_INVALID, "attn_bwd: q_offset must be a multiple of 256 and q_offset + T <= T_kv");
     if (D == 128)
         return attn_bwd_tc_d<128>(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq,
-                                  lddkv, T, nq, nkv, scale, s);
+                                  lddkv, T, nq, nkv, scale, T_kv, q_offset, s);
     if (D == 64)
         return attn_bwd_tc_d<64>(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq,
-                                 lddkv, T, nq, nkv, scale, s);
+                                 lddkv, T, nq, nkv, scale, T_kv, q_offset, s);
     return set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }
 

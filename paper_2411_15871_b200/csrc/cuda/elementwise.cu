@@ -214,53 +214,6 @@ __global__ void __launch_bounds__(RB == 1 ? 1024 : 512) rmsnorm_bwd_rows(const u
     dst[1] = make_float4(dg[4], dg[5], dg[6], dg[7]);
 }
 
-__global__ void rmsnorm_bwd_cols(const uint4* __restrict__ x, const uint4* __restrict__ g,
-                                 const float* __restrict__ rstd, const uint4* __restrict__ dy,
-                                 const uint4* __restrict__ resid, uint4* __restrict__ dx,
-                                 float* __restrict__ partial, int rows, int vec_cols, float inv_cols) {
-    __shared__ float red[2][32];
-    const int t = threadIdx.x;
-    const int lane = t % 32, wid = t / 32, nw = (blockDim.x + 31) / 32;
-    float gam[8], dg[8];
-    unpack8(g[t], gam);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) dg[k] = 0.f;
-    int parity = 0;
-    for (int row = blockIdx.x; row < rows; row += gridDim.x, parity ^= 1) {
-        const long long off = static_cast<long long>(row) * vec_cols + t;
-        const float r = rstd[row];
-        float xv[8], dv[8];
-        unpack8(x[off], xv);
-        unpack8(dy[off], dv);
-        float dot = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            xv[k] *= r;             // xhat
-            dg[k] += dv[k] * xv[k];
-            dv[k] *= gam[k];        // dxhat
-            dot += dv[k] * xv[k];
-        }
-        dot = warp_sum(dot);
-        if (lane == 0) red[parity][wid] = dot;
-        __syncthreads();
-        float tot = 0.f;
-        for (int w = 0; w < nw; ++w) tot += red[parity][w];
-        tot *= inv_cols;
-        float o[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = r * (dv[k] - xv[k] * tot);
-        if (resid) {
-            float rv[8];
-            unpack8(resid[off], rv);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) o[k] += rv[k];
-        }
-        dx[off] = pack8(o);
-    }
-    float4* dst = reinterpret_cast<float4*>(partial + static_cast<long long>(blockIdx.x) * vec_cols * 8 + t * 8);
-    dst[0] = make_float4(dg[0], dg[1], dg[2], dg[3]);
-    dst[1] = make_float4(dg[4], dg[5], dg[6], dg[7]);
-}
 
 // dgamma_acc[c] += sum_w partial[w][c]. Block = 32 columns x 8 warps; warp j
 // sums rows j, j+8, ... and the 8 warp partials are combined in warp order, so

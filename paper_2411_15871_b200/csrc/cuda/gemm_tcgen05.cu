@@ -20,6 +20,7 @@
 // the epilogue of tile i overlaps the main loop of tile i+1. The grid is persistent: min(tiles, SMs allowed), which
 // is how the SI executor caps a GEMM's SM footprint next to NCCL kernels.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -62,7 +63,28 @@ struct KParams {
     const __nv_bfloat16* aux1;
     long long ld_aux;
     int aux_is_up;  // kEpiSwiGLUFwd: acc is the gate projection and aux0 holds up
+    // Raster order of the persistent tile loop (tile_coords): groups of `group`
+    // m-tiles (b_resident == 0: their A panels stay in L2 while every n-tile
+    // streams past) or of `group` n-tiles (b_resident == 1), the grouped
+    // dimension fastest inside a group.
+    int b_resident, group;
 };
+
+void raster_for(KParams& p, int bm, int bn, int k);
+
+// Tile index -> (m-tile, n-tile) in the raster order chosen by the host
+// (raster_for): the operand panels a group touches stay L2-resident while the
+// other operand's panels stream through once per group.
+__device__ __forceinline__ void tile_coords(int tile, const KParams& p, int* mi, int* ni) {
+    const int fast = p.b_resident ? p.tiles_n : p.tiles_m;  // grouped dimension
+    const int slow = p.b_resident ? p.tiles_m : p.tiles_n;
+    const int per_group = p.group * slow;
+    const int g = tile / per_group, r = tile - g * per_group;
+    const int width = min(p.group, fast - g * p.group);
+    const int f = g * p.group + r % width, sl = r / width;
+    *mi = p.b_resident ? sl : f;
+    *ni = p.b_resident ? f : sl;
+}
 
 template <int BN, bool A_MN, bool B_MN, int EPI, bool D_F32>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -113,8 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int m0 = (tile % p.tiles_m) * BM;
-                const int n0 = (tile / p.tiles_m) * BN;
+                int mi, ni;
+                tile_coords(tile, p, &mi, &ni);
+                const int m0 = mi * BM;
+                const int n0 = ni * BN;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], Cfg::kStageBytes);
@@ -186,8 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         int chunk = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int m0 = (tile % p.tiles_m) * BM;
-            const int n0 = (tile / p.tiles_m) * BN;
+            int mi, ni;
+            tile_coords(tile, p, &mi, &ni);
+            const int m0 = mi * BM;
+            const int n0 = ni * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if constexpr (EPI == kEpiStoreBf16) {
@@ -391,8 +417,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs) {
-                const int m0 = (tile % tiles_m) * 256 + rank * BM;             // this CTA's A rows
-                const int n0 = (tile / tiles_m) * PBN + rank * C::kHalfB;      // this CTA's B half
+                int mi, ni;
+                tile_coords(tile, p, &mi, &ni);
+                const int m0 = mi * 256 + rank * BM;             // this CTA's A rows
+                const int n0 = ni * PBN + rank * C::kHalfB;      // this CTA's B half
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full[stage], 2 * C::kStage);
@@ -461,8 +489,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
         uint32_t acc_phase = 0;
         int chunk = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs) {
-            const int m0 = (tile % tiles_m) * 256 + rank * BM;
-            const int n0 = (tile / tiles_m) * PBN;
+            int mi, ni;
+            tile_coords(tile, p, &mi, &ni);
+            const int m0 = mi * 256 + rank * BM;
+            const int n0 = ni * PBN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if constexpr (kFused) {
@@ -527,7 +557,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
                         if (nc == kChunks) nt += npairs, nc = 0;
                         if (nt < num_tiles) {
                             bulk_wait_read<1>();
-                            load_aux(chunk + 1, (nt % tiles_m) * 256 + rank * BM, (nt / tiles_m) * PBN + nc * 64);
+                            int nmi, nni;
+                            tile_coords(nt, p, &nmi, &nni);
+                            load_aux(chunk + 1, nmi * 256 + rank * BM, nni * PBN + nc * 64);
                         }
                     }
                 }
@@ -677,6 +709,7 @@ int launch(const dh_gemm_args* g, cudaStream_t stream) {
     p.accumulate = g->accumulate;
     p.tiles_m = (g->m + BM - 1) / BM;
     p.tiles_n = (g->n + BN - 1) / BN;
+    raster_for(p, BM, BN, g->k);
     const int tiles = p.tiles_m * p.tiles_n;
     int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
     ctas = std::min(ctas, tiles);
@@ -690,6 +723,42 @@ int launch(const dh_gemm_args* g, cudaStream_t stream) {
     kern<<<ctas, kThreads, Cfg::kSmemBytes, stream>>>(ma, mb, md, p);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
+}
+
+// Raster order for the tile loop: estimate the DRAM bytes of each order and
+// group size (the grouped operand's panels read once, the other operand's once
+// per group; a group's panels must fit an L2 budget that leaves room for the
+// streamed operand and the output) and keep the cheapest. The all-of-M group
+// (b_resident 0, group tiles_m) is the plain m-fastest order.
+void raster_for(KParams& p, int bm, int bn, int k) {
+    constexpr double kBudget = 40.0 * (1 << 20);
+    const double pa = static_cast<double>(bm) * k * 2, pb = static_cast<double>(bn) * k * 2;  // panel bytes
+    const double A = pa * p.tiles_m, B = pb * p.tiles_n;
+    double best = -1.0;
+    for (int br = 0; br < 2; ++br) {
+        const int fast = br ? p.tiles_n : p.tiles_m;
+        const double panel = br ? pb : pa;
+        for (int gsz = fast; gsz >= 1; --gsz) {
+            if (gsz * panel > kBudget && gsz > 1) continue;
+            const int groups = (fast + gsz - 1) / gsz;
+            const double bytes = br ? B + A * groups : A + B * groups;
+            if (best < 0 || bytes < best * 0.999) {
+                best = bytes;
+                p.b_resident = br;
+                p.group = gsz;
+            }
+            break;  // the largest group within the budget is the cheapest for this order
+        }
+    }
+    // DH_GEMM_RASTER=m: the plain m-fastest order (A/B comparisons)
+    static const bool plain = [] {
+        const char* e = std::getenv("DH_GEMM_RASTER");
+        return e && e[0] == 'm';
+    }();
+    if (plain) {
+        p.b_resident = 0;
+        p.group = p.tiles_m;
+    }
 }
 
 template <int PBN, bool A_MN, bool B_MN, int EPI>
@@ -726,6 +795,7 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
     p.accumulate = g->accumulate;
     p.tiles_m = (g->m + 255) / 256;
     p.tiles_n = (g->n + PBN - 1) / PBN;
+    raster_for(p, 256, PBN, g->k);
     const int tiles = p.tiles_m * p.tiles_n;
     const int grid = 2 * std::min(ctas / 2, tiles);
     auto kern = gemm_pair_kernel<PBN, A_MN, B_MN, EPI>;

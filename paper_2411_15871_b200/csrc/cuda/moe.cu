@@ -171,17 +171,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             sl[k] = slot[t * KT + k];
             w[k] = wts[t * KT + k];
         }
-        for (int c0 = lane; c0 < hvec; c0 += 64) {
-            uint4 v[KT][2];
+        // NJ 16-byte columns per lane in flight per slot row (one for top-k > 4,
+        // where two would exceed the register budget)
+        constexpr int NJ = KT > 4 ? 1 : 2;
+        for (int c0 = lane; c0 < hvec; c0 += 32 * NJ) {
+            uint4 v[KT][NJ];
 #pragma unroll
             for (int k = 0; k < KT; ++k)
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < NJ; ++j) {
                     const int c = c0 + 32 * j;
                     v[k][j] = sl[k] >= 0 && c < hvec ? y[static_cast<long long>(sl[k]) * hvec + c] : make_uint4(0, 0, 0, 0);
                 }
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < NJ; ++j) {
                 const int c = c0 + 32 * j;
                 if (c >= hvec) break;
                 float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -87,6 +87,17 @@ int derive_cfg(const dh_model_cfg* c, int tp, int rank, ModelCfg* out) {
         k.capacity = c->capacity > 0 ? c->capacity : moe_capacity(c->seq_len, k.experts, k.topk);
         k.moe_rows = k.experts * k.capacity;
     }
+    k.seq_full = c->seq_len;
+    if (c->context_parallel) {
+        if (c->experts > 1) return set_error(DH_ERR_CONFIG, "model: context parallelism is dense-only");
+        k.cp = tp;
+        k.cp_rank = rank;
+        k.tp = 1;
+        k.rank = 0;
+        if (c->seq_len % (256 * k.cp))
+            return set_error(DH_ERR_INFEASIBLE, "model: context parallelism needs seq_len % (256 * group size) == 0");
+        k.seq = c->seq_len / k.cp;
+    }
     if (k.split < 0 || k.split >= c->layers || k.slots < 0 || k.pp_rank < 0 || k.pp_rank >= k.pp_size)
         return set_error(DH_ERR_CONFIG, "model: bad pipeline stage fields (split_layer, slots, pp_rank/pp_size)");
     if (k.hidden <= 0 || k.layers <= 0 || k.seq <= 0 || k.micro_batches < 1 || k.head_dim <= 0 ||
@@ -130,10 +141,11 @@ int build_dags(Model& m, const weft::ClusterSpec& cl, const weft::SoloTimeTable*
     ms.hidden = m.cfg.hidden;
     ms.intermediate = m.cfg.ffn;
     ms.layers = m.cfg.layers;
-    ms.seq_len = m.cfg.seq;
+    ms.seq_len = m.cfg.seq_full;  // the template's node costs use seq / cp per rank
     weft::ParallelismSpec par;
     par.tp = m.cfg.tp;
     par.sp = m.cfg.tp > 1;
+    par.cp = m.cfg.cp;  // cp > 1 activates cp_kv_exchange / cp_kv_exchange_bwd
     if (m.cfg.moe) {  // moe_ep template (reference op_model.cpp:410)
         ms.name = "dh-moe";
         ms.family = weft::ModelFamily::phi_moe;
@@ -229,6 +241,10 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     m->fs.part = pool.take(tp1 ? 0 : S * H * 2, "act.fwd_transient");
     m->fs.rs_out = pool.take(T * H * 2, "act.fwd_transient");
     const bool a2a = k.moe && k.ep > 1;
+    const size_t KV = 2 * static_cast<size_t>(k.nkv_l) * k.head_dim;  // K|V columns
+    const size_t SF = k.cp > 1 ? static_cast<size_t>(k.seq_full) : 0;
+    m->fs.kv_loc = pool.take(SF ? S * KV * 2 : 0, "act.fwd_transient");
+    m->fs.kv_full = pool.take(SF * KV * 2, "act.fwd_transient");
     m->fs.xp = pool.take(a2a ? MR * H * 2 : 0, "act.fwd_transient");
     m->fs.ye = pool.take(a2a ? MR * H * 2 : 0, "act.fwd_transient");
     auto& b = m->bs;
@@ -262,10 +278,17 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     b.dx1_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
     b.d_o = pool.take(S * A * 2, "act.bwd_transient");
     b.dqkv = pool.take(S * Q * 2, "act.bwd_transient");
-    b.attn_scratch = pool.take(std::max<size_t>(S * k.nq_l * (2 * k.head_dim + 1),
-                                                static_cast<size_t>(dh_attn_fwd_scratch_floats(
-                                                    static_cast<int>(S), k.nq_l, k.nkv_l, k.head_dim))) * 4,
-                               "act.bwd_transient");
+    b.kv_loc = pool.take(SF ? S * KV * 2 : 0, "act.bwd_transient");
+    b.kv_full = pool.take(SF * KV * 2, "act.bwd_transient");
+    b.dkv_full = pool.take(SF * KV * 2, "act.bwd_transient");
+    b.dkv_loc = pool.take(SF ? S * KV * 2 : 0, "act.bwd_transient");
+    {
+        const int SK = SF ? k.seq_full : static_cast<int>(S), qoff = k.cp_rank * static_cast<int>(S);
+        const size_t bwd = static_cast<size_t>(dh_attn_bwd_scratch_floats(static_cast<int>(S), k.nq_l, k.head_dim, SK));
+        const size_t fwd = static_cast<size_t>(
+            dh_attn_fwd_scratch_floats_ex(static_cast<int>(S), k.nq_l, k.nkv_l, k.head_dim, SK, SF ? qoff : 0));
+        b.attn_scratch = pool.take(std::max(bwd, fwd) * 4, "act.bwd_transient");
+    }
     b.ln_partial = pool.take(std::min<size_t>(T, 1184) * H * 4, "act.bwd_transient");
     b.rs_out = pool.take(T * H * 2, "act.bwd_transient");
     for (int i = 0; i < k.micro_batches; ++i) {
@@ -330,7 +353,7 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     RT_TRY(build_dags(*m, default_cluster(), nullptr));
     // EP > 1: replicated weights need their data-parallel gradient all-reduce
     // before AdamW, so the optimizer runs after the program
-    if (k.moe && k.ep > 1) m->fuse_optimizer = false;
+    if ((k.moe && k.ep > 1) || k.cp > 1) m->fuse_optimizer = false;
     *out = m.release();
     return DH_OK;
 }
@@ -387,6 +410,17 @@ int xfer_tag(const Op& op) {
     return (act ? 0 : 1) + 2 * op.strand;
 }
 
+// Context parallelism: pack this chunk's post-RoPE K|V columns (a strided view
+// of the slot's qkv rows) and all-gather them over the CP group; rank r's rows
+// land at [r * seq, (r + 1) * seq), i.e. in global position order.
+int cp_gather_kv(Model& m, const Slot& sl, const Buf& kv_loc, const Buf& kv_full, cudaStream_t s) {
+    const ModelCfg& k = m.cfg;
+    const size_t D = k.head_dim, Q = k.qkv_n, KV = 2 * static_cast<size_t>(k.nkv_l) * D;
+    RT_CUDA(cudaMemcpy2DAsync(m.ptr(kv_loc), KV * 2, m.ptr<__nv_bfloat16>(sl.qkv) + k.nq_l * D, Q * 2, KV * 2,
+                              static_cast<size_t>(k.seq), cudaMemcpyDeviceToDevice, s));
+    return m.ctx->comm->all_gather(m.ptr(kv_loc), m.ptr(kv_full), static_cast<size_t>(k.seq) * KV, s);
+}
+
 int launch_node(Model& m, const Op& op, cudaStream_t s) {
     const ModelCfg& k = m.cfg;
     const int H = k.hidden, S = k.seq, T = k.tok_loc, Q = k.qkv_n, A = k.attn_n, F = k.ffn_l;
@@ -434,12 +468,22 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 1:  // ag0
             RT_TRY(need_comm());
             return comm->all_gather(P(m.fs.ln_loc), P(sl.ln0_full), TH, s);
-        case 2:  // qkv (+ RoPE on q, k)
+        case 2:  // qkv (+ RoPE on q, k at the chunk's global positions)
             RT_TRY(gemm(P(sl.ln0_full), H, false, W + p.wqkv, H, false, P(sl.qkv), Q, false, S, Q, H,
                         false, cap, s));
-            return dh_rope(P(sl.qkv), Q, S, k.nq_l, k.nkv_l, D, k.rope_theta, 0, 0, s);
+            return dh_rope(P(sl.qkv), Q, S, k.nq_l, k.nkv_l, D, k.rope_theta, k.cp_rank * S, 0, s);
+        case 3:  // cp_kv_exchange: all-gather the group's K|V rows (position order)
+            RT_TRY(need_comm());
+            return cp_gather_kv(m, sl, m.fs.kv_loc, m.fs.kv_full, s);
         case 4: {  // attn
             auto* qkv = m.ptr<__nv_bfloat16>(sl.qkv);
+            if (k.cp > 1) {  // this chunk's queries against every key up to them
+                auto* kv = m.ptr<__nv_bfloat16>(m.fs.kv_full);
+                return dh_attn_fwd_ex(qkv, kv, kv + k.nkv_l * D, Q, 2LL * k.nkv_l * D, P(sl.o), A,
+                                      m.ptr<float>(sl.lse), m.ptr<float>(m.bs.attn_scratch),
+                                      static_cast<long long>(m.bs.attn_scratch.bytes / 4), S, k.seq_full,
+                                      k.cp_rank * S, k.nq_l, k.nkv_l, D, scale, s);
+            }
             // the transient attention scratch is shared with attn_bwd: both run on the compute lane
             return dh_attn_fwd(qkv, qkv + k.nq_l * D, qkv + (k.nq_l + k.nkv_l) * D, Q, Q, P(sl.o), A,
                                m.ptr<float>(sl.lse), m.ptr<float>(m.bs.attn_scratch),
@@ -541,9 +585,29 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
             const void* src = tp1 ? P(m.bs.d_x1) : P(m.bs.dx1_full);
             return gemm(src, H, true, P(sl.o), A, true, G + p.wo, A, true, H, A, S, true, cap, s);
         }
+        case 33:  // cp_kv_exchange_bwd: re-gather K|V for attn_bwd (the slot keeps only this chunk's)
+            RT_TRY(need_comm());
+            return cp_gather_kv(m, sl, m.bs.kv_loc, m.bs.kv_full, s);
         case 34: {  // attn_bwd (+ RoPE bwd on dq, dk)
             auto* qkv = m.ptr<__nv_bfloat16>(sl.qkv);
             auto* dqkv = m.ptr<__nv_bfloat16>(m.bs.dqkv);
+            if (k.cp > 1) {
+                // dK|dV over every key from this chunk's queries, then reduce-scattered
+                // to the owners (rank-order sum) and unpacked into dqkv's K|V columns
+                RT_TRY(need_comm());
+                auto* kv = m.ptr<__nv_bfloat16>(m.bs.kv_full);
+                auto* dkv = m.ptr<__nv_bfloat16>(m.bs.dkv_full);
+                const long long KV = 2LL * k.nkv_l * D;
+                RT_TRY(dh_attn_bwd_ex(qkv, kv, kv + k.nkv_l * D, Q, KV, P(sl.o), A, m.ptr<float>(sl.lse),
+                                      P(m.bs.d_o), dqkv, dkv, dkv + k.nkv_l * D, Q, KV,
+                                      m.ptr<float>(m.bs.attn_scratch), S, k.seq_full, k.cp_rank * S, k.nq_l,
+                                      k.nkv_l, D, scale, s));
+                RT_TRY(comm->reduce_scatter(dkv, P(m.bs.dkv_loc), static_cast<size_t>(S) * KV, s));
+                RT_CUDA(cudaMemcpy2DAsync(dqkv + k.nq_l * D, static_cast<size_t>(Q) * 2, P(m.bs.dkv_loc),
+                                          static_cast<size_t>(KV) * 2, static_cast<size_t>(KV) * 2, S,
+                                          cudaMemcpyDeviceToDevice, s));
+                return dh_rope(dqkv, Q, S, k.nq_l, k.nkv_l, D, k.rope_theta, k.cp_rank * S, 1, s);
+            }
             RT_TRY(dh_attn_bwd(qkv, qkv + k.nq_l * D, qkv + (k.nq_l + k.nkv_l) * D, Q, Q, P(sl.o), A,
                                m.ptr<float>(sl.lse), P(m.bs.d_o), dqkv, dqkv + k.nq_l * D,
                                dqkv + (k.nq_l + k.nkv_l) * D, Q, Q, m.ptr<float>(m.bs.attn_scratch),
@@ -594,6 +658,11 @@ int run_optimizer(Model& m, const dh_optim_cfg* oc, cudaStream_t s) {
         // LayerNorm gammas are replicated across the TP group but see only
         // their sequence shard: sum their gradients (Megatron SP rule).
         RT_TRY(m.ctx->comm->all_reduce_f32(m.ptr<float>(m.w_grad), m.gamma_elems, s));
+    }
+    if (k.cp > 1 && m.ctx->comm) {
+        // context parallelism: every weight is replicated over the CP group and
+        // saw only this rank's tokens: sum the gradients (Megatron CP rule)
+        RT_TRY(m.ctx->comm->all_reduce_f32(m.ptr<float>(m.w_grad), m.n_params, s));
     }
     if (k.moe && k.ep > 1 && m.ctx->comm) {
         // data-parallel replicas (gammas, attention, router): sum over the EP group

@@ -104,6 +104,9 @@ struct ModelCfg {
     bool moe = false;
     int ep = 1, ep_rank = 0, e_loc = 0;  // EP group, experts held by this rank
     int moe_rows = 0;                    // experts * capacity: slot rows on either side of the a2a
+    // context parallelism (the context group is the CP group; TP = 1): `seq` is
+    // this rank's token chunk, starting at global position cp_rank * seq
+    int cp = 1, cp_rank = 0, seq_full = 0;
     // derived (per TP rank)
     int tp = 1, rank = 0;
     int tok_loc = 0;  // seq / tp (sequence-parallel shard)
@@ -126,6 +129,7 @@ struct Slot {
 
 struct FwdScratch {
     Buf ln_loc, part, rs_out;
+    Buf kv_loc, kv_full;  // CP: this rank's K|V rows packed, and the group's gathered
     Buf xp, ye;  // MoE with ep > 1: a2a send buffer of the permuted rows, expert outputs
 };
 
@@ -133,6 +137,7 @@ struct BwdScratch {
     Buf grad[2], d_x1, dy_full, d_gate, d_up, d_act, dx_part, dx1_full, d_o, dqkv, attn_scratch,
         ln_partial, rs_out;
     Buf dys, dys_e, dxe, dxp, dw, router_scratch;  // MoE
+    Buf kv_loc, kv_full, dkv_full, dkv_loc;        // CP: re-gathered K|V, dK|dV partials and sums
 };
 
 struct LayerParams {

@@ -54,6 +54,13 @@ _SIGS = {
     "dh_attn_bwd": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
                     c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_int, c_int, c_int,
                     c_int, c_float, c_void_p],
+    "dh_attn_fwd_scratch_floats_ex": [c_int, c_int, c_int, c_int, c_int, c_int],
+    "dh_attn_bwd_scratch_floats": [c_int, c_int, c_int, c_int],
+    "dh_attn_fwd_ex": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
+                       c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_float, c_void_p],
+    "dh_attn_bwd_ex": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
+                       c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_int, c_int, c_int, c_int, c_int,
+                       c_int, c_float, c_void_p],
     "dh_adamw": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_ll, c_float, c_float,
                  c_float, c_float, c_float, c_int, c_float, c_int, c_void_p],
     "dh_init_normal": [c_void_p, c_void_p, c_ll, c_ull, c_float, c_void_p],
@@ -89,6 +96,8 @@ def lib():
             fn.restype = c_int
         l.dh_last_error.restype = ctypes.c_char_p
         l.dh_attn_fwd_scratch_floats.restype = c_ll
+        l.dh_attn_fwd_scratch_floats_ex.restype = c_ll
+        l.dh_attn_bwd_scratch_floats.restype = c_ll
         if hasattr(l, "dh_moe_router_bwd_scratch_floats"):
             l.dh_moe_router_bwd_scratch_floats.restype = c_ll
         _lib = l
@@ -200,6 +209,31 @@ def attn_bwd(q, k, v, o, lse, do, dq, dk, dv, n_q_heads, n_kv_heads, head_dim, s
                             o.stride(0), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv),
                             dq.stride(0), dk.stride(0), _ptr(scratch), tokens, n_q_heads,
                             n_kv_heads, head_dim, scale, _stream(stream)))
+
+
+def attn_fwd_cp(q, k, v, o, lse, q_offset, n_q_heads, n_kv_heads, head_dim, scale, stream=None):
+    """Context-parallel forward: q rows at global positions [q_offset, q_offset + len(q))
+    against every key row of k / v (causal)."""
+    import torch
+    tq, tk = q.shape[0], k.shape[0]
+    n = int(lib().dh_attn_fwd_scratch_floats_ex(tq, n_q_heads, n_kv_heads, head_dim, tk, q_offset))
+    scratch = torch.empty(max(n, 1), dtype=torch.float32, device=q.device) if n else None
+    check(lib().dh_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o), o.stride(0),
+                               _ptr(lse), _ptr(scratch) if n else None, n, tq, tk, q_offset, n_q_heads,
+                               n_kv_heads, head_dim, scale, _stream(stream)))
+
+
+def attn_bwd_cp(q, k, v, o, lse, do, dq, dk, dv, q_offset, n_q_heads, n_kv_heads, head_dim, scale, stream=None):
+    """Context-parallel backward: dq for the local rows, dk / dv for every key row
+    (the gradient from these queries only)."""
+    import torch
+    tq, tk = q.shape[0], k.shape[0]
+    scratch = torch.empty(int(lib().dh_attn_bwd_scratch_floats(tq, n_q_heads, head_dim, tk)), dtype=torch.float32,
+                          device=q.device)
+    check(lib().dh_attn_bwd_ex(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o), o.stride(0),
+                               _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv), dq.stride(0), dk.stride(0),
+                               _ptr(scratch), tq, tk, q_offset, n_q_heads, n_kv_heads, head_dim, scale,
+                               _stream(stream)))
 
 
 def adamw(master, weight, grad, m, v, lr, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0, step=1,

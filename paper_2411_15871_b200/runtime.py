@@ -22,7 +22,7 @@ class ModelCfg(ctypes.Structure):
                 ("micro_batches", c_int), ("rope_theta", c_float), ("norm_eps", c_float),
                 ("seed", ctypes.c_ulonglong), ("init_std", c_float),
                 ("slots", c_int), ("split_layer", c_int), ("pp_rank", c_int), ("pp_size", c_int),
-                ("experts", c_int), ("topk", c_int), ("capacity", c_int)]
+                ("experts", c_int), ("topk", c_int), ("capacity", c_int), ("context_parallel", c_int)]
 
 
 class OptimCfg(ctypes.Structure):
@@ -184,6 +184,8 @@ class LlamaShape:
     experts: int = 0
     topk: int = 0
     capacity: int = 0
+    # context parallelism: 1 = the context's group is the CP group (TP = 1)
+    context_parallel: int = 0
 
     @property
     def moe(self) -> bool:
@@ -193,7 +195,8 @@ class LlamaShape:
         return ModelCfg(self.hidden, self.ffn, self.n_heads, self.n_kv_heads, self.head_dim,
                         self.layers, self.seq_len, self.micro_batches, self.rope_theta,
                         self.norm_eps, self.seed, self.init_std, self.slots, self.split_layer,
-                        self.pp_rank, self.pp_size, self.experts, self.topk, self.capacity)
+                        self.pp_rank, self.pp_size, self.experts, self.topk, self.capacity,
+                        self.context_parallel)
 
     def planner_model(self) -> dict:
         if self.moe:

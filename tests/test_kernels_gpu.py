@@ -325,3 +325,38 @@ def test_add_rmsnorm_fused_equals_add_then_norm(rows, cols):
     dh.add_rmsnorm_fwd(x, r, x2, g, y2, s2)
     torch.cuda.synchronize()
     assert torch.equal(x1, x2) and torch.equal(y1, y2) and torch.equal(s1, s2)
+
+
+@pytest.mark.parametrize("T,cp,rank,nq,nkv,d", [(1024, 2, 1, 4, 2, 128), (2048, 4, 2, 4, 1, 128),
+                                                 (2048, 4, 3, 8, 2, 64), (4096, 8, 5, 4, 1, 128),
+                                                 (1024, 4, 0, 2, 2, 64)])
+def test_attention_context_parallel_chunk(T, cp, rank, nq, nkv, d):
+    """Context parallelism (cp_kv_exchange path): one rank's query chunk at
+    global offset rank * T / cp against every key (dh_attn_fwd_ex / _bwd_ex)
+    equals the same rows of the full causal attention, and its dK/dV are the
+    gradient from these queries only (checked against torch autograd with the
+    other chunks' queries detached)."""
+    scale = d ** -0.5
+    tl = T // cp
+    off = rank * tl
+    qkv = (torch.randn(T, (nq + 2 * nkv) * d, device="cuda") * 0.5).to(torch.bfloat16)
+    q_all, k, v = qkv[:, :nq * d], qkv[:, nq * d:(nq + nkv) * d], qkv[:, (nq + nkv) * d:]
+    q = q_all[off:off + tl]
+    o = torch.empty(tl, nq * d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nq, tl, device="cuda")
+    dh.attn_fwd_cp(q, k, v, o, lse, off, nq, nkv, d, scale)
+    qf, kf, vf = (t.float().requires_grad_() for t in (q_all, k, v))
+    o_ref, lse_ref = _attn_ref(qf, kf, vf, nq, nkv, d, scale)
+    assert _rel(o, o_ref[off:off + tl]) < 6e-3
+    assert (lse - lse_ref[:, off:off + tl]).abs().max().item() < 2e-3
+    do = torch.randn_like(o)
+    o_ref[off:off + tl].backward(do.float())
+    dq = torch.empty(tl, nq * d, device="cuda", dtype=torch.bfloat16)
+    dkv = torch.empty(T, 2 * nkv * d, device="cuda", dtype=torch.bfloat16)
+    dk, dv = dkv[:, :nkv * d], dkv[:, nkv * d:]
+    dh.attn_bwd_cp(q, k, v, o, lse, do, dq, dk, dv, off, nq, nkv, d, scale)
+    assert _rel(dq, qf.grad[off:off + tl]) < 1e-2
+    assert _rel(dk, kf.grad) < 1e-2
+    assert _rel(dv, vf.grad) < 1e-2
+    if off + tl < T:  # keys after the chunk's last query get no gradient from it
+        assert dk[off + tl:].abs().max().item() == 0 and dv[off + tl:].abs().max().item() == 0
