@@ -26,8 +26,9 @@ for r in rows[start + 1:]:
     unit = r[h.index("Metric Unit")]
     key = (r[h.index("ID")], name)
     v = float(val.replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0,
-             "Gbyte": 1e3}.get(unit, 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+             "byte": 1e-6, "B": 1e-6, "Kbyte": 1e-3, "KB": 1e-3, "Mbyte": 1.0, "MB": 1.0, "Gbyte": 1e3,
+             "GB": 1e3}.get(unit, 1.0)
     kern.setdefault(key, {})[metric] = v * scale
 match = {"rmsnorm_fwd": "rmsnorm_fwd", "rmsnorm_bwd": "rmsnorm_bwd", "add_kernel": "add", "swiglu_fwd": "swiglu_fwd",
          "swiglu_bwd": "swiglu_bwd", "rope": "rope", "adamw": "adamw"}
@@ -35,6 +36,8 @@ print(f"HBM-bound kernels, TP=1 Llama-3-8B shapes, one launch each, ncu --clock-
       f"peak {pk} GB/s (MEASURED_PEAKS.json hbm_gbs)")
 print(f"{'kernel':45s} {'us':>8s} {'algo MB':>9s} {'algo GB/s':>10s} {'frac':>6s} {'dram MB':>9s}")
 for (kid, name), m in kern.items():
+    if "dh::" not in name:  # torch's input initialisation
+        continue
     base = next((v for k, v in match.items() if k in name), None)
     us = m.get("gpu__time_duration.sum", 0.0)
     dram = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
