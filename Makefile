@@ -49,7 +49,7 @@ $(LIB)/libweft_b200.so: $(PLANNER_OBJ)
 
 $(OBJ)/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(CUDA_HDR)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(NVFLAGS) -c $< -o $@
+	$(NVCC) $(NVFLAGS) $(NVFLAGS_EXTRA) -c $< -o $@
 
 $(OBJ)/runtime/%.o: $(PKG)/csrc/runtime/%.cpp $(CUDA_HDR) $(wildcard include/weft/*.hpp) \
                     $(wildcard $(PKG)/csrc/runtime/*.hpp) $(PKG)/csrc/planner/lane_sim.hpp

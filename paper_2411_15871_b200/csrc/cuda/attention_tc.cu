@@ -630,58 +630,70 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
 
 // ===========================================================================
 // Backward (attn_bwd node): one launch, two deterministic tcgen05 work kinds.
+// Every MMA has N >= 128: at M = 128 a tcgen05.mma with N = 64 takes ~51
+// cycles per K = 16 step against 64 at N = 128 (tools/micro/mma_rate.cu on
+// B200: N = 32 / 64 reach 0.31 / 0.62 of the dense rate, N >= 128 1.00), so
+// both kinds use 128-row tiles and single-buffered S / dP in TMEM, with the
+// MMA issue order arranged so the tensor pipe never waits on the elementwise
+// warps in steady state (see each body).
 //
-// dK/dV item — one CTA per (128-key block, q head); inner q tiles of 64:
-//   S^T  = K Q^T        M128 N64  K128   A=K (smem)      B=Q (smem, K-major)
-//   dP^T = V dO^T       M128 N64  K128   A=V (smem)      B=dO (smem, K-major)
+// dK/dV item — one CTA per (128-key block, q head); inner q tiles of 128:
+//   S^T  = K Q^T        M128 N128 K=D   A=K (smem)      B=Q (smem, K-major)
+//   dP^T = V dO^T       M128 N128 K=D   A=V (smem)      B=dO (smem, K-major)
 //   P^T = exp(scale S^T - lse_q), dS^T = P^T (dP^T - D_q)      (thread = key row)
-//   dV  += P^T dO       M128 N128 K64    A=P^T (TMEM)    B=dO (smem, MN-major)
-//   dK  += dS^T Q       M128 N128 K64    A=dS^T (TMEM)   B=Q  (smem, MN-major)
-//   TMEM: S^T x2 (64) | dP^T x2 (64) | dV (128) | dK (128) = 512 columns;
-//   P^T / dS^T (bf16 pairs) overwrite the fp32 S^T / dP^T columns of the half
-//   of the q tile they come from (columns [32 h, 32 h + 16) for half h), so the
-//   elementwise results never pass through shared memory and the two halves of
-//   the elementwise warps never write columns the other reads (no barrier).
-// dQ item — one CTA per (128-query block, q head); inner key tiles of 64:
-//   S = Q K^T, dP = dO V^T (M128 N64 K128), dS = P (dP - D)    (thread = query row)
-//   dQ += dS K          M128 N128 K64    A=dS (TMEM)     B=K (smem, MN-major)
-//   TMEM: S x2 | dP x2 | dQ = 384 columns.
-// S/dP buffers are double-buffered: the MMA warp computes tile it+1 while the
-// elementwise warps work on tile it. No atomics: dQ is produced by its own
-// items and per-head dK/dV partials of a GQA group are reduced in head order
-// by attn_bwd_group_reduce (attention.cu).
+//   dV  += P^T dO       M128 N=D K128   A=P^T (TMEM)    B=dO (smem, MN-major)
+//   dK  += dS^T Q       M128 N=D K128   A=dS^T (TMEM)   B=Q  (smem, MN-major)
+//   TMEM: S^T (128) | dP^T (128) | dV (D) | dK (D); P^T / dS^T (bf16 pairs)
+//   overwrite the first 32 columns of each 64-column half of S^T / dP^T that
+//   the same threads read (no cross-thread hazard).
+//   Issue order: S(0) dP(0) | dV(i) S(i+1) dK(i) dP(i+1) | ... — the softmax
+//   exponentials of tile i+1 run under dK(i) and dP(i+1), dS(i) under dV(i)
+//   and S(i+1).
+// dQ item — one CTA per (128-query block, q head); inner key tiles of 128:
+//   S = Q K^T, dP = dO V^T (M128 N128 K=D, A = Q / dO resident in TMEM),
+//   dS = P (dP - D)    (thread = query row)
+//   dQ += dS K          M128 N=D K128   A=dS (TMEM)     B=K (smem, MN-major)
+//   TMEM: S (128) | dP (128) | dQ (D) | Q (D/2) | dO (D/2).
+//   Issue order: S(0) dP(0) | S(i+1) dQ(i) dP(i+1) | ... — S(i+1) is issued as
+//   soon as the elementwise warps have read S(i) into registers.
+// No atomics: dQ is produced by its own items and per-head dK/dV partials of a
+// GQA group are reduced in head order by attn_bwd_group_reduce (attention.cu).
 // ===========================================================================
 
 namespace dh {
 namespace {
 
-constexpr int BT64 = 64;
-constexpr int kHalf64 = BT64 * 64 * 2;  // 8 KB: one d-half of a 64-row tile
-constexpr int kStages = 4;              // Q/dO (dK/dV items) or K/V (dQ items) ring
-
+// The Q ring is one stage deeper than the dO ring: a Q slot is refilled after
+// dK(i) and read again by S^T(i + kQS), so at D = 128 (three Q stages, two dO
+// stages, 227 KB exactly) every refill has five to six MMAs (> 2.5k cycles) to
+// land. Small vectors and barriers come first, the 1024-aligned tiles after
+// them: this layout needs a 1024-aligned dynamic shared memory base (checked).
 template <int D>
 struct KvSmem {
-    static constexpr int kTile = tile_bytes<D>();        // 128-row K / V tile
-    static constexpr int kTile64 = BT64 * D * 2;         // 64-row tile: [D/64 d-halves][64 rows][128 B]
-    static constexpr int k = 0;
+    static constexpr int kTile = tile_bytes<D>();         // 128-row tile
+    static constexpr int kQS = D == 128 ? 3 : 4;          // Q ring stages (+ lse rows)
+    static constexpr int kOS = D == 128 ? 2 : 4;          // dO ring stages (+ D rows)
+    static constexpr int lse = 0;                         // [kQS][128] fp32 (raw lse)
+    static constexpr int dvec = lse + kQS * 512;          // [kOS][128] fp32
+    static constexpr int bars = dvec + kOS * 512;
+    static constexpr int k = (bars + 256 + 1023) / 1024 * 1024;
     static constexpr int v = k + kTile;
-    static constexpr int q = v + kTile;                  // kStages 64-row tiles
-    static constexpr int dout = q + kStages * kTile64;   // kStages 64-row tiles
-    static constexpr int vec = dout + kStages * kTile64; // per stage: lse[64], D[64] (raw)
-    static constexpr int bars = vec + kStages * 128 * 4;
-    static constexpr int total = bars + 256 + 1024;
+    static constexpr int q = v + kTile;                   // kQS tiles
+    static constexpr int dout = q + kQS * kTile;          // kOS tiles
+    static constexpr int total = dout + kOS * kTile;
 };
 
-constexpr int kDqStages = 6;  // K/V ring of the dQ items (Q and dO live in TMEM)
 template <int D>
 struct DqSmem {
-    static constexpr int kTile64 = BT64 * D * 2;
-    static constexpr int k = 0;                          // kDqStages 64-row tiles
-    static constexpr int v = k + kDqStages * kTile64;    // kDqStages 64-row tiles
-    static constexpr int bars = v + kDqStages * kTile64;
+    static constexpr int kTile = tile_bytes<D>();
+    static constexpr int kSt = D == 128 ? 3 : 6;          // K/V ring stages (Q and dO live in TMEM)
+    static constexpr int k = 0;                           // kSt tiles
+    static constexpr int v = k + kSt * kTile;             // kSt tiles
+    static constexpr int bars = v + kSt * kTile;
     static constexpr int total = bars + 256 + 1024;
 };
 static_assert(KvSmem<128>::total <= 232448 && DqSmem<128>::total <= 232448, "backward smem exceeds the sm_100 limit");
+static_assert(KvSmem<64>::total <= 232448 && DqSmem<64>::total <= 232448, "backward smem exceeds the sm_100 limit");
 
 struct BwdParams {
     const __nv_bfloat16* q;     // raw rows for the TMEM-resident Q / dO of the dQ items
@@ -701,42 +713,79 @@ struct BwdParams {
     int qo;         // query offset in 128-blocks (context parallelism), even
 };
 
-// K-major 64-row tile (one 64-wide K atom per half): k-step kk over d (0..7).
-__device__ __forceinline__ uint64_t desc_k64(uint32_t base, int kk) {
-    return umma_desc_sw128(base + (kk >> 2) * kHalf64 + (kk & 3) * 32, 16, 1024);
-}
-// MN-major 64-row tile used as B with N = d: k-step kk over rows (0..3).
-__device__ __forceinline__ uint64_t desc_mn64(uint32_t base, int kk) {
-    return umma_desc_sw128(base + kk * 2048, kHalf64, 1024);
+constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
+
+// A operand from TMEM (bf16 pairs) for k-step kk (16 rows of the 128-wide
+// tile): each 64-column half of the fp32 tile holds its 64 values packed
+// into its first 32 columns.
+__device__ __forceinline__ uint32_t packed_col(int kk) { return (kk >> 2) * 64 + (kk & 3) * 8; }
+
+// 64 fp32 columns [c0, c0 + 64) of this warp's TMEM lane quadrant.
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+    tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+    tmem_ld_wait();
 }
 
-constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
+// p = 2^(s * scale_log2 + bias), bias per column (-log2e lse_j, PER_COL) or
+// per row; half of the pairs on the FMA pipe (the MUFU alone would need
+// 16384 / 16 = 1024 cycles per 128 x 128 tile).
+template <bool PER_COL>
+__device__ __forceinline__ void bwd_exp64(uint32_t (&s)[64], const float* bias, float bias_row, float scale_log2) {
+    const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        uint64_t b2;
+        if constexpr (PER_COL) {  // bias = raw lse of the columns (smem): -log2e * lse
+            const float2 l2 = reinterpret_cast<const float2*>(bias)[u];
+            b2 = ffma2(f2_pack(l2.x, l2.y), f2_pack(-kLog2e, -kLog2e), 0ull);
+        } else {
+            b2 = f2_pack(bias_row, bias_row);
+        }
+        const uint64_t x = ffma2(f2_pack(__uint_as_float(s[2 * u]), __uint_as_float(s[2 * u + 1])), sc2, b2);
+        float x0, x1;
+        f2_unpack(x, x0, x1);
+        float e0, e1;
+        if (DH_ATTN_POLY && (u & 1)) {
+            f2_unpack(exp2_fma2(x0, x1), e0, e1);
+        } else {
+            e0 = fast_exp2(x0);
+            e1 = fast_exp2(x1);
+        }
+        s[2 * u] = __float_as_uint(e0);
+        s[2 * u + 1] = __float_as_uint(e1);
+    }
+}
 
 template <int D>
 __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                    const CUtensorMap& tm_q, const CUtensorMap& tm_do,
                                                    const BwdParams& p, const int kb, const int h) {
-    using KvSmem = dh::KvSmem<D>;
-    constexpr int kTile = KvSmem::kTile, kTile64 = KvSmem::kTile64;
+    using Smem = dh::KvSmem<D>;
+    constexpr int kTile = Smem::kTile, kQS = Smem::kQS, kOS = Smem::kOS;
     extern __shared__ uint8_t smem_raw[];
-    // offset arithmetic on the __shared__ array keeps the pointer in the shared
-    // space (plain loads compile to LDS rather than generic LD)
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + KvSmem::bars);
+    uint8_t* sm = smem_raw;  // 1024-aligned (see KvSmem)
+    if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u)) __trap();
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Smem::bars);
     uint64_t* kv_full = bars + 0;
-    uint64_t* q_full = bars + 1;                // [kStages] Q/dO ring
-    uint64_t* q_empty = q_full + kStages;       // [kStages]
-    uint64_t* s_full = q_empty + kStages;       // [2] TMEM S^T/dP^T buffers
-    uint64_t* p_full = s_full + 2;              // P^T/dS^T of the current tile in TMEM
-    uint64_t* acc_done = p_full + 1;            // dK/dV complete
+    uint64_t* q_full = bars + 1;                // [kQS] Q ring (+ lse)
+    uint64_t* q_empty = q_full + kQS;           // [kQS]
+    uint64_t* o_full = q_empty + kQS;           // [kOS] dO ring (+ D)
+    uint64_t* o_empty = o_full + kOS;           // [kOS]
+    uint64_t* s_full = o_empty + kOS;           // S^T in TMEM
+    uint64_t* dp_full = s_full + 1;             // dP^T in TMEM
+    uint64_t* p_full = dp_full + 1;             // P^T (bf16) in TMEM
+    uint64_t* ds_full = p_full + 1;             // dS^T (bf16) in TMEM
+    uint64_t* acc_done = ds_full + 1;           // dK/dV complete
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
-    float* vec = reinterpret_cast<float*>(sm + KvSmem::vec);  // [stage][lse 64 | D 64]
+    float* lse_s = reinterpret_cast<float*>(sm + Smem::lse);    // [kQS][128]
+    float* dvec_s = reinterpret_cast<float*>(sm + Smem::dvec);  // [kOS][128]
 
     const int kvh = h / p.group;
-    const int nq64 = (p.T + BT64 - 1) / BT64;
+    const int nq128 = (p.T + BQ - 1) / BQ;
     // first local q tile with a query at or after the block's first key
-    const int i0 = max(0, (kb - p.qo) * BKV / BT64);
-    const int n_it = max(0, nq64 - i0);
+    const int i0 = max(0, kb - p.qo);
+    const int n_it = max(0, nq128 - i0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -745,12 +794,18 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
         mbar_init(kv_full, 1);
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < kQS; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
+        for (int i = 0; i < kOS; ++i) {
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(dp_full, 1);
         mbar_init(p_full, 256);
+        mbar_init(ds_full, 256);
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -759,80 +814,99 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384;
-    const bool bulk_vec = (p.T % BT64) == 0;  // lse / D rows fetched by bulk copy
+    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+    const bool bulk_vec = (p.T % BQ) == 0;  // lse / D rows fetched by bulk copy
 
     if (warp == 0) {
         if (lane == 0) {
             mbar_expect_tx(kv_full, 2 * kTile);
 #pragma unroll
             for (int hh = 0; hh < D / 64; ++hh) {
-                tma_load_2d(sm + KvSmem::k + hh * kHalf, &tm_k, kv_full, kvh * D + 64 * hh, kb * BKV);
-                tma_load_2d(sm + KvSmem::v + hh * kHalf, &tm_v, kv_full, kvh * D + 64 * hh, kb * BKV);
+                tma_load_2d(sm + Smem::k + hh * kHalf, &tm_k, kv_full, kvh * D + 64 * hh, kb * BKV);
+                tma_load_2d(sm + Smem::v + hh * kHalf, &tm_v, kv_full, kvh * D + 64 * hh, kb * BKV);
             }
             for (int it = 0; it < n_it; ++it) {
-                const int st = it % kStages, qi = i0 + it;
-                mbar_wait(&q_empty[st], ((it / kStages) & 1) ^ 1);
-                mbar_expect_tx(&q_full[st], 2 * kTile64 + (bulk_vec ? 512 : 0));
-                if (bulk_vec) {
-                    const long long off = static_cast<long long>(h) * p.T + qi * BT64;
-                    bulk_load_1d(vec + st * 128, p.lse + off, 256, &q_full[st]);
-                    bulk_load_1d(vec + st * 128 + 64, p.dvec + off, 256, &q_full[st]);
-                }
-                uint8_t* qd = sm + KvSmem::q + st * kTile64;
-                uint8_t* od = sm + KvSmem::dout + st * kTile64;
+                const int qs = it % kQS, os = it % kOS, qi = i0 + it;
+                const long long off = static_cast<long long>(h) * p.T + qi * BQ;
+                mbar_wait(&q_empty[qs], ((it / kQS) & 1) ^ 1);
+                mbar_expect_tx(&q_full[qs], kTile + (bulk_vec ? 512 : 0));
+                if (bulk_vec) bulk_load_1d(lse_s + qs * 128, p.lse + off, 512, &q_full[qs]);
 #pragma unroll
-                for (int hh = 0; hh < D / 64; ++hh) {
-                    tma_load_2d(qd + hh * kHalf64, &tm_q, &q_full[st], h * D + 64 * hh, qi * BT64);
-                    tma_load_2d(od + hh * kHalf64, &tm_do, &q_full[st], h * D + 64 * hh, qi * BT64);
-                }
+                for (int hh = 0; hh < D / 64; ++hh)
+                    tma_load_2d(sm + Smem::q + qs * kTile + hh * kHalf, &tm_q, &q_full[qs], h * D + 64 * hh, qi * BQ);
+                mbar_wait(&o_empty[os], ((it / kOS) & 1) ^ 1);
+                mbar_expect_tx(&o_full[os], kTile + (bulk_vec ? 512 : 0));
+                if (bulk_vec) bulk_load_1d(dvec_s + os * 128, p.dvec + off, 512, &o_full[os]);
+#pragma unroll
+                for (int hh = 0; hh < D / 64; ++hh)
+                    tma_load_2d(sm + Smem::dout + os * kTile + hh * kHalf, &tm_do, &o_full[os], h * D + 64 * hh,
+                                qi * BQ);
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
+        constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);
         constexpr uint32_t id_g = umma_idesc_bf16(128, D, false, true);
-        const uint32_t k_addr = smem_u32(sm + KvSmem::k), v_addr = smem_u32(sm + KvSmem::v);
-        auto issue_s = [&](int it) {
-            const int qs = it % kStages, sb = it & 1;  // smem ring stage, TMEM buffer
-            mbar_wait(&q_full[qs], (it / kStages) & 1);
+        const uint32_t k_addr = smem_u32(sm + Smem::k), v_addr = smem_u32(sm + Smem::v);
+        auto q_addr = [&](int it) { return smem_u32(sm + Smem::q + (it % kQS) * kTile); };
+        auto o_addr = [&](int it) { return smem_u32(sm + Smem::dout + (it % kOS) * kTile); };
+        auto issue_s = [&](int it) {  // S^T(it) = K Q(it)^T
+            mbar_wait(&q_full[it % kQS], (it / kQS) & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t q_addr = smem_u32(sm + KvSmem::q + qs * kTile64);
-                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + qs * kTile64);
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    tc_mma_bf16(t_s + sb * 64, desc_kmajor(k_addr, kk), desc_k64(q_addr, kk), id_s, kk > 0);
-                    tc_mma_bf16(t_dp + sb * 64, desc_kmajor(v_addr, kk), desc_k64(o_addr, kk), id_s, kk > 0);
-                }
-                tc_commit(&s_full[sb]);
+                for (int kk = 0; kk < D / 16; ++kk)
+                    tc_mma_bf16(t_s, desc_kmajor(k_addr, kk), desc_kmajor(q_addr(it), kk), id_s, kk > 0);
+                tc_commit(s_full);
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int it) {  // dP^T(it) = V dO(it)^T
+            mbar_wait(&o_full[it % kOS], (it / kOS) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    tc_mma_bf16(t_dp, desc_kmajor(v_addr, kk), desc_kmajor(o_addr(it), kk), id_s, kk > 0);
+                tc_commit(dp_full);
             }
             __syncwarp();
         };
         mbar_wait(kv_full, 0);
-        if (n_it > 0) issue_s(0);
+        if (n_it > 0) {
+            issue_s(0);
+            issue_dp(0);
+        }
         for (int it = 0; it < n_it; ++it) {
-            const int sb = it & 1, qs = it % kStages;
-            // S^T/dP^T(it+1) go into the other buffer, whose P^T/dS^T were
-            // consumed by the dV/dK MMAs of it-1 (issued before, in order).
-            if (it + 1 < n_it) issue_s(it + 1);
+            // dV += P^T(it) dO(it)
             if (lane == 0) ATR(it * 8 + 0);
             mbar_wait(p_full, it & 1);
             if (lane == 0) ATR(it * 8 + 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t q_addr = smem_u32(sm + KvSmem::q + qs * kTile64);
-                const uint32_t o_addr = smem_u32(sm + KvSmem::dout + qs * kTile64);
 #pragma unroll
-                for (int kk = 0; kk < BT64 / 16; ++kk) {
-                    // P^T / dS^T: q columns [32 h, 32 h + 32) packed at column 32 h (see below)
-                    const uint32_t pc = (kk >> 1) * 32 + (kk & 1) * 8;
-                    tc_mma_bf16_ts(t_dv, t_s + sb * 64 + pc, desc_mn64(o_addr, kk), id_g, (it | kk) != 0);
-                    tc_mma_bf16_ts(t_dk, t_dp + sb * 64 + pc, desc_mn64(q_addr, kk), id_g, (it | kk) != 0);
-                }
-                tc_commit(&q_empty[qs]);
+                for (int kk = 0; kk < BQ / 16; ++kk)
+                    tc_mma_bf16_ts(t_dv, t_s + packed_col(kk), desc_mnmajor(o_addr(it), kk), id_g, (it | kk) != 0);
+            }
+            __syncwarp();
+            // S^T(it+1) overwrites P^T(it): the dV MMAs above were issued first
+            if (it + 1 < n_it) issue_s(it + 1);
+            // dK += dS^T(it) Q(it)
+            mbar_wait(ds_full, it & 1);
+            if (lane == 0) ATR(it * 8 + 2);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk)
+                    tc_mma_bf16_ts(t_dk, t_dp + packed_col(kk), desc_mnmajor(q_addr(it), kk), id_g, (it | kk) != 0);
+                // dK(it) is the last reader of Q(it) and of the lse / D rows the
+                // elementwise warps used (they arrived on ds_full first)
+                tc_commit(&q_empty[it % kQS]);
+                tc_commit(&o_empty[it % kOS]);
                 if (it + 1 == n_it) tc_commit(acc_done);
             }
             __syncwarp();
+            // dP^T(it+1) overwrites dS^T(it): the dK MMAs above were issued first
+            if (it + 1 < n_it) issue_dp(it + 1);
         }
     } else {
         // 8 warps: quadrant (TMEM lanes) = warp & 3, column half = (warp - 2) >> 2
@@ -842,72 +916,76 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         const int key = kb * BKV + r;
         const int t_sm = threadIdx.x - 64;  // 0..255 among the elementwise warps
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        const uint32_t col = lane_off + half * 64;
         const int key_hi = kb * BKV + BKV - 1;
-        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), m1 = f2_pack(-1.f, -1.f);
-        const uint64_t nl2e = f2_pack(-kLog2e, -kLog2e);
         for (int it = 0; it < n_it; ++it) {
-            const int sb = it & 1, qi = i0 + it;
+            const int qi = i0 + it;
+            float* sl = lse_s + (it % kQS) * 128;
+            float* sd = dvec_s + (it % kOS) * 128;
             if (!bulk_vec) {
-                // ragged T: stage the vectors with plain loads (s_full implies q_full)
-                named_barrier(1, 256);  // previous readers of this stage are done
-                if (t_sm < BT64) {
-                    const int q = qi * BT64 + t_sm;
-                    vec[(it % kStages) * 128 + t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] : 0.f;
-                    vec[(it % kStages) * 128 + 64 + t_sm] =
-                        q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
+                // ragged T: stage the vectors with plain loads
+                named_barrier(1, 256);  // previous readers of these slots are done
+                if (t_sm < BQ) {
+                    const int q = qi * BQ + t_sm;
+                    sl[t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] : 0.f;
+                    sd[t_sm] = q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
                 }
                 named_barrier(1, 256);
             }
-            if (threadIdx.x == 64) ATR(it * 8 + 2);
-            mbar_wait(&s_full[sb], (it >> 1) & 1);
+            // whole tile causal-visible and in range: no per-element masking
+            const int qg0 = (p.qo + qi) * BQ;  // global position of the tile's first query
+            const bool full_tile = qg0 >= key_hi && qi * BQ + BQ <= p.T && key_hi < p.T_kv;
+            // ---- P^T = exp2(scale_log2 S^T - log2e lse_q)
+            if (threadIdx.x == 64) ATR(it * 8 + 7);
+            mbar_wait(s_full, it & 1);
             if (threadIdx.x == 64) ATR(it * 8 + 3);
             tc_fence_after();
-            uint32_t a[32], b[32];
-            tmem_ld32(t_s + sb * 64 + lane_off + half * 32, a);
-            tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
-            tmem_ld_wait();
-            if (threadIdx.x == 64) ATR(it * 8 + 5);
-            if (threadIdx.x == 64) ATR(it * 8 + 6);
-            // whole tile causal-visible and in range: no per-element masking
-            const int qg0 = p.qo * BQ + qi * BT64;  // global position of the tile's first query
-            const bool full_tile = qg0 >= key_hi && qi * BT64 + BT64 <= p.T && key_hi < p.T_kv;
-            const float2* lv = reinterpret_cast<const float2*>(vec + (it % kStages) * 128 + half * 32);
-            const float2* dv2 = reinterpret_cast<const float2*>(vec + (it % kStages) * 128 + 64 + half * 32);
-            uint32_t pp[16], pd[16];
+            uint32_t pv[64];
+            tmem_ld64(t_s + col, pv);
+            bwd_exp64<true>(pv, sl + half * 64, 0.f, p.scale_log2);
+            if (!full_tile) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const float2 l2 = lv[u], d2 = dv2[u];
-                // x = scale_log2 * s - log2e * lse
-                const uint64_t x = ffma2(f2_pack(__uint_as_float(a[2 * u]), __uint_as_float(a[2 * u + 1])), sc2,
-                                         ffma2(f2_pack(l2.x, l2.y), nl2e, 0ull));
-                float x0, x1;
-                f2_unpack(x, x0, x1);
-                float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
-                if (!full_tile) {
-                    const int q = qi * BT64 + half * 32 + 2 * u;  // local row; global position q + qo * BQ
-                    const int qg = q + p.qo * BQ;
-                    if (qg < key || q >= p.T || key >= p.T_kv) e0 = 0.f;
-                    if (qg + 1 < key || q + 1 >= p.T || key >= p.T_kv) e1 = 0.f;
+                for (int j = 0; j < 64; ++j) {
+                    const int q = qi * BQ + half * 64 + j;  // local row; global position q + qo * BQ
+                    if (q + p.qo * BQ < key || q >= p.T || key >= p.T_kv) pv[j] = 0u;
                 }
-                const uint64_t e = f2_pack(e0, e1);
-                // dS^T = P^T (dP^T - D)
-                const uint64_t ds = ffma2(e, ffma2(f2_pack(d2.x, d2.y), m1,
-                                                   f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1]))),
-                                          0ull);
-                float s0, s1;
-                f2_unpack(ds, s0, s1);
-                pp[u] = pack2(e0, e1);
-                pd[u] = pack2(s0, s1);
             }
-            if (threadIdx.x == 64) ATR(it * 8 + 7);
-            // each half packs its bf16 pairs over the start of the fp32 columns it
-            // read itself, so no half overwrites columns the other still reads
-            tmem_st16(t_s + sb * 64 + lane_off + half * 32, pp);
-            tmem_st16(t_dp + sb * 64 + lane_off + half * 32, pd);
+            {
+                uint32_t pp[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) pp[u] = pack2(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1]));
+                tmem_st32(t_s + col, pp);
+            }
             tmem_st_wait();
             tc_fence_before();
             if (threadIdx.x == 64) ATR(it * 8 + 4);
             mbar_arrive(p_full);
+            // ---- dS^T = P^T (dP^T - D_q), in two 32-column chunks
+            mbar_wait(dp_full, it & 1);
+            if (threadIdx.x == 64) ATR(it * 8 + 5);
+            tc_fence_after();
+            {
+                uint32_t b[64];
+                tmem_ld64(t_dp + col, b);
+                const float2* d2 = reinterpret_cast<const float2*>(sd + half * 64);
+                uint32_t pd[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const float2 dd = d2[u];
+                    const uint64_t ds = ffma2(
+                        f2_pack(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1])),
+                        fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), f2_pack(-dd.x, -dd.y)),
+                        0ull);
+                    float s0, s1;
+                    f2_unpack(ds, s0, s1);
+                    pd[u] = pack2(s0, s1);
+                }
+                tmem_st32(t_dp + col, pd);  // over the first 32 columns of this half (read above)
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            if (threadIdx.x == 64) ATR(it * 8 + 6);
+            mbar_arrive(ds_full);
         }
         if (n_it > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
@@ -963,39 +1041,40 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
 }
 
 template <int D>
-__device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const CUtensorMap& tm_do,
-                                                 const CUtensorMap& tm_k, const CUtensorMap& tm_v,
+__device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                  const BwdParams& p, const int qb, const int h) {
-    using DqSmem = dh::DqSmem<D>;
-    constexpr int kTile64 = DqSmem::kTile64;
+    using Smem = dh::DqSmem<D>;
+    constexpr int kTile = Smem::kTile, kSt = Smem::kSt;
     extern __shared__ uint8_t smem_raw[];
-    // offset arithmetic on the __shared__ array keeps the pointer in the shared
-    // space (plain loads compile to LDS rather than generic LD)
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DqSmem::bars);
-    uint64_t* q_full = bars + 0;               // Q / dO rows stored into TMEM
-    uint64_t* kv_full = bars + 1;              // [kDqStages] K/V ring
-    uint64_t* kv_empty = kv_full + kDqStages;  // [kDqStages]
-    uint64_t* s_full = kv_empty + kDqStages;   // [2]
-    uint64_t* p_full = s_full + 2;
-    uint64_t* acc_done = p_full + 1;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Smem::bars);
+    uint64_t* q_full = bars + 0;           // Q / dO rows stored into TMEM
+    uint64_t* kv_full = bars + 1;          // [kSt] K/V ring
+    uint64_t* kv_empty = kv_full + kSt;    // [kSt]
+    uint64_t* s_full = kv_empty + kSt;
+    uint64_t* dp_full = s_full + 1;
+    uint64_t* s_free = dp_full + 1;        // S read into registers
+    uint64_t* ds_full = s_free + 1;        // dS (bf16) in TMEM
+    uint64_t* acc_done = ds_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
     const int kvh = h / p.group;
     // key tiles 0 .. covering the block's last query (global position)
-    const int n_it = min((p.qo * BQ + qb * BQ + BQ) / BT64, (p.T_kv + BT64 - 1) / BT64);
+    const int n_it = min(p.qo + qb + 1, (p.T_kv + BKV - 1) / BKV);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         mbar_init(q_full, 256);
-        for (int i = 0; i < kDqStages; ++i) {
+        for (int i = 0; i < kSt; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-        mbar_init(p_full, 256);
+        mbar_init(s_full, 1);
+        mbar_init(dp_full, 1);
+        mbar_init(s_free, 256);
+        mbar_init(ds_full, 256);
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -1004,64 +1083,75 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    // S x2 | dP x2 | dQ | Q (bf16 pairs) | dO (bf16 pairs): Q and dO are the A
+    // S | dP | dQ | Q (bf16 pairs) | dO (bf16 pairs): Q and dO are the A
     // operands of every S / dP MMA, so they are read from TMEM, not shared memory
-    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256, t_qa = tmem + 384, t_doa = tmem + 448;
+    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256, t_qa = tmem + 384,
+                   t_doa = tmem + 384 + D / 2;
 
     if (warp == 0) {
         if (lane == 0) {
             for (int it = 0; it < n_it; ++it) {
-                const int st = it % kDqStages;
-                mbar_wait(&kv_empty[st], ((it / kDqStages) & 1) ^ 1);
-                mbar_expect_tx(&kv_full[st], 2 * kTile64);
-                uint8_t* kd = sm + DqSmem::k + st * kTile64;
-                uint8_t* vd = sm + DqSmem::v + st * kTile64;
+                const int st = it % kSt;
+                mbar_wait(&kv_empty[st], ((it / kSt) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[st], 2 * kTile);
+                uint8_t* kd = sm + Smem::k + st * kTile;
+                uint8_t* vd = sm + Smem::v + st * kTile;
 #pragma unroll
                 for (int hh = 0; hh < D / 64; ++hh) {
-                    tma_load_2d(kd + hh * kHalf64, &tm_k, &kv_full[st], kvh * D + 64 * hh, it * BT64);
-                    tma_load_2d(vd + hh * kHalf64, &tm_v, &kv_full[st], kvh * D + 64 * hh, it * BT64);
+                    tma_load_2d(kd + hh * kHalf, &tm_k, &kv_full[st], kvh * D + 64 * hh, it * BKV);
+                    tma_load_2d(vd + hh * kHalf, &tm_v, &kv_full[st], kvh * D + 64 * hh, it * BKV);
                 }
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
+        constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);
         constexpr uint32_t id_g = umma_idesc_bf16(128, D, false, true);
-        auto issue_s = [&](int it) {
-            const int ks = it % kDqStages, sb = it & 1;
-            mbar_wait(&kv_full[ks], (it / kDqStages) & 1);
+        auto k_addr = [&](int it) { return smem_u32(sm + Smem::k + (it % kSt) * kTile); };
+        auto v_addr = [&](int it) { return smem_u32(sm + Smem::v + (it % kSt) * kTile); };
+        auto issue_s = [&](int it) {  // S(it) = Q K(it)^T
+            mbar_wait(&kv_full[it % kSt], (it / kSt) & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
-                const uint32_t v_addr = smem_u32(sm + DqSmem::v + ks * kTile64);
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    tc_mma_bf16_ts(t_s + sb * 64, t_qa + kk * 8, desc_k64(k_addr, kk), id_s, kk > 0);
-                    tc_mma_bf16_ts(t_dp + sb * 64, t_doa + kk * 8, desc_k64(v_addr, kk), id_s, kk > 0);
-                }
-                tc_commit(&s_full[sb]);
+                for (int kk = 0; kk < D / 16; ++kk)
+                    tc_mma_bf16_ts(t_s, t_qa + kk * 8, desc_kmajor(k_addr(it), kk), id_s, kk > 0);
+                tc_commit(s_full);
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int it) {  // dP(it) = dO V(it)^T (stage already waited)
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    tc_mma_bf16_ts(t_dp, t_doa + kk * 8, desc_kmajor(v_addr(it), kk), id_s, kk > 0);
+                tc_commit(dp_full);
             }
             __syncwarp();
         };
         mbar_wait(q_full, 0);
         tc_fence_after();
         issue_s(0);
+        issue_dp(0);
         for (int it = 0; it < n_it; ++it) {
-            const int sb = it & 1, ks = it % kDqStages;
-            if (it + 1 < n_it) issue_s(it + 1);
             if (lane == 0) ATR(it * 8 + 0);
-            mbar_wait(p_full, it & 1);
-            if (lane == 0) ATR(it * 8 + 1);
+            if (it + 1 < n_it) {
+                mbar_wait(s_free, it & 1);  // S(it) is in registers
+                if (lane == 0) ATR(it * 8 + 1);
+                issue_s(it + 1);
+            }
+            mbar_wait(ds_full, it & 1);
+            if (lane == 0) ATR(it * 8 + 2);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t k_addr = smem_u32(sm + DqSmem::k + ks * kTile64);
 #pragma unroll
-                for (int kk = 0; kk < BT64 / 16; ++kk)
-                    tc_mma_bf16_ts(t_dq, t_dp + sb * 64 + (kk >> 1) * 32 + (kk & 1) * 8, desc_mn64(k_addr, kk), id_g,
-                                   (it | kk) != 0);
-                tc_commit(&kv_empty[ks]);
+                for (int kk = 0; kk < BKV / 16; ++kk)
+                    tc_mma_bf16_ts(t_dq, t_dp + packed_col(kk), desc_mnmajor(k_addr(it), kk), id_g, (it | kk) != 0);
+                tc_commit(&kv_empty[it % kSt]);
                 if (it + 1 == n_it) tc_commit(acc_done);
             }
             __syncwarp();
+            // dP(it+1) overwrites dS(it): the dQ MMAs above were issued first
+            if (it + 1 < n_it) issue_dp(it + 1);
         }
     } else {
         const int quad = warp & 3;
@@ -1069,10 +1159,10 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
         const int r = quad * 32 + lane;
         const int qrow = qb * BQ + r;
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        const uint32_t col = lane_off + half * 64;
         const int qc = min(qrow, p.T - 1);
-        const float lse2 = p.lse[static_cast<long long>(h) * p.T + qc] * kLog2e;
+        const float nlse2 = -p.lse[static_cast<long long>(h) * p.T + qc] * kLog2e;
         const float dd = p.dvec[static_cast<long long>(h) * p.T + qc];
-        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nl2 = f2_pack(-lse2, -lse2);
         const uint64_t nd2 = f2_pack(-dd, -dd);
         {
             // this thread's query row of Q (half 0) or dO (half 1) into its TMEM lane:
@@ -1097,46 +1187,49 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
             tc_fence_before();
             mbar_arrive(q_full);
         }
+        const int qpos = (p.qo + qb) * BQ + r;  // this row's global query position
         for (int it = 0; it < n_it; ++it) {
-            const int sb = it & 1;
-            if (threadIdx.x == 64) ATR(it * 8 + 2);
-            mbar_wait(&s_full[sb], (it >> 1) & 1);
+            if (threadIdx.x == 64) ATR(it * 8 + 7);
+            mbar_wait(s_full, it & 1);
             if (threadIdx.x == 64) ATR(it * 8 + 3);
             tc_fence_after();
-            uint32_t a[32], b[32];
-            tmem_ld32(t_s + sb * 64 + lane_off + half * 32, a);
-            tmem_ld32(t_dp + sb * 64 + lane_off + half * 32, b);
-            tmem_ld_wait();
-            if (threadIdx.x == 64) ATR(it * 8 + 5);
-            if (threadIdx.x == 64) ATR(it * 8 + 6);
+            uint32_t pv[64];
+            tmem_ld64(t_s + col, pv);
+            tc_fence_before();
+            mbar_arrive(s_free);
             const int qg0 = (p.qo + qb) * BQ;  // global position of the block's first query
-            const bool full_tile = it * BT64 + BT64 - 1 <= qg0 && it * BT64 + BT64 <= p.T_kv && qb * BQ + BQ <= p.T;
-            uint32_t pd[16];
+            const bool full_tile = it * BKV + BKV - 1 <= qg0 && it * BKV + BKV <= p.T_kv && qb * BQ + BQ <= p.T;
+            bwd_exp64<false>(pv, nullptr, nlse2, p.scale_log2);
+            if (!full_tile) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const uint64_t x = ffma2(f2_pack(__uint_as_float(a[2 * u]), __uint_as_float(a[2 * u + 1])), sc2, nl2);
-                float x0, x1;
-                f2_unpack(x, x0, x1);
-                float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
-                if (!full_tile) {
-                    const int key = it * BT64 + half * 32 + 2 * u;
-                    const int qpos = qg0 + r;
-                    if (key > qpos || key >= p.T_kv) e0 = 0.f;
-                    if (key + 1 > qpos || key + 1 >= p.T_kv) e1 = 0.f;
+                for (int j = 0; j < 64; ++j) {
+                    const int key = it * BKV + half * 64 + j;
+                    if (key > qpos || key >= p.T_kv) pv[j] = 0u;
                 }
-                const uint64_t ds =
-                    ffma2(f2_pack(e0, e1), fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), nd2),
-                          0ull);
-                float s0, s1;
-                f2_unpack(ds, s0, s1);
-                pd[u] = pack2(s0, s1);
             }
-            if (threadIdx.x == 64) ATR(it * 8 + 7);
-            tmem_st16(t_dp + sb * 64 + lane_off + half * 32, pd);  // over this half's own fp32 columns
+            if (threadIdx.x == 64) ATR(it * 8 + 4);
+            mbar_wait(dp_full, it & 1);
+            if (threadIdx.x == 64) ATR(it * 8 + 5);
+            tc_fence_after();
+            {
+                uint32_t b[64];
+                tmem_ld64(t_dp + col, b);
+                uint32_t pd[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const uint64_t ds = ffma2(
+                        f2_pack(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1])),
+                        fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), nd2), 0ull);
+                    float s0, s1;
+                    f2_unpack(ds, s0, s1);
+                    pd[u] = pack2(s0, s1);
+                }
+                tmem_st32(t_dp + col, pd);  // over the first 32 columns of this half (read above)
+            }
             tmem_st_wait();
             tc_fence_before();
-            if (threadIdx.x == 64) ATR(it * 8 + 4);
-            mbar_arrive(p_full);
+            if (threadIdx.x == 64) ATR(it * 8 + 6);
+            mbar_arrive(ds_full);
         }
         mbar_wait(acc_done, 0);
         tc_fence_after();
@@ -1174,9 +1267,7 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_q, const 
 template <int D>
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                       const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
                        const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                       const __grid_constant__ CUtensorMap tm_k64, const __grid_constant__ CUtensorMap tm_v64,
                        const BwdParams p, const int nq, const int nb_kv, const int nb_q) {
     // rank r: key block r (the low blocks see the most queries) and query
     // block nb_q - 1 - r (the high blocks see the most keys), every head;
@@ -1196,9 +1287,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         dkdv = nb_kv > nb_q;
     }
     if (dkdv)
-        attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q64, tm_do64, p, rank, rem);
+        attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q, tm_do, p, rank, rem);
     else
-        attn_bwd_dq_body<D>(tm_q, tm_do, tm_k64, tm_v64, p, nb_q - 1 - rank, rem);
+        attn_bwd_dq_body<D>(tm_k, tm_v, p, nb_q - 1 - rank, rem);
 }
 
 template <int D>
@@ -1206,16 +1297,12 @@ int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
                   long long ldo, const float* lse, const float* dvec, float* dk_part, float* dv_part, void* dq,
                   void* dk, void* dv, long long lddq, long long lddkv, int T, int nq, int nkv, float scale,
                   int T_kv, int q_offset, cudaStream_t s) {
-    CUtensorMap mk, mv, mq64, mdo64, mq, mdo, mk64, mv64;
+    CUtensorMap mk, mv, mq, mdo;
     const long long qcols = static_cast<long long>(nq) * D, kvcols = static_cast<long long>(nkv) * D;
     int rc = make_tma_2d(&mk, k, kvcols, T_kv, ldkv, 64, 128);
     if (!rc) rc = make_tma_2d(&mv, v, kvcols, T_kv, ldkv, 64, 128);
-    if (!rc) rc = make_tma_2d(&mq64, q, qcols, T, ldq, 64, 64);
-    if (!rc) rc = make_tma_2d(&mdo64, dout, qcols, T, ldo, 64, 64);
     if (!rc) rc = make_tma_2d(&mq, q, qcols, T, ldq, 64, 128);
     if (!rc) rc = make_tma_2d(&mdo, dout, qcols, T, ldo, 64, 128);
-    if (!rc) rc = make_tma_2d(&mk64, k, kvcols, T_kv, ldkv, 64, 64);
-    if (!rc) rc = make_tma_2d(&mv64, v, kvcols, T_kv, ldkv, 64, 64);
     if (rc) return rc;
     constexpr int smem = KvSmem<D>::total > DqSmem<D>::total ? KvSmem<D>::total : DqSmem<D>::total;
     static bool cfg = false;
@@ -1228,8 +1315,8 @@ int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
                   nq / nkv, scale, scale * kLog2e, T_kv, q_offset / BQ};
     const int nb_kv = (T_kv + BKV - 1) / BKV, nb_q = (T + BQ - 1) / BQ;
-    attn_bwd_tc_kernel<D><<<(nb_kv + nb_q) * nq, kThreadsBwd, smem, s>>>(mk, mv, mq64, mdo64, mq, mdo, mk64, mv64,
-                                                                        prm, nq, nb_kv, nb_q);
+    attn_bwd_tc_kernel<D><<<(nb_kv + nb_q) * nq, kThreadsBwd, smem, s>>>(mk, mv, mq, mdo, prm, nq, nb_kv,
+                                                                        nb_q);
     DH_CUDA_CHECK(cudaGetLastError());
     return DH_OK;
 }

@@ -1,4 +1,7 @@
-"""clock64 timeline of one attention-backward CTA (build with -DDH_ATTN_TRACE=<block>)."""
+"""clock64 timeline of one attention-backward CTA. Build a traced copy of the
+library first:  make cuda NVFLAGS_EXTRA=-DDH_ATTN_TRACE=<block>  (block 0 = the
+heaviest dK/dV item of head 0; block nq = the heaviest dQ item).
+usage: attn_trace.py <nq> [iterations]"""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -19,7 +22,13 @@ torch.cuda.synchronize()
 buf = (ctypes.c_longlong * 1024)()
 dh.lib().dh_attn_trace_read(buf, 1024)
 t0 = buf[3]
-print("it mma_s_issued(it+1) mma_got_p(it) | ew: wait_s got_s ld_done bar_done math_done arrive   (cycles rel. to it0 s_full)")
-for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 64):
+print("cycles relative to the first S ready (EW). mma: [0] before wait P / s_free, [1] after, [2] got dS | "
+      "ew: [7] iter start, [3] got S, [4] P done / S read, [5] got dP, [6] dS done")
+prev = None
+for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 32):
     r = [buf[it * 8 + j] - t0 for j in range(8)]
-    print(it, r[0], r[1], "|", r[2], r[3], r[5], r[6], r[7], r[4])
+    if r[3] < 0 and it > 0:
+        break
+    dt = "" if prev is None else f"  (+{r[3] - prev})"
+    prev = r[3]
+    print(it, "mma", r[0], r[1], r[2], "| ew", r[7], r[3], r[4], r[5], r[6], dt)
