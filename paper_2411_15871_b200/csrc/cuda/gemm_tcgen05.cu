@@ -26,6 +26,26 @@
 #include "common.cuh"
 #include "dh_capi.h"
 
+#ifdef DH_GEMM_TRACE
+// per-CTA globaltimer stamps of the last pair-kernel launch (tools/gemm_trace.py):
+// [0] entry [1] prologue done [2] first stage consumed by the MMA [3] last
+// accumulator ready [4] last store issued and drained [5] exit
+__device__ unsigned long long g_gemm_trace[512 * 8];
+extern "C" int dh_gemm_trace_read(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#define GTR(i, cond)                                                                     \
+    do {                                                                                 \
+        if (cond) {                                                                      \
+            unsigned long long t_;                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                       \
+            g_gemm_trace[blockIdx.x * 8 + (i)] = t_;                                     \
+        }                                                                                \
+    } while (0)
+#else
+#define GTR(i, cond) do { } while (0)
+#endif
+
 namespace dh {
 namespace {
 
@@ -385,6 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
     const int tiles_m = p.tiles_m;  // in units of 256 rows
     const int num_tiles = tiles_m * p.tiles_n;
     const int num_kb = (p.k + BK - 1) / BK;
+    GTR(0, threadIdx.x == 0);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
@@ -411,6 +432,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
     cluster_sync();  // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    GTR(1, threadIdx.x == 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -458,6 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
                 const uint32_t d_tmem = tmem_base + acc * PBN;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    GTR(2, lane == 0 && tile == pair && kb == 0);
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t a_addr = smem_u32(sA + stage * C::kStageA);
@@ -494,6 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
             const int m0 = mi * 256 + rank * BM;
             const int n0 = ni * PBN;
             mbar_wait(&tfull[acc], acc_phase);
+            GTR(3, store_leader);
             tc_fence_after();
             if constexpr (kFused) {
                 // SwiGLU fused into the epilogue. Per 64-column chunk, one staging
@@ -609,10 +633,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
             if (++acc == 2) acc = 0, acc_phase ^= 1;
         }
         if (store_leader) bulk_wait<0>();
+        GTR(4, store_leader);
     }
 
     tc_fence_before();
     cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+    GTR(5, threadIdx.x == 0);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_pair(tmem_base, 512);
