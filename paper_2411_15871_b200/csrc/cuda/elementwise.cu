@@ -215,6 +215,98 @@ __global__ void __launch_bounds__(RB == 1 ? 1024 : 512) rmsnorm_bwd_rows(const u
 }
 
 
+// One-launch RMSNorm backward (cols % 64 == 0): blocks [0, n_dg) reduce
+// dgamma over 64-column slices of all rows (dgamma needs only x, dy and the
+// saved rstd, no row reduction), the remaining blocks each produce one dx row.
+// Both kinds read their inputs independently, so the launch has no second
+// pass and no cross-block reduction; dgamma is summed in a fixed order (row
+// lanes, then lane order), hence deterministic. T = cols / 8 threads per block.
+__global__ void __launch_bounds__(1024) rmsnorm_bwd_fused(const uint4* __restrict__ x, const uint4* __restrict__ g,
+                                                          const float* __restrict__ rstd, const uint4* __restrict__ dy,
+                                                          const uint4* __restrict__ resid, uint4* __restrict__ dx,
+                                                          float* __restrict__ dgamma_acc, int rows, int vec_cols,
+                                                          float inv_cols, int n_dg) {
+    __shared__ float red[1024 / 8 * 65];  // dgamma: [row lane][64 columns (+1 pad)]; dx: per-warp dots
+    const int t = threadIdx.x, T = blockDim.x;
+    if (static_cast<int>(blockIdx.x) < n_dg) {
+        if (!dgamma_acc) return;
+        const int cl = t & 7, rl = t >> 3, RL = T >> 3;
+        const int vc = blockIdx.x * 8 + cl;  // this thread's 16-byte column vector
+        float acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+        int r = rl;
+        for (; r + 3 * RL < rows; r += 4 * RL) {  // four rows' loads in flight
+            uint4 xv[4], dv[4];
+            float rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long off = static_cast<long long>(r + u * RL) * vec_cols + vc;
+                xv[u] = __ldcs(x + off);
+                dv[u] = __ldcs(dy + off);
+                rr[u] = rstd[r + u * RL];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                float a[8], b[8];
+                unpack8(xv[u], a);
+                unpack8(dv[u], b);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[k] += b[k] * (a[k] * rr[u]);
+            }
+        }
+        for (; r < rows; r += RL) {
+            const long long off = static_cast<long long>(r) * vec_cols + vc;
+            float a[8], b[8];
+            unpack8(__ldcs(x + off), a);
+            unpack8(__ldcs(dy + off), b);
+            const float rr = rstd[r];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] += b[k] * (a[k] * rr);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) red[rl * 65 + cl * 8 + k] = acc[k];
+        __syncthreads();
+        for (int c = t; c < 64; c += T) {
+            float sum = 0.f;
+            for (int j = 0; j < RL; ++j) sum += red[j * 65 + c];
+            dgamma_acc[blockIdx.x * 64 + c] += sum;
+        }
+        return;
+    }
+    const int row = blockIdx.x - n_dg;
+    const int lane = t & 31, wid = t >> 5, nw = T >> 5;
+    const long long off = static_cast<long long>(row) * vec_cols + t;
+    float xv[8], dv[8], gam[8];
+    unpack8(__ldcs(x + off), xv);
+    unpack8(__ldcs(dy + off), dv);
+    unpack8(g[t], gam);
+    const float rr = rstd[row];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        xv[k] *= rr;        // xhat
+        dv[k] *= gam[k];    // dxhat
+        dot += dv[k] * xv[k];
+    }
+    dot = warp_sum(dot);
+    if (lane == 0) red[wid] = dot;
+    __syncthreads();
+    float tot = 0.f;
+    for (int w = 0; w < nw; ++w) tot += red[w];
+    tot *= inv_cols;
+    float o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = rr * (dv[k] - xv[k] * tot);
+    if (resid) {
+        float rv[8];
+        unpack8(__ldcs(resid + off), rv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] += rv[k];
+    }
+    dx[off] = pack8(o);
+}
+
 // dgamma_acc[c] += sum_w partial[w][c]. Block = 32 columns x 8 warps; warp j
 // sums rows j, j+8, ... and the 8 warp partials are combined in warp order, so
 // the summation order is fixed (deterministic) yet the read is parallel.
@@ -640,6 +732,18 @@ int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const vo
         return set_error(DH_ERR_INVALID, "rmsnorm_bwd: cols % 8, cols <= 8192 and 16-byte alignment required");
     if (rows <= 0) return DH_OK;
     auto s = static_cast<cudaStream_t>(stream);
+    static const bool fused_off = [] {  // DH_RMSNORM_BWD_FUSED=0: the two-kernel path (A/B runs)
+        const char* e = std::getenv("DH_RMSNORM_BWD_FUSED");
+        return e && e[0] == '0';
+    }();
+    if (cols % 64 == 0 && cols / 8 >= 32 && !fused_off) {
+        const int n_dg = cols / 64;
+        rmsnorm_bwd_fused<<<n_dg + rows, cols / 8, 0, s>>>(
+            static_cast<const uint4*>(x), static_cast<const uint4*>(gamma), rstd, static_cast<const uint4*>(dy),
+            static_cast<const uint4*>(resid), static_cast<uint4*>(dx), dgamma_acc, rows, cols / 8, 1.f / cols, n_dg);
+        DH_CUDA_CHECK(cudaGetLastError());
+        return DH_OK;
+    }
     // up to 4096 columns: 4 rows per barrier (512 threads); wider rows (e.g.
     // hidden 8192 at 1024 threads) one row, within the 64-register budget
     const bool wide = cols / 8 > 512;
