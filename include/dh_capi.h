@@ -121,10 +121,14 @@ long long dh_attn_fwd_scratch_floats_ex(int tokens, int n_q_heads, int n_kv_head
 int dh_attn_fwd_ex(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
                    long long ldo, float* lse, float* scratch, long long scratch_floats, int tokens, int tokens_kv,
                    int q_offset, int n_q_heads, int n_kv_heads, int head_dim, float scale, void* stream);
-/* dq/dk/dv written (not accumulated); `scratch` fp32 >= tokens*n_q_heads*(2*head_dim+1) floats
- * (dh_attn_bwd_scratch_floats; the _ex form: dk/dv cover all tokens_kv key rows, each the
- * gradient from this call's queries only). */
+/* dq/dk/dv written (not accumulated); `scratch` fp32 of dh_attn_bwd_scratch_floats_ex floats for
+ * this shape (the backward's work plan: rowsum(dO*O) plus the partial slots of GQA groups and of
+ * items split across SMs; dh_attn_bwd_scratch_floats covers any n_kv_heads at q_offset 0). The _ex
+ * form: dk/dv cover all tokens_kv key rows, each the gradient from this call's queries only. */
 long long dh_attn_bwd_scratch_floats(int tokens, int n_q_heads, int head_dim, int tokens_kv);
+/* exact scratch of dh_attn_bwd_ex for this GQA shape and query offset */
+long long dh_attn_bwd_scratch_floats_ex(int tokens, int n_q_heads, int n_kv_heads, int head_dim, int tokens_kv,
+                                        int q_offset);
 int dh_attn_bwd_ex(const void* q, const void* k, const void* v, long long ldq, long long ldkv, const void* o,
                    long long ldo, const float* lse, const void* dout, void* dq, void* dk, void* dv, long long lddq,
                    long long lddkv, float* scratch, int tokens, int tokens_kv, int q_offset, int n_q_heads,

@@ -3,10 +3,11 @@
 // attention_tc.cu, for head_dim 64 and 128, plus the backward's two small
 // helpers: rowsum(dO * O) and the fixed-order GQA group reduction.
 //
-// Determinism: no atomics anywhere. The backward runs dK/dV items (one CTA per
-// (kv block, q head); fp32 per-head partials reduced over the GQA group in
-// head order) and dQ items (one CTA per (q block, q head)), so the interleaved
-// SI schedule reproduces the sequential numbers bit for bit.
+// Determinism: no atomics anywhere. The backward runs planned dK/dV items (per
+// (kv block, q head[, q-tile chunk])) and dQ items (per (q block, q head[,
+// key-tile chunk])); partial slots (GQA groups, split items) are summed in a
+// fixed order, so the interleaved SI schedule reproduces the sequential numbers
+// bit for bit.
 //
 // Layout: q/k/v/o rows are tokens, columns head-major (head h occupies
 // [h*D, (h+1)*D)), arbitrary row pitch. lse is fp32 [n_q_heads, tokens],
@@ -51,50 +52,6 @@ __global__ void attn_bwd_dot_kernel(const bf16* __restrict__ o, long long ldo,
     if (ok && sub == 0) dvec[static_cast<long long>(h) * T + t] = sum;
 }
 
-// Sum the GQA group's per-head partials in head order -> bf16 dk, dv.
-// VEC: 8 consecutive d per thread (two 16-byte loads per partial, one 16-byte
-// store) when the partials are 16-byte aligned; else one element per thread.
-template <bool VEC>
-__global__ void attn_bwd_group_reduce(const float* __restrict__ dk_part,
-                                      const float* __restrict__ dv_part, bf16* __restrict__ dk,
-                                      bf16* __restrict__ dv, long long lddkv, int T, int n_kv,
-                                      int group, int D) {
-    constexpr int W = VEC ? 8 : 1;
-    const long long total = static_cast<long long>(n_kv) * T * (D / W);
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int d = static_cast<int>(i % (D / W)) * W;
-        const long long rest = i / (D / W);
-        const int t = static_cast<int>(rest % T);
-        const int kvh = static_cast<int>(rest / T);
-        float sk[W] = {}, sv[W] = {};
-        for (int j = 0; j < group; ++j) {  // head order: deterministic
-            const long long off = (static_cast<long long>(kvh * group + j) * T + t) * D + d;
-#pragma unroll
-            for (int u = 0; u < W; u += (VEC ? 4 : 1)) {
-                if constexpr (VEC) {
-                    const float4 kk = *reinterpret_cast<const float4*>(dk_part + off + u);
-                    const float4 vv = *reinterpret_cast<const float4*>(dv_part + off + u);
-                    sk[u] += kk.x; sk[u + 1] += kk.y; sk[u + 2] += kk.z; sk[u + 3] += kk.w;
-                    sv[u] += vv.x; sv[u + 1] += vv.y; sv[u + 2] += vv.z; sv[u + 3] += vv.w;
-                } else {
-                    sk[u] += dk_part[off + u];
-                    sv[u] += dv_part[off + u];
-                }
-            }
-        }
-        bf16* pk = dk + static_cast<long long>(t) * lddkv + kvh * D + d;
-        bf16* pv = dv + static_cast<long long>(t) * lddkv + kvh * D + d;
-        if constexpr (VEC) {
-            *reinterpret_cast<uint4*>(pk) = pack8(sk);
-            *reinterpret_cast<uint4*>(pv) = pack8(sv);
-        } else {
-            *pk = __float2bfloat16(sk[0]);
-            *pv = __float2bfloat16(sv[0]);
-        }
-    }
-}
-
 }  // namespace
 
 int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,
@@ -102,9 +59,10 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
                 long long scratch_floats, int T_kv, int q_offset, cudaStream_t s);
 long long attn_fwd_tc_scratch_floats(int T, int nq, int D, int T_kv, int q_offset);
 int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
-                const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
-                float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
-                int nq, int nkv, int D, float scale, int T_kv, int q_offset, cudaStream_t s);
+                const void* dout, long long ldo, const float* lse, float* scratch, void* dq, void* dk, void* dv,
+                long long lddq, long long lddkv, int T, int nq, int nkv, int D, float scale, int T_kv,
+                int q_offset, cudaStream_t s);
+long long attn_bwd_tc_scratch_floats(int T, int nq, int nkv, int D, int T_kv, int q_offset);
 
 }  // namespace dh
 
@@ -116,35 +74,19 @@ int launch_bwd(const void* q, const void* k, const void* v, long long ldq, long 
                void* dv, long long lddq, long long lddkv, float* scratch, int T, int nq, int nkv,
                float scale, int T_kv, int q_offset, cudaStream_t s) {
     using namespace dh;
-    const int group = nq / nkv;
     float* dvec = scratch;
-    float* dk_part = scratch + static_cast<long long>(nq) * T;
-    float* dv_part = dk_part + static_cast<long long>(nq) * T_kv * D;
     if (ldo % 8 || (reinterpret_cast<uintptr_t>(o) & 15) || (reinterpret_cast<uintptr_t>(dout) & 15))
         return set_error(DH_ERR_INVALID, "attn_bwd: O / dO need 16-byte aligned rows (ldo % 8 == 0)");
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (lddq % 8 || lddkv % 8 || !al16(dq) || !al16(dk) || !al16(dv) || !al16(scratch))
+        return set_error(DH_ERR_INVALID, "attn_bwd: dq / dk / dv / scratch need 16-byte aligned rows");
     attn_bwd_dot_kernel<D><<<static_cast<int>((static_cast<long long>(T) * nq * (D / 8) + 255) / 256), 256, 0, s>>>(
         static_cast<const bf16*>(o), ldo, static_cast<const bf16*>(dout), dvec, T, nq);
     DH_CUDA_CHECK(cudaGetLastError());
-    // tcgen05/TMEM kernel (attention_tc.cu): dK/dV items + dQ items in one launch
-    const int rc = attn_bwd_tc(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq, lddkv,
-                               T, nq, nkv, D, scale, T_kv, q_offset, s);
-    if (rc != DH_OK) return rc;
-    if (group > 1) {  // sum the GQA group's per-head dK/dV partials in head order
-        const bool vec = (reinterpret_cast<uintptr_t>(dk_part) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(dv_part) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(dv) & 15) == 0 &&
-                         lddkv % 8 == 0;
-        const long long total = static_cast<long long>(nkv) * T_kv * (vec ? D / 8 : D);
-        const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-        if (vec)
-            attn_bwd_group_reduce<true><<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
-                                                               static_cast<bf16*>(dv), lddkv, T_kv, nkv, group, D);
-        else
-            attn_bwd_group_reduce<false><<<blocks, 256, 0, s>>>(dk_part, dv_part, static_cast<bf16*>(dk),
-                                                                static_cast<bf16*>(dv), lddkv, T_kv, nkv, group, D);
-        DH_CUDA_CHECK(cudaGetLastError());
-    }
-    return DH_OK;
+    // tcgen05/TMEM kernel (attention_tc.cu): planned dK/dV + dQ items in one
+    // launch, then the fixed-order reduction of any partial slots
+    return attn_bwd_tc(q, k, v, ldq, ldkv, dout, ldo, lse, scratch, dq, dk, dv, lddq, lddkv, T, nq, nkv, D, scale,
+                       T_kv, q_offset, s);
 }
 
 }  // namespace
@@ -160,8 +102,17 @@ extern "C" long long dh_attn_fwd_scratch_floats(int tokens, int n_q_heads, int n
     return dh_attn_fwd_scratch_floats_ex(tokens, n_q_heads, n_kv_heads, head_dim, tokens, 0);
 }
 
+extern "C" long long dh_attn_bwd_scratch_floats_ex(int tokens, int n_q_heads, int n_kv_heads, int head_dim,
+                                                   int tokens_kv, int q_offset) {
+    if ((head_dim != 128 && head_dim != 64) || tokens <= 0 || n_q_heads <= 0) return 0;
+    return dh::attn_bwd_tc_scratch_floats(tokens, n_q_heads, n_kv_heads, head_dim, tokens_kv, q_offset);
+}
+
+// Without the GQA shape or query offset: enough for any n_kv_heads at offset 0
+// (a GQA group > 1 gives every key block partial slots).
 extern "C" long long dh_attn_bwd_scratch_floats(int tokens, int n_q_heads, int head_dim, int tokens_kv) {
-    return static_cast<long long>(n_q_heads) * (tokens + 2LL * tokens_kv * head_dim);
+    return std::max(dh_attn_bwd_scratch_floats_ex(tokens, n_q_heads, n_q_heads, head_dim, tokens_kv, 0),
+                    dh_attn_bwd_scratch_floats_ex(tokens, n_q_heads, 1, head_dim, tokens_kv, 0));
 }
 
 extern "C" int dh_attn_fwd_ex(const void* q, const void* k, const void* v, long long ldq, long long ldkv, void* o,

@@ -48,6 +48,28 @@ extern "C" int dh_attn_trace_read(long long* out, int n) {
 #else
 #define ATR(idx) do { } while (0)
 #endif
+#ifdef DH_ATTN_BLKTRACE
+// per-block (start ns, end ns, SM id) of the last backward launch (tools/attn_blocks.py)
+__device__ unsigned long long g_attn_blk[8192 * 3];
+extern "C" int dh_attn_blk_read(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_attn_blk, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+__device__ __forceinline__ void blk_stamp(int i) {
+    if (threadIdx.x == 0 && blockIdx.x < 8192) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_attn_blk[blockIdx.x * 3 + i] = t;
+        if (i == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_attn_blk[blockIdx.x * 3 + 2] = sm;
+        }
+    }
+}
+#define BLK(i) blk_stamp(i)
+#else
+#define BLK(i) do { } while (0)
+#endif
 
 namespace dh {
 namespace {
@@ -656,8 +678,13 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
 //   TMEM: S (128) | dP (128) | dQ (D) | Q (D/2) | dO (D/2).
 //   Issue order: S(0) dP(0) | S(i+1) dQ(i) dP(i+1) | ... — S(i+1) is issued as
 //   soon as the elementwise warps have read S(i) into registers.
-// No atomics: dQ is produced by its own items and per-head dK/dV partials of a
-// GQA group are reduced in head order by attn_bwd_group_reduce (attention.cu).
+// Work items come from a host plan (bwd_plan): with few heads per GPU (high
+// TP) the longest causal items would be the critical path, so items costlier
+// than the per-SM average are split into chunks of their inner loop (q tiles
+// of a dK/dV item, key tiles of a dQ item), dispatched heaviest first. No
+// atomics: an item writes bf16 directly when it alone owns its output rows;
+// otherwise (GQA group > 1, or split) it writes an fp32 partial slot and
+// attn_bwd_reduce sums the slots in a fixed (head, chunk) order.
 // ===========================================================================
 
 namespace dh {
@@ -701,8 +728,9 @@ struct BwdParams {
     long long ldq, ldo;
     const float* lse;
     const float* dvec;
-    float* dk_part;
+    float* dk_part;             // [slot][128 keys][D] fp32 (scaled)
     float* dv_part;
+    float* dq_part;             // [slot][128 queries][D] fp32 (scaled)
     __nv_bfloat16* dk;
     __nv_bfloat16* dv;
     __nv_bfloat16* dq;
@@ -714,6 +742,23 @@ struct BwdParams {
 };
 
 constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
+constexpr uint32_t kDirect = 0xFFFFFFFFu;  // item owns its output rows: bf16 store, no slot
+
+// Explicit schedule (kernel parameter): item.x = kind << 31 (1 = dQ) | head << 24
+// | block << 16 | c0 << 8 | c1, item.y = partial slot or kDirect; heaviest first.
+constexpr int kMaxBwdItems = 2900;
+struct BwdSched {
+    int n;  // 0: implicit rank order, no splits (see attn_bwd_tc_kernel)
+    uint2 item[kMaxBwdItems];
+};
+// Partial-slot tables of the reduction: slot of (head h, block b, chunk c) =
+// base[b] + h * nck[b] + c, so a GQA group's heads and a block's chunks are
+// contiguous and summed in that order.
+constexpr int kMaxBwdBlocks = 256;
+struct BwdSlots {
+    uint32_t kv_base[kMaxBwdBlocks], q_base[kMaxBwdBlocks];  // kDirect: no partials for the block
+    uint8_t kv_nck[kMaxBwdBlocks], q_nck[kMaxBwdBlocks];
+};
 
 // A operand from TMEM (bf16 pairs) for k-step kk (16 rows of the 128-wide
 // tile): each 64-column half of the fp32 tile holds its 64 values packed
@@ -760,7 +805,8 @@ __device__ __forceinline__ void bwd_exp64(uint32_t (&s)[64], const float* bias, 
 template <int D>
 __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                    const CUtensorMap& tm_q, const CUtensorMap& tm_do,
-                                                   const BwdParams& p, const int kb, const int h) {
+                                                   const BwdParams& p, const int kb, const int h, const int c0,
+                                                   const int c1, const uint32_t slot) {
     using Smem = dh::KvSmem<D>;
     constexpr int kTile = Smem::kTile, kQS = Smem::kQS, kOS = Smem::kOS;
     extern __shared__ uint8_t smem_raw[];
@@ -782,10 +828,11 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
     float* dvec_s = reinterpret_cast<float*>(sm + Smem::dvec);  // [kOS][128]
 
     const int kvh = h / p.group;
+    // q tiles [c0, c1) of the tiles from the first one with a query at or after
+    // the block's first key (c1 < 0: all of them)
     const int nq128 = (p.T + BQ - 1) / BQ;
-    // first local q tile with a query at or after the block's first key
-    const int i0 = max(0, kb - p.qo);
-    const int n_it = max(0, nq128 - i0);
+    const int i0 = max(0, kb - p.qo) + c0;
+    const int n_it = c1 < 0 ? max(0, nq128 - i0) : c1 - c0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -997,7 +1044,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             tmem_ld32(t_dv + lane_off + c * 32, va);
             tmem_ld_wait();
             if (!ok) continue;
-            if (p.group == 1) {
+            if (slot == kDirect) {
                 __nv_bfloat16* kr = p.dk + static_cast<long long>(key) * p.lddkv + kvh * D + c * 32;
                 __nv_bfloat16* vr = p.dv + static_cast<long long>(key) * p.lddkv + kvh * D + c * 32;
 #pragma unroll
@@ -1012,8 +1059,8 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                     *reinterpret_cast<uint4*>(vr + t) = pack8(fv);
                 }
             } else {
-                float* kr = p.dk_part + (static_cast<long long>(h) * p.T_kv + key) * D + c * 32;
-                float* vr = p.dv_part + (static_cast<long long>(h) * p.T_kv + key) * D + c * 32;
+                float* kr = p.dk_part + (static_cast<long long>(slot) * BKV + r) * D + c * 32;
+                float* vr = p.dv_part + (static_cast<long long>(slot) * BKV + r) * D + c * 32;
                 // keys after every query of this rank (context parallelism) get no
                 // gradient; TMEM was never written for them (select, not multiply)
                 const bool any = n_it > 0;
@@ -1042,7 +1089,8 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
 
 template <int D>
 __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const CUtensorMap& tm_v,
-                                                 const BwdParams& p, const int qb, const int h) {
+                                                 const BwdParams& p, const int qb, const int h, const int c0,
+                                                 const int c1, const uint32_t slot) {
     using Smem = dh::DqSmem<D>;
     constexpr int kTile = Smem::kTile, kSt = Smem::kSt;
     extern __shared__ uint8_t smem_raw[];
@@ -1059,8 +1107,9 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
     const int kvh = h / p.group;
-    // key tiles 0 .. covering the block's last query (global position)
-    const int n_it = min(p.qo + qb + 1, (p.T_kv + BKV - 1) / BKV);
+    // key tiles [c0, c1) of those covering the block's last query (global
+    // position); c1 < 0: all of them. `it` below counts from c0.
+    const int n_it = (c1 < 0 ? min(p.qo + qb + 1, (p.T_kv + BKV - 1) / BKV) : c1) - c0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -1098,8 +1147,8 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
                 uint8_t* vd = sm + Smem::v + st * kTile;
 #pragma unroll
                 for (int hh = 0; hh < D / 64; ++hh) {
-                    tma_load_2d(kd + hh * kHalf, &tm_k, &kv_full[st], kvh * D + 64 * hh, it * BKV);
-                    tma_load_2d(vd + hh * kHalf, &tm_v, &kv_full[st], kvh * D + 64 * hh, it * BKV);
+                    tma_load_2d(kd + hh * kHalf, &tm_k, &kv_full[st], kvh * D + 64 * hh, (c0 + it) * BKV);
+                    tma_load_2d(vd + hh * kHalf, &tm_v, &kv_full[st], kvh * D + 64 * hh, (c0 + it) * BKV);
                 }
             }
         }
@@ -1198,12 +1247,13 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
             tc_fence_before();
             mbar_arrive(s_free);
             const int qg0 = (p.qo + qb) * BQ;  // global position of the block's first query
-            const bool full_tile = it * BKV + BKV - 1 <= qg0 && it * BKV + BKV <= p.T_kv && qb * BQ + BQ <= p.T;
+            const int kt = c0 + it;  // absolute key tile
+            const bool full_tile = kt * BKV + BKV - 1 <= qg0 && kt * BKV + BKV <= p.T_kv && qb * BQ + BQ <= p.T;
             bwd_exp64<false>(pv, nullptr, nlse2, p.scale_log2);
             if (!full_tile) {
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
-                    const int key = it * BKV + half * 64 + j;
+                    const int key = kt * BKV + half * 64 + j;
                     if (key > qpos || key >= p.T_kv) pv[j] = 0u;
                 }
             }
@@ -1235,18 +1285,27 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
         tc_fence_after();
         const bool ok = qrow < p.T;
         __nv_bfloat16* row = p.dq + static_cast<long long>(qrow) * p.lddq + h * D;
+        float* prow = p.dq_part + (static_cast<long long>(slot) * BQ + r) * D;
 #pragma unroll 1
         for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
             uint32_t a[32];
             tmem_ld32(t_dq + lane_off + c * 32, a);
             tmem_ld_wait();
             if (!ok) continue;
+            if (slot == kDirect) {
 #pragma unroll
-            for (int t = 0; t < 32; t += 8) {
-                float f[8];
+                for (int t = 0; t < 32; t += 8) {
+                    float f[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(a[t + u]) * p.scale;
-                *reinterpret_cast<uint4*>(row + c * 32 + t) = pack8(f);
+                    for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(a[t + u]) * p.scale;
+                    *reinterpret_cast<uint4*>(row + c * 32 + t) = pack8(f);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < 32; t += 4)
+                    *reinterpret_cast<float4*>(prow + c * 32 + t) =
+                        make_float4(__uint_as_float(a[t]) * p.scale, __uint_as_float(a[t + 1]) * p.scale,
+                                    __uint_as_float(a[t + 2]) * p.scale, __uint_as_float(a[t + 3]) * p.scale);
             }
         }
     }
@@ -1260,18 +1319,27 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
 }
 
 // One launch for both kinds: the dK/dV and dQ work items are independent, so
-// interleaving them (rank r = r-th heaviest block of either kind, all heads)
-// lets the light items of one kind fill the tail of the other. With few heads
-// per GPU (high TP) two separate grids each left their longest causal block as
-// an exposed critical path.
+// interleaving them lets the light items of one kind fill the tail of the
+// other. Explicit schedule: item blockIdx.x of the host plan. Implicit (plans
+// too large for the parameter block): rank r = key block r and query block
+// nb_q - 1 - r, every head, unsplit, GQA partial slot kb * nq + h.
 template <int D>
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                       const BwdParams p, const int nq, const int nb_kv, const int nb_q) {
-    // rank r: key block r (the low blocks see the most queries) and query
-    // block nb_q - 1 - r (the high blocks see the most keys), every head;
-    // past the shorter of the two ranges only the longer kind remains
+                       const BwdParams p, const __grid_constant__ BwdSched sched, const int nq, const int nb_kv,
+                       const int nb_q) {
+    if (sched.n > 0) {
+        BLK(0);
+        const uint2 it = sched.item[blockIdx.x];
+        const int h = (it.x >> 24) & 127, b = (it.x >> 16) & 255, c0 = (it.x >> 8) & 255, c1 = it.x & 255;
+        if (it.x >> 31)
+            attn_bwd_dq_body<D>(tm_k, tm_v, p, b, h, c0, c1, it.y);
+        else
+            attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q, tm_do, p, b, h, c0, c1, it.y);
+        BLK(1);
+        return;
+    }
     const int both = min(nb_kv, nb_q);
     int rank, rem;
     bool dkdv;
@@ -1287,16 +1355,178 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         dkdv = nb_kv > nb_q;
     }
     if (dkdv)
-        attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q, tm_do, p, rank, rem);
+        attn_bwd_dkdv_body<D>(tm_k, tm_v, tm_q, tm_do, p, rank, rem, 0, -1,
+                              p.group > 1 ? static_cast<uint32_t>(rank * nq + rem) : kDirect);
     else
-        attn_bwd_dq_body<D>(tm_k, tm_v, p, nb_q - 1 - rank, rem);
+        attn_bwd_dq_body<D>(tm_k, tm_v, p, nb_q - 1 - rank, rem, 0, -1, kDirect);
 }
+
+// Fixed-order sum of the partial slots -> bf16 dK / dV (blocks with partials:
+// GQA group > 1 or split) and dQ (split blocks). Thread = 8 consecutive d of one
+// row; the slots of (kv head, block) are its heads' chunks in (head, chunk) order.
+// (A variant where the last-arriving contributor CTA summed its block's slots
+// instead of this launch measured slower on B200: 75 -> 113 us at TP = 8.)
+template <int D>
+__global__ void __launch_bounds__(256) attn_bwd_reduce(const float* __restrict__ dk_part,
+                                                       const float* __restrict__ dv_part,
+                                                       const float* __restrict__ dq_part, __nv_bfloat16* dk,
+                                                       __nv_bfloat16* dv, __nv_bfloat16* dq, long long lddkv,
+                                                       long long lddq, int T, int T_kv, int nq, int group,
+                                                       int nb_kv, int nb_q, const __grid_constant__ BwdSlots tb) {
+    constexpr int V = D / 8;
+    const int nkv = nq / group;
+    const long long n_kv = static_cast<long long>(nkv) * nb_kv * BKV * V;
+    const long long n_all = n_kv + static_cast<long long>(nq) * nb_q * BQ * V;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_all;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const bool kv = i < n_kv;
+        const long long j = kv ? i : i - n_kv;
+        const int d8 = static_cast<int>(j % V);
+        const int r = static_cast<int>((j / V) % BKV);
+        const long long hb = j / (static_cast<long long>(V) * BKV);
+        const int nb = kv ? nb_kv : nb_q;
+        const int b = static_cast<int>(hb % nb), hh = static_cast<int>(hb / nb);
+        const uint32_t base = kv ? tb.kv_base[b] : tb.q_base[b];
+        const int row = b * BKV + r;
+        if (base == kDirect || row >= (kv ? T_kv : T)) continue;
+        const int nck = kv ? tb.kv_nck[b] : tb.q_nck[b];
+        const int heads = kv ? group : 1, h0 = kv ? hh * group : hh;
+        float sk[8] = {}, sv[8] = {};
+        for (int s2 = 0; s2 < heads * nck; ++s2) {
+            const long long off = ((static_cast<long long>(base) + h0 * nck + s2) * BKV + r) * D + d8 * 8;
+            const float* src = kv ? dk_part : dq_part;
+            const float4 a0 = *reinterpret_cast<const float4*>(src + off);
+            const float4 a1 = *reinterpret_cast<const float4*>(src + off + 4);
+            sk[0] += a0.x; sk[1] += a0.y; sk[2] += a0.z; sk[3] += a0.w;
+            sk[4] += a1.x; sk[5] += a1.y; sk[6] += a1.z; sk[7] += a1.w;
+            if (kv) {
+                const float4 b0 = *reinterpret_cast<const float4*>(dv_part + off);
+                const float4 b1 = *reinterpret_cast<const float4*>(dv_part + off + 4);
+                sv[0] += b0.x; sv[1] += b0.y; sv[2] += b0.z; sv[3] += b0.w;
+                sv[4] += b1.x; sv[5] += b1.y; sv[6] += b1.z; sv[7] += b1.w;
+            }
+        }
+        if (kv) {
+            *reinterpret_cast<uint4*>(dk + static_cast<long long>(row) * lddkv + hh * D + d8 * 8) = pack8(sk);
+            *reinterpret_cast<uint4*>(dv + static_cast<long long>(row) * lddkv + hh * D + d8 * 8) = pack8(sv);
+        } else {
+            *reinterpret_cast<uint4*>(dq + static_cast<long long>(row) * lddq + hh * D + d8 * 8) = pack8(sk);
+        }
+    }
+}
+
+// Backward work plan: items and partial slots for (T, T_kv, query offset,
+// heads, GQA group, SMs). Costs per item in cycles from clock64 traces of the
+// kernel on B200 (tools/attn_trace.py): dK/dV 2650 per 128-query tile + 3000,
+// dQ 1755 per 128-key tile + 2500. An item costlier than the average per-SM
+// load is split into ceil(cost / average) chunks of its inner loop.
+struct BwdPlan {
+    std::vector<uint2> items;  // empty: implicit schedule
+    BwdSlots slots;
+    long long kv_slots = 0, q_slots = 0;
+};
+
+const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int, int>, BwdPlan> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(T, T_kv, qo, nq, group);
+    auto f = cache.find(key);
+    if (f != cache.end()) return &f->second;
+    const int nb_kv = (T_kv + BKV - 1) / BKV, nb_q = (T + BQ - 1) / BQ, nq128 = nb_q;
+    if (nb_kv > kMaxBwdBlocks || nb_q > kMaxBwdBlocks) return nullptr;
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    auto n_kv = [&](int kb) { return std::max(0, nq128 - std::max(0, kb - qo)); };
+    auto n_q = [&](int qb) { return std::min(qo + qb + 1, nb_kv); };
+    auto cost_kv = [](int n) { return 2650.0 * n + 3000.0; };
+    auto cost_q = [](int n) { return 1755.0 * n + 2500.0; };
+    double W = 0.0;
+    for (int b = 0; b < nb_kv; ++b) W += nq * cost_kv(n_kv(b));
+    for (int b = 0; b < nb_q; ++b) W += nq * cost_q(n_q(b));
+    // split threshold: a fraction of the mean per-SM load. Off by default
+    // (DH_ATTN_SPLIT_FRAC unset): on B200 the TP = 8 shapes ran slower split
+    // (frac 1: 75.0 -> 80.3 us, 0.5: 90.1 us) - the kernel is power-capped, so
+    // the partial-slot traffic costs more than the better balance recovers.
+    static const double frac = [] {
+        const char* e = std::getenv("DH_ATTN_SPLIT_FRAC");
+        return e ? std::atof(e) : 1e30;
+    }();
+    const double L = W / sms * frac;
+    auto chunks = [&](double c, int n) { return n < 2 ? 1 : std::clamp(static_cast<int>(std::ceil(c / L)), 1, std::min(n, 255)); };
+    BwdPlan pl;
+    long long count = 0;
+    std::vector<int> nck_kv(nb_kv), nck_q(nb_q);
+    for (int b = 0; b < nb_kv; ++b) count += nq * (nck_kv[b] = chunks(cost_kv(n_kv(b)), n_kv(b)));
+    for (int b = 0; b < nb_q; ++b) count += nq * (nck_q[b] = chunks(cost_q(n_q(b)), n_q(b)));
+    const bool expl = count <= kMaxBwdItems && nq <= 127 && nq128 <= 255 && nb_kv <= 255;
+    uint32_t run = 0;
+    for (int b = 0; b < kMaxBwdBlocks; ++b) {
+        pl.slots.kv_base[b] = pl.slots.q_base[b] = kDirect;
+        pl.slots.kv_nck[b] = pl.slots.q_nck[b] = 1;
+    }
+    for (int b = 0; b < nb_kv; ++b) {
+        const int nck = expl ? nck_kv[b] : 1;
+        pl.slots.kv_nck[b] = static_cast<uint8_t>(nck);
+        if (group > 1 || nck > 1) {
+            pl.slots.kv_base[b] = run;
+            run += nq * nck;
+        }
+    }
+    pl.kv_slots = run;
+    run = 0;
+    for (int b = 0; b < nb_q; ++b) {
+        const int nck = expl ? nck_q[b] : 1;
+        pl.slots.q_nck[b] = static_cast<uint8_t>(nck);
+        if (nck > 1) {
+            pl.slots.q_base[b] = run;
+            run += nq * nck;
+        }
+    }
+    pl.q_slots = run;
+    if (expl) {
+        struct It {
+            double cost;
+            uint2 it;
+        };
+        std::vector<It> its;
+        for (int kind = 0; kind < 2; ++kind) {
+            const int nb = kind ? nb_q : nb_kv;
+            for (int b = 0; b < nb; ++b) {
+                const int n = kind ? n_q(b) : n_kv(b);
+                const int nck = kind ? pl.slots.q_nck[b] : pl.slots.kv_nck[b];
+                const uint32_t base = kind ? pl.slots.q_base[b] : pl.slots.kv_base[b];
+                for (int h = 0; h < nq; ++h)
+                    for (int c = 0; c < nck; ++c) {
+                        const int c0 = n * c / nck, c1 = n * (c + 1) / nck;
+                        const uint32_t x = (static_cast<uint32_t>(kind) << 31) | (static_cast<uint32_t>(h) << 24) |
+                                           (static_cast<uint32_t>(b) << 16) | (static_cast<uint32_t>(c0) << 8) |
+                                           static_cast<uint32_t>(c1);
+                        const uint32_t y = base == kDirect ? kDirect : base + h * nck + c;
+                        its.push_back({kind ? cost_q(c1 - c0) : cost_kv(c1 - c0), make_uint2(x, y)});
+                    }
+            }
+        }
+        std::stable_sort(its.begin(), its.end(), [](const It& a, const It& b) { return a.cost > b.cost; });
+        for (const It& t : its) pl.items.push_back(t.it);
+    }
+    return &cache.emplace(key, std::move(pl)).first->second;
+}
+
+long long align4(long long n) { return (n + 3) / 4 * 4; }
 
 template <int D>
 int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, long long ldkv, const void* dout,
-                  long long ldo, const float* lse, const float* dvec, float* dk_part, float* dv_part, void* dq,
-                  void* dk, void* dv, long long lddq, long long lddkv, int T, int nq, int nkv, float scale,
-                  int T_kv, int q_offset, cudaStream_t s) {
+                  long long ldo, const float* lse, const float* dvec, float* part, void* dq, void* dk, void* dv,
+                  long long lddq, long long lddkv, int T, int nq, int nkv, float scale, int T_kv, int q_offset,
+                  cudaStream_t s) {
+    const int group = nq / nkv;
+    const BwdPlan* pl = bwd_plan(T, T_kv, q_offset / BQ, nq, group);
+    if (!pl) return set_error(DH_ERR_INVALID, "attn_bwd: more than 256 blocks of 128 rows");
     CUtensorMap mk, mv, mq, mdo;
     const long long qcols = static_cast<long long>(nq) * D, kvcols = static_cast<long long>(nkv) * D;
     int rc = make_tma_2d(&mk, k, kvcols, T_kv, ldkv, 64, 128);
@@ -1310,33 +1540,59 @@ int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
         DH_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
-    BwdParams prm{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(dout), ldq, ldo,
-                  lse, dvec, dk_part, dv_part, static_cast<__nv_bfloat16*>(dk),
-                  static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
-                  nq / nkv, scale, scale * kLog2e, T_kv, q_offset / BQ};
     const int nb_kv = (T_kv + BKV - 1) / BKV, nb_q = (T + BQ - 1) / BQ;
-    attn_bwd_tc_kernel<D><<<(nb_kv + nb_q) * nq, kThreadsBwd, smem, s>>>(mk, mv, mq, mdo, prm, nq, nb_kv,
-                                                                        nb_q);
+    float* dk_part = part;
+    float* dv_part = dk_part + pl->kv_slots * BKV * D;
+    float* dq_part = dv_part + pl->kv_slots * BKV * D;
+    BwdParams prm{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(dout), ldq, ldo,
+                  lse, dvec, dk_part, dv_part, dq_part, static_cast<__nv_bfloat16*>(dk),
+                  static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
+                  group, scale, scale * kLog2e, T_kv, q_offset / BQ};
+    static BwdSched sched;  // host staging of the kernel parameter (launches are serialised per process)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    sched.n = static_cast<int>(pl->items.size());
+    std::copy(pl->items.begin(), pl->items.end(), sched.item);
+    const int grid = sched.n > 0 ? sched.n : (nb_kv + nb_q) * nq;
+    attn_bwd_tc_kernel<D><<<grid, kThreadsBwd, smem, s>>>(mk, mv, mq, mdo, prm, sched, nq, nb_kv, nb_q);
     DH_CUDA_CHECK(cudaGetLastError());
+    if (pl->kv_slots + pl->q_slots > 0) {
+        const long long work = (static_cast<long long>(nkv) * nb_kv + static_cast<long long>(nq) * nb_q) * BKV * (D / 8);
+        const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 148 * 8));
+        attn_bwd_reduce<D><<<blocks, 256, 0, s>>>(dk_part, dv_part, dq_part, static_cast<__nv_bfloat16*>(dk),
+                                                  static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq),
+                                                  lddkv, lddq, T, T_kv, nq, group, nb_kv, nb_q, pl->slots);
+        DH_CUDA_CHECK(cudaGetLastError());
+    }
     return DH_OK;
 }
 
 }  // namespace
 
-// Host launcher for the tcgen05 backward (dvec must already hold
-// D_i = rowsum(dO * O)); dk_part / dv_part are used only when group > 1.
+// Scratch of the tcgen05 backward: D_i = rowsum(dO * O) [nq * T] (16-byte
+// aligned), then the plan's dK, dV and dQ partial slots.
+long long attn_bwd_tc_scratch_floats(int T, int nq, int nkv, int D, int T_kv, int q_offset) {
+    if (nkv <= 0 || nq % nkv || T <= 0) return 0;
+    const BwdPlan* pl = bwd_plan(T, T_kv, q_offset / BQ, nq, nq / nkv);
+    if (!pl) return 0;
+    return align4(static_cast<long long>(nq) * T) + (2 * pl->kv_slots + pl->q_slots) * BKV * D;
+}
+
+// Host launcher for the tcgen05 backward. scratch: attn_bwd_tc_scratch_floats
+// floats; dvec (its first nq * T floats) must already hold rowsum(dO * O).
 int attn_bwd_tc(const void* q, const void* k, const void* v, long long ldq, long long ldkv,
-                const void* dout, long long ldo, const float* lse, const float* dvec, float* dk_part,
-                float* dv_part, void* dq, void* dk, void* dv, long long lddq, long long lddkv, int T,
-                int nq, int nkv, int D, float scale, int T_kv, int q_offset, cudaStream_t s) {
+                const void* dout, long long ldo, const float* lse, float* scratch, void* dq, void* dk, void* dv,
+                long long lddq, long long lddkv, int T, int nq, int nkv, int D, float scale, int T_kv,
+                int q_offset, cudaStream_t s) {
     if (q_offset % (2 * BQ) || q_offset + T > T_kv)
         return set_error(DH_ERR_INVALID, "attn_bwd: q_offset must be a multiple of 256 and q_offset + T <= T_kv");
+    float* part = scratch + align4(static_cast<long long>(nq) * T);
     if (D == 128)
-        return attn_bwd_tc_d<128>(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq,
-                                  lddkv, T, nq, nkv, scale, T_kv, q_offset, s);
+        return attn_bwd_tc_d<128>(q, k, v, ldq, ldkv, dout, ldo, lse, scratch, part, dq, dk, dv, lddq, lddkv, T, nq,
+                                  nkv, scale, T_kv, q_offset, s);
     if (D == 64)
-        return attn_bwd_tc_d<64>(q, k, v, ldq, ldkv, dout, ldo, lse, dvec, dk_part, dv_part, dq, dk, dv, lddq,
-                                 lddkv, T, nq, nkv, scale, T_kv, q_offset, s);
+        return attn_bwd_tc_d<64>(q, k, v, ldq, ldkv, dout, ldo, lse, scratch, part, dq, dk, dv, lddq, lddkv, T, nq,
+                                 nkv, scale, T_kv, q_offset, s);
     return set_error(DH_ERR_INVALID, "attn: head_dim must be 64 or 128");
 }
 

@@ -284,7 +284,8 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     b.dkv_loc = pool.take(SF ? S * KV * 2 : 0, "act.bwd_transient");
     {
         const int SK = SF ? k.seq_full : static_cast<int>(S), qoff = k.cp_rank * static_cast<int>(S);
-        const size_t bwd = static_cast<size_t>(dh_attn_bwd_scratch_floats(static_cast<int>(S), k.nq_l, k.head_dim, SK));
+        const size_t bwd = static_cast<size_t>(
+            dh_attn_bwd_scratch_floats_ex(static_cast<int>(S), k.nq_l, k.nkv_l, k.head_dim, SK, SF ? qoff : 0));
         const size_t fwd = static_cast<size_t>(
             dh_attn_fwd_scratch_floats_ex(static_cast<int>(S), k.nq_l, k.nkv_l, k.head_dim, SK, SF ? qoff : 0));
         b.attn_scratch = pool.take(std::max(bwd, fwd) * 4, "act.bwd_transient");

@@ -56,6 +56,7 @@ _SIGS = {
                     c_int, c_float, c_void_p],
     "dh_attn_fwd_scratch_floats_ex": [c_int, c_int, c_int, c_int, c_int, c_int],
     "dh_attn_bwd_scratch_floats": [c_int, c_int, c_int, c_int],
+    "dh_attn_bwd_scratch_floats_ex": [c_int, c_int, c_int, c_int, c_int, c_int],
     "dh_attn_fwd_ex": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
                        c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_float, c_void_p],
     "dh_attn_bwd_ex": [c_void_p, c_void_p, c_void_p, c_ll, c_ll, c_void_p, c_ll, c_void_p, c_void_p,
@@ -98,6 +99,7 @@ def lib():
         l.dh_attn_fwd_scratch_floats.restype = c_ll
         l.dh_attn_fwd_scratch_floats_ex.restype = c_ll
         l.dh_attn_bwd_scratch_floats.restype = c_ll
+        l.dh_attn_bwd_scratch_floats_ex.restype = c_ll
         if hasattr(l, "dh_moe_router_bwd_scratch_floats"):
             l.dh_moe_router_bwd_scratch_floats.restype = c_ll
         _lib = l
@@ -198,13 +200,21 @@ def attn_fwd(q, k, v, o, lse, n_q_heads, n_kv_heads, head_dim, scale, stream=Non
                             n_q_heads, n_kv_heads, head_dim, scale, _stream(stream)))
 
 
+def attn_bwd_scratch_floats(tokens, n_q_heads, n_kv_heads, head_dim, tokens_kv=None, q_offset=0):
+    """fp32 scratch of the attention backward (its work plan's partial slots)."""
+    return int(lib().dh_attn_bwd_scratch_floats_ex(tokens, n_q_heads, n_kv_heads, head_dim,
+                                                   tokens if tokens_kv is None else tokens_kv, q_offset))
+
+
 def attn_bwd(q, k, v, o, lse, do, dq, dk, dv, n_q_heads, n_kv_heads, head_dim, scale,
              scratch=None, stream=None):
     import torch
     tokens = q.shape[0]
+    need = attn_bwd_scratch_floats(tokens, n_q_heads, n_kv_heads, head_dim)
     if scratch is None:
-        scratch = torch.empty(tokens * n_q_heads * (2 * head_dim + 1), dtype=torch.float32,
-                              device=q.device)
+        scratch = torch.empty(need, dtype=torch.float32, device=q.device)
+    elif scratch.numel() < need:
+        raise DeviceError(f"attn_bwd: scratch has {scratch.numel()} floats, needs {need}")
     check(lib().dh_attn_bwd(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o),
                             o.stride(0), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv),
                             dq.stride(0), dk.stride(0), _ptr(scratch), tokens, n_q_heads,
@@ -228,8 +238,8 @@ def attn_bwd_cp(q, k, v, o, lse, do, dq, dk, dv, q_offset, n_q_heads, n_kv_heads
     (the gradient from these queries only)."""
     import torch
     tq, tk = q.shape[0], k.shape[0]
-    scratch = torch.empty(int(lib().dh_attn_bwd_scratch_floats(tq, n_q_heads, head_dim, tk)), dtype=torch.float32,
-                          device=q.device)
+    scratch = torch.empty(attn_bwd_scratch_floats(tq, n_q_heads, n_kv_heads, head_dim, tk, q_offset),
+                          dtype=torch.float32, device=q.device)
     check(lib().dh_attn_bwd_ex(_ptr(q), _ptr(k), _ptr(v), q.stride(0), k.stride(0), _ptr(o), o.stride(0),
                                _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv), dq.stride(0), dk.stride(0),
                                _ptr(scratch), tq, tk, q_offset, n_q_heads, n_kv_heads, head_dim, scale,

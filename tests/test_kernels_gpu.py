@@ -145,7 +145,7 @@ def _attn_ref(q, k, v, nq, nkv, d, scale):
 
 @pytest.mark.parametrize("T,nq,nkv,d", [(128, 4, 1, 64), (256, 4, 4, 128), (1000, 8, 2, 128),
                                         (4096, 4, 1, 128), (1000, 8, 2, 64), (2048, 4, 1, 64),
-                                        (384, 2, 2, 64)])
+                                        (384, 2, 2, 64), (8192, 1, 1, 128), (2048, 16, 4, 128)])
 def test_attention_fwd_bwd(T, nq, nkv, d):
     scale = d ** -0.5
     # packed qkv rows, as the qkv GEMM writes them
@@ -162,6 +162,8 @@ def test_attention_fwd_bwd(T, nq, nkv, d):
     o_ref.backward(do.float())
     dqkv = torch.empty_like(qkv)
     dq, dk, dv = dqkv[:, :nq * d], dqkv[:, nq * d:(nq + nkv) * d], dqkv[:, (nq + nkv) * d:]
+    # the backward's work plan: split items (few heads) write partial slots
+    assert dh.attn_bwd_scratch_floats(T, nq, nkv, d) >= nq * T
     dh.attn_bwd(q, k, v, o, lse, do, dq, dk, dv, nq, nkv, d, scale)
     assert _rel(dq, qf.grad) < 1e-2
     assert _rel(dk, kf.grad) < 1e-2

@@ -20,7 +20,7 @@ for T, nq, nkv, d in [(4096, 4, 1, 128), (4096, 8, 2, 128), (4096, 16, 4, 128), 
     lse = torch.empty(nq, T, device="cuda")
     do = torch.randn_like(o)
     dqkv = torch.empty_like(qkv)
-    scratch = torch.empty(T * nq * (2 * d + 1), device="cuda")
+    scratch = torch.empty(dh.attn_bwd_scratch_floats(T, nq, nkv, d), device="cuda")
     f = timeit(lambda: dh.attn_fwd(q, k, v, o, lse, nq, nkv, d, d ** -0.5))
     f_nosplit = timeit(lambda: dh.attn_fwd(q, k, v, o, lse, nq, nkv, d, d ** -0.5, split=False))
     b = timeit(lambda: dh.attn_bwd(q, k, v, o, lse, do, dqkv[:, :nq * d], dqkv[:, nq * d:(nq + nkv) * d],

@@ -11,7 +11,7 @@ o = torch.empty(T, nq * d, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(nq, T, device="cuda")
 do = torch.randn_like(o)
 dqkv = torch.empty_like(qkv)
-scratch = torch.empty(T * nq * (2 * d + 1), device="cuda")
+scratch = torch.empty(dh.attn_bwd_scratch_floats(T, nq, nkv, d), device="cuda")
 for _ in range(2):
     dh.attn_fwd(q, k, v, o, lse, nq, nkv, d, d ** -0.5)
     dh.attn_bwd(q, k, v, o, lse, do, dqkv[:, :nq * d], dqkv[:, nq * d:(nq + nkv) * d],
