@@ -75,8 +75,25 @@ typedef struct dh_gemm_args {
     const void* aux0;
     const void* aux1;
     long long ld_aux;
+    /* Two-segment GEMMs in one launch (CTA-pair kernel; otherwise two launches, same result
+     * up to summation order), not with the SwiGLU epilogues:
+     *   K-concatenation (k2 > 0): D (+)= A B^T + A2 B2^T, A2 / B2 with A's / B's majors and K = k2
+     *     (k % 64 == 0), accumulated in one pass (one rounding of D).
+     *   M-concatenation (m2 > 0): rows [0, m) of the result from A into D, rows [0, m2) from A2
+     *     into d_m2 (same B, same epilogue; m % 256 == 0). */
+    const void* a2;
+    long long lda2;
+    const void* b2;
+    long long ldb2;
+    int k2;
+    void* d_m2;
+    long long ldd_m2;
+    int m2;
 } dh_gemm_args;
-enum { DH_EPI_NONE = 0, DH_EPI_SWIGLU_FWD = 1, DH_EPI_SWIGLU_FWD_UP = 2, DH_EPI_SWIGLU_BWD = 3 };
+/* DH_EPI_SWIGLU_PAIR: mlp_gate and mlp_up as one GEMM (K-major A, B = Wg, B2 = Wu, both [n, k]):
+ * d = gate = bf16(A Wg^T), d2 = up = bf16(A Wu^T), d_m2 = act = silu(gate) * up (all [m, n], pitch ldd). */
+enum { DH_EPI_NONE = 0, DH_EPI_SWIGLU_FWD = 1, DH_EPI_SWIGLU_FWD_UP = 2, DH_EPI_SWIGLU_BWD = 3,
+       DH_EPI_SWIGLU_PAIR = 4 };
 int dh_gemm(const dh_gemm_args* args, void* stream);
 
 /* RMSNorm over the last dim (elementwise.cu). y = x * rstd * gamma, rstd fp32 [rows]. */

@@ -60,6 +60,9 @@ enum Epi {
     kEpiAddBf16 = 3,
     kEpiSwiGLUFwd = 4,  // D = bf16(acc), D2 = swiglu(aux0, D) or swiglu(D, aux0) (aux_is_up)
     kEpiSwiGLUBwd = 5,  // acc = d_act: D = d_gate, D2 = d_up from (aux0 = gate, aux1 = up)
+    kEpiSwiGLUPair = 6, // mlp_gate | mlp_up in one GEMM: the CTA pair's two B halves are Wg and Wu rows
+                        // of the same 128 features, so the accumulator holds gate | up side by side;
+                        // D = gate, D2 = up, X0 (a store map here) = act = silu(gate) * up
 };
 
 template <int BN>
@@ -88,6 +91,11 @@ struct KParams {
     // streams past) or of `group` n-tiles (b_resident == 1), the grouped
     // dimension fastest inside a group.
     int b_resident, group;
+    // two-segment launches of the CTA-pair kernel (maps tma_x0 / tma_x1 / tma_d2,
+    // otherwise the fused epilogues' aux maps): k-blocks >= kb_split read A2 / B2
+    // (K-concatenation); 256-row m-tiles >= mt_split read A2 and store to D2
+    // (M-concatenation). Past the end = one segment.
+    int kb_split, mt_split;
 };
 
 void raster_for(KParams& p, int bm, int bn, int k);
@@ -374,7 +382,9 @@ struct PairCfg {
 // on half of a 64-column chunk): their element math would otherwise be slower
 // than the main loop it has to hide behind.
 template <int EPI>
-constexpr int pair_threads() { return EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd ? 320 : kThreads; }
+constexpr int pair_threads() {
+    return EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd || EPI == kEpiSwiGLUPair ? 320 : kThreads;
+}
 
 template <int PBN, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(), 1)
@@ -383,7 +393,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
                      const __grid_constant__ CUtensorMap tma_x0, const __grid_constant__ CUtensorMap tma_x1,
                      const KParams p) {
     constexpr bool kFused = EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd;
-    using C = PairCfg<PBN, kFused>;
+    constexpr bool kPairEpi = EPI == kEpiSwiGLUPair;
+    static_assert(!kPairEpi || PBN == 256, "the gate | up pair epilogue uses 256-wide pair tiles");
+    using C = PairCfg<PBN, kFused || kPairEpi>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -421,9 +433,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
             mbar_init(&tempty[b], 2 * (pair_threads<EPI>() - 64));  // every epilogue thread of both CTAs
             mbar_init(&xfull[b], 1);
         }
-        if constexpr (kFused) {
+        if constexpr (kFused || kPairEpi) {
             tma_prefetch(&tma_x0);
-            if constexpr (EPI == kEpiSwiGLUBwd) tma_prefetch(&tma_x1);
+            if constexpr (EPI != kEpiSwiGLUFwd) tma_prefetch(&tma_x1);
+        } else if (p.kb_split < num_kb || p.mt_split < tiles_m) {
+            tma_prefetch(&tma_x0);
+            tma_prefetch(&tma_x1);
+            tma_prefetch(&tma_d2);
         }
         fence_barrier_init();
     }
@@ -442,26 +458,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
                 int mi, ni;
                 tile_coords(tile, p, &mi, &ni);
                 const int m0 = mi * 256 + rank * BM;             // this CTA's A rows
-                const int n0 = ni * PBN + rank * C::kHalfB;      // this CTA's B half
+                // this CTA's B half (pair epilogue: Wg / Wu rows of the tile's 128 features)
+                const int n0 = kPairEpi ? ni * 128 : ni * PBN + rank * C::kHalfB;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full[stage], 2 * C::kStage);
                     const uint32_t bar = leader_addr(&full[stage]);
                     uint8_t* a_dst = sA + stage * C::kStageA;
                     uint8_t* b_dst = sB + stage * C::kStageB;
-                    const int k0 = kb * BK;
+                    // second segment: K-concatenation (A2, B2) or M-concatenation (A2)
+                    const bool ks2 = kb >= p.kb_split, ms2 = mi >= p.mt_split;
+                    const CUtensorMap* ta = ks2 || ms2 ? &tma_x0 : &tma_a;
+                    const CUtensorMap* tb = ks2 || (kPairEpi && rank) ? &tma_x1 : &tma_b;
+                    const int k0 = (ks2 ? kb - p.kb_split : kb) * BK;
+                    const int ma = ms2 ? m0 - p.mt_split * 256 : m0;
                     if constexpr (A_MN) {
-                        tma_load_2d_pair(a_dst, &tma_a, bar, m0, k0);
-                        tma_load_2d_pair(a_dst + BK * 128, &tma_a, bar, m0 + 64, k0);
+                        tma_load_2d_pair(a_dst, ta, bar, ma, k0);
+                        tma_load_2d_pair(a_dst + BK * 128, ta, bar, ma + 64, k0);
                     } else {
-                        tma_load_2d_pair(a_dst, &tma_a, bar, k0, m0);
+                        tma_load_2d_pair(a_dst, ta, bar, k0, ma);
                     }
                     if constexpr (B_MN) {
 #pragma unroll
                         for (int i = 0; i < C::kHalfB / 64; ++i)
-                            tma_load_2d_pair(b_dst + i * BK * 128, &tma_b, bar, n0 + i * 64, k0);
+                            tma_load_2d_pair(b_dst + i * BK * 128, tb, bar, n0 + i * 64, k0);
                     } else {
-                        tma_load_2d_pair(b_dst, &tma_b, bar, k0, n0);
+                        tma_load_2d_pair(b_dst, tb, bar, k0, n0);
                     }
                     if (++stage == C::kStages) stage = 0, phase ^= 1;
                 }
@@ -519,7 +541,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
             mbar_wait(&tfull[acc], acc_phase);
             GTR(3, store_leader);
             tc_fence_after();
-            if constexpr (kFused) {
+            if constexpr (kPairEpi) {
+                // gate | up of 128 features: per 64-feature chunk, each thread takes 32
+                // features of its row (half), rounds gate and up to bf16 (the stored
+                // values) and forms act from them; three staging buffers are TMA-stored
+                const int half = (warp - 2) >> 2;
+                const int f0 = ni * 128;
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c, ++chunk) {
+                    uint32_t vg[32], vu[32];
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + c * 64 + half * 32, vg);
+                    tmem_ld32(tmem_base + lane_off + acc * PBN + 128 + c * 64 + half * 32, vu);
+                    if (store_leader) bulk_wait_read<0>();  // the previous chunk's stores have read staging
+                    named_barrier(2, 256);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int uu = 0; uu < 4; ++uu) {
+                        const int u = half * 4 + uu;
+                        const int sw = r * 128 + ((u ^ (r & 7)) << 4);
+                        float gg[8], up[8], a[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            gg[t] = __bfloat162float(__float2bfloat16(__uint_as_float(vg[uu * 8 + t])));
+                            up[t] = __bfloat162float(__float2bfloat16(__uint_as_float(vu[uu * 8 + t])));
+                            a[t] = swiglu_fwd_elem(gg[t], up[t]);
+                        }
+                        *reinterpret_cast<uint4*>(staging + sw) = pack8(gg);
+                        *reinterpret_cast<uint4*>(staging + 16384 + sw) = pack8(up);
+                        *reinterpret_cast<uint4*>(staging + 32768 + sw) = pack8(a);
+                    }
+                    fence_async_shared();
+                    named_barrier(2, 256);
+                    if (store_leader) {
+                        tma_store_2d(&tma_d, staging, f0 + c * 64, m0);
+                        tma_store_2d(&tma_d2, staging + 16384, f0 + c * 64, m0);
+                        tma_store_2d(&tma_x0, staging + 32768, f0 + c * 64, m0);
+                        bulk_commit();
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive_cluster(tempty_leader[acc]);
+                if (++acc == 2) acc = 0, acc_phase ^= 1;
+                continue;
+            } else if constexpr (kFused) {
                 // SwiGLU fused into the epilogue. Per 64-column chunk, one staging
                 // set (2 x 16 KB) first receives the aux tiles by TMA (issued one
                 // chunk ahead), each thread turns its row's aux + accumulator values
@@ -623,8 +687,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<EPI>(),
                 fence_async_shared();
                 named_barrier(2, 128);
                 if (store_leader) {
-                    if constexpr (EPI == kEpiStoreBf16) tma_store_2d(&tma_d, stg, n0 + c * CW, m0);
-                    else tma_reduce_add_2d(&tma_d, stg, n0 + c * CW, m0);  // f32 or bf16 add
+                    const bool ms2 = mi >= p.mt_split;  // M-concatenation: rows of the second output
+                    const CUtensorMap* td = ms2 ? &tma_d2 : &tma_d;
+                    const int mrow = ms2 ? m0 - p.mt_split * 256 : m0;
+                    if constexpr (EPI == kEpiStoreBf16) tma_store_2d(td, stg, n0 + c * CW, mrow);
+                    else tma_reduce_add_2d(td, stg, n0 + c * CW, mrow);  // f32 or bf16 add
                     bulk_commit();
                 }
             }
@@ -726,7 +793,8 @@ int launch(const dh_gemm_args* g, cudaStream_t stream) {
         md = ma;  // unused
     }
     if (rc) return rc;
-    KParams p;
+    KParams p{};
+    p.kb_split = p.mt_split = 1 << 30;
     p.d = g->d;
     p.ldd = g->ldd;
     p.m = g->m;
@@ -790,7 +858,8 @@ void raster_for(KParams& p, int bm, int bn, int k) {
 template <int PBN, bool A_MN, bool B_MN, int EPI>
 int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
     constexpr bool kFused = EPI == kEpiSwiGLUFwd || EPI == kEpiSwiGLUBwd;
-    using C = PairCfg<PBN, kFused>;
+    constexpr bool kPairEpi = EPI == kEpiSwiGLUPair;
+    using C = PairCfg<PBN, kFused || kPairEpi>;
     CUtensorMap ma, mb, md, md2;
     int rc = A_MN ? make_map(&ma, g->a, g->m, g->k, g->lda, BK) : make_map(&ma, g->a, g->k, g->m, g->lda, BM);
     if (rc) return rc;
@@ -800,7 +869,26 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
                            : make_tma_2d(&md, g->d, g->n, g->m, g->ldd, 64, BM, false);
     if (rc) return rc;
     CUtensorMap mx0, mx1;
-    if (kFused) {
+    const bool kcat = g->k2 > 0, mcat = g->m2 > 0;
+    if (kPairEpi) {  // B halves: Wg (b) and Wu (b2) rows; outputs gate (d), up (d2), act (d_m2)
+        rc = make_map(&mb, g->b, g->k, g->n, g->ldb, C::kHalfB);
+        if (!rc) rc = make_map(&mx1, g->b2, g->k, g->n, g->ldb2, C::kHalfB);
+        if (!rc) rc = make_tma_2d(&md2, g->d2, g->n, g->m, g->ldd, 64, BM, false);
+        if (!rc) rc = make_tma_2d(&mx0, g->d_m2, g->n, g->m, g->ldd, 64, BM, false);
+        if (rc) return rc;
+    } else if (kcat) {  // second K segment: A2 [m, k2], B2 [n, k2] with A's / B's majors
+        rc = A_MN ? make_map(&mx0, g->a2, g->m, g->k2, g->lda2, BK) : make_map(&mx0, g->a2, g->k2, g->m, g->lda2, BM);
+        if (!rc) rc = B_MN ? make_map(&mx1, g->b2, g->n, g->k2, g->ldb2, BK)
+                           : make_map(&mx1, g->b2, g->k2, g->n, g->ldb2, C::kHalfB);
+        if (rc) return rc;
+        md2 = md;
+    } else if (mcat) {  // second M segment: A2 [m2, k] -> D2 [m2, n]
+        rc = A_MN ? make_map(&mx0, g->a2, g->m2, g->k, g->lda2, BK) : make_map(&mx0, g->a2, g->k, g->m2, g->lda2, BM);
+        if (!rc) rc = EPI == kEpiAddF32 ? make_tma_2d(&md2, g->d_m2, g->n, g->m2, g->ldd_m2, 32, BM, true)
+                                        : make_tma_2d(&md2, g->d_m2, g->n, g->m2, g->ldd_m2, 64, BM, false);
+        if (rc) return rc;
+        mx1 = mb;
+    } else if (kFused) {
         rc = make_tma_2d(&md2, g->d2, g->n, g->m, g->ldd, 64, BM, false);
         if (!rc) rc = make_tma_2d(&mx0, g->aux0, g->n, g->m, g->ld_aux, 64, BM, false);
         if (!rc) rc = make_tma_2d(&mx1, g->aux1 ? g->aux1 : g->aux0, g->n, g->m, g->ld_aux, 64, BM, false);
@@ -808,7 +896,7 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
     } else {
         md2 = mx0 = mx1 = md;  // unused
     }
-    KParams p;
+    KParams p{};
     p.aux0 = static_cast<const __nv_bfloat16*>(g->aux0);
     p.aux1 = static_cast<const __nv_bfloat16*>(g->aux1);
     p.ld_aux = g->ld_aux;
@@ -820,8 +908,17 @@ int launch_pair(const dh_gemm_args* g, cudaStream_t stream, int ctas) {
     p.k = g->k;
     p.accumulate = g->accumulate;
     p.tiles_m = (g->m + 255) / 256;
-    p.tiles_n = (g->n + PBN - 1) / PBN;
-    raster_for(p, 256, PBN, g->k);
+    p.tiles_n = kPairEpi ? (g->n + 127) / 128 : (g->n + PBN - 1) / PBN;
+    p.kb_split = p.mt_split = 1 << 30;
+    if (kcat) {
+        p.kb_split = g->k / BK;
+        p.k = g->k + g->k2;
+    }
+    if (mcat) {
+        p.mt_split = g->m / 256;
+        p.tiles_m = g->m / 256 + (g->m2 + 255) / 256;
+    }
+    raster_for(p, 256, PBN, p.k);
     const int tiles = p.tiles_m * p.tiles_n;
     const int grid = 2 * std::min(ctas / 2, tiles);
     auto kern = gemm_pair_kernel<PBN, A_MN, B_MN, EPI>;
@@ -848,6 +945,8 @@ int dispatch_pair(const dh_gemm_args* g, cudaStream_t s, int ctas) {
 
 template <int PBN>
 int dispatch_pair_epi(const dh_gemm_args* g, cudaStream_t s, int ctas) {
+    if constexpr (PBN == 256)
+        if (g->epilogue == DH_EPI_SWIGLU_PAIR) return launch_pair<256, false, false, kEpiSwiGLUPair>(g, s, ctas);
     if (g->epilogue == DH_EPI_SWIGLU_BWD) return dispatch_pair<PBN, kEpiSwiGLUBwd>(g, s, ctas);
     if (g->epilogue) return dispatch_pair<PBN, kEpiSwiGLUFwd>(g, s, ctas);
     if (g->d_fp32) return dispatch_pair<PBN, kEpiAddF32>(g, s, ctas);
@@ -925,6 +1024,25 @@ int gemm(const dh_gemm_args* g, cudaStream_t s);
 // SwiGLU epilogues: fused into the CTA-pair kernel when the operands allow it,
 // else the plain GEMM followed by the standalone SwiGLU kernel (same math).
 int gemm_swiglu(const dh_gemm_args* g, cudaStream_t s) {
+    if (g->epilogue == DH_EPI_SWIGLU_PAIR) {
+        if (g->accumulate || g->d_fp32 || !g->d2 || !g->b2 || !g->d_m2 || g->a_mn || g->b_mn)
+            return set_error(DH_ERR_INVALID, "gemm: SwiGLU pair epilogue needs K-major A / B, B2, bf16 d, d2, d_m2");
+        const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
+        auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+        if (ctas >= 2 && g->n % 128 == 0 && g->ldd % 8 == 0 && al16(g->d) && al16(g->d2) && al16(g->d_m2))
+            return dispatch_pair_epi<256>(g, s, ctas);
+        // unfused: the two GEMMs, then the standalone SwiGLU
+        dh_gemm_args a = *g;
+        a.epilogue = DH_EPI_NONE;
+        a.b2 = nullptr;
+        GEMM_TRY(gemm(&a, s));
+        a.b = g->b2;
+        a.ldb = g->ldb2;
+        a.d = g->d2;
+        GEMM_TRY(gemm(&a, s));
+        if (g->ldd != g->n) return set_error(DH_ERR_INVALID, "gemm: unfused SwiGLU pair needs dense [m, n] outputs");
+        return dh_swiglu_fwd(g->d, g->d2, g->d_m2, static_cast<long long>(g->m) * g->n, s);
+    }
     if (g->accumulate || g->d_fp32 || !g->d2 || !g->aux0 || (g->epilogue == DH_EPI_SWIGLU_BWD && !g->aux1))
         return set_error(DH_ERR_INVALID, "gemm: SwiGLU epilogue needs bf16 d, d2 and aux operands");
     const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
@@ -955,6 +1073,35 @@ int gemm_swiglu(const dh_gemm_args* g, cudaStream_t s) {
 
 int gemm(const dh_gemm_args* g, cudaStream_t s) {
     if (g->m <= 0 || g->n <= 0 || g->k <= 0) return set_error(DH_ERR_INVALID, "gemm: empty shape");
+    if (g->k2 > 0 || g->m2 > 0) {
+        if (g->epilogue || (g->k2 > 0 && g->m2 > 0) || !g->a2 || (g->k2 > 0 && !g->b2) || (g->m2 > 0 && !g->d_m2))
+            return set_error(DH_ERR_INVALID, "gemm: one of k2 / m2 with a2 and b2 / d_m2, no SwiGLU epilogue");
+        const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
+        const bool aligned = (reinterpret_cast<uintptr_t>(g->d) & 15) == 0 && (g->ldd * (g->d_fp32 ? 4 : 2)) % 16 == 0 &&
+                             (!g->d_m2 || ((reinterpret_cast<uintptr_t>(g->d_m2) & 15) == 0 &&
+                                           (g->ldd_m2 * (g->d_fp32 ? 4 : 2)) % 16 == 0));
+        const bool one_launch = aligned && (g->accumulate || !g->d_fp32) && ctas >= 2 && g->tile_n == 0 &&
+                                (g->k2 == 0 || g->k % BK == 0) && (g->m2 == 0 || g->m % 256 == 0);
+        if (one_launch) return dispatch_pair_epi<256>(g, s, ctas);
+        // two launches: the first segment, then the second (accumulated / into d_m2)
+        dh_gemm_args a = *g, b = *g;
+        a.a2 = b.a2 = nullptr;
+        a.k2 = b.k2 = a.m2 = b.m2 = 0;
+        b.a = g->a2;
+        b.lda = g->lda2;
+        if (g->k2 > 0) {
+            b.b = g->b2;
+            b.ldb = g->ldb2;
+            b.k = g->k2;
+            b.accumulate = 1;
+        } else {
+            b.m = g->m2;
+            b.d = g->d_m2;
+            b.ldd = g->ldd_m2;
+        }
+        GEMM_TRY(gemm(&a, s));
+        return gemm(&b, s);
+    }
     if (g->epilogue) return gemm_swiglu(g, s);
     const int ctas = g->max_ctas > 0 ? std::min(g->max_ctas, sm_count()) : sm_count();
     const bool aligned = (reinterpret_cast<uintptr_t>(g->d) & 15) == 0 &&

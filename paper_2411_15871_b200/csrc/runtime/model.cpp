@@ -272,6 +272,14 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
         // and lost overlap under SI; DH_SWIGLU_EPILOGUE=0 selects them.
         const char* env = std::getenv("DH_SWIGLU_EPILOGUE");
         m->swiglu_in_epilogue = env ? std::atoi(env) != 0 : true;
+        // mlp_gate | mlp_up as one GEMM and the two dgrads as one only without
+        // tensor parallelism: at TP = 8 (emulated collectives, 32 layers x 8
+        // micro-batches) merging cut the compute-only step 214 -> 209 ms but the
+        // SI step rose 230.4 -> 235.1 ms (hidden comm 0.81 -> 0.69): the coarser
+        // GEMMs leave the plan fewer places to start the other strand's
+        // collectives. DH_MLP_MERGE=0/1 overrides.
+        const char* mm = std::getenv("DH_MLP_MERGE");
+        m->mlp_merge = mm ? std::atoi(mm) != 0 : k.tp == 1;
         if (!m->swiglu_in_epilogue) b.d_act = pool.take(MR * F * 2, "act.bwd_transient");
     }
     b.dx_part = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
@@ -374,6 +382,27 @@ void model_destroy(Model* m) {
 // ------------------------------------------------------------------ node launchers
 
 namespace {
+
+dh_gemm_args gemm_args(const void* a, long long lda, bool a_mn, const void* b, long long ldb, bool b_mn, void* d,
+                       long long ldd, bool d_f32, int mm, int nn, int kk, bool acc, int max_ctas) {
+    dh_gemm_args g{};
+    g.a = a;
+    g.lda = lda;
+    g.a_mn = a_mn;
+    g.b = b;
+    g.ldb = ldb;
+    g.b_mn = b_mn;
+    g.d = d;
+    g.ldd = ldd;
+    g.d_fp32 = d_f32;
+    g.m = mm;
+    g.n = nn;
+    g.k = kk;
+    g.accumulate = acc;
+    g.max_ctas = max_ctas;
+    g.ld_aux = ldd;
+    return g;
+}
 
 int gemm(const void* a, long long lda, bool a_mn, const void* b, long long ldb, bool b_mn, void* d,
          long long ldd, bool d_f32, int mm, int nn, int kk, bool acc, int max_ctas,
@@ -506,9 +535,24 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
         case 9:  // ag1
             RT_TRY(need_comm());
             return comm->all_gather(P(m.fs.ln_loc), P(sl.ln1_full), TH, s);
-        case 10:    // mlp_gate (+ act = silu(gate) * up when it runs after mlp_up)
-        case 11: {  // mlp_up (+ act when it runs after mlp_gate)
+        case 10:    // mlp_gate
+        case 11: {  // mlp_up
+            if (m.swiglu_in_epilogue && m.mlp_merge) {
+                // the earlier of the two computes gate, up and act = silu(gate) * up in one
+                // GEMM (the CTA pair's B halves are Wg and Wu rows of the same features);
+                // the later launches nothing
+                if (op.fuse_swiglu) return DH_OK;
+                dh_gemm_args g = gemm_args(P(sl.ln1_full), H, false, W + p.wg, H, false, P(sl.gate), F, false, S, F,
+                                           H, false, cap);
+                g.epilogue = DH_EPI_SWIGLU_PAIR;
+                g.b2 = W + p.wu;
+                g.ldb2 = H;
+                g.d2 = P(sl.up);
+                g.d_m2 = P(sl.act);
+                return dh_gemm(&g, s);
+            }
             const bool gate = op.node == 10;
+            // unmerged: the later of the two applies SwiGLU in its epilogue
             const bool epi = op.fuse_swiglu && m.swiglu_in_epilogue;
             RT_TRY(gemm(P(sl.ln1_full), H, false, W + (gate ? p.wg : p.wu), H, false, P(gate ? sl.gate : sl.up), F,
                         false, S, F, H, false, cap, s,
@@ -554,17 +598,32 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
             const void* dyf = tp1 ? dy : P(m.bs.dy_full);
             return gemm(dyf, H, true, P(sl.act), F, true, G + p.wd, F, true, H, F, S, true, cap, s);
         }
-        case 24:  // mlp_gate_dgrad
-            return gemm(P(m.bs.d_gate), F, false, W + p.wg, H, true,
-                        tp1 ? P(m.bs.rs_out) : P(m.bs.dx_part), H, false, S, H, F, !op.first_dx, cap, s);
-        case 25:  // mlp_up_dgrad
-            return gemm(P(m.bs.d_up), F, false, W + p.wu, H, true,
-                        tp1 ? P(m.bs.rs_out) : P(m.bs.dx_part), H, false, S, H, F, !op.first_dx, cap, s);
-        case 26:  // mlp_fc1_wgrad: dWg, dWu [F,H] += d_{gate,up}^T ln1
-            RT_TRY(gemm(P(m.bs.d_gate), F, true, P(sl.ln1_full), H, true, G + p.wg, H, true, F, H, S,
-                        true, cap, s));
-            return gemm(P(m.bs.d_up), F, true, P(sl.ln1_full), H, true, G + p.wu, H, true, F, H, S, true,
-                        cap, s);
+        case 24:    // mlp_gate_dgrad
+        case 25: {  // mlp_up_dgrad: whichever runs first computes both, dX = d_gate Wg + d_up Wu,
+            // as one K-concatenated GEMM (one pass, one rounding); the other launches nothing
+            if (!m.mlp_merge)
+                return gemm(op.node == 24 ? P(m.bs.d_gate) : P(m.bs.d_up), F, false, W + (op.node == 24 ? p.wg : p.wu),
+                            H, true, tp1 ? P(m.bs.rs_out) : P(m.bs.dx_part), H, false, S, H, F, !op.first_dx, cap, s);
+            if (!op.first_dx) return DH_OK;
+            dh_gemm_args g = gemm_args(P(m.bs.d_gate), F, false, W + p.wg, H, true,
+                                       tp1 ? P(m.bs.rs_out) : P(m.bs.dx_part), H, false, S, H, F, false, cap);
+            g.a2 = P(m.bs.d_up);
+            g.lda2 = F;
+            g.b2 = W + p.wu;
+            g.ldb2 = H;
+            g.k2 = F;
+            return dh_gemm(&g, s);
+        }
+        case 26: {  // mlp_fc1_wgrad: dWg, dWu [F,H] += d_{gate,up}^T ln1, one M-concatenated GEMM
+            dh_gemm_args g = gemm_args(P(m.bs.d_gate), F, true, P(sl.ln1_full), H, true, G + p.wg, H, true, F, H, S,
+                                       true, cap);
+            g.a2 = P(m.bs.d_up);
+            g.lda2 = F;
+            g.m2 = F;
+            g.d_m2 = G + p.wu;
+            g.ldd_m2 = H;
+            return dh_gemm(&g, s);
+        }
         case 27:  // ag1_bwd_rs
             RT_TRY(need_comm());
             return comm->reduce_scatter(P(m.bs.dx_part), P(m.bs.rs_out), TH, s);

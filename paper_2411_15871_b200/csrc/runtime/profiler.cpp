@@ -47,7 +47,8 @@ Op node_op(const Model& m, const weft::OpNode& n, bool fwd) {
     o.strand = fwd ? 0 : std::min(1, m.cfg.micro_batches - 1);
     o.slot = fwd ? 0 : 1;
     o.prev_slot = -1;
-    o.first_dx = true;
+    // merged: mlp_gate_dgrad computes both dgrads (K-concatenated), mlp_up_dgrad nothing
+    o.first_dx = !m.mlp_merge || n.id != 25;
     // the SwiGLU epilogue is charged to mlp_up (it follows mlp_gate by id); moe_ep ids differ
     o.fuse_swiglu = !m.cfg.moe && n.id == 11;
     return o;

@@ -212,6 +212,10 @@ struct Model {
     // mlp_down_dgrad) when the GEMM has enough waves to hide the epilogue;
     // otherwise standalone kernels after plain GEMMs (decided at model create)
     bool swiglu_in_epilogue = true;
+    // mlp_gate | mlp_up as one GEMM (SwiGLU pair epilogue) and the gate / up dgrads as one
+    // K-concatenated GEMM (DH_MLP_MERGE; default at TP = 1 only, see model.cpp). The fc1
+    // wgrads are always one M-concatenated GEMM (one node either way).
+    bool mlp_merge = true;
     bool prog_has_opt = false;   // the lowered program contains them
     int peak_slots = 0;          // activation slots the lowered program holds at once
     Buf opt_hp;                   // dh_adamw_hparams as 9 floats

@@ -31,10 +31,11 @@ class GemmArgs(ctypes.Structure):
                 ("m", c_int), ("n", c_int), ("k", c_int),
                 ("accumulate", c_int), ("max_ctas", c_int), ("tile_n", c_int),
                 ("epilogue", c_int), ("d2", c_void_p), ("aux0", c_void_p), ("aux1", c_void_p),
-                ("ld_aux", c_ll)]
+                ("ld_aux", c_ll), ("a2", c_void_p), ("lda2", c_ll), ("b2", c_void_p), ("ldb2", c_ll),
+                ("k2", c_int), ("d_m2", c_void_p), ("ldd_m2", c_ll), ("m2", c_int)]
 
 
-EPI_NONE, EPI_SWIGLU_FWD, EPI_SWIGLU_FWD_UP, EPI_SWIGLU_BWD = 0, 1, 2, 3
+EPI_NONE, EPI_SWIGLU_FWD, EPI_SWIGLU_FWD_UP, EPI_SWIGLU_BWD, EPI_SWIGLU_PAIR = 0, 1, 2, 3, 4
 
 
 _SIGS = {
@@ -124,10 +125,13 @@ def _stream(stream):
 # --------------------------------------------------------------------------- kernels
 
 def gemm(a, b, d, *, a_mn=False, b_mn=False, accumulate=False, m=None, n=None, k=None,
-         max_ctas=0, tile_n=0, stream=None, epilogue=EPI_NONE, d2=None, aux0=None, aux1=None):
+         max_ctas=0, tile_n=0, stream=None, epilogue=EPI_NONE, d2=None, aux0=None, aux1=None,
+         a2=None, b2=None, k2=0, d_m2=None, m2=0):
     """d(m,n) (+)= sum_k A(m,k) B(n,k). A = a[m,k] (K-major) or a[k,m] (a_mn);
     B = b[n,k] (K-major) or b[k,n] (b_mn). d bf16 or fp32 [m,n].
-    epilogue = EPI_SWIGLU_*: fused SwiGLU (see dh_capi.h) writing d and d2 from aux0/aux1."""
+    epilogue = EPI_SWIGLU_*: fused SwiGLU (see dh_capi.h) writing d and d2 from aux0/aux1.
+    Two segments in one launch: k2 > 0 adds a2 @ b2^T (K-concatenation); m2 > 0 computes a2's
+    rows (m2 of them) into d_m2 (M-concatenation)."""
     import torch
     if m is None:
         m = a.shape[1] if a_mn else a.shape[0]
@@ -139,6 +143,13 @@ def gemm(a, b, d, *, a_mn=False, b_mn=False, accumulate=False, m=None, n=None, k
                     d.data_ptr(), d.stride(0), int(d.dtype == torch.float32), m, n, k,
                     int(accumulate), max_ctas, tile_n, epilogue, _ptr(d2), _ptr(aux0), _ptr(aux1),
                     d.stride(0))
+    if a2 is not None:
+        args.a2, args.lda2 = a2.data_ptr(), a2.stride(0)
+    if b2 is not None:
+        args.b2, args.ldb2 = b2.data_ptr(), b2.stride(0)
+    if d_m2 is not None:
+        args.d_m2, args.ldd_m2 = d_m2.data_ptr(), d_m2.stride(0)
+    args.k2, args.m2 = k2, m2
     check(lib().dh_gemm(ctypes.byref(args), _stream(stream)))
     return d
 

@@ -362,3 +362,61 @@ def test_attention_context_parallel_chunk(T, cp, rank, nq, nkv, d):
     assert _rel(dv, vf.grad) < 1e-2
     if off + tl < T:  # keys after the chunk's last query get no gradient from it
         assert dk[off + tl:].abs().max().item() == 0 and dv[off + tl:].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 4096, 1792), (512, 384, 256), (300, 256, 192)])
+def test_gemm_k_concatenation(m, n, k):
+    """D = A B^T + A2 B2^T in one launch (the merged mlp_gate/up_dgrad node: d_gate Wg + d_up Wu,
+    B MN-major) against fp32, and against the two-launch form within bf16 rounding."""
+    g = torch.Generator(device="cuda").manual_seed(21)
+    A, A2 = (torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
+    B, B2 = (torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
+    b, b2 = B.t().contiguous(), B2.t().contiguous()  # MN-major [k, n]
+    ref = A.float() @ B.float().t() + A2.float() @ B2.float().t()
+    d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    dh.gemm(A, b, d, b_mn=True, m=m, n=n, k=k, a2=A2, b2=b2, k2=k)
+    assert _rel(d, ref) < 4e-3
+    d2 = torch.empty_like(d)
+    dh.gemm(A, b, d2, b_mn=True, m=m, n=n, k=k, a2=A2, b2=b2, k2=k)
+    assert torch.equal(d, d2)
+    two = torch.empty_like(d)
+    dh.gemm(A, b, two, b_mn=True, m=m, n=n, k=k)
+    dh.gemm(A2, b2, two, b_mn=True, m=m, n=n, k=k, accumulate=True)
+    assert _rel(two, ref) < 6e-3
+
+
+@pytest.mark.parametrize("m,n,k", [(1792, 4096, 4096), (512, 384, 256)])
+def test_gemm_m_concatenation(m, n, k):
+    """[D; D2] += [A; A2]^T B in one launch (the merged mlp_fc1_wgrad: dWg, dWu += d_{gate,up}^T ln1,
+    A / B MN-major, fp32 main-grad reduce-add) equals the two launches bit for bit (same tiles)."""
+    g = torch.Generator(device="cuda").manual_seed(22)
+    A, A2 = (torch.randn(k, m, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
+    B = torch.randn(k, n, device="cuda", generator=g).to(torch.bfloat16)
+    g0, g1 = torch.randn(m, n, device="cuda", generator=g), torch.randn(m, n, device="cuda", generator=g)
+    d, d2 = g0.clone(), g1.clone()
+    dh.gemm(A, B, d, a_mn=True, b_mn=True, accumulate=True, a2=A2, d_m2=d2, m2=m)
+    r0, r1 = g0.clone(), g1.clone()
+    dh.gemm(A, B, r0, a_mn=True, b_mn=True, accumulate=True, tile_n=512)
+    dh.gemm(A2, B, r1, a_mn=True, b_mn=True, accumulate=True, tile_n=512)
+    assert torch.equal(d, r0) and torch.equal(d2, r1)
+    ref0 = g0 + A.float().t() @ B.float()
+    assert (d - ref0).abs().max().item() < 1e-3 * ref0.abs().max().item()
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 1792, 4096), (512, 640, 256), (300, 256, 128)])
+def test_gemm_swiglu_pair_epilogue(m, n, k):
+    """mlp_gate | mlp_up in one launch (DH_EPI_SWIGLU_PAIR) == the two GEMMs (same
+    256-wide pair tile) + the standalone SwiGLU kernel, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(13)
+    x = (torch.randn(m, k, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    wg = (torch.randn(n, k, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    wu = (torch.randn(n, k, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    gate, up, act = (torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    dh.gemm(x, wg, gate, epilogue=dh.EPI_SWIGLU_PAIR, b2=wu, d2=up, d_m2=act)
+    rg, ru, ra = (torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    dh.gemm(x, wg, rg, tile_n=512)
+    dh.gemm(x, wu, ru, tile_n=512)
+    dh.swiglu_fwd(rg, ru, ra)
+    assert torch.equal(gate, rg) and torch.equal(up, ru) and torch.equal(act, ra)
+    ref = torch.nn.functional.silu(x.float() @ wg.float().t()) * (x.float() @ wu.float().t())
+    assert _rel(act, ref) < 1e-2
