@@ -277,6 +277,11 @@ struct Lowering {
     // ids of the current pair already issued ahead of their step (never cleared
     // within the pair, so a later step cannot issue them a second time)
     std::vector<int> issued_early;
+    // DH_SI_DEFER_DOWN_WGRAD=0: keep mlp_down_wgrad in its own pair (mode 4)
+    bool defer_down_wgrad = [] {
+        const char* e = std::getenv("DH_SI_DEFER_DOWN_WGRAD");
+        return !e || std::atoi(e) != 0;
+    }();
 
     void si_layer_pair(int fs, int lf, int bs, int lb, const weft::OverlapTable& tbl, bool relaxed) {
         take_slot(fs, lf);
@@ -303,13 +308,18 @@ struct Lowering {
             if (hoist.empty() || lane_of.at(hoist.back()) == 0) hoist.clear();  // no collective
         }
         auto hoisted = [&](int id) { return std::find(hoist.begin(), hoist.end(), id) != hoist.end(); };
-        // this pair's deferrable tail: the attention weight gradients after the
-        // backward layer's last collective (dense template ids 32, 36)
+        // this pair's deferrable ops: the attention weight gradients after the
+        // backward layer's last collective (dense template ids 32, 36), and
+        // mlp_down_wgrad (23) wherever the plan put it: a sink whose inputs (the
+        // layer's slot, the parity-indexed gathered gradient) outlive this pair, so
+        // it fills the next pair's opening, where both strands start with a
+        // collective (rs1_bwd_ag, ag0) and little compute of their own
         std::vector<int> defer_now;
         if (defer_wgrads && !m.cfg.moe) {
             int last_comm = -1;
             for (std::size_t i = 0; i < m.plan.bwd_seq.size(); ++i)
                 if (lane_of.at(m.plan.bwd_seq[i]) != 0) last_comm = static_cast<int>(i);
+            if (defer_down_wgrad && m.cfg.tp > 1) defer_now.push_back(23);
             for (std::size_t i = last_comm + 1; last_comm >= 0 && i < m.plan.bwd_seq.size(); ++i) {
                 const int id = m.plan.bwd_seq[i];
                 if (id == 32 || id == 36) defer_now.push_back(id);

@@ -251,7 +251,7 @@ int model_create(Ctx* ctx, const dh_model_cfg* c, Model** out) {
     b.grad[0] = pool.take(T * H * 2, "act.bwd_transient");
     b.grad[1] = pool.take(T * H * 2, "act.bwd_transient");
     b.d_x1 = pool.take(T * H * 2, "act.bwd_transient");
-    b.dy_full = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
+    for (int i = 0; i < 2; ++i) b.dy_full[i] = pool.take(tp1 ? 0 : S * H * 2, "act.bwd_transient");
     b.d_gate = pool.take(MR * F * 2, "act.bwd_transient");
     b.d_up = pool.take(MR * F * 2, "act.bwd_transient");
     if (k.moe) {
@@ -584,9 +584,9 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
             return DH_OK;
         case 21:  // rs1_bwd_ag
             RT_TRY(need_comm());
-            return comm->all_gather(dy, P(m.bs.dy_full), TH, s);
+            return comm->all_gather(dy, P(m.bs.dy_full[op.layer & 1]), TH, s);
         case 22: {  // mlp_down_dgrad + SwiGLU backward (in its epilogue: d_act never stored)
-            const void* dyf = tp1 ? dy : P(m.bs.dy_full);
+            const void* dyf = tp1 ? dy : P(m.bs.dy_full[op.layer & 1]);
             if (m.swiglu_in_epilogue)
                 return gemm(dyf, H, false, W + p.wd, F, true, P(m.bs.d_gate), F, false, S, F, H, false, cap, s,
                             DH_EPI_SWIGLU_BWD, P(m.bs.d_up), P(sl.gate), P(sl.up));
@@ -595,7 +595,7 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
                                  static_cast<long long>(S) * F, s);
         }
         case 23: {  // mlp_down_wgrad: dWd[H,F] += dY^T act
-            const void* dyf = tp1 ? dy : P(m.bs.dy_full);
+            const void* dyf = tp1 ? dy : P(m.bs.dy_full[op.layer & 1]);
             return gemm(dyf, H, true, P(sl.act), F, true, G + p.wd, F, true, H, F, S, true, cap, s);
         }
         case 24:    // mlp_gate_dgrad

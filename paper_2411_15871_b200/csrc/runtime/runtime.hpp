@@ -134,7 +134,9 @@ struct FwdScratch {
 };
 
 struct BwdScratch {
-    Buf grad[2], d_x1, dy_full, d_gate, d_up, d_act, dx_part, dx1_full, d_o, dqkv, attn_scratch,
+    // dy_full: the gathered output gradient, double-buffered by layer parity so that a
+    // deferred mlp_down_wgrad (mode 4) can still read it while the next layer gathers
+    Buf grad[2], d_x1, dy_full[2], d_gate, d_up, d_act, dx_part, dx1_full, d_o, dqkv, attn_scratch,
         ln_partial, rs_out;
     Buf dys, dys_e, dxe, dxp, dw, router_scratch;  // MoE
     Buf kv_loc, kv_full, dkv_full, dkv_loc;        // CP: re-gathered K|V, dK|dV partials and sums

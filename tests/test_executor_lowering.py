@@ -70,7 +70,7 @@ def check_program(prog, shape, mb, strict_order=True):
             assert mine == expect, f"strand {s} order"
         else:
             assert sorted(mine) == sorted(expect), f"strand {s} ops"
-            moved = {32, 36}  # deferrable attention weight gradients
+            moved = {23, 32, 36}  # deferrable weight gradients (mlp_down_wgrad, attention)
             for l in range(L):
                 fb = [n for (ll, n) in mine if ll == l and n not in moved]
                 want = [n for n in list(prog["fwd_seq"]) + list(prog["bwd_seq"]) if n not in moved]
@@ -294,9 +294,9 @@ def _dense_access(node, tp, L, l, s):
         R |= {"fs.rs_out"} | ({f"mb_dy{s}", "loss"} if l == L - 1 else set())
         W |= {"loss"} if l == L - 1 else set()
     elif node == 21:
-        R |= {dy}; W |= {"bs.dy_full"}
+        R |= {dy}; W |= {f"bs.dy_full{l & 1}"}
     elif node in (22, 23):
-        R |= {dy if t1 else "bs.dy_full"}; W |= {"bs.d_gate", "bs.d_up"} if node == 22 else set()
+        R |= {dy if t1 else f"bs.dy_full{l & 1}"}; W |= {"bs.d_gate", "bs.d_up"} if node == 22 else set()
     elif node in (24, 25):
         R |= {"bs.d_gate", "bs.d_up", dpart}; W |= {dpart}
     elif node == 26:
