@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const __grid_constant__ FwdSched sched) {
     using FwdSmem = dh::FwdSmem<D>;
     constexpr int kTile = FwdSmem::kTile;
+    BLK(0);
     extern __shared__ uint8_t smem_raw[];
     // offset arithmetic on the __shared__ array keeps the pointer in the shared
     // space (plain loads compile to LDS rather than generic LD)
@@ -442,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
+    BLK(1);
 }
 
 // Merge the KV-chunk partials of every split row: O = sum_c 2^(m_c-M) O_c / L,

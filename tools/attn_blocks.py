@@ -7,6 +7,7 @@ import torch
 from paper_2411_15871_b200 import device as dh
 nq = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+fwd_only = len(sys.argv) > 3 and sys.argv[3] == "fwd"
 nkv, d = max(1, nq // 4), 128
 qkv = (torch.randn(T, (nq + 2 * nkv) * d, device="cuda") * 0.5).to(torch.bfloat16)
 q, k, v = qkv[:, :nq * d], qkv[:, nq * d:(nq + nkv) * d], qkv[:, (nq + nkv) * d:]
@@ -16,6 +17,8 @@ do = torch.randn_like(o)
 dqkv = torch.empty_like(qkv)
 for _ in range(3):
     dh.attn_fwd(q, k, v, o, lse, nq, nkv, d, d ** -0.5)
+    if fwd_only:
+        continue
     dh.attn_bwd(q, k, v, o, lse, do, dqkv[:, :nq * d], dqkv[:, nq * d:(nq + nkv) * d], dqkv[:, (nq + nkv) * d:],
                 nq, nkv, d, d ** -0.5)
 torch.cuda.synchronize()
