@@ -24,12 +24,12 @@ ap.add_argument("--mb", type=int, default=4)
 ap.add_argument("--mode", default="si")
 a = ap.parse_args()
 shape = LlamaShape(**{**LLAMA3_8B.__dict__, "layers": a.layers, "micro_batches": a.mb, "slots": a.layers + 2})
-ctx = Context.emulated(0, a.tp, 16, 770.0)
+ctx = Context.emulated(0, a.tp, 16, 770.0) if a.tp > 1 else Context.create(0)
 m = Model(ctx, shape)
 m.set_overlap_ctas(148 - 16)
 prof = json.loads(m.profile(iters=5))
 caps = {"sequences": 16, "segments": 14, "candidates": 200000}
-plan = planner.lib().search_si_plan(shape.planner_model(), {"tp": a.tp, "sp": True}, B200_CLUSTER, prof,
+plan = planner.lib().search_si_plan(shape.planner_model(), {"tp": a.tp, "sp": a.tp > 1}, B200_CLUSTER, prof,
                                     caps=caps, parallel=True)["plan_json"]
 m.set_plan(plan, json.dumps(prof), mode=a.mode)
 m.set_overlap_ctas(148 - 16)
@@ -45,7 +45,7 @@ del os.environ["DH_OP_TIMES"]
 ops = [json.loads(line) for line in open(path)]
 prog = lower(shape, a.tp, plan, a.mode, profile_json=json.dumps(prof))["ops"]
 assert len(prog) == len(ops)
-names = {n["id"]: n["name"] for d in planner.lib().build_layer_dag(shape.planner_model(), {"tp": a.tp, "sp": True},
+names = {n["id"]: n["name"] for d in planner.lib().build_layer_dag(shape.planner_model(), {"tp": a.tp, "sp": a.tp > 1},
                                                                    B200_CLUSTER, profile=prof) for n in d["nodes"]}
 names[100] = "adamw"
 
