@@ -738,6 +738,8 @@ struct BwdParams {
     __nv_bfloat16* dq;
     long long lddkv, lddq;
     int T, group;   // T: query rows (this rank's)
+    int hpi;        // q heads per dK/dV item: 1, or the GQA group (its heads accumulate into
+                    // one dK / dV in TMEM, no partial slots; TP = 1 shapes, see bwd_plan)
     float scale, scale_log2;
     int T_kv;       // key rows
     int qo;         // query offset in 128-blocks (context parallelism), even
@@ -831,10 +833,12 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
 
     const int kvh = h / p.group;
     // q tiles [c0, c1) of the tiles from the first one with a query at or after
-    // the block's first key (c1 < 0: all of them)
+    // the block's first key (c1 < 0: all of them), for p.hpi consecutive q heads
+    // from h (iteration it: head h + it / n_head, tile i0 + it % n_head)
     const int nq128 = (p.T + BQ - 1) / BQ;
     const int i0 = max(0, kb - p.qo) + c0;
-    const int n_it = c1 < 0 ? max(0, nq128 - i0) : c1 - c0;
+    const int n_head = c1 < 0 ? max(0, nq128 - i0) : c1 - c0;
+    const int n_it = n_head * p.hpi;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -875,20 +879,20 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 tma_load_2d(sm + Smem::v + hh * kHalf, &tm_v, kv_full, kvh * D + 64 * hh, kb * BKV);
             }
             for (int it = 0; it < n_it; ++it) {
-                const int qs = it % kQS, os = it % kOS, qi = i0 + it;
-                const long long off = static_cast<long long>(h) * p.T + qi * BQ;
+                const int qs = it % kQS, os = it % kOS, qi = i0 + it % n_head, hq = h + it / n_head;
+                const long long off = static_cast<long long>(hq) * p.T + qi * BQ;
                 mbar_wait(&q_empty[qs], ((it / kQS) & 1) ^ 1);
                 mbar_expect_tx(&q_full[qs], kTile + (bulk_vec ? 512 : 0));
                 if (bulk_vec) bulk_load_1d(lse_s + qs * 128, p.lse + off, 512, &q_full[qs]);
 #pragma unroll
                 for (int hh = 0; hh < D / 64; ++hh)
-                    tma_load_2d(sm + Smem::q + qs * kTile + hh * kHalf, &tm_q, &q_full[qs], h * D + 64 * hh, qi * BQ);
+                    tma_load_2d(sm + Smem::q + qs * kTile + hh * kHalf, &tm_q, &q_full[qs], hq * D + 64 * hh, qi * BQ);
                 mbar_wait(&o_empty[os], ((it / kOS) & 1) ^ 1);
                 mbar_expect_tx(&o_full[os], kTile + (bulk_vec ? 512 : 0));
                 if (bulk_vec) bulk_load_1d(dvec_s + os * 128, p.dvec + off, 512, &o_full[os]);
 #pragma unroll
                 for (int hh = 0; hh < D / 64; ++hh)
-                    tma_load_2d(sm + Smem::dout + os * kTile + hh * kHalf, &tm_do, &o_full[os], h * D + 64 * hh,
+                    tma_load_2d(sm + Smem::dout + os * kTile + hh * kHalf, &tm_do, &o_full[os], hq * D + 64 * hh,
                                 qi * BQ);
             }
         }
@@ -968,7 +972,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         const uint32_t col = lane_off + half * 64;
         const int key_hi = kb * BKV + BKV - 1;
         for (int it = 0; it < n_it; ++it) {
-            const int qi = i0 + it;
+            const int qi = i0 + it % n_head, hq = h + it / n_head;
             float* sl = lse_s + (it % kQS) * 128;
             float* sd = dvec_s + (it % kOS) * 128;
             if (!bulk_vec) {
@@ -976,8 +980,8 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                 named_barrier(1, 256);  // previous readers of these slots are done
                 if (t_sm < BQ) {
                     const int q = qi * BQ + t_sm;
-                    sl[t_sm] = q < p.T ? p.lse[static_cast<long long>(h) * p.T + q] : 0.f;
-                    sd[t_sm] = q < p.T ? p.dvec[static_cast<long long>(h) * p.T + q] : 0.f;
+                    sl[t_sm] = q < p.T ? p.lse[static_cast<long long>(hq) * p.T + q] : 0.f;
+                    sd[t_sm] = q < p.T ? p.dvec[static_cast<long long>(hq) * p.T + q] : 0.f;
                 }
                 named_barrier(1, 256);
             }
@@ -1426,6 +1430,7 @@ struct BwdPlan {
     std::vector<uint2> items;  // empty: implicit schedule
     BwdSlots slots;
     long long kv_slots = 0, q_slots = 0;
+    int hpi = 1;               // q heads per dK/dV item (GQA group loop)
 };
 
 const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
@@ -1466,6 +1471,19 @@ const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
     for (int b = 0; b < nb_kv; ++b) count += nq * (nck_kv[b] = chunks(cost_kv(n_kv(b)), n_kv(b)));
     for (int b = 0; b < nb_q; ++b) count += nq * (nck_q[b] = chunks(cost_q(n_q(b)), n_q(b)));
     const bool expl = count <= kMaxBwdItems && nq <= 127 && nq128 <= 255 && nb_kv <= 255;
+    // GQA group loop: one dK/dV item per (key block, kv head) accumulates all of
+    // its group's q heads in TMEM (no fp32 partial slots, no reduction) when even
+    // the heaviest such item stays within the mean per-SM load (many heads per
+    // GPU: TP = 1 Llama-3-8B has 8 kv heads; at TP = 8 one kv head's items would
+    // be the critical path)
+    static const bool group_loop = [] {  // DH_ATTN_GROUP_LOOP=0: per-head items + reduction (A/B)
+        const char* e = std::getenv("DH_ATTN_GROUP_LOOP");
+        return !e || e[0] != '0';
+    }();
+    if (group_loop && expl && group > 1 && cost_kv(group * n_kv(0)) <= L / frac) {
+        pl.hpi = group;
+        std::fill(nck_kv.begin(), nck_kv.end(), 1);
+    }
     uint32_t run = 0;
     for (int b = 0; b < kMaxBwdBlocks; ++b) {
         pl.slots.kv_base[b] = pl.slots.q_base[b] = kDirect;
@@ -1474,7 +1492,7 @@ const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
     for (int b = 0; b < nb_kv; ++b) {
         const int nck = expl ? nck_kv[b] : 1;
         pl.slots.kv_nck[b] = static_cast<uint8_t>(nck);
-        if (group > 1 || nck > 1) {
+        if ((group > 1 && pl.hpi == 1) || nck > 1) {
             pl.slots.kv_base[b] = run;
             run += nq * nck;
         }
@@ -1502,14 +1520,15 @@ const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
                 const int n = kind ? n_q(b) : n_kv(b);
                 const int nck = kind ? pl.slots.q_nck[b] : pl.slots.kv_nck[b];
                 const uint32_t base = kind ? pl.slots.q_base[b] : pl.slots.kv_base[b];
-                for (int h = 0; h < nq; ++h)
+                const int hstep = kind ? 1 : pl.hpi;  // group loop: one item per kv head
+                for (int h = 0; h < nq; h += hstep)
                     for (int c = 0; c < nck; ++c) {
                         const int c0 = n * c / nck, c1 = n * (c + 1) / nck;
                         const uint32_t x = (static_cast<uint32_t>(kind) << 31) | (static_cast<uint32_t>(h) << 24) |
                                            (static_cast<uint32_t>(b) << 16) | (static_cast<uint32_t>(c0) << 8) |
                                            static_cast<uint32_t>(c1);
                         const uint32_t y = base == kDirect ? kDirect : base + h * nck + c;
-                        its.push_back({kind ? cost_q(c1 - c0) : cost_kv(c1 - c0), make_uint2(x, y)});
+                        its.push_back({kind ? cost_q(c1 - c0) : cost_kv(hstep * (c1 - c0)), make_uint2(x, y)});
                     }
             }
         }
@@ -1549,7 +1568,7 @@ int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
     BwdParams prm{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(dout), ldq, ldo,
                   lse, dvec, dk_part, dv_part, dq_part, static_cast<__nv_bfloat16*>(dk),
                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq), lddkv, lddq, T,
-                  group, scale, scale * kLog2e, T_kv, q_offset / BQ};
+                  group, pl->hpi, scale, scale * kLog2e, T_kv, q_offset / BQ};
     static BwdSched sched;  // host staging of the kernel parameter (launches are serialised per process)
     static std::mutex mu;
     std::lock_guard<std::mutex> lk(mu);

@@ -145,7 +145,8 @@ def _attn_ref(q, k, v, nq, nkv, d, scale):
 
 @pytest.mark.parametrize("T,nq,nkv,d", [(128, 4, 1, 64), (256, 4, 4, 128), (1000, 8, 2, 128),
                                         (4096, 4, 1, 128), (1000, 8, 2, 64), (2048, 4, 1, 64),
-                                        (384, 2, 2, 64), (8192, 1, 1, 128), (2048, 16, 4, 128)])
+                                        (384, 2, 2, 64), (8192, 1, 1, 128), (2048, 16, 4, 128),
+                                        (4096, 32, 8, 128)])  # TP=1 shape: GQA group loop in the backward
 def test_attention_fwd_bwd(T, nq, nkv, d):
     scale = d ** -0.5
     # packed qkv rows, as the qkv GEMM writes them
