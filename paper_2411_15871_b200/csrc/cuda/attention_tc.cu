@@ -1377,7 +1377,7 @@ __global__ void __launch_bounds__(256) attn_bwd_reduce(const float* __restrict__
                                                        const float* __restrict__ dv_part,
                                                        const float* __restrict__ dq_part, __nv_bfloat16* dk,
                                                        __nv_bfloat16* dv, __nv_bfloat16* dq, long long lddkv,
-                                                       long long lddq, int T, int T_kv, int nq, int group,
+                                                       long long lddq, int T, int T_kv, int nq, int group, int hpi,
                                                        int nb_kv, int nb_q, const __grid_constant__ BwdSlots tb) {
     constexpr int V = D / 8;
     const int nkv = nq / group;
@@ -1396,7 +1396,7 @@ __global__ void __launch_bounds__(256) attn_bwd_reduce(const float* __restrict__
         const int row = b * BKV + r;
         if (base == kDirect || row >= (kv ? T_kv : T)) continue;
         const int nck = kv ? tb.kv_nck[b] : tb.q_nck[b];
-        const int heads = kv ? group : 1, h0 = kv ? hh * group : hh;
+        const int heads = kv ? group / hpi : 1, h0 = kv ? hh * (group / hpi) : hh;
         float sk[8] = {}, sv[8] = {};
         for (int s2 = 0; s2 < heads * nck; ++s2) {
             const long long off = ((static_cast<long long>(base) + h0 * nck + s2) * BKV + r) * D + d8 * 8;
@@ -1474,8 +1474,8 @@ const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
     // GQA group loop: one dK/dV item per (key block, kv head) accumulates all of
     // its group's q heads in TMEM (no fp32 partial slots, no reduction) when even
     // the heaviest such item stays within the mean per-SM load (many heads per
-    // GPU: TP = 1 Llama-3-8B has 8 kv heads; at TP = 8 one kv head's items would
-    // be the critical path)
+    // GPU: TP = 1 Llama-3-8B has 8 kv heads); otherwise, with at least two kv
+    // heads, the group items are split into chunks (fewer slots than per head)
     static const bool group_loop = [] {  // DH_ATTN_GROUP_LOOP=0: per-head items + reduction (A/B)
         const char* e = std::getenv("DH_ATTN_GROUP_LOOP");
         return !e || e[0] != '0';
@@ -1483,6 +1483,17 @@ const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
     if (group_loop && expl && group > 1 && cost_kv(group * n_kv(0)) <= L / frac) {
         pl.hpi = group;
         std::fill(nck_kv.begin(), nck_kv.end(), 1);
+    } else if (group_loop && expl && group > 1 && nq / group >= 2) {
+        // group loop with the group items split into chunks of at most the mean
+        // per-SM load (partial slots per chunk). B200, T = 4096: 8 q / 2 kv heads
+        // 130.1 -> 114.9 us, 16 / 4: 246.0 -> 209.1 us; with a single kv head
+        // (4 / 1) 72.2 -> 74.3 us, so that case keeps per-head items.
+        pl.hpi = group;
+        for (int b = 0; b < nb_kv; ++b) {
+            const int n = n_kv(b) * group;
+            nck_kv[b] = n < 2 ? 1 : std::clamp(static_cast<int>(std::ceil(cost_kv(n) / (W / sms))), 1,
+                                               std::min(n_kv(b), 255));
+        }
     }
     uint32_t run = 0;
     for (int b = 0; b < kMaxBwdBlocks; ++b) {
@@ -1494,7 +1505,7 @@ const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
         pl.slots.kv_nck[b] = static_cast<uint8_t>(nck);
         if ((group > 1 && pl.hpi == 1) || nck > 1) {
             pl.slots.kv_base[b] = run;
-            run += nq * nck;
+            run += nq / pl.hpi * nck;
         }
     }
     pl.kv_slots = run;
@@ -1527,7 +1538,7 @@ const BwdPlan* bwd_plan(int T, int T_kv, int qo, int nq, int group) {
                         const uint32_t x = (static_cast<uint32_t>(kind) << 31) | (static_cast<uint32_t>(h) << 24) |
                                            (static_cast<uint32_t>(b) << 16) | (static_cast<uint32_t>(c0) << 8) |
                                            static_cast<uint32_t>(c1);
-                        const uint32_t y = base == kDirect ? kDirect : base + h * nck + c;
+                        const uint32_t y = base == kDirect ? kDirect : base + h / hstep * nck + c;
                         its.push_back({kind ? cost_q(c1 - c0) : cost_kv(hstep * (c1 - c0)), make_uint2(x, y)});
                     }
             }
@@ -1582,7 +1593,8 @@ int attn_bwd_tc_d(const void* q, const void* k, const void* v, long long ldq, lo
         const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 148 * 8));
         attn_bwd_reduce<D><<<blocks, 256, 0, s>>>(dk_part, dv_part, dq_part, static_cast<__nv_bfloat16*>(dk),
                                                   static_cast<__nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dq),
-                                                  lddkv, lddq, T, T_kv, nq, group, nb_kv, nb_q, pl->slots);
+                                                  lddkv, lddq, T, T_kv, nq, group, pl->hpi, nb_kv, nb_q,
+                                                  pl->slots);
         DH_CUDA_CHECK(cudaGetLastError());
     }
     return DH_OK;
