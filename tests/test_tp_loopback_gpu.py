@@ -48,8 +48,12 @@ def _tp8_shape():
                       seq_len=512, micro_batches=2, rope_theta=500000.0, slots=4)
 
 
-@pytest.mark.parametrize("tp", [2, 4, 8])
-def test_tp_loopback_vs_oracle_and_si_equals_sequential(tp):
+@pytest.mark.parametrize("tp,merge", [(2, None), (4, None), (8, None), (2, "1")])
+def test_tp_loopback_vs_oracle_and_si_equals_sequential(tp, merge, monkeypatch):
+    # merge="1": the merged MLP GEMMs (SwiGLU pair, K-concatenated dgrads), off by
+    # default at TP > 1, also under tensor parallelism
+    if merge is not None:
+        monkeypatch.setenv("DH_MLP_MERGE", merge)
     # one spare activation slot: mode 4 (deferred weight gradients) needs L + 2
     shape = _tp8_shape() if tp == 8 else LlamaShape(**{**_tiny(mb=2, layers=2, nkv=4).__dict__, "slots": 4})
     orc = LlamaTPOracle(shape.hidden, shape.ffn, shape.n_heads, shape.n_kv_heads, shape.head_dim,
