@@ -881,18 +881,22 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             for (int it = 0; it < n_it; ++it) {
                 const int qs = it % kQS, os = it % kOS, qi = i0 + it % n_head, hq = h + it / n_head;
                 const long long off = static_cast<long long>(hq) * p.T + qi * BQ;
+                // Q(it), dO(it) and their vectors all complete on q_full[qs]: the
+                // MMA thread waits once per iteration for its TMA operands (each
+                // wait between MMA groups costs the tensor pipe ~150 cycles on
+                // B200, tools/micro/mma_rate.cu); the two rings keep separate
+                // empty barriers (different depths)
                 mbar_wait(&q_empty[qs], ((it / kQS) & 1) ^ 1);
-                mbar_expect_tx(&q_full[qs], kTile + (bulk_vec ? 512 : 0));
+                mbar_expect_tx(&q_full[qs], 2 * kTile + (bulk_vec ? 1024 : 0));
                 if (bulk_vec) bulk_load_1d(lse_s + qs * 128, p.lse + off, 512, &q_full[qs]);
 #pragma unroll
                 for (int hh = 0; hh < D / 64; ++hh)
                     tma_load_2d(sm + Smem::q + qs * kTile + hh * kHalf, &tm_q, &q_full[qs], hq * D + 64 * hh, qi * BQ);
                 mbar_wait(&o_empty[os], ((it / kOS) & 1) ^ 1);
-                mbar_expect_tx(&o_full[os], kTile + (bulk_vec ? 512 : 0));
-                if (bulk_vec) bulk_load_1d(dvec_s + os * 128, p.dvec + off, 512, &o_full[os]);
+                if (bulk_vec) bulk_load_1d(dvec_s + os * 128, p.dvec + off, 512, &q_full[qs]);
 #pragma unroll
                 for (int hh = 0; hh < D / 64; ++hh)
-                    tma_load_2d(sm + Smem::dout + os * kTile + hh * kHalf, &tm_do, &o_full[os], hq * D + 64 * hh,
+                    tma_load_2d(sm + Smem::dout + os * kTile + hh * kHalf, &tm_do, &q_full[qs], hq * D + 64 * hh,
                                 qi * BQ);
             }
         }
@@ -902,9 +906,8 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         const uint32_t k_addr = smem_u32(sm + Smem::k), v_addr = smem_u32(sm + Smem::v);
         auto q_addr = [&](int it) { return smem_u32(sm + Smem::q + (it % kQS) * kTile); };
         auto o_addr = [&](int it) { return smem_u32(sm + Smem::dout + (it % kOS) * kTile); };
-        auto issue_s = [&](int it) {  // S^T(it) = K Q(it)^T
+        auto issue_s = [&](int it) {  // S^T(it) = K Q(it)^T; Q(it) and dO(it) landed
             mbar_wait(&q_full[it % kQS], (it / kQS) & 1);
-            tc_fence_after();
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
@@ -913,9 +916,7 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             }
             __syncwarp();
         };
-        auto issue_dp = [&](int it) {  // dP^T(it) = V dO(it)^T
-            mbar_wait(&o_full[it % kOS], (it / kOS) & 1);
-            tc_fence_after();
+        auto issue_dp = [&](int it) {  // dP^T(it) = V dO(it)^T (dO(it) waited with Q(it) in issue_s)
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
@@ -1163,9 +1164,8 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
         constexpr uint32_t id_g = umma_idesc_bf16(128, D, false, true);
         auto k_addr = [&](int it) { return smem_u32(sm + Smem::k + (it % kSt) * kTile); };
         auto v_addr = [&](int it) { return smem_u32(sm + Smem::v + (it % kSt) * kTile); };
-        auto issue_s = [&](int it) {  // S(it) = Q K(it)^T
+        auto issue_s = [&](int it) {  // S(it) = Q K(it)^T (TMA operands: no tcgen05 fence, as CUTLASS)
             mbar_wait(&kv_full[it % kSt], (it / kSt) & 1);
-            tc_fence_after();
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)

@@ -11,6 +11,18 @@
 
 using namespace dh;
 
+// completed-phase probe without the try_wait suspend path
+__device__ __forceinline__ void mbar_wait_probe(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "PROBE_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra PROBE_%=;\n}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
 // sequence ids
 //  0: SS M128 N32  K128          1: SS M128 N64  K128     2: SS M128 N128 K128   3: SS M128 N256 K128
 //  4: TS M128 N32  K128          5: TS M128 N64  K128     6: TS M128 N128 K128
@@ -21,7 +33,8 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int seq, int iters, long long
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ uint32_t slot;
-    __shared__ uint64_t bar, bar2;
+    __shared__ uint64_t bar, bar2, bar3;
+    __shared__ volatile int flag;
     // seq 13, 14: random bf16 operands (N(0, 1)-like), else zeros
     for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) {
         uint4 v = make_uint4(0, 0, 0, 0);
@@ -42,6 +55,9 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int seq, int iters, long long
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_init(&bar2, 1 << 20);  // commits arrive here and never complete a phase
+        mbar_init(&bar3, 1);
+        mbar_arrive(&bar3);          // phase 0 complete: waits on it return at once
+        flag = 1;
         fence_barrier_init();
     }
     if (warp == 0) tmem_alloc(&slot, 512);
@@ -140,11 +156,22 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int seq, int iters, long long
                 }
                 case 10:    // round-2 dK/dV iteration (128 queries): S^T, dP^T SS N128 K128; dV, dK TS N128 K128
                 case 15:    // + tcgen05.fence::after_thread_sync before each group (the kernel's pattern)
-                case 16: {  // + a commit to an mbarrier after each group
+                case 16:    // + a commit to an mbarrier after each group
+                case 17:    // + an mbarrier wait (already-completed phase) before each group
+                case 19:    // + mbarrier.test_wait probe instead
+                case 20:    // + a volatile shared-memory flag read instead
+                case 18: {  // + two waits before each group
                     const uint32_t ids = umma_idesc_bf16(128, 128, false, false), idg = umma_idesc_bf16(128, 128, false, true);
                     auto sep = [&]() {
-                        if (mseq >= 15) tc_fence_after();
+                        if (mseq == 15 || mseq == 16) tc_fence_after();
                         if (mseq == 16) tc_commit(&bar2);
+                        if (mseq == 17 || mseq == 18) mbar_wait(&bar3, 0);
+                        if (mseq == 18) mbar_wait(&bar3, 0);
+                        if (mseq == 19) mbar_wait_probe(&bar3, 0);
+                        if (mseq == 20) {
+                            while (flag == 0) {
+                            }
+                        }
                     };
                     sep();
                     for (int kk = 0; kk < 8; ++kk) tc_mma_bf16(tmem, kmaj(a_s, kk), kmaj(b_s, kk), ids, 1);
@@ -195,19 +222,22 @@ int main() {
     cudaMemset(gsrc, 0, 64 << 16);
     cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     // FLOP per round of each sequence
-    const double fl[17] = {2.0 * 128 * 32 * 128,  2.0 * 128 * 64 * 128,  2.0 * 128 * 128 * 128, 2.0 * 128 * 256 * 128,
+    const double fl[21] = {2.0 * 128 * 32 * 128,  2.0 * 128 * 64 * 128,  2.0 * 128 * 128 * 128, 2.0 * 128 * 256 * 128,
                            2.0 * 128 * 32 * 128,  2.0 * 128 * 64 * 128,  2.0 * 128 * 128 * 128,
                            4 * 2.0 * 128 * 64 * 128, 8 * 2.0 * 128 * 32 * 128, 4 * 2.0 * 128 * 64 * 128,
                            4 * 2.0 * 128 * 128 * 128, 4 * 2.0 * 128 * 128 * 128, 4 * 2.0 * 128 * 128 * 128,
                            2.0 * 128 * 128 * 128, 4 * 2.0 * 128 * 128 * 128, 4 * 2.0 * 128 * 128 * 128,
-                           4 * 2.0 * 128 * 128 * 128};
-    const char* name[17] = {"SS N32", "SS N64", "SS N128", "SS N256", "TS N32", "TS N64", "TS N128",
+                           4 * 2.0 * 128 * 128 * 128, 4 * 2.0 * 128 * 128 * 128, 4 * 2.0 * 128 * 128 * 128,
+                           4 * 2.0 * 128 * 128 * 128, 4 * 2.0 * 128 * 128 * 128};
+    const char* name[21] = {"SS N32", "SS N64", "SS N128", "SS N256", "TS N32", "TS N64", "TS N128",
                             "dkdv current (SS N64 + TS N128 K64)", "dkdv proposed (TS N32 + TS N128 K32) x2",
                             "dkdv TS N64 + TS N128 K64", "dkdv r2 (SS N128 x2 + TS N128 K128 x2)",
                             "dkdv r2 + concurrent tcgen05.ld/st traffic", "dkdv r2 + concurrent bulk copies to smem",
                             "SS N128, random operands", "dkdv r2, random operands",
-                            "dkdv r2 + fence::after_thread_sync per group", "dkdv r2 + fence + commit per group"};
-    for (int seq = 0; seq < 17; ++seq) {
+                            "dkdv r2 + fence::after_thread_sync per group", "dkdv r2 + fence + commit per group",
+                            "dkdv r2 + completed mbarrier wait per group", "dkdv r2 + 2 completed waits per group",
+                            "dkdv r2 + test_wait probe per group", "dkdv r2 + volatile smem flag read per group"};
+    for (int seq = 0; seq < 21; ++seq) {
         const int iters = 2000;
         mma_rate<<<148, 128, smem>>>(seq, 20, cyc, gsrc);
         mma_rate<<<148, 128, smem>>>(seq, iters, cyc, gsrc);
