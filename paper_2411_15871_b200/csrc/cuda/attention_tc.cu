@@ -668,8 +668,8 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, long long ldq, long
 //   dV  += P^T dO       M128 N=D K128   A=P^T (TMEM)    B=dO (smem, MN-major)
 //   dK  += dS^T Q       M128 N=D K128   A=dS^T (TMEM)   B=Q  (smem, MN-major)
 //   TMEM: S^T (128) | dP^T (128) | dV (D) | dK (D); P^T / dS^T (bf16 pairs)
-//   overwrite the first 32 columns of each 64-column half of S^T / dP^T that
-//   the same threads read (no cross-thread hazard).
+//   overwrite the first kEwCols / 2 columns of each kEwCols-column part of
+//   S^T / dP^T that the same threads read (no cross-thread hazard).
 //   Issue order: S(0) dP(0) | dV(i) S(i+1) dK(i) dP(i+1) | ... — the softmax
 //   exponentials of tile i+1 run under dK(i) and dP(i+1), dS(i) under dV(i)
 //   and S(i+1).
@@ -745,7 +745,21 @@ struct BwdParams {
     int qo;         // query offset in 128-blocks (context parallelism), even
 };
 
-constexpr int kThreadsBwd = 320;  // producer, MMA, 8 elementwise warps (2 per TMEM quadrant)
+// Elementwise warps of the backward kernel: kEwWarps / 4 per TMEM lane
+// quadrant, each owning kEwCols of the 128 tile columns. 16 (4 per quadrant,
+// 32 columns each) halves the per-thread latency of the exp / dS phases that
+// sit between the MMA groups (8 warps: 64 columns each); the per-SM MUFU and
+// FMA work is the same.
+#ifndef DH_ATTN_BWD_EW
+#define DH_ATTN_BWD_EW 8
+#endif
+constexpr int kEwWarps = DH_ATTN_BWD_EW;
+static_assert(kEwWarps == 8 || kEwWarps == 16, "elementwise warps: 2 or 4 per TMEM quadrant");
+constexpr int kEwParts = kEwWarps / 4;          // column parts per lane quadrant
+constexpr int kEwCols = 128 / kEwParts;         // tile columns per elementwise thread
+constexpr int kEwThreads = 32 * kEwWarps;
+constexpr int kEw0 = 2;                              // first elementwise warp
+constexpr int kThreadsBwd = 32 * kEw0 + kEwThreads;  // producer, MMA issuer, elementwise warps
 constexpr uint32_t kDirect = 0xFFFFFFFFu;  // item owns its output rows: bf16 store, no slot
 
 // Explicit schedule (kernel parameter): item.x = kind << 31 (1 = dQ) | head << 24
@@ -765,25 +779,48 @@ struct BwdSlots {
 };
 
 // A operand from TMEM (bf16 pairs) for k-step kk (16 rows of the 128-wide
-// tile): each 64-column half of the fp32 tile holds its 64 values packed
-// into its first 32 columns.
-__device__ __forceinline__ uint32_t packed_col(int kk) { return (kk >> 2) * 64 + (kk & 3) * 8; }
+// tile): each kEwCols-column part of the fp32 tile holds its values packed
+// into its first kEwCols / 2 columns (by the thread that read them).
+__device__ __forceinline__ uint32_t packed_col(int kk) {
+    constexpr int kps = kEwCols / 16;  // k-steps per part
+    return (kk / kps) * kEwCols + (kk % kps) * 8;
+}
 
-// 64 fp32 columns [c0, c0 + 64) of this warp's TMEM lane quadrant.
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
-    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-    tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+// N consecutive fp32 columns of this warp's TMEM lane quadrant (waited).
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t (&r)[N]) {
+    static_assert(N % 16 == 0, "16-column granules");
+    if constexpr (N % 32 == 0) {
+#pragma unroll
+        for (int c = 0; c < N / 32; ++c) tmem_ld32(taddr + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]));
+    } else {
+#pragma unroll
+        for (int c = 0; c < N / 16; ++c) tmem_ld16(taddr + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(&r[16 * c]));
+    }
     tmem_ld_wait();
+}
+template <int N>
+__device__ __forceinline__ void tmem_stn(uint32_t taddr, const uint32_t (&r)[N]) {
+    static_assert(N % 16 == 0, "16-column granules");
+    if constexpr (N % 32 == 0) {
+#pragma unroll
+        for (int c = 0; c < N / 32; ++c)
+            tmem_st32(taddr + 32 * c, *reinterpret_cast<const uint32_t(*)[32]>(&r[32 * c]));
+    } else {
+#pragma unroll
+        for (int c = 0; c < N / 16; ++c)
+            tmem_st16(taddr + 16 * c, *reinterpret_cast<const uint32_t(*)[16]>(&r[16 * c]));
+    }
 }
 
 // p = 2^(s * scale_log2 + bias), bias per column (-log2e lse_j, PER_COL) or
 // per row; half of the pairs on the FMA pipe (the MUFU alone would need
 // 16384 / 16 = 1024 cycles per 128 x 128 tile).
-template <bool PER_COL>
-__device__ __forceinline__ void bwd_exp64(uint32_t (&s)[64], const float* bias, float bias_row, float scale_log2) {
+template <bool PER_COL, int N>
+__device__ __forceinline__ void bwd_exp(uint32_t (&s)[N], const float* bias, float bias_row, float scale_log2) {
     const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
+    for (int u = 0; u < N / 2; ++u) {
         uint64_t b2;
         if constexpr (PER_COL) {  // bias = raw lse of the columns (smem): -log2e * lse
             const float2 l2 = reinterpret_cast<const float2*>(bias)[u];
@@ -804,6 +841,28 @@ __device__ __forceinline__ void bwd_exp64(uint32_t (&s)[64], const float* bias, 
         s[2 * u] = __float_as_uint(e0);
         s[2 * u + 1] = __float_as_uint(e1);
     }
+}
+
+// dS = P (dP - D), packed to bf16 pairs over the first N / 2 columns read.
+template <bool PER_COL, int N>
+__device__ __forceinline__ void bwd_ds_store(uint32_t taddr, const uint32_t (&pv)[N], const float* dcol, uint64_t nd_row) {
+    uint32_t b[N];
+    tmem_ldn<N>(taddr, b);
+    uint32_t pd[N / 2];
+#pragma unroll
+    for (int u = 0; u < N / 2; ++u) {
+        uint64_t nd = nd_row;
+        if constexpr (PER_COL) {
+            const float2 dd = reinterpret_cast<const float2*>(dcol)[u];
+            nd = f2_pack(-dd.x, -dd.y);
+        }
+        const uint64_t ds = ffma2(f2_pack(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1])),
+                                  fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), nd), 0ull);
+        float s0, s1;
+        f2_unpack(ds, s0, s1);
+        pd[u] = pack2(s0, s1);
+    }
+    tmem_stn<N / 2>(taddr, pd);
 }
 
 template <int D>
@@ -857,8 +916,8 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
         }
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
-        mbar_init(p_full, 256);
-        mbar_init(ds_full, 256);
+        mbar_init(p_full, kEwThreads);
+        mbar_init(ds_full, kEwThreads);
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -963,14 +1022,14 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             if (it + 1 < n_it) issue_dp(it + 1);
         }
     } else {
-        // 8 warps: quadrant (TMEM lanes) = warp & 3, column half = (warp - 2) >> 2
+        // quadrant (TMEM lanes) = warp & 3, column part = (warp - kEw0) >> 2
         const int quad = warp & 3;
-        const int half = (warp - 2) >> 2;
+        const int part = (warp - kEw0) >> 2;
         const int r = quad * 32 + lane;  // key row within the block
         const int key = kb * BKV + r;
-        const int t_sm = threadIdx.x - 64;  // 0..255 among the elementwise warps
+        const int t_sm = threadIdx.x - 32 * kEw0;  // among the elementwise warps
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const uint32_t col = lane_off + half * 64;
+        const uint32_t col = lane_off + part * kEwCols;
         const int key_hi = kb * BKV + BKV - 1;
         for (int it = 0; it < n_it; ++it) {
             const int qi = i0 + it % n_head, hq = h + it / n_head;
@@ -978,84 +1037,69 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
             float* sd = dvec_s + (it % kOS) * 128;
             if (!bulk_vec) {
                 // ragged T: stage the vectors with plain loads
-                named_barrier(1, 256);  // previous readers of these slots are done
+                named_barrier(1, kEwThreads);  // previous readers of these slots are done
                 if (t_sm < BQ) {
                     const int q = qi * BQ + t_sm;
                     sl[t_sm] = q < p.T ? p.lse[static_cast<long long>(hq) * p.T + q] : 0.f;
                     sd[t_sm] = q < p.T ? p.dvec[static_cast<long long>(hq) * p.T + q] : 0.f;
                 }
-                named_barrier(1, 256);
+                named_barrier(1, kEwThreads);
             }
             // whole tile causal-visible and in range: no per-element masking
             const int qg0 = (p.qo + qi) * BQ;  // global position of the tile's first query
             const bool full_tile = qg0 >= key_hi && qi * BQ + BQ <= p.T && key_hi < p.T_kv;
             // ---- P^T = exp2(scale_log2 S^T - log2e lse_q)
-            if (threadIdx.x == 64) ATR(it * 8 + 7);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 7);
             mbar_wait(s_full, it & 1);
-            if (threadIdx.x == 64) ATR(it * 8 + 3);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 3);
             tc_fence_after();
-            uint32_t pv[64];
-            tmem_ld64(t_s + col, pv);
-            bwd_exp64<true>(pv, sl + half * 64, 0.f, p.scale_log2);
+            uint32_t pv[kEwCols];
+            tmem_ldn<kEwCols>(t_s + col, pv);
+            bwd_exp<true>(pv, sl + part * kEwCols, 0.f, p.scale_log2);
             if (!full_tile) {
 #pragma unroll
-                for (int j = 0; j < 64; ++j) {
-                    const int q = qi * BQ + half * 64 + j;  // local row; global position q + qo * BQ
+                for (int j = 0; j < kEwCols; ++j) {
+                    const int q = qi * BQ + part * kEwCols + j;  // local row; global position q + qo * BQ
                     if (q + p.qo * BQ < key || q >= p.T || key >= p.T_kv) pv[j] = 0u;
                 }
             }
             {
-                uint32_t pp[32];
+                uint32_t pp[kEwCols / 2];
 #pragma unroll
-                for (int u = 0; u < 32; ++u) pp[u] = pack2(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1]));
-                tmem_st32(t_s + col, pp);
+                for (int u = 0; u < kEwCols / 2; ++u)
+                    pp[u] = pack2(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1]));
+                tmem_stn<kEwCols / 2>(t_s + col, pp);
             }
             tmem_st_wait();
             tc_fence_before();
-            if (threadIdx.x == 64) ATR(it * 8 + 4);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 4);
             mbar_arrive(p_full);
-            // ---- dS^T = P^T (dP^T - D_q), in two 32-column chunks
+            // ---- dS^T = P^T (dP^T - D_q)
             mbar_wait(dp_full, it & 1);
-            if (threadIdx.x == 64) ATR(it * 8 + 5);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 5);
             tc_fence_after();
-            {
-                uint32_t b[64];
-                tmem_ld64(t_dp + col, b);
-                const float2* d2 = reinterpret_cast<const float2*>(sd + half * 64);
-                uint32_t pd[32];
-#pragma unroll
-                for (int u = 0; u < 32; ++u) {
-                    const float2 dd = d2[u];
-                    const uint64_t ds = ffma2(
-                        f2_pack(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1])),
-                        fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), f2_pack(-dd.x, -dd.y)),
-                        0ull);
-                    float s0, s1;
-                    f2_unpack(ds, s0, s1);
-                    pd[u] = pack2(s0, s1);
-                }
-                tmem_st32(t_dp + col, pd);  // over the first 32 columns of this half (read above)
-            }
+            bwd_ds_store<true>(t_dp + col, pv, sd + part * kEwCols, 0ull);
             tmem_st_wait();
             tc_fence_before();
-            if (threadIdx.x == 64) ATR(it * 8 + 6);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 6);
             mbar_arrive(ds_full);
         }
         if (n_it > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
         const bool ok = key < p.T_kv;
+        constexpr int kPc = D / kEwParts;          // dK / dV columns per part
+        constexpr int kW = kPc < 32 ? kPc : 32;    // per TMEM load
 #pragma unroll 1
-        for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
-            uint32_t ka[32], va[32];
-            tmem_ld32(t_dk + lane_off + c * 32, ka);
-            tmem_ld32(t_dv + lane_off + c * 32, va);
-            tmem_ld_wait();
+        for (int c = part * kPc; c < (part + 1) * kPc; c += kW) {
+            uint32_t ka[kW], va[kW];
+            tmem_ldn<kW>(t_dk + lane_off + c, ka);
+            tmem_ldn<kW>(t_dv + lane_off + c, va);
             if (!ok) continue;
             if (slot == kDirect) {
-                __nv_bfloat16* kr = p.dk + static_cast<long long>(key) * p.lddkv + kvh * D + c * 32;
-                __nv_bfloat16* vr = p.dv + static_cast<long long>(key) * p.lddkv + kvh * D + c * 32;
+                __nv_bfloat16* kr = p.dk + static_cast<long long>(key) * p.lddkv + kvh * D + c;
+                __nv_bfloat16* vr = p.dv + static_cast<long long>(key) * p.lddkv + kvh * D + c;
 #pragma unroll
-                for (int t = 0; t < 32; t += 8) {
+                for (int t = 0; t < kW; t += 8) {
                     float fk[8], fv[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
@@ -1066,13 +1110,13 @@ __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, cons
                     *reinterpret_cast<uint4*>(vr + t) = pack8(fv);
                 }
             } else {
-                float* kr = p.dk_part + (static_cast<long long>(slot) * BKV + r) * D + c * 32;
-                float* vr = p.dv_part + (static_cast<long long>(slot) * BKV + r) * D + c * 32;
+                float* kr = p.dk_part + (static_cast<long long>(slot) * BKV + r) * D + c;
+                float* vr = p.dv_part + (static_cast<long long>(slot) * BKV + r) * D + c;
                 // keys after every query of this rank (context parallelism) get no
                 // gradient; TMEM was never written for them (select, not multiply)
                 const bool any = n_it > 0;
 #pragma unroll
-                for (int t = 0; t < 32; t += 4) {
+                for (int t = 0; t < kW; t += 4) {
                     float k4[4], v4[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -1122,15 +1166,15 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
     if (threadIdx.x == 0) {
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
-        mbar_init(q_full, 256);
+        mbar_init(q_full, kEwThreads);
         for (int i = 0; i < kSt; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
-        mbar_init(s_free, 256);
-        mbar_init(ds_full, 256);
+        mbar_init(s_free, kEwThreads);
+        mbar_init(ds_full, kEwThreads);
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -1210,33 +1254,39 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
         }
     } else {
         const int quad = warp & 3;
-        const int half = (warp - 2) >> 2;
+        const int part = (warp - kEw0) >> 2;
         const int r = quad * 32 + lane;
         const int qrow = qb * BQ + r;
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const uint32_t col = lane_off + half * 64;
+        const uint32_t col = lane_off + part * kEwCols;
         const int qc = min(qrow, p.T - 1);
         const float nlse2 = -p.lse[static_cast<long long>(h) * p.T + qc] * kLog2e;
         const float dd = p.dvec[static_cast<long long>(h) * p.T + qc];
         const uint64_t nd2 = f2_pack(-dd, -dd);
         {
-            // this thread's query row of Q (half 0) or dO (half 1) into its TMEM lane:
-            // row-major bf16 pairs are exactly the packed A-operand columns
-            const __nv_bfloat16* src = half ? p.dout + static_cast<long long>(qc) * p.ldo + h * D
-                                            : p.q + static_cast<long long>(qc) * p.ldq + h * D;
+            // this thread's query row of Q (first half of the parts) or dO (second
+            // half) into its TMEM lane: row-major bf16 pairs are exactly the packed
+            // A-operand columns; each part stages D / kEwParts pair columns
+            constexpr int kSub = kEwParts / 2;            // parts per operand
+            constexpr int kPw = D / 2 / kSub;             // pair columns per part
+            constexpr int kW = kPw < 32 ? kPw : 32;       // per TMEM store
+            const bool is_do = part >= kSub;
+            const int sub = part % kSub;
+            const __nv_bfloat16* src = is_do ? p.dout + static_cast<long long>(qc) * p.ldo + h * D
+                                             : p.q + static_cast<long long>(qc) * p.ldq + h * D;
             const bool in = qrow < p.T;
 #pragma unroll
-            for (int c = 0; c < D / 64; ++c) {
-                uint32_t w[32];
+            for (int c = sub * kPw; c < (sub + 1) * kPw; c += kW) {
+                uint32_t w[kW];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint4 x = in ? *reinterpret_cast<const uint4*>(src + c * 64 + u * 8) : make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < kW / 4; ++u) {
+                    const uint4 x = in ? *reinterpret_cast<const uint4*>(src + 2 * c + u * 8) : make_uint4(0, 0, 0, 0);
                     w[4 * u] = x.x;
                     w[4 * u + 1] = x.y;
                     w[4 * u + 2] = x.z;
                     w[4 * u + 3] = x.w;
                 }
-                tmem_st32((half ? t_doa : t_qa) + lane_off + c * 32, w);
+                tmem_stn<kW>((is_do ? t_doa : t_qa) + lane_off + c, w);
             }
             tmem_st_wait();
             tc_fence_before();
@@ -1244,47 +1294,33 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
         }
         const int qpos = (p.qo + qb) * BQ + r;  // this row's global query position
         for (int it = 0; it < n_it; ++it) {
-            if (threadIdx.x == 64) ATR(it * 8 + 7);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 7);
             mbar_wait(s_full, it & 1);
-            if (threadIdx.x == 64) ATR(it * 8 + 3);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 3);
             tc_fence_after();
-            uint32_t pv[64];
-            tmem_ld64(t_s + col, pv);
+            uint32_t pv[kEwCols];
+            tmem_ldn<kEwCols>(t_s + col, pv);
             tc_fence_before();
             mbar_arrive(s_free);
             const int qg0 = (p.qo + qb) * BQ;  // global position of the block's first query
             const int kt = c0 + it;  // absolute key tile
             const bool full_tile = kt * BKV + BKV - 1 <= qg0 && kt * BKV + BKV <= p.T_kv && qb * BQ + BQ <= p.T;
-            bwd_exp64<false>(pv, nullptr, nlse2, p.scale_log2);
+            bwd_exp<false>(pv, nullptr, nlse2, p.scale_log2);
             if (!full_tile) {
 #pragma unroll
-                for (int j = 0; j < 64; ++j) {
-                    const int key = kt * BKV + half * 64 + j;
+                for (int j = 0; j < kEwCols; ++j) {
+                    const int key = kt * BKV + part * kEwCols + j;
                     if (key > qpos || key >= p.T_kv) pv[j] = 0u;
                 }
             }
-            if (threadIdx.x == 64) ATR(it * 8 + 4);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 4);
             mbar_wait(dp_full, it & 1);
-            if (threadIdx.x == 64) ATR(it * 8 + 5);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 5);
             tc_fence_after();
-            {
-                uint32_t b[64];
-                tmem_ld64(t_dp + col, b);
-                uint32_t pd[32];
-#pragma unroll
-                for (int u = 0; u < 32; ++u) {
-                    const uint64_t ds = ffma2(
-                        f2_pack(__uint_as_float(pv[2 * u]), __uint_as_float(pv[2 * u + 1])),
-                        fadd2(f2_pack(__uint_as_float(b[2 * u]), __uint_as_float(b[2 * u + 1])), nd2), 0ull);
-                    float s0, s1;
-                    f2_unpack(ds, s0, s1);
-                    pd[u] = pack2(s0, s1);
-                }
-                tmem_st32(t_dp + col, pd);  // over the first 32 columns of this half (read above)
-            }
+            bwd_ds_store<false>(t_dp + col, pv, nullptr, nd2);
             tmem_st_wait();
             tc_fence_before();
-            if (threadIdx.x == 64) ATR(it * 8 + 6);
+            if (threadIdx.x == 32 * kEw0) ATR(it * 8 + 6);
             mbar_arrive(ds_full);
         }
         mbar_wait(acc_done, 0);
@@ -1292,24 +1328,25 @@ __device__ __forceinline__ void attn_bwd_dq_body(const CUtensorMap& tm_k, const 
         const bool ok = qrow < p.T;
         __nv_bfloat16* row = p.dq + static_cast<long long>(qrow) * p.lddq + h * D;
         float* prow = p.dq_part + (static_cast<long long>(slot) * BQ + r) * D;
+        constexpr int kPc = D / kEwParts;          // dQ columns per part
+        constexpr int kW = kPc < 32 ? kPc : 32;
 #pragma unroll 1
-        for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
-            uint32_t a[32];
-            tmem_ld32(t_dq + lane_off + c * 32, a);
-            tmem_ld_wait();
+        for (int c = part * kPc; c < (part + 1) * kPc; c += kW) {
+            uint32_t a[kW];
+            tmem_ldn<kW>(t_dq + lane_off + c, a);
             if (!ok) continue;
             if (slot == kDirect) {
 #pragma unroll
-                for (int t = 0; t < 32; t += 8) {
+                for (int t = 0; t < kW; t += 8) {
                     float f[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(a[t + u]) * p.scale;
-                    *reinterpret_cast<uint4*>(row + c * 32 + t) = pack8(f);
+                    *reinterpret_cast<uint4*>(row + c + t) = pack8(f);
                 }
             } else {
 #pragma unroll
-                for (int t = 0; t < 32; t += 4)
-                    *reinterpret_cast<float4*>(prow + c * 32 + t) =
+                for (int t = 0; t < kW; t += 4)
+                    *reinterpret_cast<float4*>(prow + c + t) =
                         make_float4(__uint_as_float(a[t]) * p.scale, __uint_as_float(a[t + 1]) * p.scale,
                                     __uint_as_float(a[t + 2]) * p.scale, __uint_as_float(a[t + 3]) * p.scale);
             }
