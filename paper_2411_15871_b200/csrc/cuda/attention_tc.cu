@@ -87,6 +87,10 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units
 #ifndef DH_ATTN_POLY
 #define DH_ATTN_POLY 1
 #endif
+// quarters of the backward's exponentials on the FMA pipe (0..3)
+#ifndef DH_ATTN_BWD_POLY_Q
+#define DH_ATTN_BWD_POLY_Q 1
+#endif
 
 template <int D>
 struct FwdSmem {
@@ -814,8 +818,10 @@ __device__ __forceinline__ void tmem_stn(uint32_t taddr, const uint32_t (&r)[N])
 }
 
 // p = 2^(s * scale_log2 + bias), bias per column (-log2e lse_j, PER_COL) or
-// per row; half of the pairs on the FMA pipe (the MUFU alone would need
-// 16384 / 16 = 1024 cycles per 128 x 128 tile).
+// per row; DH_ATTN_BWD_POLY_Q quarters of the pairs on the FMA pipe. The
+// split barely matters (attention bench, TP=1 bwd: 0.401 ms for a quarter,
+// 0.405 for a half or none, 0.419 for three quarters): the exp phase is not
+// MUFU-bound (profiles/r02_attn_bwd_investigation.txt).
 template <bool PER_COL, int N>
 __device__ __forceinline__ void bwd_exp(uint32_t (&s)[N], const float* bias, float bias_row, float scale_log2) {
     const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
@@ -832,7 +838,7 @@ __device__ __forceinline__ void bwd_exp(uint32_t (&s)[N], const float* bias, flo
         float x0, x1;
         f2_unpack(x, x0, x1);
         float e0, e1;
-        if (DH_ATTN_POLY && (u & 1)) {
+        if (DH_ATTN_POLY && (u & 3) >= 4 - DH_ATTN_BWD_POLY_Q) {
             f2_unpack(exp2_fma2(x0, x1), e0, e1);
         } else {
             e0 = fast_exp2(x0);
