@@ -215,39 +215,134 @@ __global__ void __launch_bounds__(RB == 1 ? 1024 : 512) rmsnorm_bwd_rows(const u
 }
 
 
-// One-launch RMSNorm backward (cols % 64 == 0): blocks [0, n_dg) reduce
-// dgamma over 64-column slices of all rows (dgamma needs only x, dy and the
-// saved rstd, no row reduction), the remaining blocks each produce one dx row.
-// Both kinds read their inputs independently, so the launch has no second
-// pass and no cross-block reduction; dgamma is summed in a fixed order (row
-// lanes, then lane order), hence deterministic. T = cols / 8 threads per block.
+// RMSNorm backward over row tiles (cols == VPT * TPR * 8): a block of TPR
+// threads owns R consecutive rows, produces their dx rows one after another
+// (the next row's loads issued before the current row's reduction) and its
+// fp32 dgamma partial over the R rows, partial[block][cols]; column_reduce_add
+// sums the partials in block order (deterministic). Long-lived blocks keep the
+// loads streaming: one-row blocks of cols / 8 threads spend most of their
+// life launching and synchronising (tools/micro/rmsnorm_var.cu).
+template <int VPT, int TPR, int R>
+__global__ void __launch_bounds__(TPR) rmsnorm_bwd_tile(const uint4* __restrict__ x, const uint4* __restrict__ g,
+                                                        const float* __restrict__ rstd, const uint4* __restrict__ dy,
+                                                        const uint4* __restrict__ resid, uint4* __restrict__ dx,
+                                                        float* __restrict__ partial, int rows, float inv_cols) {
+    constexpr int kW = TPR / 32, kVc = VPT * TPR;
+    __shared__ float red[2][kW];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int row0 = blockIdx.x * R;
+    float gam[VPT][8], dg[VPT][8];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        unpack8(g[i * TPR + t], gam[i]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dg[i][k] = 0.f;
+    }
+    uint4 xn[VPT], dn[VPT];
+    float rn = 0.f;
+    auto load = [&](int row) {
+        const bool ok = row < rows;
+        const long long base = static_cast<long long>(row) * kVc + t;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            xn[i] = ok ? __ldcs(x + base + i * TPR) : make_uint4(0, 0, 0, 0);
+            dn[i] = ok ? __ldcs(dy + base + i * TPR) : make_uint4(0, 0, 0, 0);
+        }
+        rn = ok ? rstd[row] : 0.f;
+    };
+    load(row0);
+#pragma unroll 1
+    for (int j = 0; j < R; ++j) {
+        const int row = row0 + j;
+        float xv[VPT][8], dv[VPT][8];
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            unpack8(xn[i], xv[i]);
+            unpack8(dn[i], dv[i]);
+        }
+        const float rr = rn;
+        if (j + 1 < R) load(row + 1);
+        float dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                xv[i][k] *= rr;                 // xhat
+                dg[i][k] += dv[i][k] * xv[i][k];
+                dv[i][k] *= gam[i][k];          // dxhat
+                dot += dv[i][k] * xv[i][k];
+            }
+        dot = warp_sum(dot);
+        if (lane == 0) red[j & 1][wid] = dot;
+        __syncthreads();
+        float tot = 0.f;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) tot += red[j & 1][w];
+        tot *= inv_cols;
+        if (row < rows) {
+            const long long base = static_cast<long long>(row) * kVc + t;
+#pragma unroll
+            for (int i = 0; i < VPT; ++i) {
+                float o[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o[k] = rr * (dv[i][k] - xv[i][k] * tot);
+                if (resid) {
+                    float rv[8];
+                    unpack8(__ldcs(resid + base + i * TPR), rv);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) o[k] += rv[k];
+                }
+                dx[base + i * TPR] = pack8(o);
+            }
+        }
+    }
+    float* prow = partial + static_cast<long long>(blockIdx.x) * kVc * 8;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        float4* dst = reinterpret_cast<float4*>(prow + (i * TPR + t) * 8);
+        dst[0] = make_float4(dg[i][0], dg[i][1], dg[i][2], dg[i][3]);
+        dst[1] = make_float4(dg[i][4], dg[i][5], dg[i][6], dg[i][7]);
+    }
+}
+
+// One-launch RMSNorm backward (cols % (8 CV) == 0): blocks [0, n_dg) reduce
+// dgamma over (8 CV)-column slices of all rows (dgamma needs only x, dy and
+// the saved rstd, no row reduction), the remaining blocks each produce one dx
+// row. Both kinds read their inputs independently, so the launch has no
+// second pass and no cross-block reduction; dgamma is summed in a fixed order
+// (row lanes, then lane order), hence deterministic. T = cols / 8 threads per
+// block. A dgamma block streams all rows of its slice, so it is latency-bound:
+// U rows per thread in flight, and narrow slices (CV = 4: 32 columns, cols / 32
+// blocks) keep it shorter than the dx rows.
+template <int CV, int U, int RPB>
 __global__ void __launch_bounds__(1024) rmsnorm_bwd_fused(const uint4* __restrict__ x, const uint4* __restrict__ g,
                                                           const float* __restrict__ rstd, const uint4* __restrict__ dy,
                                                           const uint4* __restrict__ resid, uint4* __restrict__ dx,
                                                           float* __restrict__ dgamma_acc, int rows, int vec_cols,
                                                           float inv_cols, int n_dg) {
-    __shared__ float red[1024 / 8 * 65];  // dgamma: [row lane][64 columns (+1 pad)]; dx: per-warp dots
+    constexpr int kSc = 8 * CV;  // columns per dgamma slice
+    __shared__ float red[1024 / CV * (kSc + 1)];  // dgamma: [row lane][slice columns (+1 pad)]; dx: per-warp dots
     const int t = threadIdx.x, T = blockDim.x;
     if (static_cast<int>(blockIdx.x) < n_dg) {
         if (!dgamma_acc) return;
-        const int cl = t & 7, rl = t >> 3, RL = T >> 3;
-        const int vc = blockIdx.x * 8 + cl;  // this thread's 16-byte column vector
+        const int cl = t % CV, rl = t / CV, RL = T / CV;
+        const int vc = blockIdx.x * CV + cl;  // this thread's 16-byte column vector
         float acc[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc[k] = 0.f;
         int r = rl;
-        for (; r + 3 * RL < rows; r += 4 * RL) {  // four rows' loads in flight
-            uint4 xv[4], dv[4];
-            float rr[4];
+        for (; r + (U - 1) * RL < rows; r += U * RL) {  // U rows' loads in flight
+            uint4 xv[U], dv[U];
+            float rr[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const long long off = static_cast<long long>(r + u * RL) * vec_cols + vc;
                 xv[u] = __ldcs(x + off);
                 dv[u] = __ldcs(dy + off);
                 rr[u] = rstd[r + u * RL];
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 float a[8], b[8];
                 unpack8(xv[u], a);
                 unpack8(dv[u], b);
@@ -265,46 +360,60 @@ __global__ void __launch_bounds__(1024) rmsnorm_bwd_fused(const uint4* __restric
             for (int k = 0; k < 8; ++k) acc[k] += b[k] * (a[k] * rr);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) red[rl * 65 + cl * 8 + k] = acc[k];
+        for (int k = 0; k < 8; ++k) red[rl * (kSc + 1) + cl * 8 + k] = acc[k];
         __syncthreads();
-        for (int c = t; c < 64; c += T) {
+        for (int c = t; c < kSc; c += T) {
             float sum = 0.f;
-            for (int j = 0; j < RL; ++j) sum += red[j * 65 + c];
-            dgamma_acc[blockIdx.x * 64 + c] += sum;
+            for (int j = 0; j < RL; ++j) sum += red[j * (kSc + 1) + c];
+            dgamma_acc[blockIdx.x * kSc + c] += sum;
         }
         return;
     }
-    const int row = blockIdx.x - n_dg;
-    const int lane = t & 31, wid = t >> 5, nw = T >> 5;
-    const long long off = static_cast<long long>(row) * vec_cols + t;
-    float xv[8], dv[8], gam[8];
-    unpack8(__ldcs(x + off), xv);
-    unpack8(__ldcs(dy + off), dv);
-    unpack8(g[t], gam);
-    const float rr = rstd[row];
+    // dx: RPB rows per block, T / RPB threads per row, RPB vectors per thread;
+    // the residual is loaded with x and dy (one memory round trip per block)
+    const int tpr = T / RPB, sub = t / tpr, tt = t % tpr;
+    const int row = (blockIdx.x - n_dg) * RPB + sub;
+    const bool ok = row < rows;
+    const int lane = t & 31, wid = t >> 5, wpr = tpr >> 5;
+    const long long base = static_cast<long long>(row) * vec_cols + tt;
+    uint4 xr[RPB], dr[RPB], rr4[RPB];
+#pragma unroll
+    for (int i = 0; i < RPB; ++i) {
+        xr[i] = ok ? __ldcs(x + base + i * tpr) : make_uint4(0, 0, 0, 0);
+        dr[i] = ok ? __ldcs(dy + base + i * tpr) : make_uint4(0, 0, 0, 0);
+        rr4[i] = ok && resid ? __ldcs(resid + base + i * tpr) : make_uint4(0, 0, 0, 0);
+    }
+    const float rr = ok ? rstd[row] : 0.f;
+    float xv[RPB][8], dv[RPB][8];
     float dot = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        xv[k] *= rr;        // xhat
-        dv[k] *= gam[k];    // dxhat
-        dot += dv[k] * xv[k];
+    for (int i = 0; i < RPB; ++i) {
+        float gam[8];
+        unpack8(xr[i], xv[i]);
+        unpack8(dr[i], dv[i]);
+        unpack8(g[tt + i * tpr], gam);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            xv[i][k] *= rr;        // xhat
+            dv[i][k] *= gam[k];    // dxhat
+            dot += dv[i][k] * xv[i][k];
+        }
     }
     dot = warp_sum(dot);
     if (lane == 0) red[wid] = dot;
     __syncthreads();
+    if (!ok) return;
     float tot = 0.f;
-    for (int w = 0; w < nw; ++w) tot += red[w];
+    for (int w = 0; w < wpr; ++w) tot += red[sub * wpr + w];
     tot *= inv_cols;
-    float o[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = rr * (dv[k] - xv[k] * tot);
-    if (resid) {
-        float rv[8];
-        unpack8(__ldcs(resid + off), rv);
+    for (int i = 0; i < RPB; ++i) {
+        float o[8], rv[8];
+        unpack8(rr4[i], rv);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] += rv[k];
+        for (int k = 0; k < 8; ++k) o[k] = rr * (dv[i][k] - xv[i][k] * tot) + rv[k];
+        dx[base + i * tpr] = pack8(o);
     }
-    dx[off] = pack8(o);
 }
 
 // dgamma_acc[c] += sum_w partial[w][c]. Block = 32 columns x 8 warps; warp j
@@ -317,14 +426,14 @@ __global__ void column_reduce_add(const float* __restrict__ partial, float* __re
     const int c = blockIdx.x * 32 + lane;
     float s = 0.f;
     if (c < cols) {
-        float a[4] = {0.f, 0.f, 0.f, 0.f};  // 4 loads in flight; combined in a fixed order
+        float a[8] = {};  // 8 loads in flight; combined in a fixed order
         int w = warp;
-        for (; w + 24 < nw; w += 32) {
+        for (; w + 56 < nw; w += 64) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) a[u] += partial[static_cast<long long>(w + 8 * u) * cols + c];
+            for (int u = 0; u < 8; ++u) a[u] += partial[static_cast<long long>(w + 8 * u) * cols + c];
         }
         for (; w < nw; w += 8) a[0] += partial[static_cast<long long>(w) * cols + c];
-        s = (a[0] + a[1]) + (a[2] + a[3]);
+        s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
     red[warp][lane] = s;
     __syncthreads();
@@ -708,8 +817,8 @@ int dh_add_rmsnorm_fwd(const void* x, const void* resid, void* x_out, const void
         case 512: rmsnorm_fwd_reg<2><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO); break;
         case 1024: rmsnorm_fwd_reg<4><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO); break;
         case 2048: rmsnorm_fwd_reg<8><<<grid, block, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO); break;
-        case 4096:
-            rmsnorm_fwd_split<4, 128, 2><<<(rows + 1) / 2, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO);
+        case 4096:  // one row per 256-thread block (16.5 -> 14.4 us at 4096 rows, tools/micro/rmsnorm_var.cu)
+            rmsnorm_fwd_split<2, 256, 1><<<rows, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO);
             break;
         case 8192:
             rmsnorm_fwd_split<4, 256, 1><<<rows, 256, 0, s>>>(X, G, Y, rstd, rows, ic, eps, B, XO);
@@ -737,8 +846,12 @@ int dh_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const vo
         return e && e[0] == '0';
     }();
     if (cols % 64 == 0 && cols / 8 >= 32 && !fused_off) {
+        // two dx rows per block where a half row is whole warps (4096 columns:
+        // 36.7 -> 26.7 us at 4096 rows, tools/micro/rmsnorm_var.cu)
         const int n_dg = cols / 64;
-        rmsnorm_bwd_fused<<<n_dg + rows, cols / 8, 0, s>>>(
+        const bool two = cols % 512 == 0;
+        auto kern = two ? rmsnorm_bwd_fused<8, 4, 2> : rmsnorm_bwd_fused<8, 4, 1>;
+        kern<<<n_dg + (two ? (rows + 1) / 2 : rows), cols / 8, 0, s>>>(
             static_cast<const uint4*>(x), static_cast<const uint4*>(gamma), rstd, static_cast<const uint4*>(dy),
             static_cast<const uint4*>(resid), static_cast<uint4*>(dx), dgamma_acc, rows, cols / 8, 1.f / cols, n_dg);
         DH_CUDA_CHECK(cudaGetLastError());
