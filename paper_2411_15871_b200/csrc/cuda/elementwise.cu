@@ -497,59 +497,36 @@ __global__ void swiglu_bwd_kernel(const uint4* __restrict__ gate, const uint4* _
 // Vectorised form (head_dim % 16 == 0, 16-byte aligned rows): the block's
 // threads first compute the token's half cos/sin pairs once (fp64, same formula),
 // then rotate 8 consecutive pairs per thread with 16-byte loads and stores.
-template <int TOK>  // tokens per block, 128 threads each
-__global__ void __launch_bounds__(128 * TOK) rope_vec_kernel(__nv_bfloat16* __restrict__ qkv, long long ld,
-                                                             int tokens, int heads, int head_dim,
-                                                             double log_theta, int pos0, float sign) {
-    constexpr int kPre = 4;  // 8-element pairs per thread loaded before the table is built
-    __shared__ float cs[TOK][2][256];
-    const int sub = threadIdx.x / 128, tid = threadIdx.x % 128;
+__global__ void __launch_bounds__(128) rope_vec_kernel(__nv_bfloat16* __restrict__ qkv, long long ld,
+                                                       int tokens, int heads, int head_dim,
+                                                       double log_theta, int pos0, float sign) {
+    __shared__ float cs[2][256];
     const int half = head_dim / 2;
-    const int t = blockIdx.x * TOK + sub;
-    const bool ok = t < tokens;
-    const int per_head = half / 8, items = heads * per_head;
-    __nv_bfloat16* row = qkv + static_cast<long long>(ok ? t : 0) * ld;
-    // issue this thread's loads first: the table (fp64 trig) is built while
-    // they are in flight
-    uint4 ua[kPre], ub[kPre];
-#pragma unroll
-    for (int j = 0; j < kPre; ++j) {
-        const int w = tid + j * 128;
-        if (ok && w < items) {
-            const int h = w / per_head, i0 = (w % per_head) * 8;
-            ua[j] = *reinterpret_cast<const uint4*>(row + h * head_dim + i0);
-            ub[j] = *reinterpret_cast<const uint4*>(row + h * head_dim + half + i0);
-        }
-    }
-    for (int i = tid; i < half; i += 128) {
+    const int t = blockIdx.x;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
         const double inv_freq = exp(-log_theta * (2.0 * i) / head_dim);
         const double ang = static_cast<double>(t + pos0) * inv_freq;
-        cs[sub][0][i] = static_cast<float>(cos(ang));
-        cs[sub][1][i] = sign * static_cast<float>(sin(ang));
+        cs[0][i] = static_cast<float>(cos(ang));
+        cs[1][i] = sign * static_cast<float>(sin(ang));
     }
     __syncthreads();
-    if (!ok) return;
-    auto rotate = [&](int w, uint4 va, uint4 vb) {
+    __nv_bfloat16* row = qkv + static_cast<long long>(t) * ld;
+    const int per_head = half / 8;
+    for (int w = threadIdx.x; w < heads * per_head; w += blockDim.x) {
         const int h = w / per_head, i0 = (w % per_head) * 8;
+        uint4* pa = reinterpret_cast<uint4*>(row + h * head_dim + i0);
+        uint4* pb = reinterpret_cast<uint4*>(row + h * head_dim + half + i0);
         float a[8], b[8], oa[8], ob[8];
-        unpack8(va, a);
-        unpack8(vb, b);
+        unpack8(*pa, a);
+        unpack8(*pb, b);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const float c = cs[sub][0][i0 + k], sn = cs[sub][1][i0 + k];
+            const float c = cs[0][i0 + k], sn = cs[1][i0 + k];
             oa[k] = a[k] * c - b[k] * sn;
             ob[k] = b[k] * c + a[k] * sn;
         }
-        *reinterpret_cast<uint4*>(row + h * head_dim + i0) = pack8(oa);
-        *reinterpret_cast<uint4*>(row + h * head_dim + half + i0) = pack8(ob);
-    };
-#pragma unroll
-    for (int j = 0; j < kPre; ++j)
-        if (tid + j * 128 < items) rotate(tid + j * 128, ua[j], ub[j]);
-    for (int w = tid + kPre * 128; w < items; w += 128) {  // wide rows (> 512 pairs)
-        const int h = w / per_head, i0 = (w % per_head) * 8;
-        rotate(w, *reinterpret_cast<const uint4*>(row + h * head_dim + i0),
-               *reinterpret_cast<const uint4*>(row + h * head_dim + half + i0));
+        *pa = pack8(oa);
+        *pb = pack8(ob);
     }
 }
 
@@ -935,7 +912,7 @@ int dh_rope(void* qkv, long long ld, int tokens, int n_q_heads, int n_kv_heads, 
     if (head_dim % 2) return set_error(DH_ERR_INVALID, "rope: odd head_dim");
     if (tokens <= 0) return DH_OK;
     if (head_dim % 16 == 0 && head_dim <= 512 && aligned16(qkv) && ld % 8 == 0) {
-        rope_vec_kernel<1><<<tokens, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        rope_vec_kernel<<<tokens, 128, 0, static_cast<cudaStream_t>(stream)>>>(
             static_cast<__nv_bfloat16*>(qkv), ld, tokens, n_q_heads + n_kv_heads, head_dim,
             std::log(static_cast<double>(theta)), pos0, inverse ? -1.f : 1.f);
         DH_CUDA_CHECK(cudaGetLastError());

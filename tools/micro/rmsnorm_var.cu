@@ -1,4 +1,4 @@
-// Microbenchmark (tooling, not product): RMSNorm forward / backward and RoPE kernel
+// Microbenchmark (tooling, not product): RMSNorm forward / backward kernel
 // variants of csrc/cuda/elementwise.cu at the Llama-3-8B row width (4096) for
 // the TP=1 (4096 rows) and TP=8 (512 rows) shapes; each variant launched 50x
 // back to back between CUDA events after warm-up (warm L2 as in the step).
@@ -96,18 +96,6 @@ int main() {
         rep("bwd dx rows only <8,4,2>", mb3 + mb2 / 2, time_us([&] {
                 rmsnorm_bwd_fused<8, 4, 2><<<64 + rows / 2, vc>>>(x, g, rstd, dy, res, dx, nullptr, rows, vc, ic, 64);
             }));
-        {  // RoPE over the q and k heads of the fused qkv rows (TP=1: 32 + 8 heads, TP=8: 4 + 1)
-            const int heads = rows == 4096 ? 40 : 5, D = 128, ldq = (heads + (rows == 4096 ? 8 : 1)) * D;
-            __nv_bfloat16* qkv;
-            cudaMalloc(&qkv, static_cast<size_t>(rows) * ldq * 2);
-            cudaMemset(qkv, 0x3c, static_cast<size_t>(rows) * ldq * 2);
-            const double mb = 2.0 * rows * heads * D * 2 / 1e6, lt = std::log(500000.0);
-            rep("rope<1>", mb, time_us([&] { rope_vec_kernel<1><<<rows, 128>>>(qkv, ldq, rows, heads, D, lt, 0, 1.f); }));
-            rep("rope<2>", mb, time_us([&] {
-                    rope_vec_kernel<2><<<(rows + 1) / 2, 256>>>(qkv, ldq, rows, heads, D, lt, 0, 1.f);
-                }));
-            cudaFree(qkv);
-        }
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
         cudaFree(x); cudaFree(y); cudaFree(dy); cudaFree(dx); cudaFree(res); cudaFree(g); cudaFree(rstd); cudaFree(dg);
