@@ -22,13 +22,15 @@ ap.add_argument("--tp", type=int, default=8)
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--mb", type=int, default=4)
 ap.add_argument("--mode", default="si")
+ap.add_argument("--wide", action="store_true", help="the bench's wide search caps (si_wide* variants)")
 a = ap.parse_args()
 shape = LlamaShape(**{**LLAMA3_8B.__dict__, "layers": a.layers, "micro_batches": a.mb, "slots": a.layers + 2})
 ctx = Context.emulated(0, a.tp, 16, 770.0) if a.tp > 1 else Context.create(0)
 m = Model(ctx, shape)
 m.set_overlap_ctas(148 - 16)
 prof = json.loads(m.profile(iters=5))
-caps = {"sequences": 16, "segments": 14, "candidates": 200000}
+caps = ({"sequences": 64, "segments": 14, "candidates": 1000000} if a.wide
+        else {"sequences": 16, "segments": 14, "candidates": 200000})
 plan = planner.lib().search_si_plan(shape.planner_model(), {"tp": a.tp, "sp": a.tp > 1}, B200_CLUSTER, prof,
                                     caps=caps, parallel=True)["plan_json"]
 m.set_plan(plan, json.dumps(prof), mode=a.mode)
@@ -81,6 +83,14 @@ hidden = overlap(comp, comm)
 # compute-lane idle gaps, attributed to the op that ends each gap and what it waited on
 gaps = collections.Counter()
 gap_n = collections.Counter()
+steady = collections.Counter()  # gaps before ops of the paired middle (not F_0 / B_last)
+
+
+def at_end(o):
+    fwd = o["node"] < 20
+    return (fwd and o["strand"] == 0) or (not fwd and o["node"] != 100 and o["strand"] == a.mb - 1)
+
+
 comp_ops = sorted((o for o in ops if o["lane"] == 0), key=lambda o: o["start_ms"])
 prev_end = 0.0
 for o in comp_ops:
@@ -91,12 +101,16 @@ for o in comp_ops:
         key = f"{names.get(o['node'], o['node'])} <- {why}"
         gaps[key] += g
         gap_n[key] += 1
+        if not at_end(o):
+            steady[key] += g
     prev_end = max(prev_end, o["end_ms"])
 res = {"tp": a.tp, "layers": a.layers, "micro_batches": a.mb, "mode": a.mode, "step_ms": round(end, 3),
        "compute_busy_ms": round(comp_busy, 3), "compute_idle_ms": round(end - comp_busy, 3),
        "comm_busy_ms": round(comm_busy, 3), "comm_hidden_ms": round(hidden, 3),
        "comm_exposed_ms": round(comm_busy - hidden, 3),
-       "top_compute_gaps": [{"gap": k, "ms": round(v, 3), "count": gap_n[k]} for k, v in gaps.most_common(15)]}
+       "top_compute_gaps": [{"gap": k, "ms": round(v, 3), "count": gap_n[k]} for k, v in gaps.most_common(15)],
+       "steady_gaps_ms": round(sum(steady.values()), 3),
+       "top_steady_gaps": [{"gap": k, "ms": round(v, 3)} for k, v in steady.most_common(10)]}
 print(json.dumps(res, indent=1))
 json.dump({"summary": res, "ops": ops}, open(os.path.join(ROOT, "gpurun_out", f"op_timeline_tp{a.tp}.json"), "w"))
 # Chrome trace (chrome://tracing, Perfetto): one row per lane, an event per op
