@@ -87,7 +87,10 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units
 #ifndef DH_ATTN_POLY
 #define DH_ATTN_POLY 1
 #endif
-// quarters of the backward's exponentials on the FMA pipe (0..3)
+// quarters of the forward's / backward's exponentials on the FMA pipe (0..3)
+#ifndef DH_ATTN_FWD_POLY_Q
+#define DH_ATTN_FWD_POLY_Q 1
+#endif
 #ifndef DH_ATTN_BWD_POLY_Q
 #define DH_ATTN_BWD_POLY_Q 1
 #endif
@@ -375,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // a quarter of the exponentials run on the FMA pipe: both
                     // softmax tiles together would otherwise saturate the MUFU
                     uint64_t pp;
-                    if (DH_ATTN_POLY && (u & 3) == 3) {
+                    if (DH_ATTN_POLY && (u & 3) >= 4 - DH_ATTN_FWD_POLY_Q) {
                         float x0, x1;
                         f2_unpack(x, x0, x1);
                         pp = exp2_fma2(x0, x1);
