@@ -874,6 +874,9 @@ __device__ __forceinline__ void bwd_ds_store(uint32_t taddr, const uint32_t (&pv
     tmem_stn<N / 2>(taddr, pd);
 }
 
+// ptxas spills two scalars of this body (the item's slot and kv head, 12 bytes,
+// read once in the epilogue); re-reading them from shared memory instead
+// removes the spill but measured 1-2% slower (register allocation of the loop).
 template <int D>
 __device__ __forceinline__ void attn_bwd_dkdv_body(const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                                    const CUtensorMap& tm_q, const CUtensorMap& tm_do,
