@@ -179,6 +179,22 @@ struct Lowering {
     // of its readers (tests/test_executor_lowering.py, buffer hazards). GEMMs
     // issued while a collective of the layer is still open are capped like
     // co-running ones.
+    //
+    // Mode 4 at TP > 1 also moves the lone strand's weight gradients under its
+    // collectives (the plan's order leaves three of the four exposed:
+    // tools/op_timeline.py): mlp_down_wgrad after ag1_bwd_rs (the RS of the MLP
+    // input gradient), mlp_fc1_wgrad after rs0_bwd_ag (the AG before
+    // attn_proj_dgrad), and the attention weight gradients (attn_proj_wgrad,
+    // qkv_wgrad) into the next layer, right after its rs1_bwd_ag — the mode-4
+    // deferral of the SI pairs. Their inputs are rewritten only by later ops
+    // of the next layer (d_gate / d_up by mlp_down_dgrad, dx1_full by
+    // rs0_bwd_ag, dqkv by attn_bwd), which the buffer-hazard tests check.
+    bool lone_reorder = [] {
+        const char* e = std::getenv("DH_SI_LONE_REORDER");
+        return !e || std::atoi(e) != 0;
+    }();
+    bool lone_defers() const { return defer_wgrads && lone_reorder && !m.cfg.moe && m.cfg.tp > 1; }
+
     void backward_layer_dag(int strand, int layer) {
         std::map<int, std::vector<int>> preds;
         for (const auto& [a, b] : m.bwd_dag.edges) preds[b].push_back(a);
@@ -186,7 +202,24 @@ struct Lowering {
         std::vector<int> open_comm;  // comm nodes whose consumers are not emitted yet
         const int prev_last = strand_last[strand];
         int last = prev_last;
-        for (int id : m.plan.bwd_seq) {
+        std::vector<int> seq = m.plan.bwd_seq;
+        const bool reorder = lone_defers();
+        auto has = [&](int id) { return std::find(seq.begin(), seq.end(), id) != seq.end(); };
+        if (reorder && has(23) && has(26) && has(27) && has(30) && has(32) && has(36)) {
+            auto move_after = [&](int id, int anchor) {
+                seq.erase(std::find(seq.begin(), seq.end(), id));
+                seq.insert(std::find(seq.begin(), seq.end(), anchor) + 1, id);
+            };
+            move_after(23, 27);
+            move_after(26, 30);
+            seq.erase(std::find(seq.begin(), seq.end(), 32));
+            seq.erase(std::find(seq.begin(), seq.end(), 36));
+        } else if (reorder) {
+            flush_deferred();
+        }
+        const bool defer_attn = reorder && !has(32);
+        bool flushed = false;
+        for (int id : seq) {
             std::vector<int> deps;
             for (int p : preds[id]) deps.push_back(at.at(p));
             if (deps.empty() && prev_last >= 0) deps.push_back(prev_last);
@@ -195,14 +228,29 @@ struct Lowering {
             capped = !comm && !open_comm.empty();
             emit(strand, layer, id, -1, &deps);
             at[id] = static_cast<int>(prog.ops.size()) - 1;
+            bwd_op_at[{strand, layer, id}] = at[id];
             if (comm) open_comm.push_back(id);
             // the layer's completion point for the next layer's sources: its
             // compute-lane tail (every comm op feeds a later compute op)
             if (prog.ops.back().lane == 0) last = at[id];
+            if (comm && !flushed && deferred.strand >= 0) {
+                // the previous layer's attention weight gradients run under this
+                // layer's first collective
+                strand_last[strand] = last;
+                flush_deferred();
+                flushed = true;
+            }
         }
         capped = false;
+        if (!flushed) flush_deferred();
         strand_last[strand] = last;
-        give_slot(strand, layer);
+        if (defer_attn) {
+            deferred.strand = strand;
+            deferred.layer = layer;
+            deferred.nodes = {32, 36};  // slot released by flush_deferred()
+        } else {
+            give_slot(strand, layer);
+        }
     }
 
     double solo(int id, const weft::LayerDag& dag) {
@@ -513,10 +561,23 @@ int lower_ops(Model& m, int mode) {
                 if (blk.kind == weft::BlockKind::F) {
                     for (int l = 0; l < L; ++l) lw.forward_layer(*blk.fwd_mb - 1, l);
                 } else if (blk.kind == weft::BlockKind::B) {
+                    // mode 4: the lone strand defers each layer's attention weight
+                    // gradients into the next layer, so that layer's AdamW follows
+                    // the next layer's backward
+                    const bool last_strand = *blk.bwd_mb == mb;
+                    lw.defer_wgrads = mode == 4;
+                    const bool lag = lw.lone_defers();
                     for (int l = L - 1; l >= 0; --l) {
                         lw.backward_layer_dag(*blk.bwd_mb - 1, l);
-                        if (*blk.bwd_mb == mb) lw.emit_opt(mb - 1, l);
+                        if (last_strand && !lag) lw.emit_opt(mb - 1, l);
+                        if (last_strand && lag && l + 1 < L) lw.emit_opt(mb - 1, l + 1);
                     }
+                    if (lw.deferred.strand >= 0) {
+                        lw.flush_deferred();
+                        lw.strand_last[*blk.bwd_mb - 1] = lw.lane_last[0];  // AdamW(0) follows them
+                    }
+                    if (last_strand && lag) lw.emit_opt(mb - 1, 0);
+                    lw.defer_wgrads = false;
                 } else {
                     lw.defer_wgrads = mode == 4;
                     for (int k = 0; k < L; ++k)
