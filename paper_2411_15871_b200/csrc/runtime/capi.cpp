@@ -284,7 +284,7 @@ int dh_lower_json(const dh_model_cfg* cfg, int tp, int rank, const char* plan_js
     for (const auto& o : m.prog.ops) {
         ops.push_back({{"strand", o.strand}, {"layer", o.layer}, {"node", o.node}, {"lane", o.lane},
                        {"slot", o.slot}, {"prev_slot", o.prev_slot}, {"first_dx", o.first_dx},
-                       {"peer", o.peer}, {"waits", o.waits}});
+                       {"peer", o.peer}, {"part", o.part}, {"waits", o.waits}});
     }
     json j = {{"ops", ops}, {"slots", m.cfg.slots > 0 ? m.cfg.slots : m.cfg.layers + 1},
               {"peak_slots", m.peak_slots}, {"fwd_seq", m.plan.fwd_seq},

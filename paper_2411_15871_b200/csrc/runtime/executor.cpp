@@ -74,6 +74,7 @@ struct Lowering {
     // time), so their GEMMs never share the GPU with a collective and take
     // every SM; inside a block the cap applies wherever a collective may co-run.
     bool capped = false;
+    int cur_part = -1;  // Op::part of the next mlp_fc1_wgrad emitted
 
     // deps (optional): the op's data predecessors (op indices) replace the
     // strand-order wait, so a strand can overlap its own independent ops
@@ -92,6 +93,7 @@ struct Lowering {
         o.slot = slot_of[strand][layer];
         o.prev_slot = layer > 0 ? slot_of[strand][layer - 1] : -1;
         o.capped = capped;
+        o.part = node == 26 ? cur_part : -1;
         if (xfer) {
             // nothing node-specific
         } else if (m.cfg.moe) {
@@ -183,12 +185,14 @@ struct Lowering {
     // Mode 4 at TP > 1 also moves the lone strand's weight gradients under its
     // collectives (the plan's order leaves three of the four exposed:
     // tools/op_timeline.py): mlp_down_wgrad after ag1_bwd_rs (the RS of the MLP
-    // input gradient), mlp_fc1_wgrad after rs0_bwd_ag (the AG before
-    // attn_proj_dgrad), and the attention weight gradients (attn_proj_wgrad,
-    // qkv_wgrad) into the next layer, right after its rs1_bwd_ag — the mode-4
-    // deferral of the SI pairs. Their inputs are rewritten only by later ops
-    // of the next layer (d_gate / d_up by mlp_down_dgrad, dx1_full by
-    // rs0_bwd_ag, dqkv by attn_bwd), which the buffer-hazard tests check.
+    // input gradient), mlp_fc1_wgrad split into its gate and up launches after
+    // rs0_bwd_ag (the AG before attn_proj_dgrad) and after ag0_bwd_rs (the RS
+    // of the layer's input gradient), and the attention weight gradients
+    // (attn_proj_wgrad, qkv_wgrad) into the next layer, right after its
+    // rs1_bwd_ag — the mode-4 deferral of the SI pairs. Their inputs are
+    // rewritten only by later ops of the next layer (d_gate / d_up by
+    // mlp_down_dgrad, dx1_full by rs0_bwd_ag, dqkv by attn_bwd), which the
+    // buffer-hazard tests check.
     bool lone_reorder = [] {
         const char* e = std::getenv("DH_SI_LONE_REORDER");
         return !e || std::atoi(e) != 0;
@@ -205,28 +209,37 @@ struct Lowering {
         std::vector<int> seq = m.plan.bwd_seq;
         const bool reorder = lone_defers();
         auto has = [&](int id) { return std::find(seq.begin(), seq.end(), id) != seq.end(); };
-        if (reorder && has(23) && has(26) && has(27) && has(30) && has(32) && has(36)) {
+        std::vector<int> part_of(seq.size(), -1);
+        if (reorder && has(23) && has(26) && has(27) && has(30) && has(32) && has(36) && has(37)) {
             auto move_after = [&](int id, int anchor) {
                 seq.erase(std::find(seq.begin(), seq.end(), id));
                 seq.insert(std::find(seq.begin(), seq.end(), anchor) + 1, id);
             };
             move_after(23, 27);
             move_after(26, 30);
+            seq.insert(std::find(seq.begin(), seq.end(), 37) + 1, 26);  // the up half
             seq.erase(std::find(seq.begin(), seq.end(), 32));
             seq.erase(std::find(seq.begin(), seq.end(), 36));
+            part_of.assign(seq.size(), -1);
+            int k = 0;
+            for (std::size_t i = 0; i < seq.size(); ++i)
+                if (seq[i] == 26) part_of[i] = k++;
         } else if (reorder) {
             flush_deferred();
         }
         const bool defer_attn = reorder && !has(32);
         bool flushed = false;
-        for (int id : seq) {
+        for (std::size_t si = 0; si < seq.size(); ++si) {
+            const int id = seq[si];
             std::vector<int> deps;
             for (int p : preds[id]) deps.push_back(at.at(p));
             if (deps.empty() && prev_last >= 0) deps.push_back(prev_last);
             for (int p : preds[id]) open_comm.erase(std::remove(open_comm.begin(), open_comm.end(), p), open_comm.end());
             const bool comm = lane_of.at(id) != 0;
             capped = !comm && !open_comm.empty();
+            cur_part = part_of[si];
             emit(strand, layer, id, -1, &deps);
+            cur_part = -1;
             at[id] = static_cast<int>(prog.ops.size()) - 1;
             bwd_op_at[{strand, layer, id}] = at[id];
             if (comm) open_comm.push_back(id);

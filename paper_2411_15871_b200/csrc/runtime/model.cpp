@@ -615,6 +615,11 @@ int launch_node(Model& m, const Op& op, cudaStream_t s) {
             return dh_gemm(&g, s);
         }
         case 26: {  // mlp_fc1_wgrad: dWg, dWu [F,H] += d_{gate,up}^T ln1, one M-concatenated GEMM
+            if (op.part >= 0) {  // one of the two (the executor placed them under different collectives)
+                dh_gemm_args g = gemm_args(P(op.part ? m.bs.d_up : m.bs.d_gate), F, true, P(sl.ln1_full), H, true,
+                                           G + (op.part ? p.wu : p.wg), H, true, F, H, S, true, cap);
+                return dh_gemm(&g, s);
+            }
             dh_gemm_args g = gemm_args(P(m.bs.d_gate), F, true, P(sl.ln1_full), H, true, G + p.wg, H, true, F, H, S,
                                        true, cap);
             g.a2 = P(m.bs.d_up);

@@ -173,6 +173,7 @@ struct Op {
     bool barrier = false;    // step barrier before this op (all lanes joined)
     bool capped = true;      // GEMMs may co-run with a collective: limit them to gemm_ctas_overlap SMs
     int peer = -1;           // pipeline transfers: the other stage
+    int part = -1;           // mlp_fc1_wgrad issued as two launches: 0 gate rows, 1 up rows (-1: both)
 };
 
 struct Program {
