@@ -182,7 +182,7 @@ struct Lowering {
     // issued while a collective of the layer is still open are capped like
     // co-running ones.
     //
-    // Mode 4 at TP > 1 also moves the lone strand's weight gradients under its
+    // In the SI modes at TP > 1 (EP > 1) it also moves its weight gradients under its
     // collectives (the plan's order leaves three of the four exposed:
     // tools/op_timeline.py): mlp_down_wgrad after ag1_bwd_rs (the RS of the MLP
     // input gradient), mlp_fc1_wgrad split into its gate and up launches after
@@ -197,7 +197,13 @@ struct Lowering {
         const char* e = std::getenv("DH_SI_LONE_REORDER");
         return !e || std::atoi(e) != 0;
     }();
-    bool lone_defers() const { return defer_wgrads && lone_reorder && !m.cfg.moe && m.cfg.tp > 1; }
+    // moe_ep (EP > 1): only the attention weight gradients (attn_proj_wgrad 34,
+    // qkv_wgrad 38) move, under the next layer's a2a_combine_bwd; the dispatch
+    // all-to-all already runs under expert_fc1_wgrad in the plan's order
+    bool lone_block = false;  // lowering the unpaired last backward strand of an SI schedule
+    bool lone_defers() const {
+        return lone_block && lone_reorder && (m.cfg.moe ? m.cfg.ep > 1 : m.cfg.tp > 1);
+    }
 
     void backward_layer_dag(int strand, int layer) {
         std::map<int, std::vector<int>> preds;
@@ -210,7 +216,14 @@ struct Lowering {
         const bool reorder = lone_defers();
         auto has = [&](int id) { return std::find(seq.begin(), seq.end(), id) != seq.end(); };
         std::vector<int> part_of(seq.size(), -1);
-        if (reorder && has(23) && has(26) && has(27) && has(30) && has(32) && has(36) && has(37)) {
+        int defer_a = 32, defer_b = 36;  // the attention weight gradients
+        if (reorder && m.cfg.moe && has(34) && has(38)) {
+            defer_a = 34;
+            defer_b = 38;
+            seq.erase(std::find(seq.begin(), seq.end(), 34));
+            seq.erase(std::find(seq.begin(), seq.end(), 38));
+        } else if (reorder && !m.cfg.moe && has(23) && has(26) && has(27) && has(30) && has(32) && has(36) &&
+                   has(37)) {
             auto move_after = [&](int id, int anchor) {
                 seq.erase(std::find(seq.begin(), seq.end(), id));
                 seq.insert(std::find(seq.begin(), seq.end(), anchor) + 1, id);
@@ -227,7 +240,7 @@ struct Lowering {
         } else if (reorder) {
             flush_deferred();
         }
-        const bool defer_attn = reorder && !has(32);
+        const bool defer_attn = reorder && !has(defer_a) && !has(defer_b);
         bool flushed = false;
         for (std::size_t si = 0; si < seq.size(); ++si) {
             const int id = seq[si];
@@ -260,7 +273,7 @@ struct Lowering {
         if (defer_attn) {
             deferred.strand = strand;
             deferred.layer = layer;
-            deferred.nodes = {32, 36};  // slot released by flush_deferred()
+            deferred.nodes = {defer_a, defer_b};  // slot released by flush_deferred()
         } else {
             give_slot(strand, layer);
         }
@@ -578,7 +591,7 @@ int lower_ops(Model& m, int mode) {
                     // gradients into the next layer, so that layer's AdamW follows
                     // the next layer's backward
                     const bool last_strand = *blk.bwd_mb == mb;
-                    lw.defer_wgrads = mode == 4;
+                    lw.lone_block = true;  // (no forward strand takes slots here: no extra slot needed)
                     const bool lag = lw.lone_defers();
                     for (int l = L - 1; l >= 0; --l) {
                         lw.backward_layer_dag(*blk.bwd_mb - 1, l);
@@ -590,7 +603,7 @@ int lower_ops(Model& m, int mode) {
                         lw.strand_last[*blk.bwd_mb - 1] = lw.lane_last[0];  // AdamW(0) follows them
                     }
                     if (last_strand && lag) lw.emit_opt(mb - 1, 0);
-                    lw.defer_wgrads = false;
+                    lw.lone_block = false;
                 } else {
                     lw.defer_wgrads = mode == 4;
                     for (int k = 0; k < L; ++k)
