@@ -96,6 +96,15 @@ int main() {
         rep("bwd dx rows only <8,4,2>", mb3 + mb2 / 2, time_us([&] {
                 rmsnorm_bwd_fused<8, 4, 2><<<64 + rows / 2, vc>>>(x, g, rstd, dy, res, dx, nullptr, rows, vc, ic, 64);
             }));
+        {  // RoPE over the q and k heads of the fused qkv rows (TP=1: 32 + 8 heads, TP=8: 4 + 1)
+            const int heads = rows == 4096 ? 40 : 5, D = 128, ldq = (heads + (rows == 4096 ? 8 : 1)) * D;
+            __nv_bfloat16* qkv;
+            cudaMalloc(&qkv, static_cast<size_t>(rows) * ldq * 2);
+            cudaMemset(qkv, 0x3c, static_cast<size_t>(rows) * ldq * 2);
+            const double mb = 2.0 * rows * heads * D * 2 / 1e6, lt = std::log(500000.0);
+            rep("rope", mb, time_us([&] { rope_vec_kernel<<<rows, 128>>>(qkv, ldq, rows, heads, D, lt, 0, 1.f); }));
+            cudaFree(qkv);
+        }
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
         cudaFree(x); cudaFree(y); cudaFree(dy); cudaFree(dx); cudaFree(res); cudaFree(g); cudaFree(rstd); cudaFree(dg);
