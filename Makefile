@@ -33,7 +33,7 @@ all: planner cuda oracle
 
 planner: $(LIB)/libweft_b200.so
 cuda: $(LIB)/libdh_b200.so
-oracle:
+oracle: planner
 	$(MAKE) -C oracle
 
 $(OBJ)/planner/%.o: $(PKG)/csrc/planner/%.cpp $(wildcard include/weft/*.hpp) $(PKG)/csrc/planner/lane_sim.hpp
