@@ -143,6 +143,55 @@ int time_solo_stream(Model& m, const Op& o, int iters, double* us) {
     return DH_OK;
 }
 
+// DH_PROFILE_SOLO_GRAPH (default 1): the back-to-back launches are captured
+// into one CUDA graph and replayed, so the solo table holds device time only.
+// Eager issue adds the host's per-launch cost (tensor-map encoding, launch
+// calls) whenever it exceeds a short node's duration, while the executor
+// replays a captured graph with no host work between kernels.
+bool solo_graph() {
+    static const bool on = [] {
+        const char* e = std::getenv("DH_PROFILE_SOLO_GRAPH");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+int time_solo_graph(Model& m, const Op& o, int iters, double* us) {
+    cudaStream_t s = m.ctx->lane[o.lane];
+    for (int i = 0; i < 2; ++i) RT_TRY(launch_node(m, o, s));  // lazy setup outside the capture
+    RT_CUDA(cudaStreamSynchronize(s));
+    cudaGraph_t g = nullptr;
+    RT_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int rc = DH_OK;
+    for (int i = 0; i < iters && rc == DH_OK; ++i) rc = launch_node(m, o, s);
+    const cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (rc != DH_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    RT_CUDA(ce);
+    cudaGraphExec_t ge = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    RT_CUDA(ie);
+    Timer t;
+    rc = DH_OK;
+    if (cudaGraphLaunch(ge, s) != cudaSuccess) rc = set_error(DH_ERR_CUDA, "profiler: graph launch");
+    if (rc == DH_OK && m.ctx->comm) rc = m.ctx->comm->barrier(s);
+    if (rc == DH_OK) {
+        cudaEventRecord(t.a, s);
+        if (cudaGraphLaunch(ge, s) != cudaSuccess) rc = set_error(DH_ERR_CUDA, "profiler: graph launch");
+        cudaEventRecord(t.b, s);
+        cudaEventSynchronize(t.b);
+    }
+    cudaGraphExecDestroy(ge);
+    if (rc != DH_OK) return rc;
+    float ms = 0.f;
+    RT_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    *us = 1e3 * ms / iters;
+    return DH_OK;
+}
+
 int time_pair(Model& m, const Op& a, const Op& b, int iters, double* us) { return time_gated(m, a, &b, iters, us); }
 
 }  // namespace
@@ -163,7 +212,10 @@ int profile_model(Model& m, int iters, std::string* out_json) {
         const bool fwd = table == &fwd_nodes;
         for (const auto& [id, n] : *table) {
             double us = 0.0, ug = 0.0;
-            RT_TRY(time_solo_stream(m, node_op(m, *n, fwd), iters, &us));
+            if (solo_graph() && (!m.ctx->comm || m.ctx->comm->capturable()))
+                RT_TRY(time_solo_graph(m, node_op(m, *n, fwd), iters, &us));
+            else
+                RT_TRY(time_solo_stream(m, node_op(m, *n, fwd), iters, &us));
             RT_TRY(time_solo_gated(m, node_op(m, *n, fwd), iters, &ug));
             // event-timer floor: a sub-microsecond node can read as 0, which Eq. 1 rejects
             us = std::max(us, 1e-3);
@@ -219,6 +271,7 @@ int profile_model(Model& m, int iters, std::string* out_json) {
     md["hidden"] = std::to_string(m.cfg.hidden);
     md["iters"] = std::to_string(iters);
     md["harness"] = std::to_string(harness_mode());
+    md["solo_timing"] = solo_graph() && (!m.ctx->comm || m.ctx->comm->capturable()) ? "graph" : "stream";
     md["pairs_measured"] = std::to_string(pairs.size());
     // The Profile document plus the raw pair table; parse_profile reads only
     // solo / oef / interference / metadata, so the extra key is inert.

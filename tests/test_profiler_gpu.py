@@ -23,6 +23,8 @@ def test_profile_tp1_solo_table():
     assert all(e["t_us"] > 0 for e in prof["solo"])
     assert prof["oef"] == []  # tp=1: no communication lane, nothing co-runs
     assert prof["interference"] == {"launch_overhead_frac": 0.0, "slowdown_factor": 0.0}
+    # the solo table is device time of graph-replayed launches, as the executor runs them
+    assert prof["metadata"]["solo_timing"] == "graph"
     # the planner consumes it unchanged; durations now come from the measurement
     fwd, bwd = planner.lib().build_layer_dag(shape.planner_model(), {"tp": 1}, B200, profile=prof)
     measured = {e["shape"]: e["t_us"] for e in prof["solo"]}

@@ -1,20 +1,29 @@
 """Where a single-wave CTA-pair GEMM spends its time: per-CTA globaltimer
-stamps (build with NVFLAGS_EXTRA=-DDH_GEMM_TRACE). usage: gemm_trace.py m n k"""
+stamps (build with NVFLAGS_EXTRA=-DDH_GEMM_TRACE).
+usage: gemm_trace.py m n k [pair_tile_n (256|192|128)] [b_mn 0|1] [flush 0|1] [rewarm a|b]
+(rewarm: after the L2 flush, read A or B once so only the other operand is cold)"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2411_15871_b200 import device as dh
 m, n, k = (int(x) for x in sys.argv[1:4])
-kw = dict(tile_n=512)  # the 256 x 256 CTA-pair kernel
+pbn = int(sys.argv[4]) if len(sys.argv) > 4 else 256
+b_mn = len(sys.argv) > 5 and sys.argv[5] == "1"
+do_flush = not (len(sys.argv) > 6 and sys.argv[6] == "0")
+kw = dict(tile_n=512 if pbn == 256 else -pbn, b_mn=b_mn)  # a CTA-pair kernel, 256 x pbn tiles
 a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
-b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
+b = torch.randn((k, n) if b_mn else (n, k), device="cuda", dtype=torch.bfloat16)
 d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
 flush = torch.empty(256 << 20, dtype=torch.int8, device="cuda")
 for _ in range(3):
     dh.gemm(a, b, d, **kw)
 torch.cuda.synchronize()
 torch.cuda.synchronize()
-flush.zero_()
+if do_flush:
+    flush.zero_()
+    rewarm = sys.argv[7] if len(sys.argv) > 7 else ""
+    if rewarm:
+        (a if rewarm == "a" else b).sum(dtype=torch.float32)
 s, e = torch.cuda.Event(True), torch.cuda.Event(True)
 s.record()
 dh.gemm(a, b, d, **kw)
@@ -22,7 +31,7 @@ e.record()
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * (512 * 8))()
 dh.lib().dh_gemm_trace_read(buf, 512 * 8)
-tiles = -(-m // 256) * -(-n // 256)
+tiles = -(-m // 256) * -(-n // pbn)
 ctas = 2 * min(torch.cuda.get_device_properties(0).multi_processor_count // 2, tiles)
 rows = [[buf[c * 8 + i] for i in range(6)] for c in range(ctas)]
 t0 = min(r[0] for r in rows)
