@@ -314,6 +314,30 @@ def test_gemm_swiglu_epilogues(m, n, k, tile_n):
     assert torch.equal(dup, ru)
 
 
+@pytest.mark.parametrize("tile_n", [512, -192, -128])
+@pytest.mark.parametrize("ctas", [2, 6, 16])
+def test_gemm_swiglu_epilogues_many_tiles_per_pair(tile_n, ctas):
+    """Few CTA pairs, many tiles each: the fused epilogues' aux tiles rotate
+    through three staging sets two chunks ahead, across tile boundaries."""
+    m, n, k = 1024, 1536, 192
+    g = torch.Generator(device="cuda").manual_seed(ctas)
+    x = (torch.randn(m, k, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    gate = torch.randn(m, n, device="cuda", generator=g).to(torch.bfloat16)
+    other = torch.randn(m, n, device="cuda", generator=g).to(torch.bfloat16)
+    ref = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    dh.gemm(x, w, ref, tile_n=512)
+    d, act, ref_act = torch.empty_like(ref), torch.empty_like(ref), torch.empty_like(ref)
+    dh.gemm(x, w, d, tile_n=tile_n, max_ctas=ctas, epilogue=dh.EPI_SWIGLU_FWD, d2=act, aux0=other)
+    dh.swiglu_fwd(other, ref, ref_act)
+    assert torch.equal(d, ref) and torch.equal(act, ref_act)
+    dgate, dup, rg, ru = (torch.empty_like(ref) for _ in range(4))
+    dh.gemm(x, w, dgate, tile_n=tile_n, max_ctas=ctas, epilogue=dh.EPI_SWIGLU_BWD, d2=dup, aux0=gate, aux1=other)
+    dh.swiglu_bwd(gate, other, ref, rg, ru)
+    torch.cuda.synchronize()
+    assert torch.equal(dgate, rg) and torch.equal(dup, ru)
+
+
 @pytest.mark.parametrize("rows,cols", [(96, 256), (512, 4096), (33, 8192), (40, 1000)])
 def test_add_rmsnorm_fused_equals_add_then_norm(rows, cols):
     """The fused bda0 + ln1 kernel is bitwise dh_add followed by dh_rmsnorm_fwd."""

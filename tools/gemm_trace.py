@@ -1,7 +1,8 @@
 """Where a single-wave CTA-pair GEMM spends its time: per-CTA globaltimer
 stamps (build with NVFLAGS_EXTRA=-DDH_GEMM_TRACE).
 usage: gemm_trace.py m n k [pair_tile_n (256|192|128)] [b_mn 0|1] [flush 0|1] [rewarm a|b]
-(rewarm: after the L2 flush, read A or B once so only the other operand is cold)"""
+(rewarm: after the L2 flush, read A or B once so only the other operand is cold)
+env EPI=fwd|bwd: the fused SwiGLU forward / backward epilogue (aux operands random)"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -14,6 +15,13 @@ kw = dict(tile_n=512 if pbn == 256 else -pbn, b_mn=b_mn)  # a CTA-pair kernel, 2
 a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
 b = torch.randn((k, n) if b_mn else (n, k), device="cuda", dtype=torch.bfloat16)
 d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+epi = os.environ.get("EPI", "")
+if epi:
+    x0 = torch.randn(m, n, device="cuda", dtype=torch.bfloat16)
+    x1 = torch.randn(m, n, device="cuda", dtype=torch.bfloat16)
+    d2 = torch.empty_like(d)
+    kw.update(epilogue=dh.EPI_SWIGLU_FWD if epi == "fwd" else dh.EPI_SWIGLU_BWD, d2=d2, aux0=x0,
+              aux1=x1 if epi == "bwd" else None)
 flush = torch.empty(256 << 20, dtype=torch.int8, device="cuda")
 for _ in range(3):
     dh.gemm(a, b, d, **kw)
