@@ -1,6 +1,7 @@
 """Time every GEMM of one TP=8 layer (Llama-3-8B shapes, seq 4096) the way the
 model calls it (majors, fp32 accumulate / bf16 outputs), for each tile choice
-and the overlap CTA cap. CUDA events, L2 flushed between launches."""
+and the overlap CTA cap. CUDA events over graph-replayed back-to-back launches
+(GRAPH=0: eager single launches after an L2 flush)."""
 import json
 import os
 import sys
@@ -14,8 +15,30 @@ flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")
 
 
 def timeit(fn, iters=15):
+    """Device time per launch: `iters` launches captured in one CUDA graph (no host
+    cost between them) and replayed; GRAPH=0 for eager single launches after an L2
+    flush (host launch cost included)."""
     for _ in range(3):
         fn()
+    torch.cuda.synchronize()
+    if os.environ.get("GRAPH", "1") != "0":
+        st = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(iters):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+            s.record()
+            g.replay()
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e) / iters)
+        ts.sort()
+        return ts[1]
     ts = []
     for _ in range(iters):
         flush.zero_()
