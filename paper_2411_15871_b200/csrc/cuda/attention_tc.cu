@@ -67,8 +67,24 @@ __device__ __forceinline__ void blk_stamp(int i) {
     }
 }
 #define BLK(i) blk_stamp(i)
+// forward phases per block (globaltimer ns): [0] prologue done, [1] Q and K_0
+// landed (MMA warp), [2] first S_0 ready (softmax tile 0), [3] tile 0's O done,
+// [4] tile 0's epilogue stores issued
+__device__ unsigned long long g_attn_ph[8192 * 8];
+extern "C" int dh_attn_phase_read(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_attn_ph, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#define PH(i, cond)                                                        \
+    do {                                                                   \
+        if ((cond) && blockIdx.x < 8192) {                                 \
+            unsigned long long t_;                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
+            g_attn_ph[blockIdx.x * 8 + (i)] = t_;                          \
+        }                                                                  \
+    } while (0)
 #else
 #define BLK(i) do { } while (0)
+#define PH(i, cond) do { } while (0)
 #endif
 
 namespace dh {
@@ -220,6 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t t_s = tmem, t_o = tmem + 256;  // S_t at t_s + 128 t, O_t at t_o + 128 t
+    PH(0, threadIdx.x == 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -268,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         mbar_wait(q_full, 0);
         wait_kv(0);
+        PH(1, lane == 0);
         issue_s(0, 0);
         issue_s(1, 0);
         release(0);
@@ -311,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < nt; ++j) {
             mbar_wait(&s_full[t], j & 1);
             tc_fence_after();
+            PH(2, j == 0 && t == 0 && r == 0);
             // all four 32-column loads in flight before one wait
             uint32_t sr[BKV];
 #pragma unroll
@@ -406,6 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(&o_done[t], 0);
         tc_fence_after();
+        PH(3, t == 0 && r == 0);
         if (split) {
             // unnormalised partial, [d][row] so a warp's stores are coalesced
             const long long slot = (static_cast<long long>(h) * (2 * p.npairs) + qb) * p.maxc + ch;
@@ -421,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float* pml = p.part + static_cast<long long>(p.nq) * (2 * p.npairs) * p.maxc * (BQ * D) +
                          slot * (2 * BQ);
             *reinterpret_cast<float2*>(pml + 2 * r) = make_float2(m_used, l);
+            PH(4, t == 0 && r == 0);
         } else {
             const float inv = l > 0.f ? 1.f / l : 0.f;
             const bool ok = qrow < p.T;

@@ -1,6 +1,6 @@
 """Per-block timeline of one attention-backward launch (build with
 NVFLAGS_EXTRA=-DDH_ATTN_BLKTRACE): makespan, per-SM busy time, the critical
-SM's items. usage: attn_blocks.py <nq> [T]"""
+SM's items. usage: attn_blocks.py <nq> [T] [fwd]; env DH_ATTN_FWD_CHUNK forces the forward KV chunk"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -42,3 +42,27 @@ ends = sorted((max(e for s, e in v), sm) for sm, v in busy.items())
 print("SM finish times (us): min %.1f median %.1f max %.1f" % (ends[0][0], ends[len(ends) // 2][0], ends[-1][0]))
 crit = ends[-1][1]
 print("critical SM items:", [(round(s, 1), round(e, 1)) for s, e in sorted(busy[crit])])
+cnt = {}
+for sm, v in busy.items():
+    cnt.setdefault(len(v), []).append(sum(e - s for s, e in v))
+print("items per SM -> (SMs, mean busy us, max busy us):",
+      {k: (len(v), round(sum(v) / len(v), 1), round(max(v), 1)) for k, v in sorted(cnt.items())})
+print("item durations (us) deciles:", [round(dur[int(i * (len(dur) - 1) / 10)][0], 1) for i in range(11)])
+if fwd_only and hasattr(dh.lib(), "dh_attn_phase_read"):
+    ph = (ctypes.c_ulonglong * (n * 8))()
+    dh.lib().dh_attn_phase_read(ph, n * 8)
+    names = ["prologue done", "Q + K_0 landed", "first S_0 ready", "tile 0 O done", "partials issued", "block end"]
+    rel = {k: [] for k in names}
+    for i in range(n):
+        s0, e0 = buf[3 * i], buf[3 * i + 1]
+        if not s0 or e0 < s0:
+            continue
+        vals = [ph[8 * i + j] for j in range(5)] + [e0]
+        for k, v in zip(names, vals):
+            if v >= s0:
+                rel[k].append((v - s0) / 1e3)
+    print("forward phases, us after block start (median / p90):")
+    for k, v in rel.items():
+        if v:
+            v.sort()
+            print(f"  {k:18s} {v[len(v) // 2]:6.2f} / {v[int(0.9 * (len(v) - 1))]:6.2f}  ({len(v)} blocks)")
