@@ -6,7 +6,7 @@ from paper_2411_15871_b200 import device as dh
 which = sys.argv[1] if len(sys.argv) > 1 else "gemm_tp1"
 if which.startswith("gemm"):
     shapes = {"gemm_tp1": (4096, 14336, 4096), "gemm_tp8": (4096, 1792, 4096),
-              "gemm_proj8": (4096, 4096, 512)}
+              "gemm_proj8": (4096, 4096, 512), "gemm_qkv8": (4096, 768, 4096)}
     m, n, k = shapes[which]
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
     b = torch.randn(n, k, device="cuda", dtype=torch.bfloat16)
